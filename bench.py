@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""bench.py -- B200 benchmark of the graph-Laplacian multigrid hot path.
+
+One STEP = one pass of the whole hot path over
+the workload resident in HBM: lap_setup (random order, elimination /
+aggregation hierarchy, Galerkin, lambda-hat, coarsest L^+) followed by
+lap_solve (PCG + V-cycle to 1e-8 relative residual), both through the C ABI
+of liblap.so.
+
+metric  = SpMV edges/s: nonzeros of L traversed by all SpMV-shaped passes of
+          the step (setup semiring SpMVs + every solve-phase L_l application),
+          per second of device time (max over ranks).  BASELINE.json names
+          "V-cycle SpMV edges/s & HBM GB/s vs roofline; time to 1e-8 relative
+          residual": the line also carries the solve-only V-cycle edges/s,
+          time_to_1e8_ms, the setup time and the roofline of the dominant
+          kernel (fused Chebyshev/Jacobi SpMV, H2).
+workload (N=1) = BASELINE.json configs[1]: 3D 7-point grid 128^3, log-uniform
+          weights in [1e-3, 1] (the other configs are parity-test cases).
+
+--impl reference runs the CPU oracle (oracle/, the paper's method as plain C)
+on a bounded sample of the same workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import lapgen  # noqa: E402
+
+CFG = 2
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+
+
+def peaks():
+    fn = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(fn):
+        with open(fn) as f:
+            return json.load(f), "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------- clocks
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md recipe)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+                out = ""
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- edge model
+def pass_counts(levels, iters, vcycles, params):
+    """SpMV-shaped passes of one setup + solve (same accounting as liblap's
+    lap_stats): nonzeros of L traversed."""
+    K = params.get("cheby_degree", 2)
+    setup = solve = 0
+    prev_elim = False
+    for i, L in enumerate(levels):
+        kind, nnz = L["kind"], L["nnz"]
+        if kind == 2:
+            break
+        if kind == 1:
+            setup += 2 * nnz                       # Alg. 2 select + Schur build
+            prev_elim = True
+            continue
+        if not prev_elim:
+            setup += nnz                           # rejected elimination attempt
+        setup += nnz * (params.get("lanczos_steps", 10) + 3 + 2 + 10 + 1)  # Lanczos, sweeps, C/S, votes, Galerkin
+        solve += vcycles * nnz * (2 * K)           # (K-1) pre + resid + K post
+        prev_elim = False
+    solve += (iters + 2) * levels[0]["nnz"]        # PCG q = L p, true residuals
+    return setup, solve
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1705_06266_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device=dev)
+
+    g = lapgen.config(args.config)
+    b = lapgen.rhs(g.n)
+    # inputs resident in HBM
+    rp_d = torch.from_numpy(g.row_ptr).to(dev)
+    col_d = torch.from_numpy(g.col).to(dev)
+    w_d = torch.from_numpy(g.w).to(dev)
+    b_d = torch.from_numpy(b).to(dev)
+    x_d = torch.zeros_like(b_d)
+    gd = lapgen.Graph(g.n, rp_d, col_d, w_d, g.name)
+    # pinned host copies for the end-to-end measurement
+    rp_h = torch.from_numpy(g.row_ptr).pin_memory()
+    col_h = torch.from_numpy(g.col).pin_memory()
+    w_h = torch.from_numpy(g.w).pin_memory()
+    b_h = torch.from_numpy(b).pin_memory()
+    x_h = torch.zeros(g.n, dtype=torch.float64).pin_memory()
+
+    class _HostG:  # host-pointer graph (on_device = 0) from pinned tensors
+        n = g.n
+        row_ptr, col, w = rp_h.numpy(), col_h.numpy(), w_h.numpy()
+
+    def step(graph, bb, xx):
+        h = P.Hierarchy(graph, stream=stream)
+        k_setup = h.stats()["kernel_launches"]
+        _, it, rr, rc = h.solve(bb, xx, stream=stream)
+        st = h.stats()
+        st["kernel_launches"] += k_setup
+        levels = [dict(kind=h.level_info(l)[0], n=h.level_info(l)[1], nnz=h.level_info(l)[2]) for l in range(h.nlev)]
+        h.close()
+        return it, rr, rc, st, levels
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            it, rr, rc, st, levels = step(gd, b_d, x_d)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        setup_ms, solve_ms, launches, lib_edges = [], [], 0, 0
+        with Clocks(local) as clk:
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            t0.record(stream)
+            for _ in range(args.steps):
+                it, rr, rc, st, levels = step(gd, b_d, x_d)
+                solve_ms.append(st["solve_ms"])
+                launches += st["kernel_launches"]
+                lib_edges += st["spmv_edges"]
+            t1.record(stream)
+            torch.cuda.synchronize()
+        total_ms = t0.elapsed_time(t1)
+        if world > 1:
+            dist.barrier()
+        # setup/solve split (separately timed steps, CUDA events inside the library)
+        hs = P.Hierarchy(gd, stream=stream)
+        torch.cuda.synchronize()
+        s_setup = hs.stats()
+        setup_launches = s_setup["kernel_launches"]
+        _, it_s, rr_s, _ = hs.solve(b_d, x_d, stream=stream)
+        s_solve = hs.stats()
+        # dominant kernel: fused Chebyshev SpMV on the finest aggregation level, timed with CUDA events
+        ms_k, bytes_k, lvl_k = hs.bench_smoother(50, stream=stream)
+        hs.close()
+        # end-to-end through the C ABI with HOST buffers (H2D of graph + b, D2H of x inside)
+        e2e_ms = []
+        for _ in range(max(1, min(args.steps, 3))):
+            torch.cuda.synchronize()
+            e0 = time.perf_counter()
+            he = P.Hierarchy(_HostG, stream=stream)
+            he.solve(b_h.numpy(), x_h.numpy(), stream=stream)
+            torch.cuda.synchronize()
+            e2e_ms.append((time.perf_counter() - e0) * 1e3)
+            he.close()
+
+    ms = total_ms / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    setup_edges, solve_edges = pass_counts(levels, it, s_solve["vcycles"], {})
+    edges = setup_edges + solve_edges
+    pk, pk_src = peaks()
+    hbm = float(pk.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
+    achieved = bytes_k / (ms_k * 1e-3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get("cheb_spmv_bytes_per_launch")
+        except Exception:
+            traffic = None
+    clocks = clk.summary()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    cpu = cpu_baseline(args) if (world == 1 and not args.no_cpu) else None
+    h2d = g.row_ptr.nbytes + g.col.nbytes + g.w.nbytes + b.nbytes
+    line = {
+        "metric": "SpMV edges/s over one setup + PCG/V-cycle solve to 1e-8 rel. residual",
+        "value": world * edges / (ms * 1e-3),
+        "unit": "edges/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (lapgen, seeded)",
+        "config": {"workload": lapgen.CONFIG_NAMES[args.config], "n": g.n, "nnz_off": g.nnz,
+                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (2D sharding: next)",
+                   "l2": "inputs > L2: level-0 CSR is 150 MB, solve re-streams it every SpMV",
+                   "levels": [[L["kind"], L["n"], L["nnz"]] for L in levels]},
+        "iters": it, "rel_residual": rr,
+        "time_to_1e8_ms": s_solve["solve_ms"],
+        "setup_ms": s_setup["setup_ms"],
+        "vcycle_edges_per_s": solve_edges / (s_solve["solve_ms"] * 1e-3),
+        "setup_edges": setup_edges, "solve_edges": solve_edges,
+        "lib_counted_edges_per_step": lib_edges / args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": traffic,
+                     "kernel": f"fused Chebyshev/Jacobi SpMV (H2) on level {lvl_k}",
+                     "bytes_per_launch": bytes_k, "ms_per_launch": ms_k,
+                     "frac_of_8000": achieved / 8000.0, "peak_source": pk_src},
+        "e2e": {"value": edges / (statistics.median(e2e_ms) * 1e-3), "unit": "edges/s",
+                "ms": statistics.median(e2e_ms), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": b.nbytes},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------- CPU oracle arm
+def oracle_sample(budget_s: float):
+    """Same workload family at a bounded size: 3D 7-point grid side s with the
+    cfg-2 weight distribution (the full 128^3 oracle run takes ~2 min)."""
+    side = 48 if budget_s < 15 else 64
+    return side, lapgen.grid3d(side, True, 1, f"grid3d_{side}")
+
+
+def run_oracle_once(g):
+    import oracle
+    b = lapgen.rhs(g.n)
+    t0 = time.perf_counter()
+    h = oracle.Hierarchy(g)
+    x, it, rr, rc = h.solve(b)
+    dt = time.perf_counter() - t0
+    levels = [dict(kind=L.kind, n=L.n, nnz=L.nnz) for L in h.levels()]
+    nv = it + 1
+    setup_e, solve_e = pass_counts(levels, it, nv, {})
+    return dt, setup_e + solve_e, it, rr
+
+
+def cpu_baseline(args):
+    side, g = oracle_sample(20.0)
+    dt, edges, it, rr = run_oracle_once(g)
+    return {"value": edges / dt, "unit": "edges/s", "cores": 1, "kind": "oracle",
+            "sample": f"one full oracle setup + solve to 1e-8 on a {side}^3 3D grid (cfg-2 weights), "
+                      f"{dt:.1f} s, {it} iters; oracle is single-threaded"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    side, g = oracle_sample(budget)
+    for _ in range(args.warmup):
+        run_oracle_once(g)
+    tot_t, tot_e = 0.0, 0
+    for _ in range(args.steps):
+        dt, e, it, rr = run_oracle_once(g)
+        tot_t += dt
+        tot_e += e
+    v = tot_e / tot_t
+    print(json.dumps({
+        "impl": "reference",
+        "metric": "SpMV edges/s over one setup + PCG/V-cycle solve to 1e-8 rel. residual",
+        "value": v, "unit": "edges/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (lapgen, seeded)",
+        "config": {"workload": lapgen.CONFIG_NAMES[args.config], "sample": f"{side}^3 3D grid, cfg-2 weights"},
+        "cpu_baseline": {"value": v, "unit": "edges/s", "cores": 1, "kind": "oracle",
+                         "sample": f"{side}^3 3D 7-pt grid, log-uniform w; full setup + solve per step"},
+        "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="lap", choices=["lap", "reference"])
+    ap.add_argument("--config", type=int, default=CFG)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,160 @@
+/*
+ * include/lap.h -- C ABI of liblap.so, the B200-native (sm_100a) hot path of
+ * the unsmoothed-aggregation multigrid solver for graph Laplacians of
+ * Konolige & Brown, "A Parallel Solver for Graph Laplacians" (arXiv
+ * 1705.06266).  Citations: P:NNN = PAPER.md line, S:NNN = SPEC.md line,
+ * O-xx = SURVEY.md §8(c) reading.
+ *
+ * Problem: given a connected, positively weighted,
+ * undirected graph G = (V, E, w) with Laplacian L = D - A, compute x with
+ * L x = b for b projected orthogonal to the constant vector.
+ *
+ * Two calls carry the method:
+ *   lap_setup  -- builds the multigrid hierarchy on the GPU:
+ *                 random vertex order, low-degree elimination levels
+ *                 (Alg. 2 + Schur complement), aggregation levels (affinity
+ *                 strength, Alg. 3 voting, Galerkin R L P), lambda-hat by
+ *                 Lanczos, dense coarsest pseudo-inverse.
+ *   lap_solve  -- PCG preconditioned by one V-cycle (Alg. 1, gamma = 1) with
+ *                 degree-2 Chebyshev/Jacobi smoothing.
+ *
+ * Conventions for every function:
+ *   - Return value is a lap_status; LAP_OK = 0.  No C++ exception crosses
+ *     the ABI.  On failure, *out pointers are set to NULL and
+ *     lap_last_error() returns a thread-local message.
+ *   - `cuda_stream` is a cudaStream_t (NULL = legacy default stream).  All
+ *     device work is enqueued on it.  Calls that return host-visible scalars
+ *     (lap_setup, lap_solve, lap_level_*) synchronise that stream.
+ *   - Vector arguments of lap_solve / lap_spmv / lap_vcycle may be host
+ *     (pageable or pinned) or device pointers on the current device; the
+ *     library detects which with cudaPointerGetAttributes and copies host
+ *     data itself.  The caller owns them; the library never retains them.
+ *   - The hierarchy owns all its device memory until lap_free.  One solve
+ *     may be in flight per hierarchy at a time (work vectors live in it).
+ *   - Everything computes in IEEE fp64.  Setup reductions that feed discrete
+ *     decisions use the order-independent canonical sum of O-S11 (int128
+ *     fixed point), so hierarchies are bit-identical to the CPU oracle.
+ */
+#ifndef LAP_H
+#define LAP_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    LAP_OK = 0,
+    LAP_EINVAL = 1,        /* bad argument / parameter                               */
+    LAP_EGRAPH = 2,        /* asymmetric, self loop, w<=0/NaN, unsorted/duplicate col */
+    LAP_EDISCONNECTED = 3, /* graph not connected                      */
+    LAP_ENOMEM = 4,        /* device allocation failed                               */
+    LAP_ECUDA = 5,         /* CUDA runtime error                                     */
+    LAP_ENCCL = 6,         /* reserved: collective failure                           */
+    LAP_ENOCONV = 7,       /* PCG hit max_iters; x holds the last iterate    */
+    LAP_ESTALL = 8         /* warning: aggregation stalled twice, coarsest is large  */
+} lap_status;
+
+/* Symmetric off-diagonal adjacency of G in CSR (the Laplacian is implied:
+ * L_ij = -w_ij, L_ii = sum_j w_ij).  n >= 1; row_ptr[0] = 0; col strictly
+ * ascending within each row, no i == i entries; w_ij == w_ji bitwise, finite,
+ * > 0; w == NULL means unit weights.  on_device: 0 = host arrays,
+ * 1 = device arrays on the current device.  lap_setup deep-copies. */
+typedef struct {
+    int64_t n;
+    const int64_t *row_ptr;   /* n+1 */
+    const int32_t *col;       /* row_ptr[n] */
+    const double *w;          /* row_ptr[n] or NULL */
+    int32_t on_device;
+} lap_graph;
+
+/* Parameters; lap_params_default() sets the paper's values. */
+typedef struct {
+    double tol;               /* 1e-8 relative residual        */
+    int32_t max_iters;        /* 500                              S:547, O-R43 */
+    int32_t cheby_degree;     /* 2 (pre and post)        */
+    double cheby_lo;          /* 0.3 * lambda-hat                 P:643, O-R2  */
+    double cheby_hi;          /* 1.1 * lambda-hat                 P:643, O-R2  */
+    int32_t lanczos_steps;    /* 10                               P:643, O-R3  */
+    int32_t elim_max_degree;  /* 4    */
+    int32_t elim_enable;      /* 1        */
+    int32_t n_test_vectors;   /* 4 (only 4 supported)        */
+    int32_t tv_sweeps;        /* 3 Jacobi sweeps        */
+    double tv_omega;          /* 2/3                              O-R6         */
+    int32_t vote_rounds;      /* 10   */
+    int32_t vote_threshold;   /* 8, seed iff votes >= 8           P:619, O-R8  */
+    int64_t coarse_nnz;       /* 1000: coarsest iff n+nnz <= this P:672, O-R27 */
+    int32_t max_levels;       /* 40        */
+    uint64_t seed;            /* 0: salts of O-S11                             */
+    int32_t random_order;     /* 1: Pi_rand on the input only    */
+    int32_t affinity_power;   /* 1 = LAMG affinity (O-R5); 2 = literal P:564   */
+    int32_t keep_strength;    /* 1: retain S per aggregation level (tests)     */
+    int32_t use_graphs;       /* 1: capture the V-cycle as a CUDA graph        */
+} lap_params;
+
+typedef struct lap_hierarchy lap_hierarchy;
+
+void lap_params_default(lap_params *p);
+const char *lap_last_error(void);
+const char *lap_version(void);
+
+/* Build the hierarchy (SURVEY O-S0..O-S10).
+ * Validates the graph (LAP_EGRAPH / LAP_EDISCONNECTED); returns LAP_ESTALL
+ * (with a usable hierarchy) if aggregation stalled twice (O-R28). */
+lap_status lap_setup(const lap_graph *g, const lap_params *p, void *cuda_stream,
+                     lap_hierarchy **out);
+
+/* Solve L x = b to relative residual tol (<= 0: use params.tol) with PCG +
+ * V-cycle (O-S8).  b, x: length n in the caller's
+ * numbering.  A copy of b is projected to mean zero; x is returned mean-zero.
+ * *iters = number of L p products; *rel_residual = ||b - L x|| / ||b||
+ * recomputed at the end.  b = const -> x = 0, iters = 0, LAP_OK.
+ * LAP_ENOCONV if max_iters was reached (x = last iterate). */
+lap_status lap_solve(lap_hierarchy *h, const double *b, double *x, double tol,
+                     int32_t *iters, double *rel_residual, void *cuda_stream);
+
+void lap_free(lap_hierarchy *h);   /* NULL-safe */
+
+/* ---- introspection (host output buffers sized from lap_level_info) ------ */
+lap_status lap_num_levels(const lap_hierarchy *h, int32_t *nlev);
+/* kind: 0 aggregation, 1 elimination, 2 coarsest.  lambda_hat only for kind 0. */
+lap_status lap_level_info(const lap_hierarchy *h, int32_t l, int32_t *kind, int64_t *n,
+                          int64_t *nnz_off, double *lambda_hat);
+/* Copies level l to host arrays (any may be NULL): row_ptr[n+1], col[nnz],
+ * w[nnz], d[n], map[n] = agg[] (kind 0) or fmap[] (kind 1: coarse index for
+ * C vertices, -1-slot for F vertices). */
+lap_status lap_level_export(const lap_hierarchy *h, int32_t l, int64_t *row_ptr, int32_t *col,
+                            double *w, double *d, int32_t *map);
+/* Strength S[nnz] of aggregation level l (requires params.keep_strength). */
+lap_status lap_level_strength(const lap_hierarchy *h, int32_t l, double *S);
+/* Coarsest pseudo-inverse, n*n row-major (host buffer). */
+lap_status lap_coarse_pinv(const lap_hierarchy *h, double *pinv);
+/* perm[i] = internal (level-0) id of caller vertex i (Pi_rand). */
+lap_status lap_perm(const lap_hierarchy *h, int64_t *perm);
+/* y = L_l x on level l, internal numbering (H1). */
+lap_status lap_spmv(const lap_hierarchy *h, int32_t l, const double *x, double *y, void *cuda_stream);
+/* z = V(0, r): one V-cycle on the internal (permuted) level-0 numbering (O-S7). */
+lap_status lap_vcycle(lap_hierarchy *h, const double *r, double *z, void *cuda_stream);
+
+/* ---- counters for the benchmark ----------------------------------------- */
+typedef struct {
+    int64_t kernel_launches;  /* kernels launched by the last lap_solve / lap_setup   */
+    int64_t spmv_edges;       /* sum of nnz_off over SpMV-shaped passes (last call)   */
+    int64_t spmv_bytes;       /* algorithmic HBM bytes of those passes    */
+    double  setup_ms;         /* device time of the last lap_setup (CUDA events)      */
+    double  solve_ms;         /* device time of the last lap_solve (CUDA events)      */
+    int32_t vcycles;          /* V-cycles applied by the last lap_solve               */
+} lap_stats;
+lap_status lap_get_stats(const lap_hierarchy *h, lap_stats *s);
+
+/* Time the dominant solve kernel (the fused Chebyshev/Jacobi SpMV step on the
+ * finest aggregation level, H2) over `reps` launches on `cuda_stream` with
+ * CUDA events; returns mean ms per launch and its algorithmic bytes. */
+lap_status lap_bench_smoother(lap_hierarchy *h, int32_t reps, void *cuda_stream,
+                              double *ms_per_launch, double *bytes_per_launch,
+                              int32_t *level);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

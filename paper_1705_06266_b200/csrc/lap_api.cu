@@ -1,0 +1,526 @@
+// lap_api.cu -- the extern "C" boundary of liblap.so (include/lap.h) and the
+// host-side sequencing of setup/solve.  No C++ exception crosses the ABI.
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <cstring>
+
+#include "lap_internal.cuh"
+
+namespace lap {
+void vcycle_apply(lap_hierarchy *h, const double *r, double *z, cudaStream_t s);
+
+static thread_local std::string g_err;
+void set_error(const std::string &m) { g_err = m; }
+
+static bool g_pool_init = false;
+void *dalloc(size_t bytes, cudaStream_t s) {
+    if (!g_pool_init) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        g_pool_init = true;
+    }
+    void *p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, bytes ? bytes : 1, s);
+    if (e != cudaSuccess)
+        throw Error{e == cudaErrorMemoryAllocation ? LAP_ENOMEM : LAP_ECUDA,
+                    std::string("cudaMallocAsync: ") + cudaGetErrorString(e)};
+    return p;
+}
+void dfree(void *p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
+// ---------------------------------------------------------------- members CSR
+__global__ void k_iota(int64_t n, int32_t *v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        v[i] = (int32_t)i;
+}
+__global__ void k_lower_bound_i32(int64_t m, int64_t n, const int32_t *keys, int64_t *ptr) {
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a <= m; a += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if (keys[mid] < a) lo = mid + 1;
+            else hi = mid;
+        }
+        ptr[a] = lo;
+    }
+}
+__global__ void k_scatter_perm(int64_t n, const int64_t *perm, const double *in, double *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[perm[i]] = in[i];
+}
+__global__ void k_gather_perm(int64_t n, const int64_t *perm, const double *in, double *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in[perm[i]];
+}
+__global__ void k_sub_mean2(int64_t n, double *v, const double *sum) {
+    double mean = *sum / (double)n;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        v[i] -= mean;
+}
+
+static void build_members(Level &L, cudaStream_t s) {
+    int64_t n = L.n;
+    DBuf<int32_t> ids(n, s), keys2(n, s);
+    L.members = (int32_t *)dalloc(sizeof(int32_t) * n, s);
+    L.mem_ptr = (int64_t *)dalloc(sizeof(int64_t) * (L.m + 1), s);
+    k_iota<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(n, ids.p);
+    int end_bit = 1;
+    while (end_bit < 31 && ((int64_t)1 << end_bit) <= L.m) end_bit++;
+    size_t bytes = 0;
+    LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, L.agg, keys2.p, ids.p, L.members, n, 0, end_bit, s));
+    DBuf<char> tmp((int64_t)bytes, s);
+    LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, L.agg, keys2.p, ids.p, L.members, n, 0, end_bit, s));
+    k_lower_bound_i32<<<grid_for(L.m + 1, 256, 148 * 8), 256, 0, s>>>(L.m, n, keys2.p, L.mem_ptr);
+    g_kl += 3;
+    LAP_CHECK_LAUNCH();
+}
+
+void finalize_solve_structures(lap_hierarchy *h, cudaStream_t s) {
+    for (size_t l = 0; l < h->lev.size(); l++) {
+        Level &L = h->lev[l];
+        int64_t n = L.n > 0 ? L.n : 1;
+        L.b = (double *)dalloc(8 * n, s);
+        L.x = (double *)dalloc(8 * n, s);
+        L.x2 = (double *)dalloc(8 * n, s);
+        L.t = (double *)dalloc(8 * n, s);
+        L.r = (double *)dalloc(8 * n, s);
+        L.dv = (double *)dalloc(8 * n, s);
+        if (L.kind == KIND_AGG) {
+            double a = h->p.cheby_lo * L.lambda, b = h->p.cheby_hi * L.lambda;
+            L.cheb_theta = 0.5 * (b + a);
+            L.cheb_delta = 0.5 * (b - a);
+            L.cheb_sigma = L.cheb_theta / L.cheb_delta;
+            build_members(L, s);
+        }
+    }
+    int64_t n0 = h->lev[0].n;
+    double **vecs[] = {&h->pb, &h->px, &h->pr, &h->pz, &h->pp, &h->pq, &h->stage_in, &h->stage_out};
+    for (double **v : vecs) *v = (double *)dalloc(8 * (n0 > 0 ? n0 : 1), s);
+    h->scal = (double *)dalloc(8 * 16, s);
+    LAP_CUDA(cudaMemsetAsync(h->scal, 0, 8 * 16, s));
+    int64_t np = std::max<int64_t>(1024, spmv_partial_slots(h->lev[0]));
+    for (auto &L : h->lev) np = std::max<int64_t>(np, spmv_partial_slots(L));
+    h->partials = (double *)dalloc(8 * np, s);
+    h->npartials = np;
+    LAP_CUDA(cudaMallocHost(&h->host_scal, 64));
+}
+
+static void free_level(Level &L, cudaStream_t s) {
+    void *ps[] = {L.row_ptr, L.col, L.w, L.d, L.dinv, L.bins.rows, L.bins.chunk_row_first, L.bins.chunk_partial,
+                  L.agg, L.mem_ptr, L.members, L.S, L.fmap, L.cid, L.fid, L.ct_ptr, L.ct_f, L.ct_coef,
+                  L.pinv, L.b, L.x, L.x2, L.t, L.r, L.dv};
+    for (void *p : ps) dfree(p, s);
+}
+
+// V-cycle launch (graph when captured)
+struct VcCounts {
+    int64_t launches = 0, edges = 0, bytes = 0;
+};
+static std::vector<std::pair<lap_hierarchy *, VcCounts>> g_vc;  // per-hierarchy V-cycle counts (captured graph)
+static VcCounts &vc_of(lap_hierarchy *h) {
+    for (auto &e : g_vc)
+        if (e.first == h) return e.second;
+    g_vc.push_back({h, VcCounts{}});
+    return g_vc.back().second;
+}
+static void vc_forget(lap_hierarchy *h) {
+    for (size_t i = 0; i < g_vc.size(); i++)
+        if (g_vc[i].first == h) {
+            g_vc.erase(g_vc.begin() + i);
+            return;
+        }
+}
+
+void launch_vcycle(lap_hierarchy *h, cudaStream_t s) {
+    if (h->vgraph) {
+        LAP_CUDA(cudaGraphLaunch(h->vgraph, s));
+        VcCounts &c = vc_of(h);
+        h->cur.launches += c.launches;
+        h->cur.edges += c.edges;
+        h->cur.bytes += c.bytes;
+    } else {
+        vcycle_apply(h, h->pr, h->pz, s);
+    }
+}
+
+static void capture_vcycle(lap_hierarchy *h) {
+    cudaStream_t cs;
+    LAP_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    Stats save = h->cur;
+    h->cur = Stats{};
+    cudaGraph_t g;
+    LAP_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    try {
+        vcycle_apply(h, h->pr, h->pz, cs);
+    } catch (...) {
+        cudaStreamEndCapture(cs, &g);
+        cudaStreamDestroy(cs);
+        throw;
+    }
+    LAP_CUDA(cudaStreamEndCapture(cs, &g));
+    LAP_CUDA(cudaGraphInstantiate(&h->vgraph, g, 0));
+    LAP_CUDA(cudaGraphDestroy(g));
+    LAP_CUDA(cudaStreamDestroy(cs));
+    VcCounts &c = vc_of(h);
+    c.launches = h->cur.launches;
+    c.edges = h->cur.edges;
+    c.bytes = h->cur.bytes;
+    h->cur = save;
+}
+
+static bool is_device_ptr(const void *p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace lap
+
+// =========================================================================
+// extern "C"
+// =========================================================================
+
+#define LAP_API_BEGIN try {
+#define LAP_API_END                                 \
+    }                                               \
+    catch (const lap::Error &e) {                   \
+        lap::set_error(e.msg);                      \
+        return e.code;                              \
+    }                                               \
+    catch (const std::exception &e) {               \
+        lap::set_error(e.what());                   \
+        return LAP_ECUDA;                           \
+    }                                               \
+    catch (...) {                                   \
+        lap::set_error("unknown error");            \
+        return LAP_ECUDA;                           \
+    }
+
+extern "C" {
+
+void lap_params_default(lap_params *p) {
+    std::memset(p, 0, sizeof(*p));
+    p->tol = 1e-8;
+    p->max_iters = 500;
+    p->cheby_degree = 2;
+    p->cheby_lo = 0.3;
+    p->cheby_hi = 1.1;
+    p->lanczos_steps = 10;
+    p->elim_max_degree = 4;
+    p->elim_enable = 1;
+    p->n_test_vectors = 4;
+    p->tv_sweeps = 3;
+    p->tv_omega = 2.0 / 3.0;
+    p->vote_rounds = 10;
+    p->vote_threshold = 8;
+    p->coarse_nnz = 1000;
+    p->max_levels = 40;
+    p->seed = 0;
+    p->random_order = 1;
+    p->affinity_power = 1;
+    p->keep_strength = 0;
+    p->use_graphs = 1;
+}
+
+const char *lap_last_error(void) { return lap::g_err.c_str(); }
+const char *lap_version(void) { return "liblap 0.1 (sm_100a)"; }
+
+lap_status lap_setup(const lap_graph *g, const lap_params *pp, void *stream, lap_hierarchy **out) {
+    if (out) *out = nullptr;
+    if (!g || !out || g->n < 1 || !g->row_ptr || (g->row_ptr && !g->col && g->n > 1)) {
+        lap::set_error("lap_setup: invalid arguments");
+        return LAP_EINVAL;
+    }
+    lap_params p;
+    if (pp) p = *pp;
+    else lap_params_default(&p);
+    if (p.n_test_vectors != 4 || p.cheby_degree < 1 || p.tv_sweeps < 0 || p.vote_rounds < 0 ||
+        p.lanczos_steps < 1 || p.lanczos_steps > 64 || !(p.cheby_hi > p.cheby_lo) || !(p.cheby_lo > 0) ||
+        p.max_levels < 1) {
+        lap::set_error("lap_setup: unsupported parameter values");
+        return LAP_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    lap_hierarchy *h = new lap_hierarchy();
+    h->p = p;
+    cudaGetDevice(&h->device);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    try {
+        LAP_CUDA(cudaEventCreate(&e0));
+        LAP_CUDA(cudaEventCreate(&e1));
+        LAP_CUDA(cudaEventRecord(e0, s));
+        h->cur = lap::Stats{};
+        int64_t kl0 = lap::g_kl;
+        lap::build_hierarchy(h, g, s);
+        lap::finalize_solve_structures(h, s);
+        LAP_CUDA(cudaEventRecord(e1, s));
+        LAP_CUDA(cudaStreamSynchronize(s));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        h->stats.setup_ms = ms;
+        h->stats.kernel_launches = h->cur.launches + (lap::g_kl - kl0);
+        h->stats.spmv_edges = h->cur.edges;
+        h->stats.spmv_bytes = h->cur.bytes;
+        if (p.use_graphs) lap::capture_vcycle(h);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    } catch (const lap::Error &e) {
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+        lap::set_error(e.msg);
+        cudaStreamSynchronize(s);
+        lap_free(h);
+        cudaGetLastError();
+        return e.code;
+    } catch (...) {
+        lap::set_error("lap_setup: unexpected exception");
+        lap_free(h);
+        return LAP_ECUDA;
+    }
+    *out = h;
+    return h->status;
+}
+
+void lap_free(lap_hierarchy *h) {
+    if (!h) return;
+    cudaStream_t s = nullptr;
+    cudaDeviceSynchronize();
+    if (h->vgraph) cudaGraphExecDestroy(h->vgraph);
+    for (auto &L : h->lev) lap::free_level(L, s);
+    void *ps[] = {h->perm, h->pb, h->px, h->pr, h->pz, h->pp, h->pq, h->scal, h->partials, h->stage_in, h->stage_out};
+    for (void *p : ps) lap::dfree(p, s);
+    if (h->host_scal) cudaFreeHost(h->host_scal);
+    cudaStreamSynchronize(s);
+    lap::vc_forget(h);
+    delete h;
+}
+
+lap_status lap_solve(lap_hierarchy *h, const double *b, double *x, double tol, int32_t *iters, double *rel_residual,
+                     void *stream) {
+    if (!h || !b || !x) {
+        lap::set_error("lap_solve: invalid arguments");
+        return LAP_EINVAL;
+    }
+    LAP_API_BEGIN
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t n = h->n0;
+    if (tol <= 0) tol = h->p.tol;
+    cudaEvent_t e0, e1;
+    LAP_CUDA(cudaEventCreate(&e0));
+    LAP_CUDA(cudaEventCreate(&e1));
+    h->cur = lap::Stats{};
+    LAP_CUDA(cudaEventRecord(e0, s));
+    const double *bd = b;
+    if (!lap::is_device_ptr(b)) {
+        LAP_CUDA(cudaMemcpyAsync(h->stage_in, b, 8 * n, cudaMemcpyHostToDevice, s));
+        bd = h->stage_in;
+    }
+    unsigned g = lap::grid_for(n, 256, 148 * 8);
+    lap::k_scatter_perm<<<g, 256, 0, s>>>(n, h->perm, bd, h->pb);            // b' = Pi b
+    lap::dot(h, h->pb, nullptr, n, h->scal + 7, s);
+    lap::k_sub_mean2<<<g, 256, 0, s>>>(n, h->pb, h->scal + 7);               // project out 1
+    h->cur.launches += 2;
+    LAP_CHECK_LAUNCH();
+    int32_t it = 0;
+    double rr = 0;
+    int conv = 0;
+    lap::run_pcg(h, tol, &it, &rr, &conv, s);
+    bool xdev = lap::is_device_ptr(x);
+    double *xd = xdev ? x : h->stage_out;
+    lap::k_gather_perm<<<g, 256, 0, s>>>(n, h->perm, h->px, xd);             // x = Pi^T x'
+    h->cur.launches++;
+    LAP_CHECK_LAUNCH();
+    if (!xdev) LAP_CUDA(cudaMemcpyAsync(x, xd, 8 * n, cudaMemcpyDeviceToHost, s));
+    LAP_CUDA(cudaEventRecord(e1, s));
+    LAP_CUDA(cudaStreamSynchronize(s));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    h->stats.solve_ms = ms;
+    h->stats.kernel_launches = h->cur.launches;
+    h->stats.spmv_edges = h->cur.edges;
+    h->stats.spmv_bytes = h->cur.bytes;
+    if (iters) *iters = it;
+    if (rel_residual) *rel_residual = rr;
+    return conv ? LAP_OK : LAP_ENOCONV;
+    LAP_API_END
+}
+
+lap_status lap_num_levels(const lap_hierarchy *h, int32_t *nlev) {
+    if (!h || !nlev) return LAP_EINVAL;
+    *nlev = (int32_t)h->lev.size();
+    return LAP_OK;
+}
+
+lap_status lap_level_info(const lap_hierarchy *h, int32_t l, int32_t *kind, int64_t *n, int64_t *nnz,
+                          double *lambda_hat) {
+    if (!h || l < 0 || l >= (int32_t)h->lev.size()) return LAP_EINVAL;
+    const lap::Level &L = h->lev[l];
+    if (kind) *kind = L.kind;
+    if (n) *n = L.n;
+    if (nnz) *nnz = L.nnz;
+    if (lambda_hat) *lambda_hat = L.lambda;
+    return LAP_OK;
+}
+
+lap_status lap_level_export(const lap_hierarchy *h, int32_t l, int64_t *row_ptr, int32_t *col, double *w, double *d,
+                            int32_t *map) {
+    if (!h || l < 0 || l >= (int32_t)h->lev.size()) return LAP_EINVAL;
+    LAP_API_BEGIN
+    const lap::Level &L = h->lev[l];
+    if (row_ptr) LAP_CUDA(cudaMemcpy(row_ptr, L.row_ptr, 8 * (L.n + 1), cudaMemcpyDeviceToHost));
+    if (col && L.nnz) LAP_CUDA(cudaMemcpy(col, L.col, 4 * L.nnz, cudaMemcpyDeviceToHost));
+    if (w && L.nnz) LAP_CUDA(cudaMemcpy(w, L.w, 8 * L.nnz, cudaMemcpyDeviceToHost));
+    if (d) LAP_CUDA(cudaMemcpy(d, L.d, 8 * L.n, cudaMemcpyDeviceToHost));
+    if (map) {
+        if (L.kind == lap::KIND_AGG) LAP_CUDA(cudaMemcpy(map, L.agg, 4 * L.n, cudaMemcpyDeviceToHost));
+        else if (L.kind == lap::KIND_ELIM) LAP_CUDA(cudaMemcpy(map, L.fmap, 4 * L.n, cudaMemcpyDeviceToHost));
+    }
+    return LAP_OK;
+    LAP_API_END
+}
+
+lap_status lap_level_strength(const lap_hierarchy *h, int32_t l, double *S) {
+    if (!h || l < 0 || l >= (int32_t)h->lev.size() || !S) return LAP_EINVAL;
+    const lap::Level &L = h->lev[l];
+    if (!L.S) {
+        lap::set_error("strength not retained (set keep_strength)");
+        return LAP_EINVAL;
+    }
+    LAP_API_BEGIN
+    if (L.nnz) LAP_CUDA(cudaMemcpy(S, L.S, 8 * L.nnz, cudaMemcpyDeviceToHost));
+    return LAP_OK;
+    LAP_API_END
+}
+
+lap_status lap_coarse_pinv(const lap_hierarchy *h, double *pinv) {
+    if (!h || !pinv) return LAP_EINVAL;
+    LAP_API_BEGIN
+    const lap::Level &L = h->lev.back();
+    LAP_CUDA(cudaMemcpy(pinv, L.pinv, 8 * L.n * L.n, cudaMemcpyDeviceToHost));
+    return LAP_OK;
+    LAP_API_END
+}
+
+lap_status lap_perm(const lap_hierarchy *h, int64_t *perm) {
+    if (!h || !perm) return LAP_EINVAL;
+    LAP_API_BEGIN
+    LAP_CUDA(cudaMemcpy(perm, h->perm, 8 * h->n0, cudaMemcpyDeviceToHost));
+    return LAP_OK;
+    LAP_API_END
+}
+
+lap_status lap_spmv(const lap_hierarchy *hc, int32_t l, const double *x, double *y, void *stream) {
+    lap_hierarchy *h = const_cast<lap_hierarchy *>(hc);
+    if (!h || l < 0 || l >= (int32_t)h->lev.size() || !x || !y) return LAP_EINVAL;
+    LAP_API_BEGIN
+    cudaStream_t s = (cudaStream_t)stream;
+    const lap::Level &L = h->lev[l];
+    int64_t n = L.n;
+    lap::DBuf<double> xin, yout;
+    const double *xd = x;
+    double *yd = y;
+    bool xdev = lap::is_device_ptr(x), ydev = lap::is_device_ptr(y);
+    if (!xdev) {
+        xin.alloc(n, s);
+        LAP_CUDA(cudaMemcpyAsync(xin.p, x, 8 * n, cudaMemcpyHostToDevice, s));
+        xd = xin.p;
+    }
+    if (!ydev) {
+        yout.alloc(n, s);
+        yd = yout.p;
+    }
+    lap::EpiArgs a;
+    a.x = xd;
+    a.y = yd;
+    lap::spmv_level(h, L, lap::EPI_SPMV, a, s);
+    if (!ydev) LAP_CUDA(cudaMemcpyAsync(y, yd, 8 * n, cudaMemcpyDeviceToHost, s));
+    LAP_CUDA(cudaStreamSynchronize(s));
+    return LAP_OK;
+    LAP_API_END
+}
+
+lap_status lap_vcycle(lap_hierarchy *h, const double *r, double *z, void *stream) {
+    if (!h || !r || !z) return LAP_EINVAL;
+    LAP_API_BEGIN
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t n = h->lev[0].n;
+    bool rdev = lap::is_device_ptr(r), zdev = lap::is_device_ptr(z);
+    if (rdev) LAP_CUDA(cudaMemcpyAsync(h->pr, r, 8 * n, cudaMemcpyDeviceToDevice, s));
+    else LAP_CUDA(cudaMemcpyAsync(h->pr, r, 8 * n, cudaMemcpyHostToDevice, s));
+    lap::launch_vcycle(h, s);
+    LAP_CUDA(cudaMemcpyAsync(z, h->pz, 8 * n, zdev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+    LAP_CUDA(cudaStreamSynchronize(s));
+    return LAP_OK;
+    LAP_API_END
+}
+
+lap_status lap_get_stats(const lap_hierarchy *h, lap_stats *st) {
+    if (!h || !st) return LAP_EINVAL;
+    *st = h->stats;
+    return LAP_OK;
+}
+
+lap_status lap_bench_smoother(lap_hierarchy *h, int32_t reps, void *stream, double *ms_per_launch,
+                              double *bytes_per_launch, int32_t *level) {
+    if (!h || reps < 1) return LAP_EINVAL;
+    LAP_API_BEGIN
+    cudaStream_t s = (cudaStream_t)stream;
+    int l = -1;
+    for (size_t i = 0; i < h->lev.size(); i++)
+        if (h->lev[i].kind == lap::KIND_AGG) {
+            l = (int)i;
+            break;
+        }
+    if (l < 0) {
+        lap::set_error("no aggregation level");
+        return LAP_EINVAL;
+    }
+    lap::Level &L = h->lev[l];
+    LAP_CUDA(cudaMemsetAsync(L.dv, 0, 8 * L.n, s));
+    LAP_CUDA(cudaMemsetAsync(L.x2, 0, 8 * L.n, s));
+    LAP_CUDA(cudaMemsetAsync(L.b, 0, 8 * L.n, s));
+    lap::EpiArgs a;
+    a.b = L.b;
+    a.dv = L.dv;
+    a.c1 = 0.5;
+    a.c2 = 0.5;
+    a.x = L.x2;
+    a.y = L.t;
+    for (int i = 0; i < 3; i++) lap::spmv_level(h, L, lap::EPI_CHEB, a, s);
+    cudaEvent_t e0, e1;
+    LAP_CUDA(cudaEventCreate(&e0));
+    LAP_CUDA(cudaEventCreate(&e1));
+    LAP_CUDA(cudaEventRecord(e0, s));
+    double *bufs[2] = {L.x2, L.t};
+    for (int i = 0; i < reps; i++) {
+        a.x = bufs[i & 1];
+        a.y = bufs[(i + 1) & 1];
+        lap::spmv_level(h, L, lap::EPI_CHEB, a, s);
+    }
+    LAP_CUDA(cudaEventRecord(e1, s));
+    LAP_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (ms_per_launch) *ms_per_launch = ms / reps;
+    if (bytes_per_launch) *bytes_per_launch = 12.0 * L.nnz + 56.0 * L.n;
+    if (level) *level = l;
+    return LAP_OK;
+    LAP_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,1112 @@
+// setup.cu -- hierarchy construction on the GPU (sm_100a).
+//
+// Implements SURVEY.md O-S0..O-S10 (§3.3-3.6)
+// with kernels; the host loop below only sequences them and reads back a few
+// scalars per level (|F|, m, nnz, lambda-hat).  Every floating reduction that
+// feeds a discrete decision (diagonals, test-vector sweeps, Schur and Galerkin
+// sums) uses the canonical int128 sum of canon.cuh, so the hierarchy is
+// bit-identical to the CPU oracle for any launch geometry.  IEEE rounding of
+// each step is explicit (__dmul_rn/__dadd_rn/__ddiv_rn; the file is compiled
+// with -fmad=false as well).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+#include "canon.cuh"
+#include "lap_internal.cuh"
+
+namespace lap {
+
+int64_t g_kl = 0;  // kernels launched by setup (CUB calls counted once each)
+
+// =========================================================================
+// small utilities
+// =========================================================================
+
+template <class T>
+static void h2d(T *dst, const T *src, int64_t n, cudaStream_t s) {
+    LAP_CUDA(cudaMemcpyAsync(dst, src, sizeof(T) * (size_t)n, cudaMemcpyHostToDevice, s));
+}
+template <class T>
+static T d2h_scalar(const T *src, cudaStream_t s) {
+    T v;
+    LAP_CUDA(cudaMemcpyAsync(&v, src, sizeof(T), cudaMemcpyDeviceToHost, s));
+    LAP_CUDA(cudaStreamSynchronize(s));
+    return v;
+}
+
+static void exclusive_scan_i64(const int64_t *in, int64_t *out, int64_t n, cudaStream_t s) {
+    size_t bytes = 0;
+    LAP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s));
+    DBuf<char> tmp((int64_t)bytes, s);
+    LAP_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, in, out, n, s)); ++g_kl;
+}
+
+// max |v| as an exact order-independent reduction (bit pattern of a
+// non-negative double orders like the value).
+__global__ void k_max_abs(const double *__restrict__ v, int64_t n, unsigned long long *out) {
+    unsigned long long m = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long b = (unsigned long long)__double_as_longlong(fabs(v[i]));
+        m = b > m ? b : m;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long t = __shfl_xor_sync(0xffffffffu, m, o);
+        m = t > m ? t : m;
+    }
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+static double max_abs(const double *v, int64_t n, cudaStream_t s) {
+    DBuf<unsigned long long> r(1, s);
+    LAP_CUDA(cudaMemsetAsync(r.p, 0, 8, s));
+    if (n > 0) {
+        k_max_abs<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(v, n, r.p); ++g_kl;
+        LAP_CHECK_LAUNCH();
+    }
+    unsigned long long b = d2h_scalar(r.p, s);
+    double d;
+    memcpy(&d, &b, 8);
+    return d;
+}
+
+// =========================================================================
+// O-S0 validation: warp per row
+// =========================================================================
+
+__device__ __forceinline__ int64_t find_col(const int64_t *row_ptr, const int32_t *col, int64_t r, int32_t c) {
+    int64_t lo = row_ptr[r], hi = row_ptr[r + 1];
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (col[mid] < c) lo = mid + 1;
+        else hi = mid;
+    }
+    return (lo < row_ptr[r + 1] && col[lo] == c) ? lo : -1;
+}
+
+__global__ void k_validate(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                           const double *__restrict__ w, int *flag) {
+    int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < n; i += nwarps) {
+        int64_t a = row_ptr[i], e = row_ptr[i + 1];
+        if (lane == 0 && e < a) atomicOr(flag, 1);
+        for (int64_t k = a + lane; k < e; k += 32) {
+            int32_t j = col[k];
+            bool bad = (j < 0) || (j >= n) || (j == i) || (k > a && col[k - 1] >= j);
+            double wk = w ? w[k] : 1.0;
+            bad |= !(wk > 0.0) || !isfinite(wk);
+            if (!bad) {
+                int64_t t = find_col(row_ptr, col, j, (int32_t)i);
+                bad |= (t < 0);
+                if (!bad && w) bad |= (__double_as_longlong(w[t]) != __double_as_longlong(wk));
+            }
+            if (bad) atomicOr(flag, 1);
+        }
+    }
+}
+
+// ---- connectivity: lock-free union-find (parents only ever decrease) ----
+__global__ void k_cc_init(int64_t n, int32_t *p) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = (int32_t)i;
+}
+__device__ __forceinline__ int32_t cc_find(int32_t *p, int32_t v) {
+    int32_t cur = p[v];
+    if (cur != v) {
+        int32_t prev = v, nxt;
+        while (cur > (nxt = p[cur])) {  // path halving
+            p[prev] = nxt;
+            prev = cur;
+            cur = nxt;
+        }
+    }
+    return cur;
+}
+__global__ void k_cc_union(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                           int32_t *p) {
+    int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < n; i += nwarps) {
+        for (int64_t k = row_ptr[i] + lane; k < row_ptr[i + 1]; k += 32) {
+            int32_t j = col[k];
+            if (j < i) continue;                       // each undirected edge once
+            int32_t a = cc_find(p, (int32_t)i), b = cc_find(p, j);
+            while (a != b) {
+                if (a < b) {
+                    int32_t t = a; a = b; b = t;
+                }
+                int32_t ret = atomicCAS(&p[a], a, b);  // hook the larger root under the smaller
+                if (ret == a) break;
+                a = ret;
+            }
+        }
+    }
+}
+__global__ void k_cc_count_roots(int64_t n, int32_t *p, unsigned long long *cnt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (cc_find(p, (int32_t)i) == i) atomicAdd(cnt, 1ULL);
+}
+
+static bool is_connected(int64_t n, const int64_t *row_ptr, const int32_t *col, cudaStream_t s) {
+    if (n <= 1) return true;
+    DBuf<int32_t> p(n, s);
+    unsigned g = grid_for(n, 256, 148 * 16);
+    k_cc_init<<<g, 256, 0, s>>>(n, p.p); ++g_kl;
+    k_cc_union<<<grid_for(n * 32, 256, 148 * 16), 256, 0, s>>>(n, row_ptr, col, p.p); ++g_kl;
+    DBuf<unsigned long long> c(1, s);
+    LAP_CUDA(cudaMemsetAsync(c.p, 0, 8, s));
+    k_cc_count_roots<<<g, 256, 0, s>>>(n, p.p, c.p); ++g_kl;
+    LAP_CHECK_LAUNCH();
+    return d2h_scalar(c.p, s) == 1;
+}
+
+// =========================================================================
+// generic: sorted (row,col) terms -> CSR with canonical sums
+// =========================================================================
+
+__global__ void k_quantize(int64_t T, const double *__restrict__ v, int elo, I128 *__restrict__ q) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < T; k += (int64_t)gridDim.x * blockDim.x)
+        q[k] = to_I128(canon_q(v[k], elo));
+}
+
+__global__ void k_terms_to_csr(int64_t U, const uint64_t *__restrict__ ukeys, const I128 *__restrict__ qsum,
+                               int cb, int elo, int32_t *__restrict__ col, double *__restrict__ w) {
+    uint64_t mask = (1ULL << cb) - 1;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < U; u += (int64_t)gridDim.x * blockDim.x) {
+        col[u] = (int32_t)(ukeys[u] & mask);
+        w[u] = canon_result(from_I128(qsum[u]), elo);
+    }
+}
+
+__global__ void k_decode_cols(int64_t T, const uint64_t *__restrict__ k, uint64_t mask, int32_t *__restrict__ c) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < T; i += (int64_t)gridDim.x * blockDim.x)
+        c[i] = (int32_t)(k[i] & mask);
+}
+
+// row_ptr[r] = first u with (ukeys[u] >> cb) >= r
+__global__ void k_row_ptr_from_keys(int64_t nrows, int64_t U, const uint64_t *__restrict__ ukeys, int cb,
+                                    int64_t *__restrict__ row_ptr) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= nrows; r += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t key = ((uint64_t)r) << cb;
+        int64_t lo = 0, hi = U;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if (ukeys[mid] < key) lo = mid + 1;
+            else hi = mid;
+        }
+        row_ptr[r] = lo;
+    }
+}
+
+// d_i = CanonSum of row i (warp per row); instance (e_max, K)
+__global__ void k_row_canon_sum(int64_t n, const int64_t *__restrict__ row_ptr, const double *__restrict__ w,
+                                int elo, double *__restrict__ d) {
+    int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < n; i += nwarps) {
+        i128 acc = 0;
+        for (int64_t k = row_ptr[i] + lane; k < row_ptr[i + 1]; k += 32) acc += canon_q(w[k], elo);
+        acc = warp_sum_i128(acc);
+        if (lane == 0) d[i] = canon_result(acc, elo);
+    }
+}
+
+static void row_sums(int64_t n, int64_t nnz, const int64_t *row_ptr, const double *w, double *d, double *maxw_out,
+                     cudaStream_t s) {
+    double mw = max_abs(w, nnz, s);
+    if (maxw_out) *maxw_out = mw;
+    int elo = canon_elo(ilogb_pos(mw) + 1, nnz);
+    if (n > 0) {
+        k_row_canon_sum<<<grid_for(n * 32, 256, 148 * 16), 256, 0, s>>>(n, row_ptr, w, elo, d); ++g_kl;
+        LAP_CHECK_LAUNCH();
+    }
+}
+
+// Build a level's CSR from unsorted (key=(row<<cb)|col, value) terms whose
+// duplicates are combined by CanonSum with instance (e_max, K).
+static void csr_from_terms(int64_t nrows, int cb, int64_t T, DBuf<uint64_t> &keys, DBuf<double> &vals,
+                           int e_max, int64_t K, bool combine, Level &out, cudaStream_t s) {
+    int rb = bitlen_u64((uint64_t)(nrows > 0 ? nrows : 1));
+    int end_bit = std::min(64, cb + rb);
+    DBuf<uint64_t> k2(T, s);
+    DBuf<double> v2(T, s);
+    if (T > 0) {
+        size_t bytes = 0;
+        LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, k2.p, vals.p, v2.p, T, 0, end_bit, s));
+        DBuf<char> tmp((int64_t)bytes, s);
+        LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, keys.p, k2.p, vals.p, v2.p, T, 0, end_bit, s)); ++g_kl;
+    }
+    keys.release();
+    vals.release();
+    int64_t U = T;
+    out.n = nrows;
+    out.row_ptr = (int64_t *)dalloc(sizeof(int64_t) * (size_t)(nrows + 1), s);
+    if (combine && T > 0) {
+        int elo = canon_elo(e_max, K);
+        DBuf<I128> q(T, s);
+        k_quantize<<<grid_for(T, 256, 148 * 16), 256, 0, s>>>(T, v2.p, elo, q.p); ++g_kl;
+        LAP_CHECK_LAUNCH();
+        v2.release();
+        DBuf<uint64_t> uk(T, s);
+        DBuf<I128> uq(T, s);
+        DBuf<int64_t> nu(1, s);
+        size_t bytes = 0;
+        LAP_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, bytes, k2.p, uk.p, q.p, uq.p, nu.p, I128Add(), T, s));
+        DBuf<char> tmp((int64_t)bytes, s);
+        LAP_CUDA(cub::DeviceReduce::ReduceByKey(tmp.p, bytes, k2.p, uk.p, q.p, uq.p, nu.p, I128Add(), T, s)); ++g_kl;
+        U = d2h_scalar(nu.p, s);
+        out.nnz = U;
+        out.col = (int32_t *)dalloc(sizeof(int32_t) * (size_t)(U + 1), s);
+        out.w = (double *)dalloc(sizeof(double) * (size_t)(U + 1), s);
+        if (U > 0) {
+            k_terms_to_csr<<<grid_for(U, 256, 148 * 16), 256, 0, s>>>(U, uk.p, uq.p, cb, elo, out.col, out.w); ++g_kl;
+            LAP_CHECK_LAUNCH();
+        }
+        k_row_ptr_from_keys<<<grid_for(nrows + 1, 256, 148 * 16), 256, 0, s>>>(nrows, U, uk.p, cb, out.row_ptr); ++g_kl;
+        LAP_CHECK_LAUNCH();
+    } else {
+        out.nnz = T;
+        out.col = (int32_t *)dalloc(sizeof(int32_t) * (size_t)(T + 1), s);
+        out.w = v2.take();
+        if (T > 0) {
+            k_decode_cols<<<grid_for(T, 256, 148 * 16), 256, 0, s>>>(T, k2.p, (1ULL << cb) - 1, out.col); ++g_kl;
+            LAP_CHECK_LAUNCH();
+        }
+        k_row_ptr_from_keys<<<grid_for(nrows + 1, 256, 148 * 16), 256, 0, s>>>(nrows, T, k2.p, cb, out.row_ptr); ++g_kl;
+        LAP_CHECK_LAUNCH();
+    }
+    out.d = (double *)dalloc(sizeof(double) * (size_t)(nrows > 0 ? nrows : 1), s);
+    row_sums(nrows, out.nnz, out.row_ptr, out.w, out.d, &out.maxw, s);
+}
+
+// =========================================================================
+// O-S1 level 0: random order (O-R31) and relabel
+// =========================================================================
+
+__global__ void k_perm_keys(int64_t n, uint64_t salt, uint64_t *keys, int32_t *ids) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        keys[i] = mix64((uint64_t)i ^ salt);
+        ids[i] = (int32_t)i;
+    }
+}
+__global__ void k_perm_from_order(int64_t n, const int32_t *order, int64_t *perm) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+        perm[order[r]] = r;
+}
+__global__ void k_identity_i64(int64_t n, int64_t *p) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = i;
+}
+// emit (newrow<<cb | perm[col], w) for every stored entry; warp per old row
+__global__ void k_relabel_emit(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                               const double *__restrict__ w, const int64_t *__restrict__ perm, int cb,
+                               uint64_t *__restrict__ keys, double *__restrict__ vals) {
+    int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < n; i += nwarps) {
+        uint64_t r = (uint64_t)perm[i];
+        for (int64_t k = row_ptr[i] + lane; k < row_ptr[i + 1]; k += 32) {
+            keys[k] = (r << cb) | (uint64_t)perm[col[k]];
+            vals[k] = w ? w[k] : 1.0;
+        }
+    }
+}
+
+// =========================================================================
+// O-S2 elimination (Alg. 2; O-R17..O-R22) and Schur
+// =========================================================================
+
+__global__ void k_elim_select(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                              int maxdeg, uint64_t salt2, uint8_t *__restrict__ F, unsigned long long *nF) {
+    int64_t cnt = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t a = row_ptr[i], e = row_ptr[i + 1];
+        uint8_t f = 0;
+        if (e - a <= maxdeg) {                       // candidate (O-R19)
+            uint64_t bh = mix64((uint64_t)i ^ salt2);
+            int64_t bj = i;
+            for (int64_t k = a; k < e; k++) {         // oplus_elim over the closed neighbourhood
+                int64_t j = col[k];
+                if (row_ptr[j + 1] - row_ptr[j] > maxdeg) continue;
+                uint64_t hj = mix64((uint64_t)j ^ salt2);
+                if (hj < bh || (hj == bh && j < bj)) { bh = hj; bj = j; }
+            }
+            f = (bj == i);
+        }
+        F[i] = f;
+        cnt += f;
+    }
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(nF, (unsigned long long)cnt);
+}
+
+__global__ void k_flag_not(int64_t n, const uint8_t *F, int64_t *isc) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        isc[i] = F[i] ? 0 : 1;
+}
+__global__ void k_flag_f(int64_t n, const uint8_t *F, int64_t *isf) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        isf[i] = F[i] ? 1 : 0;
+}
+// fmap: C -> coarse index (order preserving, O-R22), F -> -1-slot
+__global__ void k_fmap(int64_t n, const uint8_t *F, const int64_t *cpos, const int64_t *fpos, int32_t *fmap,
+                       int32_t *cid, int32_t *fid) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (F[i]) {
+            fmap[i] = (int32_t)(-1 - fpos[i]);
+            fid[fpos[i]] = (int32_t)i;
+        } else {
+            fmap[i] = (int32_t)cpos[i];
+            cid[cpos[i]] = (int32_t)i;
+        }
+    }
+}
+// number of Schur terms of each C row (thread per coarse row)
+__global__ void k_schur_count(int64_t nc, const int32_t *__restrict__ cid, const int64_t *__restrict__ row_ptr,
+                              const int32_t *__restrict__ col, const uint8_t *__restrict__ F, int64_t *cnt) {
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = cid[a], c = 0;
+        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; k++) {
+            int32_t j = col[k];
+            c += F[j] ? (row_ptr[j + 1] - row_ptr[j] - 1) : 1;
+        }
+        cnt[a] = c;
+    }
+}
+// emit W'[a,b] terms: w_ab, and fl(fl(w_fa*w_fb)/d_f) through each f (O-R25)
+__global__ void k_schur_emit(int64_t nc, const int32_t *__restrict__ cid, const int64_t *__restrict__ row_ptr,
+                             const int32_t *__restrict__ col, const double *__restrict__ w,
+                             const double *__restrict__ d, const uint8_t *__restrict__ F,
+                             const int32_t *__restrict__ fmap, const int64_t *__restrict__ off, int cb,
+                             uint64_t *__restrict__ keys, double *__restrict__ vals) {
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = cid[a], o = off[a];
+        uint64_t ra = ((uint64_t)a) << cb;
+        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; k++) {
+            int32_t j = col[k];
+            if (!F[j]) {
+                keys[o] = ra | (uint64_t)fmap[j];
+                vals[o] = w[k];
+                o++;
+            } else {
+                int64_t kf = find_col(row_ptr, col, j, (int32_t)i);
+                double wfa = w[kf], df = d[j];
+                for (int64_t q = row_ptr[j]; q < row_ptr[j + 1]; q++) {
+                    int32_t bb = col[q];
+                    if (bb == i) continue;
+                    keys[o] = ra | (uint64_t)fmap[bb];
+                    vals[o] = __ddiv_rn(__dmul_rn(wfa, w[q]), df);
+                    o++;
+                }
+            }
+        }
+    }
+}
+// transposed L_FC for the restriction: per coarse c, (f, w_fc/d_f) for f ~ c in F
+__global__ void k_ct_count(int64_t nc, const int32_t *cid, const int64_t *row_ptr, const int32_t *col,
+                           const uint8_t *F, int64_t *cnt) {
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = cid[a], c = 0;
+        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; k++) c += F[col[k]] ? 1 : 0;
+        cnt[a] = c;
+    }
+}
+__global__ void k_ct_fill(int64_t nc, const int32_t *cid, const int64_t *row_ptr, const int32_t *col,
+                          const double *w, const double *d, const uint8_t *F, const int64_t *off, int32_t *ct_f,
+                          double *ct_coef) {
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = cid[a], o = off[a];
+        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; k++) {
+            int32_t j = col[k];
+            if (F[j]) {
+                ct_f[o] = j;
+                ct_coef[o] = w[k] / d[j];
+                o++;
+            }
+        }
+    }
+}
+
+// =========================================================================
+// O-S3 strength
+// =========================================================================
+
+// X0[i,k] = 2 u01(mix64(base ^ (4i+k))) - 1, base = mix64(salt3 ^ (2l+attempt))
+__global__ void k_tv_init(int64_t n, uint64_t base, double *X) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < 4 * n; t += (int64_t)gridDim.x * blockDim.x)
+        X[t] = __dsub_rn(__dmul_rn(2.0, unit_from(mix64(base ^ (uint64_t)t))), 1.0);
+}
+
+// one synchronous damped-Jacobi sweep on the 4 columns; warp per row
+__global__ void k_tv_sweep(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                           const double *__restrict__ w, const double *__restrict__ d, int elo, double omega,
+                           const double *__restrict__ X, double *__restrict__ Xn) {
+    int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < n; i += nwarps) {
+        i128 a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+        for (int64_t k = row_ptr[i] + lane; k < row_ptr[i + 1]; k += 32) {
+            int64_t j = col[k];
+            double wk = w[k];
+            const double2 *xj = reinterpret_cast<const double2 *>(X + 4 * j);
+            double2 u = xj[0], v = xj[1];
+            a0 += canon_q(__dmul_rn(wk, u.x), elo);
+            a1 += canon_q(__dmul_rn(wk, u.y), elo);
+            a2 += canon_q(__dmul_rn(wk, v.x), elo);
+            a3 += canon_q(__dmul_rn(wk, v.y), elo);
+        }
+        a0 = warp_sum_i128(a0);
+        a1 = warp_sum_i128(a1);
+        a2 = warp_sum_i128(a2);
+        a3 = warp_sum_i128(a3);
+        if (lane < 4) {
+            i128 a = lane == 0 ? a0 : lane == 1 ? a1 : lane == 2 ? a2 : a3;
+            double sk = canon_result(a, elo);
+            double di = d[i];
+            double xi = X[4 * i + lane];
+            double r = __dsub_rn(__dmul_rn(di, xi), sk);
+            double q = __ddiv_rn(r, di);
+            Xn[4 * i + lane] = __dsub_rn(xi, __dmul_rn(omega, q));
+        }
+    }
+}
+
+__device__ __forceinline__ double dot4_rn(const double *a, const double *b) {
+    double s = __dmul_rn(a[0], b[0]);
+    s = __dadd_rn(s, __dmul_rn(a[1], b[1]));
+    s = __dadd_rn(s, __dmul_rn(a[2], b[2]));
+    s = __dadd_rn(s, __dmul_rn(a[3], b[3]));
+    return s;
+}
+
+// C_ij (O-R5) and row max M_i; warp per row
+__global__ void k_affinity(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                           const double *__restrict__ X, int power, double *__restrict__ C, double *__restrict__ M) {
+    int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < n; i += nwarps) {
+        double xi[4] = {X[4 * i], X[4 * i + 1], X[4 * i + 2], X[4 * i + 3]};
+        double ni = dot4_rn(xi, xi);
+        double mx = 0.0;
+        for (int64_t k = row_ptr[i] + lane; k < row_ptr[i + 1]; k += 32) {
+            int64_t j = col[k];
+            double xj[4] = {X[4 * j], X[4 * j + 1], X[4 * j + 2], X[4 * j + 3]};
+            double nj = dot4_rn(xj, xj);
+            double g = dot4_rn(xi, xj);
+            double num = __dmul_rn(g, g);
+            double den = power == 2 ? __dmul_rn(__dmul_rn(ni, ni), __dmul_rn(nj, nj)) : __dmul_rn(ni, nj);
+            double c = den > 0.0 ? __ddiv_rn(num, den) : 0.0;
+            C[k] = c;
+            mx = c > mx ? c : mx;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            double t = __shfl_xor_sync(0xffffffffu, mx, o);
+            mx = t > mx ? t : mx;
+        }
+        if (lane == 0) M[i] = mx;
+    }
+}
+// S_ij = C_ij / max(M_i, M_j), 0 if that max is 0 (O-R16); in place
+__global__ void k_normalize(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                            const double *__restrict__ M, double *__restrict__ CS) {
+    int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < n; i += nwarps) {
+        double mi = M[i];
+        for (int64_t k = row_ptr[i] + lane; k < row_ptr[i + 1]; k += 32) {
+            double mj = M[col[k]];
+            double den = mi > mj ? mi : mj;
+            CS[k] = den > 0.0 ? __ddiv_rn(CS[k], den) : 0.0;
+        }
+    }
+}
+
+// =========================================================================
+// O-S4 voting (Alg. 3; O-R8..O-R15)
+// =========================================================================
+enum { ST_DEC = 0, ST_UND = 1, ST_SEED = 2 };
+
+__global__ void k_vote_init(int64_t n, int8_t *st, int32_t *idx, int32_t *votes) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        st[i] = ST_UND;
+        idx[i] = (int32_t)i;
+        votes[i] = 0;
+    }
+}
+
+// d = S_filt oplus_agg.otimes_agg status for Undecided rows; warp per row.
+// Reads round-start state st/idx, writes nst/nidx and votes.
+__global__ void k_vote_round(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                             const double *__restrict__ S, double filt, const int8_t *__restrict__ st,
+                             int8_t *__restrict__ nst, int32_t *__restrict__ nidx, int32_t *__restrict__ votes) {
+    int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < n; i += nwarps) {
+        if (st[i] != ST_UND) continue;                      // only Undecided act (O-R9)
+        int br = -1;
+        double bs = 0.0;
+        int32_t bj = 0x7fffffff;
+        for (int64_t k = row_ptr[i] + lane; k < row_ptr[i + 1]; k += 32) {
+            double sv = S[k];
+            if (sv == 0.0 || sv < filt) continue;           // filter 2^-t, w != 0 (O-R13)
+            int32_t j = col[k];
+            int r = st[j];
+            if (r == ST_DEC) continue;                      // (O-R12)
+            if (r > br || (r == br && (sv > bs || (sv == bs && j < bj)))) { br = r; bs = sv; bj = j; }
+        }
+        for (int o = 16; o > 0; o >>= 1) {                  // warp arg-max under (rank, S, -j)
+            int r2 = __shfl_xor_sync(0xffffffffu, br, o);
+            double s2 = __shfl_xor_sync(0xffffffffu, bs, o);
+            int32_t j2 = __shfl_xor_sync(0xffffffffu, bj, o);
+            if (r2 > br || (r2 == br && (s2 > bs || (s2 == bs && j2 < bj)))) { br = r2; bs = s2; bj = j2; }
+        }
+        if (lane == 0 && br >= 0) {
+            if (br == ST_SEED) {
+                nst[i] = ST_DEC;
+                nidx[i] = bj;
+            } else {
+                atomicAdd(&votes[bj], 1);
+            }
+        }
+    }
+}
+__global__ void k_vote_promote(int64_t n, int8_t *nst, const int32_t *votes, int thr) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        if (nst[i] == ST_UND && votes[i] >= thr) nst[i] = ST_SEED;
+}
+__global__ void k_root_flags(int64_t n, const int8_t *st, int64_t *flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        flag[i] = st[i] != ST_DEC ? 1 : 0;
+}
+__global__ void k_agg_ids(int64_t n, const int8_t *st, const int32_t *idx, const int64_t *rid, int32_t *agg) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        agg[i] = (int32_t)(st[i] != ST_DEC ? rid[i] : rid[idx[i]]);
+}
+
+// =========================================================================
+// O-S5 Galerkin (O-R24)
+// =========================================================================
+
+__global__ void k_gal_count(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                            const int32_t *__restrict__ agg, int64_t *cnt) {
+    int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < n; i += nwarps) {
+        int32_t a = agg[i];
+        int64_t c = 0;
+        for (int64_t k = row_ptr[i] + lane; k < row_ptr[i + 1]; k += 32) c += (agg[col[k]] != a);
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) cnt[i] = c;
+    }
+}
+__global__ void k_gal_emit(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                           const double *__restrict__ w, const int32_t *__restrict__ agg,
+                           const int64_t *__restrict__ off, int cb, uint64_t *__restrict__ keys,
+                           double *__restrict__ vals) {
+    int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < n; i += nwarps) {
+        uint64_t a = (uint64_t)agg[i];
+        int64_t o = off[i];
+        for (int64_t base = row_ptr[i]; base < row_ptr[i + 1]; base += 32) {
+            int64_t k = base + lane;
+            bool take = false;
+            uint64_t b = 0;
+            if (k < row_ptr[i + 1]) {
+                b = (uint64_t)agg[col[k]];
+                take = (b != a);
+            }
+            unsigned m = __ballot_sync(0xffffffffu, take);
+            if (take) {
+                int64_t p = o + __popc(m & ((1u << lane) - 1));
+                keys[p] = (a << cb) | b;
+                vals[p] = w[k];
+            }
+            o += __popc(m);
+        }
+    }
+}
+
+// =========================================================================
+// O-S6 lambda-hat: Lanczos on D^-1/2 L D^-1/2 (O-R3)
+// =========================================================================
+
+__global__ void k_lz_init(int64_t n, uint64_t base, const double *d, double *v, double *rs) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        v[i] = 2.0 * unit_from(mix64(base ^ (uint64_t)i)) - 1.0;
+        rs[i] = 1.0 / sqrt(d[i]);
+    }
+}
+__global__ void k_scale_by(int64_t n, double *v, const double *nrm2) {
+    double f = 1.0 / sqrt(*nrm2);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) v[i] *= f;
+}
+__global__ void k_hadamard(int64_t n, const double *a, const double *b, double *o) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) o[i] = a[i] * b[i];
+}
+// y = rs o y - beta_prev vprev  (sc[0] = alpha, sc[1] = beta^2 of previous step, sc[3]=stopped)
+__global__ void k_lz_a(int64_t n, double *y, const double *rs, const double *vp, const double *sc) {
+    if (sc[3] != 0.0) return;
+    double bp = sc[4];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = rs[i] * y[i] - bp * vp[i];
+}
+__global__ void k_lz_b(int64_t n, double *y, const double *v, const double *sc) {
+    if (sc[3] != 0.0) return;
+    double a = sc[0];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] -= a * v[i];
+}
+// record alpha/beta, test breakdown, advance (single thread)
+__global__ void k_lz_record(double *sc, double *alpha, double *beta, int *k, int step) {
+    if (sc[3] != 0.0) return;
+    double a = sc[0], b = sqrt(sc[1]);
+    alpha[*k] = a;
+    beta[*k] = b;
+    *k += 1;
+    sc[2] = b;
+    if (b <= 1e-14 * fabs(a)) sc[3] = 1.0;
+    sc[4] = b;
+}
+__global__ void k_lz_c(int64_t n, double *v, double *vp, const double *y, const double *sc) {
+    if (sc[3] != 0.0) return;
+    double b = sc[2];
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        vp[i] = v[i];
+        v[i] = y[i] / b;
+    }
+}
+// largest eigenvalue of the k x k tridiagonal by Sturm bisection (one thread)
+__global__ void k_tridiag_max(const double *alpha, const double *beta, const int *kp, double *out) {
+    int k = *kp;
+    if (k <= 0) { *out = 0.0; return; }
+    double lo = alpha[0], hi = alpha[0];
+    for (int i = 0; i < k; i++) {
+        double r = (i > 0 ? fabs(beta[i - 1]) : 0.0) + (i < k - 1 ? fabs(beta[i]) : 0.0);
+        lo = fmin(lo, alpha[i] - r);
+        hi = fmax(hi, alpha[i] + r);
+    }
+    for (int it = 0; it < 200; it++) {
+        double mid = 0.5 * (lo + hi);
+        if (mid <= lo || mid >= hi) break;
+        int le = 0;
+        double q = 1.0;
+        for (int i = 0; i < k; i++) {
+            q = (alpha[i] - mid) - (i > 0 ? beta[i - 1] * beta[i - 1] / q : 0.0);
+            if (q == 0.0) q = -1e-300;
+            le += q < 0.0;
+        }
+        if (le == k) hi = mid;
+        else lo = mid;
+    }
+    *out = hi;
+}
+
+static double lanczos(lap_hierarchy *h, Level &L, int l, cudaStream_t s) {
+    int64_t n = L.n;
+    int steps = h->p.lanczos_steps;
+    DBuf<double> v(n, s), vp(n, s), y(n, s), u(n, s), rs(n, s), sc(8, s), al(64, s), be(64, s), lam(1, s);
+    DBuf<int> k(1, s);
+    LAP_CUDA(cudaMemsetAsync(vp.p, 0, sizeof(double) * n, s));
+    LAP_CUDA(cudaMemsetAsync(sc.p, 0, sizeof(double) * 8, s));
+    LAP_CUDA(cudaMemsetAsync(k.p, 0, sizeof(int), s));
+    uint64_t base = mix64(salt_of(h->p.seed, 4) ^ (uint64_t)(2 * l));
+    unsigned g = grid_for(n, 256, 148 * 8);
+    k_lz_init<<<g, 256, 0, s>>>(n, base, L.d, v.p, rs.p); ++g_kl;
+    dot(h, v.p, v.p, n, sc.p + 5, s);
+    k_scale_by<<<g, 256, 0, s>>>(n, v.p, sc.p + 5); ++g_kl;
+    for (int j = 0; j < steps && j < 64; j++) {
+        k_hadamard<<<g, 256, 0, s>>>(n, rs.p, v.p, u.p); ++g_kl;
+        EpiArgs a;
+        a.x = u.p;
+        a.y = y.p;
+        spmv_level(h, L, EPI_SPMV, a, s);
+        k_lz_a<<<g, 256, 0, s>>>(n, y.p, rs.p, vp.p, sc.p); ++g_kl;
+        dot(h, y.p, v.p, n, sc.p + 0, s);
+        k_lz_b<<<g, 256, 0, s>>>(n, y.p, v.p, sc.p); ++g_kl;
+        dot(h, y.p, y.p, n, sc.p + 1, s);
+        k_lz_record<<<1, 1, 0, s>>>(sc.p, al.p, be.p, k.p, j); ++g_kl;
+        k_lz_c<<<g, 256, 0, s>>>(n, v.p, vp.p, y.p, sc.p); ++g_kl;
+        LAP_CHECK_LAUNCH();
+    }
+    k_tridiag_max<<<1, 1, 0, s>>>(al.p, be.p, k.p, lam.p); ++g_kl;
+    LAP_CHECK_LAUNCH();
+    h->cur.edges += (int64_t)steps * L.nnz;
+    return d2h_scalar(lam.p, s);
+}
+
+// =========================================================================
+// O-S10 coarsest pseudo-inverse (O-R26): ground the last vertex,
+// in-place Gauss-Jordan inverse of the SPD block, project with I - J/n.
+// =========================================================================
+
+__global__ void k_dense_fill(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *w,
+                             const double *d, double *A) {
+    int64_t g = n - 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g; i += (int64_t)gridDim.x * blockDim.x) {
+        A[i * g + i] = d[i];
+        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; k++)
+            if (col[k] < g) A[i * g + col[k]] = -w[k];
+    }
+}
+// one pivot step of the in-place Gauss-Jordan (sweep) inversion
+__global__ void k_gj_pivot_row(int64_t g, int64_t kk, double *A, double *colbuf, double *rowbuf) {
+    double piv = A[kk * g + kk];
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < g; t += (int64_t)gridDim.x * blockDim.x) {
+        colbuf[t] = A[t * g + kk];
+        rowbuf[t] = (t == kk) ? 1.0 / piv : A[kk * g + t] / piv;
+    }
+}
+__global__ void k_gj_update(int64_t g, int64_t kk, double *A, const double *colbuf, const double *rowbuf) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < g * g; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = t / g, j = t % g;
+        if (i == kk) {
+            A[t] = rowbuf[j];
+        } else {
+            double c = colbuf[i];
+            A[t] = (j == kk) ? -c * rowbuf[kk] : A[t] - c * rowbuf[j];
+        }
+    }
+}
+// single-CTA variant for small g (one launch for all pivots)
+__global__ void k_gj_small(int64_t g, double *A, double *colbuf, double *rowbuf) {
+    for (int64_t kk = 0; kk < g; kk++) {
+        double piv = A[kk * g + kk];
+        for (int64_t t = threadIdx.x; t < g; t += blockDim.x) {
+            colbuf[t] = A[t * g + kk];
+            rowbuf[t] = (t == kk) ? 1.0 / piv : A[kk * g + t] / piv;
+        }
+        __syncthreads();
+        for (int64_t t = threadIdx.x; t < g * g; t += blockDim.x) {
+            int64_t i = t / g, j = t % g;
+            if (i == kk) A[t] = rowbuf[j];
+            else {
+                double c = colbuf[i];
+                A[t] = (j == kk) ? -c * rowbuf[kk] : A[t] - c * rowbuf[j];
+            }
+        }
+        __syncthreads();
+    }
+}
+// G = [[Ainv,0],[0,0]] (n x n); pinv = G - r_i/n - c_j/n + tot/n^2 (row sums r, col sums c)
+__global__ void k_pinv_sums(int64_t n, const double *Ai, double *rsum, double *csum) {
+    int64_t g = n - 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double r = 0.0, c = 0.0;
+        if (i < g)
+            for (int64_t j = 0; j < g; j++) {
+                r += Ai[i * g + j];
+                c += Ai[j * g + i];
+            }
+        rsum[i] = r;
+        csum[i] = c;
+    }
+}
+__global__ void k_pinv_total(int64_t n, const double *rsum, double *tot) {
+    double t = 0.0;
+    for (int64_t i = 0; i < n; i++) t += rsum[i];
+    *tot = t;
+}
+__global__ void k_pinv_assemble(int64_t n, const double *Ai, const double *rsum, const double *csum,
+                                const double *tot, double *P) {
+    int64_t g = n - 1;
+    double T = *tot, nn = (double)n;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * n; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t i = t / n, j = t % n;
+        double G = (i < g && j < g) ? Ai[i * g + j] : 0.0;
+        P[t] = G - rsum[i] / nn - csum[j] / nn + T / (nn * nn);
+    }
+}
+
+static void coarse_pinv(Level &L, cudaStream_t s) {
+    int64_t n = L.n;
+    L.pinv = (double *)dalloc(sizeof(double) * (size_t)(n * n), s);
+    if (n <= 1) {
+        LAP_CUDA(cudaMemsetAsync(L.pinv, 0, sizeof(double) * (size_t)(n * n > 0 ? n * n : 1), s));
+        return;
+    }
+    int64_t g = n - 1;
+    DBuf<double> A(g * g, s), cb(g, s), rb(g, s), rsum(n, s), csum(n, s), tot(1, s);
+    LAP_CUDA(cudaMemsetAsync(A.p, 0, sizeof(double) * (size_t)(g * g), s));
+    k_dense_fill<<<grid_for(g, 128, 148 * 4), 128, 0, s>>>(n, L.row_ptr, L.col, L.w, L.d, A.p); ++g_kl;
+    if (g <= 1024) {
+        k_gj_small<<<1, 1024, 0, s>>>(g, A.p, cb.p, rb.p); ++g_kl;
+    } else {
+        for (int64_t kk = 0; kk < g; kk++) {
+            k_gj_pivot_row<<<grid_for(g, 256, 148 * 4), 256, 0, s>>>(g, kk, A.p, cb.p, rb.p); ++g_kl;
+            k_gj_update<<<grid_for(g * g, 256, 148 * 16), 256, 0, s>>>(g, kk, A.p, cb.p, rb.p); ++g_kl;
+        }
+    }
+    k_pinv_sums<<<grid_for(n, 128, 148 * 4), 128, 0, s>>>(n, A.p, rsum.p, csum.p); ++g_kl;
+    k_pinv_total<<<1, 1, 0, s>>>(n, rsum.p, tot.p); ++g_kl;
+    k_pinv_assemble<<<grid_for(n * n, 256, 148 * 8), 256, 0, s>>>(n, A.p, rsum.p, csum.p, tot.p, L.pinv); ++g_kl;
+    LAP_CHECK_LAUNCH();
+}
+
+// =========================================================================
+// per-level builders
+// =========================================================================
+
+static int64_t elim_select(lap_hierarchy *h, Level &L, DBuf<uint8_t> &F, cudaStream_t s) {
+    F.alloc(L.n, s);
+    DBuf<unsigned long long> nF(1, s);
+    LAP_CUDA(cudaMemsetAsync(nF.p, 0, 8, s));
+    k_elim_select<<<grid_for(L.n, 256, 148 * 16), 256, 0, s>>>(L.n, L.row_ptr, L.col, h->p.elim_max_degree,
+                                                                salt_of(h->p.seed, 2), F.p, nF.p); ++g_kl;
+    LAP_CHECK_LAUNCH();
+    h->cur.edges += L.nnz;
+    return (int64_t)d2h_scalar(nF.p, s);
+}
+
+static void build_elim_level(lap_hierarchy *h, Level &L, const DBuf<uint8_t> &F, int64_t nF, Level &N,
+                             cudaStream_t s) {
+    int64_t n = L.n, nc = n - nF;
+    L.kind = KIND_ELIM;
+    L.nF = nF;
+    DBuf<int64_t> isc(n, s), cpos(n, s), isf(n, s), fpos(n, s);
+    unsigned g = grid_for(n, 256, 148 * 16);
+    k_flag_not<<<g, 256, 0, s>>>(n, F.p, isc.p); ++g_kl;
+    k_flag_f<<<g, 256, 0, s>>>(n, F.p, isf.p); ++g_kl;
+    LAP_CHECK_LAUNCH();
+    exclusive_scan_i64(isc.p, cpos.p, n, s);
+    exclusive_scan_i64(isf.p, fpos.p, n, s);
+    L.fmap = (int32_t *)dalloc(sizeof(int32_t) * n, s);
+    L.cid = (int32_t *)dalloc(sizeof(int32_t) * (nc + 1), s);
+    L.fid = (int32_t *)dalloc(sizeof(int32_t) * (nF + 1), s);
+    k_fmap<<<g, 256, 0, s>>>(n, F.p, cpos.p, fpos.p, L.fmap, L.cid, L.fid); ++g_kl;
+    LAP_CHECK_LAUNCH();
+    // terms of the Schur complement
+    DBuf<int64_t> cnt(nc + 1, s), off(nc + 1, s);
+    LAP_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int64_t) * (nc + 1), s));
+    unsigned gc = grid_for(nc, 128, 148 * 16);
+    k_schur_count<<<gc, 128, 0, s>>>(nc, L.cid, L.row_ptr, L.col, F.p, cnt.p); ++g_kl;
+    LAP_CHECK_LAUNCH();
+    exclusive_scan_i64(cnt.p, off.p, nc + 1, s);
+    int64_t T = d2h_scalar(off.p + nc, s);
+    int cb = bitlen_u64((uint64_t)(nc > 0 ? nc : 1));
+    DBuf<uint64_t> keys(T, s);
+    DBuf<double> vals(T, s);
+    k_schur_emit<<<gc, 128, 0, s>>>(nc, L.cid, L.row_ptr, L.col, L.w, L.d, F.p, L.fmap, off.p, cb, keys.p, vals.p); ++g_kl;
+    LAP_CHECK_LAUNCH();
+    int e_max = ilogb_pos(L.maxw) + 1;
+    csr_from_terms(nc, cb, T, keys, vals, e_max, 4 * L.nnz, true, N, s);
+    // transposed L_FC for the restriction P^T b
+    DBuf<int64_t> tc(nc + 1, s);
+    LAP_CUDA(cudaMemsetAsync(tc.p, 0, sizeof(int64_t) * (nc + 1), s));
+    k_ct_count<<<gc, 128, 0, s>>>(nc, L.cid, L.row_ptr, L.col, F.p, tc.p); ++g_kl;
+    L.ct_ptr = (int64_t *)dalloc(sizeof(int64_t) * (nc + 1), s);
+    exclusive_scan_i64(tc.p, L.ct_ptr, nc + 1, s);
+    int64_t TT = d2h_scalar(L.ct_ptr + nc, s);
+    L.ct_f = (int32_t *)dalloc(sizeof(int32_t) * (TT + 1), s);
+    L.ct_coef = (double *)dalloc(sizeof(double) * (TT + 1), s);
+    k_ct_fill<<<gc, 128, 0, s>>>(nc, L.cid, L.row_ptr, L.col, L.w, L.d, F.p, L.ct_ptr, L.ct_f, L.ct_coef); ++g_kl;
+    LAP_CHECK_LAUNCH();
+    h->cur.edges += L.nnz;
+}
+
+// strength + voting for one attempt; returns m, fills L.agg
+static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt, DBuf<double> &S, cudaStream_t s) {
+    int64_t n = L.n, nnz = L.nnz;
+    const lap_params &p = h->p;
+    unsigned gw = grid_for(n * 32, 256, 148 * 16), ge = grid_for(n, 256, 148 * 16);
+    // test vectors
+    DBuf<double> X(4 * n, s), Xn(4 * n, s), M(n, s);
+    uint64_t base = mix64(salt_of(p.seed, 3) ^ (uint64_t)(2 * l + attempt));
+    k_tv_init<<<grid_for(4 * n, 256, 148 * 16), 256, 0, s>>>(n, base, X.p); ++g_kl;
+    LAP_CHECK_LAUNCH();
+    int ew = ilogb_pos(L.maxw);
+    for (int sw = 0; sw < p.tv_sweeps; sw++) {
+        double mx = max_abs(X.p, 4 * n, s);
+        int e_max = mx > 0.0 ? ew + ilogb_pos(mx) + 2 : ew + 1;
+        k_tv_sweep<<<gw, 256, 0, s>>>(n, L.row_ptr, L.col, L.w, L.d, canon_elo(e_max, nnz), p.tv_omega, X.p, Xn.p); ++g_kl;
+        LAP_CHECK_LAUNCH();
+        std::swap(X.p, Xn.p);
+        h->cur.edges += nnz;
+    }
+    // affinity + normalisation
+    k_affinity<<<gw, 256, 0, s>>>(n, L.row_ptr, L.col, X.p, p.affinity_power, S.p, M.p); ++g_kl;
+    k_normalize<<<gw, 256, 0, s>>>(n, L.row_ptr, L.col, M.p, S.p); ++g_kl;
+    LAP_CHECK_LAUNCH();
+    h->cur.edges += 2 * nnz;
+    // voting rounds (Alg. 3)
+    DBuf<int8_t> st(n, s), nst(n, s);
+    DBuf<int32_t> idx(n, s), nidx(n, s), votes(n, s);
+    k_vote_init<<<ge, 256, 0, s>>>(n, st.p, idx.p, votes.p); ++g_kl;
+    for (int t = 1; t <= p.vote_rounds; t++) {
+        double filt = ldexp(1.0, -t);
+        LAP_CUDA(cudaMemcpyAsync(nst.p, st.p, n, cudaMemcpyDeviceToDevice, s));
+        LAP_CUDA(cudaMemcpyAsync(nidx.p, idx.p, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
+        k_vote_round<<<gw, 256, 0, s>>>(n, L.row_ptr, L.col, S.p, filt, st.p, nst.p, nidx.p, votes.p); ++g_kl;
+        k_vote_promote<<<ge, 256, 0, s>>>(n, nst.p, votes.p, p.vote_threshold); ++g_kl;
+        LAP_CHECK_LAUNCH();
+        std::swap(st.p, nst.p);
+        std::swap(idx.p, nidx.p);
+        h->cur.edges += nnz;
+    }
+    // renumber roots by ascending id (O-R15)
+    DBuf<int64_t> flag(n + 1, s), rid(n + 1, s);
+    LAP_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int64_t) * (n + 1), s));
+    k_root_flags<<<ge, 256, 0, s>>>(n, st.p, flag.p); ++g_kl;
+    exclusive_scan_i64(flag.p, rid.p, n + 1, s);
+    if (!L.agg) L.agg = (int32_t *)dalloc(sizeof(int32_t) * n, s);
+    k_agg_ids<<<ge, 256, 0, s>>>(n, st.p, idx.p, rid.p, L.agg); ++g_kl;
+    LAP_CHECK_LAUNCH();
+    return d2h_scalar(rid.p + n, s);
+}
+
+static void galerkin(lap_hierarchy *h, Level &L, Level &N, cudaStream_t s) {
+    int64_t n = L.n, m = L.m;
+    DBuf<int64_t> cnt(n + 1, s), off(n + 1, s);
+    LAP_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int64_t) * (n + 1), s));
+    unsigned gw = grid_for(n * 32, 256, 148 * 16);
+    k_gal_count<<<gw, 256, 0, s>>>(n, L.row_ptr, L.col, L.agg, cnt.p); ++g_kl;
+    LAP_CHECK_LAUNCH();
+    exclusive_scan_i64(cnt.p, off.p, n + 1, s);
+    int64_t T = d2h_scalar(off.p + n, s);
+    int cb = bitlen_u64((uint64_t)(m > 0 ? m : 1));
+    DBuf<uint64_t> keys(T, s);
+    DBuf<double> vals(T, s);
+    k_gal_emit<<<gw, 256, 0, s>>>(n, L.row_ptr, L.col, L.w, L.agg, off.p, cb, keys.p, vals.p); ++g_kl;
+    LAP_CHECK_LAUNCH();
+    csr_from_terms(m, cb, T, keys, vals, ilogb_pos(L.maxw) + 1, L.nnz, true, N, s);
+    h->cur.edges += L.nnz;
+}
+
+// =========================================================================
+// O-S9 hierarchy loop
+// =========================================================================
+
+void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
+    const lap_params &p = h->p;
+    int64_t n = g->n;
+    h->n0 = n;
+    // --- input on device
+    DBuf<int64_t> rp_in;
+    DBuf<int32_t> col_in;
+    DBuf<double> w_in;
+    const int64_t *rp;
+    const int32_t *col;
+    const double *w;
+    int64_t nnz;
+    if (g->on_device) {
+        rp = g->row_ptr;
+        col = g->col;
+        w = g->w;
+        nnz = d2h_scalar(g->row_ptr + n, s);
+    } else {
+        nnz = g->row_ptr[n];
+        rp_in.alloc(n + 1, s);
+        col_in.alloc(nnz, s);
+        h2d(rp_in.p, g->row_ptr, n + 1, s);
+        if (nnz) h2d(col_in.p, g->col, nnz, s);
+        if (g->w) {
+            w_in.alloc(nnz, s);
+            if (nnz) h2d(w_in.p, g->w, nnz, s);
+        }
+        rp = rp_in.p;
+        col = col_in.p;
+        w = g->w ? w_in.p : nullptr;
+    }
+    if (nnz >= (int64_t)1 << 40 || n >= ((int64_t)1 << 31) - 1) throw Error{LAP_EINVAL, "graph too large"};
+    // --- O-S0 validate
+    {
+        DBuf<int> flag(1, s);
+        LAP_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+        if (n > 0) {
+            int64_t first = d2h_scalar(rp, s);
+            if (first != 0) throw Error{LAP_EGRAPH, "row_ptr[0] != 0"};
+            k_validate<<<grid_for(n * 32, 256, 148 * 16), 256, 0, s>>>(n, rp, col, w, flag.p); ++g_kl;
+            LAP_CHECK_LAUNCH();
+        }
+        if (d2h_scalar(flag.p, s)) throw Error{LAP_EGRAPH, "graph is not a valid symmetric positive-weight adjacency"};
+        if (!is_connected(n, rp, col, s)) throw Error{LAP_EDISCONNECTED, "graph is disconnected"};
+    }
+    // --- O-S1 level 0
+    h->perm = (int64_t *)dalloc(sizeof(int64_t) * (size_t)n, s);
+    if (p.random_order && n > 1) {
+        DBuf<uint64_t> k1(n, s), k2(n, s);
+        DBuf<int32_t> i1(n, s), i2(n, s);
+        k_perm_keys<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, salt_of(p.seed, 1), k1.p, i1.p); ++g_kl;
+        LAP_CHECK_LAUNCH();
+        size_t bytes = 0;
+        LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k1.p, k2.p, i1.p, i2.p, n, 0, 64, s));
+        DBuf<char> tmp((int64_t)bytes, s);
+        LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, k1.p, k2.p, i1.p, i2.p, n, 0, 64, s)); ++g_kl;
+        k_perm_from_order<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, i2.p, h->perm); ++g_kl;
+    } else {
+        k_identity_i64<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, h->perm); ++g_kl;
+    }
+    LAP_CHECK_LAUNCH();
+    h->lev.clear();
+    h->lev.reserve(64);
+    h->lev.emplace_back();
+    {
+        Level &L0 = h->lev[0];
+        int cb = bitlen_u64((uint64_t)(n > 0 ? n : 1));
+        DBuf<uint64_t> keys(nnz, s);
+        DBuf<double> vals(nnz, s);
+        if (nnz) {
+            k_relabel_emit<<<grid_for(n * 32, 256, 148 * 16), 256, 0, s>>>(n, rp, col, w, h->perm, cb, keys.p, vals.p); ++g_kl;
+            LAP_CHECK_LAUNCH();
+        }
+        csr_from_terms(n, cb, nnz, keys, vals, 0, 0, false, L0, s);
+    }
+    rp_in.release();
+    col_in.release();
+    w_in.release();
+
+    bool prev_elim = false;
+    for (int l = 0;; l++) {
+        Level &L = h->lev[l];
+        build_row_bins(L, s);
+        if (L.n + L.nnz <= p.coarse_nnz || l == p.max_levels - 1 || l == 63) {     // O-R27
+            L.kind = KIND_COARSEST;
+            break;
+        }
+        if (p.elim_enable && !prev_elim) {                                          // O-R21
+            DBuf<uint8_t> F;
+            int64_t nF = elim_select(h, L, F, s);
+            if (20 * nF > L.n) {                                                    // O-R20
+                h->lev.emplace_back();
+                Level &L2 = h->lev[l];
+                build_elim_level(h, L2, F, nF, h->lev[l + 1], s);
+                prev_elim = true;
+                continue;
+            }
+        }
+        // aggregation level
+        L.kind = KIND_AGG;
+        L.lambda = lanczos(h, L, l, s);
+        DBuf<double> S(L.nnz, s);
+        int64_t m = L.n;
+        for (int attempt = 0; attempt < 2 && m == L.n; attempt++) m = aggregate_attempt(h, L, l, attempt, S, s);
+        if (m == L.n) {                                                             // stalled twice (O-R28)
+            if (L.agg) dfree(L.agg, s);
+            L.agg = nullptr;
+            L.kind = KIND_COARSEST;
+            h->status = LAP_ESTALL;
+            if (L.n > 8192) throw Error{LAP_ESTALL, "aggregation stalled on a level with more than 8192 vertices"};
+            break;
+        }
+        L.m = m;
+        if (p.keep_strength) L.S = S.take();
+        h->lev.emplace_back();
+        Level &L2 = h->lev[l];
+        galerkin(h, L2, h->lev[l + 1], s);
+        prev_elim = false;
+    }
+    coarse_pinv(h->lev.back(), s);
+}
+
+}  // namespace lap

@@ -1,0 +1,236 @@
+"""ctypes binding of liblap.so (include/lap.h): argument marshalling only.
+
+Every step of setup and solve runs in the CUDA kernels of liblap.so; there is
+no CPU fallback.  If the library is missing or fails to load, importing this
+module raises.  Vectors may be numpy arrays (host) or CUDA torch tensors
+(device pointers are passed straight through).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblap.so")
+
+LAP_OK, LAP_EINVAL, LAP_EGRAPH, LAP_EDISCONNECTED, LAP_ENOMEM, LAP_ECUDA, LAP_ENCCL, LAP_ENOCONV, LAP_ESTALL = range(9)
+KIND_AGG, KIND_ELIM, KIND_COARSEST = 0, 1, 2
+
+
+class LapError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"liblap status {code}: {msg}")
+        self.code = code
+
+
+class lap_graph(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("row_ptr", ctypes.c_void_p), ("col", ctypes.c_void_p),
+                ("w", ctypes.c_void_p), ("on_device", ctypes.c_int32)]
+
+
+class lap_params(ctypes.Structure):
+    _fields_ = [
+        ("tol", ctypes.c_double), ("max_iters", ctypes.c_int32), ("cheby_degree", ctypes.c_int32),
+        ("cheby_lo", ctypes.c_double), ("cheby_hi", ctypes.c_double), ("lanczos_steps", ctypes.c_int32),
+        ("elim_max_degree", ctypes.c_int32), ("elim_enable", ctypes.c_int32), ("n_test_vectors", ctypes.c_int32),
+        ("tv_sweeps", ctypes.c_int32), ("tv_omega", ctypes.c_double), ("vote_rounds", ctypes.c_int32),
+        ("vote_threshold", ctypes.c_int32), ("coarse_nnz", ctypes.c_int64), ("max_levels", ctypes.c_int32),
+        ("seed", ctypes.c_uint64), ("random_order", ctypes.c_int32), ("affinity_power", ctypes.c_int32),
+        ("keep_strength", ctypes.c_int32), ("use_graphs", ctypes.c_int32),
+    ]
+
+
+class lap_stats(ctypes.Structure):
+    _fields_ = [("kernel_launches", ctypes.c_int64), ("spmv_edges", ctypes.c_int64), ("spmv_bytes", ctypes.c_int64),
+                ("setup_ms", ctypes.c_double), ("solve_ms", ctypes.c_double), ("vcycles", ctypes.c_int32)]
+
+
+EXPORTS = [
+    "lap_params_default", "lap_last_error", "lap_version", "lap_setup", "lap_solve", "lap_free",
+    "lap_num_levels", "lap_level_info", "lap_level_export", "lap_level_strength", "lap_coarse_pinv",
+    "lap_perm", "lap_spmv", "lap_vcycle", "lap_get_stats", "lap_bench_smoother",
+]
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    if not os.path.exists(path):
+        raise ImportError(f"liblap.so not built at {path}; run __graft_entry__.build() "
+                          "(there is no CPU fallback)")
+    L = ctypes.CDLL(path)
+    P, i32, i64, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    pi32, pi64, pdbl = ctypes.POINTER(i32), ctypes.POINTER(i64), ctypes.POINTER(dbl)
+    sig = {
+        "lap_params_default": (None, [ctypes.POINTER(lap_params)]),
+        "lap_last_error": (ctypes.c_char_p, []),
+        "lap_version": (ctypes.c_char_p, []),
+        "lap_setup": (ctypes.c_int, [ctypes.POINTER(lap_graph), ctypes.POINTER(lap_params), P, ctypes.POINTER(P)]),
+        "lap_solve": (ctypes.c_int, [P, P, P, dbl, pi32, pdbl, P]),
+        "lap_free": (None, [P]),
+        "lap_num_levels": (ctypes.c_int, [P, pi32]),
+        "lap_level_info": (ctypes.c_int, [P, i32, pi32, pi64, pi64, pdbl]),
+        "lap_level_export": (ctypes.c_int, [P, i32, P, P, P, P, P]),
+        "lap_level_strength": (ctypes.c_int, [P, i32, P]),
+        "lap_coarse_pinv": (ctypes.c_int, [P, P]),
+        "lap_perm": (ctypes.c_int, [P, P]),
+        "lap_spmv": (ctypes.c_int, [P, i32, P, P, P]),
+        "lap_vcycle": (ctypes.c_int, [P, P, P, P]),
+        "lap_get_stats": (ctypes.c_int, [P, ctypes.POINTER(lap_stats)]),
+        "lap_bench_smoother": (ctypes.c_int, [P, i32, P, pdbl, pdbl, pi32]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    return L
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        _lib = load()
+    return _lib
+
+
+def _check(rc, allow=()):
+    if rc != LAP_OK and rc not in allow:
+        raise LapError(rc, lib().lap_last_error().decode())
+    return rc
+
+
+def _ptr(a):
+    """Device pointer of a CUDA tensor or host pointer of a numpy array."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return ctypes.c_void_p(a.data_ptr())
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def _stream(stream):
+    if stream is None:
+        return None
+    if hasattr(stream, "cuda_stream"):
+        return ctypes.c_void_p(stream.cuda_stream)
+    return ctypes.c_void_p(int(stream))
+
+
+def lap_params_default(**kw) -> lap_params:
+    p = lap_params()
+    lib().lap_params_default(ctypes.byref(p))
+    for k, v in kw.items():
+        if not hasattr(p, k):
+            raise AttributeError(k)
+        setattr(p, k, v)
+    return p
+
+
+class Hierarchy:
+    """lap_setup(graph, params) -> hierarchy ; .solve(b) -> (x, iters, residual)."""
+
+    def __init__(self, graph, params: lap_params | None = None, stream=None, **kw):
+        self.params = params if params is not None else lap_params_default(**kw)
+        dev = hasattr(graph.row_ptr, "data_ptr") and getattr(graph.row_ptr, "is_cuda", False)
+        if not dev:
+            self._keep = (np.ascontiguousarray(graph.row_ptr, np.int64), np.ascontiguousarray(graph.col, np.int32),
+                          None if graph.w is None else np.ascontiguousarray(graph.w, np.float64))
+        else:
+            self._keep = (graph.row_ptr, graph.col, graph.w)
+        g = lap_graph(int(graph.n), _ptr(self._keep[0]), _ptr(self._keep[1]), _ptr(self._keep[2]), 1 if dev else 0)
+        self._h = ctypes.c_void_p()
+        self.status = _check(lib().lap_setup(ctypes.byref(g), ctypes.byref(self.params), _stream(stream),
+                                             ctypes.byref(self._h)), allow=(LAP_ESTALL,))
+        self._keep = None
+        self.n = int(graph.n)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().lap_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- the two calls of the method
+    def solve(self, b, x=None, tol: float = 0.0, stream=None):
+        if x is None:
+            x = np.zeros(self.n) if not hasattr(b, "data_ptr") else b.new_zeros(self.n)
+        it = ctypes.c_int32(0)
+        rr = ctypes.c_double(0.0)
+        rc = _check(lib().lap_solve(self._h, _ptr(b), _ptr(x), tol, ctypes.byref(it), ctypes.byref(rr),
+                                    _stream(stream)), allow=(LAP_ENOCONV,))
+        return x, int(it.value), float(rr.value), rc
+
+    # ---- introspection
+    @property
+    def nlev(self) -> int:
+        v = ctypes.c_int32(0)
+        _check(lib().lap_num_levels(self._h, ctypes.byref(v)))
+        return v.value
+
+    def level_info(self, l: int):
+        k, n, z, lam = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_double()
+        _check(lib().lap_level_info(self._h, l, ctypes.byref(k), ctypes.byref(n), ctypes.byref(z), ctypes.byref(lam)))
+        return k.value, n.value, z.value, lam.value
+
+    def level(self, l: int) -> dict:
+        kind, n, z, lam = self.level_info(l)
+        rp = np.zeros(n + 1, np.int64)
+        col = np.zeros(max(z, 1), np.int32)
+        w = np.zeros(max(z, 1), np.float64)
+        d = np.zeros(max(n, 1), np.float64)
+        mp = np.zeros(max(n, 1), np.int32)
+        _check(lib().lap_level_export(self._h, l, _ptr(rp), _ptr(col), _ptr(w), _ptr(d), _ptr(mp)))
+        out = dict(kind=kind, n=n, nnz=z, lam=lam, row_ptr=rp, col=col[:z], w=w[:z], d=d[:n])
+        if kind == KIND_AGG:
+            out["agg"] = mp[:n]
+            out["m"] = int(mp[:n].max()) + 1 if n else 0
+        elif kind == KIND_ELIM:
+            out["fmap"] = mp[:n]
+            out["nF"] = int((mp[:n] < 0).sum())
+        else:
+            P = np.zeros(n * n)
+            _check(lib().lap_coarse_pinv(self._h, _ptr(P)))
+            out["pinv"] = P.reshape(n, n)
+        return out
+
+    def strength(self, l: int) -> np.ndarray:
+        _, n, z, _ = self.level_info(l)
+        S = np.zeros(max(z, 1))
+        _check(lib().lap_level_strength(self._h, l, _ptr(S)))
+        return S[:z]
+
+    def perm(self) -> np.ndarray:
+        p = np.zeros(self.n, np.int64)
+        _check(lib().lap_perm(self._h, _ptr(p)))
+        return p
+
+    def spmv(self, l: int, x, y=None, stream=None):
+        if y is None:
+            y = np.zeros(len(x)) if not hasattr(x, "data_ptr") else x.new_zeros(len(x))
+        _check(lib().lap_spmv(self._h, l, _ptr(x), _ptr(y), _stream(stream)))
+        return y
+
+    def vcycle(self, r, z=None, stream=None):
+        if z is None:
+            z = np.zeros(len(r)) if not hasattr(r, "data_ptr") else r.new_zeros(len(r))
+        _check(lib().lap_vcycle(self._h, _ptr(r), _ptr(z), _stream(stream)))
+        return z
+
+    def stats(self) -> dict:
+        s = lap_stats()
+        _check(lib().lap_get_stats(self._h, ctypes.byref(s)))
+        return {k: getattr(s, k) for k, _ in s._fields_}
+
+    def bench_smoother(self, reps: int = 50, stream=None):
+        ms, by, lv = ctypes.c_double(), ctypes.c_double(), ctypes.c_int32()
+        _check(lib().lap_bench_smoother(self._h, reps, _stream(stream), ctypes.byref(ms), ctypes.byref(by),
+                                        ctypes.byref(lv)))
+        return ms.value, by.value, lv.value

@@ -1,0 +1,193 @@
+"""GPU parity: liblap.so (through the C ABI) against the CPU oracle.
+
+Contract (BASELINE.json north_star):
+  - aggregates, F sets, every coarse operator (col, w, d) and S: bit-exact
+  - SpMV: |dy_i| <= 1e-12 (d_i |x_i| + sum_j w_ij |x_j|)   (O-P2)
+  - lambda-hat: <= 1e-10 relative
+  - solve: true relative residual <= 1e-8, iterations within +-1 of the oracle
+"""
+import numpy as np
+import pytest
+
+import lapgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1705_06266_b200 as P
+    from paper_1705_06266_b200 import build
+    build.build()
+    return P
+
+
+def _bits(a):
+    return np.asarray(a, np.float64).view(np.int64)
+
+
+def compare_hierarchy(h, ho, check_S=False):
+    assert h.nlev == ho.nlev
+    for l in range(ho.nlev):
+        a, o = h.level(l), ho.level(l)
+        assert (a["kind"], a["n"], a["nnz"]) == (o.kind, o.n, o.nnz), f"level {l}"
+        assert np.array_equal(a["row_ptr"], o.row_ptr), f"row_ptr level {l}"
+        assert np.array_equal(a["col"], o.col), f"col level {l}"
+        assert np.array_equal(_bits(a["w"]), _bits(o.w)), f"w level {l}"
+        assert np.array_equal(_bits(a["d"]), _bits(o.d)), f"d level {l}"
+        if o.kind == oracle.AGG:
+            assert np.array_equal(a["agg"], o.agg), f"agg level {l}"
+            assert abs(a["lam"] - o.lam) <= 1e-10 * o.lam, (a["lam"], o.lam)
+            if check_S:
+                assert np.array_equal(_bits(h.strength(l)), _bits(o.S)), f"S level {l}"
+        elif o.kind == oracle.ELIM:
+            assert np.array_equal(a["fmap"], o.fmap), f"fmap level {l}"
+        else:
+            assert np.allclose(a["pinv"], o.pinv, rtol=0, atol=1e-9 * max(1.0, np.abs(o.pinv).max()))
+
+
+def spmv_bound(row_ptr, col, w, d, x):
+    rows = np.repeat(np.arange(len(d)), np.diff(row_ptr))
+    s = np.zeros(len(d))
+    np.add.at(s, rows, np.abs(w) * np.abs(x[col]))
+    return 1e-12 * (np.abs(d) * np.abs(x) + s)
+
+
+SMALL = [
+    lambda: lapgen.grid2d(64, 64, "cfg1"),
+    lambda: lapgen.grid2d(37, 29),
+    lambda: lapgen.grid3d(12),
+    lambda: lapgen.rmat(12),
+    lambda: lapgen.barabasi_albert(5000, 8),
+    lambda: lapgen.random_connected(3000, 9000, 7),
+    lambda: lapgen.path(777),
+    lambda: lapgen.star(40000),          # hub row > 16384 entries: split-chunk SpMV path
+    lambda: lapgen.complete(70),
+]
+
+
+@pytest.mark.parametrize("mk", SMALL, ids=["cfg1", "grid37x29", "grid3d12", "rmat12", "ba5000", "rand3000",
+                                           "path777", "star40000", "K70"])
+def test_hierarchy_spmv_vcycle_solve_parity(P, mk):
+    g = mk()
+    h = P.Hierarchy(g, keep_strength=1)
+    ho = oracle.Hierarchy(g)
+    compare_hierarchy(h, ho, check_S=True)
+    assert np.array_equal(h.perm(), ho.perm())
+    rng = np.random.default_rng(0)
+    # H1 on every level, device pointers through the C ABI
+    for l in range(ho.nlev):
+        o = ho.level(l)
+        x = rng.standard_normal(o.n)
+        y = h.spmv(l, torch.from_numpy(x).cuda()).cpu().numpy()
+        yo = oracle.spmv(o.n, o.row_ptr, o.col, o.w, o.d, x)
+        assert np.all(np.abs(y - yo) <= spmv_bound(o.row_ptr, o.col, o.w, o.d, x) + 1e-300), f"spmv level {l}"
+    # one V-cycle (O-S7) in the internal numbering
+    r = rng.standard_normal(g.n)
+    r -= r.mean()
+    z = h.vcycle(torch.from_numpy(r).cuda()).cpu().numpy()
+    zo = ho.vcycle(0, r)
+    assert np.abs(z - zo).max() <= 1e-9 * np.abs(zo).max()
+    # full solve, host buffers (O-S8)
+    b = lapgen.rhs(g.n, seed=3)
+    x, it, rr, rc = h.solve(b)
+    xo, ito, rro, rco = ho.solve(b)
+    assert rc == rco == 0
+    assert rr <= 1e-8 and abs(it - ito) <= 1, (it, ito, rr)
+    assert np.abs(x - xo).max() <= 1e-6 * np.abs(xo).max()
+    assert abs(x.mean()) <= 1e-10 * np.abs(x).max()
+
+
+def test_degenerate_inputs(P):
+    # n = 1: coarsest only, x = 0
+    g1 = lapgen.Graph(1, np.array([0, 0], np.int64), np.zeros(0, np.int32), np.zeros(0))
+    h = P.Hierarchy(g1)
+    x, it, rr, rc = h.solve(np.array([5.0]))
+    assert h.nlev == 1 and it == 0 and x.tolist() == [0.0]
+    # constant RHS projects to zero
+    g = lapgen.grid2d(20, 20)
+    h = P.Hierarchy(g)
+    x, it, rr, rc = h.solve(np.full(g.n, 2.0))
+    assert it == 0 and np.all(x == 0)
+    # single edge
+    g2 = lapgen.path(2)
+    x, it, rr, rc = P.Hierarchy(g2).solve(np.array([1.0, -1.0]))
+    assert np.allclose(x, [0.5, -0.5])
+
+
+def test_invalid_graphs_rejected(P):
+    bad_sym = lapgen.Graph(2, np.array([0, 1, 1]), np.array([1], np.int32), np.array([1.0]))
+    with pytest.raises(P.LapError) as e:
+        P.Hierarchy(bad_sym)
+    assert e.value.code == P.LAP_EGRAPH
+    neg = lapgen.Graph(2, np.array([0, 1, 2]), np.array([1, 0], np.int32), np.array([-1.0, -1.0]))
+    with pytest.raises(P.LapError) as e:
+        P.Hierarchy(neg)
+    assert e.value.code == P.LAP_EGRAPH
+    loop = lapgen.Graph(2, np.array([0, 2, 3]), np.array([0, 1, 0], np.int32), np.ones(3))
+    with pytest.raises(P.LapError) as e:
+        P.Hierarchy(loop)
+    assert e.value.code == P.LAP_EGRAPH
+    disc = lapgen.csr_from_edges(4, [0, 2], [1, 3])
+    with pytest.raises(P.LapError) as e:
+        P.Hierarchy(disc)
+    assert e.value.code == P.LAP_EDISCONNECTED
+
+
+def test_device_graph_and_determinism(P):
+    g = lapgen.rmat(11)
+    dev = lapgen.Graph(g.n, torch.from_numpy(g.row_ptr).cuda(), torch.from_numpy(g.col).cuda(),
+                       torch.from_numpy(g.w).cuda())
+    h1 = P.Hierarchy(dev)
+    h2 = P.Hierarchy(g)
+    compare_hierarchy(h1, oracle.Hierarchy(g))
+    b = lapgen.rhs(g.n)
+    x1, i1, r1, _ = h1.solve(b)
+    x2, i2, r2, _ = h2.solve(b)
+    assert i1 == i2 and np.array_equal(_bits(x1), _bits(x2))   # bitwise run-to-run reproducible
+
+
+@pytest.mark.parametrize("kw", [dict(random_order=0), dict(affinity_power=2), dict(seed=5),
+                                dict(elim_enable=0), dict(cheby_degree=3), dict(use_graphs=0)])
+def test_parameter_variants(P, kw):
+    g = lapgen.rmat(11)
+    h = P.Hierarchy(g, **kw)
+    okw = {k: v for k, v in kw.items() if k != "use_graphs"}
+    ho = oracle.Hierarchy(g, **okw)
+    compare_hierarchy(h, ho)
+    b = lapgen.rhs(g.n)
+    x, it, rr, rc = h.solve(b)
+    xo, ito, _, _ = ho.solve(b)
+    assert rr <= 1e-8 and abs(it - ito) <= 1
+
+
+FULL = {2: "cfg2", 3: "cfg3", 4: "cfg4"}
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_full_size_configs(P, k):
+    """BASELINE.json configs at full size, default (bench) launch configuration:
+    bit-exact hierarchy, sampled-row SpMV check, solve residual and iterations."""
+    g = lapgen.config(k)
+    h = P.Hierarchy(g)
+    ho = oracle.Hierarchy(g)
+    compare_hierarchy(h, ho)
+    rng = np.random.default_rng(k)
+    o = ho.level(0)
+    x = rng.standard_normal(o.n)
+    y = h.spmv(0, torch.from_numpy(x).cuda()).cpu().numpy()
+    rows = rng.choice(o.n, 20000, replace=False)
+    yo = oracle.spmv(o.n, o.row_ptr, o.col, o.w, o.d, x)
+    bound = spmv_bound(o.row_ptr, o.col, o.w, o.d, x)
+    assert np.all(np.abs(y[rows] - yo[rows]) <= bound[rows] + 1e-300)
+    b = lapgen.rhs(g.n)
+    bt = torch.from_numpy(b).cuda()
+    xg, it, rr, rc = h.solve(bt)
+    xo, ito, rro, _ = ho.solve(b)
+    assert rc == 0 and rr <= 1e-8 and abs(it - ito) <= 1, (it, ito, rr)
+    xg = xg.cpu().numpy()
+    assert np.abs(xg - xo).max() <= 1e-6 * np.abs(xo).max()
