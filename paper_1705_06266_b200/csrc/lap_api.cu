@@ -12,6 +12,16 @@ void vcycle_apply(lap_hierarchy *h, const double *r, double *z, cudaStream_t s);
 
 static thread_local std::string g_err;
 void set_error(const std::string &m) { g_err = m; }
+static bool g_capturing = false;
+bool debug_sync() {
+    if (g_capturing) return false;
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("LAP_DEBUG_SYNC");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
 
 static bool g_pool_init = false;
 void *dalloc(size_t bytes, cudaStream_t s) {
@@ -108,8 +118,11 @@ void finalize_solve_structures(lap_hierarchy *h, cudaStream_t s) {
     LAP_CUDA(cudaMemsetAsync(h->scal, 0, 8 * 16, s));
     int64_t np = std::max<int64_t>(1024, spmv_partial_slots(h->lev[0]));
     for (auto &L : h->lev) np = std::max<int64_t>(np, spmv_partial_slots(L));
-    h->partials = (double *)dalloc(8 * np, s);
-    h->npartials = np;
+    if (np > h->npartials) {
+        dfree(h->partials, s);
+        h->partials = (double *)dalloc(8 * np, s);
+        h->npartials = np;
+    }
     LAP_CUDA(cudaMallocHost(&h->host_scal, 64));
 }
 
@@ -158,9 +171,12 @@ static void capture_vcycle(lap_hierarchy *h) {
     h->cur = Stats{};
     cudaGraph_t g;
     LAP_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    g_capturing = true;
     try {
         vcycle_apply(h, h->pr, h->pz, cs);
+        g_capturing = false;
     } catch (...) {
+        g_capturing = false;
         cudaStreamEndCapture(cs, &g);
         cudaStreamDestroy(cs);
         throw;
@@ -262,6 +278,8 @@ lap_status lap_setup(const lap_graph *g, const lap_params *pp, void *stream, lap
         LAP_CUDA(cudaEventRecord(e0, s));
         h->cur = lap::Stats{};
         int64_t kl0 = lap::g_kl;
+        h->npartials = 1024;  // reduction scratch used during setup (Lanczos dots)
+        h->partials = (double *)lap::dalloc(8 * h->npartials, s);
         lap::build_hierarchy(h, g, s);
         lap::finalize_solve_structures(h, s);
         LAP_CUDA(cudaEventRecord(e1, s));

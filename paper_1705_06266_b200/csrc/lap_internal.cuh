@@ -19,15 +19,24 @@ struct Error {
 };
 void set_error(const std::string &m);
 
-#define LAP_CUDA(call)                                                                   \
-    do {                                                                                 \
-        cudaError_t _e = (call);                                                         \
-        if (_e != cudaSuccess)                                                           \
-            throw ::lap::Error{_e == cudaErrorMemoryAllocation ? LAP_ENOMEM : LAP_ECUDA, \
-                               std::string(#call) + ": " + cudaGetErrorString(_e)};      \
+#define LAP_STR2(x) #x
+#define LAP_STR(x) LAP_STR2(x)
+#define LAP_CUDA(call)                                                                          \
+    do {                                                                                        \
+        cudaError_t _e = (call);                                                                \
+        if (_e != cudaSuccess)                                                                  \
+            throw ::lap::Error{_e == cudaErrorMemoryAllocation ? LAP_ENOMEM : LAP_ECUDA,        \
+                               std::string(__FILE__ ":" LAP_STR(__LINE__) " ") + #call + ": " + \
+                                   cudaGetErrorString(_e)};                                     \
     } while (0)
 
-#define LAP_CHECK_LAUNCH() LAP_CUDA(cudaGetLastError())
+// LAP_DEBUG_SYNC=1 in the environment: synchronise after every launch check
+bool debug_sync();
+#define LAP_CHECK_LAUNCH()                                   \
+    do {                                                     \
+        LAP_CUDA(cudaGetLastError());                        \
+        if (::lap::debug_sync()) LAP_CUDA(cudaDeviceSynchronize()); \
+    } while (0)
 
 // ---------------------------------------------------------------- memory
 // Stream-ordered device allocation (cudaMallocAsync pool).

@@ -780,7 +780,7 @@ __global__ void k_gj_update(int64_t g, int64_t kk, double *A, const double *colb
     }
 }
 // single-CTA variant for small g (one launch for all pivots)
-__global__ void k_gj_small(int64_t g, double *A, double *colbuf, double *rowbuf) {
+__global__ void __launch_bounds__(1024, 1) k_gj_small(int64_t g, double *A, double *colbuf, double *rowbuf) {
     for (int64_t kk = 0; kk < g; kk++) {
         double piv = A[kk * g + kk];
         for (int64_t t = threadIdx.x; t < g; t += blockDim.x) {
