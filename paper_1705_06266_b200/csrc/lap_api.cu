@@ -40,6 +40,12 @@ void *dalloc(size_t bytes, cudaStream_t s) {
     if (e != cudaSuccess)
         throw Error{e == cudaErrorMemoryAllocation ? LAP_ENOMEM : LAP_ECUDA,
                     std::string("cudaMallocAsync: ") + cudaGetErrorString(e)};
+    static int poison = -1;  // LAP_POISON=1: fill new allocations with NaN bytes (tests)
+    if (poison < 0) {
+        const char *v = getenv("LAP_POISON");
+        poison = (v && v[0] == '1') ? 1 : 0;
+    }
+    if (poison) cudaMemsetAsync(p, 0xFF, bytes ? bytes : 1, s);
     return p;
 }
 void dfree(void *p, cudaStream_t s) {
@@ -76,21 +82,13 @@ __global__ void k_sub_mean2(int64_t n, double *v, const double *sum) {
         v[i] -= mean;
 }
 
-static void build_members(Level &L, cudaStream_t s) {
-    int64_t n = L.n;
-    DBuf<int32_t> ids(n, s), keys2(n, s);
-    L.members = (int32_t *)dalloc(sizeof(int32_t) * n, s);
-    L.mem_ptr = (int64_t *)dalloc(sizeof(int64_t) * (L.m + 1), s);
-    k_iota<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(n, ids.p);
-    int end_bit = 1;
-    while (end_bit < 31 && ((int64_t)1 << end_bit) <= L.m) end_bit++;
-    size_t bytes = 0;
-    LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, L.agg, keys2.p, ids.p, L.members, n, 0, end_bit, s));
-    DBuf<char> tmp((int64_t)bytes, s);
-    LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, L.agg, keys2.p, ids.p, L.members, n, 0, end_bit, s));
-    k_lower_bound_i32<<<grid_for(L.m + 1, 256, 148 * 8), 256, 0, s>>>(L.m, n, keys2.p, L.mem_ptr);
-    g_kl += 3;
-    LAP_CHECK_LAUNCH();
+__global__ void k_gather_i32map(int64_t n, const int32_t *map, const double *in, double *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in[map[i]];
+}
+__global__ void k_scatter_i32map(int64_t n, const int32_t *map, const double *in, double *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[map[i]] = in[i];
 }
 
 void finalize_solve_structures(lap_hierarchy *h, cudaStream_t s) {
@@ -108,9 +106,9 @@ void finalize_solve_structures(lap_hierarchy *h, cudaStream_t s) {
             L.cheb_theta = 0.5 * (b + a);
             L.cheb_delta = 0.5 * (b - a);
             L.cheb_sigma = L.cheb_theta / L.cheb_delta;
-            build_members(L, s);
         }
     }
+    build_transfers(h, s);
     int64_t n0 = h->lev[0].n;
     double **vecs[] = {&h->pb, &h->px, &h->pr, &h->pz, &h->pp, &h->pq, &h->stage_in, &h->stage_out};
     for (double **v : vecs) *v = (double *)dalloc(8 * (n0 > 0 ? n0 : 1), s);
@@ -127,9 +125,10 @@ void finalize_solve_structures(lap_hierarchy *h, cudaStream_t s) {
 }
 
 static void free_level(Level &L, cudaStream_t s) {
-    void *ps[] = {L.row_ptr, L.col, L.w, L.d, L.dinv, L.bins.rows, L.bins.chunk_row_first, L.bins.chunk_partial,
-                  L.agg, L.mem_ptr, L.members, L.S, L.fmap, L.cid, L.fid, L.ct_ptr, L.ct_f, L.ct_coef,
-                  L.pinv, L.b, L.x, L.x2, L.t, L.r, L.dv};
+    void *ps[] = {L.row_ptr, L.col, L.w, L.d, L.agg, L.S, L.fmap, L.cid, L.fid, L.ct_ptr, L.ct_f, L.ct_coef,
+                  L.pinv, L.sid, L.spos, L.srp, L.scol, L.sw, L.sd, L.tile_first, L.chunk_first, L.chunk_part,
+                  L.agg_s, L.mem_ptr, L.members, L.cid_s, L.flist, L.ct_ptr_s, L.ct_f_s, L.ct_coef_s, L.fmap_s,
+                  L.pinv_s, L.b, L.x, L.x2, L.t, L.r, L.dv};
     for (void *p : ps) dfree(p, s);
 }
 
@@ -316,7 +315,8 @@ void lap_free(lap_hierarchy *h) {
     cudaDeviceSynchronize();
     if (h->vgraph) cudaGraphExecDestroy(h->vgraph);
     for (auto &L : h->lev) lap::free_level(L, s);
-    void *ps[] = {h->perm, h->pb, h->px, h->pr, h->pz, h->pp, h->pq, h->scal, h->partials, h->stage_in, h->stage_out};
+    void *ps[] = {h->perm, h->cmap, h->pb, h->px, h->pr, h->pz, h->pp, h->pq, h->scal, h->partials, h->stage_in,
+                  h->stage_out};
     for (void *p : ps) lap::dfree(p, s);
     if (h->host_scal) cudaFreeHost(h->host_scal);
     cudaStreamSynchronize(s);
@@ -345,7 +345,7 @@ lap_status lap_solve(lap_hierarchy *h, const double *b, double *x, double tol, i
         bd = h->stage_in;
     }
     unsigned g = lap::grid_for(n, 256, 148 * 8);
-    lap::k_scatter_perm<<<g, 256, 0, s>>>(n, h->perm, bd, h->pb);            // b' = Pi b
+    lap::k_scatter_perm<<<g, 256, 0, s>>>(n, h->cmap, bd, h->pb);            // b' = Pi b (storage order)
     lap::dot(h, h->pb, nullptr, n, h->scal + 7, s);
     lap::k_sub_mean2<<<g, 256, 0, s>>>(n, h->pb, h->scal + 7);               // project out 1
     h->cur.launches += 2;
@@ -356,7 +356,7 @@ lap_status lap_solve(lap_hierarchy *h, const double *b, double *x, double tol, i
     lap::run_pcg(h, tol, &it, &rr, &conv, s);
     bool xdev = lap::is_device_ptr(x);
     double *xd = xdev ? x : h->stage_out;
-    lap::k_gather_perm<<<g, 256, 0, s>>>(n, h->perm, h->px, xd);             // x = Pi^T x'
+    lap::k_gather_perm<<<g, 256, 0, s>>>(n, h->cmap, h->px, xd);             // x = Pi^T x'
     h->cur.launches++;
     LAP_CHECK_LAUNCH();
     if (!xdev) LAP_CUDA(cudaMemcpyAsync(x, xd, 8 * n, cudaMemcpyDeviceToHost, s));
@@ -460,10 +460,15 @@ lap_status lap_spmv(const lap_hierarchy *hc, int32_t l, const double *x, double 
         yout.alloc(n, s);
         yd = yout.p;
     }
+    lap::DBuf<double> xs(n, s), ys(n, s);  // logical <-> storage order
+    unsigned g = lap::grid_for(n, 256, 148 * 8);
+    lap::k_gather_i32map<<<g, 256, 0, s>>>(n, L.sid, xd, xs.p);
     lap::EpiArgs a;
-    a.x = xd;
-    a.y = yd;
+    a.x = xs.p;
+    a.y = ys.p;
     lap::spmv_level(h, L, lap::EPI_SPMV, a, s);
+    lap::k_scatter_i32map<<<g, 256, 0, s>>>(n, L.sid, ys.p, yd);
+    LAP_CHECK_LAUNCH();
     if (!ydev) LAP_CUDA(cudaMemcpyAsync(y, yd, 8 * n, cudaMemcpyDeviceToHost, s));
     LAP_CUDA(cudaStreamSynchronize(s));
     return LAP_OK;
@@ -476,10 +481,14 @@ lap_status lap_vcycle(lap_hierarchy *h, const double *r, double *z, void *stream
     cudaStream_t s = (cudaStream_t)stream;
     int64_t n = h->lev[0].n;
     bool rdev = lap::is_device_ptr(r), zdev = lap::is_device_ptr(z);
-    if (rdev) LAP_CUDA(cudaMemcpyAsync(h->pr, r, 8 * n, cudaMemcpyDeviceToDevice, s));
-    else LAP_CUDA(cudaMemcpyAsync(h->pr, r, 8 * n, cudaMemcpyHostToDevice, s));
+    const lap::Level &L0 = h->lev[0];
+    unsigned g = lap::grid_for(n, 256, 148 * 8);
+    LAP_CUDA(cudaMemcpyAsync(h->stage_in, r, 8 * n, rdev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    lap::k_gather_i32map<<<g, 256, 0, s>>>(n, L0.sid, h->stage_in, h->pr);      // logical -> storage
     lap::launch_vcycle(h, s);
-    LAP_CUDA(cudaMemcpyAsync(z, h->pz, 8 * n, zdev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+    lap::k_scatter_i32map<<<g, 256, 0, s>>>(n, L0.sid, h->pz, h->stage_out);    // storage -> logical
+    LAP_CHECK_LAUNCH();
+    LAP_CUDA(cudaMemcpyAsync(z, h->stage_out, 8 * n, zdev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
     LAP_CUDA(cudaStreamSynchronize(s));
     return LAP_OK;
     LAP_API_END
@@ -508,6 +517,7 @@ lap_status lap_bench_smoother(lap_hierarchy *h, int32_t reps, void *stream, doub
     }
     lap::Level &L = h->lev[l];
     LAP_CUDA(cudaMemsetAsync(L.dv, 0, 8 * L.n, s));
+    LAP_CUDA(cudaMemsetAsync(L.t, 0, 8 * L.n, s));
     LAP_CUDA(cudaMemsetAsync(L.x2, 0, 8 * L.n, s));
     LAP_CUDA(cudaMemsetAsync(L.b, 0, 8 * L.n, s));
     lap::EpiArgs a;

@@ -75,57 +75,72 @@ struct DBuf {
 // ---------------------------------------------------------------- levels
 enum { KIND_AGG = 0, KIND_ELIM = 1, KIND_COARSEST = 2 };
 
-// Degree-binned row schedule for the SpMV (H0).  Bins by stored degree:
-//   0: deg <= 8      -> 8 lanes per row
-//   1: 9..32         -> 32 lanes (warp) per row
-//   2: 33..1024      -> warp per row, unrolled
-//   3: 1025..16384   -> one 256-thread block per row
-//   4: > 16384       -> split into 16384-entry chunks (block per chunk) + ordered combine
-constexpr int NBINS = 5;
+// Solve-phase storage (H0).  The hierarchy's logical ids are fixed by the
+// method (random order, aggregate numbering: bit-identical to the oracle);
+// the solve kernels run on a per-level STORAGE ORDER chosen for the GPU:
+//   key(level 0)   = caller's vertex id (undoes Pi_rand for locality)
+//   key(aggregate) = min storage position of its members
+//   key(C vertex)  = its storage position on the finer level
+// sorted by (degree class, key), so each class is a contiguous row range:
+//   class 0: deg <= 64        CSR-stream tiles of <= TILE_NNZ entries (block per tile)
+//   class 1: 65..1024         warp per row
+//   class 2: 1025..16384      256-thread block per row
+//   class 3: > 16384          HUB_CHUNK-entry chunks (block per chunk) + ordered combine
+constexpr int NCLASS = 4;
+constexpr int64_t SHORT_MAX = 64;
+constexpr int64_t TILE_NNZ = 2048;
 constexpr int64_t HUB_CHUNK = 16384;
-
-struct RowBins {
-    int64_t cnt[NBINS] = {0, 0, 0, 0, 0};
-    int64_t off[NBINS + 1] = {0, 0, 0, 0, 0, 0};
-    int32_t *rows = nullptr;       // permutation of rows grouped by bin (nullptr: identity, single bin)
-    bool identity = false;
-    int identity_bin = 0;
-    // hub chunks (bin 4)
-    int64_t nchunks = 0;
-    int64_t *chunk_row_first = nullptr;  // per hub row: first chunk index (nhub+1)
-    double *chunk_partial = nullptr;     // per chunk partial sum
-};
 
 struct Level {
     int kind = KIND_COARSEST;
     int64_t n = 0, nnz = 0;
+    // logical CSR (setup numbering, bit-identical to the oracle)
     int64_t *row_ptr = nullptr;
     int32_t *col = nullptr;
     double *w = nullptr;
     double *d = nullptr;
-    double *dinv = nullptr;
     double maxw = 0.0;
-    RowBins bins;
-    // aggregation
+    // aggregation (logical)
     double lambda = 0.0;
     int64_t m = 0;
     int32_t *agg = nullptr;
-    int64_t *mem_ptr = nullptr;   // aggregate -> members (m+1)
-    int32_t *members = nullptr;   // n, ascending within each aggregate
     double *S = nullptr;          // optional (keep_strength)
+    // elimination (logical)
+    int64_t nF = 0;
+    int32_t *fmap = nullptr;      // n: C -> coarse index, F -> -1-slot
+    int32_t *cid = nullptr;       // nC: logical fine id of coarse index
+    int32_t *fid = nullptr;       // nF
+    int64_t *ct_ptr = nullptr;    // nC+1: transposed L_FC (coarse -> F neighbours)
+    int32_t *ct_f = nullptr;
+    double *ct_coef = nullptr;    // w_fc / d_f
+    // coarsest (logical)
+    double *pinv = nullptr;
+    // ---- solve storage (see above)
+    int32_t *sid = nullptr;       // storage -> logical
+    int32_t *spos = nullptr;      // logical -> storage
+    int64_t *srp = nullptr;
+    int32_t *scol = nullptr;
+    double *sw = nullptr, *sd = nullptr;
+    int64_t c_end[NCLASS] = {0, 0, 0, 0};
+    int64_t ntiles = 0;
+    int64_t *tile_first = nullptr;  // ntiles+1 row indices
+    int64_t nchunks = 0;
+    int64_t *chunk_first = nullptr; // per hub row (nhub+1)
+    double *chunk_part = nullptr;
+    // transfer maps in storage space
+    int32_t *agg_s = nullptr;       // agg: coarse storage index of each fine storage row
+    int64_t *mem_ptr = nullptr;     // agg: coarse storage index -> members (m+1)
+    int32_t *members = nullptr;     // agg: fine storage rows, ascending
+    int32_t *cid_s = nullptr;       // elim: fine storage row of each coarse storage index
+    int32_t *flist = nullptr;       // elim: fine storage rows of F (ascending), nF
+    int64_t *ct_ptr_s = nullptr;    // elim: coarse storage -> F neighbours (storage), coef
+    int32_t *ct_f_s = nullptr;
+    double *ct_coef_s = nullptr;
+    int32_t *fmap_s = nullptr;      // elim: coarse storage index of a C storage row, -1 for F
+    double *pinv_s = nullptr;       // coarsest: L^+ in storage order
     // Chebyshev constants (O-S6), host
     double cheb_theta = 0, cheb_delta = 0, cheb_sigma = 0;
-    // elimination
-    int64_t nF = 0;
-    int32_t *fmap = nullptr;      // n
-    int32_t *cid = nullptr;       // nC: fine id of coarse index
-    int32_t *fid = nullptr;       // nF: fine id of F slot
-    int64_t *ct_ptr = nullptr;    // nC+1: transposed L_FC (coarse -> F neighbours)
-    int32_t *ct_f = nullptr;      // fine id of the F neighbour
-    double *ct_coef = nullptr;    // w_fc / d_f
-    // coarsest
-    double *pinv = nullptr;       // n*n
-    // solve work vectors (length n, n >= 1)
+    // solve work vectors (storage order, length n >= 1)
     double *b = nullptr, *x = nullptr, *x2 = nullptr, *t = nullptr, *r = nullptr, *dv = nullptr;
 };
 
@@ -141,6 +156,7 @@ struct lap_hierarchy {
     lap_params p;
     int64_t n0 = 0;
     int64_t *perm = nullptr;       // device: perm[i] = internal id of caller vertex i
+    int64_t *cmap = nullptr;       // device: caller vertex -> level-0 storage row
     std::vector<lap::Level> lev;
     lap_status status = LAP_OK;
     // PCG workspaces (level 0, internal numbering)
@@ -178,7 +194,9 @@ struct EpiArgs {
     double *partials = nullptr;   // SPMV_DOT partial sums (one per block per bin)
 };
 void spmv_level(lap_hierarchy *h, const Level &L, EpiKind kind, const EpiArgs &a, cudaStream_t s);
-void build_row_bins(Level &L, cudaStream_t s);
+// storage (storage.cu)
+void build_storage(lap_hierarchy *h, int l, cudaStream_t s);
+void build_transfers(lap_hierarchy *h, cudaStream_t s);
 int64_t spmv_partial_slots(const Level &L);
 void vcycle(lap_hierarchy *h, int l, cudaStream_t s);   // x_l = V(l, b_l)
 void run_pcg(lap_hierarchy *h, double tol, int32_t *iters, double *relres, int *conv, cudaStream_t s);

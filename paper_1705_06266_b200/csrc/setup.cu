@@ -642,10 +642,11 @@ __global__ void k_gal_emit(int64_t n, const int64_t *__restrict__ row_ptr, const
 // O-S6 lambda-hat: Lanczos on D^-1/2 L D^-1/2 (O-R3)
 // =========================================================================
 
-__global__ void k_lz_init(int64_t n, uint64_t base, const double *d, double *v, double *rs) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        v[i] = 2.0 * unit_from(mix64(base ^ (uint64_t)i)) - 1.0;
-        rs[i] = 1.0 / sqrt(d[i]);
+// start vector u_i = 2 U'(l,i) - 1 of logical vertex i, laid out in storage order
+__global__ void k_lz_init(int64_t n, uint64_t base, const int32_t *sid, const double *sd, double *v, double *rs) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        v[p] = 2.0 * unit_from(mix64(base ^ (uint64_t)sid[p])) - 1.0;
+        rs[p] = 1.0 / sqrt(sd[p]);
     }
 }
 __global__ void k_scale_by(int64_t n, double *v, const double *nrm2) {
@@ -723,7 +724,7 @@ static double lanczos(lap_hierarchy *h, Level &L, int l, cudaStream_t s) {
     LAP_CUDA(cudaMemsetAsync(k.p, 0, sizeof(int), s));
     uint64_t base = mix64(salt_of(h->p.seed, 4) ^ (uint64_t)(2 * l));
     unsigned g = grid_for(n, 256, 148 * 8);
-    k_lz_init<<<g, 256, 0, s>>>(n, base, L.d, v.p, rs.p); ++g_kl;
+    k_lz_init<<<g, 256, 0, s>>>(n, base, L.sid, L.sd, v.p, rs.p); ++g_kl;
     dot(h, v.p, v.p, n, sc.p + 5, s);
     k_scale_by<<<g, 256, 0, s>>>(n, v.p, sc.p + 5); ++g_kl;
     for (int j = 0; j < steps && j < 64; j++) {
@@ -1069,7 +1070,7 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
     bool prev_elim = false;
     for (int l = 0;; l++) {
         Level &L = h->lev[l];
-        build_row_bins(L, s);
+        build_storage(h, l, s);
         if (L.n + L.nnz <= p.coarse_nnz || l == p.max_levels - 1 || l == 63) {     // O-R27
             L.kind = KIND_COARSEST;
             break;

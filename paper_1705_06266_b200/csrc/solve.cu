@@ -68,30 +68,43 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
     return r;  // valid in thread 0
 }
 
-// V lanes per row; the warp processes 32/V rows per iteration (warp-uniform loop)
-template <int V, int EPI, bool IDENT>
-__global__ void __launch_bounds__(256) k_spmv_group(int64_t cnt, const int32_t *__restrict__ rows, int64_t row0,
-                                                    Csr A, EpiArgs a, double *__restrict__ partials) {
-    constexpr int RPW = 32 / V;
+// class 0: CSR-stream tile (rows of <= SHORT_MAX entries, <= TILE_NNZ entries per
+// tile).  Entries are streamed with coalesced 8-deep independent loads, the
+// products staged in shared memory, then one thread per row sums its segment.
+template <int EPI>
+__global__ void __launch_bounds__(256) k_spmv_tiles(int64_t ntiles, const int64_t *__restrict__ tf, Csr A, EpiArgs a,
+                                                    double *__restrict__ partials) {
+    __shared__ double prod[TILE_NNZ];
     __shared__ double sh[8];
-    const int lane = threadIdx.x & 31;
-    const int sub = lane % V, grp = lane / V;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    constexpr int U = TILE_NNZ / 256;
     double dacc = 0.0;
-    for (int64_t base = warp * RPW; base < cnt; base += nwarps * RPW) {
-        int64_t t = base + grp;
-        double acc = 0.0;
-        int64_t i = -1;
-        if (t < cnt) {
-            i = IDENT ? row0 + t : (int64_t)rows[t];
-            int64_t s = A.rp[i], e = A.rp[i + 1];
-#pragma unroll 4
-            for (int64_t k = s + sub; k < e; k += V) acc += __ldg(&A.w[k]) * a.x[__ldg(&A.col[k])];
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t r0 = tf[t], r1 = tf[t + 1];
+        const int64_t e0 = A.rp[r0];
+        const int ne = (int)(A.rp[r1] - e0);
+        int c[U];
+        double wv[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            int k = threadIdx.x + u * 256;
+            if (k < ne) {
+                c[u] = __ldg(&A.col[e0 + k]);
+                wv[u] = __ldg(&A.w[e0 + k]);
+            }
         }
 #pragma unroll
-        for (int o = V / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (sub == 0 && i >= 0) apply_epi<EPI>(i, acc, A, a, dacc);
+        for (int u = 0; u < U; u++) {
+            int k = threadIdx.x + u * 256;
+            if (k < ne) prod[k] = wv[u] * a.x[c[u]];
+        }
+        __syncthreads();
+        for (int64_t r = r0 + threadIdx.x; r < r1; r += 256) {
+            int k0 = (int)(A.rp[r] - e0), k1 = (int)(A.rp[r + 1] - e0);
+            double acc = 0.0;
+            for (int k = k0; k < k1; k++) acc += prod[k];
+            apply_epi<EPI>(r, acc, A, a, dacc);
+        }
+        __syncthreads();
     }
     if (EPI == E_DOT) {
         double r = block_sum(dacc, sh);
@@ -99,14 +112,46 @@ __global__ void __launch_bounds__(256) k_spmv_group(int64_t cnt, const int32_t *
     }
 }
 
-// one 256-thread block per row
-template <int EPI, bool IDENT>
-__global__ void __launch_bounds__(256) k_spmv_block(int64_t cnt, const int32_t *__restrict__ rows, int64_t row0,
-                                                    Csr A, EpiArgs a, double *__restrict__ partials) {
+// class 1: warp per row, rows [row0, row0 + cnt)
+template <int EPI>
+__global__ void __launch_bounds__(256) k_spmv_warp(int64_t cnt, int64_t row0, Csr A, EpiArgs a,
+                                                   double *__restrict__ partials) {
+    __shared__ double sh[8];
+    const int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double dacc = 0.0;
+    for (int64_t t = warp; t < cnt; t += nwarps) {
+        int64_t i = row0 + t;
+        int64_t s = A.rp[i], e = A.rp[i + 1];
+        double a0 = 0.0, a1 = 0.0;
+        int64_t k = s + lane;
+        for (; k + 32 < e; k += 64) {
+            int c0 = __ldg(&A.col[k]), c1 = __ldg(&A.col[k + 32]);
+            double w0 = __ldg(&A.w[k]), w1 = __ldg(&A.w[k + 32]);
+            a0 += w0 * a.x[c0];
+            a1 += w1 * a.x[c1];
+        }
+        if (k < e) a0 += __ldg(&A.w[k]) * a.x[__ldg(&A.col[k])];
+        double acc = a0 + a1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) apply_epi<EPI>(i, acc, A, a, dacc);
+    }
+    if (EPI == E_DOT) {
+        double r = block_sum(dacc, sh);
+        if (threadIdx.x == 0) partials[blockIdx.x] = r;
+    }
+}
+
+// class 2: one 256-thread block per row
+template <int EPI>
+__global__ void __launch_bounds__(256) k_spmv_block(int64_t cnt, int64_t row0, Csr A, EpiArgs a,
+                                                    double *__restrict__ partials) {
     __shared__ double sh[8];
     double dacc = 0.0;
     for (int64_t t = blockIdx.x; t < cnt; t += gridDim.x) {
-        int64_t i = IDENT ? row0 + t : (int64_t)rows[t];
+        int64_t i = row0 + t;
         int64_t s = A.rp[i], e = A.rp[i + 1];
         double acc = 0.0;
 #pragma unroll 4
@@ -121,8 +166,8 @@ __global__ void __launch_bounds__(256) k_spmv_block(int64_t cnt, const int32_t *
     }
 }
 
-// hub rows: block per HUB_CHUNK-entry chunk -> ordered partial sums
-__global__ void __launch_bounds__(256) k_spmv_hub_chunks(int64_t nchunks, int64_t nhub, const int32_t *__restrict__ rows,
+// class 3: block per HUB_CHUNK-entry chunk -> ordered partial sums, then epilogue
+__global__ void __launch_bounds__(256) k_spmv_hub_chunks(int64_t nchunks, int64_t nhub, int64_t row0,
                                                          const int64_t *__restrict__ cfirst, Csr A,
                                                          const double *__restrict__ x, double *__restrict__ cpart) {
     __shared__ double sh[8];
@@ -133,7 +178,7 @@ __global__ void __launch_bounds__(256) k_spmv_hub_chunks(int64_t nchunks, int64_
             if (cfirst[mid] <= c) lo = mid;
             else hi = mid;
         }
-        int64_t i = rows[lo];
+        int64_t i = row0 + lo;
         int64_t s = A.rp[i] + (c - cfirst[lo]) * HUB_CHUNK;
         int64_t e = min(A.rp[i + 1], s + HUB_CHUNK);
         double acc = 0.0;
@@ -144,14 +189,14 @@ __global__ void __launch_bounds__(256) k_spmv_hub_chunks(int64_t nchunks, int64_
     }
 }
 template <int EPI>
-__global__ void k_spmv_hub_epi(int64_t nhub, const int32_t *__restrict__ rows, const int64_t *__restrict__ cfirst,
+__global__ void k_spmv_hub_epi(int64_t nhub, int64_t row0, const int64_t *__restrict__ cfirst,
                                const double *__restrict__ cpart, Csr A, EpiArgs a, double *__restrict__ partials) {
     __shared__ double sh[8];
     double dacc = 0.0;
     for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < nhub; h += (int64_t)gridDim.x * blockDim.x) {
         double ax = 0.0;
         for (int64_t c = cfirst[h]; c < cfirst[h + 1]; c++) ax += cpart[c];
-        apply_epi<EPI>(rows[h], ax, A, a, dacc);
+        apply_epi<EPI>(row0 + h, ax, A, a, dacc);
     }
     if (EPI == E_DOT) {
         double r = block_sum(dacc, sh);
@@ -159,133 +204,44 @@ __global__ void k_spmv_hub_epi(int64_t nhub, const int32_t *__restrict__ rows, c
     }
 }
 
-// ------------------------------------------------------------------ bins
-__global__ void k_bin_of(int64_t n, const int64_t *__restrict__ rp, uint8_t *bin, unsigned long long *cnt) {
-    __shared__ unsigned long long c[NBINS];
-    if (threadIdx.x < NBINS) c[threadIdx.x] = 0;
-    __syncthreads();
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t dg = rp[i + 1] - rp[i];
-        int b = dg <= 8 ? 0 : dg <= 32 ? 1 : dg <= 1024 ? 2 : dg <= HUB_CHUNK ? 3 : 4;
-        bin[i] = (uint8_t)b;
-        atomicAdd(&c[b], 1ULL);
-    }
-    __syncthreads();
-    if (threadIdx.x < NBINS && c[threadIdx.x]) atomicAdd(&cnt[threadIdx.x], c[threadIdx.x]);
-}
-__global__ void k_iota32(int64_t n, int32_t *v) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        v[i] = (int32_t)i;
-}
-__global__ void k_hub_chunk_counts(int64_t nhub, const int32_t *rows, const int64_t *rp, int64_t *cnt) {
-    for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < nhub; h += (int64_t)gridDim.x * blockDim.x) {
-        int64_t i = rows[h];
-        cnt[h] = (rp[i + 1] - rp[i] + HUB_CHUNK - 1) / HUB_CHUNK;
-    }
-}
-
-void build_row_bins(Level &L, cudaStream_t s) {
-    RowBins &B = L.bins;
-    int64_t n = L.n;
-    if (n <= 0) return;
-    DBuf<uint8_t> bin(n, s), bin2(n, s);
-    DBuf<unsigned long long> cnt(NBINS, s);
-    LAP_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long) * NBINS, s));
-    k_bin_of<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(n, L.row_ptr, bin.p, cnt.p);
-    g_kl++;
-    LAP_CHECK_LAUNCH();
-    unsigned long long hc[NBINS];
-    LAP_CUDA(cudaMemcpyAsync(hc, cnt.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
-    LAP_CUDA(cudaStreamSynchronize(s));
-    int nonempty = 0, last = 0;
-    B.off[0] = 0;
-    for (int b = 0; b < NBINS; b++) {
-        B.cnt[b] = (int64_t)hc[b];
-        B.off[b + 1] = B.off[b] + B.cnt[b];
-        if (hc[b]) { nonempty++; last = b; }
-    }
-    if (nonempty == 1 && last != 4) {
-        B.identity = true;
-        B.identity_bin = last;
-        B.rows = nullptr;
-    } else {
-        B.identity = false;
-        DBuf<int32_t> ids(n, s);
-        B.rows = (int32_t *)dalloc(sizeof(int32_t) * n, s);
-        k_iota32<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(n, ids.p);
-        size_t bytes = 0;
-        LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, bin.p, bin2.p, ids.p, B.rows, n, 0, 3, s));
-        DBuf<char> tmp((int64_t)bytes, s);
-        LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, bin.p, bin2.p, ids.p, B.rows, n, 0, 3, s));
-        g_kl += 2;
-    }
-    int64_t nhub = B.cnt[4];
-    if (nhub > 0) {
-        DBuf<int64_t> cc(nhub + 1, s);
-        LAP_CUDA(cudaMemsetAsync(cc.p, 0, sizeof(int64_t) * (nhub + 1), s));
-        k_hub_chunk_counts<<<grid_for(nhub, 256), 256, 0, s>>>(nhub, B.rows + B.off[4], L.row_ptr, cc.p);
-        B.chunk_row_first = (int64_t *)dalloc(sizeof(int64_t) * (nhub + 1), s);
-        size_t bytes = 0;
-        LAP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cc.p, B.chunk_row_first, nhub + 1, s));
-        DBuf<char> tmp((int64_t)bytes, s);
-        LAP_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, cc.p, B.chunk_row_first, nhub + 1, s));
-        g_kl += 2;
-        LAP_CUDA(cudaMemcpyAsync(&B.nchunks, B.chunk_row_first + nhub, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-        LAP_CUDA(cudaStreamSynchronize(s));
-        B.chunk_partial = (double *)dalloc(sizeof(double) * (B.nchunks + 1), s);
-    }
-    LAP_CHECK_LAUNCH();
-}
-
-// launch geometry per bin (fixed for a level -> deterministic partial slots)
-static unsigned bin_grid(int b, int64_t cnt) {
+// launch geometry per class (fixed for a level -> deterministic partial slots)
+static unsigned class_grid(const Level &L, int c) {
+    int64_t lo = c == 0 ? 0 : L.c_end[c - 1];
+    int64_t cnt = L.c_end[c] - lo;
     if (cnt <= 0) return 0;
-    switch (b) {
-        case 0: return grid_for(cnt * 8, 256, 148 * 16);
-        case 1: return grid_for(cnt * 32, 256, 148 * 16);
-        case 2: return grid_for(cnt * 32, 256, 148 * 16);
-        case 3: return (unsigned)std::min<int64_t>(cnt, 148 * 8);
+    switch (c) {
+        case 0: return (unsigned)std::min<int64_t>(L.ntiles, 148 * 8);
+        case 1: return grid_for(cnt * 32, 256, 148 * 8);
+        case 2: return (unsigned)std::min<int64_t>(cnt, 148 * 8);
         default: return grid_for(cnt, 256, 148);
     }
 }
 
 int64_t spmv_partial_slots(const Level &L) {
     int64_t t = 0;
-    for (int b = 0; b < NBINS; b++) t += bin_grid(b, L.bins.cnt[b]);
+    for (int c = 0; c < NCLASS; c++) t += class_grid(L, c);
     return t;
 }
 
 template <int EPI>
 static void spmv_dispatch(lap_hierarchy *h, const Level &L, const EpiArgs &a, cudaStream_t s) {
-    const RowBins &B = L.bins;
-    Csr A{L.row_ptr, L.col, L.w, L.d};
+    Csr A{L.srp, L.scol, L.sw, L.sd};
     double *part = a.partials;
     int64_t slot = 0;
-    for (int b = 0; b < NBINS; b++) {
-        int64_t cnt = B.cnt[b];
-        if (!cnt) continue;
-        unsigned g = bin_grid(b, cnt);
-        const int32_t *rows = B.identity ? nullptr : B.rows + B.off[b];
+    for (int c = 0; c < NCLASS; c++) {
+        int64_t row0 = c == 0 ? 0 : L.c_end[c - 1];
+        int64_t cnt = L.c_end[c] - row0;
+        if (cnt <= 0) continue;
+        unsigned g = class_grid(L, c);
         double *pp = part ? part + slot : nullptr;
-        bool id = B.identity;
-        switch (b) {
-            case 0:
-                if (id) k_spmv_group<8, EPI, true><<<g, 256, 0, s>>>(cnt, rows, 0, A, a, pp);
-                else k_spmv_group<8, EPI, false><<<g, 256, 0, s>>>(cnt, rows, 0, A, a, pp);
-                break;
-            case 1:
-            case 2:
-                if (id) k_spmv_group<32, EPI, true><<<g, 256, 0, s>>>(cnt, rows, 0, A, a, pp);
-                else k_spmv_group<32, EPI, false><<<g, 256, 0, s>>>(cnt, rows, 0, A, a, pp);
-                break;
-            case 3:
-                if (id) k_spmv_block<EPI, true><<<g, 256, 0, s>>>(cnt, rows, 0, A, a, pp);
-                else k_spmv_block<EPI, false><<<g, 256, 0, s>>>(cnt, rows, 0, A, a, pp);
-                break;
-            case 4: {
-                unsigned gc = (unsigned)std::min<int64_t>(B.nchunks, 148 * 8);
-                k_spmv_hub_chunks<<<gc, 256, 0, s>>>(B.nchunks, cnt, rows, B.chunk_row_first, A, a.x, B.chunk_partial);
-                k_spmv_hub_epi<EPI><<<g, 256, 0, s>>>(cnt, rows, B.chunk_row_first, B.chunk_partial, A, a, pp);
+        switch (c) {
+            case 0: k_spmv_tiles<EPI><<<g, 256, 0, s>>>(L.ntiles, L.tile_first, A, a, pp); break;
+            case 1: k_spmv_warp<EPI><<<g, 256, 0, s>>>(cnt, row0, A, a, pp); break;
+            case 2: k_spmv_block<EPI><<<g, 256, 0, s>>>(cnt, row0, A, a, pp); break;
+            default: {
+                unsigned gc = (unsigned)std::min<int64_t>(L.nchunks, 148 * 8);
+                k_spmv_hub_chunks<<<gc, 256, 0, s>>>(L.nchunks, cnt, row0, L.chunk_first, A, a.x, L.chunk_part);
+                k_spmv_hub_epi<EPI><<<g, 256, 0, s>>>(cnt, row0, L.chunk_first, L.chunk_part, A, a, pp);
                 h->cur.launches++;
                 break;
             }
@@ -384,14 +340,15 @@ __global__ void k_elim_restrict(int64_t nc, const int32_t *__restrict__ cid, con
     }
 }
 // x = P x' + Fsmooth(b): x_c = x'_idx(c); x_f = (b_f + sum_c w_fc x'_idx(c)) / d_f
-__global__ void k_elim_prolong(int64_t nc, int64_t nf, const int32_t *__restrict__ cid, const int32_t *__restrict__ fid,
+// (storage order: cid_s maps coarse -> fine row, flist lists F rows, fmap_s maps C rows -> coarse)
+__global__ void k_elim_prolong(int64_t nc, int64_t nf, const int32_t *__restrict__ cid, const int32_t *__restrict__ flist,
                                const int32_t *__restrict__ fmap, Csr A, const double *__restrict__ b,
                                const double *__restrict__ xc, double *__restrict__ x) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nc + nf; t += (int64_t)gridDim.x * blockDim.x) {
         if (t < nc) {
             x[cid[t]] = xc[t];
         } else {
-            int64_t f = fid[t - nc];
+            int64_t f = flist[t - nc];
             double s = b[f];
             for (int64_t q = A.rp[f]; q < A.rp[f + 1]; q++) s += A.w[q] * xc[fmap[A.col[q]]];
             x[f] = s / A.d[f];
@@ -419,7 +376,7 @@ static void vcycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, c
     Level &L = h->lev[l];
     int64_t n = L.n;
     if (L.kind == KIND_COARSEST) {
-        k_coarse_gemv<<<grid_for(n * 32, 256, 148), 256, 0, s>>>(n, L.pinv, b, xout);
+        k_coarse_gemv<<<grid_for(n * 32, 256, 148), 256, 0, s>>>(n, L.pinv_s, b, xout);
         h->cur.launches++;
         LAP_CHECK_LAUNCH();
         return;
@@ -427,11 +384,11 @@ static void vcycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, c
     Level &C = h->lev[l + 1];
     if (L.kind == KIND_ELIM) {
         int64_t nc = C.n;
-        k_elim_restrict<<<eg(nc), 256, 0, s>>>(nc, L.cid, L.ct_ptr, L.ct_f, L.ct_coef, b, C.b);
+        k_elim_restrict<<<eg(nc), 256, 0, s>>>(nc, L.cid_s, L.ct_ptr_s, L.ct_f_s, L.ct_coef_s, b, C.b);
         h->cur.launches++;
         vcycle_rec(h, l + 1, C.b, C.x, s);
-        Csr A{L.row_ptr, L.col, L.w, L.d};
-        k_elim_prolong<<<eg(nc + L.nF), 256, 0, s>>>(nc, L.nF, L.cid, L.fid, L.fmap, A, b, C.x, xout);
+        Csr A{L.srp, L.scol, L.sw, L.sd};
+        k_elim_prolong<<<eg(nc + L.nF), 256, 0, s>>>(nc, L.nF, L.cid_s, L.flist, L.fmap_s, A, b, C.x, xout);
         h->cur.launches++;
         h->cur.bytes += 16 * n + 24 * (n - nc) * 4;
         LAP_CHECK_LAUNCH();
@@ -442,7 +399,7 @@ static void vcycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, c
     const double theta = L.cheb_theta, delta = L.cheb_delta, sigma = L.cheb_sigma;
     double *cur = L.x2, *alt = L.t;  // ping-pong pair, distinct from xout and r
     // pre-smoothing from x = 0
-    k_cheb_first<<<eg(n), 256, 0, s>>>(n, b, L.d, 1.0 / theta, cur, L.dv);
+    k_cheb_first<<<eg(n), 256, 0, s>>>(n, b, L.sd, 1.0 / theta, cur, L.dv);
     h->cur.launches++;
     h->cur.bytes += 32 * n;
     double rho_old = 1.0 / sigma;
@@ -468,7 +425,7 @@ static void vcycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, c
     h->cur.bytes += 16 * n + 8 * L.m;
     vcycle_rec(h, l + 1, C.b, C.x, s);
     // prolongation x += P x_c (H4)
-    k_prolong<<<eg(n), 256, 0, s>>>(n, L.agg, C.x, cur);
+    k_prolong<<<eg(n), 256, 0, s>>>(n, L.agg_s, C.x, cur);
     h->cur.launches++;
     h->cur.bytes += 20 * n + 8 * L.m;
     // post-smoothing from the corrected x
@@ -536,7 +493,7 @@ __global__ void k_pcg_p(int64_t n, const double *__restrict__ z, double *__restr
                         int first) {
     double beta = first ? 0.0 : sc[4] / sc[0];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        p[i] = z[i] + beta * p[i];
+        p[i] = first ? z[i] : z[i] + beta * p[i];  // first: p is uninitialised (0*NaN must not leak)
 }
 __global__ void k_copy_scalar(double *sc, int dst, int src) { sc[dst] = sc[src]; }
 __global__ void k_sub_mean(int64_t n, double *__restrict__ v, const double *__restrict__ sum) {

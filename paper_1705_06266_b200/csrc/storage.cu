@@ -1,0 +1,314 @@
+// storage.cu -- the B200 solve-phase data layout.
+//
+// The method fixes each level's LOGICAL vertex ids (random order at level 0,
+// P:371-376; aggregates by ascending root; C vertices order-preserving,
+// O-R22).  Those ids are what the oracle sees and they stay bit-identical.
+// The solve phase, however, is HBM/L2 bound, so each level is additionally
+// stored in a STORAGE ORDER designed for sm_100a:
+//   * rows grouped by degree class so each SpMV schedule (CSR-stream tiles,
+//     warp per row, block per row, split hub rows) is a contiguous range;
+//   * within a class, rows ordered by a locality key inherited from the
+//     caller's numbering (level 0 undoes Pi_rand; an aggregate takes the
+//     smallest storage position of its members; a C vertex keeps its fine
+//     position), so x-gathers of neighbouring rows share cache lines.
+// A storage order is a symmetric permutation of L_l: it changes no value of
+// the method, only the order in which the GPU sums (solve parity is by
+// tolerance, O-P2).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "lap_internal.cuh"
+
+namespace lap {
+
+template <class T>
+static T d2h(const T *p, cudaStream_t s) {
+    T v;
+    LAP_CUDA(cudaMemcpyAsync(&v, p, sizeof(T), cudaMemcpyDeviceToHost, s));
+    LAP_CUDA(cudaStreamSynchronize(s));
+    return v;
+}
+
+#define GRID_STRIDE(i, n) for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
+
+__global__ void k_key_level0(int64_t n, const int64_t *perm, uint64_t *key) {
+    GRID_STRIDE(c, n) key[perm[c]] = (uint64_t)c;  // logical id perm[c] <- caller id c
+}
+__global__ void k_key_fill(int64_t n, uint64_t v, uint64_t *key) {
+    GRID_STRIDE(i, n) key[i] = v;
+}
+__global__ void k_key_agg(int64_t nf, const int32_t *agg, const int32_t *fspos, unsigned long long *key) {
+    GRID_STRIDE(i, nf) atomicMin(&key[agg[i]], (unsigned long long)fspos[i]);
+}
+__global__ void k_key_elim(int64_t nc, const int32_t *cid, const int32_t *fspos, uint64_t *key) {
+    GRID_STRIDE(k, nc) key[k] = (uint64_t)fspos[cid[k]];
+}
+__device__ __forceinline__ int deg_class(int64_t dg) {
+    return dg <= SHORT_MAX ? 0 : dg <= 1024 ? 1 : dg <= HUB_CHUNK ? 2 : 3;
+}
+__global__ void k_class_key(int64_t n, const int64_t *rp, uint64_t *key, int32_t *ids, unsigned long long *cnt) {
+    GRID_STRIDE(i, n) {
+        int c = deg_class(rp[i + 1] - rp[i]);
+        key[i] |= ((uint64_t)c) << 40;
+        ids[i] = (int32_t)i;
+        atomicAdd(&cnt[c], 1ULL);
+    }
+}
+__global__ void k_inverse(int64_t n, const int32_t *sid, int32_t *spos) {
+    GRID_STRIDE(p, n) spos[sid[p]] = (int32_t)p;
+}
+__global__ void k_storage_deg(int64_t n, const int32_t *sid, const int64_t *rp, const double *d, int64_t *deg,
+                              double *sd) {
+    GRID_STRIDE(p, n) {
+        int64_t i = sid[p];
+        deg[p] = rp[i + 1] - rp[i];
+        sd[p] = d[i];
+    }
+}
+// copy logical row sid[p] into storage row p, columns translated (warp per row)
+__global__ void k_storage_fill(int64_t n, const int32_t *sid, const int32_t *spos, const int64_t *rp,
+                               const int32_t *col, const double *w, const int64_t *srp, int32_t *scol, double *sw) {
+    int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t p = warp; p < n; p += nwarps) {
+        int64_t i = sid[p], a = rp[i], o = srp[p], len = rp[i + 1] - a;
+        for (int64_t k = lane; k < len; k += 32) {
+            scol[o + k] = spos[col[a + k]];
+            sw[o + k] = w[a + k];
+        }
+    }
+}
+// tile t of the short class starts at the first row r with srp[r] >= t*C
+__global__ void k_tiles(int64_t ntiles, int64_t nshort, const int64_t *srp, int64_t C, int64_t *tf) {
+    GRID_STRIDE(t, ntiles + 1) {
+        if (t == ntiles) {
+            tf[t] = nshort;
+            continue;
+        }
+        int64_t key = t * C, lo = 0, hi = nshort;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if (srp[mid] < key) lo = mid + 1;
+            else hi = mid;
+        }
+        tf[t] = lo;
+    }
+}
+__global__ void k_hub_counts(int64_t nhub, int64_t row0, const int64_t *srp, int64_t *cnt) {
+    GRID_STRIDE(h, nhub) {
+        int64_t i = row0 + h;
+        cnt[h] = (srp[i + 1] - srp[i] + HUB_CHUNK - 1) / HUB_CHUNK;
+    }
+}
+
+template <class T>
+static void scan_excl(const T *in, T *out, int64_t n, cudaStream_t s) {
+    size_t bytes = 0;
+    LAP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s));
+    DBuf<char> tmp((int64_t)bytes, s);
+    LAP_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, in, out, n, s));
+    g_kl += 2;
+}
+
+void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
+    Level &L = h->lev[l];
+    int64_t n = L.n;
+    unsigned g = grid_for(n, 256, 148 * 8);
+    DBuf<uint64_t> key(n, s), key2(n, s);
+    DBuf<int32_t> ids(n, s);
+    if (l == 0) {
+        k_key_level0<<<g, 256, 0, s>>>(n, h->perm, key.p);
+    } else {
+        Level &F = h->lev[l - 1];
+        if (F.kind == KIND_AGG) {
+            k_key_fill<<<g, 256, 0, s>>>(n, ~0ULL, key.p);
+            k_key_agg<<<grid_for(F.n, 256, 148 * 8), 256, 0, s>>>(F.n, F.agg, F.spos, (unsigned long long *)key.p);
+            g_kl++;
+        } else {
+            k_key_elim<<<g, 256, 0, s>>>(n, F.cid, F.spos, key.p);
+        }
+    }
+    g_kl++;
+    DBuf<unsigned long long> cnt(NCLASS, s);
+    LAP_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long) * NCLASS, s));
+    k_class_key<<<g, 256, 0, s>>>(n, L.row_ptr, key.p, ids.p, cnt.p);
+    g_kl++;
+    LAP_CHECK_LAUNCH();
+    L.sid = (int32_t *)dalloc(sizeof(int32_t) * n, s);
+    L.spos = (int32_t *)dalloc(sizeof(int32_t) * n, s);
+    {
+        size_t bytes = 0;
+        LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.p, key2.p, ids.p, L.sid, n, 0, 42, s));
+        DBuf<char> tmp((int64_t)bytes, s);
+        LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, key.p, key2.p, ids.p, L.sid, n, 0, 42, s));
+        g_kl += 2;
+    }
+    k_inverse<<<g, 256, 0, s>>>(n, L.sid, L.spos);
+    g_kl++;
+    unsigned long long hc[NCLASS];
+    LAP_CUDA(cudaMemcpyAsync(hc, cnt.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
+    LAP_CUDA(cudaStreamSynchronize(s));
+    int64_t acc = 0;
+    for (int c = 0; c < NCLASS; c++) {
+        acc += (int64_t)hc[c];
+        L.c_end[c] = acc;
+    }
+    // storage CSR
+    DBuf<int64_t> deg(n + 1, s);
+    LAP_CUDA(cudaMemsetAsync(deg.p + n, 0, sizeof(int64_t), s));
+    L.sd = (double *)dalloc(sizeof(double) * n, s);
+    k_storage_deg<<<g, 256, 0, s>>>(n, L.sid, L.row_ptr, L.d, deg.p, L.sd);
+    g_kl++;
+    L.srp = (int64_t *)dalloc(sizeof(int64_t) * (n + 1), s);
+    scan_excl(deg.p, L.srp, n + 1, s);
+    L.scol = (int32_t *)dalloc(sizeof(int32_t) * (L.nnz + 1), s);
+    L.sw = (double *)dalloc(sizeof(double) * (L.nnz + 1), s);
+    if (L.nnz) {
+        k_storage_fill<<<grid_for(n * 32, 256, 148 * 16), 256, 0, s>>>(n, L.sid, L.spos, L.row_ptr, L.col, L.w, L.srp,
+                                                                        L.scol, L.sw);
+        g_kl++;
+    }
+    // CSR-stream tiles over the short class
+    int64_t nshort = L.c_end[0];
+    if (nshort > 0) {
+        int64_t nnz_short = d2h(L.srp + nshort, s);
+        const int64_t C = TILE_NNZ - SHORT_MAX;
+        L.ntiles = std::max<int64_t>(1, (nnz_short + C - 1) / C);
+        L.tile_first = (int64_t *)dalloc(sizeof(int64_t) * (L.ntiles + 1), s);
+        k_tiles<<<grid_for(L.ntiles + 1, 256, 148 * 8), 256, 0, s>>>(L.ntiles, nshort, L.srp, C, L.tile_first);
+        g_kl++;
+    }
+    // hub chunks
+    int64_t nhub = n - L.c_end[2];
+    if (nhub > 0) {
+        DBuf<int64_t> cc(nhub + 1, s);
+        LAP_CUDA(cudaMemsetAsync(cc.p, 0, sizeof(int64_t) * (nhub + 1), s));
+        k_hub_counts<<<grid_for(nhub, 256), 256, 0, s>>>(nhub, L.c_end[2], L.srp, cc.p);
+        g_kl++;
+        L.chunk_first = (int64_t *)dalloc(sizeof(int64_t) * (nhub + 1), s);
+        scan_excl(cc.p, L.chunk_first, nhub + 1, s);
+        L.nchunks = d2h(L.chunk_first + nhub, s);
+        L.chunk_part = (double *)dalloc(sizeof(double) * (L.nchunks + 1), s);
+    }
+    LAP_CHECK_LAUNCH();
+}
+
+// ---------------------------------------------------------------- transfer maps
+__global__ void k_agg_s(int64_t n, const int32_t *sid, const int32_t *agg, const int32_t *cspos, int32_t *agg_s,
+                        int32_t *ids) {
+    GRID_STRIDE(p, n) {
+        agg_s[p] = cspos[agg[sid[p]]];
+        ids[p] = (int32_t)p;
+    }
+}
+__global__ void k_lower_bound32(int64_t m, int64_t n, const int32_t *keys, int64_t *ptr) {
+    GRID_STRIDE(a, m + 1) {
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if (keys[mid] < a) lo = mid + 1;
+            else hi = mid;
+        }
+        ptr[a] = lo;
+    }
+}
+__global__ void k_cid_s(int64_t nc, const int32_t *csid, const int32_t *cid, const int32_t *fspos, int32_t *cid_s) {
+    GRID_STRIDE(k, nc) cid_s[k] = fspos[cid[csid[k]]];
+}
+__global__ void k_fflags(int64_t n, const int32_t *sid, const int32_t *fmap, const int32_t *cspos, int64_t *isf,
+                         int32_t *fmap_s) {
+    GRID_STRIDE(p, n) {
+        int32_t f = fmap[sid[p]];
+        isf[p] = f < 0 ? 1 : 0;
+        fmap_s[p] = f < 0 ? -1 : cspos[f];
+    }
+}
+__global__ void k_flist(int64_t n, const int64_t *isf, const int64_t *pos, int32_t *flist) {
+    GRID_STRIDE(p, n) if (isf[p]) flist[pos[p]] = (int32_t)p;
+}
+__global__ void k_ct_deg(int64_t nc, const int32_t *csid, const int64_t *ct_ptr, int64_t *deg) {
+    GRID_STRIDE(k, nc) {
+        int64_t kc = csid[k];
+        deg[k] = ct_ptr[kc + 1] - ct_ptr[kc];
+    }
+}
+__global__ void k_ct_fill_s(int64_t nc, const int32_t *csid, const int64_t *ct_ptr, const int32_t *ct_f,
+                            const double *ct_coef, const int32_t *fspos, const int64_t *ptr_s, int32_t *f_s,
+                            double *coef_s) {
+    GRID_STRIDE(k, nc) {
+        int64_t kc = csid[k], o = ptr_s[k];
+        for (int64_t q = ct_ptr[kc]; q < ct_ptr[kc + 1]; q++, o++) {
+            f_s[o] = fspos[ct_f[q]];
+            coef_s[o] = ct_coef[q];
+        }
+    }
+}
+__global__ void k_pinv_s(int64_t n, const int32_t *sid, const double *P, double *Ps) {
+    GRID_STRIDE(t, n * n) {
+        int64_t p = t / n, q = t % n;
+        Ps[t] = P[(int64_t)sid[p] * n + sid[q]];
+    }
+}
+__global__ void k_cmap(int64_t n, const int64_t *perm, const int32_t *spos0, int64_t *cmap) {
+    GRID_STRIDE(c, n) cmap[c] = spos0[perm[c]];
+}
+
+void build_transfers(lap_hierarchy *h, cudaStream_t s) {
+    for (size_t l = 0; l < h->lev.size(); l++) {
+        Level &L = h->lev[l];
+        int64_t n = L.n;
+        unsigned g = grid_for(n, 256, 148 * 8);
+        if (L.kind == KIND_AGG) {
+            Level &C = h->lev[l + 1];
+            DBuf<int32_t> ids(n, s), keys2(n, s);
+            L.agg_s = (int32_t *)dalloc(sizeof(int32_t) * n, s);
+            L.members = (int32_t *)dalloc(sizeof(int32_t) * n, s);
+            L.mem_ptr = (int64_t *)dalloc(sizeof(int64_t) * (L.m + 1), s);
+            k_agg_s<<<g, 256, 0, s>>>(n, L.sid, L.agg, C.spos, L.agg_s, ids.p);
+            int end_bit = 1;
+            while (end_bit < 31 && ((int64_t)1 << end_bit) <= L.m) end_bit++;
+            size_t bytes = 0;
+            LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, L.agg_s, keys2.p, ids.p, L.members, n, 0, end_bit, s));
+            DBuf<char> tmp((int64_t)bytes, s);
+            LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, L.agg_s, keys2.p, ids.p, L.members, n, 0, end_bit, s));
+            k_lower_bound32<<<grid_for(L.m + 1, 256, 148 * 8), 256, 0, s>>>(L.m, n, keys2.p, L.mem_ptr);
+            g_kl += 4;
+        } else if (L.kind == KIND_ELIM) {
+            Level &C = h->lev[l + 1];
+            int64_t nc = C.n;
+            L.cid_s = (int32_t *)dalloc(sizeof(int32_t) * (nc + 1), s);
+            k_cid_s<<<grid_for(nc, 256, 148 * 8), 256, 0, s>>>(nc, C.sid, L.cid, L.spos, L.cid_s);
+            DBuf<int64_t> isf(n + 1, s), pos(n + 1, s);
+            LAP_CUDA(cudaMemsetAsync(isf.p + n, 0, sizeof(int64_t), s));
+            L.fmap_s = (int32_t *)dalloc(sizeof(int32_t) * n, s);
+            k_fflags<<<g, 256, 0, s>>>(n, L.sid, L.fmap, C.spos, isf.p, L.fmap_s);
+            scan_excl(isf.p, pos.p, n + 1, s);
+            L.flist = (int32_t *)dalloc(sizeof(int32_t) * (L.nF + 1), s);
+            k_flist<<<g, 256, 0, s>>>(n, isf.p, pos.p, L.flist);
+            DBuf<int64_t> deg(nc + 1, s);
+            LAP_CUDA(cudaMemsetAsync(deg.p + nc, 0, sizeof(int64_t), s));
+            k_ct_deg<<<grid_for(nc, 256, 148 * 8), 256, 0, s>>>(nc, C.sid, L.ct_ptr, deg.p);
+            L.ct_ptr_s = (int64_t *)dalloc(sizeof(int64_t) * (nc + 1), s);
+            scan_excl(deg.p, L.ct_ptr_s, nc + 1, s);
+            int64_t T = d2h(L.ct_ptr_s + nc, s);
+            L.ct_f_s = (int32_t *)dalloc(sizeof(int32_t) * (T + 1), s);
+            L.ct_coef_s = (double *)dalloc(sizeof(double) * (T + 1), s);
+            k_ct_fill_s<<<grid_for(nc, 256, 148 * 8), 256, 0, s>>>(nc, C.sid, L.ct_ptr, L.ct_f, L.ct_coef, L.spos,
+                                                                    L.ct_ptr_s, L.ct_f_s, L.ct_coef_s);
+            g_kl += 5;
+        } else {
+            L.pinv_s = (double *)dalloc(sizeof(double) * (size_t)(n * n > 0 ? n * n : 1), s);
+            if (n * n > 0) k_pinv_s<<<grid_for(n * n, 256, 148 * 8), 256, 0, s>>>(n, L.sid, L.pinv, L.pinv_s);
+            g_kl++;
+        }
+        LAP_CHECK_LAUNCH();
+    }
+    h->cmap = (int64_t *)dalloc(sizeof(int64_t) * h->n0, s);
+    k_cmap<<<grid_for(h->n0, 256, 148 * 8), 256, 0, s>>>(h->n0, h->perm, h->lev[0].spos, h->cmap);
+    g_kl++;
+    LAP_CHECK_LAUNCH();
+}
+
+}  // namespace lap

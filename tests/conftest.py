@@ -3,6 +3,8 @@ import sys
 
 import pytest
 
+os.environ.setdefault("LAP_POISON", "1")  # NaN-fill liblap allocations: uninitialised reads fail loudly
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
