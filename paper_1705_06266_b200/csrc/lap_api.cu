@@ -126,7 +126,7 @@ void finalize_solve_structures(lap_hierarchy *h, cudaStream_t s) {
 
 static void free_level(Level &L, cudaStream_t s) {
     void *ps[] = {L.row_ptr, L.col, L.w, L.d, L.agg, L.S, L.fmap, L.cid, L.fid, L.ct_ptr, L.ct_f, L.ct_coef,
-                  L.pinv, L.sid, L.spos, L.srp, L.scol, L.sw, L.sd, L.tile_first, L.chunk_first, L.chunk_part,
+                  L.pinv, L.sid, L.spos, L.srp, L.scol, L.sw, L.sd, L.slice_ptr, L.ell_col, L.ell_w, L.chunk_first, L.chunk_part,
                   L.agg_s, L.mem_ptr, L.members, L.cid_s, L.flist, L.ct_ptr_s, L.ct_f_s, L.ct_coef_s, L.fmap_s,
                   L.pinv_s, L.b, L.x, L.x2, L.t, L.r, L.dv};
     for (void *p : ps) dfree(p, s);

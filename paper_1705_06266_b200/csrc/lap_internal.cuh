@@ -82,13 +82,14 @@ enum { KIND_AGG = 0, KIND_ELIM = 1, KIND_COARSEST = 2 };
 //   key(aggregate) = min storage position of its members
 //   key(C vertex)  = its storage position on the finer level
 // sorted by (degree class, key), so each class is a contiguous row range:
-//   class 0: deg <= 64        CSR-stream tiles of <= TILE_NNZ entries (block per tile)
+//   class 0: deg <= 64        SELL-32 slices (warp per 32-row slice, thread per row,
+//                             column-major padded to the slice's max degree; rows
+//                             degree-sorted first when natural order pads > 20%)
 //   class 1: 65..1024         warp per row
 //   class 2: 1025..16384      256-thread block per row
 //   class 3: > 16384          HUB_CHUNK-entry chunks (block per chunk) + ordered combine
 constexpr int NCLASS = 4;
 constexpr int64_t SHORT_MAX = 64;
-constexpr int64_t TILE_NNZ = 2048;
 constexpr int64_t HUB_CHUNK = 16384;
 
 struct Level {
@@ -122,8 +123,11 @@ struct Level {
     int32_t *scol = nullptr;
     double *sw = nullptr, *sd = nullptr;
     int64_t c_end[NCLASS] = {0, 0, 0, 0};
-    int64_t ntiles = 0;
-    int64_t *tile_first = nullptr;  // ntiles+1 row indices
+    int64_t nslices = 0;            // SELL-32 slices over the short class
+    int64_t *slice_ptr = nullptr;   // nslices+1 offsets into ell_* (multiples of 32)
+    int32_t *ell_col = nullptr;     // padded entries: column (own row for padding)
+    double *ell_w = nullptr;        // padded entries: weight (0 for padding)
+    bool sell_sorted = false;       // short rows degree-sorted
     int64_t nchunks = 0;
     int64_t *chunk_first = nullptr; // per hub row (nhub+1)
     double *chunk_part = nullptr;

@@ -68,43 +68,60 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
     return r;  // valid in thread 0
 }
 
-// class 0: CSR-stream tile (rows of <= SHORT_MAX entries, <= TILE_NNZ entries per
-// tile).  Entries are streamed with coalesced 8-deep independent loads, the
-// products staged in shared memory, then one thread per row sums its segment.
+// class 0: SELL-32 (rows of <= SHORT_MAX entries).  A warp owns a 32-row
+// slice, a thread owns a row; the slice is stored column-major and padded to
+// its widest row, so every col/w load instruction is one fully coalesced
+// 128/256-byte access.  Epilogue operands are loaded before the gather loop
+// so their latency overlaps it.  No shared memory, no barriers.
 template <int EPI>
-__global__ void __launch_bounds__(256) k_spmv_tiles(int64_t ntiles, const int64_t *__restrict__ tf, Csr A, EpiArgs a,
-                                                    double *__restrict__ partials) {
-    __shared__ double prod[TILE_NNZ];
+__global__ void __launch_bounds__(256, 6) k_spmv_sell(int64_t nslices, int64_t nrows, const int64_t *__restrict__ sp,
+                                                   const int32_t *__restrict__ ec, const double *__restrict__ ew,
+                                                   Csr A, EpiArgs a, double *__restrict__ partials) {
     __shared__ double sh[8];
-    constexpr int U = TILE_NNZ / 256;
+    const int lane = threadIdx.x & 31;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     double dacc = 0.0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int64_t r0 = tf[t], r1 = tf[t + 1];
-        const int64_t e0 = A.rp[r0];
-        const int ne = (int)(A.rp[r1] - e0);
-        int c[U];
-        double wv[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            int k = threadIdx.x + u * 256;
-            if (k < ne) {
-                c[u] = __ldg(&A.col[e0 + k]);
-                wv[u] = __ldg(&A.w[e0 + k]);
+    for (int64_t sl = warp; sl < nslices; sl += nwarps) {
+        const int64_t i = sl * 32 + lane;
+        const int64_t beg = sp[sl], end = sp[sl + 1];
+        double xi = 0.0, di = 0.0, bi = 0.0, dvi = 0.0;
+        const bool live = i < nrows;
+        if (live) {
+            xi = a.x[i];
+            di = A.d[i];
+            if (EPI == E_RESID || EPI == E_CHEB || EPI == E_CHEB0) bi = a.b[i];
+            if (EPI == E_CHEB) dvi = a.dv[i];
+        }
+        double acc0 = 0.0, acc1 = 0.0;
+        int64_t k = beg + lane;
+        for (; k + 32 < end; k += 64) {
+            int c0 = __ldg(&ec[k]), c1 = __ldg(&ec[k + 32]);
+            double w0 = __ldg(&ew[k]), w1 = __ldg(&ew[k + 32]);
+            acc0 += w0 * a.x[c0];
+            acc1 += w1 * a.x[c1];
+        }
+        if (k < end) acc0 += __ldg(&ew[k]) * a.x[__ldg(&ec[k])];
+        if (live) {
+            double ax = acc0 + acc1;
+            double lx = di * xi - ax;
+            if (EPI == E_SPMV) {
+                a.y[i] = lx;
+            } else if (EPI == E_DOT) {
+                a.y[i] = lx;
+                dacc += xi * lx;
+            } else if (EPI == E_RESID) {
+                a.y[i] = bi - lx;
+            } else if (EPI == E_CHEB) {
+                double dv = a.c1 * dvi + a.c2 * ((bi - lx) / di);
+                a.dv[i] = dv;
+                a.y[i] = xi + dv;
+            } else if (EPI == E_CHEB0) {
+                double dv = a.c2 * ((bi - lx) / di);
+                a.dv[i] = dv;
+                a.y[i] = xi + dv;
             }
         }
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            int k = threadIdx.x + u * 256;
-            if (k < ne) prod[k] = wv[u] * a.x[c[u]];
-        }
-        __syncthreads();
-        for (int64_t r = r0 + threadIdx.x; r < r1; r += 256) {
-            int k0 = (int)(A.rp[r] - e0), k1 = (int)(A.rp[r + 1] - e0);
-            double acc = 0.0;
-            for (int k = k0; k < k1; k++) acc += prod[k];
-            apply_epi<EPI>(r, acc, A, a, dacc);
-        }
-        __syncthreads();
     }
     if (EPI == E_DOT) {
         double r = block_sum(dacc, sh);
@@ -210,7 +227,7 @@ static unsigned class_grid(const Level &L, int c) {
     int64_t cnt = L.c_end[c] - lo;
     if (cnt <= 0) return 0;
     switch (c) {
-        case 0: return (unsigned)std::min<int64_t>(L.ntiles, 148 * 8);
+        case 0: return grid_for(L.nslices * 32, 256, 148 * 16);
         case 1: return grid_for(cnt * 32, 256, 148 * 8);
         case 2: return (unsigned)std::min<int64_t>(cnt, 148 * 8);
         default: return grid_for(cnt, 256, 148);
@@ -235,7 +252,7 @@ static void spmv_dispatch(lap_hierarchy *h, const Level &L, const EpiArgs &a, cu
         unsigned g = class_grid(L, c);
         double *pp = part ? part + slot : nullptr;
         switch (c) {
-            case 0: k_spmv_tiles<EPI><<<g, 256, 0, s>>>(L.ntiles, L.tile_first, A, a, pp); break;
+            case 0: k_spmv_sell<EPI><<<g, 256, 0, s>>>(L.nslices, cnt, L.slice_ptr, L.ell_col, L.ell_w, A, a, pp); break;
             case 1: k_spmv_warp<EPI><<<g, 256, 0, s>>>(cnt, row0, A, a, pp); break;
             case 2: k_spmv_block<EPI><<<g, 256, 0, s>>>(cnt, row0, A, a, pp); break;
             default: {

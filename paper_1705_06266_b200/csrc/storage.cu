@@ -5,7 +5,7 @@
 // O-R22).  Those ids are what the oracle sees and they stay bit-identical.
 // The solve phase, however, is HBM/L2 bound, so each level is additionally
 // stored in a STORAGE ORDER designed for sm_100a:
-//   * rows grouped by degree class so each SpMV schedule (CSR-stream tiles,
+//   * rows grouped by degree class so each SpMV schedule (SELL-32 slices,
 //     warp per row, block per row, split hub rows) is a contiguous range;
 //   * within a class, rows ordered by a locality key inherited from the
 //     caller's numbering (level 0 undoes Pi_rand; an aggregate takes the
@@ -17,6 +17,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <string>
+#include <vector>
 
 #include "lap_internal.cuh"
 
@@ -47,13 +49,57 @@ __global__ void k_key_elim(int64_t nc, const int32_t *cid, const int32_t *fspos,
 __device__ __forceinline__ int deg_class(int64_t dg) {
     return dg <= SHORT_MAX ? 0 : dg <= 1024 ? 1 : dg <= HUB_CHUNK ? 2 : 3;
 }
-__global__ void k_class_key(int64_t n, const int64_t *rp, uint64_t *key, int32_t *ids, unsigned long long *cnt) {
+// sort key: [63:62] degree class, [61:54] 255 - degree (short rows, only if
+// degree-sorted), [53:0] locality key
+__global__ void k_class_key(int64_t n, const int64_t *rp, const uint64_t *key, uint64_t *skey, int32_t *ids,
+                            unsigned long long *cnt, int by_degree) {
     GRID_STRIDE(i, n) {
-        int c = deg_class(rp[i + 1] - rp[i]);
-        key[i] |= ((uint64_t)c) << 40;
+        int64_t dg = rp[i + 1] - rp[i];
+        int c = deg_class(dg);
+        uint64_t k = key[i] | (((uint64_t)c) << 62);
+        if (by_degree && c == 0) k |= ((uint64_t)(255 - dg)) << 54;
+        skey[i] = k;
         ids[i] = (int32_t)i;
-        atomicAdd(&cnt[c], 1ULL);
+        if (cnt) atomicAdd(&cnt[c], 1ULL);
     }
+}
+// SELL-32 slice widths (max degree of the slice's rows) and padding statistic
+__global__ void k_slice_width(int64_t nslices, int64_t nshort, const int32_t *sid, const int64_t *rp, int64_t *width,
+                              unsigned long long *padded) {
+    GRID_STRIDE(sl, nslices) {
+        int64_t mx = 0;
+        for (int64_t p = sl * 32; p < min(nshort, sl * 32 + 32); p++) {
+            int64_t i = sid[p];
+            mx = max(mx, rp[i + 1] - rp[i]);
+        }
+        width[sl] = 32 * mx;
+        atomicAdd(padded, (unsigned long long)(32 * mx));
+    }
+}
+// fill every slot of every slice, including the lanes past the last short row
+// of a ragged final slice (col 0, w 0: gathered but contribute nothing)
+__global__ void k_sell_fill(int64_t nslots, int64_t nshort, const int64_t *srp, const int32_t *scol, const double *sw,
+                            const int64_t *slice_ptr, int32_t *ell_col, double *ell_w) {
+    GRID_STRIDE(p, nslots) {
+        int64_t sl = p >> 5, lane = p & 31;
+        int64_t base = slice_ptr[sl] + lane, width = (slice_ptr[sl + 1] - slice_ptr[sl]) >> 5;
+        bool row = p < nshort;
+        int64_t a = row ? srp[p] : 0, dg = row ? srp[p + 1] - a : 0;
+        for (int64_t k = 0; k < width; k++) {
+            bool real = k < dg;
+            ell_col[base + 32 * k] = real ? scol[a + k] : (row ? (int32_t)p : 0);
+            ell_w[base + 32 * k] = real ? sw[a + k] : 0.0;
+        }
+    }
+}
+__global__ void k_short_nnz(int64_t n, const int64_t *rp, unsigned long long *out) {
+    unsigned long long acc = 0;
+    GRID_STRIDE(i, n) {
+        int64_t dg = rp[i + 1] - rp[i];
+        if (dg <= SHORT_MAX) acc += (unsigned long long)dg;
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
 }
 __global__ void k_inverse(int64_t n, const int32_t *sid, int32_t *spos) {
     GRID_STRIDE(p, n) spos[sid[p]] = (int32_t)p;
@@ -80,22 +126,6 @@ __global__ void k_storage_fill(int64_t n, const int32_t *sid, const int32_t *spo
         }
     }
 }
-// tile t of the short class starts at the first row r with srp[r] >= t*C
-__global__ void k_tiles(int64_t ntiles, int64_t nshort, const int64_t *srp, int64_t C, int64_t *tf) {
-    GRID_STRIDE(t, ntiles + 1) {
-        if (t == ntiles) {
-            tf[t] = nshort;
-            continue;
-        }
-        int64_t key = t * C, lo = 0, hi = nshort;
-        while (lo < hi) {
-            int64_t mid = (lo + hi) >> 1;
-            if (srp[mid] < key) lo = mid + 1;
-            else hi = mid;
-        }
-        tf[t] = lo;
-    }
-}
 __global__ void k_hub_counts(int64_t nhub, int64_t row0, const int64_t *srp, int64_t *cnt) {
     GRID_STRIDE(h, nhub) {
         int64_t i = row0 + h;
@@ -112,11 +142,52 @@ static void scan_excl(const T *in, T *out, int64_t n, cudaStream_t s) {
     g_kl += 2;
 }
 
+// LAP_DEBUG_SYNC=1: host-side consistency check of a level's storage layout
+static void validate_storage(const Level &L, cudaStream_t s) {
+    LAP_CUDA(cudaStreamSynchronize(s));
+    int64_t n = L.n;
+    std::vector<int32_t> sid(n), spos(n);
+    std::vector<int64_t> srp(n + 1), rp(n + 1);
+    LAP_CUDA(cudaMemcpy(sid.data(), L.sid, 4 * n, cudaMemcpyDeviceToHost));
+    LAP_CUDA(cudaMemcpy(spos.data(), L.spos, 4 * n, cudaMemcpyDeviceToHost));
+    LAP_CUDA(cudaMemcpy(srp.data(), L.srp, 8 * (n + 1), cudaMemcpyDeviceToHost));
+    LAP_CUDA(cudaMemcpy(rp.data(), L.row_ptr, 8 * (n + 1), cudaMemcpyDeviceToHost));
+    std::vector<int32_t> scol(L.nnz + 1);
+    if (L.nnz) LAP_CUDA(cudaMemcpy(scol.data(), L.scol, 4 * L.nnz, cudaMemcpyDeviceToHost));
+    auto fail = [&](const std::string &m) { throw Error{LAP_ECUDA, "validate_storage: " + m}; };
+    for (int64_t p = 0; p < n; p++) {
+        if (sid[p] < 0 || sid[p] >= n || spos[sid[p]] != p) fail("sid/spos not inverse permutations");
+        int64_t dg = rp[sid[p] + 1] - rp[sid[p]];
+        if (srp[p + 1] - srp[p] != dg) fail("storage degree mismatch");
+        int c = dg <= SHORT_MAX ? 0 : dg <= 1024 ? 1 : dg <= HUB_CHUNK ? 2 : 3;
+        int64_t lo = c == 0 ? 0 : L.c_end[c - 1];
+        if (p < lo || p >= L.c_end[c]) fail("class range mismatch at row " + std::to_string(p));
+    }
+    if (srp[n] != L.nnz) fail("srp[n] != nnz");
+    for (int64_t k = 0; k < L.nnz; k++)
+        if (scol[k] < 0 || scol[k] >= n) fail("scol out of range");
+    if (L.nslices) {
+        std::vector<int64_t> sp(L.nslices + 1);
+        LAP_CUDA(cudaMemcpy(sp.data(), L.slice_ptr, 8 * (L.nslices + 1), cudaMemcpyDeviceToHost));
+        std::vector<int32_t> ec(sp[L.nslices] + 1);
+        LAP_CUDA(cudaMemcpy(ec.data(), L.ell_col, 4 * sp[L.nslices], cudaMemcpyDeviceToHost));
+        if (sp[0] != 0) fail("slice_ptr[0] != 0");
+        for (int64_t sl = 0; sl < L.nslices; sl++) {
+            if (sp[sl + 1] < sp[sl] || (sp[sl + 1] - sp[sl]) % 32) fail("bad slice_ptr");
+            int64_t wdt = (sp[sl + 1] - sp[sl]) / 32;
+            for (int64_t r = sl * 32; r < std::min<int64_t>(L.c_end[0], sl * 32 + 32); r++)
+                if (srp[r + 1] - srp[r] > wdt) fail("slice narrower than its row");
+        }
+        for (int64_t k = 0; k < sp[L.nslices]; k++)
+            if (ec[k] < 0 || ec[k] >= n) fail("ell_col out of range at " + std::to_string(k));
+    }
+}
+
 void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
     Level &L = h->lev[l];
     int64_t n = L.n;
     unsigned g = grid_for(n, 256, 148 * 8);
-    DBuf<uint64_t> key(n, s), key2(n, s);
+    DBuf<uint64_t> key(n, s), key2(n, s);  // locality key, sort scratch
     DBuf<int32_t> ids(n, s);
     if (l == 0) {
         k_key_level0<<<g, 256, 0, s>>>(n, h->perm, key.p);
@@ -133,20 +204,19 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
     g_kl++;
     DBuf<unsigned long long> cnt(NCLASS, s);
     LAP_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long) * NCLASS, s));
-    k_class_key<<<g, 256, 0, s>>>(n, L.row_ptr, key.p, ids.p, cnt.p);
-    g_kl++;
-    LAP_CHECK_LAUNCH();
+    DBuf<uint64_t> skey(n, s);
     L.sid = (int32_t *)dalloc(sizeof(int32_t) * n, s);
     L.spos = (int32_t *)dalloc(sizeof(int32_t) * n, s);
-    {
+    auto sort_rows = [&](int by_degree, unsigned long long *counts) {
+        k_class_key<<<g, 256, 0, s>>>(n, L.row_ptr, key.p, skey.p, ids.p, counts, by_degree);
         size_t bytes = 0;
-        LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key.p, key2.p, ids.p, L.sid, n, 0, 42, s));
+        LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, skey.p, key2.p, ids.p, L.sid, n, 0, 64, s));
         DBuf<char> tmp((int64_t)bytes, s);
-        LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, key.p, key2.p, ids.p, L.sid, n, 0, 42, s));
-        g_kl += 2;
-    }
-    k_inverse<<<g, 256, 0, s>>>(n, L.sid, L.spos);
-    g_kl++;
+        LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, skey.p, key2.p, ids.p, L.sid, n, 0, 64, s));
+        g_kl += 3;
+        LAP_CHECK_LAUNCH();
+    };
+    sort_rows(0, cnt.p);
     unsigned long long hc[NCLASS];
     LAP_CUDA(cudaMemcpyAsync(hc, cnt.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
     LAP_CUDA(cudaStreamSynchronize(s));
@@ -155,6 +225,36 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
         acc += (int64_t)hc[c];
         L.c_end[c] = acc;
     }
+    // SELL-32 over the short class: degree-sort the short rows if natural order pads > 20%
+    int64_t nshort = L.c_end[0];
+    DBuf<int64_t> width;
+    if (nshort > 0) {
+        L.nslices = (nshort + 31) / 32;
+        width.alloc(L.nslices + 1, s);
+        DBuf<unsigned long long> pad(1, s);
+        DBuf<int64_t> rs(1, s);
+        for (int pass = 0; pass < 2; pass++) {
+            LAP_CUDA(cudaMemsetAsync(pad.p, 0, 8, s));
+            LAP_CUDA(cudaMemsetAsync(width.p + L.nslices, 0, 8, s));
+            k_slice_width<<<grid_for(L.nslices, 256, 148 * 8), 256, 0, s>>>(L.nslices, nshort, L.sid, L.row_ptr, width.p,
+                                                                             pad.p);
+            g_kl++;
+            unsigned long long padded = d2h(pad.p, s);
+            // actual entries of the short class: sum of degrees of the first nshort sorted rows
+            // (all short rows come first in the sort), computed from the class counts below
+            if (pass == 1) break;
+            DBuf<unsigned long long> real(1, s);
+            LAP_CUDA(cudaMemsetAsync(real.p, 0, 8, s));
+            k_short_nnz<<<g, 256, 0, s>>>(n, L.row_ptr, real.p);
+            g_kl++;
+            unsigned long long rn = d2h(real.p, s);
+            if ((double)padded <= 1.2 * (double)rn + 64.0) break;
+            L.sell_sorted = true;
+            sort_rows(1, nullptr);
+        }
+    }
+    k_inverse<<<g, 256, 0, s>>>(n, L.sid, L.spos);
+    g_kl++;
     // storage CSR
     DBuf<int64_t> deg(n + 1, s);
     LAP_CUDA(cudaMemsetAsync(deg.p + n, 0, sizeof(int64_t), s));
@@ -170,16 +270,18 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
                                                                         L.scol, L.sw);
         g_kl++;
     }
-    // CSR-stream tiles over the short class
-    int64_t nshort = L.c_end[0];
+    // SELL-32 slices of the short class
     if (nshort > 0) {
-        int64_t nnz_short = d2h(L.srp + nshort, s);
-        const int64_t C = TILE_NNZ - SHORT_MAX;
-        L.ntiles = std::max<int64_t>(1, (nnz_short + C - 1) / C);
-        L.tile_first = (int64_t *)dalloc(sizeof(int64_t) * (L.ntiles + 1), s);
-        k_tiles<<<grid_for(L.ntiles + 1, 256, 148 * 8), 256, 0, s>>>(L.ntiles, nshort, L.srp, C, L.tile_first);
+        L.slice_ptr = (int64_t *)dalloc(sizeof(int64_t) * (L.nslices + 1), s);
+        scan_excl(width.p, L.slice_ptr, L.nslices + 1, s);
+        int64_t tot = d2h(L.slice_ptr + L.nslices, s);
+        L.ell_col = (int32_t *)dalloc(sizeof(int32_t) * (tot + 1), s);
+        L.ell_w = (double *)dalloc(sizeof(double) * (tot + 1), s);
+        k_sell_fill<<<grid_for(L.nslices * 32, 256, 148 * 8), 256, 0, s>>>(L.nslices * 32, nshort, L.srp, L.scol, L.sw, L.slice_ptr, L.ell_col,
+                                                                    L.ell_w);
         g_kl++;
     }
+    if (debug_sync()) validate_storage(L, s);
     // hub chunks
     int64_t nhub = n - L.c_end[2];
     if (nhub > 0) {

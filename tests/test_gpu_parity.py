@@ -194,3 +194,19 @@ def test_full_size_configs(P, k):
     assert rc == 0 and rr <= 1e-8 and abs(it - ito) <= 1, (it, ito, rr)
     xg = xg.cpu().numpy()
     assert np.abs(xg - xo).max() <= 1e-6 * np.abs(xo).max()
+
+
+def test_storage_layout_validated_in_debug_mode(P):
+    """LAP_DEBUG_SYNC=1 turns on host-side validation of every level's storage
+    layout (permutation, class ranges, SELL slices incl. ragged last slice) and
+    a device sync after every launch."""
+    import subprocess
+    import sys
+    code = ("import lapgen, paper_1705_06266_b200 as P\n"
+            "for g in [lapgen.grid3d(23), lapgen.rmat(12), lapgen.barabasi_albert(3001, 5), lapgen.star(20000)]:\n"
+            "    h = P.Hierarchy(g); x, it, rr, rc = h.solve(lapgen.rhs(g.n)); assert rr <= 1e-8, rr\n"
+            "print('ok')\n")
+    env = dict(__import__("os").environ, LAP_DEBUG_SYNC="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
+                       cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
