@@ -147,12 +147,18 @@ typedef struct {
 } lap_stats;
 lap_status lap_get_stats(const lap_hierarchy *h, lap_stats *s);
 
-/* Time the dominant solve kernel (the fused Chebyshev/Jacobi SpMV step on the
- * finest aggregation level, H2) over `reps` launches on `cuda_stream` with
- * CUDA events; returns mean ms per launch and its algorithmic bytes. */
-lap_status lap_bench_smoother(lap_hierarchy *h, int32_t reps, void *cuda_stream,
-                              double *ms_per_launch, double *bytes_per_launch,
-                              int32_t *level);
+/* Time `reps` back-to-back launches of one solve-phase operation on
+ * `cuda_stream` with CUDA events (an event between consecutive launches);
+ * ms[reps] (host) receives each launch's duration in milliseconds.
+ *   which = 0: y = L_l x on level l (H1)
+ *   which = 1: one fused Chebyshev/Jacobi step on aggregation level l (H2)
+ *   which = 2: one V-cycle z = V(0, r) (H16, Alg. 1; l ignored; graph launch)
+ * *bytes = algorithmic HBM bytes per launch (12 nnz + 32 n for H1,
+ * 12 nnz + 56 n for H2, the sum over the cycle's kernels for a V-cycle);
+ * *edges = nonzeros traversed per launch.  Work vectors of the hierarchy are
+ * overwritten (zeros).  LAP_EINVAL for a bad level / kind. */
+lap_status lap_bench_op(lap_hierarchy *h, int32_t which, int32_t l, int32_t reps, void *cuda_stream,
+                        double *ms, double *bytes, int64_t *edges);
 
 #ifdef __cplusplus
 }

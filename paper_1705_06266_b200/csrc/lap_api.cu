@@ -13,12 +13,25 @@ void vcycle_apply(lap_hierarchy *h, const double *r, double *z, cudaStream_t s);
 static thread_local std::string g_err;
 void set_error(const std::string &m) { g_err = m; }
 static bool g_capturing = false;
+bool g_capturing_flag(bool v) {
+    g_capturing = v;
+    return v;
+}
 bool debug_sync() {
     if (g_capturing) return false;
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("LAP_DEBUG_SYNC");
         v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
+
+bool pdl_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("LAP_PDL");
+        v = (e && e[0] == '0') ? 0 : 1;
     }
     return v == 1;
 }
@@ -121,13 +134,15 @@ void finalize_solve_structures(lap_hierarchy *h, cudaStream_t s) {
         h->partials = (double *)dalloc(8 * np, s);
         h->npartials = np;
     }
-    LAP_CUDA(cudaMallocHost(&h->host_scal, 64));
+    LAP_CUDA(cudaMallocHost(&h->host_scal, 8 * 16));
 }
 
 static void free_level(Level &L, cudaStream_t s) {
     void *ps[] = {L.row_ptr, L.col, L.w, L.d, L.agg, L.S, L.fmap, L.cid, L.fid, L.ct_ptr, L.ct_f, L.ct_coef,
-                  L.pinv, L.sid, L.spos, L.srp, L.scol, L.sw, L.sd, L.slice_ptr, L.ell_col, L.ell_w, L.chunk_first, L.chunk_part,
+                  L.pinv, L.sid, L.spos, L.srp, L.scol, L.sw, L.sd, L.slice_ptr, L.ell_col, L.ell_w, L.chunk_row, L.chunk_idx, L.chunk_slot, L.chunk_cnt,
+                  L.chunk_part,
                   L.agg_s, L.mem_ptr, L.members, L.cid_s, L.flist, L.ct_ptr_s, L.ct_f_s, L.ct_coef_s, L.fmap_s,
+                  L.ct_crow, L.ct_cidx, L.ct_cslot, L.ct_ccnt, L.ct_cpart,
                   L.pinv_s, L.b, L.x, L.x2, L.t, L.r, L.dv};
     for (void *p : ps) dfree(p, s);
 }
@@ -289,7 +304,10 @@ lap_status lap_setup(const lap_graph *g, const lap_params *pp, void *stream, lap
         h->stats.kernel_launches = h->cur.launches + (lap::g_kl - kl0);
         h->stats.spmv_edges = h->cur.edges;
         h->stats.spmv_bytes = h->cur.bytes;
-        if (p.use_graphs) lap::capture_vcycle(h);
+        if (p.use_graphs) {
+            lap::capture_vcycle(h);
+            lap::capture_pcg(h);
+        }
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
     } catch (const lap::Error &e) {
@@ -314,6 +332,7 @@ void lap_free(lap_hierarchy *h) {
     cudaStream_t s = nullptr;
     cudaDeviceSynchronize();
     if (h->vgraph) cudaGraphExecDestroy(h->vgraph);
+    lap::free_pcg(h);
     for (auto &L : h->lev) lap::free_level(L, s);
     void *ps[] = {h->perm, h->cmap, h->pb, h->px, h->pr, h->pz, h->pp, h->pq, h->scal, h->partials, h->stage_in,
                   h->stage_out};
@@ -500,53 +519,63 @@ lap_status lap_get_stats(const lap_hierarchy *h, lap_stats *st) {
     return LAP_OK;
 }
 
-lap_status lap_bench_smoother(lap_hierarchy *h, int32_t reps, void *stream, double *ms_per_launch,
-                              double *bytes_per_launch, int32_t *level) {
-    if (!h || reps < 1) return LAP_EINVAL;
+lap_status lap_bench_op(lap_hierarchy *h, int32_t which, int32_t l, int32_t reps, void *stream, double *ms,
+                        double *bytes, int64_t *edges) {
+    if (!h || reps < 1 || which < 0 || which > 2) return LAP_EINVAL;
+    if (which < 2 && (l < 0 || l >= (int32_t)h->lev.size() || h->lev[l].kind == lap::KIND_COARSEST)) return LAP_EINVAL;
+    if (which == 1 && h->lev[l].kind != lap::KIND_AGG) return LAP_EINVAL;
     LAP_API_BEGIN
     cudaStream_t s = (cudaStream_t)stream;
-    int l = -1;
-    for (size_t i = 0; i < h->lev.size(); i++)
-        if (h->lev[i].kind == lap::KIND_AGG) {
-            l = (int)i;
-            break;
+    std::vector<cudaEvent_t> ev(reps + 1);
+    for (auto &e : ev) LAP_CUDA(cudaEventCreate(&e));
+    lap::Stats save = h->cur;
+    h->cur = lap::Stats{};
+    double by = 0;
+    int64_t ed = 0;
+    auto run = [&](bool count) {
+        if (which == 2) {
+            lap::launch_vcycle(h, s);
+        } else {
+            lap::Level &L = h->lev[l];
+            lap::EpiArgs a;
+            a.x = L.x2;
+            a.y = L.t;
+            a.b = L.b;
+            a.dv = L.dv;
+            a.c1 = 0.5;
+            a.c2 = 0.5;
+            lap::spmv_level(h, L, which == 0 ? lap::EPI_SPMV : lap::EPI_CHEB, a, s);
         }
-    if (l < 0) {
-        lap::set_error("no aggregation level");
-        return LAP_EINVAL;
+        if (count) {
+            by = (double)h->cur.bytes;
+            ed = h->cur.edges;
+        }
+        h->cur = lap::Stats{};
+    };
+    if (which < 2) {
+        lap::Level &L = h->lev[l];
+        double *vs[] = {L.x2, L.t, L.b, L.dv};
+        for (double *v : vs) LAP_CUDA(cudaMemsetAsync(v, 0, 8 * (L.n > 0 ? L.n : 1), s));
+    } else {
+        LAP_CUDA(cudaMemsetAsync(h->pr, 0, 8 * h->lev[0].n, s));
     }
-    lap::Level &L = h->lev[l];
-    LAP_CUDA(cudaMemsetAsync(L.dv, 0, 8 * L.n, s));
-    LAP_CUDA(cudaMemsetAsync(L.t, 0, 8 * L.n, s));
-    LAP_CUDA(cudaMemsetAsync(L.x2, 0, 8 * L.n, s));
-    LAP_CUDA(cudaMemsetAsync(L.b, 0, 8 * L.n, s));
-    lap::EpiArgs a;
-    a.b = L.b;
-    a.dv = L.dv;
-    a.c1 = 0.5;
-    a.c2 = 0.5;
-    a.x = L.x2;
-    a.y = L.t;
-    for (int i = 0; i < 3; i++) lap::spmv_level(h, L, lap::EPI_CHEB, a, s);
-    cudaEvent_t e0, e1;
-    LAP_CUDA(cudaEventCreate(&e0));
-    LAP_CUDA(cudaEventCreate(&e1));
-    LAP_CUDA(cudaEventRecord(e0, s));
-    double *bufs[2] = {L.x2, L.t};
+    for (int i = 0; i < 3; i++) run(i == 0);  // warm-up
     for (int i = 0; i < reps; i++) {
-        a.x = bufs[i & 1];
-        a.y = bufs[(i + 1) & 1];
-        lap::spmv_level(h, L, lap::EPI_CHEB, a, s);
+        LAP_CUDA(cudaEventRecord(ev[i], s));
+        run(false);
     }
-    LAP_CUDA(cudaEventRecord(e1, s));
-    LAP_CUDA(cudaEventSynchronize(e1));
-    float ms = 0;
-    cudaEventElapsedTime(&ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    if (ms_per_launch) *ms_per_launch = ms / reps;
-    if (bytes_per_launch) *bytes_per_launch = 12.0 * L.nnz + 56.0 * L.n;
-    if (level) *level = l;
+    LAP_CUDA(cudaEventRecord(ev[reps], s));
+    LAP_CUDA(cudaEventSynchronize(ev[reps]));
+    for (int i = 0; i < reps; i++) {
+        float t = 0;
+        cudaEventElapsedTime(&t, ev[i], ev[i + 1]);
+        if (ms) ms[i] = t;
+    }
+    for (auto &e : ev) cudaEventDestroy(e);
+    h->cur = save;
+    if (which == 1) by = 12.0 * h->lev[l].nnz + 56.0 * h->lev[l].n;  // SURVEY M3, H2 with SpMV
+    if (bytes) *bytes = by;
+    if (edges) *edges = ed;
     return LAP_OK;
     LAP_API_END
 }

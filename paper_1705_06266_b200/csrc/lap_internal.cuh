@@ -85,12 +85,15 @@ enum { KIND_AGG = 0, KIND_ELIM = 1, KIND_COARSEST = 2 };
 //   class 0: deg <= 64        SELL-32 slices (warp per 32-row slice, thread per row,
 //                             column-major padded to the slice's max degree; rows
 //                             degree-sorted first when natural order pads > 20%)
-//   class 1: 65..1024         warp per row
-//   class 2: 1025..16384      256-thread block per row
-//   class 3: > 16384          HUB_CHUNK-entry chunks (block per chunk) + ordered combine
+//   classes 1-3: deg 65..1024, 1025..16384, > 16384 (grouped by magnitude);
+//                all long rows are cut into LCHUNK-entry chunks, one warp per
+//                chunk, combined in chunk order by the last-arriving warp
+// The SpMV is one launch over the work list [SELL slices | long-row chunks].
 constexpr int NCLASS = 4;
 constexpr int64_t SHORT_MAX = 64;
-constexpr int64_t HUB_CHUNK = 16384;
+constexpr int64_t HUB_CHUNK = 16384;  // class 2/3 boundary (storage grouping only)
+constexpr int64_t LCHUNK = 1024;      // long-row chunk (entries per warp work item)
+constexpr int64_t ELIM_SHORT = 32;    // elimination restriction: longer coarse lists are chunked
 
 struct Level {
     int kind = KIND_COARSEST;
@@ -128,8 +131,11 @@ struct Level {
     int32_t *ell_col = nullptr;     // padded entries: column (own row for padding)
     double *ell_w = nullptr;        // padded entries: weight (0 for padding)
     bool sell_sorted = false;       // short rows degree-sorted
-    int64_t nchunks = 0;
-    int64_t *chunk_first = nullptr; // per hub row (nhub+1)
+    int64_t nchunks = 0;            // LCHUNK chunks over the long rows [c_end[0], n)
+    int32_t *chunk_row = nullptr;   // chunk -> storage row
+    int32_t *chunk_idx = nullptr;   // chunk -> index within its row
+    int32_t *chunk_slot = nullptr;  // chunk -> arrival counter slot (-1: one-chunk row)
+    int32_t *chunk_cnt = nullptr;   // n - c_end[0] arrival counters (kept at 0 between launches)
     double *chunk_part = nullptr;
     // transfer maps in storage space
     int32_t *agg_s = nullptr;       // agg: coarse storage index of each fine storage row
@@ -140,6 +146,9 @@ struct Level {
     int64_t *ct_ptr_s = nullptr;    // elim: coarse storage -> F neighbours (storage), coef
     int32_t *ct_f_s = nullptr;
     double *ct_coef_s = nullptr;
+    int64_t ct_nchunks = 0;         // elim: LCHUNK chunks of the coarse lists longer than ELIM_SHORT
+    int32_t *ct_crow = nullptr, *ct_cidx = nullptr, *ct_cslot = nullptr, *ct_ccnt = nullptr;
+    double *ct_cpart = nullptr;
     int32_t *fmap_s = nullptr;      // elim: coarse storage index of a C storage row, -1 for F
     double *pinv_s = nullptr;       // coarsest: L^+ in storage order
     // Chebyshev constants (O-S6), host
@@ -174,6 +183,9 @@ struct lap_hierarchy {
     // graph of the V-cycle
     cudaGraphExec_t vgraph = nullptr;
     cudaStream_t vgraph_stream = nullptr;
+    // the whole PCG loop as resident graphs (WHILE conditional node, solve.cu)
+    cudaGraphExec_t pcg_start = nullptr, pcg_resume = nullptr;
+    void *pcg_counts = nullptr;
     lap_stats stats{};
     lap::Stats cur;
     int device = 0;
@@ -204,6 +216,8 @@ void build_transfers(lap_hierarchy *h, cudaStream_t s);
 int64_t spmv_partial_slots(const Level &L);
 void vcycle(lap_hierarchy *h, int l, cudaStream_t s);   // x_l = V(l, b_l)
 void run_pcg(lap_hierarchy *h, double tol, int32_t *iters, double *relres, int *conv, cudaStream_t s);
+void capture_pcg(lap_hierarchy *h);
+void free_pcg(lap_hierarchy *h);
 
 // small shared reductions (solve.cu)
 void dot(lap_hierarchy *h, const double *a, const double *b, int64_t n, double *out, cudaStream_t s);
@@ -214,6 +228,36 @@ inline unsigned grid_for(int64_t work, int threads, int64_t cap = 148 * 32) {
     if (g < 1) g = 1;
     if (g > cap) g = cap;
     return (unsigned)g;
+}
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// Solve-phase kernels are chained with programmatic dependent launch (PDL,
+// sm_90+): each kernel is launched with programmatic stream serialization,
+// lets its dependents launch as soon as all of its CTAs are resident
+// (griddepcontrol.launch_dependents) and waits for its predecessor's memory
+// (griddepcontrol.wait) before touching any input.  Inside the captured
+// V-cycle / PCG graphs this hides the ~2-4 us launch + ramp latency of every
+// small coarse-level kernel behind its predecessor's tail.  Without the
+// launch attribute both instructions are no-ops.  LAP_PDL=0 disables it.
+bool pdl_enabled();
+__device__ __forceinline__ void pdl_begin() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    LAP_CUDA(cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...));
 }
 
 }  // namespace lap

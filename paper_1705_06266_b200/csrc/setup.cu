@@ -43,6 +43,52 @@ static void exclusive_scan_i64(const int64_t *in, int64_t *out, int64_t n, cudaS
     LAP_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, in, out, n, s)); ++g_kl;
 }
 
+// Row groups: a row is handled by G lanes (G | 32, chosen per level from the
+// average degree, group_size()), so low-degree levels do not idle 80% of a
+// warp and long rows still get several lanes.  Every lane of a warp runs the
+// same number of outer iterations (rows past n are empty), so the group
+// shuffles below always see converged warps.  All reductions done this way
+// are exact (integer / int128 / max / total-order arg-max), so the result is
+// independent of G.
+#define GROUP_LOOP_BEGIN(G, n)                                                         \
+    const int lane = threadIdx.x & 31, gl = lane & ((G)-1);                            \
+    (void)gl;                                                                          \
+    const int64_t _gpw = 32 / (G);                                                     \
+    const int64_t _stride = (((int64_t)gridDim.x * blockDim.x) >> 5) * _gpw;           \
+    for (int64_t _base = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * _gpw; \
+         _base < (n); _base += _stride) {                                              \
+        const int64_t i = _base + lane / (G);                                          \
+        const bool live = i < (n);                                                     \
+        (void)live;
+#define GROUP_LOOP_END }
+
+template <int G, class T>
+__device__ __forceinline__ T grp_sum(T v) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+template <int G>
+__device__ __forceinline__ i128 grp_sum_i128(i128 v) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += shfl_xor_i128(v, o);
+    return v;
+}
+static int group_size(int64_t n, int64_t nnz) {
+    double avg = n > 0 ? (double)nnz / (double)n : 0.0;
+    return avg <= 4.0 ? 4 : avg <= 8.0 ? 8 : avg <= 16.0 ? 16 : 32;
+}
+#define LAUNCH_G(G, kern, rows, s, ...)                                                                 \
+    do {                                                                                                \
+        switch (G) {                                                                                    \
+            case 4: kern<4><<<grid_for((rows) * 4, 256, 148 * 16), 256, 0, s>>>(__VA_ARGS__); break;    \
+            case 8: kern<8><<<grid_for((rows) * 8, 256, 148 * 16), 256, 0, s>>>(__VA_ARGS__); break;    \
+            case 16: kern<16><<<grid_for((rows) * 16, 256, 148 * 16), 256, 0, s>>>(__VA_ARGS__); break; \
+            default: kern<32><<<grid_for((rows) * 32, 256, 148 * 16), 256, 0, s>>>(__VA_ARGS__); break; \
+        }                                                                                               \
+        ++g_kl;                                                                                         \
+    } while (0)
+
 // max |v| as an exact order-independent reduction (bit pattern of a
 // non-negative double orders like the value).
 __global__ void k_max_abs(const double *__restrict__ v, int64_t n, unsigned long long *out) {
@@ -85,15 +131,14 @@ __device__ __forceinline__ int64_t find_col(const int64_t *row_ptr, const int32_
     return (lo < row_ptr[r + 1] && col[lo] == c) ? lo : -1;
 }
 
+template <int G>
 __global__ void k_validate(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                            const double *__restrict__ w, int *flag) {
-    int lane = threadIdx.x & 31;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = warp; i < n; i += nwarps) {
+    GROUP_LOOP_BEGIN(G, n)
+    if (live) {
         int64_t a = row_ptr[i], e = row_ptr[i + 1];
-        if (lane == 0 && e < a) atomicOr(flag, 1);
-        for (int64_t k = a + lane; k < e; k += 32) {
+        if (gl == 0 && e < a) atomicOr(flag, 1);
+        for (int64_t k = a + gl; k < e; k += G) {
             int32_t j = col[k];
             bool bad = (j < 0) || (j >= n) || (j == i) || (k > a && col[k - 1] >= j);
             double wk = w ? w[k] : 1.0;
@@ -106,6 +151,7 @@ __global__ void k_validate(int64_t n, const int64_t *__restrict__ row_ptr, const
             if (bad) atomicOr(flag, 1);
         }
     }
+    GROUP_LOOP_END
 }
 
 // ---- connectivity: lock-free union-find (parents only ever decrease) ----
@@ -125,13 +171,12 @@ __device__ __forceinline__ int32_t cc_find(int32_t *p, int32_t v) {
     }
     return cur;
 }
+template <int G>
 __global__ void k_cc_union(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                            int32_t *p) {
-    int lane = threadIdx.x & 31;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = warp; i < n; i += nwarps) {
-        for (int64_t k = row_ptr[i] + lane; k < row_ptr[i + 1]; k += 32) {
+    GROUP_LOOP_BEGIN(G, n)
+    if (live) {
+        for (int64_t k = row_ptr[i] + gl; k < row_ptr[i + 1]; k += G) {
             int32_t j = col[k];
             if (j < i) continue;                       // each undirected edge once
             int32_t a = cc_find(p, (int32_t)i), b = cc_find(p, j);
@@ -145,18 +190,19 @@ __global__ void k_cc_union(int64_t n, const int64_t *__restrict__ row_ptr, const
             }
         }
     }
+    GROUP_LOOP_END
 }
 __global__ void k_cc_count_roots(int64_t n, int32_t *p, unsigned long long *cnt) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         if (cc_find(p, (int32_t)i) == i) atomicAdd(cnt, 1ULL);
 }
 
-static bool is_connected(int64_t n, const int64_t *row_ptr, const int32_t *col, cudaStream_t s) {
+static bool is_connected(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col, cudaStream_t s) {
     if (n <= 1) return true;
     DBuf<int32_t> p(n, s);
     unsigned g = grid_for(n, 256, 148 * 16);
     k_cc_init<<<g, 256, 0, s>>>(n, p.p); ++g_kl;
-    k_cc_union<<<grid_for(n * 32, 256, 148 * 16), 256, 0, s>>>(n, row_ptr, col, p.p); ++g_kl;
+    LAUNCH_G(group_size(n, nnz), k_cc_union, n, s, n, row_ptr, col, p.p);
     DBuf<unsigned long long> c(1, s);
     LAP_CUDA(cudaMemsetAsync(c.p, 0, 8, s));
     k_cc_count_roots<<<g, 256, 0, s>>>(n, p.p, c.p); ++g_kl;
@@ -203,17 +249,16 @@ __global__ void k_row_ptr_from_keys(int64_t nrows, int64_t U, const uint64_t *__
 }
 
 // d_i = CanonSum of row i (warp per row); instance (e_max, K)
+template <int G>
 __global__ void k_row_canon_sum(int64_t n, const int64_t *__restrict__ row_ptr, const double *__restrict__ w,
                                 int elo, double *__restrict__ d) {
-    int lane = threadIdx.x & 31;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = warp; i < n; i += nwarps) {
-        i128 acc = 0;
-        for (int64_t k = row_ptr[i] + lane; k < row_ptr[i + 1]; k += 32) acc += canon_q(w[k], elo);
-        acc = warp_sum_i128(acc);
-        if (lane == 0) d[i] = canon_result(acc, elo);
-    }
+    GROUP_LOOP_BEGIN(G, n)
+    i128 acc = 0;
+    if (live)
+        for (int64_t k = row_ptr[i] + gl; k < row_ptr[i + 1]; k += G) acc += canon_q(w[k], elo);
+    acc = grp_sum_i128<G>(acc);
+    if (live && gl == 0) d[i] = canon_result(acc, elo);
+    GROUP_LOOP_END
 }
 
 static void row_sums(int64_t n, int64_t nnz, const int64_t *row_ptr, const double *w, double *d, double *maxw_out,
@@ -222,7 +267,7 @@ static void row_sums(int64_t n, int64_t nnz, const int64_t *row_ptr, const doubl
     if (maxw_out) *maxw_out = mw;
     int elo = canon_elo(ilogb_pos(mw) + 1, nnz);
     if (n > 0) {
-        k_row_canon_sum<<<grid_for(n * 32, 256, 148 * 16), 256, 0, s>>>(n, row_ptr, w, elo, d); ++g_kl;
+        LAUNCH_G(group_size(n, nnz), k_row_canon_sum, n, s, n, row_ptr, w, elo, d);
         LAP_CHECK_LAUNCH();
     }
 }
@@ -302,19 +347,19 @@ __global__ void k_identity_i64(int64_t n, int64_t *p) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = i;
 }
 // emit (newrow<<cb | perm[col], w) for every stored entry; warp per old row
+template <int G>
 __global__ void k_relabel_emit(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                                const double *__restrict__ w, const int64_t *__restrict__ perm, int cb,
                                uint64_t *__restrict__ keys, double *__restrict__ vals) {
-    int lane = threadIdx.x & 31;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = warp; i < n; i += nwarps) {
+    GROUP_LOOP_BEGIN(G, n)
+    if (live) {
         uint64_t r = (uint64_t)perm[i];
-        for (int64_t k = row_ptr[i] + lane; k < row_ptr[i + 1]; k += 32) {
+        for (int64_t k = row_ptr[i] + gl; k < row_ptr[i + 1]; k += G) {
             keys[k] = (r << cb) | (uint64_t)perm[col[k]];
             vals[k] = w ? w[k] : 1.0;
         }
     }
+    GROUP_LOOP_END
 }
 
 // =========================================================================
@@ -443,15 +488,14 @@ __global__ void k_tv_init(int64_t n, uint64_t base, double *X) {
 }
 
 // one synchronous damped-Jacobi sweep on the 4 columns; warp per row
+template <int G>
 __global__ void k_tv_sweep(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                            const double *__restrict__ w, const double *__restrict__ d, int elo, double omega,
                            const double *__restrict__ X, double *__restrict__ Xn) {
-    int lane = threadIdx.x & 31;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = warp; i < n; i += nwarps) {
+    GROUP_LOOP_BEGIN(G, n)
         i128 a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-        for (int64_t k = row_ptr[i] + lane; k < row_ptr[i + 1]; k += 32) {
+        const int64_t kb = live ? row_ptr[i] : 0, ke = live ? row_ptr[i + 1] : 0;
+        for (int64_t k = kb + gl; k < ke; k += G) {
             int64_t j = col[k];
             double wk = w[k];
             const double2 *xj = reinterpret_cast<const double2 *>(X + 4 * j);
@@ -461,20 +505,20 @@ __global__ void k_tv_sweep(int64_t n, const int64_t *__restrict__ row_ptr, const
             a2 += canon_q(__dmul_rn(wk, v.x), elo);
             a3 += canon_q(__dmul_rn(wk, v.y), elo);
         }
-        a0 = warp_sum_i128(a0);
-        a1 = warp_sum_i128(a1);
-        a2 = warp_sum_i128(a2);
-        a3 = warp_sum_i128(a3);
-        if (lane < 4) {
-            i128 a = lane == 0 ? a0 : lane == 1 ? a1 : lane == 2 ? a2 : a3;
+        a0 = grp_sum_i128<G>(a0);
+        a1 = grp_sum_i128<G>(a1);
+        a2 = grp_sum_i128<G>(a2);
+        a3 = grp_sum_i128<G>(a3);
+        if (live && gl < 4) {
+            i128 a = gl == 0 ? a0 : gl == 1 ? a1 : gl == 2 ? a2 : a3;
             double sk = canon_result(a, elo);
             double di = d[i];
-            double xi = X[4 * i + lane];
+            double xi = X[4 * i + gl];
             double r = __dsub_rn(__dmul_rn(di, xi), sk);
             double q = __ddiv_rn(r, di);
-            Xn[4 * i + lane] = __dsub_rn(xi, __dmul_rn(omega, q));
+            Xn[4 * i + gl] = __dsub_rn(xi, __dmul_rn(omega, q));
         }
-    }
+    GROUP_LOOP_END
 }
 
 __device__ __forceinline__ double dot4_rn(const double *a, const double *b) {
@@ -486,16 +530,16 @@ __device__ __forceinline__ double dot4_rn(const double *a, const double *b) {
 }
 
 // C_ij (O-R5) and row max M_i; warp per row
+template <int G>
 __global__ void k_affinity(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                            const double *__restrict__ X, int power, double *__restrict__ C, double *__restrict__ M) {
-    int lane = threadIdx.x & 31;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = warp; i < n; i += nwarps) {
-        double xi[4] = {X[4 * i], X[4 * i + 1], X[4 * i + 2], X[4 * i + 3]};
+    GROUP_LOOP_BEGIN(G, n)
+        const int64_t ii = live ? i : 0;
+        double xi[4] = {X[4 * ii], X[4 * ii + 1], X[4 * ii + 2], X[4 * ii + 3]};
         double ni = dot4_rn(xi, xi);
         double mx = 0.0;
-        for (int64_t k = row_ptr[i] + lane; k < row_ptr[i + 1]; k += 32) {
+        const int64_t kb = live ? row_ptr[i] : 0, ke = live ? row_ptr[i + 1] : 0;
+        for (int64_t k = kb + gl; k < ke; k += G) {
             int64_t j = col[k];
             double xj[4] = {X[4 * j], X[4 * j + 1], X[4 * j + 2], X[4 * j + 3]};
             double nj = dot4_rn(xj, xj);
@@ -506,27 +550,27 @@ __global__ void k_affinity(int64_t n, const int64_t *__restrict__ row_ptr, const
             C[k] = c;
             mx = c > mx ? c : mx;
         }
-        for (int o = 16; o > 0; o >>= 1) {
+        for (int o = G / 2; o > 0; o >>= 1) {
             double t = __shfl_xor_sync(0xffffffffu, mx, o);
             mx = t > mx ? t : mx;
         }
-        if (lane == 0) M[i] = mx;
-    }
+        if (live && gl == 0) M[i] = mx;
+    GROUP_LOOP_END
 }
 // S_ij = C_ij / max(M_i, M_j), 0 if that max is 0 (O-R16); in place
+template <int G>
 __global__ void k_normalize(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                             const double *__restrict__ M, double *__restrict__ CS) {
-    int lane = threadIdx.x & 31;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = warp; i < n; i += nwarps) {
+    GROUP_LOOP_BEGIN(G, n)
+    if (live) {
         double mi = M[i];
-        for (int64_t k = row_ptr[i] + lane; k < row_ptr[i + 1]; k += 32) {
+        for (int64_t k = row_ptr[i] + gl; k < row_ptr[i + 1]; k += G) {
             double mj = M[col[k]];
             double den = mi > mj ? mi : mj;
             CS[k] = den > 0.0 ? __ddiv_rn(CS[k], den) : 0.0;
         }
     }
+    GROUP_LOOP_END
 }
 
 // =========================================================================
@@ -544,18 +588,17 @@ __global__ void k_vote_init(int64_t n, int8_t *st, int32_t *idx, int32_t *votes)
 
 // d = S_filt oplus_agg.otimes_agg status for Undecided rows; warp per row.
 // Reads round-start state st/idx, writes nst/nidx and votes.
+template <int G>
 __global__ void k_vote_round(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                              const double *__restrict__ S, double filt, const int8_t *__restrict__ st,
                              int8_t *__restrict__ nst, int32_t *__restrict__ nidx, int32_t *__restrict__ votes) {
-    int lane = threadIdx.x & 31;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = warp; i < n; i += nwarps) {
-        if (st[i] != ST_UND) continue;                      // only Undecided act (O-R9)
+    GROUP_LOOP_BEGIN(G, n)
+        const bool act = live && st[i] == ST_UND;           // only Undecided act (O-R9)
         int br = -1;
         double bs = 0.0;
         int32_t bj = 0x7fffffff;
-        for (int64_t k = row_ptr[i] + lane; k < row_ptr[i + 1]; k += 32) {
+        const int64_t kb = act ? row_ptr[i] : 0, ke = act ? row_ptr[i + 1] : 0;
+        for (int64_t k = kb + gl; k < ke; k += G) {
             double sv = S[k];
             if (sv == 0.0 || sv < filt) continue;           // filter 2^-t, w != 0 (O-R13)
             int32_t j = col[k];
@@ -563,13 +606,13 @@ __global__ void k_vote_round(int64_t n, const int64_t *__restrict__ row_ptr, con
             if (r == ST_DEC) continue;                      // (O-R12)
             if (r > br || (r == br && (sv > bs || (sv == bs && j < bj)))) { br = r; bs = sv; bj = j; }
         }
-        for (int o = 16; o > 0; o >>= 1) {                  // warp arg-max under (rank, S, -j)
+        for (int o = G / 2; o > 0; o >>= 1) {               // group arg-max under (rank, S, -j)
             int r2 = __shfl_xor_sync(0xffffffffu, br, o);
             double s2 = __shfl_xor_sync(0xffffffffu, bs, o);
             int32_t j2 = __shfl_xor_sync(0xffffffffu, bj, o);
             if (r2 > br || (r2 == br && (s2 > bs || (s2 == bs && j2 < bj)))) { br = r2; bs = s2; bj = j2; }
         }
-        if (lane == 0 && br >= 0) {
+        if (act && gl == 0 && br >= 0) {
             if (br == ST_SEED) {
                 nst[i] = ST_DEC;
                 nidx[i] = bj;
@@ -577,7 +620,7 @@ __global__ void k_vote_round(int64_t n, const int64_t *__restrict__ row_ptr, con
                 atomicAdd(&votes[bj], 1);
             }
         }
-    }
+    GROUP_LOOP_END
 }
 __global__ void k_vote_promote(int64_t n, int8_t *nst, const int32_t *votes, int thr) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -596,38 +639,44 @@ __global__ void k_agg_ids(int64_t n, const int8_t *st, const int32_t *idx, const
 // O-S5 Galerkin (O-R24)
 // =========================================================================
 
+template <int G>
 __global__ void k_gal_count(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                             const int32_t *__restrict__ agg, int64_t *cnt) {
-    int lane = threadIdx.x & 31;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = warp; i < n; i += nwarps) {
-        int32_t a = agg[i];
+    GROUP_LOOP_BEGIN(G, n)
         int64_t c = 0;
-        for (int64_t k = row_ptr[i] + lane; k < row_ptr[i + 1]; k += 32) c += (agg[col[k]] != a);
-        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        if (lane == 0) cnt[i] = c;
-    }
+        if (live) {
+            int32_t a = agg[i];
+            for (int64_t k = row_ptr[i] + gl; k < row_ptr[i + 1]; k += G) c += (agg[col[k]] != a);
+        }
+        c = grp_sum<G>(c);
+        if (live && gl == 0) cnt[i] = c;
+    GROUP_LOOP_END
 }
+template <int G>
 __global__ void k_gal_emit(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                            const double *__restrict__ w, const int32_t *__restrict__ agg,
                            const int64_t *__restrict__ off, int cb, uint64_t *__restrict__ keys,
                            double *__restrict__ vals) {
-    int lane = threadIdx.x & 31;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = warp; i < n; i += nwarps) {
-        uint64_t a = (uint64_t)agg[i];
-        int64_t o = off[i];
-        for (int64_t base = row_ptr[i]; base < row_ptr[i + 1]; base += 32) {
-            int64_t k = base + lane;
+    GROUP_LOOP_BEGIN(G, n)
+        const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (lane & ~(G - 1));
+        uint64_t a = live ? (uint64_t)agg[i] : 0;
+        int64_t o = live ? off[i] : 0;
+        const int64_t kb = live ? row_ptr[i] : 0, ke = live ? row_ptr[i + 1] : 0;
+        // the group with the longest row sets the trip count for the warp
+        int64_t len = ke - kb;
+        for (int sh = 16; sh > 0; sh >>= 1) {
+            int64_t t = __shfl_xor_sync(0xffffffffu, len, sh);
+            len = t > len ? t : len;
+        }
+        for (int64_t q = 0; q < len; q += G) {
+            int64_t k = kb + q + gl;
             bool take = false;
             uint64_t b = 0;
-            if (k < row_ptr[i + 1]) {
+            if (k < ke) {
                 b = (uint64_t)agg[col[k]];
                 take = (b != a);
             }
-            unsigned m = __ballot_sync(0xffffffffu, take);
+            unsigned m = __ballot_sync(0xffffffffu, take) & gmask;
             if (take) {
                 int64_t p = o + __popc(m & ((1u << lane) - 1));
                 keys[p] = (a << cb) | b;
@@ -635,7 +684,7 @@ __global__ void k_gal_emit(int64_t n, const int64_t *__restrict__ row_ptr, const
             }
             o += __popc(m);
         }
-    }
+    GROUP_LOOP_END
 }
 
 // =========================================================================
@@ -920,7 +969,8 @@ static void build_elim_level(lap_hierarchy *h, Level &L, const DBuf<uint8_t> &F,
 static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt, DBuf<double> &S, cudaStream_t s) {
     int64_t n = L.n, nnz = L.nnz;
     const lap_params &p = h->p;
-    unsigned gw = grid_for(n * 32, 256, 148 * 16), ge = grid_for(n, 256, 148 * 16);
+    unsigned ge = grid_for(n, 256, 148 * 16);
+    const int G = group_size(n, nnz);
     // test vectors
     DBuf<double> X(4 * n, s), Xn(4 * n, s), M(n, s);
     uint64_t base = mix64(salt_of(p.seed, 3) ^ (uint64_t)(2 * l + attempt));
@@ -930,14 +980,14 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
     for (int sw = 0; sw < p.tv_sweeps; sw++) {
         double mx = max_abs(X.p, 4 * n, s);
         int e_max = mx > 0.0 ? ew + ilogb_pos(mx) + 2 : ew + 1;
-        k_tv_sweep<<<gw, 256, 0, s>>>(n, L.row_ptr, L.col, L.w, L.d, canon_elo(e_max, nnz), p.tv_omega, X.p, Xn.p); ++g_kl;
+        LAUNCH_G(G, k_tv_sweep, n, s, n, L.row_ptr, L.col, L.w, L.d, canon_elo(e_max, nnz), p.tv_omega, X.p, Xn.p);
         LAP_CHECK_LAUNCH();
         std::swap(X.p, Xn.p);
         h->cur.edges += nnz;
     }
     // affinity + normalisation
-    k_affinity<<<gw, 256, 0, s>>>(n, L.row_ptr, L.col, X.p, p.affinity_power, S.p, M.p); ++g_kl;
-    k_normalize<<<gw, 256, 0, s>>>(n, L.row_ptr, L.col, M.p, S.p); ++g_kl;
+    LAUNCH_G(G, k_affinity, n, s, n, L.row_ptr, L.col, X.p, p.affinity_power, S.p, M.p);
+    LAUNCH_G(G, k_normalize, n, s, n, L.row_ptr, L.col, M.p, S.p);
     LAP_CHECK_LAUNCH();
     h->cur.edges += 2 * nnz;
     // voting rounds (Alg. 3)
@@ -948,7 +998,7 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
         double filt = ldexp(1.0, -t);
         LAP_CUDA(cudaMemcpyAsync(nst.p, st.p, n, cudaMemcpyDeviceToDevice, s));
         LAP_CUDA(cudaMemcpyAsync(nidx.p, idx.p, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
-        k_vote_round<<<gw, 256, 0, s>>>(n, L.row_ptr, L.col, S.p, filt, st.p, nst.p, nidx.p, votes.p); ++g_kl;
+        LAUNCH_G(G, k_vote_round, n, s, n, L.row_ptr, L.col, S.p, filt, st.p, nst.p, nidx.p, votes.p);
         k_vote_promote<<<ge, 256, 0, s>>>(n, nst.p, votes.p, p.vote_threshold); ++g_kl;
         LAP_CHECK_LAUNCH();
         std::swap(st.p, nst.p);
@@ -970,15 +1020,15 @@ static void galerkin(lap_hierarchy *h, Level &L, Level &N, cudaStream_t s) {
     int64_t n = L.n, m = L.m;
     DBuf<int64_t> cnt(n + 1, s), off(n + 1, s);
     LAP_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int64_t) * (n + 1), s));
-    unsigned gw = grid_for(n * 32, 256, 148 * 16);
-    k_gal_count<<<gw, 256, 0, s>>>(n, L.row_ptr, L.col, L.agg, cnt.p); ++g_kl;
+    const int G = group_size(n, L.nnz);
+    LAUNCH_G(G, k_gal_count, n, s, n, L.row_ptr, L.col, L.agg, cnt.p);
     LAP_CHECK_LAUNCH();
     exclusive_scan_i64(cnt.p, off.p, n + 1, s);
     int64_t T = d2h_scalar(off.p + n, s);
     int cb = bitlen_u64((uint64_t)(m > 0 ? m : 1));
     DBuf<uint64_t> keys(T, s);
     DBuf<double> vals(T, s);
-    k_gal_emit<<<gw, 256, 0, s>>>(n, L.row_ptr, L.col, L.w, L.agg, off.p, cb, keys.p, vals.p); ++g_kl;
+    LAUNCH_G(G, k_gal_emit, n, s, n, L.row_ptr, L.col, L.w, L.agg, off.p, cb, keys.p, vals.p);
     LAP_CHECK_LAUNCH();
     csr_from_terms(m, cb, T, keys, vals, ilogb_pos(L.maxw) + 1, L.nnz, true, N, s);
     h->cur.edges += L.nnz;
@@ -1027,11 +1077,11 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
         if (n > 0) {
             int64_t first = d2h_scalar(rp, s);
             if (first != 0) throw Error{LAP_EGRAPH, "row_ptr[0] != 0"};
-            k_validate<<<grid_for(n * 32, 256, 148 * 16), 256, 0, s>>>(n, rp, col, w, flag.p); ++g_kl;
+            LAUNCH_G(group_size(n, nnz), k_validate, n, s, n, rp, col, w, flag.p);
             LAP_CHECK_LAUNCH();
         }
         if (d2h_scalar(flag.p, s)) throw Error{LAP_EGRAPH, "graph is not a valid symmetric positive-weight adjacency"};
-        if (!is_connected(n, rp, col, s)) throw Error{LAP_EDISCONNECTED, "graph is disconnected"};
+        if (!is_connected(n, nnz, rp, col, s)) throw Error{LAP_EDISCONNECTED, "graph is disconnected"};
     }
     // --- O-S1 level 0
     h->perm = (int64_t *)dalloc(sizeof(int64_t) * (size_t)n, s);
@@ -1058,7 +1108,7 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
         DBuf<uint64_t> keys(nnz, s);
         DBuf<double> vals(nnz, s);
         if (nnz) {
-            k_relabel_emit<<<grid_for(n * 32, 256, 148 * 16), 256, 0, s>>>(n, rp, col, w, h->perm, cb, keys.p, vals.p); ++g_kl;
+            LAUNCH_G(group_size(n, nnz), k_relabel_emit, n, s, n, rp, col, w, h->perm, cb, keys.p, vals.p);
             LAP_CHECK_LAUNCH();
         }
         csr_from_terms(n, cb, nnz, keys, vals, 0, 0, false, L0, s);

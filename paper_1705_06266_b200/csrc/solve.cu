@@ -68,92 +68,167 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
     return r;  // valid in thread 0
 }
 
-// class 0: SELL-32 (rows of <= SHORT_MAX entries).  A warp owns a 32-row
-// slice, a thread owns a row; the slice is stored column-major and padded to
-// its widest row, so every col/w load instruction is one fully coalesced
-// 128/256-byte access.  Epilogue operands are loaded before the gather loop
-// so their latency overlaps it.  No shared memory, no barriers.
+// One SpMV = ONE launch over a combined work list of warp-sized items:
+//
+//   items [0, nslices)               SELL-32 slices of the short rows (deg <= 64):
+//                                    a warp owns a 32-row slice, a thread owns a
+//                                    row; the slice is column-major and padded to
+//                                    its widest row, so every col/w load is one
+//                                    fully coalesced 128/256-byte access.
+//   items [nslices, nslices+nchunks) LCHUNK-entry chunks of the long rows
+//                                    (deg > 64, any length up to hubs): a warp
+//                                    streams one chunk (32 lanes x 4 independent
+//                                    accumulators), reduces it with shuffles and
+//                                    either applies the epilogue (one-chunk row)
+//                                    or stores a chunk partial; the LAST warp to
+//                                    finish a row (per-row arrival counter) sums
+//                                    that row's partials in chunk order and
+//                                    applies the epilogue.
+//
+// Every warp does at most ~2K entries, so hubs of any degree and dense-ish
+// coarse levels are load balanced, and no class runs alone on a partly idle
+// GPU.  No fp64 atomics: per-chunk sums and the in-order combine are fixed, so
+// results are bitwise reproducible run to run.
 template <int EPI>
-__global__ void __launch_bounds__(256, 6) k_spmv_sell(int64_t nslices, int64_t nrows, const int64_t *__restrict__ sp,
-                                                   const int32_t *__restrict__ ec, const double *__restrict__ ew,
-                                                   Csr A, EpiArgs a, double *__restrict__ partials) {
-    __shared__ double sh[8];
-    const int lane = threadIdx.x & 31;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    double dacc = 0.0;
-    for (int64_t sl = warp; sl < nslices; sl += nwarps) {
-        const int64_t i = sl * 32 + lane;
-        const int64_t beg = sp[sl], end = sp[sl + 1];
-        double xi = 0.0, di = 0.0, bi = 0.0, dvi = 0.0;
-        const bool live = i < nrows;
-        if (live) {
-            xi = a.x[i];
-            di = A.d[i];
-            if (EPI == E_RESID || EPI == E_CHEB || EPI == E_CHEB0) bi = a.b[i];
-            if (EPI == E_CHEB) dvi = a.dv[i];
-        }
-        double acc0 = 0.0, acc1 = 0.0;
-        int64_t k = beg + lane;
-        for (; k + 32 < end; k += 64) {
-            int c0 = __ldg(&ec[k]), c1 = __ldg(&ec[k + 32]);
-            double w0 = __ldg(&ew[k]), w1 = __ldg(&ew[k + 32]);
-            acc0 += w0 * a.x[c0];
-            acc1 += w1 * a.x[c1];
-        }
-        if (k < end) acc0 += __ldg(&ew[k]) * a.x[__ldg(&ec[k])];
-        if (live) {
-            double ax = acc0 + acc1;
-            double lx = di * xi - ax;
-            if (EPI == E_SPMV) {
-                a.y[i] = lx;
-            } else if (EPI == E_DOT) {
-                a.y[i] = lx;
-                dacc += xi * lx;
-            } else if (EPI == E_RESID) {
-                a.y[i] = bi - lx;
-            } else if (EPI == E_CHEB) {
-                double dv = a.c1 * dvi + a.c2 * ((bi - lx) / di);
-                a.dv[i] = dv;
-                a.y[i] = xi + dv;
-            } else if (EPI == E_CHEB0) {
-                double dv = a.c2 * ((bi - lx) / di);
-                a.dv[i] = dv;
-                a.y[i] = xi + dv;
+__device__ __forceinline__ void sell_slice(int64_t sl, int lane, int64_t nrows, const int64_t *__restrict__ sp,
+                                           const int32_t *__restrict__ ec, const double *__restrict__ ew, const Csr &A,
+                                           const EpiArgs &a, double &dacc) {
+    const int64_t i = sl * 32 + lane;
+    const int64_t beg = sp[sl], end = sp[sl + 1];
+    double xi = 0.0, di = 0.0, bi = 0.0, dvi = 0.0;
+    const bool live = i < nrows;
+    if (live) {
+        xi = a.x[i];
+        di = A.d[i];
+        if (EPI == E_RESID || EPI == E_CHEB || EPI == E_CHEB0) bi = a.b[i];
+        if (EPI == E_CHEB) dvi = a.dv[i];
+    }
+    // batches of 8 padded columns: all 16 index/weight loads of a batch are
+    // issued before the 8 dependent x gathers (memory-level parallelism for
+    // the short rows of grids and power-law tails)
+    const int width = (int)((end - beg) >> 5);
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int q = 0; q < width; q += 8) {
+        int c[8];
+        double wv[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            if (q + u < width) {
+                c[u] = __ldg(&ec[beg + (int64_t)(q + u) * 32 + lane]);
+                wv[u] = __ldg(&ew[beg + (int64_t)(q + u) * 32 + lane]);
             }
         }
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) {
+            if (q + u < width) acc0 += wv[u] * a.x[c[u]];
+            if (q + u + 1 < width) acc1 += wv[u + 1] * a.x[c[u + 1]];
+        }
     }
-    if (EPI == E_DOT) {
-        double r = block_sum(dacc, sh);
-        if (threadIdx.x == 0) partials[blockIdx.x] = r;
+    if (live) {
+        double ax = acc0 + acc1;
+        double lx = di * xi - ax;
+        if (EPI == E_SPMV) {
+            a.y[i] = lx;
+        } else if (EPI == E_DOT) {
+            a.y[i] = lx;
+            dacc += xi * lx;
+        } else if (EPI == E_RESID) {
+            a.y[i] = bi - lx;
+        } else if (EPI == E_CHEB) {
+            double dv = a.c1 * dvi + a.c2 * ((bi - lx) / di);
+            a.dv[i] = dv;
+            a.y[i] = xi + dv;
+        } else if (EPI == E_CHEB0) {
+            double dv = a.c2 * ((bi - lx) / di);
+            a.dv[i] = dv;
+            a.y[i] = xi + dv;
+        }
     }
 }
 
-// class 1: warp per row, rows [row0, row0 + cnt)
+struct LongRows {
+    int64_t nchunks;
+    const int32_t *__restrict__ crow;   // chunk -> storage row
+    const int32_t *__restrict__ cidx;   // chunk -> index of the chunk within its row
+    const int32_t *__restrict__ cslot;  // chunk -> arrival-counter slot of its row (-1: one-chunk row)
+    double *__restrict__ cpart;         // chunk partial sums
+    int32_t *__restrict__ ccnt;         // per multi-chunk row: arrivals (reset by the combiner)
+};
+
+// Sum of chunk c of a long CSR row (all 32 lanes).  Returns true (on every
+// lane) iff this warp must finish the row: either the row is a single chunk,
+// or this warp is the last of the row's chunks to arrive, in which case the
+// row's partials are summed in chunk order.  *sum is valid on lane 0.
+__device__ __forceinline__ bool chunk_reduce(int64_t c, int lane, const int64_t *__restrict__ rp,
+                                             const int32_t *__restrict__ col, const double *__restrict__ w,
+                                             const double *__restrict__ x, const LongRows &R, int64_t &row,
+                                             double &sum) {
+    const int64_t i = R.crow[c];
+    const int64_t rb = rp[i], re = rp[i + 1];
+    const int64_t j = R.cidx[c];
+    const int64_t b = rb + j * LCHUNK, e = min(re, b + LCHUNK);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int64_t k = b + lane;
+    for (; k + 96 < e; k += 128) {
+        int c0 = __ldg(&col[k]), c1 = __ldg(&col[k + 32]), c2 = __ldg(&col[k + 64]), c3 = __ldg(&col[k + 96]);
+        double w0 = __ldg(&w[k]), w1 = __ldg(&w[k + 32]), w2 = __ldg(&w[k + 64]), w3 = __ldg(&w[k + 96]);
+        a0 += w0 * x[c0];
+        a1 += w1 * x[c1];
+        a2 += w2 * x[c2];
+        a3 += w3 * x[c3];
+    }
+    for (; k < e; k += 32) a0 += __ldg(&w[k]) * x[__ldg(&col[k])];
+    double acc = (a0 + a1) + (a2 + a3);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    row = i;
+    const int slot = R.cslot[c];
+    if (slot < 0) {  // the whole row in one chunk
+        sum = acc;
+        return true;
+    }
+    const int nch = (int)((re - rb + LCHUNK - 1) / LCHUNK);
+    int last = 0;
+    if (lane == 0) {
+        R.cpart[c] = acc;
+        __threadfence();
+        last = atomicAdd(&R.ccnt[slot], 1) == nch - 1;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) return false;
+    __threadfence();
+    const int64_t c0 = c - j;  // first chunk of the row
+    double s2 = 0.0;
+    for (int q = lane; q < nch; q += 32) s2 += __ldcg(&R.cpart[c0 + q]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    if (lane == 0) R.ccnt[slot] = 0;
+    sum = s2;
+    return true;
+}
+
 template <int EPI>
-__global__ void __launch_bounds__(256) k_spmv_warp(int64_t cnt, int64_t row0, Csr A, EpiArgs a,
-                                                   double *__restrict__ partials) {
+__device__ __forceinline__ void long_chunk(int64_t c, int lane, const Csr &A, const LongRows &R, const EpiArgs &a,
+                                           double &dacc) {
+    int64_t i;
+    double ax;
+    if (chunk_reduce(c, lane, A.rp, A.col, A.w, a.x, R, i, ax) && lane == 0) apply_epi<EPI>(i, ax, A, a, dacc);
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(256, 4) k_spmv(int64_t nslices, int64_t nshort, const int64_t *__restrict__ sp,
+                                              const int32_t *__restrict__ ec, const double *__restrict__ ew, Csr A,
+                                              LongRows R, EpiArgs a, double *__restrict__ partials) {
+    pdl_begin();
     __shared__ double sh[8];
     const int lane = threadIdx.x & 31;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nitems = nslices + R.nchunks;
     double dacc = 0.0;
-    for (int64_t t = warp; t < cnt; t += nwarps) {
-        int64_t i = row0 + t;
-        int64_t s = A.rp[i], e = A.rp[i + 1];
-        double a0 = 0.0, a1 = 0.0;
-        int64_t k = s + lane;
-        for (; k + 32 < e; k += 64) {
-            int c0 = __ldg(&A.col[k]), c1 = __ldg(&A.col[k + 32]);
-            double w0 = __ldg(&A.w[k]), w1 = __ldg(&A.w[k + 32]);
-            a0 += w0 * a.x[c0];
-            a1 += w1 * a.x[c1];
-        }
-        if (k < e) a0 += __ldg(&A.w[k]) * a.x[__ldg(&A.col[k])];
-        double acc = a0 + a1;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) apply_epi<EPI>(i, acc, A, a, dacc);
+    for (int64_t t = warp; t < nitems; t += nwarps) {
+        if (t < nslices) sell_slice<EPI>(t, lane, nshort, sp, ec, ew, A, a, dacc);
+        else long_chunk<EPI>(t - nslices, lane, A, R, a, dacc);
     }
     if (EPI == E_DOT) {
         double r = block_sum(dacc, sh);
@@ -161,111 +236,21 @@ __global__ void __launch_bounds__(256) k_spmv_warp(int64_t cnt, int64_t row0, Cs
     }
 }
 
-// class 2: one 256-thread block per row
-template <int EPI>
-__global__ void __launch_bounds__(256) k_spmv_block(int64_t cnt, int64_t row0, Csr A, EpiArgs a,
-                                                    double *__restrict__ partials) {
-    __shared__ double sh[8];
-    double dacc = 0.0;
-    for (int64_t t = blockIdx.x; t < cnt; t += gridDim.x) {
-        int64_t i = row0 + t;
-        int64_t s = A.rp[i], e = A.rp[i + 1];
-        double acc = 0.0;
-#pragma unroll 4
-        for (int64_t k = s + threadIdx.x; k < e; k += blockDim.x) acc += __ldg(&A.w[k]) * a.x[__ldg(&A.col[k])];
-        double r = block_sum(acc, sh);
-        if (threadIdx.x == 0) apply_epi<EPI>(i, r, A, a, dacc);
-    }
-    if (EPI == E_DOT) {
-        __syncthreads();
-        double r = block_sum(threadIdx.x == 0 ? dacc : 0.0, sh);
-        if (threadIdx.x == 0) partials[blockIdx.x] = r;
-    }
+// fixed launch geometry per level (deterministic partial slots for E_DOT)
+static unsigned spmv_grid(const Level &L) {
+    int64_t items = L.nslices + L.nchunks;
+    return grid_for(items * 32, 256, 148 * 4);  // one resident wave (4 CTAs of 256 per SM at 64 regs)
 }
 
-// class 3: block per HUB_CHUNK-entry chunk -> ordered partial sums, then epilogue
-__global__ void __launch_bounds__(256) k_spmv_hub_chunks(int64_t nchunks, int64_t nhub, int64_t row0,
-                                                         const int64_t *__restrict__ cfirst, Csr A,
-                                                         const double *__restrict__ x, double *__restrict__ cpart) {
-    __shared__ double sh[8];
-    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-        int64_t lo = 0, hi = nhub;  // last h with cfirst[h] <= c
-        while (hi - lo > 1) {
-            int64_t mid = (lo + hi) >> 1;
-            if (cfirst[mid] <= c) lo = mid;
-            else hi = mid;
-        }
-        int64_t i = row0 + lo;
-        int64_t s = A.rp[i] + (c - cfirst[lo]) * HUB_CHUNK;
-        int64_t e = min(A.rp[i + 1], s + HUB_CHUNK);
-        double acc = 0.0;
-#pragma unroll 4
-        for (int64_t k = s + threadIdx.x; k < e; k += blockDim.x) acc += __ldg(&A.w[k]) * x[__ldg(&A.col[k])];
-        double r = block_sum(acc, sh);
-        if (threadIdx.x == 0) cpart[c] = r;
-    }
-}
-template <int EPI>
-__global__ void k_spmv_hub_epi(int64_t nhub, int64_t row0, const int64_t *__restrict__ cfirst,
-                               const double *__restrict__ cpart, Csr A, EpiArgs a, double *__restrict__ partials) {
-    __shared__ double sh[8];
-    double dacc = 0.0;
-    for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < nhub; h += (int64_t)gridDim.x * blockDim.x) {
-        double ax = 0.0;
-        for (int64_t c = cfirst[h]; c < cfirst[h + 1]; c++) ax += cpart[c];
-        apply_epi<EPI>(row0 + h, ax, A, a, dacc);
-    }
-    if (EPI == E_DOT) {
-        double r = block_sum(dacc, sh);
-        if (threadIdx.x == 0) partials[blockIdx.x] = r;
-    }
-}
-
-// launch geometry per class (fixed for a level -> deterministic partial slots)
-static unsigned class_grid(const Level &L, int c) {
-    int64_t lo = c == 0 ? 0 : L.c_end[c - 1];
-    int64_t cnt = L.c_end[c] - lo;
-    if (cnt <= 0) return 0;
-    switch (c) {
-        case 0: return grid_for(L.nslices * 32, 256, 148 * 16);
-        case 1: return grid_for(cnt * 32, 256, 148 * 8);
-        case 2: return (unsigned)std::min<int64_t>(cnt, 148 * 8);
-        default: return grid_for(cnt, 256, 148);
-    }
-}
-
-int64_t spmv_partial_slots(const Level &L) {
-    int64_t t = 0;
-    for (int c = 0; c < NCLASS; c++) t += class_grid(L, c);
-    return t;
-}
+int64_t spmv_partial_slots(const Level &L) { return spmv_grid(L); }
 
 template <int EPI>
 static void spmv_dispatch(lap_hierarchy *h, const Level &L, const EpiArgs &a, cudaStream_t s) {
     Csr A{L.srp, L.scol, L.sw, L.sd};
-    double *part = a.partials;
-    int64_t slot = 0;
-    for (int c = 0; c < NCLASS; c++) {
-        int64_t row0 = c == 0 ? 0 : L.c_end[c - 1];
-        int64_t cnt = L.c_end[c] - row0;
-        if (cnt <= 0) continue;
-        unsigned g = class_grid(L, c);
-        double *pp = part ? part + slot : nullptr;
-        switch (c) {
-            case 0: k_spmv_sell<EPI><<<g, 256, 0, s>>>(L.nslices, cnt, L.slice_ptr, L.ell_col, L.ell_w, A, a, pp); break;
-            case 1: k_spmv_warp<EPI><<<g, 256, 0, s>>>(cnt, row0, A, a, pp); break;
-            case 2: k_spmv_block<EPI><<<g, 256, 0, s>>>(cnt, row0, A, a, pp); break;
-            default: {
-                unsigned gc = (unsigned)std::min<int64_t>(L.nchunks, 148 * 8);
-                k_spmv_hub_chunks<<<gc, 256, 0, s>>>(L.nchunks, cnt, row0, L.chunk_first, A, a.x, L.chunk_part);
-                k_spmv_hub_epi<EPI><<<g, 256, 0, s>>>(cnt, row0, L.chunk_first, L.chunk_part, A, a, pp);
-                h->cur.launches++;
-                break;
-            }
-        }
-        h->cur.launches++;
-        slot += g;
-    }
+    LongRows R{L.nchunks, L.chunk_row, L.chunk_idx, L.chunk_slot, L.chunk_part, L.chunk_cnt};
+    launch_pdl(k_spmv<EPI>, spmv_grid(L), 256, s, L.nslices, L.c_end[0], (const int64_t *)L.slice_ptr,
+               (const int32_t *)L.ell_col, (const double *)L.ell_w, A, R, a, a.partials);
+    h->cur.launches++;
     LAP_CHECK_LAUNCH();
 }
 
@@ -288,6 +273,7 @@ constexpr int RED_BLOCKS = 296;  // fixed: deterministic two-pass reductions
 
 __global__ void __launch_bounds__(256) k_dot_partial(int64_t n, const double *__restrict__ a,
                                                      const double *__restrict__ b, double *__restrict__ part) {
+    pdl_begin();
     __shared__ double sh[8];
     double acc = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -297,6 +283,7 @@ __global__ void __launch_bounds__(256) k_dot_partial(int64_t n, const double *__
 }
 __global__ void __launch_bounds__(256) k_reduce_final(const double *__restrict__ part, int64_t np,
                                                       double *__restrict__ out) {
+    pdl_begin();
     __shared__ double sh[8];
     double acc = 0.0;
     for (int64_t i = threadIdx.x; i < np; i += blockDim.x) acc += part[i];
@@ -305,13 +292,13 @@ __global__ void __launch_bounds__(256) k_reduce_final(const double *__restrict__
 }
 
 void reduce_partials(lap_hierarchy *h, const double *partials, int64_t np, double *out, cudaStream_t s) {
-    k_reduce_final<<<1, 256, 0, s>>>(partials, np, out);
+    launch_pdl(k_reduce_final, 1, 256, s, partials, np, out);
     h->cur.launches++;
     LAP_CHECK_LAUNCH();
 }
 
 void dot(lap_hierarchy *h, const double *a, const double *b, int64_t n, double *out, cudaStream_t s) {
-    k_dot_partial<<<RED_BLOCKS, 256, 0, s>>>(n, a, b, h->partials);
+    launch_pdl(k_dot_partial, RED_BLOCKS, 256, s, n, a, b, h->partials);
     h->cur.launches++;
     reduce_partials(h, h->partials, RED_BLOCKS, out, s);
 }
@@ -319,6 +306,7 @@ void dot(lap_hierarchy *h, const double *a, const double *b, int64_t n, double *
 // ------------------------------------------------------------------ V-cycle kernels
 __global__ void k_cheb_first(int64_t n, const double *__restrict__ b, const double *__restrict__ d, double inv_theta,
                              double *__restrict__ x, double *__restrict__ dv) {
+    pdl_begin();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         double v = (b[i] / d[i]) * inv_theta;
         dv[i] = v;
@@ -329,6 +317,7 @@ __global__ void k_cheb_first(int64_t n, const double *__restrict__ b, const doub
 __global__ void __launch_bounds__(256) k_restrict(int64_t m, const int64_t *__restrict__ mp,
                                                   const int32_t *__restrict__ mem, const double *__restrict__ r,
                                                   double *__restrict__ rc) {
+    pdl_begin();
     const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
     int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -343,17 +332,40 @@ __global__ void __launch_bounds__(256) k_restrict(int64_t m, const int64_t *__re
 }
 __global__ void k_prolong(int64_t n, const int32_t *__restrict__ agg, const double *__restrict__ xc,
                           double *__restrict__ x) {
+    pdl_begin();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         x[i] += xc[agg[i]];
 }
 // P^T b on an elimination level: b'_k = b_{cid[k]} + sum_{f ~ cid[k]} (w_fc/d_f) b_f
-__global__ void k_elim_restrict(int64_t nc, const int32_t *__restrict__ cid, const int64_t *__restrict__ ctp,
-                                const int32_t *__restrict__ ctf, const double *__restrict__ ctc,
-                                const double *__restrict__ b, double *__restrict__ bc) {
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nc; k += (int64_t)gridDim.x * blockDim.x) {
-        double s = b[cid[k]];
-        for (int64_t q = ctp[k]; q < ctp[k + 1]; q++) s += ctc[q] * b[ctf[q]];
-        bc[k] = s;
+// Work list: warps of 32 coarse rows (thread per row, lists of <= ELIM_SHORT
+// entries) followed by LCHUNK chunks of the long lists (hub C vertices with
+// thousands of eliminated neighbours), combined in chunk order.
+template <int UNUSED>
+__global__ void __launch_bounds__(256) k_elim_restrict(int64_t nc, const int32_t *__restrict__ cid,
+                                                       const int64_t *__restrict__ ctp, const int32_t *__restrict__ ctf,
+                                                       const double *__restrict__ ctc, LongRows R,
+                                                       const double *__restrict__ b, double *__restrict__ bc) {
+    pdl_begin();
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nrw = (nc + 31) / 32;
+    for (int64_t t = warp; t < nrw + R.nchunks; t += nwarps) {
+        if (t < nrw) {
+            const int64_t k = t * 32 + lane;
+            if (k < nc) {
+                const int64_t q0 = ctp[k], q1 = ctp[k + 1];
+                if (q1 - q0 <= ELIM_SHORT) {
+                    double s = b[cid[k]];
+                    for (int64_t q = q0; q < q1; q++) s += ctc[q] * b[ctf[q]];
+                    bc[k] = s;
+                }
+            }
+        } else {
+            int64_t k;
+            double s;
+            if (chunk_reduce(t - nrw, lane, ctp, ctf, ctc, b, R, k, s) && lane == 0) bc[k] = b[cid[k]] + s;
+        }
     }
 }
 // x = P x' + Fsmooth(b): x_c = x'_idx(c); x_f = (b_f + sum_c w_fc x'_idx(c)) / d_f
@@ -361,6 +373,7 @@ __global__ void k_elim_restrict(int64_t nc, const int32_t *__restrict__ cid, con
 __global__ void k_elim_prolong(int64_t nc, int64_t nf, const int32_t *__restrict__ cid, const int32_t *__restrict__ flist,
                                const int32_t *__restrict__ fmap, Csr A, const double *__restrict__ b,
                                const double *__restrict__ xc, double *__restrict__ x) {
+    pdl_begin();
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nc + nf; t += (int64_t)gridDim.x * blockDim.x) {
         if (t < nc) {
             x[cid[t]] = xc[t];
@@ -375,6 +388,7 @@ __global__ void k_elim_prolong(int64_t nc, int64_t nf, const int32_t *__restrict
 // x = L_c^+ b (warp per row)
 __global__ void k_coarse_gemv(int64_t n, const double *__restrict__ P, const double *__restrict__ b,
                               double *__restrict__ x) {
+    pdl_begin();
     int lane = threadIdx.x & 31;
     int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -393,7 +407,7 @@ static void vcycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, c
     Level &L = h->lev[l];
     int64_t n = L.n;
     if (L.kind == KIND_COARSEST) {
-        k_coarse_gemv<<<grid_for(n * 32, 256, 148), 256, 0, s>>>(n, L.pinv_s, b, xout);
+        launch_pdl(k_coarse_gemv, grid_for(n * 32, 256, 148), 256, s, n, L.pinv_s, b, xout);
         h->cur.launches++;
         LAP_CHECK_LAUNCH();
         return;
@@ -401,11 +415,14 @@ static void vcycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, c
     Level &C = h->lev[l + 1];
     if (L.kind == KIND_ELIM) {
         int64_t nc = C.n;
-        k_elim_restrict<<<eg(nc), 256, 0, s>>>(nc, L.cid_s, L.ct_ptr_s, L.ct_f_s, L.ct_coef_s, b, C.b);
+        LongRows R{L.ct_nchunks, L.ct_crow, L.ct_cidx, L.ct_cslot, L.ct_cpart, L.ct_ccnt};
+        launch_pdl(k_elim_restrict<0>, grid_for(((nc + 31) / 32 + L.ct_nchunks) * 32, 256, 148 * 8), 256, s, nc,
+                   (const int32_t *)L.cid_s, (const int64_t *)L.ct_ptr_s, (const int32_t *)L.ct_f_s,
+                   (const double *)L.ct_coef_s, R, b, C.b);
         h->cur.launches++;
         vcycle_rec(h, l + 1, C.b, C.x, s);
         Csr A{L.srp, L.scol, L.sw, L.sd};
-        k_elim_prolong<<<eg(nc + L.nF), 256, 0, s>>>(nc, L.nF, L.cid_s, L.flist, L.fmap_s, A, b, C.x, xout);
+        launch_pdl(k_elim_prolong, eg(nc + L.nF), 256, s, nc, L.nF, L.cid_s, L.flist, L.fmap_s, A, b, C.x, xout);
         h->cur.launches++;
         h->cur.bytes += 16 * n + 24 * (n - nc) * 4;
         LAP_CHECK_LAUNCH();
@@ -416,7 +433,7 @@ static void vcycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, c
     const double theta = L.cheb_theta, delta = L.cheb_delta, sigma = L.cheb_sigma;
     double *cur = L.x2, *alt = L.t;  // ping-pong pair, distinct from xout and r
     // pre-smoothing from x = 0
-    k_cheb_first<<<eg(n), 256, 0, s>>>(n, b, L.sd, 1.0 / theta, cur, L.dv);
+    launch_pdl(k_cheb_first, eg(n), 256, s, n, b, L.sd, 1.0 / theta, cur, L.dv);
     h->cur.launches++;
     h->cur.bytes += 32 * n;
     double rho_old = 1.0 / sigma;
@@ -437,12 +454,12 @@ static void vcycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, c
     a.x = cur;
     a.y = L.r;
     spmv_level(h, L, EPI_RESID, a, s);
-    k_restrict<<<grid_for(L.m * 8, 256, 148 * 8), 256, 0, s>>>(L.m, L.mem_ptr, L.members, L.r, C.b);
+    launch_pdl(k_restrict, grid_for(L.m * 8, 256, 148 * 8), 256, s, L.m, L.mem_ptr, L.members, L.r, C.b);
     h->cur.launches++;
     h->cur.bytes += 16 * n + 8 * L.m;
     vcycle_rec(h, l + 1, C.b, C.x, s);
     // prolongation x += P x_c (H4)
-    k_prolong<<<eg(n), 256, 0, s>>>(n, L.agg_s, C.x, cur);
+    launch_pdl(k_prolong, eg(n), 256, s, n, L.agg_s, C.x, cur);
     h->cur.launches++;
     h->cur.bytes += 20 * n + 8 * L.m;
     // post-smoothing from the corrected x
@@ -479,6 +496,7 @@ void vcycle_apply(lap_hierarchy *h, const double *r, double *z, cudaStream_t s) 
 __global__ void __launch_bounds__(256) k_pcg_xr(int64_t n, const double *__restrict__ p, const double *__restrict__ q,
                                                 double *__restrict__ x, double *__restrict__ r,
                                                 const double *__restrict__ sc, double *__restrict__ part) {
+    pdl_begin();
     __shared__ double sh[8];
     double alpha = sc[0] / sc[1];
     double acc = 0.0;
@@ -494,6 +512,7 @@ __global__ void __launch_bounds__(256) k_pcg_xr(int64_t n, const double *__restr
 // z -= mean(z) ; partial r.z
 __global__ void __launch_bounds__(256) k_pcg_proj_dot(int64_t n, double *__restrict__ z, const double *__restrict__ r,
                                                       const double *__restrict__ sc, double *__restrict__ part) {
+    pdl_begin();
     __shared__ double sh[8];
     double mean = sc[3] / (double)n;
     double acc = 0.0;
@@ -508,17 +527,38 @@ __global__ void __launch_bounds__(256) k_pcg_proj_dot(int64_t n, double *__restr
 // p = z + (rho_new/rho) p ; rho = rho_new  (last block updates the scalar after all read it: done by k_pcg_rho)
 __global__ void k_pcg_p(int64_t n, const double *__restrict__ z, double *__restrict__ p, const double *__restrict__ sc,
                         int first) {
+    pdl_begin();
     double beta = first ? 0.0 : sc[4] / sc[0];
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         p[i] = first ? z[i] : z[i] + beta * p[i];  // first: p is uninitialised (0*NaN must not leak)
 }
-__global__ void k_copy_scalar(double *sc, int dst, int src) { sc[dst] = sc[src]; }
+__global__ void k_copy_scalar(double *sc, int dst, int src) {
+    pdl_begin();
+    sc[dst] = sc[src];
+}
 __global__ void k_sub_mean(int64_t n, double *__restrict__ v, const double *__restrict__ sum) {
+    pdl_begin();
     double mean = *sum / (double)n;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         v[i] -= mean;
 }
 
+// iteration counter + stopping test of O-S8 on the device: k = 1 (first) or
+// k + 1; continue iff ||r||/||b|| > tol and k < max_iters.  With a graph
+// handle it drives the WHILE node of the resident PCG graph.
+// scal: 2 rr, 5 ||b||^2, 8 tol, 9 max_iters, 10 k
+__global__ void k_pcg_cond(double *sc, int first, cudaGraphConditionalHandle hd, int use_handle) {
+    pdl_begin();
+    double k = first ? 1.0 : sc[10] + 1.0;
+    sc[10] = k;
+    bool go = !(sqrt(sc[2]) / sqrt(sc[5]) <= sc[8]) && k < sc[9];
+    if (use_handle) cudaGraphSetConditional(hd, go ? 1u : 0u);
+}
+
+static void read_scalars(lap_hierarchy *h, int cnt, cudaStream_t s) {
+    LAP_CUDA(cudaMemcpyAsync(h->host_scal, h->scal, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s));
+    LAP_CUDA(cudaStreamSynchronize(s));
+}
 static double read_scalar(lap_hierarchy *h, const double *dptr, cudaStream_t s) {
     LAP_CUDA(cudaMemcpyAsync(h->host_scal, dptr, sizeof(double), cudaMemcpyDeviceToHost, s));
     LAP_CUDA(cudaStreamSynchronize(s));
@@ -526,78 +566,229 @@ static double read_scalar(lap_hierarchy *h, const double *dptr, cudaStream_t s) 
 }
 
 void launch_vcycle(lap_hierarchy *h, cudaStream_t s);
+void vcycle_apply(lap_hierarchy *h, const double *r, double *z, cudaStream_t s);
+
+// z = V(r) ; z -= mean z ; rho' = r.z ; p = z + (rho'/rho) p ; rho = rho'   (O-S8)
+static void pcg_precond_part(lap_hierarchy *h, bool first, bool inline_vcycle, cudaStream_t s) {
+    Level &L0 = h->lev[0];
+    int64_t n = L0.n;
+    double *sc = h->scal;
+    if (inline_vcycle) vcycle_apply(h, h->pr, h->pz, s);
+    else launch_vcycle(h, s);
+    dot(h, h->pz, nullptr, n, sc + 3, s);
+    launch_pdl(k_pcg_proj_dot, RED_BLOCKS, 256, s, n, h->pz, (const double *)h->pr, (const double *)sc, h->partials);
+    reduce_partials(h, h->partials, RED_BLOCKS, sc + (first ? 0 : 4), s);
+    launch_pdl(k_pcg_p, eg(n), 256, s, n, (const double *)h->pz, h->pp, (const double *)sc, first ? 1 : 0);
+    h->cur.launches += 2;
+    if (!first) {
+        launch_pdl(k_copy_scalar, 1, 1, s, sc, 0, 4);
+        h->cur.launches++;
+    }
+}
+// q = L p ; pq = p.q ; x += alpha p ; r -= alpha q ; rr = r.r   (H1 fused with H7)
+static void pcg_spmv_part(lap_hierarchy *h, cudaStream_t s) {
+    Level &L0 = h->lev[0];
+    int64_t n = L0.n;
+    double *sc = h->scal;
+    EpiArgs a;
+    a.x = h->pp;
+    a.y = h->pq;
+    a.partials = h->partials;
+    spmv_level(h, L0, EPI_SPMV_DOT, a, s);
+    reduce_partials(h, h->partials, spmv_partial_slots(L0), sc + 1, s);
+    launch_pdl(k_pcg_xr, RED_BLOCKS, 256, s, n, (const double *)h->pp, (const double *)h->pq, h->px, h->pr,
+               (const double *)sc, h->partials);
+    h->cur.launches++;
+    reduce_partials(h, h->partials, RED_BLOCKS, sc + 2, s);
+}
+
+// ---- the PCG loop as one resident CUDA graph (WHILE conditional node)
+//   start : r = b ; [precond, first] ; [spmv] ; cond(k=1) ; WHILE { [precond] ; [spmv] ; cond(k+1) }
+//   resume: WHILE(default 1) { same body }      (after a failed true-residual check, O-R30)
+struct PcgCounts {
+    Stats pro, body;
+};
+static void add_stats(Stats &a, const Stats &b, int64_t times) {
+    a.launches += b.launches * times;
+    a.edges += b.edges * times;
+    a.bytes += b.bytes * times;
+}
+
+static void capture_body(lap_hierarchy *h, cudaGraph_t body, cudaGraphConditionalHandle hd, cudaStream_t cs,
+                         Stats &cnt) {
+    LAP_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    Stats save = h->cur;
+    h->cur = Stats{};
+    pcg_precond_part(h, false, true, cs);
+    pcg_spmv_part(h, cs);
+    launch_pdl(k_pcg_cond, 1, 1, cs, h->scal, 0, hd, 1);
+    h->cur.launches++;
+    cnt = h->cur;
+    h->cur = save;
+    cudaGraph_t out;
+    LAP_CUDA(cudaStreamEndCapture(cs, &out));
+}
+
+static cudaGraphNode_t add_while(cudaGraph_t g, cudaGraphConditionalHandle hd, const cudaGraphNode_t *deps, size_t nd,
+                                 cudaGraph_t *body) {
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = hd;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    LAP_CUDA(cudaGraphAddNode(&node, g, deps, nd, &cp));
+    *body = cp.conditional.phGraph_out[0];
+    return node;
+}
+
+extern bool g_capturing_flag(bool v);
+
+void capture_pcg(lap_hierarchy *h) {
+    cudaStream_t cs;
+    LAP_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    PcgCounts *pc = new PcgCounts();
+    Stats save = h->cur;
+    g_capturing_flag(true);
+    try {
+        // ---- start graph
+        cudaGraph_t g;
+        LAP_CUDA(cudaGraphCreate(&g, 0));
+        cudaGraphConditionalHandle hd;
+        LAP_CUDA(cudaGraphConditionalHandleCreate(&hd, g, 0, cudaGraphCondAssignDefault));
+        LAP_CUDA(cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        h->cur = Stats{};
+        LAP_CUDA(cudaMemcpyAsync(h->pr, h->pb, sizeof(double) * h->lev[0].n, cudaMemcpyDeviceToDevice, cs));
+        pcg_precond_part(h, true, true, cs);
+        pcg_spmv_part(h, cs);
+        launch_pdl(k_pcg_cond, 1, 1, cs, h->scal, 1, hd, 1);
+        h->cur.launches++;
+        pc->pro = h->cur;
+        cudaStreamCaptureStatus st;
+        const cudaGraphNode_t *deps = nullptr;
+        size_t nd = 0;
+        LAP_CUDA(cudaStreamGetCaptureInfo(cs, &st, nullptr, nullptr, &deps, &nd));
+        cudaGraph_t body;
+        cudaGraphNode_t wn = add_while(g, hd, deps, nd, &body);
+        LAP_CUDA(cudaStreamUpdateCaptureDependencies(cs, &wn, 1, cudaStreamSetCaptureDependencies));
+        cudaGraph_t out;
+        LAP_CUDA(cudaStreamEndCapture(cs, &out));
+        capture_body(h, body, hd, cs, pc->body);
+        LAP_CUDA(cudaGraphInstantiate(&h->pcg_start, g, 0));
+        LAP_CUDA(cudaGraphDestroy(g));
+        // ---- resume graph
+        cudaGraph_t g2;
+        LAP_CUDA(cudaGraphCreate(&g2, 0));
+        cudaGraphConditionalHandle hd2;
+        LAP_CUDA(cudaGraphConditionalHandleCreate(&hd2, g2, 1, cudaGraphCondAssignDefault));
+        cudaGraph_t body2;
+        add_while(g2, hd2, nullptr, 0, &body2);
+        Stats tmp;
+        capture_body(h, body2, hd2, cs, tmp);
+        LAP_CUDA(cudaGraphInstantiate(&h->pcg_resume, g2, 0));
+        LAP_CUDA(cudaGraphDestroy(g2));
+    } catch (...) {
+        g_capturing_flag(false);
+        h->cur = save;
+        cudaStreamDestroy(cs);
+        delete pc;
+        throw;
+    }
+    g_capturing_flag(false);
+    h->cur = save;
+    LAP_CUDA(cudaStreamDestroy(cs));
+    h->pcg_counts = pc;
+}
+
+void free_pcg(lap_hierarchy *h) {
+    if (h->pcg_start) cudaGraphExecDestroy(h->pcg_start);
+    if (h->pcg_resume) cudaGraphExecDestroy(h->pcg_resume);
+    delete (PcgCounts *)h->pcg_counts;
+    h->pcg_start = h->pcg_resume = nullptr;
+    h->pcg_counts = nullptr;
+}
+
+// O-R30: confirm a recursive-residual stop with the true residual b - L x
+static bool true_residual_ok(lap_hierarchy *h, double bn, double tol, cudaStream_t s) {
+    EpiArgs t;
+    t.x = h->px;
+    t.b = h->pb;
+    t.y = h->pq;
+    spmv_level(h, h->lev[0], EPI_RESID, t, s);
+    dot(h, h->pq, h->pq, h->lev[0].n, h->scal + 6, s);
+    double tr = read_scalar(h, h->scal + 6, s);
+    return std::sqrt(tr) / bn <= tol;
+}
 
 // PCG on the internal numbering: h->pb holds b' (projected); result in h->px  (O-S8)
 void run_pcg(lap_hierarchy *h, double tol, int32_t *iters, double *relres, int *conv, cudaStream_t s) {
     Level &L0 = h->lev[0];
     int64_t n = L0.n;
     double *sc = h->scal;
-    unsigned g = RED_BLOCKS;
     *conv = 0;
     h->stats.vcycles = 0;
     dot(h, h->pb, h->pb, n, sc + 5, s);
-    double bn = std::sqrt(read_scalar(h, sc + 5, s));
     LAP_CUDA(cudaMemsetAsync(h->px, 0, sizeof(double) * n, s));
+    double bn = std::sqrt(read_scalar(h, sc + 5, s));
     if (bn == 0.0) {
         *iters = 0;
         *relres = 0.0;
         *conv = 1;
         return;
     }
-    LAP_CUDA(cudaMemcpyAsync(h->pr, h->pb, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
-    // z = V(r); project; rho = r.z; p = z
-    launch_vcycle(h, s);
-    h->stats.vcycles++;
-    dot(h, h->pz, nullptr, n, sc + 3, s);
-    k_pcg_proj_dot<<<g, 256, 0, s>>>(n, h->pz, h->pr, sc, h->partials);
-    reduce_partials(h, h->partials, g, sc + 0, s);
-    k_pcg_p<<<eg(n), 256, 0, s>>>(n, h->pz, h->pp, sc, 1);
-    h->cur.launches += 2;
-    int64_t slots = spmv_partial_slots(L0);
-    int k;
-    for (k = 1; k <= h->p.max_iters; k++) {
-        // q = L p ; pq = p.q   (H1 fused with H7)
-        EpiArgs a;
-        a.x = h->pp;
-        a.y = h->pq;
-        a.partials = h->partials;
-        spmv_level(h, L0, EPI_SPMV_DOT, a, s);
-        reduce_partials(h, h->partials, slots, sc + 1, s);
-        // x += alpha p ; r -= alpha q ; rr = r.r
-        k_pcg_xr<<<g, 256, 0, s>>>(n, h->pp, h->pq, h->px, h->pr, sc, h->partials);
-        h->cur.launches++;
-        reduce_partials(h, h->partials, g, sc + 2, s);
-        double rr = read_scalar(h, sc + 2, s);
-        if (std::sqrt(rr) / bn <= tol) {  // O-R30: confirm with the true residual
-            EpiArgs t;
-            t.x = h->px;
-            t.b = h->pb;
-            t.y = h->pq;
-            spmv_level(h, L0, EPI_RESID, t, s);
-            dot(h, h->pq, h->pq, n, sc + 6, s);
-            double tr = read_scalar(h, sc + 6, s);
-            if (std::sqrt(tr) / bn <= tol) {
-                *conv = 1;
-                break;
+    const int maxit = h->p.max_iters;
+    h->host_scal[1] = tol;
+    h->host_scal[2] = (double)maxit;
+    LAP_CUDA(cudaMemcpyAsync(sc + 8, h->host_scal + 1, 2 * sizeof(double), cudaMemcpyHostToDevice, s));
+    int k = 0;
+    if (h->pcg_start && maxit >= 1) {
+        PcgCounts *pc = (PcgCounts *)h->pcg_counts;
+        LAP_CUDA(cudaGraphLaunch(h->pcg_start, s));
+        add_stats(h->cur, pc->pro, 1);
+        int64_t k_prev = 1;
+        for (;;) {
+            read_scalars(h, 11, s);
+            k = (int)h->host_scal[10];
+            double rr = h->host_scal[2];
+            add_stats(h->cur, pc->body, k - k_prev);
+            h->stats.vcycles = k;
+            if (std::sqrt(rr) / bn <= tol) {
+                if (true_residual_ok(h, bn, tol, s)) {
+                    *conv = 1;
+                    break;
+                }
+                LAP_CUDA(cudaMemcpyAsync(h->pr, h->pq, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
             }
-            LAP_CUDA(cudaMemcpyAsync(h->pr, h->pq, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+            if (k >= maxit) break;
+            LAP_CUDA(cudaGraphLaunch(h->pcg_resume, s));
+            k_prev = k;
         }
-        // z = V(r) ; z -= mean z ; rho' = r.z ; p = z + (rho'/rho) p
-        launch_vcycle(h, s);
+    } else {
+        // eager path (use_graphs = 0): same kernels, host-driven loop
+        LAP_CUDA(cudaMemcpyAsync(h->pr, h->pb, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+        pcg_precond_part(h, true, false, s);
         h->stats.vcycles++;
-        dot(h, h->pz, nullptr, n, sc + 3, s);
-        k_pcg_proj_dot<<<g, 256, 0, s>>>(n, h->pz, h->pr, sc, h->partials);
-        reduce_partials(h, h->partials, g, sc + 4, s);
-        k_pcg_p<<<eg(n), 256, 0, s>>>(n, h->pz, h->pp, sc, 0);
-        k_copy_scalar<<<1, 1, 0, s>>>(sc, 0, 4);
-        h->cur.launches += 3;
-        LAP_CHECK_LAUNCH();
+        for (k = 1; k <= maxit; k++) {
+            pcg_spmv_part(h, s);
+            double rr = read_scalar(h, sc + 2, s);
+            if (std::sqrt(rr) / bn <= tol) {
+                if (true_residual_ok(h, bn, tol, s)) {
+                    *conv = 1;
+                    break;
+                }
+                LAP_CUDA(cudaMemcpyAsync(h->pr, h->pq, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+            }
+            if (k == maxit) break;
+            pcg_precond_part(h, false, false, s);
+            h->stats.vcycles++;
+            LAP_CHECK_LAUNCH();
+        }
+        if (k > maxit) k = maxit;
     }
-    if (!*conv) k = h->p.max_iters;
     *iters = k;
     // x -= mean(x) ; true relative residual
     dot(h, h->px, nullptr, n, sc + 3, s);
-    k_sub_mean<<<eg(n), 256, 0, s>>>(n, h->px, sc + 3);
+    launch_pdl(k_sub_mean, eg(n), 256, s, n, h->px, (const double *)(sc + 3));
     h->cur.launches++;
     EpiArgs t;
     t.x = h->px;

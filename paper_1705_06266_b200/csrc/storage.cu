@@ -60,7 +60,13 @@ __global__ void k_class_key(int64_t n, const int64_t *rp, const uint64_t *key, u
         if (by_degree && c == 0) k |= ((uint64_t)(255 - dg)) << 54;
         skey[i] = k;
         ids[i] = (int32_t)i;
-        if (cnt) atomicAdd(&cnt[c], 1ULL);
+        if (cnt) {  // warp-aggregated class counts (one atomic per class per warp, not per row)
+            const unsigned am = __activemask();
+            for (int q = 0; q < NCLASS; q++) {
+                unsigned m = __ballot_sync(am, c == q);
+                if (m && (threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(&cnt[q], (unsigned long long)__popc(m));
+            }
+        }
     }
 }
 // SELL-32 slice widths (max degree of the slice's rows) and padding statistic
@@ -126,10 +132,24 @@ __global__ void k_storage_fill(int64_t n, const int32_t *sid, const int32_t *spo
         }
     }
 }
-__global__ void k_hub_counts(int64_t nhub, int64_t row0, const int64_t *srp, int64_t *cnt) {
-    GRID_STRIDE(h, nhub) {
-        int64_t i = row0 + h;
-        cnt[h] = (srp[i + 1] - srp[i] + HUB_CHUNK - 1) / HUB_CHUNK;
+// LCHUNK work items over rows [row0, row0+nrows) of a CSR whose length
+// exceeds minlen (the others get no chunk); slot = row - row0 for rows of
+// several chunks (their arrival counter), -1 for one-chunk rows.
+__global__ void k_chunk_counts(int64_t nrows, int64_t row0, const int64_t *rp, int64_t minlen, int64_t *cnt) {
+    GRID_STRIDE(h, nrows) {
+        int64_t i = row0 + h, dg = rp[i + 1] - rp[i];
+        cnt[h] = dg > minlen ? (dg + LCHUNK - 1) / LCHUNK : 0;
+    }
+}
+__global__ void k_chunk_fill(int64_t nrows, int64_t row0, const int64_t *first, int32_t *crow, int32_t *cidx,
+                             int32_t *cslot) {
+    GRID_STRIDE(h, nrows) {
+        int64_t f = first[h], nch = first[h + 1] - f;
+        for (int64_t j = 0; j < nch; j++) {
+            crow[f + j] = (int32_t)(row0 + h);
+            cidx[f + j] = (int32_t)j;
+            cslot[f + j] = nch > 1 ? (int32_t)h : -1;
+        }
     }
 }
 
@@ -140,6 +160,29 @@ static void scan_excl(const T *in, T *out, int64_t n, cudaStream_t s) {
     DBuf<char> tmp((int64_t)bytes, s);
     LAP_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, in, out, n, s));
     g_kl += 2;
+}
+
+static int64_t build_chunks(const int64_t *rp, int64_t row0, int64_t nrows, int64_t minlen, int32_t **crow,
+                            int32_t **cidx, int32_t **cslot, double **cpart, int32_t **ccnt, cudaStream_t s) {
+    if (nrows <= 0) return 0;
+    DBuf<int64_t> cc(nrows + 1, s), first(nrows + 1, s);
+    LAP_CUDA(cudaMemsetAsync(cc.p, 0, sizeof(int64_t) * (nrows + 1), s));
+    k_chunk_counts<<<grid_for(nrows, 256, 148 * 8), 256, 0, s>>>(nrows, row0, rp, minlen, cc.p);
+    g_kl++;
+    scan_excl(cc.p, first.p, nrows + 1, s);
+    int64_t nch = d2h(first.p + nrows, s);
+    *crow = (int32_t *)dalloc(sizeof(int32_t) * (nch + 1), s);
+    *cidx = (int32_t *)dalloc(sizeof(int32_t) * (nch + 1), s);
+    *cslot = (int32_t *)dalloc(sizeof(int32_t) * (nch + 1), s);
+    *cpart = (double *)dalloc(sizeof(double) * (nch + 1), s);
+    *ccnt = (int32_t *)dalloc(sizeof(int32_t) * nrows, s);
+    LAP_CUDA(cudaMemsetAsync(*ccnt, 0, sizeof(int32_t) * nrows, s));
+    if (nch > 0) {
+        k_chunk_fill<<<grid_for(nrows, 256, 148 * 8), 256, 0, s>>>(nrows, row0, first.p, *crow, *cidx, *cslot);
+        g_kl++;
+    }
+    LAP_CHECK_LAUNCH();
+    return nch;
 }
 
 // LAP_DEBUG_SYNC=1: host-side consistency check of a level's storage layout
@@ -282,18 +325,9 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
         g_kl++;
     }
     if (debug_sync()) validate_storage(L, s);
-    // hub chunks
-    int64_t nhub = n - L.c_end[2];
-    if (nhub > 0) {
-        DBuf<int64_t> cc(nhub + 1, s);
-        LAP_CUDA(cudaMemsetAsync(cc.p, 0, sizeof(int64_t) * (nhub + 1), s));
-        k_hub_counts<<<grid_for(nhub, 256), 256, 0, s>>>(nhub, L.c_end[2], L.srp, cc.p);
-        g_kl++;
-        L.chunk_first = (int64_t *)dalloc(sizeof(int64_t) * (nhub + 1), s);
-        scan_excl(cc.p, L.chunk_first, nhub + 1, s);
-        L.nchunks = d2h(L.chunk_first + nhub, s);
-        L.chunk_part = (double *)dalloc(sizeof(double) * (L.nchunks + 1), s);
-    }
+    // long rows: LCHUNK-entry warp work items (solve.cu k_spmv)
+    L.nchunks = build_chunks(L.srp, L.c_end[0], n - L.c_end[0], SHORT_MAX, &L.chunk_row, &L.chunk_idx, &L.chunk_slot,
+                             &L.chunk_part, &L.chunk_cnt, s);
     LAP_CHECK_LAUNCH();
 }
 
@@ -400,6 +434,8 @@ void build_transfers(lap_hierarchy *h, cudaStream_t s) {
             k_ct_fill_s<<<grid_for(nc, 256, 148 * 8), 256, 0, s>>>(nc, C.sid, L.ct_ptr, L.ct_f, L.ct_coef, L.spos,
                                                                     L.ct_ptr_s, L.ct_f_s, L.ct_coef_s);
             g_kl += 5;
+            L.ct_nchunks = build_chunks(L.ct_ptr_s, 0, nc, ELIM_SHORT, &L.ct_crow, &L.ct_cidx, &L.ct_cslot, &L.ct_cpart,
+                                        &L.ct_ccnt, s);
         } else {
             L.pinv_s = (double *)dalloc(sizeof(double) * (size_t)(n * n > 0 ? n * n : 1), s);
             if (n * n > 0) k_pinv_s<<<grid_for(n * n, 256, 148 * 8), 256, 0, s>>>(n, L.sid, L.pinv, L.pinv_s);

@@ -50,7 +50,7 @@ class lap_stats(ctypes.Structure):
 EXPORTS = [
     "lap_params_default", "lap_last_error", "lap_version", "lap_setup", "lap_solve", "lap_free",
     "lap_num_levels", "lap_level_info", "lap_level_export", "lap_level_strength", "lap_coarse_pinv",
-    "lap_perm", "lap_spmv", "lap_vcycle", "lap_get_stats", "lap_bench_smoother",
+    "lap_perm", "lap_spmv", "lap_vcycle", "lap_get_stats", "lap_bench_op",
 ]
 
 
@@ -77,7 +77,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "lap_spmv": (ctypes.c_int, [P, i32, P, P, P]),
         "lap_vcycle": (ctypes.c_int, [P, P, P, P]),
         "lap_get_stats": (ctypes.c_int, [P, ctypes.POINTER(lap_stats)]),
-        "lap_bench_smoother": (ctypes.c_int, [P, i32, P, pdbl, pdbl, pi32]),
+        "lap_bench_op": (ctypes.c_int, [P, i32, i32, i32, P, P, pdbl, pi64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -229,8 +229,18 @@ class Hierarchy:
         _check(lib().lap_get_stats(self._h, ctypes.byref(s)))
         return {k: getattr(s, k) for k, _ in s._fields_}
 
-    def bench_smoother(self, reps: int = 50, stream=None):
-        ms, by, lv = ctypes.c_double(), ctypes.c_double(), ctypes.c_int32()
-        _check(lib().lap_bench_smoother(self._h, reps, _stream(stream), ctypes.byref(ms), ctypes.byref(by),
-                                        ctypes.byref(lv)))
-        return ms.value, by.value, lv.value
+    def bench_op(self, which: int, level: int = 0, reps: int = 50, stream=None):
+        """CUDA-event time of `reps` launches of an operation (lap_bench_op):
+        which 0 = SpMV on `level`, 1 = fused Chebyshev step, 2 = V-cycle.
+        Returns (ms per launch array, algorithmic bytes, edges) per launch."""
+        ms = np.zeros(reps)
+        by, ed = ctypes.c_double(), ctypes.c_int64()
+        _check(lib().lap_bench_op(self._h, which, level, reps, _stream(stream), _ptr(ms), ctypes.byref(by),
+                                  ctypes.byref(ed)))
+        return ms, by.value, ed.value
+
+    def first_agg_level(self) -> int:
+        for l in range(self.nlev):
+            if self.level_info(l)[0] == KIND_AGG:
+                return l
+        return -1
