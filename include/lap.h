@@ -148,8 +148,11 @@ typedef struct {
 lap_status lap_get_stats(const lap_hierarchy *h, lap_stats *s);
 
 /* Time `reps` back-to-back launches of one solve-phase operation on
- * `cuda_stream` with CUDA events (an event between consecutive launches);
- * ms[reps] (host) receives each launch's duration in milliseconds.
+ * `cuda_stream` with CUDA events; ms[reps] (host) receives per-launch times in
+ * milliseconds.  V-cycles (which = 2) are timed one graph launch each; single
+ * kernels (which = 0, 1) are captured `reps` at a time into one CUDA graph (as
+ * the solve runs them) and every ms[i] is the mean per launch of a timed
+ * graph launch.
  *   which = 0: y = L_l x on level l (H1)
  *   which = 1: one fused Chebyshev/Jacobi step on aggregation level l (H2)
  *   which = 2: one V-cycle z = V(0, r) (H16, Alg. 1; l ignored; graph launch)

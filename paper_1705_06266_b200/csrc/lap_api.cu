@@ -140,7 +140,7 @@ void finalize_solve_structures(lap_hierarchy *h, cudaStream_t s) {
 static void free_level(Level &L, cudaStream_t s) {
     void *ps[] = {L.row_ptr, L.col, L.w, L.d, L.agg, L.S, L.fmap, L.cid, L.fid, L.ct_ptr, L.ct_f, L.ct_coef,
                   L.pinv, L.sid, L.spos, L.srp, L.scol, L.sw, L.sd, L.slice_ptr, L.ell_col, L.ell_w, L.chunk_row, L.chunk_idx, L.chunk_slot, L.chunk_cnt,
-                  L.chunk_part,
+                  L.chunk_part, L.ell_col16, L.scol16,
                   L.agg_s, L.mem_ptr, L.members, L.cid_s, L.flist, L.ct_ptr_s, L.ct_f_s, L.ct_coef_s, L.fmap_s,
                   L.ct_crow, L.ct_cidx, L.ct_cslot, L.ct_ccnt, L.ct_cpart,
                   L.pinv_s, L.b, L.x, L.x2, L.t, L.r, L.dv};
@@ -560,16 +560,53 @@ lap_status lap_bench_op(lap_hierarchy *h, int32_t which, int32_t l, int32_t reps
         LAP_CUDA(cudaMemsetAsync(h->pr, 0, 8 * h->lev[0].n, s));
     }
     for (int i = 0; i < 3; i++) run(i == 0);  // warm-up
-    for (int i = 0; i < reps; i++) {
-        LAP_CUDA(cudaEventRecord(ev[i], s));
-        run(false);
-    }
-    LAP_CUDA(cudaEventRecord(ev[reps], s));
-    LAP_CUDA(cudaEventSynchronize(ev[reps]));
-    for (int i = 0; i < reps; i++) {
-        float t = 0;
-        cudaEventElapsedTime(&t, ev[i], ev[i + 1]);
-        if (ms) ms[i] = t;
+    if (which == 2) {
+        // one graph launch per V-cycle, an event between consecutive launches
+        for (int i = 0; i < reps; i++) {
+            LAP_CUDA(cudaEventRecord(ev[i], s));
+            run(false);
+        }
+        LAP_CUDA(cudaEventRecord(ev[reps], s));
+        LAP_CUDA(cudaEventSynchronize(ev[reps]));
+        for (int i = 0; i < reps; i++) {
+            float t = 0;
+            cudaEventElapsedTime(&t, ev[i], ev[i + 1]);
+            if (ms) ms[i] = t;
+        }
+    } else {
+        // single kernels are too short to time one by one from the host (the
+        // host-side launch rate would be measured): capture the `reps`
+        // launches into one graph, as the solve runs them, and time 5 graph
+        // launches; every entry of ms[] is the mean per launch of one of them
+        cudaStream_t cs;
+        LAP_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        cudaGraph_t g;
+        lap::g_capturing_flag(true);
+        LAP_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        cudaStream_t keep = s;
+        s = cs;
+        for (int i = 0; i < reps; i++) run(false);
+        s = keep;
+        LAP_CUDA(cudaStreamEndCapture(cs, &g));
+        lap::g_capturing_flag(false);
+        cudaGraphExec_t ge;
+        LAP_CUDA(cudaGraphInstantiate(&ge, g, 0));
+        LAP_CUDA(cudaGraphDestroy(g));
+        LAP_CUDA(cudaStreamDestroy(cs));
+        LAP_CUDA(cudaGraphLaunch(ge, s));  // warm
+        int nt = reps < 5 ? reps : 5;
+        for (int i = 0; i < nt; i++) {
+            LAP_CUDA(cudaEventRecord(ev[i], s));
+            LAP_CUDA(cudaGraphLaunch(ge, s));
+        }
+        LAP_CUDA(cudaEventRecord(ev[nt], s));
+        LAP_CUDA(cudaEventSynchronize(ev[nt]));
+        for (int i = 0; i < reps; i++) {
+            float t = 0;
+            cudaEventElapsedTime(&t, ev[i % nt], ev[i % nt + 1]);
+            if (ms) ms[i] = t / reps;
+        }
+        cudaGraphExecDestroy(ge);
     }
     for (auto &e : ev) cudaEventDestroy(e);
     h->cur = save;

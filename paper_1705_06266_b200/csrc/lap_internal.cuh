@@ -94,6 +94,8 @@ constexpr int64_t SHORT_MAX = 64;
 constexpr int64_t HUB_CHUNK = 16384;  // class 2/3 boundary (storage grouping only)
 constexpr int64_t LCHUNK = 1024;      // long-row chunk (entries per warp work item)
 constexpr int64_t ELIM_SHORT = 32;    // elimination restriction: longer coarse lists are chunked
+constexpr int64_t SMEM_X_MAX = 26624;   // levels with n <= this (208 KB of x) ...
+constexpr int64_t SMEM_X_MIN_DEG = 256; // ... and average degree >= this gather x from shared memory
 
 struct Level {
     int kind = KIND_COARSEST;
@@ -131,6 +133,9 @@ struct Level {
     int32_t *ell_col = nullptr;     // padded entries: column (own row for padding)
     double *ell_w = nullptr;        // padded entries: weight (0 for padding)
     bool sell_sorted = false;       // short rows degree-sorted
+    bool smem_x = false;            // small dense-ish level: k_spmv_smem (x in shared memory, 16-bit columns)
+    uint16_t *ell_col16 = nullptr;  // smem_x: 16-bit copies of ell_col / scol
+    uint16_t *scol16 = nullptr;
     int64_t nchunks = 0;            // LCHUNK chunks over the long rows [c_end[0], n)
     int32_t *chunk_row = nullptr;   // chunk -> storage row
     int32_t *chunk_idx = nullptr;   // chunk -> index within its row
@@ -251,6 +256,21 @@ inline void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cu
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(block);
     cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    LAP_CUDA(cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...));
+}
+template <typename... KArgs, typename... Args>
+inline void launch_pdl_smem(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
+                            Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -89,10 +89,10 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
 // coarse levels are load balanced, and no class runs alone on a partly idle
 // GPU.  No fp64 atomics: per-chunk sums and the in-order combine are fixed, so
 // results are bitwise reproducible run to run.
-template <int EPI>
+template <int EPI, class CT>
 __device__ __forceinline__ void sell_slice(int64_t sl, int lane, int64_t nrows, const int64_t *__restrict__ sp,
-                                           const int32_t *__restrict__ ec, const double *__restrict__ ew, const Csr &A,
-                                           const EpiArgs &a, double &dacc) {
+                                           const CT *__restrict__ ec, const double *__restrict__ ew, const Csr &A,
+                                           const EpiArgs &a, const double *__restrict__ xg, double &dacc) {
     const int64_t i = sl * 32 + lane;
     const int64_t beg = sp[sl], end = sp[sl + 1];
     double xi = 0.0, di = 0.0, bi = 0.0, dvi = 0.0;
@@ -109,7 +109,7 @@ __device__ __forceinline__ void sell_slice(int64_t sl, int lane, int64_t nrows, 
     const int width = (int)((end - beg) >> 5);
     double acc0 = 0.0, acc1 = 0.0;
     for (int q = 0; q < width; q += 8) {
-        int c[8];
+        int c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         double wv[8];
 #pragma unroll
         for (int u = 0; u < 8; u++) {
@@ -120,8 +120,8 @@ __device__ __forceinline__ void sell_slice(int64_t sl, int lane, int64_t nrows, 
         }
 #pragma unroll
         for (int u = 0; u < 8; u += 2) {
-            if (q + u < width) acc0 += wv[u] * a.x[c[u]];
-            if (q + u + 1 < width) acc1 += wv[u + 1] * a.x[c[u + 1]];
+            if (q + u < width) acc0 += wv[u] * xg[c[u]];
+            if (q + u + 1 < width) acc1 += wv[u + 1] * xg[c[u + 1]];
         }
     }
     if (live) {
@@ -159,8 +159,9 @@ struct LongRows {
 // lane) iff this warp must finish the row: either the row is a single chunk,
 // or this warp is the last of the row's chunks to arrive, in which case the
 // row's partials are summed in chunk order.  *sum is valid on lane 0.
+template <class CT>
 __device__ __forceinline__ bool chunk_reduce(int64_t c, int lane, const int64_t *__restrict__ rp,
-                                             const int32_t *__restrict__ col, const double *__restrict__ w,
+                                             const CT *__restrict__ col, const double *__restrict__ w,
                                              const double *__restrict__ x, const LongRows &R, int64_t &row,
                                              double &sum) {
     const int64_t i = R.crow[c];
@@ -207,12 +208,13 @@ __device__ __forceinline__ bool chunk_reduce(int64_t c, int lane, const int64_t 
     return true;
 }
 
-template <int EPI>
-__device__ __forceinline__ void long_chunk(int64_t c, int lane, const Csr &A, const LongRows &R, const EpiArgs &a,
+template <int EPI, class CT>
+__device__ __forceinline__ void long_chunk(int64_t c, int lane, const Csr &A, const CT *__restrict__ col,
+                                           const LongRows &R, const EpiArgs &a, const double *__restrict__ xg,
                                            double &dacc) {
     int64_t i;
     double ax;
-    if (chunk_reduce(c, lane, A.rp, A.col, A.w, a.x, R, i, ax) && lane == 0) apply_epi<EPI>(i, ax, A, a, dacc);
+    if (chunk_reduce(c, lane, A.rp, col, A.w, xg, R, i, ax) && lane == 0) apply_epi<EPI>(i, ax, A, a, dacc);
 }
 
 template <int EPI>
@@ -227,8 +229,8 @@ __global__ void __launch_bounds__(256, 4) k_spmv(int64_t nslices, int64_t nshort
     const int64_t nitems = nslices + R.nchunks;
     double dacc = 0.0;
     for (int64_t t = warp; t < nitems; t += nwarps) {
-        if (t < nslices) sell_slice<EPI>(t, lane, nshort, sp, ec, ew, A, a, dacc);
-        else long_chunk<EPI>(t - nslices, lane, A, R, a, dacc);
+        if (t < nslices) sell_slice<EPI>(t, lane, nshort, sp, ec, ew, A, a, a.x, dacc);
+        else long_chunk<EPI>(t - nslices, lane, A, A.col, R, a, a.x, dacc);
     }
     if (EPI == E_DOT) {
         double r = block_sum(dacc, sh);
@@ -236,10 +238,54 @@ __global__ void __launch_bounds__(256, 4) k_spmv(int64_t nslices, int64_t nshort
     }
 }
 
+// Small, dense-ish levels (n <= SMEM_X_MAX, average degree >= SMEM_X_MIN_DEG:
+// the levels under the first aggregation of power-law graphs, ~10^4 rows of
+// 10^3-10^4 entries).  Random gathers from a 100 KB x are bound by the L1
+// tag rate, not by bandwidth, so each CTA (one per SM, 1024 threads) first
+// stages the whole x in shared memory and gathers from there; column indices
+// are 16-bit (n < 65536), 10 instead of 12 bytes per nonzero.
+template <int EPI>
+__global__ void __launch_bounds__(1024, 1) k_spmv_smem(int64_t n, int64_t nslices, int64_t nshort,
+                                                       const int64_t *__restrict__ sp, const uint16_t *__restrict__ ec,
+                                                       const double *__restrict__ ew, Csr A,
+                                                       const uint16_t *__restrict__ col16, LongRows R, EpiArgs a,
+                                                       double *__restrict__ partials) {
+    extern __shared__ double xs[];
+    __shared__ double sh[32];
+    pdl_begin();
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) xs[i] = a.x[i];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nitems = nslices + R.nchunks;
+    double dacc = 0.0;
+    for (int64_t t = warp; t < nitems; t += nwarps) {
+        if (t < nslices) sell_slice<EPI>(t, lane, nshort, sp, ec, ew, A, a, xs, dacc);
+        else long_chunk<EPI>(t - nslices, lane, A, col16, R, a, xs, dacc);
+    }
+    if (EPI == E_DOT) {
+        double r = block_sum(dacc, sh);
+        if (threadIdx.x == 0) partials[blockIdx.x] = r;
+    }
+}
+
+static int num_sms() {
+    static int v = 0;
+    if (!v) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        if (v <= 0) v = 148;
+    }
+    return v;
+}
+
 // fixed launch geometry per level (deterministic partial slots for E_DOT)
 static unsigned spmv_grid(const Level &L) {
+    if (L.smem_x) return (unsigned)num_sms();
     int64_t items = L.nslices + L.nchunks;
-    return grid_for(items * 32, 256, 148 * 4);  // one resident wave (4 CTAs of 256 per SM at 64 regs)
+    return grid_for(items * 32, 256, (int64_t)num_sms() * 4);  // one resident wave (4 CTAs of 256 per SM at 64 regs)
 }
 
 int64_t spmv_partial_slots(const Level &L) { return spmv_grid(L); }
@@ -248,8 +294,20 @@ template <int EPI>
 static void spmv_dispatch(lap_hierarchy *h, const Level &L, const EpiArgs &a, cudaStream_t s) {
     Csr A{L.srp, L.scol, L.sw, L.sd};
     LongRows R{L.nchunks, L.chunk_row, L.chunk_idx, L.chunk_slot, L.chunk_part, L.chunk_cnt};
-    launch_pdl(k_spmv<EPI>, spmv_grid(L), 256, s, L.nslices, L.c_end[0], (const int64_t *)L.slice_ptr,
-               (const int32_t *)L.ell_col, (const double *)L.ell_w, A, R, a, a.partials);
+    if (L.smem_x) {
+        static bool attr_set = false;
+        if (!attr_set) {
+            LAP_CUDA(cudaFuncSetAttribute(k_spmv_smem<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(8 * SMEM_X_MAX)));
+            attr_set = true;
+        }
+        launch_pdl_smem(k_spmv_smem<EPI>, spmv_grid(L), 1024, (size_t)(8 * L.n), s, L.n, L.nslices, L.c_end[0],
+                        (const int64_t *)L.slice_ptr, (const uint16_t *)L.ell_col16, (const double *)L.ell_w, A,
+                        (const uint16_t *)L.scol16, R, a, a.partials);
+    } else {
+        launch_pdl(k_spmv<EPI>, spmv_grid(L), 256, s, L.nslices, L.c_end[0], (const int64_t *)L.slice_ptr,
+                   (const int32_t *)L.ell_col, (const double *)L.ell_w, A, R, a, a.partials);
+    }
     h->cur.launches++;
     LAP_CHECK_LAUNCH();
 }

@@ -132,6 +132,9 @@ __global__ void k_storage_fill(int64_t n, const int32_t *sid, const int32_t *spo
         }
     }
 }
+__global__ void k_to_u16(int64_t m, const int32_t *in, uint16_t *out) {
+    GRID_STRIDE(i, m) out[i] = (uint16_t)in[i];
+}
 // LCHUNK work items over rows [row0, row0+nrows) of a CSR whose length
 // exceeds minlen (the others get no chunk); slot = row - row0 for rows of
 // several chunks (their arrival counter), -1 for one-chunk rows.
@@ -325,6 +328,17 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
         g_kl++;
     }
     if (debug_sync()) validate_storage(L, s);
+    // small dense-ish level: 16-bit column copies for the shared-memory-x SpMV
+    if (n <= SMEM_X_MAX && L.nnz >= SMEM_X_MIN_DEG * n && L.nnz > 0) {
+        L.smem_x = true;
+        int64_t tot = L.nslices ? d2h(L.slice_ptr + L.nslices, s) : 0;
+        L.ell_col16 = (uint16_t *)dalloc(sizeof(uint16_t) * (tot + 1), s);
+        L.scol16 = (uint16_t *)dalloc(sizeof(uint16_t) * (L.nnz + 1), s);
+        if (tot) k_to_u16<<<grid_for(tot, 256, 148 * 8), 256, 0, s>>>(tot, L.ell_col, L.ell_col16);
+        k_to_u16<<<grid_for(L.nnz, 256, 148 * 8), 256, 0, s>>>(L.nnz, L.scol, L.scol16);
+        g_kl += 2;
+        LAP_CHECK_LAUNCH();
+    }
     // long rows: LCHUNK-entry warp work items (solve.cu k_spmv)
     L.nchunks = build_chunks(L.srp, L.c_end[0], n - L.c_end[0], SHORT_MAX, &L.chunk_row, &L.chunk_idx, &L.chunk_slot,
                              &L.chunk_part, &L.chunk_cnt, s);
