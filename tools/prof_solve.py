@@ -8,7 +8,14 @@ import lapgen, paper_1705_06266_b200 as P
 k = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 g = lapgen.config(k)
 b = torch.from_numpy(lapgen.rhs(g.n)).cuda()
+h0 = P.Hierarchy(g, use_graphs=int(os.environ.get("USE_GRAPHS", "0")))  # warm (pool, module load)
+h0.close()
+torch.cuda.synchronize()
+torch.cuda.nvtx.range_push("setup")
 h = P.Hierarchy(g, use_graphs=int(os.environ.get("USE_GRAPHS", "0")))
+torch.cuda.synchronize()
+torch.cuda.nvtx.range_pop()
+print("setup_ms", h.stats()["setup_ms"])
 for l in range(h.nlev):
     print("level", l, h.level_info(l), flush=True)
 h.solve(b)
