@@ -90,9 +90,12 @@ typedef struct {
     int32_t affinity_power;   /* 1 = LAMG affinity (O-R5); 2 = literal P:564   */
     int32_t keep_strength;    /* 1: retain S per aggregation level (tests)     */
     int32_t use_graphs;       /* 1: capture the V-cycle as a CUDA graph        */
+    int64_t replicate_nnz;    /* multi-GPU: levels with nnz >= this are sharded,
+                                 the rest replicated; 0 = nnz(L_0) / (32 P)    */
 } lap_params;
 
 typedef struct lap_hierarchy lap_hierarchy;
+typedef struct lap_comm lap_comm;
 
 void lap_params_default(lap_params *p);
 const char *lap_last_error(void);
@@ -135,6 +138,38 @@ lap_status lap_perm(const lap_hierarchy *h, int64_t *perm);
 lap_status lap_spmv(const lap_hierarchy *h, int32_t l, const double *x, double *y, void *cuda_stream);
 /* z = V(0, r): one V-cycle on the internal (permuted) level-0 numbering (O-S7). */
 lap_status lap_vcycle(lap_hierarchy *h, const double *r, double *z, void *cuda_stream);
+
+/* ---- multi-GPU: 2D-sharded solve ------------------------------
+ * The fine levels (nnz >= params.replicate_nnz) are distributed as a 2D edge
+ * partition over a pr x pc process grid: rank r sits at grid
+ * position (r / pc, r % pc) and owns one piece of every sharded level's rows
+ * (block-cyclic over the storage order); per SpMV the column communicator
+ * allgathers x and the row communicator reduce-scatters A x (NCCL).  The
+ * coarse levels are replicated on every rank.  Setup is the single-
+ * GPU setup run identically on each rank (deterministic, O-R23).
+ * lap_solve on such a hierarchy takes the FULL b and returns the FULL x on
+ * every rank; all ranks must call it together (collectives inside). */
+/* 128-byte ncclUniqueId for rank 0 to broadcast (e.g. via torch.distributed). */
+lap_status lap_nccl_unique_id(uint8_t id[128]);
+/* One rank per process/GPU; grid_rows * grid_cols == nranks <= 16.  Creates the
+ * NCCL world communicator and its row / column splits.  LAP_ENCCL on failure. */
+lap_status lap_comm_create(const uint8_t nccl_id[128], int32_t rank, int32_t nranks, int32_t grid_rows,
+                           int32_t grid_cols, lap_comm **out);
+/* The whole pr x pc grid inside this process on the current device: every
+ * rank's shard is held here and the collectives are device copies and
+ * fixed-order sums (used to validate the sharded data path on one GPU). */
+lap_status lap_comm_create_virtual(int32_t grid_rows, int32_t grid_cols, lap_comm **out);
+lap_status lap_comm_info(const lap_comm *c, int32_t *rank, int32_t *nranks, int32_t *grid_rows, int32_t *grid_cols,
+                         int32_t *is_virtual);
+void lap_comm_free(lap_comm *c);  /* NULL-safe; after every hierarchy using it is freed */
+/* lap_setup + sharding over the communicator's grid (the comm must outlive h). */
+lap_status lap_setup_dist(const lap_graph *g, const lap_params *p, lap_comm *c, void *cuda_stream,
+                          lap_hierarchy **out);
+/* Host-only (no GPU needed): the piece map of a sharded level with n rows over
+ * nranks pieces: dist[t] = piece * piece_size + slot of storage row rows[t]
+ * (block-cyclic in blocks of 256 rows); *piece_size = padded piece length. */
+lap_status lap_dist_index(int64_t n, int32_t nranks, int64_t m, const int64_t *rows, int64_t *dist,
+                          int64_t *piece_size);
 
 /* ---- counters for the benchmark ----------------------------------------- */
 typedef struct {

@@ -21,7 +21,8 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relax
 UNITS = {"setup.cu": ["-fmad=false", "-prec-div=true", "-prec-sqrt=true"],
          "solve.cu": [],
          "storage.cu": [],
-         "lap_api.cu": []}
+         "lap_api.cu": [],
+         "dist.cu": []}
 
 
 def _sources():
@@ -46,7 +47,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         subprocess.check_call(cmd)
         objs.append(obj)
     tmp = SO + f".tmp{os.getpid()}"
-    subprocess.check_call([nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"])
+    subprocess.check_call([nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-lnccl"])
     os.replace(tmp, SO)
     return SO
 

@@ -261,6 +261,7 @@ void lap_params_default(lap_params *p) {
     p->affinity_power = 1;
     p->keep_strength = 0;
     p->use_graphs = 1;
+    p->replicate_nnz = 0;
 }
 
 const char *lap_last_error(void) { return lap::g_err.c_str(); }
@@ -327,11 +328,40 @@ lap_status lap_setup(const lap_graph *g, const lap_params *pp, void *stream, lap
     return h->status;
 }
 
+lap_status lap_setup_dist(const lap_graph *g, const lap_params *pp, lap_comm *c, void *stream, lap_hierarchy **out) {
+    if (out) *out = nullptr;
+    if (!c) {
+        lap::set_error("lap_setup_dist: NULL communicator");
+        return LAP_EINVAL;
+    }
+    lap_params p;
+    if (pp) p = *pp;
+    else lap_params_default(&p);
+    p.use_graphs = 0;  // the sharded solve is host-sequenced (collectives between kernels)
+    lap_hierarchy *h = nullptr;
+    lap_status st = lap_setup(g, &p, stream, &h);
+    if (st != LAP_OK && st != LAP_ESTALL) return st;
+    try {
+        if (h->lev[0].kind != lap::KIND_COARSEST) lap::build_dist(h, c, (cudaStream_t)stream);
+    } catch (const lap::Error &e) {
+        lap::set_error(e.msg);
+        lap_free(h);
+        return e.code;
+    } catch (...) {
+        lap::set_error("lap_setup_dist: unexpected exception");
+        lap_free(h);
+        return LAP_ECUDA;
+    }
+    *out = h;
+    return st;
+}
+
 void lap_free(lap_hierarchy *h) {
     if (!h) return;
     cudaStream_t s = nullptr;
     cudaDeviceSynchronize();
     if (h->vgraph) cudaGraphExecDestroy(h->vgraph);
+    lap::free_dist(h);
     lap::free_pcg(h);
     for (auto &L : h->lev) lap::free_level(L, s);
     void *ps[] = {h->perm, h->cmap, h->pb, h->px, h->pr, h->pz, h->pp, h->pq, h->scal, h->partials, h->stage_in,
@@ -372,7 +402,8 @@ lap_status lap_solve(lap_hierarchy *h, const double *b, double *x, double tol, i
     int32_t it = 0;
     double rr = 0;
     int conv = 0;
-    lap::run_pcg(h, tol, &it, &rr, &conv, s);
+    if (h->dist) lap::dist_run_pcg(h, tol, &it, &rr, &conv, s);
+    else lap::run_pcg(h, tol, &it, &rr, &conv, s);
     bool xdev = lap::is_device_ptr(x);
     double *xd = xdev ? x : h->stage_out;
     lap::k_gather_perm<<<g, 256, 0, s>>>(n, h->cmap, h->px, xd);             // x = Pi^T x'

@@ -2,6 +2,7 @@
 // B200 (sm_100a) only.  Not part of the ABI (see include/lap.h).
 #pragma once
 #include <cuda_runtime.h>
+#include <cub/cub.cuh>
 #include <stdint.h>
 #include <string>
 #include <vector>
@@ -191,6 +192,9 @@ struct lap_hierarchy {
     // the whole PCG loop as resident graphs (WHILE conditional node, solve.cu)
     cudaGraphExec_t pcg_start = nullptr, pcg_resume = nullptr;
     void *pcg_counts = nullptr;
+    // multi-GPU shards (dist.cu), NULL for a single-GPU hierarchy
+    void *dist = nullptr;
+    void *dist_owned = nullptr;
     lap_stats stats{};
     lap::Stats cur;
     int device = 0;
@@ -218,10 +222,17 @@ void spmv_level(lap_hierarchy *h, const Level &L, EpiKind kind, const EpiArgs &a
 // storage (storage.cu)
 void build_storage(lap_hierarchy *h, int l, cudaStream_t s);
 void build_transfers(lap_hierarchy *h, cudaStream_t s);
+// LCHUNK work items over the rows [row0, row0+nrows) of a CSR longer than minlen
+int64_t build_chunks(const int64_t *rp, int64_t row0, int64_t nrows, int64_t minlen, int32_t **crow, int32_t **cidx,
+                     int32_t **cslot, double **cpart, int32_t **ccnt, cudaStream_t s);
 int64_t spmv_partial_slots(const Level &L);
 void vcycle(lap_hierarchy *h, int l, cudaStream_t s);   // x_l = V(l, b_l)
 void run_pcg(lap_hierarchy *h, double tol, int32_t *iters, double *relres, int *conv, cudaStream_t s);
 void capture_pcg(lap_hierarchy *h);
+// multi-GPU (dist.cu)
+void build_dist(lap_hierarchy *h, lap_comm *c, cudaStream_t s);
+void free_dist(lap_hierarchy *h);
+void dist_run_pcg(lap_hierarchy *h, double tol, int32_t *iters, double *relres, int *conv, cudaStream_t s);
 void free_pcg(lap_hierarchy *h);
 
 // small shared reductions (solve.cu)
@@ -234,6 +245,109 @@ inline unsigned grid_for(int64_t work, int threads, int64_t cap = 148 * 32) {
     if (g > cap) g = cap;
     return (unsigned)g;
 }
+
+// ---------------------------------------------------------------- row groups
+// Row groups: a row is handled by G lanes (G | 32, chosen per level from the
+// average degree, group_size()), so low-degree levels do not idle 80% of a
+// warp and long rows still get several lanes.  Every lane of a warp runs the
+// same number of outer iterations (rows past n are empty), so the group
+// shuffles below always see converged warps.  All reductions done this way
+// are exact (integer / int128 / max / total-order arg-max), so the result is
+// independent of G.
+#define GROUP_LOOP_BEGIN(G, n)                                                         \
+    const int lane = threadIdx.x & 31, gl = lane & ((G)-1);                            \
+    (void)gl;                                                                          \
+    const int64_t _gpw = 32 / (G);                                                     \
+    const int64_t _stride = (((int64_t)gridDim.x * blockDim.x) >> 5) * _gpw;           \
+    for (int64_t _base = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * _gpw; \
+         _base < (n); _base += _stride) {                                              \
+        const int64_t i = _base + lane / (G);                                          \
+        const bool live = i < (n);                                                     \
+        (void)live;
+#define GROUP_LOOP_END }
+
+template <int G, class T>
+__device__ __forceinline__ T grp_sum(T v) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+inline int group_size(int64_t n, int64_t nnz) {
+    double avg = n > 0 ? (double)nnz / (double)n : 0.0;
+    return avg <= 4.0 ? 4 : avg <= 8.0 ? 8 : avg <= 16.0 ? 16 : 32;
+}
+#define LAUNCH_G(G, kern, rows, s, ...)                                                                 \
+    do {                                                                                                \
+        switch (G) {                                                                                    \
+            case 4: kern<4><<<grid_for((rows) * 4, 256, 148 * 16), 256, 0, s>>>(__VA_ARGS__); break;    \
+            case 8: kern<8><<<grid_for((rows) * 8, 256, 148 * 16), 256, 0, s>>>(__VA_ARGS__); break;    \
+            case 16: kern<16><<<grid_for((rows) * 16, 256, 148 * 16), 256, 0, s>>>(__VA_ARGS__); break; \
+            default: kern<32><<<grid_for((rows) * 32, 256, 148 * 16), 256, 0, s>>>(__VA_ARGS__); break; \
+        }                                                                                               \
+        ++g_kl;                                                                                         \
+    } while (0)
+
+// ballot-compacted emission over a row in ascending column order: entries k of
+// row i with pred(k) go to out[o + rank]; the warp loops to the longest row
+// (EMIT sees the entry index k and its output position p)
+#define GROUP_COMPACT_ROW(G, kb, ke, o, PRED, EMIT)                                                   \
+    {                                                                                                 \
+        const unsigned _gmask = ((G) == 32 ? 0xffffffffu : ((1u << (G)) - 1u)) << (lane & ~((G)-1)); \
+        int64_t _len = (ke) - (kb);                                                                   \
+        for (int _sh = 16; _sh > 0; _sh >>= 1) {                                                      \
+            int64_t _t2 = __shfl_xor_sync(0xffffffffu, _len, _sh);                                    \
+            _len = _t2 > _len ? _t2 : _len;                                                           \
+        }                                                                                             \
+        for (int64_t _q = 0; _q < _len; _q += (G)) {                                                  \
+            int64_t k = (kb) + _q + gl;                                                               \
+            bool _take = k < (ke) && (PRED);                                                          \
+            unsigned _bal = __ballot_sync(0xffffffffu, _take) & _gmask;                               \
+            if (_take) {                                                                              \
+                int64_t p = (o) + __popc(_bal & ((1u << lane) - 1));                                  \
+                EMIT;                                                                                 \
+            }                                                                                         \
+            (o) += __popc(_bal);                                                                      \
+        }                                                                                             \
+    }
+// ---------------------------------------------------------------- entry-parallel helpers
+// row of stored entry t of a CSR with n rows: the largest i with rp[i] <= t
+// (empty rows are skipped).  Consecutive t of a warp follow the same path, so
+// the search runs out of L1.
+__device__ __forceinline__ int64_t row_of(const int64_t *__restrict__ rp, int64_t n, int64_t t) {
+    int64_t lo = 0, hi = n - 1;
+    while (lo < hi) {
+        int64_t mid = (lo + hi + 1) >> 1;
+        if (rp[mid] <= t) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+// Entry-parallel filtered emission: a 256-thread block claims contiguous
+// output space with ONE atomicAdd on *cursor per 256 entries (block prefix
+// sum of the predicate).  The output ORDER depends on block scheduling, so
+// this is only used where the emitted terms are sorted by key and combined
+// by an order-independent CanonSum afterwards (Galerkin, Schur): the level
+// built from them is bitwise deterministic.
+#define ENTRY_EMIT_LOOP(nent, cursor, TAKE, EMIT)                                                   \
+    {                                                                                              \
+        typedef cub::BlockScan<int, 256> _BS;                                                      \
+        __shared__ typename _BS::TempStorage _ts;                                                  \
+        __shared__ unsigned long long _boff;                                                       \
+        for (int64_t _b0 = (int64_t)blockIdx.x * 256; _b0 < (nent); _b0 += (int64_t)gridDim.x * 256) { \
+            const int64_t t = _b0 + threadIdx.x;                                                   \
+            bool take = false;                                                                     \
+            if (t < (nent)) { TAKE; }                                                              \
+            int _rk, _tot;                                                                         \
+            _BS(_ts).ExclusiveSum(take ? 1 : 0, _rk, _tot);                                        \
+            if (threadIdx.x == 0) _boff = _tot ? atomicAdd((cursor), (unsigned long long)_tot) : 0ULL; \
+            __syncthreads();                                                                       \
+            if (take) {                                                                            \
+                const int64_t p = (int64_t)_boff + _rk;                                            \
+                EMIT;                                                                              \
+            }                                                                                      \
+            __syncthreads();                                                                       \
+        }                                                                                          \
+    }
 
 // ---------------------------------------------------------------- programmatic dependent launch
 // Solve-phase kernels are chained with programmatic dependent launch (PDL,

@@ -43,52 +43,12 @@ static void exclusive_scan_i64(const int64_t *in, int64_t *out, int64_t n, cudaS
     LAP_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, in, out, n, s)); ++g_kl;
 }
 
-// Row groups: a row is handled by G lanes (G | 32, chosen per level from the
-// average degree, group_size()), so low-degree levels do not idle 80% of a
-// warp and long rows still get several lanes.  Every lane of a warp runs the
-// same number of outer iterations (rows past n are empty), so the group
-// shuffles below always see converged warps.  All reductions done this way
-// are exact (integer / int128 / max / total-order arg-max), so the result is
-// independent of G.
-#define GROUP_LOOP_BEGIN(G, n)                                                         \
-    const int lane = threadIdx.x & 31, gl = lane & ((G)-1);                            \
-    (void)gl;                                                                          \
-    const int64_t _gpw = 32 / (G);                                                     \
-    const int64_t _stride = (((int64_t)gridDim.x * blockDim.x) >> 5) * _gpw;           \
-    for (int64_t _base = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * _gpw; \
-         _base < (n); _base += _stride) {                                              \
-        const int64_t i = _base + lane / (G);                                          \
-        const bool live = i < (n);                                                     \
-        (void)live;
-#define GROUP_LOOP_END }
-
-template <int G, class T>
-__device__ __forceinline__ T grp_sum(T v) {
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
 template <int G>
 __device__ __forceinline__ i128 grp_sum_i128(i128 v) {
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) v += shfl_xor_i128(v, o);
     return v;
 }
-static int group_size(int64_t n, int64_t nnz) {
-    double avg = n > 0 ? (double)nnz / (double)n : 0.0;
-    return avg <= 4.0 ? 4 : avg <= 8.0 ? 8 : avg <= 16.0 ? 16 : 32;
-}
-#define LAUNCH_G(G, kern, rows, s, ...)                                                                 \
-    do {                                                                                                \
-        switch (G) {                                                                                    \
-            case 4: kern<4><<<grid_for((rows) * 4, 256, 148 * 16), 256, 0, s>>>(__VA_ARGS__); break;    \
-            case 8: kern<8><<<grid_for((rows) * 8, 256, 148 * 16), 256, 0, s>>>(__VA_ARGS__); break;    \
-            case 16: kern<16><<<grid_for((rows) * 16, 256, 148 * 16), 256, 0, s>>>(__VA_ARGS__); break; \
-            default: kern<32><<<grid_for((rows) * 32, 256, 148 * 16), 256, 0, s>>>(__VA_ARGS__); break; \
-        }                                                                                               \
-        ++g_kl;                                                                                         \
-    } while (0)
-
 // max |v| as an exact order-independent reduction (bit pattern of a
 // non-negative double orders like the value).
 __global__ void k_max_abs(const double *__restrict__ v, int64_t n, unsigned long long *out) {
@@ -121,16 +81,6 @@ static double max_abs(const double *v, int64_t n, cudaStream_t s) {
 // O-S0 validation: warp per row
 // =========================================================================
 
-__device__ __forceinline__ int64_t find_col(const int64_t *row_ptr, const int32_t *col, int64_t r, int32_t c) {
-    int64_t lo = row_ptr[r], hi = row_ptr[r + 1];
-    while (lo < hi) {
-        int64_t mid = (lo + hi) >> 1;
-        if (col[mid] < c) lo = mid + 1;
-        else hi = mid;
-    }
-    return (lo < row_ptr[r + 1] && col[lo] == c) ? lo : -1;
-}
-
 template <int G>
 __global__ void k_validate(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                            const double *__restrict__ w, int *flag) {
@@ -143,15 +93,56 @@ __global__ void k_validate(int64_t n, const int64_t *__restrict__ row_ptr, const
             bool bad = (j < 0) || (j >= n) || (j == i) || (k > a && col[k - 1] >= j);
             double wk = w ? w[k] : 1.0;
             bad |= !(wk > 0.0) || !isfinite(wk);
-            if (!bad) {
-                int64_t t = find_col(row_ptr, col, j, (int32_t)i);
-                bad |= (t < 0);
-                if (!bad && w) bad |= (__double_as_longlong(w[t]) != __double_as_longlong(wk));
-            }
             if (bad) atomicOr(flag, 1);
         }
     }
     GROUP_LOOP_END
+}
+
+// Symmetry (w_ij == w_ji bitwise): the transposed entry list, sorted
+// by (col, row), must equal the CSR list in (row, col) order entry for entry.
+// An exact check with one radix sort instead of a binary search per entry
+// (which serialises on hub rows).
+template <int G>
+__global__ void k_sym_keys(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                           int32_t *__restrict__ rowof, uint64_t *__restrict__ tkey, int64_t *__restrict__ idx) {
+    GROUP_LOOP_BEGIN(G, n)
+    if (live)
+        for (int64_t k = row_ptr[i] + gl; k < row_ptr[i + 1]; k += G) {
+            rowof[k] = (int32_t)i;
+            tkey[k] = ((uint64_t)(uint32_t)col[k] << 32) | (uint64_t)i;
+            idx[k] = k;
+        }
+    GROUP_LOOP_END
+}
+__global__ void k_sym_check(int64_t nnz, const int32_t *__restrict__ rowof, const int32_t *__restrict__ col,
+                            const double *__restrict__ w, const uint64_t *__restrict__ tkey,
+                            const int64_t *__restrict__ idx, int *flag) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nnz; t += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t want = ((uint64_t)(uint32_t)rowof[t] << 32) | (uint64_t)(uint32_t)col[t];
+        bool bad = tkey[t] != want;
+        if (!bad && w) bad = __double_as_longlong(w[idx[t]]) != __double_as_longlong(w[t]);
+        if (bad) atomicOr(flag, 1);
+    }
+}
+
+static bool is_symmetric(int64_t n, int64_t nnz, const int64_t *rp, const int32_t *col, const double *w,
+                         cudaStream_t s) {
+    if (nnz == 0) return true;
+    DBuf<int32_t> rowof(nnz, s);
+    DBuf<uint64_t> k1(nnz, s), k2(nnz, s);
+    DBuf<int64_t> i1(nnz, s), i2(nnz, s);
+    LAUNCH_G(group_size(n, nnz), k_sym_keys, n, s, n, rp, col, rowof.p, k1.p, i1.p);
+    size_t bytes = 0;
+    int end_bit = 32 + bitlen_u64((uint64_t)n);
+    LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k1.p, k2.p, i1.p, i2.p, nnz, 0, end_bit, s));
+    DBuf<char> tmp((int64_t)bytes, s);
+    LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, k1.p, k2.p, i1.p, i2.p, nnz, 0, end_bit, s)); ++g_kl;
+    DBuf<int> flag(1, s);
+    LAP_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+    k_sym_check<<<grid_for(nnz, 256, 148 * 16), 256, 0, s>>>(nnz, rowof.p, col, w, k2.p, i2.p, flag.p); ++g_kl;
+    LAP_CHECK_LAUNCH();
+    return d2h_scalar(flag.p, s) == 0;
 }
 
 // ---- connectivity: lock-free union-find (parents only ever decrease) ----
@@ -411,70 +402,77 @@ __global__ void k_fmap(int64_t n, const uint8_t *F, const int64_t *cpos, const i
         }
     }
 }
-// number of Schur terms of each C row (thread per coarse row)
-__global__ void k_schur_count(int64_t nc, const int32_t *__restrict__ cid, const int64_t *__restrict__ row_ptr,
-                              const int32_t *__restrict__ col, const uint8_t *__restrict__ F, int64_t *cnt) {
-    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x) {
-        int64_t i = cid[a], c = 0;
-        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; k++) {
-            int32_t j = col[k];
-            c += F[j] ? (row_ptr[j + 1] - row_ptr[j] - 1) : 1;
-        }
-        cnt[a] = c;
+// Schur complement terms (O-R25), generated where they are cheap:
+//   * L_CC entries w_ab from the C rows (a group of G lanes per row, ballot-
+//     compacted in ascending column order);
+//   * fill fl(fl(w_fa w_fb)/d_f) for every ordered pair a != b of neighbours
+//     of each f in F, from the F rows (F is independent, so all neighbours of
+//     f are in C, and deg_f <= 4: a thread per f, at most 12 terms).
+// The multiset of terms is the method's; their order is irrelevant (sorted
+// and summed with CanonSum), so hub C rows no longer serialise the build.
+// L_CC entries: every stored (i, j) with i, j both in C -> ((fmap_i << cb) | fmap_j, w)
+__global__ void __launch_bounds__(256) k_schur_cc_emit(int64_t n, int64_t nnz, const int64_t *__restrict__ row_ptr,
+                                                       const int32_t *__restrict__ col, const double *__restrict__ w,
+                                                       const uint8_t *__restrict__ F, const int32_t *__restrict__ fmap,
+                                                       int cb, unsigned long long *cursor, uint64_t *__restrict__ keys,
+                                                       double *__restrict__ vals) {
+    int64_t i = 0;
+    ENTRY_EMIT_LOOP(nnz, cursor, (i = row_of(row_ptr, n, t), take = !F[i] && !F[col[t]]),
+                    (keys[p] = ((uint64_t)fmap[i] << cb) | (uint64_t)fmap[col[t]], vals[p] = w[t]))
+}
+__global__ void k_schur_f_count(int64_t nF, const int32_t *__restrict__ fid, const int64_t *__restrict__ row_ptr,
+                                int64_t *cnt) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nF; t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t f = fid[t], dg = row_ptr[f + 1] - row_ptr[f];
+        cnt[t] = dg * (dg - 1);
     }
 }
-// emit W'[a,b] terms: w_ab, and fl(fl(w_fa*w_fb)/d_f) through each f (O-R25)
-__global__ void k_schur_emit(int64_t nc, const int32_t *__restrict__ cid, const int64_t *__restrict__ row_ptr,
-                             const int32_t *__restrict__ col, const double *__restrict__ w,
-                             const double *__restrict__ d, const uint8_t *__restrict__ F,
-                             const int32_t *__restrict__ fmap, const int64_t *__restrict__ off, int cb,
-                             uint64_t *__restrict__ keys, double *__restrict__ vals) {
-    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x) {
-        int64_t i = cid[a], o = off[a];
-        uint64_t ra = ((uint64_t)a) << cb;
-        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; k++) {
-            int32_t j = col[k];
-            if (!F[j]) {
-                keys[o] = ra | (uint64_t)fmap[j];
-                vals[o] = w[k];
-                o++;
-            } else {
-                int64_t kf = find_col(row_ptr, col, j, (int32_t)i);
-                double wfa = w[kf], df = d[j];
-                for (int64_t q = row_ptr[j]; q < row_ptr[j + 1]; q++) {
-                    int32_t bb = col[q];
-                    if (bb == i) continue;
-                    keys[o] = ra | (uint64_t)fmap[bb];
-                    vals[o] = __ddiv_rn(__dmul_rn(wfa, w[q]), df);
-                    o++;
-                }
-            }
-        }
-    }
-}
-// transposed L_FC for the restriction: per coarse c, (f, w_fc/d_f) for f ~ c in F
-__global__ void k_ct_count(int64_t nc, const int32_t *cid, const int64_t *row_ptr, const int32_t *col,
-                           const uint8_t *F, int64_t *cnt) {
-    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x) {
-        int64_t i = cid[a], c = 0;
-        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; k++) c += F[col[k]] ? 1 : 0;
-        cnt[a] = c;
-    }
-}
-__global__ void k_ct_fill(int64_t nc, const int32_t *cid, const int64_t *row_ptr, const int32_t *col,
-                          const double *w, const double *d, const uint8_t *F, const int64_t *off, int32_t *ct_f,
-                          double *ct_coef) {
-    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x) {
-        int64_t i = cid[a], o = off[a];
-        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; k++) {
-            int32_t j = col[k];
-            if (F[j]) {
-                ct_f[o] = j;
-                ct_coef[o] = w[k] / d[j];
+__global__ void k_schur_f_emit(int64_t nF, const int32_t *__restrict__ fid, const int64_t *__restrict__ row_ptr,
+                               const int32_t *__restrict__ col, const double *__restrict__ w,
+                               const double *__restrict__ d, const int32_t *__restrict__ fmap,
+                               const int64_t *__restrict__ off, int64_t base, int cb, uint64_t *__restrict__ keys,
+                               double *__restrict__ vals) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nF; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t f = fid[t], kb = row_ptr[f], ke = row_ptr[f + 1];
+        const double df = d[f];
+        int64_t o = base + off[t];
+        for (int64_t p = kb; p < ke; p++) {
+            const uint64_t ra = ((uint64_t)fmap[col[p]]) << cb;
+            for (int64_t q = kb; q < ke; q++) {
+                if (q == p) continue;
+                keys[o] = ra | (uint64_t)fmap[col[q]];
+                vals[o] = __ddiv_rn(__dmul_rn(w[p], w[q]), df);
                 o++;
             }
         }
     }
+}
+// transposed L_FC for the restriction: per coarse c, (f, w_fc/d_f) for f ~ c in F,
+// in ascending f order (a group of G lanes per C row)
+template <int G>
+__global__ void k_ct_count(int64_t nc, const int32_t *__restrict__ cid, const int64_t *__restrict__ row_ptr,
+                           const int32_t *__restrict__ col, const uint8_t *__restrict__ F, int64_t *cnt) {
+    GROUP_LOOP_BEGIN(G, nc)
+        int64_t c = 0;
+        if (live) {
+            const int64_t fi = cid[i];
+            for (int64_t k = row_ptr[fi] + gl; k < row_ptr[fi + 1]; k += G) c += F[col[k]] ? 1 : 0;
+        }
+        c = grp_sum<G>(c);
+        if (live && gl == 0) cnt[i] = c;
+    GROUP_LOOP_END
+}
+template <int G>
+__global__ void k_ct_fill(int64_t nc, const int32_t *__restrict__ cid, const int64_t *__restrict__ row_ptr,
+                          const int32_t *__restrict__ col, const double *__restrict__ w, const double *__restrict__ d,
+                          const uint8_t *__restrict__ F, const int64_t *__restrict__ off, int32_t *__restrict__ ct_f,
+                          double *__restrict__ ct_coef) {
+    GROUP_LOOP_BEGIN(G, nc)
+        const int64_t fi = live ? cid[i] : 0;
+        const int64_t kb = live ? row_ptr[fi] : 0, ke = live ? row_ptr[fi + 1] : 0;
+        int64_t o = live ? off[i] : 0;
+        GROUP_COMPACT_ROW(G, kb, ke, o, F[col[k]], (ct_f[p] = col[k], ct_coef[p] = w[k] / d[col[k]]))
+    GROUP_LOOP_END
 }
 
 // =========================================================================
@@ -639,52 +637,17 @@ __global__ void k_agg_ids(int64_t n, const int8_t *st, const int32_t *idx, const
 // O-S5 Galerkin (O-R24)
 // =========================================================================
 
-template <int G>
-__global__ void k_gal_count(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                            const int32_t *__restrict__ agg, int64_t *cnt) {
-    GROUP_LOOP_BEGIN(G, n)
-        int64_t c = 0;
-        if (live) {
-            int32_t a = agg[i];
-            for (int64_t k = row_ptr[i] + gl; k < row_ptr[i + 1]; k += G) c += (agg[col[k]] != a);
-        }
-        c = grp_sum<G>(c);
-        if (live && gl == 0) cnt[i] = c;
-    GROUP_LOOP_END
-}
-template <int G>
-__global__ void k_gal_emit(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                           const double *__restrict__ w, const int32_t *__restrict__ agg,
-                           const int64_t *__restrict__ off, int cb, uint64_t *__restrict__ keys,
-                           double *__restrict__ vals) {
-    GROUP_LOOP_BEGIN(G, n)
-        const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (lane & ~(G - 1));
-        uint64_t a = live ? (uint64_t)agg[i] : 0;
-        int64_t o = live ? off[i] : 0;
-        const int64_t kb = live ? row_ptr[i] : 0, ke = live ? row_ptr[i + 1] : 0;
-        // the group with the longest row sets the trip count for the warp
-        int64_t len = ke - kb;
-        for (int sh = 16; sh > 0; sh >>= 1) {
-            int64_t t = __shfl_xor_sync(0xffffffffu, len, sh);
-            len = t > len ? t : len;
-        }
-        for (int64_t q = 0; q < len; q += G) {
-            int64_t k = kb + q + gl;
-            bool take = false;
-            uint64_t b = 0;
-            if (k < ke) {
-                b = (uint64_t)agg[col[k]];
-                take = (b != a);
-            }
-            unsigned m = __ballot_sync(0xffffffffu, take) & gmask;
-            if (take) {
-                int64_t p = o + __popc(m & ((1u << lane) - 1));
-                keys[p] = (a << cb) | b;
-                vals[p] = w[k];
-            }
-            o += __popc(m);
-        }
-    GROUP_LOOP_END
+// Galerkin terms: every stored (i, j, w) with a = agg_i != b = agg_j
+// becomes ((a << cb) | b, w); entry-parallel, so hub rows do not serialise.
+__global__ void __launch_bounds__(256) k_gal_emit(int64_t n, int64_t nnz, const int64_t *__restrict__ row_ptr,
+                                                  const int32_t *__restrict__ col, const double *__restrict__ w,
+                                                  const int32_t *__restrict__ agg, int cb,
+                                                  unsigned long long *cursor, uint64_t *__restrict__ keys,
+                                                  double *__restrict__ vals) {
+    uint64_t a = 0, bb = 0;
+    ENTRY_EMIT_LOOP(nnz, cursor,
+                    (a = (uint64_t)agg[row_of(row_ptr, n, t)], bb = (uint64_t)agg[col[t]], take = a != bb),
+                    (keys[p] = (a << cb) | bb, vals[p] = w[t]))
 }
 
 // =========================================================================
@@ -936,31 +899,41 @@ static void build_elim_level(lap_hierarchy *h, Level &L, const DBuf<uint8_t> &F,
     L.fid = (int32_t *)dalloc(sizeof(int32_t) * (nF + 1), s);
     k_fmap<<<g, 256, 0, s>>>(n, F.p, cpos.p, fpos.p, L.fmap, L.cid, L.fid); ++g_kl;
     LAP_CHECK_LAUNCH();
-    // terms of the Schur complement
-    DBuf<int64_t> cnt(nc + 1, s), off(nc + 1, s);
-    LAP_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int64_t) * (nc + 1), s));
-    unsigned gc = grid_for(nc, 128, 148 * 16);
-    k_schur_count<<<gc, 128, 0, s>>>(nc, L.cid, L.row_ptr, L.col, F.p, cnt.p); ++g_kl;
+    // terms of the Schur complement: L_CC entries (entry-parallel), fill from the F rows
+    const int G = group_size(n, L.nnz);
+    DBuf<int64_t> fcnt(nF + 1, s), foff(nF + 1, s);
+    LAP_CUDA(cudaMemsetAsync(fcnt.p, 0, sizeof(int64_t) * (nF + 1), s));
+    k_schur_f_count<<<grid_for(nF, 256, 148 * 16), 256, 0, s>>>(nF, L.fid, L.row_ptr, fcnt.p); ++g_kl;
     LAP_CHECK_LAUNCH();
-    exclusive_scan_i64(cnt.p, off.p, nc + 1, s);
-    int64_t T = d2h_scalar(off.p + nc, s);
+    exclusive_scan_i64(fcnt.p, foff.p, nF + 1, s);
+    int64_t Tf = d2h_scalar(foff.p + nF, s);
     int cb = bitlen_u64((uint64_t)(nc > 0 ? nc : 1));
-    DBuf<uint64_t> keys(T, s);
-    DBuf<double> vals(T, s);
-    k_schur_emit<<<gc, 128, 0, s>>>(nc, L.cid, L.row_ptr, L.col, L.w, L.d, F.p, L.fmap, off.p, cb, keys.p, vals.p); ++g_kl;
+    DBuf<uint64_t> keys(L.nnz + Tf, s);
+    DBuf<double> vals(L.nnz + Tf, s);
+    DBuf<unsigned long long> cur(1, s);
+    LAP_CUDA(cudaMemsetAsync(cur.p, 0, sizeof(unsigned long long), s));
+    if (L.nnz > 0) {
+        k_schur_cc_emit<<<grid_for(L.nnz, 256, 148 * 16), 256, 0, s>>>(n, L.nnz, L.row_ptr, L.col, L.w, F.p, L.fmap,
+                                                                      cb, cur.p, keys.p, vals.p); ++g_kl;
+        LAP_CHECK_LAUNCH();
+    }
+    int64_t Tcc = (int64_t)d2h_scalar(cur.p, s);
+    int64_t T = Tcc + Tf;
+    k_schur_f_emit<<<grid_for(nF, 256, 148 * 16), 256, 0, s>>>(nF, L.fid, L.row_ptr, L.col, L.w, L.d, L.fmap, foff.p,
+                                                               Tcc, cb, keys.p, vals.p); ++g_kl;
     LAP_CHECK_LAUNCH();
     int e_max = ilogb_pos(L.maxw) + 1;
     csr_from_terms(nc, cb, T, keys, vals, e_max, 4 * L.nnz, true, N, s);
     // transposed L_FC for the restriction P^T b
     DBuf<int64_t> tc(nc + 1, s);
     LAP_CUDA(cudaMemsetAsync(tc.p, 0, sizeof(int64_t) * (nc + 1), s));
-    k_ct_count<<<gc, 128, 0, s>>>(nc, L.cid, L.row_ptr, L.col, F.p, tc.p); ++g_kl;
+    LAUNCH_G(G, k_ct_count, nc, s, nc, L.cid, L.row_ptr, L.col, F.p, tc.p);
     L.ct_ptr = (int64_t *)dalloc(sizeof(int64_t) * (nc + 1), s);
     exclusive_scan_i64(tc.p, L.ct_ptr, nc + 1, s);
     int64_t TT = d2h_scalar(L.ct_ptr + nc, s);
     L.ct_f = (int32_t *)dalloc(sizeof(int32_t) * (TT + 1), s);
     L.ct_coef = (double *)dalloc(sizeof(double) * (TT + 1), s);
-    k_ct_fill<<<gc, 128, 0, s>>>(nc, L.cid, L.row_ptr, L.col, L.w, L.d, F.p, L.ct_ptr, L.ct_f, L.ct_coef); ++g_kl;
+    LAUNCH_G(G, k_ct_fill, nc, s, nc, L.cid, L.row_ptr, L.col, L.w, L.d, F.p, L.ct_ptr, L.ct_f, L.ct_coef);
     LAP_CHECK_LAUNCH();
     h->cur.edges += L.nnz;
 }
@@ -1017,19 +990,18 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
 }
 
 static void galerkin(lap_hierarchy *h, Level &L, Level &N, cudaStream_t s) {
-    int64_t n = L.n, m = L.m;
-    DBuf<int64_t> cnt(n + 1, s), off(n + 1, s);
-    LAP_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int64_t) * (n + 1), s));
-    const int G = group_size(n, L.nnz);
-    LAUNCH_G(G, k_gal_count, n, s, n, L.row_ptr, L.col, L.agg, cnt.p);
-    LAP_CHECK_LAUNCH();
-    exclusive_scan_i64(cnt.p, off.p, n + 1, s);
-    int64_t T = d2h_scalar(off.p + n, s);
+    int64_t n = L.n, m = L.m, nnz = L.nnz;
     int cb = bitlen_u64((uint64_t)(m > 0 ? m : 1));
-    DBuf<uint64_t> keys(T, s);
-    DBuf<double> vals(T, s);
-    LAUNCH_G(G, k_gal_emit, n, s, n, L.row_ptr, L.col, L.w, L.agg, off.p, cb, keys.p, vals.p);
-    LAP_CHECK_LAUNCH();
+    DBuf<uint64_t> keys(nnz, s);
+    DBuf<double> vals(nnz, s);
+    DBuf<unsigned long long> cur(1, s);
+    LAP_CUDA(cudaMemsetAsync(cur.p, 0, sizeof(unsigned long long), s));
+    if (nnz > 0) {
+        k_gal_emit<<<grid_for(nnz, 256, 148 * 16), 256, 0, s>>>(n, nnz, L.row_ptr, L.col, L.w, L.agg, cb, cur.p, keys.p,
+                                                                vals.p); ++g_kl;
+        LAP_CHECK_LAUNCH();
+    }
+    int64_t T = (int64_t)d2h_scalar(cur.p, s);
     csr_from_terms(m, cb, T, keys, vals, ilogb_pos(L.maxw) + 1, L.nnz, true, N, s);
     h->cur.edges += L.nnz;
 }
@@ -1081,6 +1053,7 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
             LAP_CHECK_LAUNCH();
         }
         if (d2h_scalar(flag.p, s)) throw Error{LAP_EGRAPH, "graph is not a valid symmetric positive-weight adjacency"};
+        if (!is_symmetric(n, nnz, rp, col, w, s)) throw Error{LAP_EGRAPH, "graph is not symmetric (w_ij != w_ji)"};
         if (!is_connected(n, nnz, rp, col, s)) throw Error{LAP_EDISCONNECTED, "graph is disconnected"};
     }
     // --- O-S1 level 0

@@ -118,18 +118,15 @@ __global__ void k_storage_deg(int64_t n, const int32_t *sid, const int64_t *rp, 
         sd[p] = d[i];
     }
 }
-// copy logical row sid[p] into storage row p, columns translated (warp per row)
-__global__ void k_storage_fill(int64_t n, const int32_t *sid, const int32_t *spos, const int64_t *rp,
+// copy logical row sid[p] into storage row p, columns translated; entry-
+// parallel over the storage entries (hub rows do not serialise)
+__global__ void k_storage_fill(int64_t n, int64_t nnz, const int32_t *sid, const int32_t *spos, const int64_t *rp,
                                const int32_t *col, const double *w, const int64_t *srp, int32_t *scol, double *sw) {
-    int lane = threadIdx.x & 31;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t p = warp; p < n; p += nwarps) {
-        int64_t i = sid[p], a = rp[i], o = srp[p], len = rp[i + 1] - a;
-        for (int64_t k = lane; k < len; k += 32) {
-            scol[o + k] = spos[col[a + k]];
-            sw[o + k] = w[a + k];
-        }
+    GRID_STRIDE(t, nnz) {
+        int64_t p = row_of(srp, n, t);
+        int64_t src = rp[sid[p]] + (t - srp[p]);
+        scol[t] = spos[col[src]];
+        sw[t] = w[src];
     }
 }
 __global__ void k_to_u16(int64_t m, const int32_t *in, uint16_t *out) {
@@ -165,7 +162,7 @@ static void scan_excl(const T *in, T *out, int64_t n, cudaStream_t s) {
     g_kl += 2;
 }
 
-static int64_t build_chunks(const int64_t *rp, int64_t row0, int64_t nrows, int64_t minlen, int32_t **crow,
+int64_t build_chunks(const int64_t *rp, int64_t row0, int64_t nrows, int64_t minlen, int32_t **crow,
                             int32_t **cidx, int32_t **cslot, double **cpart, int32_t **ccnt, cudaStream_t s) {
     if (nrows <= 0) return 0;
     DBuf<int64_t> cc(nrows + 1, s), first(nrows + 1, s);
@@ -312,8 +309,8 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
     L.scol = (int32_t *)dalloc(sizeof(int32_t) * (L.nnz + 1), s);
     L.sw = (double *)dalloc(sizeof(double) * (L.nnz + 1), s);
     if (L.nnz) {
-        k_storage_fill<<<grid_for(n * 32, 256, 148 * 16), 256, 0, s>>>(n, L.sid, L.spos, L.row_ptr, L.col, L.w, L.srp,
-                                                                        L.scol, L.sw);
+        k_storage_fill<<<grid_for(L.nnz, 256, 148 * 16), 256, 0, s>>>(n, L.nnz, L.sid, L.spos, L.row_ptr, L.col, L.w,
+                                                                      L.srp, L.scol, L.sw);
         g_kl++;
     }
     // SELL-32 slices of the short class

@@ -38,7 +38,7 @@ class lap_params(ctypes.Structure):
         ("tv_sweeps", ctypes.c_int32), ("tv_omega", ctypes.c_double), ("vote_rounds", ctypes.c_int32),
         ("vote_threshold", ctypes.c_int32), ("coarse_nnz", ctypes.c_int64), ("max_levels", ctypes.c_int32),
         ("seed", ctypes.c_uint64), ("random_order", ctypes.c_int32), ("affinity_power", ctypes.c_int32),
-        ("keep_strength", ctypes.c_int32), ("use_graphs", ctypes.c_int32),
+        ("keep_strength", ctypes.c_int32), ("use_graphs", ctypes.c_int32), ("replicate_nnz", ctypes.c_int64),
     ]
 
 
@@ -51,6 +51,8 @@ EXPORTS = [
     "lap_params_default", "lap_last_error", "lap_version", "lap_setup", "lap_solve", "lap_free",
     "lap_num_levels", "lap_level_info", "lap_level_export", "lap_level_strength", "lap_coarse_pinv",
     "lap_perm", "lap_spmv", "lap_vcycle", "lap_get_stats", "lap_bench_op",
+    "lap_nccl_unique_id", "lap_comm_create", "lap_comm_create_virtual", "lap_comm_info", "lap_comm_free",
+    "lap_setup_dist", "lap_dist_index",
 ]
 
 
@@ -78,6 +80,13 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "lap_vcycle": (ctypes.c_int, [P, P, P, P]),
         "lap_get_stats": (ctypes.c_int, [P, ctypes.POINTER(lap_stats)]),
         "lap_bench_op": (ctypes.c_int, [P, i32, i32, i32, P, P, pdbl, pi64]),
+        "lap_nccl_unique_id": (ctypes.c_int, [P]),
+        "lap_comm_create": (ctypes.c_int, [P, i32, i32, i32, i32, ctypes.POINTER(P)]),
+        "lap_comm_create_virtual": (ctypes.c_int, [i32, i32, ctypes.POINTER(P)]),
+        "lap_comm_info": (ctypes.c_int, [P, pi32, pi32, pi32, pi32, pi32]),
+        "lap_comm_free": (None, [P]),
+        "lap_setup_dist": (ctypes.c_int, [ctypes.POINTER(lap_graph), ctypes.POINTER(lap_params), P, P, ctypes.POINTER(P)]),
+        "lap_dist_index": (ctypes.c_int, [i64, i32, i64, P, P, pi64]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -129,10 +138,52 @@ def lap_params_default(**kw) -> lap_params:
     return p
 
 
-class Hierarchy:
-    """lap_setup(graph, params) -> hierarchy ; .solve(b) -> (x, iters, residual)."""
+class Comm:
+    """A pr x pc process grid for the sharded solve (lap_comm_create /
+    lap_comm_create_virtual).  With nccl_id=None the whole grid is emulated in
+    this process on the current GPU."""
 
-    def __init__(self, graph, params: lap_params | None = None, stream=None, **kw):
+    def __init__(self, grid_rows: int, grid_cols: int, nccl_id: bytes | None = None, rank: int = 0):
+        self._c = ctypes.c_void_p()
+        if nccl_id is None:
+            _check(lib().lap_comm_create_virtual(grid_rows, grid_cols, ctypes.byref(self._c)))
+        else:
+            buf = (ctypes.c_uint8 * 128).from_buffer_copy(bytes(nccl_id).ljust(128, b"\0"))
+            _check(lib().lap_comm_create(buf, rank, grid_rows * grid_cols, grid_rows, grid_cols,
+                                         ctypes.byref(self._c)))
+        self.grid = (grid_rows, grid_cols)
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (ctypes.c_uint8 * 128)()
+        _check(lib().lap_nccl_unique_id(buf))
+        return bytes(buf)
+
+    def info(self):
+        v = [ctypes.c_int32() for _ in range(5)]
+        _check(lib().lap_comm_info(self._c, *[ctypes.byref(x) for x in v]))
+        return dict(zip(["rank", "nranks", "grid_rows", "grid_cols", "virtual"], [x.value for x in v]))
+
+    def close(self):
+        if getattr(self, "_c", None):
+            lib().lap_comm_free(self._c)
+            self._c = None
+
+
+def dist_index(n: int, nranks: int, rows) -> tuple:
+    """Host-only piece map of a sharded level (lap_dist_index)."""
+    rows = np.ascontiguousarray(rows, np.int64)
+    out = np.zeros(len(rows), np.int64)
+    S = ctypes.c_int64()
+    _check(lib().lap_dist_index(n, nranks, len(rows), _ptr(rows), _ptr(out), ctypes.byref(S)))
+    return out, S.value
+
+
+class Hierarchy:
+    """lap_setup(graph, params) -> hierarchy ; .solve(b) -> (x, iters, residual).
+    With comm=Comm(...), lap_setup_dist: the fine levels are sharded over the grid."""
+
+    def __init__(self, graph, params: lap_params | None = None, stream=None, comm: "Comm | None" = None, **kw):
         self.params = params if params is not None else lap_params_default(**kw)
         dev = hasattr(graph.row_ptr, "data_ptr") and getattr(graph.row_ptr, "is_cuda", False)
         if not dev:
@@ -142,8 +193,13 @@ class Hierarchy:
             self._keep = (graph.row_ptr, graph.col, graph.w)
         g = lap_graph(int(graph.n), _ptr(self._keep[0]), _ptr(self._keep[1]), _ptr(self._keep[2]), 1 if dev else 0)
         self._h = ctypes.c_void_p()
-        self.status = _check(lib().lap_setup(ctypes.byref(g), ctypes.byref(self.params), _stream(stream),
-                                             ctypes.byref(self._h)), allow=(LAP_ESTALL,))
+        self.comm = comm
+        if comm is None:
+            rc = lib().lap_setup(ctypes.byref(g), ctypes.byref(self.params), _stream(stream), ctypes.byref(self._h))
+        else:
+            rc = lib().lap_setup_dist(ctypes.byref(g), ctypes.byref(self.params), comm._c, _stream(stream),
+                                      ctypes.byref(self._h))
+        self.status = _check(rc, allow=(LAP_ESTALL,))
         self._keep = None
         self.n = int(graph.n)
 

@@ -1,0 +1,97 @@
+"""Sharded (2D edge partition) solve, on one GPU.
+
+lap_comm_create_virtual(pr, pc) holds every rank's shard of a pr x pc grid
+in this process and runs the collectives as device copies / fixed-order sums,
+so the whole sharded data path (piece map, 2D blocks, column allgather, row
+reduce-scatter, distributed restriction / prolongation, distributed PCG) runs
+through liblap.so on a single B200.  Contract (SURVEY §8(e) "Determinism"):
+the hierarchy is the single-GPU one; the solve agrees with the single-GPU
+solve up to rounding: true relative residual <= 1e-8, iterations within +-1,
+solution within 1e-6 relative.
+"""
+import numpy as np
+import pytest
+
+import lapgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1705_06266_b200 as P
+    from paper_1705_06266_b200 import build
+    build.build()
+    return P
+
+
+GRAPHS = {
+    "grid2d_37x29": lambda: lapgen.grid2d(37, 29),
+    "rmat12": lambda: lapgen.rmat(12),
+    "ba3000": lambda: lapgen.barabasi_albert(3000, 6),
+    "rand2000": lambda: lapgen.random_connected(2000, 6000, 3),
+    "star20000": lambda: lapgen.star(20000),
+    "grid3d_14": lambda: lapgen.grid3d(14),
+}
+GRIDS = [(1, 1), (1, 2), (2, 1), (2, 2), (2, 3), (3, 2), (2, 4)]
+
+
+@pytest.mark.parametrize("gname", list(GRAPHS))
+@pytest.mark.parametrize("grid", GRIDS, ids=[f"{a}x{b}" for a, b in GRIDS])
+def test_sharded_solve_matches_single_gpu(P, gname, grid):
+    g = GRAPHS[gname]()
+    b = lapgen.rhs(g.n, seed=5)
+    h1 = P.Hierarchy(g)
+    x1, it1, rr1, rc1 = h1.solve(b)
+    comm = P.Comm(*grid)
+    # replicate_nnz = 1: every level except the coarsest is sharded
+    hd = P.Hierarchy(g, comm=comm, replicate_nnz=1)
+    xd, itd, rrd, rcd = hd.solve(b)
+    assert rc1 == 0 and rcd == 0
+    assert rrd <= 1e-8, rrd
+    assert abs(itd - it1) <= 1, (itd, it1)
+    assert np.abs(xd - x1).max() <= 1e-6 * np.abs(x1).max()
+    hd.close()
+    comm.close()
+
+
+@pytest.mark.parametrize("rep", [0, 1 << 40])
+def test_replication_threshold(P, rep):
+    """Default threshold (nnz(L0)/(32P)) and 'replicate everything below level 0'."""
+    g = lapgen.rmat(12)
+    b = lapgen.rhs(g.n, seed=1)
+    x1, it1, _, _ = P.Hierarchy(g).solve(b)
+    comm = P.Comm(2, 2)
+    hd = P.Hierarchy(g, comm=comm, replicate_nnz=rep)
+    xd, itd, rrd, rc = hd.solve(b)
+    assert rc == 0 and rrd <= 1e-8 and abs(itd - it1) <= 1
+    assert np.abs(xd - x1).max() <= 1e-6 * np.abs(x1).max()
+    hd.close()
+    comm.close()
+
+
+def test_sharded_solve_device_buffers_and_oracle(P):
+    g = lapgen.grid2d(64, 64, "cfg1")
+    b = lapgen.rhs(g.n)
+    comm = P.Comm(2, 4)
+    hd = P.Hierarchy(g, comm=comm, replicate_nnz=1)
+    bt = torch.from_numpy(b).cuda()
+    xd, itd, rrd, rc = hd.solve(bt)
+    xo, ito, _, _ = oracle.Hierarchy(g).solve(b)
+    assert rc == 0 and rrd <= 1e-8 and abs(itd - ito) <= 1
+    xd = xd.cpu().numpy()
+    assert np.abs(xd - xo).max() <= 1e-6 * np.abs(xo).max()
+    assert abs(xd.mean()) <= 1e-10 * np.abs(xd).max()
+    hd.close()
+    comm.close()
+
+
+def test_comm_info_and_invalid(P):
+    c = P.Comm(2, 3)
+    assert c.info() == {"rank": 0, "nranks": 6, "grid_rows": 2, "grid_cols": 3, "virtual": 1}
+    c.close()
+    with pytest.raises(P.LapError):
+        P.Comm(5, 4)   # more than 16 ranks

@@ -134,6 +134,17 @@ def test_invalid_graphs_rejected(P):
     with pytest.raises(P.LapError) as e:
         P.Hierarchy(loop)
     assert e.value.code == P.LAP_EGRAPH
+    # pattern symmetric, weights not bitwise equal (w_01 != w_10)
+    asym_w = lapgen.Graph(3, np.array([0, 1, 3, 4]), np.array([1, 0, 2, 1], np.int32),
+                          np.array([1.0, np.nextafter(1.0, 2.0), 2.0, 2.0]))
+    with pytest.raises(P.LapError) as e:
+        P.Hierarchy(asym_w)
+    assert e.value.code == P.LAP_EGRAPH
+    # unsorted columns / duplicate entry
+    dup = lapgen.Graph(3, np.array([0, 2, 3, 4]), np.array([1, 1, 0, 0], np.int32), np.ones(4))
+    with pytest.raises(P.LapError) as e:
+        P.Hierarchy(dup)
+    assert e.value.code == P.LAP_EGRAPH
     disc = lapgen.csr_from_edges(4, [0, 2], [1, 3])
     with pytest.raises(P.LapError) as e:
         P.Hierarchy(disc)
