@@ -39,6 +39,7 @@ import lapgen  # noqa: E402
 
 CFG = 2
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+GRIDS = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}  # pr x pc process grids
 
 
 def peaks():
@@ -159,11 +160,21 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", init_method="env://")
-    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(device=dev)
+    # sharded solve (G1) over a pr x pc grid for N > 1 (or --shard at N = 1): the
+    # library's own NCCL communicators; torch.distributed only broadcasts the id
+    comm = None
+    grid = None
+    if world > 1 or args.shard:
+        grid = GRIDS.get(world, (1, world))
+        uid = [P.Comm.unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(uid, src=0)
+        comm = P.Comm(grid[0], grid[1], nccl_id=uid[0], rank=rank)
 
     g = lapgen.config(args.config)
     b = lapgen.rhs(g.n)
@@ -186,7 +197,7 @@ def run_gpu(args):
         row_ptr, col, w = rp_h.numpy(), col_h.numpy(), w_h.numpy()
 
     def step(graph, bb, xx):
-        h = P.Hierarchy(graph, stream=stream)
+        h = P.Hierarchy(graph, stream=stream, comm=comm)
         st0 = h.stats()
         _, it, rr, rc = h.solve(bb, xx, stream=stream)
         st = h.stats()
@@ -234,7 +245,7 @@ def run_gpu(args):
         for _ in range(max(1, min(args.steps, 3))):
             torch.cuda.synchronize()
             e0 = time.perf_counter()
-            he = P.Hierarchy(_HostG, stream=stream)
+            he = P.Hierarchy(_HostG, stream=stream, comm=comm)
             he.solve(b_h.numpy(), x_h.numpy(), stream=stream)
             torch.cuda.synchronize()
             e2e_ms.append((time.perf_counter() - e0) * 1e3)
@@ -261,6 +272,8 @@ def run_gpu(args):
             traffic = None
     clocks = clk.summary()
     if rank != 0:
+        if comm is not None:
+            comm.close()
         if world > 1:
             dist.destroy_process_group()
         return
@@ -296,12 +309,13 @@ def run_gpu(args):
         "warmup": args.warmup,
         "ms_per_step": ms,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (lapgen, seeded)",
         "config": {"workload": lapgen.CONFIG_NAMES[args.config], "n": g.n, "nnz_off": g.nnz,
-                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (2D sharding: next)",
+                   "parallelism": ("single GPU" if comm is None else
+                                   f"2D edge partition {grid[0]}x{grid[1]} of the fine levels (NCCL), coarse levels replicated"),
                    "l2": "inputs > L2: the level-0 CSR + SELL copy exceed the 126 MB L2; every SpMV re-streams them",
                    "levels": [[L["kind"], L["n"], L["nnz"]] for L in levels]},
         "iters": last["iters"], "rel_residual": dr,
@@ -322,7 +336,9 @@ def run_gpu(args):
         "clocks": clocks,
         "cpu_baseline": cpu,
     }
-    print(json.dumps(line))
+    emit(line)
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -370,20 +386,35 @@ def run_reference(args):
         tot_t += dt
         tot_e += e
     v = tot_e / tot_t
-    print(json.dumps({
+    emit({
         "impl": "reference",
         "metric": "SpMV edges/s over one setup + PCG/V-cycle solve to 1e-8 rel. residual",
         "value": v, "unit": "edges/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (lapgen, seeded)",
         "config": {"workload": lapgen.CONFIG_NAMES[args.config], "sample": f"{side}^3 3D grid, cfg-2 weights"},
         "cpu_baseline": {"value": v, "unit": "edges/s", "cores": 1, "kind": "oracle",
                          "sample": f"{side}^3 3D 7-pt grid, log-uniform w; full setup + solve per step"},
         "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }))
+    })
+
+
+_JSON_OUT = None
+
+
+def emit(line: dict):
+    """The one JSON line on the process's real stdout (libraries such as NCCL
+    may print to fd 1; everything else is redirected to stderr in main())."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 
 
 def main():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -391,6 +422,7 @@ def main():
     ap.add_argument("--impl", default="lap", choices=["lap", "reference"])
     ap.add_argument("--config", type=int, default=CFG)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--shard", action="store_true", help="sharded (NCCL 1x1 grid) path at N = 1")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -95,3 +95,20 @@ def test_comm_info_and_invalid(P):
     c.close()
     with pytest.raises(P.LapError):
         P.Comm(5, 4)   # more than 16 ranks
+
+
+def test_nccl_transport_single_rank(P):
+    """The NCCL communicator path (ncclCommInitRank + row/column splits,
+    ncclAllGather / ncclReduceScatter / ncclAllReduce) on a 1 x 1 grid."""
+    uid = P.Comm.unique_id()
+    comm = P.Comm(1, 1, nccl_id=uid, rank=0)
+    assert comm.info()["virtual"] == 0
+    g = lapgen.rmat(11)
+    b = lapgen.rhs(g.n, seed=2)
+    x1, it1, _, _ = P.Hierarchy(g).solve(b)
+    hd = P.Hierarchy(g, comm=comm, replicate_nnz=1)
+    xd, itd, rrd, rc = hd.solve(b)
+    assert rc == 0 and rrd <= 1e-8 and abs(itd - it1) <= 1
+    assert np.abs(xd - x1).max() <= 1e-6 * np.abs(x1).max()
+    hd.close()
+    comm.close()

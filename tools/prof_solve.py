@@ -26,7 +26,7 @@ torch.cuda.synchronize()
 torch.cuda.nvtx.range_pop()
 print("iters", it, "relres", rr, "solve_ms", h.stats()["solve_ms"])
 torch.cuda.nvtx.range_push("cheb")
-lv = h.first_agg_level()
+lv = int(os.environ.get("PROF_LEVEL", h.first_agg_level()))
 ms, by, ed = h.bench_op(1, lv, 5)
 torch.cuda.synchronize()
 torch.cuda.nvtx.range_pop()
