@@ -214,7 +214,8 @@ struct EpiArgs {
     double *y = nullptr;          // output (SPMV / RESID r / CHEB x_out)
     const double *b = nullptr;    // rhs (RESID / CHEB)
     double *dv = nullptr;         // Chebyshev direction (in/out)
-    const double *rs = nullptr;   // Lanczos: D^-1/2 (y_i = rs_i (L (rs o v))_i)
+    const double *rs = nullptr;   // Lanczos: D^-1/2 (y_i = rs_i (L (rs o v))_i - beta_prev vp_i)
+    const double *v = nullptr, *vp = nullptr, *lz = nullptr;  // Lanczos: v, v_prev, device scalars
     double c1 = 0, c2 = 0;        // CHEB: dv = c1 dv + c2 D^-1 r
     double *partials = nullptr;   // SPMV_DOT partial sums (one per block per bin)
 };

@@ -12,6 +12,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <ctime>
 
 #include "canon.cuh"
 #include "lap_internal.cuh"
@@ -485,11 +487,18 @@ __global__ void k_tv_init(int64_t n, uint64_t base, double *X) {
         X[t] = __dsub_rn(__dmul_rn(2.0, unit_from(mix64(base ^ (uint64_t)t))), 1.0);
 }
 
+// E_lo of a sweep's CanonSum instance from the bit pattern of max |x| (O-S11)
+__global__ void k_tv_elo(const unsigned long long *mxbits, int ew, int64_t K, int *elo) {
+    double mx = __longlong_as_double((long long)*mxbits);
+    int e_max = mx > 0.0 ? ew + ilogb(mx) + 2 : ew + 1;
+    *elo = canon_elo(e_max, K);
+}
 // one synchronous damped-Jacobi sweep on the 4 columns; warp per row
 template <int G>
 __global__ void k_tv_sweep(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                           const double *__restrict__ w, const double *__restrict__ d, int elo, double omega,
-                           const double *__restrict__ X, double *__restrict__ Xn) {
+                           const double *__restrict__ w, const double *__restrict__ d, const int *__restrict__ elo_p,
+                           double omega, const double *__restrict__ X, double *__restrict__ Xn) {
+    const int elo = *elo_p;
     GROUP_LOOP_BEGIN(G, n)
         i128 a0 = 0, a1 = 0, a2 = 0, a3 = 0;
         const int64_t kb = live ? row_ptr[i] : 0, ke = live ? row_ptr[i + 1] : 0;
@@ -589,7 +598,8 @@ __global__ void k_vote_init(int64_t n, int8_t *st, int32_t *idx, int32_t *votes)
 template <int G>
 __global__ void k_vote_round(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                              const double *__restrict__ S, double filt, const int8_t *__restrict__ st,
-                             int8_t *__restrict__ nst, int32_t *__restrict__ nidx, int32_t *__restrict__ votes) {
+                             const int32_t *__restrict__ idx, int8_t *__restrict__ nst, int32_t *__restrict__ nidx,
+                             int32_t *__restrict__ votes) {
     GROUP_LOOP_BEGIN(G, n)
         const bool act = live && st[i] == ST_UND;           // only Undecided act (O-R9)
         int br = -1;
@@ -610,13 +620,11 @@ __global__ void k_vote_round(int64_t n, const int64_t *__restrict__ row_ptr, con
             int32_t j2 = __shfl_xor_sync(0xffffffffu, bj, o);
             if (r2 > br || (r2 == br && (s2 > bs || (s2 == bs && j2 < bj)))) { br = r2; bs = s2; bj = j2; }
         }
-        if (act && gl == 0 && br >= 0) {
-            if (br == ST_SEED) {
-                nst[i] = ST_DEC;
-                nidx[i] = bj;
-            } else {
-                atomicAdd(&votes[bj], 1);
-            }
+        if (live && gl == 0) {  // every row writes its next state (no round-start copy needed)
+            bool dec = act && br == ST_SEED;
+            nst[i] = dec ? (int8_t)ST_DEC : st[i];
+            nidx[i] = dec ? bj : idx[i];
+            if (act && br == ST_UND) atomicAdd(&votes[bj], 1);
         }
     GROUP_LOOP_END
 }
@@ -668,36 +676,78 @@ __global__ void k_scale_by(int64_t n, double *v, const double *nrm2) {
 __global__ void k_hadamard(int64_t n, const double *a, const double *b, double *o) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) o[i] = a[i] * b[i];
 }
-// y = rs o y - beta_prev vprev  (sc[0] = alpha, sc[1] = beta^2 of previous step, sc[3]=stopped)
-__global__ void k_lz_a(int64_t n, double *y, const double *rs, const double *vp, const double *sc) {
-    if (sc[3] != 0.0) return;
-    double bp = sc[4];
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        y[i] = rs[i] * y[i] - bp * vp[i];
+// One Lanczos step is three launches: the SpMV with the E_LZ epilogue
+// (y = rs o (L u) - beta_prev v_prev and the partials of alpha = y.v), then
+// k_lz_mid (every block re-reduces the alpha partials in a fixed order,
+// y -= alpha v, partials of |y|^2), then k_lz_end (every block re-reduces
+// |y|^2, block 0 records alpha, beta and the breakdown test, all blocks
+// advance v_prev = v, v = y / beta, u = rs o v).  Scalars (device):
+// sc[0] alpha, sc[2] beta, sc[3] stopped, sc[4] beta_prev.
+__device__ __forceinline__ double fixed_sum(const double *__restrict__ part, int64_t np, double *sh) {
+    double acc = 0.0;
+    for (int64_t i = threadIdx.x; i < np; i += blockDim.x) acc += part[i];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) sh[wid] = acc;
+    __syncthreads();
+    if (wid == 0) {
+        double r = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+        if (lane == 0) sh[32] = r;
+    }
+    __syncthreads();
+    return sh[32];
 }
-__global__ void k_lz_b(int64_t n, double *y, const double *v, const double *sc) {
-    if (sc[3] != 0.0) return;
-    double a = sc[0];
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        y[i] -= a * v[i];
-}
-// record alpha/beta, test breakdown, advance (single thread)
-__global__ void k_lz_record(double *sc, double *alpha, double *beta, int *k, int step) {
-    if (sc[3] != 0.0) return;
-    double a = sc[0], b = sqrt(sc[1]);
-    alpha[*k] = a;
-    beta[*k] = b;
-    *k += 1;
-    sc[2] = b;
-    if (b <= 1e-14 * fabs(a)) sc[3] = 1.0;
-    sc[4] = b;
-}
-__global__ void k_lz_c(int64_t n, double *v, double *vp, const double *y, const double *sc) {
-    if (sc[3] != 0.0) return;
-    double b = sc[2];
+__global__ void __launch_bounds__(256) k_lz_mid(int64_t n, const double *__restrict__ part1, int64_t np1,
+                                                double *__restrict__ y, const double *__restrict__ v, double *sc,
+                                                double *__restrict__ part2) {
+    __shared__ double sh[33];
+    const double stopped = sc[3];
+    double alpha = fixed_sum(part1, np1, sh);
+    if (stopped != 0.0) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc[0] = alpha;
+    double acc = 0.0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        vp[i] = v[i];
-        v[i] = y[i] / b;
+        double t = y[i] - alpha * v[i];
+        y[i] = t;
+        acc += t * t;
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double r = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+        if (threadIdx.x == 0) part2[blockIdx.x] = r;
+    }
+}
+__global__ void __launch_bounds__(256) k_lz_end(int64_t n, const double *__restrict__ part2, int64_t np2,
+                                                const double *__restrict__ y, double *__restrict__ v,
+                                                double *__restrict__ vp, double *__restrict__ u,
+                                                const double *__restrict__ rs, double *sc, double *alpha_rec,
+                                                double *beta_rec, int *k) {
+    __shared__ double sh[33];
+    const double stopped = sc[3];
+    double b2 = fixed_sum(part2, np2, sh);
+    if (stopped != 0.0) return;
+    const double a = sc[0], b = sqrt(b2);
+    const bool stop = b <= 1e-14 * fabs(a);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        alpha_rec[*k] = a;
+        beta_rec[*k] = b;
+        *k += 1;
+        sc[2] = b;
+        sc[4] = b;
+        if (stop) sc[3] = 1.0;
+    }
+    if (stop) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double vi = v[i], vn = y[i] / b;
+        vp[i] = vi;
+        v[i] = vn;
+        u[i] = rs[i] * vn;
     }
 }
 // largest eigenvalue of the k x k tridiagonal by Sturm bisection (one thread)
@@ -729,7 +779,9 @@ __global__ void k_tridiag_max(const double *alpha, const double *beta, const int
 static double lanczos(lap_hierarchy *h, Level &L, int l, cudaStream_t s) {
     int64_t n = L.n;
     int steps = h->p.lanczos_steps;
-    DBuf<double> v(n, s), vp(n, s), y(n, s), u(n, s), rs(n, s), sc(8, s), al(64, s), be(64, s), lam(1, s);
+    const int64_t np1 = spmv_partial_slots(L), np2 = 296;
+    DBuf<double> v(n, s), vp(n, s), y(n, s), u(n, s), rs(n, s), sc(8, s), al(64, s), be(64, s), lam(1, s),
+        p1(np1, s), p2(np2, s);
     DBuf<int> k(1, s);
     LAP_CUDA(cudaMemsetAsync(vp.p, 0, sizeof(double) * n, s));
     LAP_CUDA(cudaMemsetAsync(sc.p, 0, sizeof(double) * 8, s));
@@ -739,18 +791,19 @@ static double lanczos(lap_hierarchy *h, Level &L, int l, cudaStream_t s) {
     k_lz_init<<<g, 256, 0, s>>>(n, base, L.sid, L.sd, v.p, rs.p); ++g_kl;
     dot(h, v.p, v.p, n, sc.p + 5, s);
     k_scale_by<<<g, 256, 0, s>>>(n, v.p, sc.p + 5); ++g_kl;
+    k_hadamard<<<g, 256, 0, s>>>(n, rs.p, v.p, u.p); ++g_kl;
     for (int j = 0; j < steps && j < 64; j++) {
-        k_hadamard<<<g, 256, 0, s>>>(n, rs.p, v.p, u.p); ++g_kl;
         EpiArgs a;
         a.x = u.p;
         a.y = y.p;
-        spmv_level(h, L, EPI_SPMV, a, s);
-        k_lz_a<<<g, 256, 0, s>>>(n, y.p, rs.p, vp.p, sc.p); ++g_kl;
-        dot(h, y.p, v.p, n, sc.p + 0, s);
-        k_lz_b<<<g, 256, 0, s>>>(n, y.p, v.p, sc.p); ++g_kl;
-        dot(h, y.p, y.p, n, sc.p + 1, s);
-        k_lz_record<<<1, 1, 0, s>>>(sc.p, al.p, be.p, k.p, j); ++g_kl;
-        k_lz_c<<<g, 256, 0, s>>>(n, v.p, vp.p, y.p, sc.p); ++g_kl;
+        a.rs = rs.p;
+        a.v = v.p;
+        a.vp = vp.p;
+        a.lz = sc.p;
+        a.partials = p1.p;
+        spmv_level(h, L, EPI_LANCZOS, a, s);
+        k_lz_mid<<<np2, 256, 0, s>>>(n, p1.p, np1, y.p, v.p, sc.p, p2.p); ++g_kl;
+        k_lz_end<<<np2, 256, 0, s>>>(n, p2.p, np2, y.p, v.p, vp.p, u.p, rs.p, sc.p, al.p, be.p, k.p); ++g_kl;
         LAP_CHECK_LAUNCH();
     }
     k_tridiag_max<<<1, 1, 0, s>>>(al.p, be.p, k.p, lam.p); ++g_kl;
@@ -950,10 +1003,15 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
     k_tv_init<<<grid_for(4 * n, 256, 148 * 16), 256, 0, s>>>(n, base, X.p); ++g_kl;
     LAP_CHECK_LAUNCH();
     int ew = ilogb_pos(L.maxw);
+    DBuf<unsigned long long> mxb(1, s);
+    DBuf<int> elo(1, s);
     for (int sw = 0; sw < p.tv_sweeps; sw++) {
-        double mx = max_abs(X.p, 4 * n, s);
-        int e_max = mx > 0.0 ? ew + ilogb_pos(mx) + 2 : ew + 1;
-        LAUNCH_G(G, k_tv_sweep, n, s, n, L.row_ptr, L.col, L.w, L.d, canon_elo(e_max, nnz), p.tv_omega, X.p, Xn.p);
+        // CanonSum instance of this sweep: e_max from the exact max |x| (O-S11), computed on
+        // the device (no host round trip)
+        LAP_CUDA(cudaMemsetAsync(mxb.p, 0, sizeof(unsigned long long), s));
+        k_max_abs<<<grid_for(4 * n, 256, 148 * 8), 256, 0, s>>>(X.p, 4 * n, mxb.p); ++g_kl;
+        k_tv_elo<<<1, 1, 0, s>>>(mxb.p, ew, nnz, elo.p); ++g_kl;
+        LAUNCH_G(G, k_tv_sweep, n, s, n, L.row_ptr, L.col, L.w, L.d, (const int *)elo.p, p.tv_omega, X.p, Xn.p);
         LAP_CHECK_LAUNCH();
         std::swap(X.p, Xn.p);
         h->cur.edges += nnz;
@@ -969,9 +1027,7 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
     k_vote_init<<<ge, 256, 0, s>>>(n, st.p, idx.p, votes.p); ++g_kl;
     for (int t = 1; t <= p.vote_rounds; t++) {
         double filt = ldexp(1.0, -t);
-        LAP_CUDA(cudaMemcpyAsync(nst.p, st.p, n, cudaMemcpyDeviceToDevice, s));
-        LAP_CUDA(cudaMemcpyAsync(nidx.p, idx.p, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
-        LAUNCH_G(G, k_vote_round, n, s, n, L.row_ptr, L.col, S.p, filt, st.p, nst.p, nidx.p, votes.p);
+        LAUNCH_G(G, k_vote_round, n, s, n, L.row_ptr, L.col, S.p, filt, st.p, idx.p, nst.p, nidx.p, votes.p);
         k_vote_promote<<<ge, 256, 0, s>>>(n, nst.p, votes.p, p.vote_threshold); ++g_kl;
         LAP_CHECK_LAUNCH();
         std::swap(st.p, nst.p);
@@ -1010,7 +1066,36 @@ static void galerkin(lap_hierarchy *h, Level &L, Level &N, cudaStream_t s) {
 // O-S9 hierarchy loop
 // =========================================================================
 
+// LAP_SETUP_TRACE=1: synchronise and print the elapsed time of every setup
+// phase to stderr (diagnostics only; changes the timing it reports on).
+struct SetupTrace {
+    bool on = false;
+    double t0 = 0;
+    cudaStream_t s = nullptr;
+    static double now() {
+        timespec ts;
+        clock_gettime(CLOCK_MONOTONIC, &ts);
+        return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+    }
+    explicit SetupTrace(cudaStream_t st) : s(st) {
+        const char *e = getenv("LAP_SETUP_TRACE");
+        on = e && e[0] == '1';
+        if (on) {
+            cudaStreamSynchronize(s);
+            t0 = now();
+        }
+    }
+    void mark(const char *what, int l) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        double t = now();
+        fprintf(stderr, "[lap setup] level %2d %-18s %9.3f ms\n", l, what, t - t0);
+        t0 = t;
+    }
+};
+
 void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
+    SetupTrace tr(s);
     const lap_params &p = h->p;
     int64_t n = g->n;
     h->n0 = n;
@@ -1053,8 +1138,11 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
             LAP_CHECK_LAUNCH();
         }
         if (d2h_scalar(flag.p, s)) throw Error{LAP_EGRAPH, "graph is not a valid symmetric positive-weight adjacency"};
+        tr.mark("validate", 0);
         if (!is_symmetric(n, nnz, rp, col, w, s)) throw Error{LAP_EGRAPH, "graph is not symmetric (w_ij != w_ji)"};
+        tr.mark("symmetry", 0);
         if (!is_connected(n, nnz, rp, col, s)) throw Error{LAP_EDISCONNECTED, "graph is disconnected"};
+        tr.mark("connectivity", 0);
     }
     // --- O-S1 level 0
     h->perm = (int64_t *)dalloc(sizeof(int64_t) * (size_t)n, s);
@@ -1085,6 +1173,7 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
             LAP_CHECK_LAUNCH();
         }
         csr_from_terms(n, cb, nnz, keys, vals, 0, 0, false, L0, s);
+        tr.mark("random order", 0);
     }
     rp_in.release();
     col_in.release();
@@ -1094,6 +1183,7 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
     for (int l = 0;; l++) {
         Level &L = h->lev[l];
         build_storage(h, l, s);
+        tr.mark("storage", l);
         if (L.n + L.nnz <= p.coarse_nnz || l == p.max_levels - 1 || l == 63) {     // O-R27
             L.kind = KIND_COARSEST;
             break;
@@ -1101,10 +1191,12 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
         if (p.elim_enable && !prev_elim) {                                          // O-R21
             DBuf<uint8_t> F;
             int64_t nF = elim_select(h, L, F, s);
+            tr.mark("elim select", l);
             if (20 * nF > L.n) {                                                    // O-R20
                 h->lev.emplace_back();
                 Level &L2 = h->lev[l];
                 build_elim_level(h, L2, F, nF, h->lev[l + 1], s);
+                tr.mark("schur", l);
                 prev_elim = true;
                 continue;
             }
@@ -1112,9 +1204,11 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
         // aggregation level
         L.kind = KIND_AGG;
         L.lambda = lanczos(h, L, l, s);
+        tr.mark("lanczos", l);
         DBuf<double> S(L.nnz, s);
         int64_t m = L.n;
         for (int attempt = 0; attempt < 2 && m == L.n; attempt++) m = aggregate_attempt(h, L, l, attempt, S, s);
+        tr.mark("strength+votes", l);
         if (m == L.n) {                                                             // stalled twice (O-R28)
             if (L.agg) dfree(L.agg, s);
             L.agg = nullptr;
@@ -1128,9 +1222,11 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
         h->lev.emplace_back();
         Level &L2 = h->lev[l];
         galerkin(h, L2, h->lev[l + 1], s);
+        tr.mark("galerkin", l);
         prev_elim = false;
     }
     coarse_pinv(h->lev.back(), s);
+    tr.mark("coarsest pinv", (int)h->lev.size() - 1);
 }
 
 }  // namespace lap

@@ -27,7 +27,7 @@ struct Csr {
 
 // ------------------------------------------------------------------ epilogues
 // Ax = sum_j w_ij x_j ; (L x)_i = d_i x_i - Ax  (L = D - A)
-enum { E_SPMV = EPI_SPMV, E_DOT = EPI_SPMV_DOT, E_RESID = EPI_RESID, E_CHEB = EPI_CHEB, E_CHEB0 = 5 };
+enum { E_SPMV = EPI_SPMV, E_DOT = EPI_SPMV_DOT, E_RESID = EPI_RESID, E_CHEB = EPI_CHEB, E_LZ = EPI_LANCZOS, E_CHEB0 = 5 };
 
 template <int EPI>
 __device__ __forceinline__ void apply_epi(int64_t i, double ax, const Csr &A, const EpiArgs &a, double &dacc) {
@@ -50,6 +50,10 @@ __device__ __forceinline__ void apply_epi(int64_t i, double ax, const Csr &A, co
         double dv = a.c2 * (r / A.d[i]);
         a.dv[i] = dv;
         a.y[i] = xi + dv;
+    } else if (EPI == E_LZ) {  // Lanczos on D^-1/2 L D^-1/2: y = rs o (L u) - beta_prev v_prev; alpha += y.v
+        double y = a.rs[i] * lx - a.lz[4] * a.vp[i];
+        a.y[i] = y;
+        dacc += y * a.v[i];
     }
 }
 
@@ -142,6 +146,10 @@ __device__ __forceinline__ void sell_slice(int64_t sl, int lane, int64_t nrows, 
             double dv = a.c2 * ((bi - lx) / di);
             a.dv[i] = dv;
             a.y[i] = xi + dv;
+        } else if (EPI == E_LZ) {
+            double y = a.rs[i] * lx - a.lz[4] * a.vp[i];
+            a.y[i] = y;
+            dacc += y * a.v[i];
         }
     }
 }
@@ -232,7 +240,7 @@ __global__ void __launch_bounds__(256, 4) k_spmv(int64_t nslices, int64_t nshort
         if (t < nslices) sell_slice<EPI>(t, lane, nshort, sp, ec, ew, A, a, a.x, dacc);
         else long_chunk<EPI>(t - nslices, lane, A, A.col, R, a, a.x, dacc);
     }
-    if (EPI == E_DOT) {
+    if (EPI == E_DOT || EPI == E_LZ) {
         double r = block_sum(dacc, sh);
         if (threadIdx.x == 0) partials[blockIdx.x] = r;
     }
@@ -264,7 +272,7 @@ __global__ void __launch_bounds__(1024, 1) k_spmv_smem(int64_t n, int64_t nslice
         if (t < nslices) sell_slice<EPI>(t, lane, nshort, sp, ec, ew, A, a, xs, dacc);
         else long_chunk<EPI>(t - nslices, lane, A, col16, R, a, xs, dacc);
     }
-    if (EPI == E_DOT) {
+    if (EPI == E_DOT || EPI == E_LZ) {
         double r = block_sum(dacc, sh);
         if (threadIdx.x == 0) partials[blockIdx.x] = r;
     }
@@ -316,6 +324,7 @@ void spmv_level(lap_hierarchy *h, const Level &L, EpiKind kind, const EpiArgs &a
     switch ((int)kind) {
         case E_SPMV: spmv_dispatch<E_SPMV>(h, L, a, s); break;
         case E_DOT: spmv_dispatch<E_DOT>(h, L, a, s); break;
+        case E_LZ: spmv_dispatch<E_LZ>(h, L, a, s); break;
         case E_RESID: spmv_dispatch<E_RESID>(h, L, a, s); break;
         case E_CHEB: spmv_dispatch<E_CHEB>(h, L, a, s); break;
         case E_CHEB0: spmv_dispatch<E_CHEB0>(h, L, a, s); break;

@@ -66,6 +66,9 @@ __global__ void k_class_key(int64_t n, const int64_t *rp, const uint64_t *key, u
                 unsigned m = __ballot_sync(am, c == q);
                 if (m && (threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(&cnt[q], (unsigned long long)__popc(m));
             }
+            // cnt[NCLASS]: entries of the short class (the SELL padding baseline)
+            unsigned sd = __reduce_add_sync(am, c == 0 ? (unsigned)dg : 0u);  // <= 32 * 64
+            if ((threadIdx.x & 31) == __ffs(am) - 1 && sd) atomicAdd(&cnt[NCLASS], (unsigned long long)sd);
         }
     }
 }
@@ -97,15 +100,6 @@ __global__ void k_sell_fill(int64_t nslots, int64_t nshort, const int64_t *srp, 
             ell_w[base + 32 * k] = real ? sw[a + k] : 0.0;
         }
     }
-}
-__global__ void k_short_nnz(int64_t n, const int64_t *rp, unsigned long long *out) {
-    unsigned long long acc = 0;
-    GRID_STRIDE(i, n) {
-        int64_t dg = rp[i + 1] - rp[i];
-        if (dg <= SHORT_MAX) acc += (unsigned long long)dg;
-    }
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
 }
 __global__ void k_inverse(int64_t n, const int32_t *sid, int32_t *spos) {
     GRID_STRIDE(p, n) spos[sid[p]] = (int32_t)p;
@@ -245,8 +239,8 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
         }
     }
     g_kl++;
-    DBuf<unsigned long long> cnt(NCLASS, s);
-    LAP_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long) * NCLASS, s));
+    DBuf<unsigned long long> cnt(NCLASS + 1, s);
+    LAP_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long) * (NCLASS + 1), s));
     DBuf<uint64_t> skey(n, s);
     L.sid = (int32_t *)dalloc(sizeof(int32_t) * n, s);
     L.spos = (int32_t *)dalloc(sizeof(int32_t) * n, s);
@@ -260,7 +254,7 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
         LAP_CHECK_LAUNCH();
     };
     sort_rows(0, cnt.p);
-    unsigned long long hc[NCLASS];
+    unsigned long long hc[NCLASS + 1];
     LAP_CUDA(cudaMemcpyAsync(hc, cnt.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
     LAP_CUDA(cudaStreamSynchronize(s));
     int64_t acc = 0;
@@ -271,27 +265,20 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
     // SELL-32 over the short class: degree-sort the short rows if natural order pads > 20%
     int64_t nshort = L.c_end[0];
     DBuf<int64_t> width;
+    int64_t sell_tot = 0;  // padded SELL entries = sum of the slice widths
     if (nshort > 0) {
         L.nslices = (nshort + 31) / 32;
         width.alloc(L.nslices + 1, s);
         DBuf<unsigned long long> pad(1, s);
-        DBuf<int64_t> rs(1, s);
+        const double rn = (double)hc[NCLASS];
         for (int pass = 0; pass < 2; pass++) {
             LAP_CUDA(cudaMemsetAsync(pad.p, 0, 8, s));
             LAP_CUDA(cudaMemsetAsync(width.p + L.nslices, 0, 8, s));
             k_slice_width<<<grid_for(L.nslices, 256, 148 * 8), 256, 0, s>>>(L.nslices, nshort, L.sid, L.row_ptr, width.p,
                                                                              pad.p);
             g_kl++;
-            unsigned long long padded = d2h(pad.p, s);
-            // actual entries of the short class: sum of degrees of the first nshort sorted rows
-            // (all short rows come first in the sort), computed from the class counts below
-            if (pass == 1) break;
-            DBuf<unsigned long long> real(1, s);
-            LAP_CUDA(cudaMemsetAsync(real.p, 0, 8, s));
-            k_short_nnz<<<g, 256, 0, s>>>(n, L.row_ptr, real.p);
-            g_kl++;
-            unsigned long long rn = d2h(real.p, s);
-            if ((double)padded <= 1.2 * (double)rn + 64.0) break;
+            sell_tot = (int64_t)d2h(pad.p, s);
+            if (pass == 1 || (double)sell_tot <= 1.2 * rn + 64.0) break;
             L.sell_sorted = true;
             sort_rows(1, nullptr);
         }
@@ -317,7 +304,7 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
     if (nshort > 0) {
         L.slice_ptr = (int64_t *)dalloc(sizeof(int64_t) * (L.nslices + 1), s);
         scan_excl(width.p, L.slice_ptr, L.nslices + 1, s);
-        int64_t tot = d2h(L.slice_ptr + L.nslices, s);
+        int64_t tot = sell_tot;
         L.ell_col = (int32_t *)dalloc(sizeof(int32_t) * (tot + 1), s);
         L.ell_w = (double *)dalloc(sizeof(double) * (tot + 1), s);
         k_sell_fill<<<grid_for(L.nslices * 32, 256, 148 * 8), 256, 0, s>>>(L.nslices * 32, nshort, L.srp, L.scol, L.sw, L.slice_ptr, L.ell_col,
@@ -328,7 +315,7 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
     // small dense-ish level: 16-bit column copies for the shared-memory-x SpMV
     if (n <= SMEM_X_MAX && L.nnz >= SMEM_X_MIN_DEG * n && L.nnz > 0) {
         L.smem_x = true;
-        int64_t tot = L.nslices ? d2h(L.slice_ptr + L.nslices, s) : 0;
+        int64_t tot = L.nslices ? sell_tot : 0;
         L.ell_col16 = (uint16_t *)dalloc(sizeof(uint16_t) * (tot + 1), s);
         L.scol16 = (uint16_t *)dalloc(sizeof(uint16_t) * (L.nnz + 1), s);
         if (tot) k_to_u16<<<grid_for(tot, 256, 148 * 8), 256, 0, s>>>(tot, L.ell_col, L.ell_col16);

@@ -1,0 +1,6 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 600 python tools/setup_trace.py 3 > gpurun_out/setup_trace3.log 2>&1
+timeout 600 python tools/setup_trace.py 2 > gpurun_out/setup_trace2.log 2>&1
+LAP_SETUP_TRACE=1 timeout 600 python tools/setup_trace.py 3 > gpurun_out/setup_trace3_phases.log 2>&1
+LAP_SETUP_TRACE=1 timeout 600 python tools/setup_trace.py 2 > gpurun_out/setup_trace2_phases.log 2>&1
