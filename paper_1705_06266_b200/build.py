@@ -22,7 +22,8 @@ UNITS = {"setup.cu": ["-fmad=false", "-prec-div=true", "-prec-sqrt=true"],
          "solve.cu": [],
          "storage.cu": [],
          "lap_api.cu": [],
-         "dist.cu": []}
+         "dist.cu": [],
+         "tail.cu": []}
 
 
 def _sources():

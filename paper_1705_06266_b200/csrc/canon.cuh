@@ -45,8 +45,23 @@ __host__ __device__ __forceinline__ int canon_elo(int e_max, int64_t K) {
     return e_max + bitlen_u64((uint64_t)K) - 125;
 }
 
-// q(t) = RNE(t * 2^-E_lo)
+// q(t) = RNE(t * 2^-E_lo), computed in fp64 without bit surgery: the power-of-
+// two scaling s = t * 2^-E_lo is exact (|s| < 2^126, and s is normal for any
+// finite t because E_lo is far below the exponent of the smallest term that
+// matters), rint() is round-half-even, and once |s| >= 2^53 s is already an
+// integer that splits exactly into hi * 2^64 + lo.  Same value as the integer
+// reference canon_q_bits below (and the oracle's), ~10 instructions instead of
+// ~200 (the int128 shift chain made the test-vector sweeps compute-bound).
 __device__ __forceinline__ i128 canon_q(double t, int elo) {
+    const double sc = scalbn(t, -elo);
+    if (fabs(sc) < 9007199254740992.0) return (i128)__double2ll_rn(sc);  // |s| < 2^53: RNE to an integer
+    const double hi = floor(sc * 0x1p-64);
+    const double lo = sc - hi * 0x1p64;                                   // exact, in [0, 2^64)
+    return (i128)__double2ll_rz(hi) * ((i128)1 << 64) + (i128)__double2ull_rz(lo);
+}
+
+// integer reference of canon_q (bit decomposition); kept for the self-check
+__device__ __forceinline__ i128 canon_q_bits(double t, int elo) {
     uint64_t bits = (uint64_t)__double_as_longlong(t);
     uint64_t mag = bits & 0x7FFFFFFFFFFFFFFFULL;
     if (mag == 0) return 0;

@@ -143,7 +143,7 @@ static void free_level(Level &L, cudaStream_t s) {
                   L.chunk_part, L.ell_col16, L.scol16,
                   L.agg_s, L.mem_ptr, L.members, L.cid_s, L.flist, L.ct_ptr_s, L.ct_f_s, L.ct_coef_s, L.fmap_s,
                   L.ct_crow, L.ct_cidx, L.ct_cslot, L.ct_ccnt, L.ct_cpart,
-                  L.pinv_s, L.b, L.x, L.x2, L.t, L.r, L.dv};
+                  L.pinv_s, L.dense, L.b, L.x, L.x2, L.t, L.r, L.dv};
     for (void *p : ps) dfree(p, s);
 }
 
@@ -297,6 +297,7 @@ lap_status lap_setup(const lap_graph *g, const lap_params *pp, void *stream, lap
         h->partials = (double *)lap::dalloc(8 * h->npartials, s);
         lap::build_hierarchy(h, g, s);
         lap::finalize_solve_structures(h, s);
+        lap::build_dense_tail(h, s);
         LAP_CUDA(cudaEventRecord(e1, s));
         LAP_CUDA(cudaStreamSynchronize(s));
         float ms = 0;

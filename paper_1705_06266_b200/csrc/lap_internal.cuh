@@ -95,6 +95,7 @@ constexpr int64_t SHORT_MAX = 64;
 constexpr int64_t HUB_CHUNK = 16384;  // class 2/3 boundary (storage grouping only)
 constexpr int64_t LCHUNK = 1024;      // long-row chunk (entries per warp work item)
 constexpr int64_t ELIM_SHORT = 32;    // elimination restriction: longer coarse lists are chunked
+constexpr int64_t DTAIL_MAX_N = 3072;  // the V-cycle below the first level this small is one dense operator (tail.cu)
 constexpr int64_t SMEM_X_MAX = 26624;   // levels with n <= this (208 KB of x) ...
 constexpr int64_t SMEM_X_MIN_DEG = 256; // ... and average degree >= this gather x from shared memory
 
@@ -157,6 +158,7 @@ struct Level {
     double *ct_cpart = nullptr;
     int32_t *fmap_s = nullptr;      // elim: coarse storage index of a C storage row, -1 for F
     double *pinv_s = nullptr;       // coarsest: L^+ in storage order
+    double *dense = nullptr;        // dense-tail level: M = [V(l, e_j)] (n x n, column-major; tail.cu)
     // Chebyshev constants (O-S6), host
     double cheb_theta = 0, cheb_delta = 0, cheb_sigma = 0;
     // solve work vectors (storage order, length n >= 1)
@@ -192,6 +194,7 @@ struct lap_hierarchy {
     // the whole PCG loop as resident graphs (WHILE conditional node, solve.cu)
     cudaGraphExec_t pcg_start = nullptr, pcg_resume = nullptr;
     void *pcg_counts = nullptr;
+    int dtail_level = -1;          // level whose V-cycle is the dense operator lev[].dense (tail.cu)
     // multi-GPU shards (dist.cu), NULL for a single-GPU hierarchy
     void *dist = nullptr;
     void *dist_owned = nullptr;
@@ -230,6 +233,9 @@ int64_t spmv_partial_slots(const Level &L);
 void vcycle(lap_hierarchy *h, int l, cudaStream_t s);   // x_l = V(l, b_l)
 void run_pcg(lap_hierarchy *h, double tol, int32_t *iters, double *relres, int *conv, cudaStream_t s);
 void capture_pcg(lap_hierarchy *h);
+// dense tail (tail.cu)
+void build_dense_tail(lap_hierarchy *h, cudaStream_t s);
+void launch_dense_gemv(const Level &L, const double *b, double *x, cudaStream_t s);
 // multi-GPU (dist.cu)
 void build_dist(lap_hierarchy *h, lap_comm *c, cudaStream_t s);
 void free_dist(lap_hierarchy *h);

@@ -106,22 +106,22 @@ __global__ void k_validate(int64_t n, const int64_t *__restrict__ row_ptr, const
 // An exact check with one radix sort instead of a binary search per entry
 // (which serialises on hub rows).
 template <int G>
-__global__ void k_sym_keys(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+__global__ void k_sym_keys(int64_t n, int cbits, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                            int32_t *__restrict__ rowof, uint64_t *__restrict__ tkey, int64_t *__restrict__ idx) {
     GROUP_LOOP_BEGIN(G, n)
     if (live)
         for (int64_t k = row_ptr[i] + gl; k < row_ptr[i + 1]; k += G) {
             rowof[k] = (int32_t)i;
-            tkey[k] = ((uint64_t)(uint32_t)col[k] << 32) | (uint64_t)i;
+            tkey[k] = ((uint64_t)(uint32_t)col[k] << cbits) | (uint64_t)i;
             idx[k] = k;
         }
     GROUP_LOOP_END
 }
-__global__ void k_sym_check(int64_t nnz, const int32_t *__restrict__ rowof, const int32_t *__restrict__ col,
+__global__ void k_sym_check(int64_t nnz, int cbits, const int32_t *__restrict__ rowof, const int32_t *__restrict__ col,
                             const double *__restrict__ w, const uint64_t *__restrict__ tkey,
                             const int64_t *__restrict__ idx, int *flag) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nnz; t += (int64_t)gridDim.x * blockDim.x) {
-        uint64_t want = ((uint64_t)(uint32_t)rowof[t] << 32) | (uint64_t)(uint32_t)col[t];
+        uint64_t want = ((uint64_t)(uint32_t)rowof[t] << cbits) | (uint64_t)(uint32_t)col[t];
         bool bad = tkey[t] != want;
         if (!bad && w) bad = __double_as_longlong(w[idx[t]]) != __double_as_longlong(w[t]);
         if (bad) atomicOr(flag, 1);
@@ -134,15 +134,16 @@ static bool is_symmetric(int64_t n, int64_t nnz, const int64_t *rp, const int32_
     DBuf<int32_t> rowof(nnz, s);
     DBuf<uint64_t> k1(nnz, s), k2(nnz, s);
     DBuf<int64_t> i1(nnz, s), i2(nnz, s);
-    LAUNCH_G(group_size(n, nnz), k_sym_keys, n, s, n, rp, col, rowof.p, k1.p, i1.p);
+    const int cbits = bitlen_u64((uint64_t)n);  // columns are validated < n before this check
+    LAUNCH_G(group_size(n, nnz), k_sym_keys, n, s, n, cbits, rp, col, rowof.p, k1.p, i1.p);
     size_t bytes = 0;
-    int end_bit = 32 + bitlen_u64((uint64_t)n);
+    int end_bit = 2 * cbits;
     LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k1.p, k2.p, i1.p, i2.p, nnz, 0, end_bit, s));
     DBuf<char> tmp((int64_t)bytes, s);
     LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, k1.p, k2.p, i1.p, i2.p, nnz, 0, end_bit, s)); ++g_kl;
     DBuf<int> flag(1, s);
     LAP_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
-    k_sym_check<<<grid_for(nnz, 256, 148 * 16), 256, 0, s>>>(nnz, rowof.p, col, w, k2.p, i2.p, flag.p); ++g_kl;
+    k_sym_check<<<grid_for(nnz, 256, 148 * 16), 256, 0, s>>>(nnz, cbits, rowof.p, col, w, k2.p, i2.p, flag.p); ++g_kl;
     LAP_CHECK_LAUNCH();
     return d2h_scalar(flag.p, s) == 0;
 }
@@ -548,7 +549,9 @@ __global__ void k_affinity(int64_t n, const int64_t *__restrict__ row_ptr, const
         const int64_t kb = live ? row_ptr[i] : 0, ke = live ? row_ptr[i + 1] : 0;
         for (int64_t k = kb + gl; k < ke; k += G) {
             int64_t j = col[k];
-            double xj[4] = {X[4 * j], X[4 * j + 1], X[4 * j + 2], X[4 * j + 3]};
+            const double2 *xj2 = reinterpret_cast<const double2 *>(X + 4 * j);  // 32-byte aligned rows
+            const double2 u0 = xj2[0], u1 = xj2[1];
+            double xj[4] = {u0.x, u0.y, u1.x, u1.y};
             double nj = dot4_rn(xj, xj);
             double g = dot4_rn(xi, xj);
             double num = __dmul_rn(g, g);

@@ -473,6 +473,13 @@ static inline unsigned eg(int64_t n) { return grid_for(n, 256, 148 * 8); }
 static void vcycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, cudaStream_t s) {
     Level &L = h->lev[l];
     int64_t n = L.n;
+    if (l == h->dtail_level && L.dense && b == L.b && xout == L.x) {  // V(l, b) = M_l b (tail.cu)
+        launch_dense_gemv(L, b, xout, s);
+        h->cur.launches++;
+        h->cur.bytes += 8 * n * n + 16 * n;
+        LAP_CHECK_LAUNCH();
+        return;
+    }
     if (L.kind == KIND_COARSEST) {
         launch_pdl(k_coarse_gemv, grid_for(n * 32, 256, 148), 256, s, n, L.pinv_s, b, xout);
         h->cur.launches++;
