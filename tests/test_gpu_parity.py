@@ -221,3 +221,28 @@ def test_storage_layout_validated_in_debug_mode(P):
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
                        cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)))
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("env", [{"LAP_DENSE_TAIL": "0"}, {"LAP_PDL": "0"}, {"LAP_DENSE_TAIL": "0", "LAP_PDL": "0"}],
+                         ids=["no-dense-tail", "no-pdl", "neither"])
+def test_solve_path_switches(P, env):
+    """The alternative solve paths (per-level kernels instead of the dense
+    tail operator, launches without programmatic dependent launch) give the
+    oracle's V-cycle and solution too (run in a subprocess: the switches are
+    read once per process)."""
+    import os
+    import subprocess
+    import sys
+    code = ("import numpy as np, lapgen, oracle, paper_1705_06266_b200 as P\n"
+            "for g in [lapgen.grid2d(64, 64), lapgen.rmat(12), lapgen.grid3d(16)]:\n"
+            "    h = P.Hierarchy(g); ho = oracle.Hierarchy(g)\n"
+            "    r = np.random.default_rng(1).standard_normal(g.n); r -= r.mean()\n"
+            "    z = h.vcycle(r); zo = ho.vcycle(0, r)\n"
+            "    assert np.abs(z - zo).max() <= 1e-9 * np.abs(zo).max()\n"
+            "    b = lapgen.rhs(g.n, seed=4); x, it, rr, rc = h.solve(b); xo, ito, _, _ = ho.solve(b)\n"
+            "    assert rc == 0 and rr <= 1e-8 and abs(it - ito) <= 1, (it, ito, rr)\n"
+            "print('ok')\n")
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, timeout=600,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
