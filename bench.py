@@ -65,11 +65,14 @@ class Clocks:
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, gpu_index: int, enabled: bool = True):
         self.idx = gpu_index
         self.p = None
+        self.enabled = enabled
 
     def __enter__(self):
+        if not self.enabled:
+            return self
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
                                        "--format=csv,noheader,nounits", "-lms", "100"],
@@ -197,13 +200,16 @@ def run_gpu(args):
         row_ptr, col, w = rp_h.numpy(), col_h.numpy(), w_h.numpy()
 
     def step(graph, bb, xx):
+        w0 = time.perf_counter()
         h = P.Hierarchy(graph, stream=stream, comm=comm)
+        w1 = time.perf_counter()
         st0 = h.stats()
         _, it, rr, rc = h.solve(bb, xx, stream=stream)
+        w2 = time.perf_counter()
         st = h.stats()
         out = dict(iters=it, relres=rr, rc=rc, setup_ms=st0["setup_ms"], solve_ms=st["solve_ms"],
                    launches=st0["kernel_launches"] + st["kernel_launches"], vcycles=st["vcycles"],
-                   solve_edges=st["spmv_edges"])
+                   solve_edges=st["spmv_edges"], wall_setup_ms=1e3 * (w1 - w0), wall_solve_ms=1e3 * (w2 - w1))
         return h, out
 
     with torch.cuda.stream(stream):
@@ -214,15 +220,17 @@ def run_gpu(args):
         if world > 1:
             dist.barrier()
         runs = []
-        with Clocks(local) as clk:
+        with Clocks(local, enabled=not args.no_clocks) as clk:
             t0 = torch.cuda.Event(enable_timing=True)
             t1 = torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             t0.record(stream)
             for _ in range(args.steps):
                 h, r = step(gd, b_d, x_d)
-                runs.append(r)
+                w3 = time.perf_counter()
                 h.close()
+                r["wall_free_ms"] = 1e3 * (time.perf_counter() - w3)
+                runs.append(r)
             t1.record(stream)
             torch.cuda.synchronize()
         total_ms = t0.elapsed_time(t1)
@@ -333,6 +341,8 @@ def run_gpu(args):
         "e2e": {"value": edges / (statistics.median(e2e_ms) * 1e-3), "unit": "edges/s",
                 "ms": statistics.median(e2e_ms), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": b.nbytes},
         "gpu_launches": int(sum(r["launches"] for r in runs)),
+        "step_breakdown_ms": {k: float(np.median([r[k] for r in runs])) for k in
+                              ["setup_ms", "solve_ms", "wall_setup_ms", "wall_solve_ms", "wall_free_ms"]},
         "clocks": clocks,
         "cpu_baseline": cpu,
     }
@@ -423,6 +433,7 @@ def main():
     ap.add_argument("--config", type=int, default=CFG)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--shard", action="store_true", help="sharded (NCCL 1x1 grid) path at N = 1")
+    ap.add_argument("--no-clocks", action="store_true", help="diagnostics: no nvidia-smi sampling")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

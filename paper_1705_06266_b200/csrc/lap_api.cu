@@ -3,6 +3,7 @@
 #include <cub/cub.cuh>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "lap_internal.cuh"
@@ -134,7 +135,10 @@ void finalize_solve_structures(lap_hierarchy *h, cudaStream_t s) {
         h->partials = (double *)dalloc(8 * np, s);
         h->npartials = np;
     }
-    LAP_CUDA(cudaMallocHost(&h->host_scal, 8 * 16));
+    // pageable (not pinned): every read of it is followed by a stream sync, and a
+    // cudaMallocHost / cudaFreeHost pair per hierarchy costs milliseconds
+    h->host_scal = (double *)calloc(16, sizeof(double));
+    if (!h->host_scal) throw Error{LAP_ENOMEM, "host scalars"};
 }
 
 static void free_level(Level &L, cudaStream_t s) {
@@ -368,7 +372,7 @@ void lap_free(lap_hierarchy *h) {
     void *ps[] = {h->perm, h->cmap, h->pb, h->px, h->pr, h->pz, h->pp, h->pq, h->scal, h->partials, h->stage_in,
                   h->stage_out};
     for (void *p : ps) lap::dfree(p, s);
-    if (h->host_scal) cudaFreeHost(h->host_scal);
+    free(h->host_scal);
     cudaStreamSynchronize(s);
     lap::vc_forget(h);
     delete h;

@@ -96,6 +96,7 @@ constexpr int64_t HUB_CHUNK = 16384;  // class 2/3 boundary (storage grouping on
 constexpr int64_t LCHUNK = 1024;      // long-row chunk (entries per warp work item)
 constexpr int64_t ELIM_SHORT = 32;    // elimination restriction: longer coarse lists are chunked
 constexpr int64_t DTAIL_MAX_N = 3072;  // the V-cycle below the first level this small is one dense operator (tail.cu)
+constexpr int64_t NB4_MAXNNZ = 0;      // default: batch width 8 everywhere (LAP_NB4_MAXNNZ overrides)
 constexpr int64_t SMEM_X_MAX = 26624;   // levels with n <= this (208 KB of x) ...
 constexpr int64_t SMEM_X_MIN_DEG = 256; // ... and average degree >= this gather x from shared memory
 
@@ -136,6 +137,7 @@ struct Level {
     double *ell_w = nullptr;        // padded entries: weight (0 for padding)
     bool sell_sorted = false;       // short rows degree-sorted
     bool smem_x = false;            // small dense-ish level: k_spmv_smem (x in shared memory, 16-bit columns)
+    int spmv_nb = 8;                // SELL batch width of k_spmv (8, or 4 for mid-size levels)
     uint16_t *ell_col16 = nullptr;  // smem_x: 16-bit copies of ell_col / scol
     uint16_t *scol16 = nullptr;
     int64_t nchunks = 0;            // LCHUNK chunks over the long rows [c_end[0], n)

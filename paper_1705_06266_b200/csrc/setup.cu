@@ -222,6 +222,42 @@ __global__ void k_terms_to_csr(int64_t U, const uint64_t *__restrict__ ukeys, co
     }
 }
 
+// CanonSum of segment u = terms v[off[u] .. off[u+1]) (sorted duplicates of key uk[u])
+constexpr int64_t SEG_LONG = 128;
+__global__ void k_seg_canon(int64_t U, const int64_t *__restrict__ off, const uint64_t *__restrict__ uk,
+                            const double *__restrict__ v, int cb, int elo, int32_t *__restrict__ col,
+                            double *__restrict__ w) {
+    const uint64_t mask = (1ULL << cb) - 1;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < U; u += (int64_t)gridDim.x * blockDim.x) {
+        col[u] = (int32_t)(uk[u] & mask);
+        const int64_t a = off[u], e = off[u + 1];
+        if (e - a > SEG_LONG) continue;  // k_seg_canon_long
+        i128 acc = 0;
+        for (int64_t t = a; t < e; t++) acc += canon_q(v[t], elo);
+        w[u] = canon_result(acc, elo);
+    }
+}
+__global__ void k_seg_canon_long(int64_t U, const int64_t *__restrict__ off, const double *__restrict__ v, int elo,
+                                 double *__restrict__ w) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t base = warp * 32; base < U; base += nwarps * 32) {  // a warp scans 32 segments ...
+        const int64_t u0 = base + lane;
+        const bool lng = u0 < U && off[u0 + 1] - off[u0] > SEG_LONG;
+        unsigned todo = __ballot_sync(0xffffffffu, lng);
+        while (todo) {  // ... and sums each long one cooperatively
+            const int j = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int64_t u = base + j, a = off[u], e = off[u + 1];
+            i128 acc = 0;
+            for (int64_t t = a + lane; t < e; t += 32) acc += canon_q(v[t], elo);
+            acc = warp_sum_i128(acc);
+            if (lane == 0) w[u] = canon_result(acc, elo);
+        }
+    }
+}
+
 __global__ void k_decode_cols(int64_t T, const uint64_t *__restrict__ k, uint64_t mask, int32_t *__restrict__ c) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < T; i += (int64_t)gridDim.x * blockDim.x)
         c[i] = (int32_t)(k[i] & mask);
@@ -286,24 +322,26 @@ static void csr_from_terms(int64_t nrows, int cb, int64_t T, DBuf<uint64_t> &key
     out.n = nrows;
     out.row_ptr = (int64_t *)dalloc(sizeof(int64_t) * (size_t)(nrows + 1), s);
     if (combine && T > 0) {
+        // duplicates of a key are one segment of the sorted terms: run-length
+        // encode the keys, then each segment's CanonSum is formed directly from
+        // the fp64 terms (thread per short segment, warp per long one)
         int elo = canon_elo(e_max, K);
-        DBuf<I128> q(T, s);
-        k_quantize<<<grid_for(T, 256, 148 * 16), 256, 0, s>>>(T, v2.p, elo, q.p); ++g_kl;
-        LAP_CHECK_LAUNCH();
-        v2.release();
         DBuf<uint64_t> uk(T, s);
-        DBuf<I128> uq(T, s);
-        DBuf<int64_t> nu(1, s);
+        DBuf<int64_t> cnt(T + 1, s), off(T + 1, s), nu(1, s);
         size_t bytes = 0;
-        LAP_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, bytes, k2.p, uk.p, q.p, uq.p, nu.p, I128Add(), T, s));
+        LAP_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, bytes, k2.p, uk.p, cnt.p, nu.p, T, s));
         DBuf<char> tmp((int64_t)bytes, s);
-        LAP_CUDA(cub::DeviceReduce::ReduceByKey(tmp.p, bytes, k2.p, uk.p, q.p, uq.p, nu.p, I128Add(), T, s)); ++g_kl;
+        LAP_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.p, bytes, k2.p, uk.p, cnt.p, nu.p, T, s)); ++g_kl;
         U = d2h_scalar(nu.p, s);
+        k2.release();
+        LAP_CUDA(cudaMemsetAsync(cnt.p + U, 0, sizeof(int64_t), s));
+        exclusive_scan_i64(cnt.p, off.p, U + 1, s);
         out.nnz = U;
         out.col = (int32_t *)dalloc(sizeof(int32_t) * (size_t)(U + 1), s);
         out.w = (double *)dalloc(sizeof(double) * (size_t)(U + 1), s);
         if (U > 0) {
-            k_terms_to_csr<<<grid_for(U, 256, 148 * 16), 256, 0, s>>>(U, uk.p, uq.p, cb, elo, out.col, out.w); ++g_kl;
+            k_seg_canon<<<grid_for(U, 256, 148 * 16), 256, 0, s>>>(U, off.p, uk.p, v2.p, cb, elo, out.col, out.w); ++g_kl;
+            k_seg_canon_long<<<grid_for(U, 256, 148 * 16), 256, 0, s>>>(U, off.p, v2.p, elo, out.w); ++g_kl;
             LAP_CHECK_LAUNCH();
         }
         k_row_ptr_from_keys<<<grid_for(nrows + 1, 256, 148 * 16), 256, 0, s>>>(nrows, U, uk.p, cb, out.row_ptr); ++g_kl;
@@ -567,20 +605,15 @@ __global__ void k_affinity(int64_t n, const int64_t *__restrict__ row_ptr, const
         if (live && gl == 0) M[i] = mx;
     GROUP_LOOP_END
 }
-// S_ij = C_ij / max(M_i, M_j), 0 if that max is 0 (O-R16); in place
-template <int G>
-__global__ void k_normalize(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                            const double *__restrict__ M, double *__restrict__ CS) {
-    GROUP_LOOP_BEGIN(G, n)
-    if (live) {
-        double mi = M[i];
-        for (int64_t k = row_ptr[i] + gl; k < row_ptr[i + 1]; k += G) {
-            double mj = M[col[k]];
-            double den = mi > mj ? mi : mj;
-            CS[k] = den > 0.0 ? __ddiv_rn(CS[k], den) : 0.0;
-        }
+// S_ij = C_ij / max(M_i, M_j), 0 if that max is 0 (O-R16); in place,
+// entry-parallel (hub rows do not serialise)
+__global__ void k_normalize(int64_t n, int64_t nnz, const int64_t *__restrict__ row_ptr,
+                            const int32_t *__restrict__ col, const double *__restrict__ M, double *__restrict__ CS) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+        const double mi = M[row_of(row_ptr, n, k)], mj = M[col[k]];
+        const double den = mi > mj ? mi : mj;
+        CS[k] = den > 0.0 ? __ddiv_rn(CS[k], den) : 0.0;
     }
-    GROUP_LOOP_END
 }
 
 // =========================================================================
@@ -1021,7 +1054,10 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
     }
     // affinity + normalisation
     LAUNCH_G(G, k_affinity, n, s, n, L.row_ptr, L.col, X.p, p.affinity_power, S.p, M.p);
-    LAUNCH_G(G, k_normalize, n, s, n, L.row_ptr, L.col, M.p, S.p);
+    if (nnz > 0) {
+        k_normalize<<<grid_for(nnz, 256, 148 * 16), 256, 0, s>>>(n, nnz, L.row_ptr, L.col, M.p, S.p);
+        ++g_kl;
+    }
     LAP_CHECK_LAUNCH();
     h->cur.edges += 2 * nnz;
     // voting rounds (Alg. 3)

@@ -93,7 +93,7 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
 // coarse levels are load balanced, and no class runs alone on a partly idle
 // GPU.  No fp64 atomics: per-chunk sums and the in-order combine are fixed, so
 // results are bitwise reproducible run to run.
-template <int EPI, class CT>
+template <int EPI, class CT, int NB = 8>
 __device__ __forceinline__ void sell_slice(int64_t sl, int lane, int64_t nrows, const int64_t *__restrict__ sp,
                                            const CT *__restrict__ ec, const double *__restrict__ ew, const Csr &A,
                                            const EpiArgs &a, const double *__restrict__ xg, double &dacc) {
@@ -112,18 +112,19 @@ __device__ __forceinline__ void sell_slice(int64_t sl, int lane, int64_t nrows, 
     // the short rows of grids and power-law tails)
     const int width = (int)((end - beg) >> 5);
     double acc0 = 0.0, acc1 = 0.0;
-    for (int q = 0; q < width; q += 8) {
-        int c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        double wv[8];
+    for (int q = 0; q < width; q += NB) {
+        int c[NB];
+        double wv[NB];
 #pragma unroll
-        for (int u = 0; u < 8; u++) {
+        for (int u = 0; u < NB; u++) {
+            c[u] = 0;
             if (q + u < width) {
                 c[u] = __ldg(&ec[beg + (int64_t)(q + u) * 32 + lane]);
                 wv[u] = __ldg(&ew[beg + (int64_t)(q + u) * 32 + lane]);
             }
         }
 #pragma unroll
-        for (int u = 0; u < 8; u += 2) {
+        for (int u = 0; u < NB; u += 2) {
             if (q + u < width) acc0 += wv[u] * xg[c[u]];
             if (q + u + 1 < width) acc1 += wv[u + 1] * xg[c[u + 1]];
         }
@@ -225,10 +226,14 @@ __device__ __forceinline__ void long_chunk(int64_t c, int lane, const Csr &A, co
     if (chunk_reduce(c, lane, A.rp, col, A.w, xg, R, i, ax) && lane == 0) apply_epi<EPI>(i, ax, A, a, dacc);
 }
 
-template <int EPI>
-__global__ void __launch_bounds__(256, 4) k_spmv(int64_t nslices, int64_t nshort, const int64_t *__restrict__ sp,
-                                              const int32_t *__restrict__ ec, const double *__restrict__ ew, Csr A,
-                                              LongRows R, EpiArgs a, double *__restrict__ partials) {
+// NB = SELL columns per batch: 8 (64 registers, 4 CTAs of 256 per SM) or 4 (48, 5 CTAs) for the
+// big levels, 4 (more resident warps, shorter per-warp slice chains) for mid-size ones
+template <int EPI, int NB>
+__global__ void __launch_bounds__(256, NB == 8 ? 4 : 5) k_spmv(int64_t nslices, int64_t nshort,
+                                                             const int64_t *__restrict__ sp,
+                                                             const int32_t *__restrict__ ec,
+                                                             const double *__restrict__ ew, Csr A, LongRows R,
+                                                             EpiArgs a, double *__restrict__ partials) {
     pdl_begin();
     __shared__ double sh[8];
     const int lane = threadIdx.x & 31;
@@ -237,7 +242,7 @@ __global__ void __launch_bounds__(256, 4) k_spmv(int64_t nslices, int64_t nshort
     const int64_t nitems = nslices + R.nchunks;
     double dacc = 0.0;
     for (int64_t t = warp; t < nitems; t += nwarps) {
-        if (t < nslices) sell_slice<EPI>(t, lane, nshort, sp, ec, ew, A, a, a.x, dacc);
+        if (t < nslices) sell_slice<EPI, int32_t, NB>(t, lane, nshort, sp, ec, ew, A, a, a.x, dacc);
         else long_chunk<EPI>(t - nslices, lane, A, A.col, R, a, a.x, dacc);
     }
     if (EPI == E_DOT || EPI == E_LZ) {
@@ -293,7 +298,8 @@ static int num_sms() {
 static unsigned spmv_grid(const Level &L) {
     if (L.smem_x) return (unsigned)num_sms();
     int64_t items = L.nslices + L.nchunks;
-    return grid_for(items * 32, 256, (int64_t)num_sms() * 4);  // one resident wave (4 CTAs of 256 per SM at 64 regs)
+    // one resident wave: 4 CTAs of 256 per SM at 64 registers (NB 8), 5 at NB 4 (48 registers)
+    return grid_for(items * 32, 256, (int64_t)num_sms() * (L.spmv_nb == 8 ? 4 : 5));
 }
 
 int64_t spmv_partial_slots(const Level &L) { return spmv_grid(L); }
@@ -313,8 +319,12 @@ static void spmv_dispatch(lap_hierarchy *h, const Level &L, const EpiArgs &a, cu
                         (const int64_t *)L.slice_ptr, (const uint16_t *)L.ell_col16, (const double *)L.ell_w, A,
                         (const uint16_t *)L.scol16, R, a, a.partials);
     } else {
-        launch_pdl(k_spmv<EPI>, spmv_grid(L), 256, s, L.nslices, L.c_end[0], (const int64_t *)L.slice_ptr,
-                   (const int32_t *)L.ell_col, (const double *)L.ell_w, A, R, a, a.partials);
+        if (L.spmv_nb == 8)
+            launch_pdl(k_spmv<EPI, 8>, spmv_grid(L), 256, s, L.nslices, L.c_end[0], (const int64_t *)L.slice_ptr,
+                       (const int32_t *)L.ell_col, (const double *)L.ell_w, A, R, a, a.partials);
+        else
+            launch_pdl(k_spmv<EPI, 4>, spmv_grid(L), 256, s, L.nslices, L.c_end[0], (const int64_t *)L.slice_ptr,
+                       (const int32_t *)L.ell_col, (const double *)L.ell_w, A, R, a, a.partials);
     }
     h->cur.launches++;
     LAP_CHECK_LAUNCH();

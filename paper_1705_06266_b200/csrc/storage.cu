@@ -323,6 +323,15 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
         g_kl += 2;
         LAP_CHECK_LAUNCH();
     }
+    // SELL batch width: 4 (more resident warps) for levels up to LAP_NB4_MAXNNZ nonzeros
+    {
+        static int64_t nb4 = -1;
+        if (nb4 < 0) {
+            const char *e = getenv("LAP_NB4_MAXNNZ");
+            nb4 = e ? atoll(e) : NB4_MAXNNZ;
+        }
+        L.spmv_nb = L.nnz <= nb4 ? 4 : 8;
+    }
     // long rows: LCHUNK-entry warp work items (solve.cu k_spmv)
     L.nchunks = build_chunks(L.srp, L.c_end[0], n - L.c_end[0], SHORT_MAX, &L.chunk_row, &L.chunk_idx, &L.chunk_slot,
                              &L.chunk_part, &L.chunk_cnt, s);
