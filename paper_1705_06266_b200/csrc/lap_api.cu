@@ -2,6 +2,7 @@
 // host-side sequencing of setup/solve.  No C++ exception crosses the ABI.
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -26,6 +27,15 @@ bool debug_sync() {
         v = (e && e[0] == '1') ? 1 : 0;
     }
     return v == 1;
+}
+
+int group_shift() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("LAP_GSHIFT");
+        v = e ? std::max(0, std::min(5, atoi(e))) : 0;
+    }
+    return v;
 }
 
 bool pdl_enabled() {

@@ -96,7 +96,7 @@ constexpr int64_t HUB_CHUNK = 16384;  // class 2/3 boundary (storage grouping on
 constexpr int64_t LCHUNK = 1024;      // long-row chunk (entries per warp work item)
 constexpr int64_t ELIM_SHORT = 32;    // elimination restriction: longer coarse lists are chunked
 constexpr int64_t DTAIL_MAX_N = 3072;  // the V-cycle below the first level this small is one dense operator (tail.cu)
-constexpr int64_t NB4_MAXNNZ = 0;      // default: batch width 8 everywhere (LAP_NB4_MAXNNZ overrides)
+constexpr int64_t NB4_MIN_NNZ = 4000000;  // SELL batch width 4 for levels this big with avg degree <= 8
 constexpr int64_t SMEM_X_MAX = 26624;   // levels with n <= this (208 KB of x) ...
 constexpr int64_t SMEM_X_MIN_DEG = 256; // ... and average degree >= this gather x from shared memory
 
@@ -109,6 +109,7 @@ struct Level {
     double *w = nullptr;
     double *d = nullptr;
     double maxw = 0.0;
+    int32_t *rowof = nullptr;       // setup only: row of every stored entry (not owned)
     // aggregation (logical)
     double lambda = 0.0;
     int64_t m = 0;
@@ -281,13 +282,18 @@ __device__ __forceinline__ T grp_sum(T v) {
     for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
+int group_shift();  // LAP_GSHIFT (lap_api.cu): experiments with narrower groups
 inline int group_size(int64_t n, int64_t nnz) {
     double avg = n > 0 ? (double)nnz / (double)n : 0.0;
-    return avg <= 4.0 ? 4 : avg <= 8.0 ? 8 : avg <= 16.0 ? 16 : 32;
+    int g = avg <= 4.0 ? 4 : avg <= 8.0 ? 8 : avg <= 16.0 ? 16 : 32;
+    g >>= group_shift();
+    return g < 1 ? 1 : g;
 }
 #define LAUNCH_G(G, kern, rows, s, ...)                                                                 \
     do {                                                                                                \
         switch (G) {                                                                                    \
+            case 1: kern<1><<<grid_for((rows) * 1, 256, 148 * 16), 256, 0, s>>>(__VA_ARGS__); break;    \
+            case 2: kern<2><<<grid_for((rows) * 2, 256, 148 * 16), 256, 0, s>>>(__VA_ARGS__); break;    \
             case 4: kern<4><<<grid_for((rows) * 4, 256, 148 * 16), 256, 0, s>>>(__VA_ARGS__); break;    \
             case 8: kern<8><<<grid_for((rows) * 8, 256, 148 * 16), 256, 0, s>>>(__VA_ARGS__); break;    \
             case 16: kern<16><<<grid_for((rows) * 16, 256, 148 * 16), 256, 0, s>>>(__VA_ARGS__); break; \

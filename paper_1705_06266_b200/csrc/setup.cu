@@ -101,6 +101,14 @@ __global__ void k_validate(int64_t n, const int64_t *__restrict__ row_ptr, const
     GROUP_LOOP_END
 }
 
+template <int G>
+__global__ void k_rowof(int64_t n, const int64_t *__restrict__ row_ptr, int32_t *__restrict__ rowof) {
+    GROUP_LOOP_BEGIN(G, n)
+    if (live)
+        for (int64_t k = row_ptr[i] + gl; k < row_ptr[i + 1]; k += G) rowof[k] = (int32_t)i;
+    GROUP_LOOP_END
+}
+
 // Symmetry (w_ij == w_ji bitwise): the transposed entry list, sorted
 // by (col, row), must equal the CSR list in (row, col) order entry for entry.
 // An exact check with one radix sort instead of a binary search per entry
@@ -452,13 +460,13 @@ __global__ void k_fmap(int64_t n, const uint8_t *F, const int64_t *cpos, const i
 // The multiset of terms is the method's; their order is irrelevant (sorted
 // and summed with CanonSum), so hub C rows no longer serialise the build.
 // L_CC entries: every stored (i, j) with i, j both in C -> ((fmap_i << cb) | fmap_j, w)
-__global__ void __launch_bounds__(256) k_schur_cc_emit(int64_t n, int64_t nnz, const int64_t *__restrict__ row_ptr,
+__global__ void __launch_bounds__(256) k_schur_cc_emit(int64_t n, int64_t nnz, const int32_t *__restrict__ rowof,
                                                        const int32_t *__restrict__ col, const double *__restrict__ w,
                                                        const uint8_t *__restrict__ F, const int32_t *__restrict__ fmap,
                                                        int cb, unsigned long long *cursor, uint64_t *__restrict__ keys,
                                                        double *__restrict__ vals) {
     int64_t i = 0;
-    ENTRY_EMIT_LOOP(nnz, cursor, (i = row_of(row_ptr, n, t), take = !F[i] && !F[col[t]]),
+    ENTRY_EMIT_LOOP(nnz, cursor, (i = rowof[t], take = !F[i] && !F[col[t]]),
                     (keys[p] = ((uint64_t)fmap[i] << cb) | (uint64_t)fmap[col[t]], vals[p] = w[t]))
 }
 __global__ void k_schur_f_count(int64_t nF, const int32_t *__restrict__ fid, const int64_t *__restrict__ row_ptr,
@@ -607,10 +615,10 @@ __global__ void k_affinity(int64_t n, const int64_t *__restrict__ row_ptr, const
 }
 // S_ij = C_ij / max(M_i, M_j), 0 if that max is 0 (O-R16); in place,
 // entry-parallel (hub rows do not serialise)
-__global__ void k_normalize(int64_t n, int64_t nnz, const int64_t *__restrict__ row_ptr,
+__global__ void k_normalize(int64_t n, int64_t nnz, const int32_t *__restrict__ rowof,
                             const int32_t *__restrict__ col, const double *__restrict__ M, double *__restrict__ CS) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
-        const double mi = M[row_of(row_ptr, n, k)], mj = M[col[k]];
+        const double mi = M[rowof[k]], mj = M[col[k]];
         const double den = mi > mj ? mi : mj;
         CS[k] = den > 0.0 ? __ddiv_rn(CS[k], den) : 0.0;
     }
@@ -683,14 +691,14 @@ __global__ void k_agg_ids(int64_t n, const int8_t *st, const int32_t *idx, const
 
 // Galerkin terms: every stored (i, j, w) with a = agg_i != b = agg_j
 // becomes ((a << cb) | b, w); entry-parallel, so hub rows do not serialise.
-__global__ void __launch_bounds__(256) k_gal_emit(int64_t n, int64_t nnz, const int64_t *__restrict__ row_ptr,
+__global__ void __launch_bounds__(256) k_gal_emit(int64_t n, int64_t nnz, const int32_t *__restrict__ rowof,
                                                   const int32_t *__restrict__ col, const double *__restrict__ w,
                                                   const int32_t *__restrict__ agg, int cb,
                                                   unsigned long long *cursor, uint64_t *__restrict__ keys,
                                                   double *__restrict__ vals) {
     uint64_t a = 0, bb = 0;
     ENTRY_EMIT_LOOP(nnz, cursor,
-                    (a = (uint64_t)agg[row_of(row_ptr, n, t)], bb = (uint64_t)agg[col[t]], take = a != bb),
+                    (a = (uint64_t)agg[rowof[t]], bb = (uint64_t)agg[col[t]], take = a != bb),
                     (keys[p] = (a << cb) | bb, vals[p] = w[t]))
 }
 
@@ -1002,7 +1010,7 @@ static void build_elim_level(lap_hierarchy *h, Level &L, const DBuf<uint8_t> &F,
     DBuf<unsigned long long> cur(1, s);
     LAP_CUDA(cudaMemsetAsync(cur.p, 0, sizeof(unsigned long long), s));
     if (L.nnz > 0) {
-        k_schur_cc_emit<<<grid_for(L.nnz, 256, 148 * 16), 256, 0, s>>>(n, L.nnz, L.row_ptr, L.col, L.w, F.p, L.fmap,
+        k_schur_cc_emit<<<grid_for(L.nnz, 256, 148 * 16), 256, 0, s>>>(n, L.nnz, L.rowof, L.col, L.w, F.p, L.fmap,
                                                                       cb, cur.p, keys.p, vals.p); ++g_kl;
         LAP_CHECK_LAUNCH();
     }
@@ -1055,7 +1063,7 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
     // affinity + normalisation
     LAUNCH_G(G, k_affinity, n, s, n, L.row_ptr, L.col, X.p, p.affinity_power, S.p, M.p);
     if (nnz > 0) {
-        k_normalize<<<grid_for(nnz, 256, 148 * 16), 256, 0, s>>>(n, nnz, L.row_ptr, L.col, M.p, S.p);
+        k_normalize<<<grid_for(nnz, 256, 148 * 16), 256, 0, s>>>(n, nnz, L.rowof, L.col, M.p, S.p);
         ++g_kl;
     }
     LAP_CHECK_LAUNCH();
@@ -1092,7 +1100,7 @@ static void galerkin(lap_hierarchy *h, Level &L, Level &N, cudaStream_t s) {
     DBuf<unsigned long long> cur(1, s);
     LAP_CUDA(cudaMemsetAsync(cur.p, 0, sizeof(unsigned long long), s));
     if (nnz > 0) {
-        k_gal_emit<<<grid_for(nnz, 256, 148 * 16), 256, 0, s>>>(n, nnz, L.row_ptr, L.col, L.w, L.agg, cb, cur.p, keys.p,
+        k_gal_emit<<<grid_for(nnz, 256, 148 * 16), 256, 0, s>>>(n, nnz, L.rowof, L.col, L.w, L.agg, cb, cur.p, keys.p,
                                                                 vals.p); ++g_kl;
         LAP_CHECK_LAUNCH();
     }
@@ -1223,6 +1231,9 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
         Level &L = h->lev[l];
         build_storage(h, l, s);
         tr.mark("storage", l);
+        DBuf<int32_t> rowof(L.nnz, s);  // row of every stored entry (entry-parallel setup kernels)
+        if (L.nnz > 0) LAUNCH_G(group_size(L.n, L.nnz), k_rowof, L.n, s, L.n, L.row_ptr, rowof.p);
+        L.rowof = rowof.p;
         if (L.n + L.nnz <= p.coarse_nnz || l == p.max_levels - 1 || l == 63) {     // O-R27
             L.kind = KIND_COARSEST;
             break;

@@ -323,14 +323,13 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
         g_kl += 2;
         LAP_CHECK_LAUNCH();
     }
-    // SELL batch width: 4 (more resident warps) for levels up to LAP_NB4_MAXNNZ nonzeros
+    // SELL batch width: 4 (5 instead of 4 resident CTAs per SM) for big, low-degree
+    // levels (3D grid level 0: 47.3 -> 44.2 us per Chebyshev step), 8 elsewhere
+    // (a mid-size level got slower at 4); LAP_NB4_MAXNNZ=x forces 4 for nnz <= x
     {
-        static int64_t nb4 = -1;
-        if (nb4 < 0) {
-            const char *e = getenv("LAP_NB4_MAXNNZ");
-            nb4 = e ? atoll(e) : NB4_MAXNNZ;
-        }
-        L.spmv_nb = L.nnz <= nb4 ? 4 : 8;
+        const char *e = getenv("LAP_NB4_MAXNNZ");
+        if (e) L.spmv_nb = L.nnz <= atoll(e) ? 4 : 8;
+        else L.spmv_nb = (L.nnz >= NB4_MIN_NNZ && L.nnz <= 8 * n) ? 4 : 8;
     }
     // long rows: LCHUNK-entry warp work items (solve.cu k_spmv)
     L.nchunks = build_chunks(L.srp, L.c_end[0], n - L.c_end[0], SHORT_MAX, &L.chunk_row, &L.chunk_idx, &L.chunk_slot,
