@@ -283,9 +283,14 @@ __device__ __forceinline__ T grp_sum(T v) {
     return v;
 }
 int group_shift();  // LAP_GSHIFT (lap_api.cu): experiments with narrower groups
-inline int group_size(int64_t n, int64_t nnz) {
+// Lanes per row.  all_short: the level has no row longer than SHORT_MAX
+// (known once its storage is built), so narrow groups cannot serialise a hub
+// and the per-row group reductions become the cost (3D grid: setup 24 -> 21
+// ms at one lane per row); with hubs keep G near the average degree.
+inline int group_size(int64_t n, int64_t nnz, bool all_short = false) {
     double avg = n > 0 ? (double)nnz / (double)n : 0.0;
-    int g = avg <= 4.0 ? 4 : avg <= 8.0 ? 8 : avg <= 16.0 ? 16 : 32;
+    int g = all_short ? (avg <= 8.0 ? 1 : avg <= 16.0 ? 2 : 4)
+                      : (avg <= 4.0 ? 4 : avg <= 8.0 ? 8 : avg <= 16.0 ? 16 : 32);
     g >>= group_shift();
     return g < 1 ? 1 : g;
 }

@@ -212,6 +212,39 @@ static bool is_connected(int64_t n, int64_t nnz, const int64_t *row_ptr, const i
     return d2h_scalar(c.p, s) == 1;
 }
 
+// LAP_SETUP_TRACE=1: synchronise and print the elapsed time of every setup
+// phase to stderr (diagnostics only; changes the timing it reports on).
+struct SetupTrace {
+    bool on = false;
+    double t0 = 0;
+    cudaStream_t s = nullptr;
+    static double now() {
+        timespec ts;
+        clock_gettime(CLOCK_MONOTONIC, &ts);
+        return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+    }
+    explicit SetupTrace(cudaStream_t st) : s(st) {
+        const char *e = getenv("LAP_SETUP_TRACE");
+        on = e && e[0] == '1';
+        if (on) {
+            cudaStreamSynchronize(s);
+            t0 = now();
+        }
+    }
+    void mark(const char *what, int l) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        double t = now();
+        fprintf(stderr, "[lap setup] level %2d %-18s %9.3f ms\n", l, what, t - t0);
+        t0 = t;
+    }
+};
+
+static SetupTrace *g_tr = nullptr;
+static void tmark(const char *what) {
+    if (g_tr) g_tr->mark(what, -1);
+}
+
 // =========================================================================
 // generic: sorted (row,col) terms -> CSR with canonical sums
 // =========================================================================
@@ -245,24 +278,43 @@ __global__ void k_seg_canon(int64_t U, const int64_t *__restrict__ off, const ui
         w[u] = canon_result(acc, elo);
     }
 }
-__global__ void k_seg_canon_long(int64_t U, const int64_t *__restrict__ off, const double *__restrict__ v, int elo,
-                                 double *__restrict__ w) {
+// long segments (> SEG_LONG terms; a dense coarse Galerkin has pairs of big
+// aggregates with millions of terms): SEG_CHUNK-term warp chunks with int128
+// partials, combined exactly per segment (integer addition: order-free)
+constexpr int64_t SEG_CHUNK = 4096;
+__global__ void k_seg_nchunks(int64_t U, const int64_t *__restrict__ off, int64_t *__restrict__ nch) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < U; u += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t len = off[u + 1] - off[u];
+        nch[u] = len > SEG_LONG ? (len + SEG_CHUNK - 1) / SEG_CHUNK : 0;
+    }
+}
+__global__ void k_seg_chunk_map(int64_t U, const int64_t *__restrict__ cfirst, int32_t *__restrict__ cseg) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < U; u += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t c = cfirst[u]; c < cfirst[u + 1]; c++) cseg[c] = (int32_t)u;
+}
+__global__ void k_seg_chunk_sum(int64_t C, const int32_t *__restrict__ cseg, const int64_t *__restrict__ cfirst,
+                                const int64_t *__restrict__ off, const double *__restrict__ v, int elo,
+                                I128 *__restrict__ part) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t base = warp * 32; base < U; base += nwarps * 32) {  // a warp scans 32 segments ...
-        const int64_t u0 = base + lane;
-        const bool lng = u0 < U && off[u0 + 1] - off[u0] > SEG_LONG;
-        unsigned todo = __ballot_sync(0xffffffffu, lng);
-        while (todo) {  // ... and sums each long one cooperatively
-            const int j = __ffs(todo) - 1;
-            todo &= todo - 1;
-            const int64_t u = base + j, a = off[u], e = off[u + 1];
-            i128 acc = 0;
-            for (int64_t t = a + lane; t < e; t += 32) acc += canon_q(v[t], elo);
-            acc = warp_sum_i128(acc);
-            if (lane == 0) w[u] = canon_result(acc, elo);
-        }
+    for (int64_t c = warp; c < C; c += nwarps) {
+        const int64_t u = cseg[c], j = c - cfirst[u];
+        const int64_t a = off[u] + j * SEG_CHUNK, e = min(off[u + 1], a + SEG_CHUNK);
+        i128 acc = 0;
+        for (int64_t t = a + lane; t < e; t += 32) acc += canon_q(v[t], elo);
+        acc = warp_sum_i128(acc);
+        if (lane == 0) part[c] = to_I128(acc);
+    }
+}
+__global__ void k_seg_long_finish(int64_t U, const int64_t *__restrict__ cfirst, const I128 *__restrict__ part,
+                                  int elo, double *__restrict__ w) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < U; u += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c0 = cfirst[u], c1 = cfirst[u + 1];
+        if (c0 == c1) continue;
+        i128 acc = 0;
+        for (int64_t c = c0; c < c1; c++) acc += from_I128(part[c]);
+        w[u] = canon_result(acc, elo);
     }
 }
 
@@ -326,6 +378,7 @@ static void csr_from_terms(int64_t nrows, int cb, int64_t T, DBuf<uint64_t> &key
     }
     keys.release();
     vals.release();
+    tmark("  terms: sort");
     int64_t U = T;
     out.n = nrows;
     out.row_ptr = (int64_t *)dalloc(sizeof(int64_t) * (size_t)(nrows + 1), s);
@@ -342,16 +395,32 @@ static void csr_from_terms(int64_t nrows, int cb, int64_t T, DBuf<uint64_t> &key
         LAP_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.p, bytes, k2.p, uk.p, cnt.p, nu.p, T, s)); ++g_kl;
         U = d2h_scalar(nu.p, s);
         k2.release();
+        tmark("  terms: rle");
         LAP_CUDA(cudaMemsetAsync(cnt.p + U, 0, sizeof(int64_t), s));
         exclusive_scan_i64(cnt.p, off.p, U + 1, s);
         out.nnz = U;
         out.col = (int32_t *)dalloc(sizeof(int32_t) * (size_t)(U + 1), s);
         out.w = (double *)dalloc(sizeof(double) * (size_t)(U + 1), s);
+        tmark("  terms: offsets");
         if (U > 0) {
             k_seg_canon<<<grid_for(U, 256, 148 * 16), 256, 0, s>>>(U, off.p, uk.p, v2.p, cb, elo, out.col, out.w); ++g_kl;
-            k_seg_canon_long<<<grid_for(U, 256, 148 * 16), 256, 0, s>>>(U, off.p, v2.p, elo, out.w); ++g_kl;
+            tmark("  terms: short segs");
+            DBuf<int64_t> nch(U + 1, s), cfirst(U + 1, s);
+            LAP_CUDA(cudaMemsetAsync(nch.p + U, 0, sizeof(int64_t), s));
+            k_seg_nchunks<<<grid_for(U, 256, 148 * 16), 256, 0, s>>>(U, off.p, nch.p); ++g_kl;
+            exclusive_scan_i64(nch.p, cfirst.p, U + 1, s);
+            const int64_t C = d2h_scalar(cfirst.p + U, s);
+            if (C > 0) {
+                DBuf<int32_t> cseg(C, s);
+                DBuf<I128> part(C, s);
+                k_seg_chunk_map<<<grid_for(U, 256, 148 * 16), 256, 0, s>>>(U, cfirst.p, cseg.p); ++g_kl;
+                k_seg_chunk_sum<<<grid_for(C * 32, 256, 148 * 16), 256, 0, s>>>(C, cseg.p, cfirst.p, off.p, v2.p, elo,
+                                                                              part.p); ++g_kl;
+                k_seg_long_finish<<<grid_for(U, 256, 148 * 16), 256, 0, s>>>(U, cfirst.p, part.p, elo, out.w); ++g_kl;
+            }
             LAP_CHECK_LAUNCH();
         }
+        tmark("  terms: canon sums");
         k_row_ptr_from_keys<<<grid_for(nrows + 1, 256, 148 * 16), 256, 0, s>>>(nrows, U, uk.p, cb, out.row_ptr); ++g_kl;
         LAP_CHECK_LAUNCH();
     } else {
@@ -367,6 +436,7 @@ static void csr_from_terms(int64_t nrows, int cb, int64_t T, DBuf<uint64_t> &key
     }
     out.d = (double *)dalloc(sizeof(double) * (size_t)(nrows > 0 ? nrows : 1), s);
     row_sums(nrows, out.nnz, out.row_ptr, out.w, out.d, &out.maxw, s);
+    tmark("  terms: row sums");
 }
 
 // =========================================================================
@@ -563,15 +633,16 @@ __global__ void k_tv_sweep(int64_t n, const int64_t *__restrict__ row_ptr, const
         a1 = grp_sum_i128<G>(a1);
         a2 = grp_sum_i128<G>(a2);
         a3 = grp_sum_i128<G>(a3);
-        if (live && gl < 4) {
-            i128 a = gl == 0 ? a0 : gl == 1 ? a1 : gl == 2 ? a2 : a3;
-            double sk = canon_result(a, elo);
-            double di = d[i];
-            double xi = X[4 * i + gl];
-            double r = __dsub_rn(__dmul_rn(di, xi), sk);
-            double q = __ddiv_rn(r, di);
-            Xn[4 * i + gl] = __dsub_rn(xi, __dmul_rn(omega, q));
-        }
+        if (live)
+            for (int cq = gl; cq < 4; cq += G) {  // every lane holds all four sums
+                i128 a = cq == 0 ? a0 : cq == 1 ? a1 : cq == 2 ? a2 : a3;
+                double sk = canon_result(a, elo);
+                double di = d[i];
+                double xi = X[4 * i + cq];
+                double r = __dsub_rn(__dmul_rn(di, xi), sk);
+                double q = __ddiv_rn(r, di);
+                Xn[4 * i + cq] = __dsub_rn(xi, __dmul_rn(omega, q));
+            }
     GROUP_LOOP_END
 }
 
@@ -997,7 +1068,7 @@ static void build_elim_level(lap_hierarchy *h, Level &L, const DBuf<uint8_t> &F,
     k_fmap<<<g, 256, 0, s>>>(n, F.p, cpos.p, fpos.p, L.fmap, L.cid, L.fid); ++g_kl;
     LAP_CHECK_LAUNCH();
     // terms of the Schur complement: L_CC entries (entry-parallel), fill from the F rows
-    const int G = group_size(n, L.nnz);
+    const int G = group_size(n, L.nnz, L.c_end[0] == L.n);
     DBuf<int64_t> fcnt(nF + 1, s), foff(nF + 1, s);
     LAP_CUDA(cudaMemsetAsync(fcnt.p, 0, sizeof(int64_t) * (nF + 1), s));
     k_schur_f_count<<<grid_for(nF, 256, 148 * 16), 256, 0, s>>>(nF, L.fid, L.row_ptr, fcnt.p); ++g_kl;
@@ -1040,7 +1111,7 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
     int64_t n = L.n, nnz = L.nnz;
     const lap_params &p = h->p;
     unsigned ge = grid_for(n, 256, 148 * 16);
-    const int G = group_size(n, nnz);
+    const int G = group_size(n, nnz, L.c_end[0] == L.n);
     // test vectors
     DBuf<double> X(4 * n, s), Xn(4 * n, s), M(n, s);
     uint64_t base = mix64(salt_of(p.seed, 3) ^ (uint64_t)(2 * l + attempt));
@@ -1060,6 +1131,7 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
         std::swap(X.p, Xn.p);
         h->cur.edges += nnz;
     }
+    tmark("  test vectors");
     // affinity + normalisation
     LAUNCH_G(G, k_affinity, n, s, n, L.row_ptr, L.col, X.p, p.affinity_power, S.p, M.p);
     if (nnz > 0) {
@@ -1068,6 +1140,7 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
     }
     LAP_CHECK_LAUNCH();
     h->cur.edges += 2 * nnz;
+    tmark("  affinity");
     // voting rounds (Alg. 3)
     DBuf<int8_t> st(n, s), nst(n, s);
     DBuf<int32_t> idx(n, s), nidx(n, s), votes(n, s);
@@ -1081,6 +1154,7 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
         std::swap(idx.p, nidx.p);
         h->cur.edges += nnz;
     }
+    tmark("  votes");
     // renumber roots by ascending id (O-R15)
     DBuf<int64_t> flag(n + 1, s), rid(n + 1, s);
     LAP_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int64_t) * (n + 1), s));
@@ -1105,6 +1179,7 @@ static void galerkin(lap_hierarchy *h, Level &L, Level &N, cudaStream_t s) {
         LAP_CHECK_LAUNCH();
     }
     int64_t T = (int64_t)d2h_scalar(cur.p, s);
+    tmark("  galerkin emit");
     csr_from_terms(m, cb, T, keys, vals, ilogb_pos(L.maxw) + 1, L.nnz, true, N, s);
     h->cur.edges += L.nnz;
 }
@@ -1113,36 +1188,12 @@ static void galerkin(lap_hierarchy *h, Level &L, Level &N, cudaStream_t s) {
 // O-S9 hierarchy loop
 // =========================================================================
 
-// LAP_SETUP_TRACE=1: synchronise and print the elapsed time of every setup
-// phase to stderr (diagnostics only; changes the timing it reports on).
-struct SetupTrace {
-    bool on = false;
-    double t0 = 0;
-    cudaStream_t s = nullptr;
-    static double now() {
-        timespec ts;
-        clock_gettime(CLOCK_MONOTONIC, &ts);
-        return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
-    }
-    explicit SetupTrace(cudaStream_t st) : s(st) {
-        const char *e = getenv("LAP_SETUP_TRACE");
-        on = e && e[0] == '1';
-        if (on) {
-            cudaStreamSynchronize(s);
-            t0 = now();
-        }
-    }
-    void mark(const char *what, int l) {
-        if (!on) return;
-        cudaStreamSynchronize(s);
-        double t = now();
-        fprintf(stderr, "[lap setup] level %2d %-18s %9.3f ms\n", l, what, t - t0);
-        t0 = t;
-    }
-};
-
 void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
     SetupTrace tr(s);
+    g_tr = tr.on ? &tr : nullptr;
+    struct Reset {
+        ~Reset() { g_tr = nullptr; }
+    } reset_tr;
     const lap_params &p = h->p;
     int64_t n = g->n;
     h->n0 = n;
@@ -1232,7 +1283,7 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
         build_storage(h, l, s);
         tr.mark("storage", l);
         DBuf<int32_t> rowof(L.nnz, s);  // row of every stored entry (entry-parallel setup kernels)
-        if (L.nnz > 0) LAUNCH_G(group_size(L.n, L.nnz), k_rowof, L.n, s, L.n, L.row_ptr, rowof.p);
+        if (L.nnz > 0) LAUNCH_G(group_size(L.n, L.nnz, L.c_end[0] == L.n), k_rowof, L.n, s, L.n, L.row_ptr, rowof.p);
         L.rowof = rowof.p;
         if (L.n + L.nnz <= p.coarse_nnz || l == p.max_levels - 1 || l == 63) {     // O-R27
             L.kind = KIND_COARSEST;

@@ -1,0 +1,7 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "not full_size" > gpurun_out/pytest_quick.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_quick.log
+timeout 300 python tools/prof_solve.py 2 > gpurun_out/p2.log 2>&1 && \
+timeout 900 ncu --nvtx --nvtx-include "setup/" --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_setup2.csv python tools/prof_solve.py 2 > gpurun_out/ncu_setup2.log 2>&1
+for k in 2 3 4; do timeout 600 python tools/setup_trace.py $k > gpurun_out/setup_trace$k.log 2>&1; done
+timeout 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "full_size" > gpurun_out/pytest_full.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_full.log
