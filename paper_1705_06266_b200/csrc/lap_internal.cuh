@@ -94,6 +94,7 @@ constexpr int NCLASS = 4;
 constexpr int64_t SHORT_MAX = 64;
 constexpr int64_t HUB_CHUNK = 16384;  // class 2/3 boundary (storage grouping only)
 constexpr int64_t LCHUNK = 1024;      // long-row chunk (entries per warp work item)
+constexpr int64_t SETUP_LONG = 4096;   // setup row kernels: longer rows go to LCHUNK warp chunks
 constexpr int64_t ELIM_SHORT = 32;    // elimination restriction: longer coarse lists are chunked
 constexpr int64_t DTAIL_MAX_N = 3072;  // the V-cycle below the first level this small is one dense operator (tail.cu)
 constexpr int64_t NB4_MIN_NNZ = 4000000;  // SELL batch width 4 for levels this big with avg degree <= 8

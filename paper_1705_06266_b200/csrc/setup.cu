@@ -618,7 +618,9 @@ __global__ void k_tv_sweep(int64_t n, const int64_t *__restrict__ row_ptr, const
     const int elo = *elo_p;
     GROUP_LOOP_BEGIN(G, n)
         i128 a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-        const int64_t kb = live ? row_ptr[i] : 0, ke = live ? row_ptr[i + 1] : 0;
+        const int64_t kb0 = live ? row_ptr[i] : 0, ke0 = live ? row_ptr[i + 1] : 0;
+        const bool skip = ke0 - kb0 > SETUP_LONG;  // long rows: k_tv_chunk
+        const int64_t kb = skip ? 0 : kb0, ke = skip ? 0 : ke0;
         for (int64_t k = kb + gl; k < ke; k += G) {
             int64_t j = col[k];
             double wk = w[k];
@@ -633,7 +635,7 @@ __global__ void k_tv_sweep(int64_t n, const int64_t *__restrict__ row_ptr, const
         a1 = grp_sum_i128<G>(a1);
         a2 = grp_sum_i128<G>(a2);
         a3 = grp_sum_i128<G>(a3);
-        if (live)
+        if (live && !skip)
             for (int cq = gl; cq < 4; cq += G) {  // every lane holds all four sums
                 i128 a = cq == 0 ? a0 : cq == 1 ? a1 : cq == 2 ? a2 : a3;
                 double sk = canon_result(a, elo);
@@ -646,6 +648,59 @@ __global__ void k_tv_sweep(int64_t n, const int64_t *__restrict__ row_ptr, const
     GROUP_LOOP_END
 }
 
+// rows longer than SETUP_LONG (hubs, up to ~10^6 entries at cfg 5): LCHUNK-entry
+// warp chunks of the four int128 sums; the last chunk of a row to arrive adds
+// the row's partials (exact integer sums: any order) and applies the update
+__global__ void k_tv_chunk(int64_t nchunks, const int32_t *__restrict__ crow, const int32_t *__restrict__ cidx,
+                           const int32_t *__restrict__ cslot, int32_t *__restrict__ ccnt, I128 *__restrict__ part,
+                           const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                           const double *__restrict__ w, const double *__restrict__ d, const int *__restrict__ elo_p,
+                           double omega, const double *__restrict__ X, double *__restrict__ Xn) {
+    const int elo = *elo_p;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = warp; c < nchunks; c += nwarps) {
+        const int64_t i = crow[c], j = cidx[c], rb = row_ptr[i], re = row_ptr[i + 1];
+        const int64_t b = rb + j * LCHUNK, e = min(re, b + LCHUNK);
+        i128 a[4] = {0, 0, 0, 0};
+        for (int64_t k = b + lane; k < e; k += 32) {
+            const double wk = w[k];
+            const double2 *xj = reinterpret_cast<const double2 *>(X + 4 * (int64_t)col[k]);
+            const double2 u = xj[0], v = xj[1];
+            a[0] += canon_q(__dmul_rn(wk, u.x), elo);
+            a[1] += canon_q(__dmul_rn(wk, u.y), elo);
+            a[2] += canon_q(__dmul_rn(wk, v.x), elo);
+            a[3] += canon_q(__dmul_rn(wk, v.y), elo);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) a[q] = warp_sum_i128(a[q]);
+        const int nch = (int)((re - rb + LCHUNK - 1) / LCHUNK);
+        int last = 0;
+        if (lane == 0) {
+            for (int q = 0; q < 4; q++) part[4 * c + q] = to_I128(a[q]);
+            __threadfence();
+            last = atomicAdd(&ccnt[cslot[c]], 1) == nch - 1;
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (!last) continue;
+        __threadfence();
+        if (lane < 4) {
+            i128 t = 0;
+            for (int64_t q = c - j; q < c - j + nch; q++) {  // L2 reads: other SMs wrote them
+                I128 pv;
+                pv.lo = __ldcg(&part[4 * q + lane].lo);
+                pv.hi = __ldcg(&part[4 * q + lane].hi);
+                t += from_I128(pv);
+            }
+            const double sk = canon_result(t, elo), di = d[i], xi = X[4 * i + lane];
+            const double r = __dsub_rn(__dmul_rn(di, xi), sk);
+            Xn[4 * i + lane] = __dsub_rn(xi, __dmul_rn(omega, __ddiv_rn(r, di)));
+        }
+        if (lane == 0) ccnt[cslot[c]] = 0;
+    }
+}
+
 __device__ __forceinline__ double dot4_rn(const double *a, const double *b) {
     double s = __dmul_rn(a[0], b[0]);
     s = __dadd_rn(s, __dmul_rn(a[1], b[1]));
@@ -654,6 +709,41 @@ __device__ __forceinline__ double dot4_rn(const double *a, const double *b) {
     return s;
 }
 
+// C_ij of one stored entry (O-R5): fixed k-order, no FMA
+__device__ __forceinline__ double affinity_of(const double *__restrict__ X, int64_t i, int64_t j, int power) {
+    const double2 *xi2 = reinterpret_cast<const double2 *>(X + 4 * i), *xj2 = reinterpret_cast<const double2 *>(X + 4 * j);
+    const double2 a0 = xi2[0], a1 = xi2[1], b0 = xj2[0], b1 = xj2[1];
+    double xi[4] = {a0.x, a0.y, a1.x, a1.y}, xj[4] = {b0.x, b0.y, b1.x, b1.y};
+    double ni = dot4_rn(xi, xi), nj = dot4_rn(xj, xj), g = dot4_rn(xi, xj);
+    double num = __dmul_rn(g, g);
+    double den = power == 2 ? __dmul_rn(__dmul_rn(ni, ni), __dmul_rn(nj, nj)) : __dmul_rn(ni, nj);
+    return den > 0.0 ? __ddiv_rn(num, den) : 0.0;
+}
+// long rows (deg > SETUP_LONG), entry-parallel over their chunks: C, and the row
+// max M_i as an atomic max of the bit pattern (non-negative doubles order like
+// their bits; max is exact and order-free)
+__global__ void k_affinity_long(int64_t nchunks, const int32_t *__restrict__ crow, const int32_t *__restrict__ cidx,
+                                const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                                const double *__restrict__ X, int power, double *__restrict__ C,
+                                unsigned long long *__restrict__ Mbits) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = warp; c < nchunks; c += nwarps) {
+        const int64_t i = crow[c], b = row_ptr[i] + (int64_t)cidx[c] * LCHUNK, e = min(row_ptr[i + 1], b + LCHUNK);
+        double mx = 0.0;
+        for (int64_t k = b + lane; k < e; k += 32) {
+            double cv = affinity_of(X, i, col[k], power);
+            C[k] = cv;
+            mx = cv > mx ? cv : mx;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            double t = __shfl_xor_sync(0xffffffffu, mx, o);
+            mx = t > mx ? t : mx;
+        }
+        if (lane == 0) atomicMax(&Mbits[i], (unsigned long long)__double_as_longlong(mx));
+    }
+}
 // C_ij (O-R5) and row max M_i; warp per row
 template <int G>
 __global__ void k_affinity(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
@@ -663,7 +753,9 @@ __global__ void k_affinity(int64_t n, const int64_t *__restrict__ row_ptr, const
         double xi[4] = {X[4 * ii], X[4 * ii + 1], X[4 * ii + 2], X[4 * ii + 3]};
         double ni = dot4_rn(xi, xi);
         double mx = 0.0;
-        const int64_t kb = live ? row_ptr[i] : 0, ke = live ? row_ptr[i + 1] : 0;
+        const int64_t kb0 = live ? row_ptr[i] : 0, ke0 = live ? row_ptr[i + 1] : 0;
+        const bool skip = ke0 - kb0 > SETUP_LONG;  // long rows: k_affinity_long
+        const int64_t kb = skip ? 0 : kb0, ke = skip ? 0 : ke0;
         for (int64_t k = kb + gl; k < ke; k += G) {
             int64_t j = col[k];
             const double2 *xj2 = reinterpret_cast<const double2 *>(X + 4 * j);  // 32-byte aligned rows
@@ -681,7 +773,7 @@ __global__ void k_affinity(int64_t n, const int64_t *__restrict__ row_ptr, const
             double t = __shfl_xor_sync(0xffffffffu, mx, o);
             mx = t > mx ? t : mx;
         }
-        if (live && gl == 0) M[i] = mx;
+        if (live && gl == 0 && !skip) M[i] = mx;
     GROUP_LOOP_END
 }
 // S_ij = C_ij / max(M_i, M_j), 0 if that max is 0 (O-R16); in place,
@@ -1120,6 +1212,19 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
     int ew = ilogb_pos(L.maxw);
     DBuf<unsigned long long> mxb(1, s);
     DBuf<int> elo(1, s);
+    // long rows (deg > SETUP_LONG): LCHUNK warp chunks (logical CSR)
+    int32_t *lc_row = nullptr, *lc_idx = nullptr, *lc_slot = nullptr, *lc_cnt = nullptr;
+    double *lc_dummy = nullptr;
+    const int64_t nlc = L.c_end[0] == L.n ? 0
+                        : build_chunks(L.row_ptr, 0, n, SETUP_LONG, &lc_row, &lc_idx, &lc_slot, &lc_dummy, &lc_cnt, s);
+    struct FreeLc {
+        void *p[5];
+        cudaStream_t s;
+        ~FreeLc() {
+            for (void *q : p) dfree(q, s);
+        }
+    } free_lc{{lc_row, lc_idx, lc_slot, lc_cnt, lc_dummy}, s};
+    DBuf<I128> lc_part(4 * (nlc > 0 ? nlc : 1), s);
     for (int sw = 0; sw < p.tv_sweeps; sw++) {
         // CanonSum instance of this sweep: e_max from the exact max |x| (O-S11), computed on
         // the device (no host round trip)
@@ -1127,13 +1232,26 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
         k_max_abs<<<grid_for(4 * n, 256, 148 * 8), 256, 0, s>>>(X.p, 4 * n, mxb.p); ++g_kl;
         k_tv_elo<<<1, 1, 0, s>>>(mxb.p, ew, nnz, elo.p); ++g_kl;
         LAUNCH_G(G, k_tv_sweep, n, s, n, L.row_ptr, L.col, L.w, L.d, (const int *)elo.p, p.tv_omega, X.p, Xn.p);
+        if (nlc > 0) {
+            k_tv_chunk<<<grid_for(nlc * 32, 256, 148 * 16), 256, 0, s>>>(nlc, lc_row, lc_idx, lc_slot, lc_cnt, lc_part.p,
+                                                                         L.row_ptr, L.col, L.w, L.d, elo.p,
+                                                                         p.tv_omega, X.p, Xn.p);
+            ++g_kl;
+        }
         LAP_CHECK_LAUNCH();
         std::swap(X.p, Xn.p);
         h->cur.edges += nnz;
     }
     tmark("  test vectors");
     // affinity + normalisation
+    if (nlc > 0) LAP_CUDA(cudaMemsetAsync(M.p, 0, sizeof(double) * n, s));
     LAUNCH_G(G, k_affinity, n, s, n, L.row_ptr, L.col, X.p, p.affinity_power, S.p, M.p);
+    if (nlc > 0) {
+        k_affinity_long<<<grid_for(nlc * 32, 256, 148 * 16), 256, 0, s>>>(nlc, lc_row, lc_idx, L.row_ptr, L.col, X.p,
+                                                                          p.affinity_power, S.p,
+                                                                          (unsigned long long *)M.p);
+        ++g_kl;
+    }
     if (nnz > 0) {
         k_normalize<<<grid_for(nnz, 256, 148 * 16), 256, 0, s>>>(n, nnz, L.rowof, L.col, M.p, S.p);
         ++g_kl;

@@ -24,6 +24,11 @@
 
 namespace lap {
 
+static bool getenv_flag_off(const char *name) {
+    const char *e = getenv(name);
+    return e && e[0] == '0';
+}
+
 template <class T>
 static T d2h(const T *p, cudaStream_t s) {
     T v;
@@ -299,6 +304,23 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
         k_storage_fill<<<grid_for(L.nnz, 256, 148 * 16), 256, 0, s>>>(n, L.nnz, L.sid, L.spos, L.row_ptr, L.col, L.w,
                                                                       L.srp, L.scol, L.sw);
         g_kl++;
+        // each storage row in ascending STORAGE column order: the u-th column of
+        // consecutive rows of a SELL slice then point the same way (-z, -y, -x, +x,
+        // ... on a grid-like level), so one gather instruction touches few lines
+        // instead of one line per lane (the L1 tag rate bounds these gathers)
+        if (L.nnz < ((int64_t)1 << 31) && n < ((int64_t)1 << 31) && !getenv_flag_off("LAP_SORT_ROWS")) {
+            DBuf<int32_t> c2(L.nnz, s);
+            DBuf<double> w2(L.nnz, s);
+            size_t bytes = 0;
+            LAP_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, bytes, L.scol, c2.p, L.sw, w2.p, (int)L.nnz, (int)n,
+                                                         L.srp, L.srp + 1, s));
+            DBuf<char> tmp((int64_t)bytes, s);
+            LAP_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp.p, bytes, L.scol, c2.p, L.sw, w2.p, (int)L.nnz, (int)n,
+                                                         L.srp, L.srp + 1, s));
+            g_kl++;
+            std::swap(L.scol, c2.p);
+            std::swap(L.sw, w2.p);
+        }
     }
     // SELL-32 slices of the short class
     if (nshort > 0) {
