@@ -808,7 +808,8 @@ __global__ void k_vote_round(int64_t n, const int64_t *__restrict__ row_ptr, con
                              const int32_t *__restrict__ idx, int8_t *__restrict__ nst, int32_t *__restrict__ nidx,
                              int32_t *__restrict__ votes) {
     GROUP_LOOP_BEGIN(G, n)
-        const bool act = live && st[i] == ST_UND;           // only Undecided act (O-R9)
+        const bool lng = live && row_ptr[i + 1] - row_ptr[i] > SETUP_LONG;  // k_vote_long_*
+        const bool act = live && !lng && st[i] == ST_UND;  // only Undecided act (O-R9)
         int br = -1;
         double bs = 0.0;
         int32_t bj = 0x7fffffff;
@@ -827,13 +828,92 @@ __global__ void k_vote_round(int64_t n, const int64_t *__restrict__ row_ptr, con
             int32_t j2 = __shfl_xor_sync(0xffffffffu, bj, o);
             if (r2 > br || (r2 == br && (s2 > bs || (s2 == bs && j2 < bj)))) { br = r2; bs = s2; bj = j2; }
         }
-        if (live && gl == 0) {  // every row writes its next state (no round-start copy needed)
+        if (live && !lng && gl == 0) {  // every row writes its next state (no round-start copy needed)
             bool dec = act && br == ST_SEED;
             nst[i] = dec ? (int8_t)ST_DEC : st[i];
             nidx[i] = dec ? bj : idx[i];
             if (act && br == ST_UND) atomicAdd(&votes[bj], 1);
         }
     GROUP_LOOP_END
+}
+// Long rows (deg > SETUP_LONG) of a vote round, chunk-parallel: the argmax
+// under (rank(state), S, -j) is an atomic max of key = rank << 62 | bits(S)
+// (S in (0, 1] has bits < 2^62) followed by an atomic min of j over the entries
+// that hit the max; both are exact and order-free.  best / bestj are reset by
+// k_vote_long_apply, so they only need initialising once.
+__device__ __forceinline__ unsigned long long vote_key(const double *__restrict__ S, const int32_t *__restrict__ col,
+                                                       const int8_t *__restrict__ st, int64_t k, double filt) {
+    const double sv = S[k];
+    if (sv == 0.0 || sv < filt) return 0ULL;
+    const int r = st[col[k]];
+    if (r == ST_DEC) return 0ULL;
+    return ((unsigned long long)r << 62) | (unsigned long long)__double_as_longlong(sv);
+}
+__global__ void k_vote_long_max(int64_t nchunks, const int32_t *__restrict__ crow, const int32_t *__restrict__ cidx,
+                                const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                                const double *__restrict__ S, double filt, const int8_t *__restrict__ st,
+                                unsigned long long *__restrict__ best) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = warp; c < nchunks; c += nwarps) {
+        const int64_t i = crow[c];
+        if (st[i] != ST_UND) continue;
+        const int64_t b = row_ptr[i] + (int64_t)cidx[c] * LCHUNK, e = min(row_ptr[i + 1], b + LCHUNK);
+        unsigned long long m = 0;
+        for (int64_t k = b + lane; k < e; k += 32) {
+            unsigned long long key = vote_key(S, col, st, k, filt);
+            m = key > m ? key : m;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            unsigned long long t = __shfl_xor_sync(0xffffffffu, m, o);
+            m = t > m ? t : m;
+        }
+        if (lane == 0 && m) atomicMax(&best[i], m);
+    }
+}
+__global__ void k_vote_long_argj(int64_t nchunks, const int32_t *__restrict__ crow, const int32_t *__restrict__ cidx,
+                                 const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                                 const double *__restrict__ S, double filt, const int8_t *__restrict__ st,
+                                 const unsigned long long *__restrict__ best, int32_t *__restrict__ bestj) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = warp; c < nchunks; c += nwarps) {
+        const int64_t i = crow[c];
+        if (st[i] != ST_UND || best[i] == 0) continue;
+        const unsigned long long bk = best[i];
+        const int64_t b = row_ptr[i] + (int64_t)cidx[c] * LCHUNK, e = min(row_ptr[i + 1], b + LCHUNK);
+        int32_t jm = 0x7fffffff;
+        for (int64_t k = b + lane; k < e; k += 32)
+            if (vote_key(S, col, st, k, filt) == bk) jm = min(jm, col[k]);
+        for (int o = 16; o > 0; o >>= 1) jm = min(jm, __shfl_xor_sync(0xffffffffu, jm, o));
+        if (lane == 0 && jm != 0x7fffffff) atomicMin(&bestj[i], jm);
+    }
+}
+__global__ void k_vote_long_apply(int64_t nchunks, const int32_t *__restrict__ crow, const int32_t *__restrict__ cidx,
+                                  const int8_t *__restrict__ st, const int32_t *__restrict__ idx,
+                                  unsigned long long *__restrict__ best, int32_t *__restrict__ bestj,
+                                  int8_t *__restrict__ nst, int32_t *__restrict__ nidx, int32_t *__restrict__ votes) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nchunks; c += (int64_t)gridDim.x * blockDim.x) {
+        if (cidx[c] != 0) continue;  // once per long row
+        const int64_t i = crow[c];
+        const unsigned long long bk = best[i];
+        const int br = bk ? (int)(bk >> 62) : -1;
+        const bool act = st[i] == ST_UND;
+        const bool dec = act && br == ST_SEED;
+        nst[i] = dec ? (int8_t)ST_DEC : st[i];
+        nidx[i] = dec ? bestj[i] : idx[i];
+        if (act && br == ST_UND) atomicAdd(&votes[bestj[i]], 1);
+        best[i] = 0;
+        bestj[i] = 0x7fffffff;
+    }
+}
+__global__ void k_vote_long_init(int64_t n, unsigned long long *best, int32_t *bestj) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        best[i] = 0;
+        bestj[i] = 0x7fffffff;
+    }
 }
 __global__ void k_vote_promote(int64_t n, int8_t *nst, const int32_t *votes, int thr) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -1263,9 +1343,24 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
     DBuf<int8_t> st(n, s), nst(n, s);
     DBuf<int32_t> idx(n, s), nidx(n, s), votes(n, s);
     k_vote_init<<<ge, 256, 0, s>>>(n, st.p, idx.p, votes.p); ++g_kl;
+    DBuf<unsigned long long> vbest(nlc > 0 ? n : 1, s);
+    DBuf<int32_t> vbestj(nlc > 0 ? n : 1, s);
+    if (nlc > 0) {
+        k_vote_long_init<<<ge, 256, 0, s>>>(n, vbest.p, vbestj.p);
+        ++g_kl;
+    }
     for (int t = 1; t <= p.vote_rounds; t++) {
         double filt = ldexp(1.0, -t);
         LAUNCH_G(G, k_vote_round, n, s, n, L.row_ptr, L.col, S.p, filt, st.p, idx.p, nst.p, nidx.p, votes.p);
+        if (nlc > 0) {
+            const unsigned gc = grid_for(nlc * 32, 256, 148 * 16);
+            k_vote_long_max<<<gc, 256, 0, s>>>(nlc, lc_row, lc_idx, L.row_ptr, L.col, S.p, filt, st.p, vbest.p);
+            k_vote_long_argj<<<gc, 256, 0, s>>>(nlc, lc_row, lc_idx, L.row_ptr, L.col, S.p, filt, st.p, vbest.p,
+                                                vbestj.p);
+            k_vote_long_apply<<<grid_for(nlc, 256, 148 * 8), 256, 0, s>>>(nlc, lc_row, lc_idx, st.p, idx.p, vbest.p,
+                                                                          vbestj.p, nst.p, nidx.p, votes.p);
+            g_kl += 3;
+        }
         k_vote_promote<<<ge, 256, 0, s>>>(n, nst.p, votes.p, p.vote_threshold); ++g_kl;
         LAP_CHECK_LAUNCH();
         std::swap(st.p, nst.p);
