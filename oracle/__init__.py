@@ -43,7 +43,7 @@ class Params(ctypes.Structure):
         ("n_test_vectors", ctypes.c_int32), ("tv_sweeps", ctypes.c_int32), ("tv_omega", ctypes.c_double),
         ("vote_rounds", ctypes.c_int32), ("vote_threshold", ctypes.c_int32), ("coarse_nnz", ctypes.c_int64),
         ("max_levels", ctypes.c_int32), ("seed", ctypes.c_uint64), ("random_order", ctypes.c_int32),
-        ("affinity_power", ctypes.c_int32),
+        ("affinity_power", ctypes.c_int32), ("cycle", ctypes.c_int32), ("kcycle_inner", ctypes.c_int32),
     ]
 
 
@@ -96,6 +96,8 @@ def lib():
             "orc_setup": (ctypes.c_int, [i64, P, P, P, P, ctypes.POINTER(P)]),
             "orc_free": (None, [P]),
             "orc_vcycle": (None, [P, i32, P, P]),
+            "orc_kcycle": (None, [P, i32, P, P]),
+            "orc_kcoarse": (None, [P, i32, P, P]),
             "orc_solve": (ctypes.c_int, [P, P, P, dbl, P, P]),
             "orc_nlev": (i32, [P]),
             "orc_get_level": (ctypes.POINTER(Level), [P, i32]),
@@ -353,6 +355,19 @@ class Hierarchy:
         n = self.level(l).n
         x = np.zeros(n)
         lib().orc_vcycle(self._h, l, _p(_c(b, np.float64)), _p(x))
+        return x
+
+    def kcycle(self, l: int, b) -> np.ndarray:
+        """K-cycle at level l (N2): x = K_l b."""
+        x = np.zeros(self.level(l).n)
+        lib().orc_kcycle(self._h, l, _p(_c(b, np.float64)), _p(x))
+        return x
+
+    def kcoarse(self, l: int, b) -> np.ndarray:
+        """The K-cycle's coarse problem at level l: kcycle_inner FCG(1)
+        iterations preconditioned by K_l (aggregation levels), else K_l b."""
+        x = np.zeros(self.level(l).n)
+        lib().orc_kcoarse(self._h, l, _p(_c(b, np.float64)), _p(x))
         return x
 
     def solve(self, b, tol: float | None = None):

@@ -41,6 +41,8 @@ void orc_params_default(orc_params *p) {
     p->seed = 0;
     p->random_order = 1;      /* P:376 */
     p->affinity_power = 1;    /* O-R5 */
+    p->cycle = 0;             /* V-cycle by default, P:733-735 */
+    p->kcycle_inner = 2;      /* S:525 / S:562 (paper: "a number of", P:650) */
 }
 
 /* ======================================================================== */
@@ -998,15 +1000,93 @@ void orc_vcycle(const orc_hier *h, int32_t l, const double *b, double *x) {
     free(r); free(rc); free(xc);
 }
 
-/* ======================================================================== */
-/* O-S8 PCG preconditioned by one V-cycle (P:255-258, 659-660, 669-671)      */
-/* ======================================================================== */
-
 static double dotp(const double *a, const double *b, int64_t n) {
     double s = 0.0;
     for (int64_t i = 0; i < n; i++) s += a[i] * b[i];
     return s;
 }
+
+/* ======================================================================== */
+/* N2 K-cycle (Notay & Vassilevski's recursive Krylov cycle):     */
+/* at each aggregation level below the finest, kcycle_inner FCG iterations    */
+/* with the rest of the hierarchy as the preconditioner; elimination levels  */
+/* are not accelerated.  Smoothing, transfers and the coarsest   */
+/* solve are those of the V-cycle above.                                      */
+/* ======================================================================== */
+
+void orc_kcycle(const orc_hier *h, int32_t l, const double *b, double *x) {
+    const orc_level *L = &h->lev[l];
+    int64_t n = L->n;
+    if (L->kind == ORC_COARSEST) { orc_vcycle(h, l, b, x); return; }
+    if (L->kind == ORC_ELIM) {
+        int64_t nc = h->lev[l + 1].n;
+        double *bc = malloc(sizeof(double) * (size_t)(nc + 1)), *xc = malloc(sizeof(double) * (size_t)(nc + 1));
+        for (int64_t i = 0; i < n; i++) if (L->fmap[i] >= 0) bc[L->fmap[i]] = b[i];
+        for (int64_t f = 0; f < n; f++) {
+            if (L->fmap[f] >= 0) continue;
+            for (int64_t q = L->row_ptr[f]; q < L->row_ptr[f + 1]; q++)
+                bc[L->fmap[L->col[q]]] += (L->w[q] / L->d[f]) * b[f];
+        }
+        orc_kcoarse(h, l + 1, bc, xc);                                       /* coarse problem */
+        for (int64_t i = 0; i < n; i++) {
+            if (L->fmap[i] >= 0) { x[i] = xc[L->fmap[i]]; continue; }
+            double s = b[i];
+            for (int64_t q = L->row_ptr[i]; q < L->row_ptr[i + 1]; q++) s += L->w[q] * xc[L->fmap[L->col[q]]];
+            x[i] = s / L->d[i];
+        }
+        free(bc); free(xc);
+        return;
+    }
+    const orc_params *p = &h->p;
+    int64_t m = L->m;
+    double *r = malloc(sizeof(double) * (size_t)n);
+    double *rc = calloc((size_t)(m + 1), sizeof(double)), *xc = malloc(sizeof(double) * (size_t)(m + 1));
+    orc_chebyshev(n, L->row_ptr, L->col, L->w, L->d, L->lambda, p->cheby_lo, p->cheby_hi,
+                  p->cheby_degree, b, x, 1);                                 /* pre-smooth from 0 */
+    orc_spmv(n, L->row_ptr, L->col, L->w, L->d, x, r);
+    for (int64_t i = 0; i < n; i++) r[i] = b[i] - r[i];                      /* residual */
+    for (int64_t i = 0; i < n; i++) rc[L->agg[i]] += r[i];                   /* R r */
+    orc_kcoarse(h, l + 1, rc, xc);                                           /* coarse problem */
+    for (int64_t i = 0; i < n; i++) x[i] += xc[L->agg[i]];                   /* x += P x_c */
+    orc_chebyshev(n, L->row_ptr, L->col, L->w, L->d, L->lambda, p->cheby_lo, p->cheby_hi,
+                  p->cheby_degree, b, x, 0);                                 /* post-smooth */
+    free(r); free(rc); free(xc);
+}
+
+/* FCG(1) (Notay 2000, truncation 1) from x = 0, k = 1..kcycle_inner:
+ *   z = B r ;  p = z  (k = 1) ,  p = z - (z.q_prev / p_prev.q_prev) p_prev  (k > 1)
+ *   q = L p ;  alpha = (p.r) / (p.q) ;  x += alpha p ;  r -= alpha q
+ * with B = orc_kcycle(l).  A direction with p.q = 0 (a zero right-hand side)
+ * takes alpha = 0 and beta = 0 (reading R-K2). */
+void orc_kcoarse(const orc_hier *h, int32_t l, const double *b, double *x) {
+    const orc_level *L = &h->lev[l];
+    int64_t n = L->n;
+    if (L->kind != ORC_AGG) { orc_kcycle(h, l, b, x); return; }
+    double *r = malloc(sizeof(double) * (size_t)n), *z = malloc(sizeof(double) * (size_t)n);
+    double *pv = malloc(sizeof(double) * (size_t)n), *q = malloc(sizeof(double) * (size_t)n);
+    memcpy(r, b, sizeof(double) * (size_t)n);
+    for (int64_t i = 0; i < n; i++) x[i] = 0.0;
+    double pq_prev = 0.0;
+    for (int32_t k = 1; k <= h->p.kcycle_inner; k++) {
+        orc_kcycle(h, l, r, z);
+        if (k == 1) {
+            memcpy(pv, z, sizeof(double) * (size_t)n);
+        } else {
+            double beta = pq_prev != 0.0 ? -dotp(z, q, n) / pq_prev : 0.0;   /* q = L p_prev here */
+            for (int64_t i = 0; i < n; i++) pv[i] = z[i] + beta * pv[i];
+        }
+        orc_spmv(n, L->row_ptr, L->col, L->w, L->d, pv, q);
+        double pq = dotp(pv, q, n);
+        double alpha = pq != 0.0 ? dotp(pv, r, n) / pq : 0.0;
+        for (int64_t i = 0; i < n; i++) { x[i] += alpha * pv[i]; r[i] -= alpha * q[i]; }
+        pq_prev = pq;
+    }
+    free(r); free(z); free(pv); free(q);
+}
+
+/* ======================================================================== */
+/* O-S8 PCG preconditioned by one V-cycle (P:255-258, 659-660, 669-671)      */
+/* ======================================================================== */
 
 static void project_mean(double *v, int64_t n) {
     double s = 0.0;
@@ -1035,11 +1115,34 @@ int orc_solve(const orc_hier *h, const double *b_in, double *x_out, double tol,
         goto done;
     }
     memcpy(r, b, sizeof(double) * (size_t)n);
+    int conv = 0;
+    if (h->p.cycle == 1) {
+        /* N2: FCG(1) preconditioned by the K-cycle ("FCG when using
+         * K-cycles"); same projection and stopping rules as the PCG below */
+        orc_kcycle(h, 0, r, z);
+        project_mean(z, n);
+        memcpy(pv, z, sizeof(double) * (size_t)n);
+        for (k = 1; k <= max_iters; k++) {
+            orc_spmv(n, L0->row_ptr, L0->col, L0->w, L0->d, pv, q);
+            double pq = dotp(pv, q, n);
+            double alpha = dotp(pv, r, n) / pq;
+            for (int64_t i = 0; i < n; i++) { x[i] += alpha * pv[i]; r[i] -= alpha * q[i]; }
+            if (sqrt(dotp(r, r, n)) / bn <= tol) {                           /* O-R30 */
+                orc_spmv(n, L0->row_ptr, L0->col, L0->w, L0->d, x, z);
+                for (int64_t i = 0; i < n; i++) z[i] = b[i] - z[i];
+                if (sqrt(dotp(z, z, n)) / bn <= tol) { conv = 1; break; }
+                memcpy(r, z, sizeof(double) * (size_t)n);
+            }
+            orc_kcycle(h, 0, r, z);
+            project_mean(z, n);                                              /* O-R29 */
+            double beta = -dotp(z, q, n) / pq;
+            for (int64_t i = 0; i < n; i++) pv[i] = z[i] + beta * pv[i];
+        }
+    } else {
     orc_vcycle(h, 0, r, z);
     project_mean(z, n);
     memcpy(pv, z, sizeof(double) * (size_t)n);
     double rho = dotp(r, z, n);
-    int conv = 0;
     for (k = 1; k <= max_iters; k++) {
         orc_spmv(n, L0->row_ptr, L0->col, L0->w, L0->d, pv, q);
         double alpha = rho / dotp(pv, q, n);
@@ -1056,6 +1159,7 @@ int orc_solve(const orc_hier *h, const double *b_in, double *x_out, double tol,
         double beta = rho2 / rho;
         for (int64_t i = 0; i < n; i++) pv[i] = z[i] + beta * pv[i];
         rho = rho2;
+    }
     }
     if (!conv) { k = max_iters; rc = ORC_ENOCONV; }
     project_mean(x, n);

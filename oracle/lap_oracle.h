@@ -51,6 +51,9 @@ typedef struct {
     uint64_t seed;           /* 0              O-S11                    */
     int32_t random_order;    /* 1                */
     int32_t affinity_power;  /* 1 (LAMG, O-R5); 2 = literal P:564-565   */
+    int32_t cycle;           /* 0 V-cycle + PCG (default);
+                                1 K-cycle + FCG (N2)         */
+    int32_t kcycle_inner;    /* 2 inner FCG iterations   */
 } orc_params;
 
 typedef struct {
@@ -141,7 +144,15 @@ int  orc_setup(int64_t n, const int64_t *row_ptr, const int32_t *col, const doub
 void orc_free(orc_hier *h);
 /* V-cycle on the permuted (internal) numbering, level l */
 void orc_vcycle(const orc_hier *h, int32_t l, const double *b, double *x);
-/* PCG on the caller's numbering; returns ORC_OK / ORC_ENOCONV */
+/* K-cycle (N2): as the V-cycle, but the coarse problem of an
+ * aggregation level is handed to orc_kcoarse instead of one recursive cycle */
+void orc_kcycle(const orc_hier *h, int32_t l, const double *b, double *x);
+/* x = kcycle_inner FCG(1) iterations on L_l x = b from x = 0, preconditioned
+ * by orc_kcycle(l) when level l is an aggregation level; orc_kcycle(l) itself
+ * otherwise (elimination levels are not accelerated) */
+void orc_kcoarse(const orc_hier *h, int32_t l, const double *b, double *x);
+/* PCG (cycle 0) or FCG(1) + K-cycle (cycle 1) on the caller's numbering;
+ * returns ORC_OK / ORC_ENOCONV */
 int  orc_solve(const orc_hier *h, const double *b, double *x, double tol,
                int32_t *iters, double *rel_residual);
 /* accessors for ctypes */

@@ -417,11 +417,30 @@ __global__ void k_prolong(int64_t n, const int32_t *__restrict__ agg, const doub
 // Work list: warps of 32 coarse rows (thread per row, lists of <= ELIM_SHORT
 // entries) followed by LCHUNK chunks of the long lists (hub C vertices with
 // thousands of eliminated neighbours), combined in chunk order.
+// Fused consumers: when the coarse level is an aggregation
+// level, its pre-smoothing step 0 (x = D^-1 b / theta, dv = x; O-S6) is
+// formed here as each coarse entry of b is produced (pre0 != null): same
+// arithmetic, one launch less.  (Fusing the aggregation prolongation into
+// k_elim_prolong the same way -- a serial scatter over each aggregate's
+// members -- measured slower: DESIGN.md §10.)
+struct Pre0 {
+    const double *d = nullptr;  // coarse diagonal; null = not fused
+    double inv_theta = 0;
+    double *x = nullptr, *dv = nullptr;
+};
+__device__ __forceinline__ void put_b(int64_t k, double s, double *__restrict__ bc, const Pre0 &p0) {
+    bc[k] = s;
+    if (p0.d) {
+        double v = (s / p0.d[k]) * p0.inv_theta;
+        p0.dv[k] = v;
+        p0.x[k] = v;
+    }
+}
 template <int UNUSED>
 __global__ void __launch_bounds__(256) k_elim_restrict(int64_t nc, const int32_t *__restrict__ cid,
                                                        const int64_t *__restrict__ ctp, const int32_t *__restrict__ ctf,
                                                        const double *__restrict__ ctc, LongRows R,
-                                                       const double *__restrict__ b, double *__restrict__ bc) {
+                                                       const double *__restrict__ b, double *__restrict__ bc, Pre0 p0) {
     pdl_begin();
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -435,13 +454,13 @@ __global__ void __launch_bounds__(256) k_elim_restrict(int64_t nc, const int32_t
                 if (q1 - q0 <= ELIM_SHORT) {
                     double s = b[cid[k]];
                     for (int64_t q = q0; q < q1; q++) s += ctc[q] * b[ctf[q]];
-                    bc[k] = s;
+                    put_b(k, s, bc, p0);
                 }
             }
         } else {
             int64_t k;
             double s;
-            if (chunk_reduce(t - nrw, lane, ctp, ctf, ctc, b, R, k, s) && lane == 0) bc[k] = b[cid[k]] + s;
+            if (chunk_reduce(t - nrw, lane, ctp, ctf, ctc, b, R, k, s) && lane == 0) put_b(k, b[cid[k]] + s, bc, p0);
         }
     }
 }
@@ -480,7 +499,18 @@ __global__ void k_coarse_gemv(int64_t n, const double *__restrict__ P, const dou
 static inline unsigned eg(int64_t n) { return grid_for(n, 256, 148 * 8); }
 
 // x_out = V(l, b)   (Alg. 1, gamma = 1; elimination levels exact, O-S7)
-static void vcycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, cudaStream_t s) {
+static bool fuse_enabled() {  // LAP_FUSE_TRANSFERS=0: separate step-0 kernel
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("LAP_FUSE_TRANSFERS");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+// pre0_done: the caller's restriction already formed this (aggregation)
+// level's pre-smoothing step 0
+static void vcycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, cudaStream_t s, bool pre0_done = false) {
     Level &L = h->lev[l];
     int64_t n = L.n;
     if (l == h->dtail_level && L.dense && b == L.b && xout == L.x) {  // V(l, b) = M_l b (tail.cu)
@@ -500,11 +530,19 @@ static void vcycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, c
     if (L.kind == KIND_ELIM) {
         int64_t nc = C.n;
         LongRows R{L.ct_nchunks, L.ct_crow, L.ct_cidx, L.ct_cslot, L.ct_cpart, L.ct_ccnt};
+        Pre0 p0;
+        const bool fuse0 = C.kind == KIND_AGG && !(l + 1 == h->dtail_level && C.dense) && fuse_enabled();
+        if (fuse0) {
+            p0.d = C.sd;
+            p0.inv_theta = 1.0 / C.cheb_theta;
+            p0.x = C.x2;
+            p0.dv = C.dv;
+        }
         launch_pdl(k_elim_restrict<0>, grid_for(((nc + 31) / 32 + L.ct_nchunks) * 32, 256, 148 * 8), 256, s, nc,
                    (const int32_t *)L.cid_s, (const int64_t *)L.ct_ptr_s, (const int32_t *)L.ct_f_s,
-                   (const double *)L.ct_coef_s, R, b, C.b);
+                   (const double *)L.ct_coef_s, R, b, C.b, p0);
         h->cur.launches++;
-        vcycle_rec(h, l + 1, C.b, C.x, s);
+        vcycle_rec(h, l + 1, C.b, C.x, s, fuse0);
         Csr A{L.srp, L.scol, L.sw, L.sd};
         launch_pdl(k_elim_prolong, eg(nc + L.nF), 256, s, nc, L.nF, L.cid_s, L.flist, L.fmap_s, A, b, C.x, xout);
         h->cur.launches++;
@@ -516,9 +554,11 @@ static void vcycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, c
     const int K = h->p.cheby_degree;
     const double theta = L.cheb_theta, delta = L.cheb_delta, sigma = L.cheb_sigma;
     double *cur = L.x2, *alt = L.t;  // ping-pong pair, distinct from xout and r
-    // pre-smoothing from x = 0
-    launch_pdl(k_cheb_first, eg(n), 256, s, n, b, L.sd, 1.0 / theta, cur, L.dv);
-    h->cur.launches++;
+    // pre-smoothing from x = 0 (step 0 formed by the caller's restriction when pre0_done)
+    if (!pre0_done) {
+        launch_pdl(k_cheb_first, eg(n), 256, s, n, b, L.sd, 1.0 / theta, cur, L.dv);
+        h->cur.launches++;
+    }
     h->cur.bytes += 32 * n;
     double rho_old = 1.0 / sigma;
     EpiArgs a;

@@ -223,8 +223,9 @@ def test_storage_layout_validated_in_debug_mode(P):
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("env", [{"LAP_DENSE_TAIL": "0"}, {"LAP_PDL": "0"}, {"LAP_DENSE_TAIL": "0", "LAP_PDL": "0"}],
-                         ids=["no-dense-tail", "no-pdl", "neither"])
+@pytest.mark.parametrize("env", [{"LAP_DENSE_TAIL": "0"}, {"LAP_PDL": "0"}, {"LAP_FUSE_TRANSFERS": "0"},
+                                 {"LAP_DENSE_TAIL": "0", "LAP_PDL": "0", "LAP_FUSE_TRANSFERS": "0"}],
+                         ids=["no-dense-tail", "no-pdl", "no-fused-transfers", "none"])
 def test_solve_path_switches(P, env):
     """The alternative solve paths (per-level kernels instead of the dense
     tail operator, launches without programmatic dependent launch) give the
@@ -246,3 +247,30 @@ def test_solve_path_switches(P, env):
     r = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, timeout=600,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_fused_transfers_bitwise(P, tmp_path):
+    """Forming an aggregation level's pre-smoothing step 0 inside the
+    restriction of the elimination level above it is the same arithmetic:
+    V-cycle outputs are bit-identical with LAP_FUSE_TRANSFERS=0 (graphs with
+    elimination levels above aggregation levels, per-level path so no level
+    is folded into the dense tail)."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys, numpy as np, lapgen, paper_1705_06266_b200 as P\n"
+            "out = []\n"
+            "for g in [lapgen.rmat(13), lapgen.barabasi_albert(20000, 3), lapgen.grid2d(200, 150)]:\n"
+            "    h = P.Hierarchy(g)\n"
+            "    r = np.random.default_rng(2).standard_normal(g.n); r -= r.mean()\n"
+            "    out.append(h.vcycle(r))\n"
+            "np.save(sys.argv[1], np.concatenate(out))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = []
+    for fuse in ["1", "0"]:
+        f = str(tmp_path / f"z{fuse}.npy")
+        e = dict(os.environ, LAP_FUSE_TRANSFERS=fuse, LAP_DENSE_TAIL="0")
+        r = subprocess.run([sys.executable, "-c", code, f], env=e, capture_output=True, text=True, timeout=600, cwd=root)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res.append(np.load(f))
+    assert res[0].tobytes() == res[1].tobytes()
