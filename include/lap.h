@@ -92,6 +92,11 @@ typedef struct {
     int32_t use_graphs;       /* 1: capture the V-cycle as a CUDA graph        */
     int64_t replicate_nnz;    /* multi-GPU: levels with nnz >= this are sharded,
                                  the rest replicated; 0 = nnz(L_0) / (32 P)    */
+    int32_t cycle;            /* 0: PCG + V-cycle (default);
+                                 1: FCG(1) + K-cycle,
+                                 single-GPU only                               */
+    int32_t kcycle_inner;     /* 2: FCG iterations per aggregation level below
+                                 the finest (paper: "a number of")      */
 } lap_params;
 
 typedef struct lap_hierarchy lap_hierarchy;
@@ -138,6 +143,16 @@ lap_status lap_perm(const lap_hierarchy *h, int64_t *perm);
 lap_status lap_spmv(const lap_hierarchy *h, int32_t l, const double *x, double *y, void *cuda_stream);
 /* z = V(0, r): one V-cycle on the internal (permuted) level-0 numbering (O-S7). */
 lap_status lap_vcycle(lap_hierarchy *h, const double *r, double *z, void *cuda_stream);
+/* z = K(l, r): one K-cycle at level l: the V-cycle's
+ * smoothing and transfers, with the coarse problem of every aggregation level
+ * below l solved by params.kcycle_inner FCG(1) iterations preconditioned by
+ * the K-cycle there (elimination levels are not accelerated).
+ * r, z: length n_l, internal (storage-independent, level-l) numbering, host
+ * or device.  with_fcg = 1 applies the FCG iterations at level l itself
+ * (l >= 1 aggregation levels; the "coarse solve" orc_kcoarse of the oracle).
+ * Any single-GPU hierarchy; LAP_EINVAL for a bad level or a sharded one. */
+lap_status lap_kcycle(lap_hierarchy *h, int32_t l, int32_t with_fcg, const double *r, double *z,
+                      void *cuda_stream);
 
 /* ---- multi-GPU: 2D-sharded solve ------------------------------
  * The fine levels (nnz >= params.replicate_nnz) are distributed as a 2D edge

@@ -23,7 +23,8 @@ UNITS = {"setup.cu": ["-fmad=false", "-prec-div=true", "-prec-sqrt=true"],
          "storage.cu": [],
          "lap_api.cu": [],
          "dist.cu": [],
-         "tail.cu": []}
+         "tail.cu": [],
+         "ktail.cu": []}
 
 
 def _sources():

@@ -125,6 +125,13 @@ void finalize_solve_structures(lap_hierarchy *h, cudaStream_t s) {
         L.t = (double *)dalloc(8 * n, s);
         L.r = (double *)dalloc(8 * n, s);
         L.dv = (double *)dalloc(8 * n, s);
+        if (L.kind == KIND_AGG && l > 0) {  // K-cycle inner FCG vectors (small: coarse levels)
+            L.kp = (double *)dalloc(8 * n, s);
+            L.kq = (double *)dalloc(8 * n, s);
+            L.kz = (double *)dalloc(8 * n, s);
+            L.kr = (double *)dalloc(8 * n, s);
+            L.ksc = (double *)dalloc(8 * 8, s);
+        }
         if (L.kind == KIND_AGG) {
             double a = h->p.cheby_lo * L.lambda, b = h->p.cheby_hi * L.lambda;
             L.cheb_theta = 0.5 * (b + a);
@@ -139,7 +146,7 @@ void finalize_solve_structures(lap_hierarchy *h, cudaStream_t s) {
     h->scal = (double *)dalloc(8 * 16, s);
     LAP_CUDA(cudaMemsetAsync(h->scal, 0, 8 * 16, s));
     int64_t np = std::max<int64_t>(1024, spmv_partial_slots(h->lev[0]));
-    for (auto &L : h->lev) np = std::max<int64_t>(np, spmv_partial_slots(L));
+    for (auto &L : h->lev) np = std::max<int64_t>(np, 2 * spmv_partial_slots(L));  // E_FCG: two dots
     if (np > h->npartials) {
         dfree(h->partials, s);
         h->partials = (double *)dalloc(8 * np, s);
@@ -157,7 +164,7 @@ static void free_level(Level &L, cudaStream_t s) {
                   L.chunk_part, L.ell_col16, L.scol16,
                   L.agg_s, L.mem_ptr, L.members, L.cid_s, L.flist, L.ct_ptr_s, L.ct_f_s, L.ct_coef_s, L.fmap_s,
                   L.ct_crow, L.ct_cidx, L.ct_cslot, L.ct_ccnt, L.ct_cpart,
-                  L.pinv_s, L.dense, L.b, L.x, L.x2, L.t, L.r, L.dv};
+                  L.pinv_s, L.dense, L.b, L.x, L.x2, L.t, L.r, L.dv, L.kp, L.kq, L.kz, L.kr, L.ksc};
     for (void *p : ps) dfree(p, s);
 }
 
@@ -274,6 +281,8 @@ void lap_params_default(lap_params *p) {
     p->random_order = 1;
     p->affinity_power = 1;
     p->keep_strength = 0;
+    p->cycle = 0;
+    p->kcycle_inner = 2;
     p->use_graphs = 1;
     p->replicate_nnz = 0;
 }
@@ -292,7 +301,7 @@ lap_status lap_setup(const lap_graph *g, const lap_params *pp, void *stream, lap
     else lap_params_default(&p);
     if (p.n_test_vectors != 4 || p.cheby_degree < 1 || p.tv_sweeps < 0 || p.vote_rounds < 0 ||
         p.lanczos_steps < 1 || p.lanczos_steps > 64 || !(p.cheby_hi > p.cheby_lo) || !(p.cheby_lo > 0) ||
-        p.max_levels < 1) {
+        p.max_levels < 1 || p.cycle < 0 || p.cycle > 1 || p.kcycle_inner < 1 || p.kcycle_inner > 8) {
         lap::set_error("lap_setup: unsupported parameter values");
         return LAP_EINVAL;
     }
@@ -312,6 +321,7 @@ lap_status lap_setup(const lap_graph *g, const lap_params *pp, void *stream, lap
         lap::build_hierarchy(h, g, s);
         lap::finalize_solve_structures(h, s);
         lap::build_dense_tail(h, s);
+        lap::build_ktail(h, s);
         LAP_CUDA(cudaEventRecord(e1, s));
         LAP_CUDA(cudaStreamSynchronize(s));
         float ms = 0;
@@ -353,6 +363,10 @@ lap_status lap_setup_dist(const lap_graph *g, const lap_params *pp, lap_comm *c,
     if (pp) p = *pp;
     else lap_params_default(&p);
     p.use_graphs = 0;  // the sharded solve is host-sequenced (collectives between kernels)
+    if (p.cycle != 0) {
+        lap::set_error("lap_setup_dist: the K-cycle (params.cycle = 1) is single-GPU only");
+        return LAP_EINVAL;
+    }
     lap_hierarchy *h = nullptr;
     lap_status st = lap_setup(g, &p, stream, &h);
     if (st != LAP_OK && st != LAP_ESTALL) return st;
@@ -378,6 +392,7 @@ void lap_free(lap_hierarchy *h) {
     if (h->vgraph) cudaGraphExecDestroy(h->vgraph);
     lap::free_dist(h);
     lap::free_pcg(h);
+    lap::free_ktail(h, s);
     for (auto &L : h->lev) lap::free_level(L, s);
     void *ps[] = {h->perm, h->cmap, h->pb, h->px, h->pr, h->pz, h->pp, h->pq, h->scal, h->partials, h->stage_in,
                   h->stage_out};
@@ -552,6 +567,26 @@ lap_status lap_vcycle(lap_hierarchy *h, const double *r, double *z, void *stream
     lap::k_gather_i32map<<<g, 256, 0, s>>>(n, L0.sid, h->stage_in, h->pr);      // logical -> storage
     lap::launch_vcycle(h, s);
     lap::k_scatter_i32map<<<g, 256, 0, s>>>(n, L0.sid, h->pz, h->stage_out);    // storage -> logical
+    LAP_CHECK_LAUNCH();
+    LAP_CUDA(cudaMemcpyAsync(z, h->stage_out, 8 * n, zdev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+    LAP_CUDA(cudaStreamSynchronize(s));
+    return LAP_OK;
+    LAP_API_END
+}
+
+lap_status lap_kcycle(lap_hierarchy *h, int32_t l, int32_t with_fcg, const double *r, double *z, void *stream) {
+    if (!h || !r || !z || l < 0 || l >= (int32_t)h->lev.size() || h->dist) return LAP_EINVAL;
+    if (with_fcg && l == 0 && h->lev[0].kind == lap::KIND_AGG) return LAP_EINVAL;  // level 0: the outer FCG
+    LAP_API_BEGIN
+    cudaStream_t s = (cudaStream_t)stream;
+    lap::Level &L = h->lev[l];
+    int64_t n = L.n;
+    bool rdev = lap::is_device_ptr(r), zdev = lap::is_device_ptr(z);
+    unsigned g = lap::grid_for(n, 256, 148 * 8);
+    LAP_CUDA(cudaMemcpyAsync(h->stage_in, r, 8 * n, rdev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    lap::k_gather_i32map<<<g, 256, 0, s>>>(n, L.sid, h->stage_in, L.b);       // logical -> storage
+    lap::kcycle_level(h, l, with_fcg != 0, s);
+    lap::k_scatter_i32map<<<g, 256, 0, s>>>(n, L.sid, L.x, h->stage_out);     // storage -> logical
     LAP_CHECK_LAUNCH();
     LAP_CUDA(cudaMemcpyAsync(z, h->stage_out, 8 * n, zdev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
     LAP_CUDA(cudaStreamSynchronize(s));

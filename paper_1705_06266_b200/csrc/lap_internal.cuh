@@ -167,6 +167,9 @@ struct Level {
     double cheb_theta = 0, cheb_delta = 0, cheb_sigma = 0;
     // solve work vectors (storage order, length n >= 1)
     double *b = nullptr, *x = nullptr, *x2 = nullptr, *t = nullptr, *r = nullptr, *dv = nullptr;
+    // K-cycle inner FCG(1) (aggregation levels l >= 1; solve.cu): direction,
+    // L*direction, preconditioned residual, residual; 8 device scalars
+    double *kp = nullptr, *kq = nullptr, *kz = nullptr, *kr = nullptr, *ksc = nullptr;
 };
 
 struct Stats {
@@ -199,6 +202,7 @@ struct lap_hierarchy {
     cudaGraphExec_t pcg_start = nullptr, pcg_resume = nullptr;
     void *pcg_counts = nullptr;
     int dtail_level = -1;          // level whose V-cycle is the dense operator lev[].dense (tail.cu)
+    void *ktail = nullptr;         // K-cycle below a small level as one single-CTA program (ktail.cu)
     // multi-GPU shards (dist.cu), NULL for a single-GPU hierarchy
     void *dist = nullptr;
     void *dist_owned = nullptr;
@@ -240,6 +244,10 @@ void capture_pcg(lap_hierarchy *h);
 // dense tail (tail.cu)
 void build_dense_tail(lap_hierarchy *h, cudaStream_t s);
 void launch_dense_gemv(const Level &L, const double *b, double *x, cudaStream_t s);
+void kcycle_level(lap_hierarchy *h, int l, bool with_fcg, cudaStream_t s);  // N2 (solve.cu)
+void build_ktail(lap_hierarchy *h, cudaStream_t s);                          // N2 (ktail.cu)
+void free_ktail(lap_hierarchy *h, cudaStream_t s);
+bool ktail_launch(lap_hierarchy *h, int l, bool pre0_done, cudaStream_t s);
 // multi-GPU (dist.cu)
 void build_dist(lap_hierarchy *h, lap_comm *c, cudaStream_t s);
 void free_dist(lap_hierarchy *h);

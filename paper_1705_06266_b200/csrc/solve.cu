@@ -27,17 +27,25 @@ struct Csr {
 
 // ------------------------------------------------------------------ epilogues
 // Ax = sum_j w_ij x_j ; (L x)_i = d_i x_i - Ax  (L = D - A)
-enum { E_SPMV = EPI_SPMV, E_DOT = EPI_SPMV_DOT, E_RESID = EPI_RESID, E_CHEB = EPI_CHEB, E_LZ = EPI_LANCZOS, E_CHEB0 = 5 };
+enum { E_SPMV = EPI_SPMV, E_DOT = EPI_SPMV_DOT, E_RESID = EPI_RESID, E_CHEB = EPI_CHEB, E_LZ = EPI_LANCZOS, E_CHEB0 = 5,
+       E_FCG = 6 };  // E_FCG: y = L x with x.y and x.b (K-cycle inner FCG: p.q and p.r in one pass)
+struct Dacc {  // per-thread dot accumulators of the E_DOT / E_LZ / E_FCG epilogues
+    double a = 0.0, b = 0.0;
+};
 
 template <int EPI>
-__device__ __forceinline__ void apply_epi(int64_t i, double ax, const Csr &A, const EpiArgs &a, double &dacc) {
+__device__ __forceinline__ void apply_epi(int64_t i, double ax, const Csr &A, const EpiArgs &a, Dacc &dacc) {
     double xi = a.x[i];
     double lx = A.d[i] * xi - ax;
     if (EPI == E_SPMV) {
         a.y[i] = lx;
     } else if (EPI == E_DOT) {
         a.y[i] = lx;
-        dacc += xi * lx;
+        dacc.a += xi * lx;
+    } else if (EPI == E_FCG) {
+        a.y[i] = lx;
+        dacc.a += xi * lx;
+        dacc.b += xi * a.b[i];
     } else if (EPI == E_RESID) {
         a.y[i] = a.b[i] - lx;
     } else if (EPI == E_CHEB) {  // dv = c1 dv + c2 D^-1 (b - L x); x_out = x + dv   (O-S6)
@@ -53,7 +61,7 @@ __device__ __forceinline__ void apply_epi(int64_t i, double ax, const Csr &A, co
     } else if (EPI == E_LZ) {  // Lanczos on D^-1/2 L D^-1/2: y = rs o (L u) - beta_prev v_prev; alpha += y.v
         double y = a.rs[i] * lx - a.lz[4] * a.vp[i];
         a.y[i] = y;
-        dacc += y * a.v[i];
+        dacc.a += y * a.v[i];
     }
 }
 
@@ -96,7 +104,7 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
 template <int EPI, class CT, int NB = 8>
 __device__ __forceinline__ void sell_slice(int64_t sl, int lane, int64_t nrows, const int64_t *__restrict__ sp,
                                            const CT *__restrict__ ec, const double *__restrict__ ew, const Csr &A,
-                                           const EpiArgs &a, const double *__restrict__ xg, double &dacc) {
+                                           const EpiArgs &a, const double *__restrict__ xg, Dacc &dacc) {
     const int64_t i = sl * 32 + lane;
     const int64_t beg = sp[sl], end = sp[sl + 1];
     double xi = 0.0, di = 0.0, bi = 0.0, dvi = 0.0;
@@ -104,7 +112,7 @@ __device__ __forceinline__ void sell_slice(int64_t sl, int lane, int64_t nrows, 
     if (live) {
         xi = a.x[i];
         di = A.d[i];
-        if (EPI == E_RESID || EPI == E_CHEB || EPI == E_CHEB0) bi = a.b[i];
+        if (EPI == E_RESID || EPI == E_CHEB || EPI == E_CHEB0 || EPI == E_FCG) bi = a.b[i];
         if (EPI == E_CHEB) dvi = a.dv[i];
     }
     // batches of 8 padded columns: all 16 index/weight loads of a batch are
@@ -136,7 +144,11 @@ __device__ __forceinline__ void sell_slice(int64_t sl, int lane, int64_t nrows, 
             a.y[i] = lx;
         } else if (EPI == E_DOT) {
             a.y[i] = lx;
-            dacc += xi * lx;
+            dacc.a += xi * lx;
+        } else if (EPI == E_FCG) {
+            a.y[i] = lx;
+            dacc.a += xi * lx;
+            dacc.b += xi * bi;
         } else if (EPI == E_RESID) {
             a.y[i] = bi - lx;
         } else if (EPI == E_CHEB) {
@@ -150,7 +162,7 @@ __device__ __forceinline__ void sell_slice(int64_t sl, int lane, int64_t nrows, 
         } else if (EPI == E_LZ) {
             double y = a.rs[i] * lx - a.lz[4] * a.vp[i];
             a.y[i] = y;
-            dacc += y * a.v[i];
+            dacc.a += y * a.v[i];
         }
     }
 }
@@ -220,7 +232,7 @@ __device__ __forceinline__ bool chunk_reduce(int64_t c, int lane, const int64_t 
 template <int EPI, class CT>
 __device__ __forceinline__ void long_chunk(int64_t c, int lane, const Csr &A, const CT *__restrict__ col,
                                            const LongRows &R, const EpiArgs &a, const double *__restrict__ xg,
-                                           double &dacc) {
+                                           Dacc &dacc) {
     int64_t i;
     double ax;
     if (chunk_reduce(c, lane, A.rp, col, A.w, xg, R, i, ax) && lane == 0) apply_epi<EPI>(i, ax, A, a, dacc);
@@ -240,14 +252,18 @@ __global__ void __launch_bounds__(256, NB == 8 ? 4 : 5) k_spmv(int64_t nslices, 
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t nitems = nslices + R.nchunks;
-    double dacc = 0.0;
+    Dacc dacc;
     for (int64_t t = warp; t < nitems; t += nwarps) {
         if (t < nslices) sell_slice<EPI, int32_t, NB>(t, lane, nshort, sp, ec, ew, A, a, a.x, dacc);
         else long_chunk<EPI>(t - nslices, lane, A, A.col, R, a, a.x, dacc);
     }
-    if (EPI == E_DOT || EPI == E_LZ) {
-        double r = block_sum(dacc, sh);
+    if (EPI == E_DOT || EPI == E_LZ || EPI == E_FCG) {
+        double r = block_sum(dacc.a, sh);
         if (threadIdx.x == 0) partials[blockIdx.x] = r;
+    }
+    if (EPI == E_FCG) {  // second dot in partials[gridDim.x + block]
+        double r = block_sum(dacc.b, sh);
+        if (threadIdx.x == 0) partials[gridDim.x + blockIdx.x] = r;
     }
 }
 
@@ -272,14 +288,18 @@ __global__ void __launch_bounds__(1024, 1) k_spmv_smem(int64_t n, int64_t nslice
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t nitems = nslices + R.nchunks;
-    double dacc = 0.0;
+    Dacc dacc;
     for (int64_t t = warp; t < nitems; t += nwarps) {
         if (t < nslices) sell_slice<EPI>(t, lane, nshort, sp, ec, ew, A, a, xs, dacc);
         else long_chunk<EPI>(t - nslices, lane, A, col16, R, a, xs, dacc);
     }
-    if (EPI == E_DOT || EPI == E_LZ) {
-        double r = block_sum(dacc, sh);
+    if (EPI == E_DOT || EPI == E_LZ || EPI == E_FCG) {
+        double r = block_sum(dacc.a, sh);
         if (threadIdx.x == 0) partials[blockIdx.x] = r;
+    }
+    if (EPI == E_FCG) {  // second dot in partials[gridDim.x + block]
+        double r = block_sum(dacc.b, sh);
+        if (threadIdx.x == 0) partials[gridDim.x + blockIdx.x] = r;
     }
 }
 
@@ -338,9 +358,11 @@ void spmv_level(lap_hierarchy *h, const Level &L, EpiKind kind, const EpiArgs &a
         case E_RESID: spmv_dispatch<E_RESID>(h, L, a, s); break;
         case E_CHEB: spmv_dispatch<E_CHEB>(h, L, a, s); break;
         case E_CHEB0: spmv_dispatch<E_CHEB0>(h, L, a, s); break;
+        case E_FCG: spmv_dispatch<E_FCG>(h, L, a, s); break;
         default: throw Error{LAP_EINVAL, "bad epilogue"};
     }
-    int64_t extra = (kind == EPI_RESID) ? 8 : (kind == EPI_CHEB) ? 24 : (kind == (EpiKind)E_CHEB0) ? 16 : 0;
+    int64_t extra = (kind == EPI_RESID) ? 8 : (kind == EPI_CHEB) ? 24 : (kind == (EpiKind)E_CHEB0) ? 16
+                    : (kind == (EpiKind)E_FCG) ? 8 : 0;
     h->cur.edges += L.nnz;
     h->cur.bytes += 12 * L.nnz + (32 + extra) * L.n;
 }
@@ -390,39 +412,12 @@ __global__ void k_cheb_first(int64_t n, const double *__restrict__ b, const doub
         x[i] = v;
     }
 }
-// r_c[a] = sum over members of a (ascending) of r_i; 8 lanes per aggregate
-__global__ void __launch_bounds__(256) k_restrict(int64_t m, const int64_t *__restrict__ mp,
-                                                  const int32_t *__restrict__ mem, const double *__restrict__ r,
-                                                  double *__restrict__ rc) {
-    pdl_begin();
-    const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t base = warp * 4; base < m; base += nwarps * 4) {
-        int64_t a = base + grp;
-        double acc = 0.0;
-        if (a < m)
-            for (int64_t k = mp[a] + sub; k < mp[a + 1]; k += 8) acc += r[mem[k]];
-        for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (sub == 0 && a < m) rc[a] = acc;
-    }
-}
-__global__ void k_prolong(int64_t n, const int32_t *__restrict__ agg, const double *__restrict__ xc,
-                          double *__restrict__ x) {
-    pdl_begin();
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        x[i] += xc[agg[i]];
-}
-// P^T b on an elimination level: b'_k = b_{cid[k]} + sum_{f ~ cid[k]} (w_fc/d_f) b_f   (P:458-461)
-// Work list: warps of 32 coarse rows (thread per row, lists of <= ELIM_SHORT
-// entries) followed by LCHUNK chunks of the long lists (hub C vertices with
-// thousands of eliminated neighbours), combined in chunk order.
-// Fused consumers: when the coarse level is an aggregation
+// Fused consumer: when the coarse level is an aggregation
 // level, its pre-smoothing step 0 (x = D^-1 b / theta, dv = x; O-S6) is
-// formed here as each coarse entry of b is produced (pre0 != null): same
-// arithmetic, one launch less.  (Fusing the aggregation prolongation into
-// k_elim_prolong the same way -- a serial scatter over each aggregate's
-// members -- measured slower: DESIGN.md §10.)
+// formed by the restriction (k_restrict or k_elim_restrict) as each coarse
+// entry of b is produced (p0.d != null): same arithmetic, one launch less.
+// (Fusing the prolongation into k_elim_prolong the same way -- a serial
+// scatter over each aggregate's members -- measured slower: DESIGN.md §7.)
 struct Pre0 {
     const double *d = nullptr;  // coarse diagonal; null = not fused
     double inv_theta = 0;
@@ -436,6 +431,34 @@ __device__ __forceinline__ void put_b(int64_t k, double s, double *__restrict__ 
         p0.x[k] = v;
     }
 }
+// r_c[a] = sum over members of a (ascending) of r_i; 8 lanes per aggregate
+__global__ void __launch_bounds__(256) k_restrict(int64_t m, const int64_t *__restrict__ mp,
+                                                  const int32_t *__restrict__ mem, const double *__restrict__ r,
+                                                  double *__restrict__ rc, Pre0 p0) {
+    pdl_begin();
+    const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
+    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t base = warp * 4; base < m; base += nwarps * 4) {
+        int64_t a = base + grp;
+        double acc = 0.0;
+        if (a < m)
+            for (int64_t k = mp[a] + sub; k < mp[a + 1]; k += 8) acc += r[mem[k]];
+        for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (sub == 0 && a < m) put_b(a, acc, rc, p0);
+    }
+}
+__global__ void k_prolong(int64_t n, const int32_t *__restrict__ agg, const double *__restrict__ xc,
+                          double *__restrict__ x) {
+    pdl_begin();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] += xc[agg[i]];
+}
+// P^T b on an elimination level: b'_k = b_{cid[k]} + sum_{f ~ cid[k]} (w_fc/d_f) b_f   (P:458-461)
+// Work list: warps of 32 coarse rows (thread per row, lists of <= ELIM_SHORT
+// entries) followed by LCHUNK chunks of the long lists (hub C vertices with
+// thousands of eliminated neighbours), combined in chunk order.
+// (coarse pre-smoothing step 0 fused as in k_restrict)
 template <int UNUSED>
 __global__ void __launch_bounds__(256) k_elim_restrict(int64_t nc, const int32_t *__restrict__ cid,
                                                        const int64_t *__restrict__ ctp, const int32_t *__restrict__ ctf,
@@ -508,12 +531,17 @@ static bool fuse_enabled() {  // LAP_FUSE_TRANSFERS=0: separate step-0 kernel
     return v == 1;
 }
 
+static void kcoarse(lap_hierarchy *h, int l, cudaStream_t s, bool pre0_done);
+
+// One cycle at level l: x = V(l, b) (kc = false, O-S7) or x = K(l, b)
+// (kc = true, N2: the coarse problem below each level goes to kcoarse).
 // pre0_done: the caller's restriction already formed this (aggregation)
 // level's pre-smoothing step 0
-static void vcycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, cudaStream_t s, bool pre0_done = false) {
+static void cycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, cudaStream_t s, bool kc,
+                      bool pre0_done = false) {
     Level &L = h->lev[l];
     int64_t n = L.n;
-    if (l == h->dtail_level && L.dense && b == L.b && xout == L.x) {  // V(l, b) = M_l b (tail.cu)
+    if (!kc && l == h->dtail_level && L.dense && b == L.b && xout == L.x) {  // (the K-cycle is not linear)  // V(l, b) = M_l b (tail.cu)
         launch_dense_gemv(L, b, xout, s);
         h->cur.launches++;
         h->cur.bytes += 8 * n * n + 16 * n;
@@ -531,7 +559,7 @@ static void vcycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, c
         int64_t nc = C.n;
         LongRows R{L.ct_nchunks, L.ct_crow, L.ct_cidx, L.ct_cslot, L.ct_cpart, L.ct_ccnt};
         Pre0 p0;
-        const bool fuse0 = C.kind == KIND_AGG && !(l + 1 == h->dtail_level && C.dense) && fuse_enabled();
+        const bool fuse0 = C.kind == KIND_AGG && (kc || !(l + 1 == h->dtail_level && C.dense)) && fuse_enabled();
         if (fuse0) {
             p0.d = C.sd;
             p0.inv_theta = 1.0 / C.cheb_theta;
@@ -542,7 +570,8 @@ static void vcycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, c
                    (const int32_t *)L.cid_s, (const int64_t *)L.ct_ptr_s, (const int32_t *)L.ct_f_s,
                    (const double *)L.ct_coef_s, R, b, C.b, p0);
         h->cur.launches++;
-        vcycle_rec(h, l + 1, C.b, C.x, s, fuse0);
+        if (kc) kcoarse(h, l + 1, s, fuse0);
+        else cycle_rec(h, l + 1, C.b, C.x, s, false, fuse0);
         Csr A{L.srp, L.scol, L.sw, L.sd};
         launch_pdl(k_elim_prolong, eg(nc + L.nF), 256, s, nc, L.nF, L.cid_s, L.flist, L.fmap_s, A, b, C.x, xout);
         h->cur.launches++;
@@ -578,10 +607,19 @@ static void vcycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, c
     a.x = cur;
     a.y = L.r;
     spmv_level(h, L, EPI_RESID, a, s);
-    launch_pdl(k_restrict, grid_for(L.m * 8, 256, 148 * 8), 256, s, L.m, L.mem_ptr, L.members, L.r, C.b);
+    Pre0 p0;
+    const bool fuse0 = C.kind == KIND_AGG && (kc || !(l + 1 == h->dtail_level && C.dense)) && fuse_enabled();
+    if (fuse0) {
+        p0.d = C.sd;
+        p0.inv_theta = 1.0 / C.cheb_theta;
+        p0.x = C.x2;
+        p0.dv = C.dv;
+    }
+    launch_pdl(k_restrict, grid_for(L.m * 8, 256, 148 * 8), 256, s, L.m, L.mem_ptr, L.members, L.r, C.b, p0);
     h->cur.launches++;
     h->cur.bytes += 16 * n + 8 * L.m;
-    vcycle_rec(h, l + 1, C.b, C.x, s);
+    if (kc) kcoarse(h, l + 1, s, fuse0);
+    else cycle_rec(h, l + 1, C.b, C.x, s, false, fuse0);
     // prolongation x += P x_c (H4)
     launch_pdl(k_prolong, eg(n), 256, s, n, L.agg_s, C.x, cur);
     h->cur.launches++;
@@ -609,11 +647,103 @@ static void vcycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, c
 
 void vcycle(lap_hierarchy *h, int l, cudaStream_t s) {
     Level &L = h->lev[l];
-    vcycle_rec(h, l, L.b, L.x, s);
+    cycle_rec(h, l, L.b, L.x, s, false);
 }
 
 // exposed for lap_vcycle / PCG: z = V(0, r)
-void vcycle_apply(lap_hierarchy *h, const double *r, double *z, cudaStream_t s) { vcycle_rec(h, 0, r, z, s); }
+void vcycle_apply(lap_hierarchy *h, const double *r, double *z, cudaStream_t s) { cycle_rec(h, 0, r, z, s, false); }
+
+// ------------------------------------------------------------------ K-cycle (N2)
+// FCG(1) on level l, x = L.x from 0, b = L.b (oracle orc_kcoarse):
+//   k = 1 : p = K b ; q = L p ; alpha = p.b / p.q ; x = alpha p ; r = b - alpha q
+//   k > 1 : z = K r ; beta = -(z.q) / (p.q) ; p = z + beta p ; q = L p ;
+//           alpha = p.r / p.q ; x += alpha p ; r -= alpha q
+// p.q = 0 (zero right-hand side) gives alpha = beta = 0 (reading R-K2).
+// Launches per iteration after K: k = 1: the SpMV with both dots in its
+// epilogue (E_FCG) and the update; k > 1: z.q partials, the direction, the
+// SpMV, the update.  A consumer finishes its producer's per-block partials
+// itself (every block sums them in the same fixed order, so all blocks see
+// the same value): no separate reduction launches, no host round trip.
+__device__ __forceinline__ double block_total(const double *__restrict__ part, int np, double *sh) {
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < np; i += blockDim.x) acc += part[i];
+    double t = block_sum(acc, sh);
+    __syncthreads();
+    if (threadIdx.x == 0) sh[8] = t;
+    __syncthreads();
+    return sh[8];
+}
+__global__ void __launch_bounds__(256) k_fcg_dir(int64_t n, const double *__restrict__ z, double *__restrict__ p,
+                                                 const double *__restrict__ part, int np,
+                                                 const double *__restrict__ sc) {
+    pdl_begin();
+    __shared__ double sh[9];
+    const double zq = block_total(part, np, sh);
+    const double beta = sc[0] != 0.0 ? -zq / sc[0] : 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = z[i] + beta * p[i];
+}
+// part[0, np): p.q ; part[np, 2np): p.r   (E_FCG partials) ; sc[0] <- p.q for the next beta
+__global__ void __launch_bounds__(256) k_fcg_update(int64_t n, const double *__restrict__ p,
+                                                    const double *__restrict__ q, const double *rin, double *x,
+                                                    double *rout, const double *__restrict__ part, int np,
+                                                    double *__restrict__ sc, int first) {
+    pdl_begin();
+    __shared__ double sh[9];
+    const double pq = block_total(part, np, sh);
+    const double pr = block_total(part + np, np, sh);
+    const double alpha = pq != 0.0 ? pr / pq : 0.0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc[0] = pq;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        x[i] = first ? alpha * p[i] : x[i] + alpha * p[i];
+        rout[i] = rin[i] - alpha * q[i];
+    }
+}
+
+static void kcoarse(lap_hierarchy *h, int l, cudaStream_t s, bool pre0_done) {
+    Level &L = h->lev[l];
+    if (ktail_launch(h, l, pre0_done, s)) return;  // the whole sub-K-cycle in one CTA (ktail.cu)
+    if (L.kind != KIND_AGG) {  // elimination levels are not accelerated; coarsest: L^+
+        cycle_rec(h, l, L.b, L.x, s, true, pre0_done);
+        return;
+    }
+    const int64_t n = L.n;
+    const int np = (int)spmv_partial_slots(L);
+    double *sc = L.ksc;
+    for (int k = 1; k <= h->p.kcycle_inner; k++) {
+        const double *rin = k == 1 ? L.b : L.kr;
+        if (k == 1) {
+            cycle_rec(h, l, L.b, L.kp, s, true, pre0_done);
+        } else {
+            cycle_rec(h, l, L.kr, L.kz, s, true);
+            launch_pdl(k_dot_partial, RED_BLOCKS, 256, s, n, (const double *)L.kz, (const double *)L.kq,
+                       h->partials);
+            launch_pdl(k_fcg_dir, eg(n), 256, s, n, (const double *)L.kz, L.kp, (const double *)h->partials,
+                       (int)RED_BLOCKS, (const double *)sc);
+            h->cur.launches += 2;
+        }
+        EpiArgs a;
+        a.x = L.kp;
+        a.y = L.kq;
+        a.b = rin;
+        a.partials = h->partials;
+        spmv_level(h, L, (EpiKind)E_FCG, a, s);
+        launch_pdl(k_fcg_update, eg(n), 256, s, n, (const double *)L.kp, (const double *)L.kq, rin, L.x, L.kr,
+                   (const double *)h->partials, np, sc, k == 1 ? 1 : 0);
+        h->cur.launches++;
+        h->cur.bytes += (k == 1 ? 40 : 80) * n;
+    }
+    LAP_CHECK_LAUNCH();
+}
+
+// lap_kcycle: level-l input in L.b, output in L.x (storage order)
+void kcycle_level(lap_hierarchy *h, int l, bool with_fcg, cudaStream_t s) {
+    Level &L = h->lev[l];
+    if (with_fcg) kcoarse(h, l, s, false);
+    else cycle_rec(h, l, L.b, L.x, s, true);
+}
+// z = K(0, r) for the outer FCG
+void kcycle_apply(lap_hierarchy *h, const double *r, double *z, cudaStream_t s) { cycle_rec(h, 0, r, z, s, true); }
 
 // ------------------------------------------------------------------ PCG kernels
 // scal layout: 0 rho, 1 pq, 2 rr, 3 sum(z), 4 rho_new, 5 bnorm2, 6 tmp
@@ -717,10 +847,82 @@ __global__ void k_pcg_p2(int64_t n, const double *__restrict__ z, double *__rest
         p[i] = first ? z[i] - mean : (z[i] - mean) + beta * p[i];  // first: p is uninitialised (0*NaN must not leak)
 }
 
+// ---- outer FCG(1) with the K-cycle (N2; oracle orc_solve, cycle 1):
+//   z = K r ; z -= mean z ; beta = -(z.q)/(p.q) ; p = z + beta p ; alpha = p.r / p.q (spmv part)
+// q = L p_prev and p.q (scal 1) are the previous iteration's.  One pass over
+// z and q gives sum z, z.q and sum q: (z - mean z).q = z.q - mean(z) sum q.
+__global__ void __launch_bounds__(256) k_fcg_zsums(int64_t n, const double *__restrict__ z,
+                                                   const double *__restrict__ q, double *__restrict__ part, int first) {
+    pdl_begin();
+    __shared__ double sh[8];
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double zi = z[i];
+        a0 += zi;
+        if (!first) {
+            double qi = q[i];
+            a1 += zi * qi;
+            a2 += qi;
+        }
+    }
+    double t0 = block_sum(a0, sh), t1 = block_sum(a1, sh), t2 = block_sum(a2, sh);
+    if (threadIdx.x == 0) {
+        part[blockIdx.x] = t0;
+        part[gridDim.x + blockIdx.x] = t1;
+        part[2 * gridDim.x + blockIdx.x] = t2;
+    }
+}
+// scal: 1 p.q (previous), 3 sum z, 13 beta
+__global__ void __launch_bounds__(256) k_fcg_zfinish(int64_t n, const double *__restrict__ part, int np,
+                                                     double *__restrict__ sc, int first) {
+    pdl_begin();
+    __shared__ double sh[8];
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int i = threadIdx.x; i < np; i += blockDim.x) {
+        a0 += part[i];
+        a1 += part[np + i];
+        a2 += part[2 * np + i];
+    }
+    double t0 = block_sum(a0, sh), t1 = block_sum(a1, sh), t2 = block_sum(a2, sh);
+    if (threadIdx.x == 0) {
+        sc[3] = t0;
+        sc[13] = first ? 0.0 : -(t1 - (t0 / (double)n) * t2) / sc[1];
+    }
+}
+// p = (z - mean z) + beta p ; partial sums of p.r (-> scal 0, the alpha numerator of k_pcg_xr)
+__global__ void __launch_bounds__(256) k_fcg_p(int64_t n, const double *__restrict__ z, double *__restrict__ p,
+                                               const double *__restrict__ r, const double *__restrict__ sc,
+                                               double *__restrict__ part, int first) {
+    pdl_begin();
+    __shared__ double sh[8];
+    const double mean = sc[3] / (double)n, beta = sc[13];
+    double acc = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double pi = first ? z[i] - mean : (z[i] - mean) + beta * p[i];
+        p[i] = pi;
+        acc += pi * r[i];
+    }
+    double t = block_sum(acc, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
+void kcycle_apply(lap_hierarchy *h, const double *r, double *z, cudaStream_t s);
+
 static void pcg_precond_part(lap_hierarchy *h, bool first, bool inline_vcycle, cudaStream_t s) {
     Level &L0 = h->lev[0];
     int64_t n = L0.n;
     double *sc = h->scal;
+    if (h->p.cycle == 1) {  // FCG + K-cycle (never a separate graph: captured inline or eager)
+        kcycle_apply(h, h->pr, h->pz, s);
+        launch_pdl(k_fcg_zsums, RED_BLOCKS, 256, s, n, (const double *)h->pz, (const double *)h->pq, h->partials,
+                   first ? 1 : 0);
+        launch_pdl(k_fcg_zfinish, 1, 256, s, n, (const double *)h->partials, (int)RED_BLOCKS, sc, first ? 1 : 0);
+        launch_pdl(k_fcg_p, RED_BLOCKS, 256, s, n, (const double *)h->pz, h->pp, (const double *)h->pr,
+                   (const double *)sc, h->partials, first ? 1 : 0);
+        h->cur.launches += 3;
+        reduce_partials(h, h->partials, RED_BLOCKS, sc + 0, s);
+        return;
+    }
     if (inline_vcycle) vcycle_apply(h, h->pr, h->pz, s);
     else launch_vcycle(h, s);
     launch_pdl(k_pcg_zsums, RED_BLOCKS, 256, s, n, (const double *)h->pz, (const double *)h->pr, h->partials);
@@ -852,13 +1054,15 @@ void free_pcg(lap_hierarchy *h) {
 }
 
 // O-R30: confirm a recursive-residual stop with the true residual b - L x
+// (scratch: pz, free until the next preconditioner application; q = L p is
+// still needed by FCG's beta)
 static bool true_residual_ok(lap_hierarchy *h, double bn, double tol, cudaStream_t s) {
     EpiArgs t;
     t.x = h->px;
     t.b = h->pb;
-    t.y = h->pq;
+    t.y = h->pz;
     spmv_level(h, h->lev[0], EPI_RESID, t, s);
-    dot(h, h->pq, h->pq, h->lev[0].n, h->scal + 6, s);
+    dot(h, h->pz, h->pz, h->lev[0].n, h->scal + 6, s);
     double tr = read_scalar(h, h->scal + 6, s);
     return std::sqrt(tr) / bn <= tol;
 }
@@ -900,7 +1104,7 @@ void run_pcg(lap_hierarchy *h, double tol, int32_t *iters, double *relres, int *
                     *conv = 1;
                     break;
                 }
-                LAP_CUDA(cudaMemcpyAsync(h->pr, h->pq, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+                LAP_CUDA(cudaMemcpyAsync(h->pr, h->pz, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
             }
             if (k >= maxit) break;
             LAP_CUDA(cudaGraphLaunch(h->pcg_resume, s));
@@ -919,7 +1123,7 @@ void run_pcg(lap_hierarchy *h, double tol, int32_t *iters, double *relres, int *
                     *conv = 1;
                     break;
                 }
-                LAP_CUDA(cudaMemcpyAsync(h->pr, h->pq, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+                LAP_CUDA(cudaMemcpyAsync(h->pr, h->pz, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
             }
             if (k == maxit) break;
             pcg_precond_part(h, false, false, s);

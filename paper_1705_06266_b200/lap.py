@@ -39,6 +39,7 @@ class lap_params(ctypes.Structure):
         ("vote_threshold", ctypes.c_int32), ("coarse_nnz", ctypes.c_int64), ("max_levels", ctypes.c_int32),
         ("seed", ctypes.c_uint64), ("random_order", ctypes.c_int32), ("affinity_power", ctypes.c_int32),
         ("keep_strength", ctypes.c_int32), ("use_graphs", ctypes.c_int32), ("replicate_nnz", ctypes.c_int64),
+        ("cycle", ctypes.c_int32), ("kcycle_inner", ctypes.c_int32),
     ]
 
 
@@ -50,7 +51,7 @@ class lap_stats(ctypes.Structure):
 EXPORTS = [
     "lap_params_default", "lap_last_error", "lap_version", "lap_setup", "lap_solve", "lap_free",
     "lap_num_levels", "lap_level_info", "lap_level_export", "lap_level_strength", "lap_coarse_pinv",
-    "lap_perm", "lap_spmv", "lap_vcycle", "lap_get_stats", "lap_bench_op",
+    "lap_perm", "lap_spmv", "lap_vcycle", "lap_kcycle", "lap_get_stats", "lap_bench_op",
     "lap_nccl_unique_id", "lap_comm_create", "lap_comm_create_virtual", "lap_comm_info", "lap_comm_free",
     "lap_setup_dist", "lap_dist_index",
 ]
@@ -78,6 +79,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "lap_perm": (ctypes.c_int, [P, P]),
         "lap_spmv": (ctypes.c_int, [P, i32, P, P, P]),
         "lap_vcycle": (ctypes.c_int, [P, P, P, P]),
+        "lap_kcycle": (ctypes.c_int, [P, i32, i32, P, P, P]),
         "lap_get_stats": (ctypes.c_int, [P, ctypes.POINTER(lap_stats)]),
         "lap_bench_op": (ctypes.c_int, [P, i32, i32, i32, P, P, pdbl, pi64]),
         "lap_nccl_unique_id": (ctypes.c_int, [P]),
@@ -278,6 +280,14 @@ class Hierarchy:
         if z is None:
             z = np.zeros(len(r)) if not hasattr(r, "data_ptr") else r.new_zeros(len(r))
         _check(lib().lap_vcycle(self._h, _ptr(r), _ptr(z), _stream(stream)))
+        return z
+
+    def kcycle(self, l: int, r, with_fcg: bool = False, z=None, stream=None):
+        """z = K(l, r) on level l's internal numbering (N2); with_fcg: the
+        level's inner FCG iterations around it (oracle.Hierarchy.kcoarse)."""
+        if z is None:
+            z = np.zeros(len(r)) if not hasattr(r, "data_ptr") else r.new_zeros(len(r))
+        _check(lib().lap_kcycle(self._h, l, 1 if with_fcg else 0, _ptr(r), _ptr(z), _stream(stream)))
         return z
 
     def stats(self) -> dict:
