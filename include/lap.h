@@ -141,6 +141,16 @@ lap_status lap_coarse_pinv(const lap_hierarchy *h, double *pinv);
 lap_status lap_perm(const lap_hierarchy *h, int64_t *perm);
 /* y = L_l x on level l, internal numbering (H1). */
 lap_status lap_spmv(const lap_hierarchy *h, int32_t l, const double *x, double *y, void *cuda_stream);
+/* k right-hand sides at once (P:102-118 -- eigenvector / embedding
+ * uses solve many systems with one Laplacian).  Column j of B (n x k,
+ * column-major, caller numbering, host or device) is solved exactly as
+ * lap_solve would (its own projection, PCG + V-cycle, stopping rule; O-S8),
+ * but the k solves advance together so every pass over a level's matrix
+ * serves all columns (SpMM).  1 <= k <= 8.  X: n x k column-major, mean-zero
+ * columns.  iters[j], rel_residual[j]: per column (length k).  LAP_ENOCONV if
+ * any column reached max_iters.  Single-GPU hierarchies only. */
+lap_status lap_solve_block(lap_hierarchy *h, int32_t k, const double *B, double *X, double tol,
+                           int32_t *iters, double *rel_residual, void *cuda_stream);
 /* z = V(0, r): one V-cycle on the internal (permuted) level-0 numbering (O-S7). */
 lap_status lap_vcycle(lap_hierarchy *h, const double *r, double *z, void *cuda_stream);
 /* z = K(l, r): one K-cycle at level l: the V-cycle's

@@ -24,7 +24,8 @@ UNITS = {"setup.cu": ["-fmad=false", "-prec-div=true", "-prec-sqrt=true"],
          "lap_api.cu": [],
          "dist.cu": [],
          "tail.cu": [],
-         "ktail.cu": []}
+         "ktail.cu": [],
+         "block.cu": []}
 
 
 def _sources():

@@ -1,0 +1,691 @@
+// block.cu -- many right-hand sides at once.
+//
+// k independent PCG solves (O-S8 per column: same projection, stopping rule,
+// iteration count per column) advanced in lockstep so every pass over a
+// level's matrix serves all k vectors: the SpMV becomes an SpMM with the k
+// values of a row stored contiguously (row-major n x K block vectors, K the
+// compile-time width >= k, unused columns zero).  A gather of x_j then reads
+// K*8 contiguous bytes -- for K = 4 one 32-byte sector, the same sector count
+// as the single-vector gather -- so the matrix and index bytes (12 per
+// stored entry) and the gather sectors are amortised over K solves:
+//   bytes per nnz * rhs ~ 12/K + 8 (vs 12 + 8 per nnz for one vector).
+// The V-cycle is the single-vector one (solve.cu cycle_rec, V mode, per-level
+// path) with every kernel widened to K columns; the Chebyshev coefficients
+// are level constants, so all columns share them.  Columns that have
+// converged are frozen (alpha = beta = 0 for them) so each column's x and
+// iteration count are those of its own solve.  The V-cycle of the block is
+// captured once per (hierarchy, K) as a CUDA graph.
+#include "lap_internal.cuh"
+
+#include <cmath>
+#include <vector>
+
+namespace lap {
+
+constexpr int BLK_RED = 296;  // fixed reduction geometry (deterministic)
+
+__device__ __forceinline__ double blk_block_sum(double v, double *sh) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (wid == 0) {
+        r = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    }
+    return r;  // thread 0
+}
+
+template <int K>
+struct Vk {
+    double v[K];
+};
+template <int K>
+__device__ __forceinline__ Vk<K> ldk(const double *p) {  // K contiguous doubles (16-byte aligned rows)
+    Vk<K> r;
+    if (K % 2 == 0) {
+#pragma unroll
+        for (int c = 0; c < K; c += 2) {
+            double2 t = __ldg((const double2 *)(p + c));
+            r.v[c] = t.x;
+            r.v[c + 1] = t.y;
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < K; c++) r.v[c] = __ldg(p + c);
+    }
+    return r;
+}
+
+enum { BE_DOT = 0, BE_RESID = 1, BE_CHEB = 2, BE_CHEB0 = 3 };
+struct BArgs {
+    const double *x;
+    double *y;
+    const double *b;
+    double *dv;
+    double c1, c2;
+    double *partials;  // BE_DOT: [K][grid]
+};
+
+// y = epilogue(L X) for a block of K columns.  Short rows (SELL-32 slices,
+// coalesced index/weight loads, a thread per row); rows longer than
+// SHORT_MAX a warp per row over the CSR (lane-strided, shuffle tree).
+template <int EPI, int K>
+__global__ void __launch_bounds__(256) k_blk_spmv(int64_t nslices, int64_t nshort, int64_t n,
+                                                  const int64_t *__restrict__ sp, const int32_t *__restrict__ ec,
+                                                  const double *__restrict__ ew, const int64_t *__restrict__ rp,
+                                                  const int32_t *__restrict__ col, const double *__restrict__ w,
+                                                  const double *__restrict__ d, BArgs a) {
+    pdl_begin();
+    __shared__ double sh[8];
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double dacc[K];
+#pragma unroll
+    for (int c = 0; c < K; c++) dacc[c] = 0.0;
+    auto epi = [&](int64_t i, const double *ax) {
+        const double di = d[i];
+        const Vk<K> xi = ldk<K>(a.x + i * K);
+#pragma unroll
+        for (int c = 0; c < K; c++) {
+            const double lx = di * xi.v[c] - ax[c];
+            if (EPI == BE_DOT) {
+                a.y[i * K + c] = lx;
+                dacc[c] += xi.v[c] * lx;
+            } else if (EPI == BE_RESID) {
+                a.y[i * K + c] = a.b[i * K + c] - lx;
+            } else if (EPI == BE_CHEB) {
+                double v = a.c1 * a.dv[i * K + c] + a.c2 * ((a.b[i * K + c] - lx) / di);
+                a.dv[i * K + c] = v;
+                a.y[i * K + c] = xi.v[c] + v;
+            } else {  // BE_CHEB0
+                double v = a.c2 * ((a.b[i * K + c] - lx) / di);
+                a.dv[i * K + c] = v;
+                a.y[i * K + c] = xi.v[c] + v;
+            }
+        }
+    };
+    const int64_t nlong = n - nshort;
+    for (int64_t t = warp; t < nslices + nlong; t += nwarps) {
+        if (t < nslices) {
+            const int64_t i = t * 32 + lane, beg = sp[t], end = sp[t + 1];
+            const int width = (int)((end - beg) >> 5);
+            double ax[K];
+#pragma unroll
+            for (int c = 0; c < K; c++) ax[c] = 0.0;
+            for (int q = 0; q < width; q++) {
+                const int32_t j = __ldg(&ec[beg + (int64_t)q * 32 + lane]);
+                const double wv = __ldg(&ew[beg + (int64_t)q * 32 + lane]);
+                const Vk<K> xj = ldk<K>(a.x + (int64_t)j * K);
+#pragma unroll
+                for (int c = 0; c < K; c++) ax[c] += wv * xj.v[c];
+            }
+            if (i < nshort) epi(i, ax);
+        } else {
+            const int64_t i = nshort + (t - nslices);
+            double ax[K];
+#pragma unroll
+            for (int c = 0; c < K; c++) ax[c] = 0.0;
+            for (int64_t q = rp[i] + lane; q < rp[i + 1]; q += 32) {
+                const double wv = __ldg(&w[q]);
+                const Vk<K> xj = ldk<K>(a.x + (int64_t)__ldg(&col[q]) * K);
+#pragma unroll
+                for (int c = 0; c < K; c++) ax[c] += wv * xj.v[c];
+            }
+#pragma unroll
+            for (int c = 0; c < K; c++)
+                for (int o = 16; o > 0; o >>= 1) ax[c] += __shfl_xor_sync(0xffffffffu, ax[c], o);
+            if (lane == 0) epi(i, ax);
+        }
+    }
+    if (EPI == BE_DOT) {
+#pragma unroll
+        for (int c = 0; c < K; c++) {
+            double r = blk_block_sum(dacc[c], sh);
+            if (threadIdx.x == 0) a.partials[c * gridDim.x + blockIdx.x] = r;
+        }
+    }
+}
+
+template <int K>
+__global__ void k_blk_cheb_first(int64_t n, const double *__restrict__ b, const double *__restrict__ d,
+                                 double inv_theta, double *__restrict__ x, double *__restrict__ dv) {
+    pdl_begin();
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * K; t += (int64_t)gridDim.x * blockDim.x) {
+        double v = (b[t] / d[t / K]) * inv_theta;
+        dv[t] = v;
+        x[t] = v;
+    }
+}
+template <int K>
+__global__ void k_blk_restrict(int64_t m, const int64_t *__restrict__ mp, const int32_t *__restrict__ mem,
+                               const double *__restrict__ r, double *__restrict__ rc) {
+    pdl_begin();
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m * K; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = t / K;
+        const int c = (int)(t - a * K);
+        double acc = 0.0;
+        for (int64_t q = mp[a]; q < mp[a + 1]; q++) acc += r[(int64_t)mem[q] * K + c];
+        rc[t] = acc;
+    }
+}
+template <int K>
+__global__ void k_blk_prolong(int64_t n, const int32_t *__restrict__ agg, const double *__restrict__ xc,
+                              double *__restrict__ x) {
+    pdl_begin();
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * K; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / K;
+        x[t] += xc[(int64_t)agg[i] * K + (t - i * K)];
+    }
+}
+template <int K>
+__global__ void k_blk_elim_restrict(int64_t nc, const int32_t *__restrict__ cid, const int64_t *__restrict__ ctp,
+                                    const int32_t *__restrict__ ctf, const double *__restrict__ ctc,
+                                    const double *__restrict__ b, double *__restrict__ bc) {
+    pdl_begin();
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nc * K; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = t / K;
+        const int c = (int)(t - k * K);
+        double s = b[(int64_t)cid[k] * K + c];
+        for (int64_t q = ctp[k]; q < ctp[k + 1]; q++) s += ctc[q] * b[(int64_t)ctf[q] * K + c];
+        bc[t] = s;
+    }
+}
+template <int K>
+__global__ void k_blk_elim_prolong(int64_t nc, int64_t nf, const int32_t *__restrict__ cid,
+                                   const int32_t *__restrict__ flist, const int32_t *__restrict__ fmap,
+                                   const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                                   const double *__restrict__ w, const double *__restrict__ d,
+                                   const double *__restrict__ b, const double *__restrict__ xc,
+                                   double *__restrict__ x) {
+    pdl_begin();
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (nc + nf) * K;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t u = t / K;
+        const int c = (int)(t - u * K);
+        if (u < nc) {
+            x[(int64_t)cid[u] * K + c] = xc[t];
+        } else {
+            const int64_t f = flist[u - nc];
+            double s = b[f * K + c];
+            for (int64_t q = rp[f]; q < rp[f + 1]; q++) s += w[q] * xc[(int64_t)fmap[col[q]] * K + c];
+            x[f * K + c] = s / d[f];
+        }
+    }
+}
+template <int K>
+__global__ void k_blk_coarse(int64_t n, const double *__restrict__ P, const double *__restrict__ b,
+                             double *__restrict__ x) {
+    pdl_begin();
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < n; i += nwarps) {
+        double acc[K];
+#pragma unroll
+        for (int c = 0; c < K; c++) acc[c] = 0.0;
+        for (int64_t j = lane; j < n; j += 32) {
+            const double p = P[i * n + j];
+#pragma unroll
+            for (int c = 0; c < K; c++) acc[c] += p * b[j * K + c];
+        }
+#pragma unroll
+        for (int c = 0; c < K; c++) {
+            for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], o);
+            if (lane == 0) x[i * K + c] = acc[c];
+        }
+    }
+}
+
+// ---- per-column PCG vector operations (scalars: sc[16 * c + slot])
+//   slots: 0 rho, 1 pq, 2 rr, 3 sum z, 4 active (1/0), 5 ||b||^2, 6 sum r, 7 beta
+template <int K, int NS>
+__global__ void __launch_bounds__(256) k_blk_sums(int64_t n, const double *__restrict__ a0, const double *__restrict__ a1,
+                                                  const double *__restrict__ a2, double *__restrict__ part) {
+    // NS = 1: sum a0*a1 ; NS = 3: sum a0, sum a0*a1, sum a1 (z, r) ; per column
+    pdl_begin();
+    __shared__ double sh[8];
+    double s0[K], s1[K], s2[K];
+#pragma unroll
+    for (int c = 0; c < K; c++) s0[c] = s1[c] = s2[c] = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int c = 0; c < K; c++) {
+            const double x0 = a0[i * K + c], x1 = a1 ? a1[i * K + c] : 1.0;
+            if (NS == 1) {
+                s0[c] += x0 * x1;
+            } else {
+                s0[c] += x0;
+                s1[c] += x0 * x1;
+                s2[c] += x1;
+            }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < K; c++) {
+        double t0 = blk_block_sum(s0[c], sh);
+        if (threadIdx.x == 0) part[(NS * c) * gridDim.x + blockIdx.x] = t0;
+        if (NS == 3) {
+            double t1 = blk_block_sum(s1[c], sh), t2 = blk_block_sum(s2[c], sh);
+            if (threadIdx.x == 0) {
+                part[(NS * c + 1) * gridDim.x + blockIdx.x] = t1;
+                part[(NS * c + 2) * gridDim.x + blockIdx.x] = t2;
+            }
+        }
+    }
+}
+// reduce nv groups of np partials each; group g -> column g / per, slot sl[g % per]
+__global__ void k_blk_reduce(const double *__restrict__ part, int np, int nv, int per, double *__restrict__ sc, int s0,
+                             int s1, int s2) {
+    pdl_begin();
+    __shared__ double sh[8];
+    for (int g = 0; g < nv; g++) {
+        double acc = 0.0;
+        for (int i = threadIdx.x; i < np; i += blockDim.x) acc += part[(int64_t)g * np + i];
+        double r = blk_block_sum(acc, sh);
+        const int j = g % per;
+        if (threadIdx.x == 0) sc[16 * (g / per) + (j == 0 ? s0 : j == 1 ? s1 : s2)] = r;
+    }
+}
+// per column: rho' = r.(z - mean z) = r.z - mean(z) sum r ; beta = rho'/rho (0 first / frozen)
+template <int K>
+__global__ void k_blk_zfinish(int64_t n, double *__restrict__ sc, int first) {
+    pdl_begin();
+    const int c = threadIdx.x;
+    if (c >= K) return;
+    double *s = sc + 16 * c;
+    const double rho_new = s[8] - (s[3] / (double)n) * s[6];
+    s[7] = (first || s[4] == 0.0) ? 0.0 : rho_new / s[0];
+    s[0] = rho_new;
+}
+template <int K>
+__global__ void k_blk_p(int64_t n, const double *__restrict__ z, double *__restrict__ p, const double *__restrict__ sc,
+                        int first) {
+    pdl_begin();
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * K; t += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(t % K);
+        const double *s = sc + 16 * c;
+        const double zm = z[t] - s[3] / (double)n;
+        p[t] = first ? zm : zm + s[7] * p[t];
+    }
+}
+// x += alpha p ; r -= alpha q (active columns) ; partial r.r
+template <int K>
+__global__ void __launch_bounds__(256) k_blk_xr(int64_t n, const double *__restrict__ p, const double *__restrict__ q,
+                                                double *__restrict__ x, double *__restrict__ r,
+                                                const double *__restrict__ sc, double *__restrict__ part) {
+    pdl_begin();
+    __shared__ double sh[8];
+    double alpha[K], acc[K];
+#pragma unroll
+    for (int c = 0; c < K; c++) {
+        const double *s = sc + 16 * c;
+        alpha[c] = (s[4] != 0.0 && s[1] != 0.0) ? s[0] / s[1] : 0.0;
+        acc[c] = 0.0;
+    }
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int c = 0; c < K; c++) {
+            x[i * K + c] += alpha[c] * p[i * K + c];
+            const double ri = r[i * K + c] - alpha[c] * q[i * K + c];
+            r[i * K + c] = ri;
+            acc[c] += ri * ri;
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < K; c++) {
+        double t = blk_block_sum(acc[c], sh);
+        if (threadIdx.x == 0) part[c * gridDim.x + blockIdx.x] = t;
+    }
+}
+// caller layout (n x k column-major, caller numbering) <-> block layout (storage order, row-major n x K)
+template <int K>
+__global__ void k_blk_in(int64_t n, int k, const int64_t *__restrict__ cmap, const double *__restrict__ B,
+                         double *__restrict__ out) {
+    pdl_begin();
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * K; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / K;
+        const int c = (int)(t - i * K);
+        out[cmap[i] * K + c] = c < k ? B[(int64_t)c * n + i] : 0.0;
+    }
+}
+template <int K>
+__global__ void k_blk_out(int64_t n, int k, const int64_t *__restrict__ cmap, const double *__restrict__ in,
+                          const double *__restrict__ sc, double *__restrict__ X) {
+    pdl_begin();
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * k; t += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(t / n);
+        const int64_t i = t - (int64_t)c * n;
+        X[t] = in[cmap[i] * K + c] - sc[16 * c + 3] / (double)n;  // x -= mean x (per column)
+    }
+}
+template <int K>
+__global__ void k_blk_sub_mean(int64_t n, double *__restrict__ v, const double *__restrict__ sc, int slot) {
+    pdl_begin();
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * K; t += (int64_t)gridDim.x * blockDim.x)
+        v[t] -= sc[16 * (t % K) + slot] / (double)n;
+}
+
+// ------------------------------------------------------------------ host
+struct BlockWork {  // per (hierarchy, K)
+    int K = 0;
+    std::vector<double *> lb, lx, lx2, lt, lr, ldv;  // per level, n_l x K
+    double *b = nullptr, *x = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr;
+    double *sc = nullptr, *part = nullptr;
+    double *hsc = nullptr;  // pinned host copy of the scalars
+    cudaGraphExec_t vgraph = nullptr;
+    Stats vcounts;
+};
+
+static inline unsigned beg(int64_t n) { return grid_for(n, 256, 148 * 8); }
+
+template <int K>
+static void blk_spmv(lap_hierarchy *h, const Level &L, int epi, const BArgs &a, cudaStream_t s, unsigned grid) {
+    const int64_t nlong = L.n - L.c_end[0];
+#define BLK_LAUNCH(E)                                                                                             \
+    launch_pdl(k_blk_spmv<E, K>, grid, 256, s, L.nslices, L.c_end[0], L.n, (const int64_t *)L.slice_ptr,         \
+               (const int32_t *)L.ell_col, (const double *)L.ell_w, (const int64_t *)L.srp,                       \
+               (const int32_t *)L.scol, (const double *)L.sw, (const double *)L.sd, a)
+    switch (epi) {
+        case BE_DOT: BLK_LAUNCH(BE_DOT); break;
+        case BE_RESID: BLK_LAUNCH(BE_RESID); break;
+        case BE_CHEB: BLK_LAUNCH(BE_CHEB); break;
+        default: BLK_LAUNCH(BE_CHEB0); break;
+    }
+#undef BLK_LAUNCH
+    (void)nlong;
+    h->cur.launches++;
+    h->cur.edges += L.nnz * K;
+    h->cur.bytes += 12 * L.nnz + (int64_t)(8 * K) * L.nnz + (int64_t)(40 * K) * L.n;
+}
+template <int K>
+static unsigned spmm_grid(const Level &L) {
+    return grid_for((L.nslices + (L.n - L.c_end[0])) * 32, 256, 148 * 8);
+}
+
+// V-cycle on K columns (solve.cu cycle_rec, V mode, per-level kernels)
+template <int K>
+static void blk_vcycle(lap_hierarchy *h, BlockWork &W, int l, const double *b, double *xout, cudaStream_t s) {
+    Level &L = h->lev[l];
+    const int64_t n = L.n;
+    if (L.kind == KIND_COARSEST) {
+        launch_pdl(k_blk_coarse<K>, grid_for(n * 32, 256, 148), 256, s, n, (const double *)L.pinv_s, b, xout);
+        h->cur.launches++;
+        return;
+    }
+    Level &C = h->lev[l + 1];
+    double *cb = W.lb[l + 1], *cx = W.lx[l + 1];
+    if (L.kind == KIND_ELIM) {
+        launch_pdl(k_blk_elim_restrict<K>, beg(C.n * K), 256, s, C.n, (const int32_t *)L.cid_s,
+                   (const int64_t *)L.ct_ptr_s, (const int32_t *)L.ct_f_s, (const double *)L.ct_coef_s, b, cb);
+        blk_vcycle<K>(h, W, l + 1, cb, cx, s);
+        launch_pdl(k_blk_elim_prolong<K>, beg((C.n + L.nF) * K), 256, s, C.n, L.nF, (const int32_t *)L.cid_s,
+                   (const int32_t *)L.flist, (const int32_t *)L.fmap_s, (const int64_t *)L.srp,
+                   (const int32_t *)L.scol, (const double *)L.sw, (const double *)L.sd, b, (const double *)cx, xout);
+        h->cur.launches += 2;
+        return;
+    }
+    const int Kd = h->p.cheby_degree;
+    const double theta = L.cheb_theta, delta = L.cheb_delta, sigma = L.cheb_sigma;
+    double *cur = W.lx2[l], *alt = W.lt[l];
+    const unsigned g = spmm_grid<K>(L);
+    launch_pdl(k_blk_cheb_first<K>, beg(n * K), 256, s, n, b, (const double *)L.sd, 1.0 / theta, cur, W.ldv[l]);
+    h->cur.launches++;
+    double rho_old = 1.0 / sigma;
+    BArgs a{};
+    a.b = b;
+    a.dv = W.ldv[l];
+    for (int k = 1; k < Kd; k++) {
+        double rho = 1.0 / (2.0 * sigma - rho_old);
+        a.c1 = rho * rho_old;
+        a.c2 = 2.0 * rho / delta;
+        a.x = cur;
+        a.y = alt;
+        blk_spmv<K>(h, L, BE_CHEB, a, s, g);
+        std::swap(cur, alt);
+        rho_old = rho;
+    }
+    a.x = cur;
+    a.y = W.lr[l];
+    blk_spmv<K>(h, L, BE_RESID, a, s, g);
+    launch_pdl(k_blk_restrict<K>, beg(L.m * K), 256, s, L.m, (const int64_t *)L.mem_ptr, (const int32_t *)L.members,
+               (const double *)W.lr[l], cb);
+    blk_vcycle<K>(h, W, l + 1, cb, cx, s);
+    launch_pdl(k_blk_prolong<K>, beg(n * K), 256, s, n, (const int32_t *)L.agg_s, (const double *)cx, cur);
+    h->cur.launches += 2;
+    rho_old = 1.0 / sigma;
+    for (int k = 0; k < Kd; k++) {
+        double *dst = (k == Kd - 1) ? xout : alt;
+        a.x = cur;
+        a.y = dst;
+        if (k == 0) {
+            a.c1 = 0.0;
+            a.c2 = 1.0 / theta;
+            blk_spmv<K>(h, L, BE_CHEB0, a, s, g);
+        } else {
+            double rho = 1.0 / (2.0 * sigma - rho_old);
+            a.c1 = rho * rho_old;
+            a.c2 = 2.0 * rho / delta;
+            blk_spmv<K>(h, L, BE_CHEB, a, s, g);
+            rho_old = rho;
+        }
+        if (k < Kd - 1) std::swap(cur, alt);
+    }
+}
+
+template <int K>
+static BlockWork *block_work(lap_hierarchy *h, cudaStream_t s) {
+    std::vector<void *> &cache = h->blk;
+    for (void *p : cache)
+        if (((BlockWork *)p)->K == K) return (BlockWork *)p;
+    BlockWork *W = new BlockWork();
+    W->K = K;
+    for (auto &L : h->lev) {
+        const size_t bytes = 8 * (size_t)K * (size_t)(L.n > 0 ? L.n : 1);
+        W->lb.push_back((double *)dalloc(bytes, s));
+        W->lx.push_back((double *)dalloc(bytes, s));
+        W->lx2.push_back((double *)dalloc(bytes, s));
+        W->lt.push_back((double *)dalloc(bytes, s));
+        W->lr.push_back((double *)dalloc(bytes, s));
+        W->ldv.push_back((double *)dalloc(bytes, s));
+    }
+    const size_t b0 = 8 * (size_t)K * (size_t)h->lev[0].n;
+    double **vs[] = {&W->b, &W->x, &W->r, &W->z, &W->p, &W->q};
+    for (double **v : vs) *v = (double *)dalloc(b0, s);
+    W->sc = (double *)dalloc(8 * 16 * K, s);
+    int64_t np = BLK_RED;
+    for (auto &L : h->lev) np = std::max<int64_t>(np, (int64_t)spmm_grid<K>(L));
+    W->part = (double *)dalloc(8 * 3 * K * (size_t)np, s);
+    LAP_CUDA(cudaMallocHost(&W->hsc, 8 * 16 * K));
+    // the block V-cycle as one graph
+    cudaStream_t cs;
+    LAP_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    LAP_CUDA(cudaStreamSynchronize(s));
+    Stats save = h->cur;
+    h->cur = Stats{};
+    cudaGraph_t g;
+    LAP_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    blk_vcycle<K>(h, *W, 0, W->r, W->z, cs);
+    LAP_CUDA(cudaStreamEndCapture(cs, &g));
+    W->vcounts = h->cur;
+    h->cur = save;
+    LAP_CUDA(cudaGraphInstantiate(&W->vgraph, g, 0));
+    LAP_CUDA(cudaGraphDestroy(g));
+    LAP_CUDA(cudaStreamDestroy(cs));
+    cache.push_back(W);
+    return W;
+}
+
+void free_block(lap_hierarchy *h) {
+    for (void *p : h->blk) {
+        BlockWork *W = (BlockWork *)p;
+        if (W->vgraph) cudaGraphExecDestroy(W->vgraph);
+        for (auto *v : {&W->lb, &W->lx, &W->lx2, &W->lt, &W->lr, &W->ldv})
+            for (double *q : *v) dfree(q, nullptr);
+        for (double *q : {W->b, W->x, W->r, W->z, W->p, W->q, W->sc, W->part}) dfree(q, nullptr);
+        if (W->hsc) cudaFreeHost(W->hsc);
+        delete W;
+    }
+    h->blk.clear();
+}
+
+template <int K>
+static void blk_launch_vcycle(lap_hierarchy *h, BlockWork &W, cudaStream_t s) {
+    LAP_CUDA(cudaGraphLaunch(W.vgraph, s));
+    h->cur.launches += W.vcounts.launches;
+    h->cur.edges += W.vcounts.edges;
+    h->cur.bytes += W.vcounts.bytes;
+}
+
+// per-column scalar slots (sc[16 c + slot]):
+enum { S_RHO = 0, S_PQ = 1, S_RR = 2, S_SUMZ = 3, S_ACTIVE = 4, S_BB = 5, S_SUMR = 6, S_BETA = 7, S_RZ = 8,
+       S_TMP = 9, S_TRUE = 10 };
+
+template <int K, int NS>
+static void blk_sums(lap_hierarchy *h, BlockWork &W, const double *a0, const double *a1, int s0, int s1, int s2,
+                     cudaStream_t s) {
+    const int64_t n = h->lev[0].n;
+    launch_pdl(k_blk_sums<K, NS>, BLK_RED, 256, s, n, a0, a1, (const double *)nullptr, W.part);
+    launch_pdl(k_blk_reduce, 1, 256, s, (const double *)W.part, BLK_RED, NS * K, NS, W.sc, s0, s1, s2);
+    h->cur.launches += 2;
+}
+
+// z = V(r) ; z -= mean z ; rho' = r.z ; p = z + (rho'/rho) p   (O-S8, per column)
+template <int K>
+static void blk_precond(lap_hierarchy *h, BlockWork &W, bool first, cudaStream_t s) {
+    const int64_t n = h->lev[0].n;
+    blk_launch_vcycle<K>(h, W, s);
+    blk_sums<K, 3>(h, W, W.z, W.r, S_SUMZ, S_RZ, S_SUMR, s);
+    launch_pdl(k_blk_zfinish<K>, 1, 32, s, n, W.sc, first ? 1 : 0);
+    launch_pdl(k_blk_p<K>, beg(n * K), 256, s, n, (const double *)W.z, W.p, (const double *)W.sc, first ? 1 : 0);
+    h->cur.launches += 2;
+}
+// q = L p ; pq ; x += alpha p ; r -= alpha q ; rr
+template <int K>
+static void blk_spmv_part(lap_hierarchy *h, BlockWork &W, cudaStream_t s) {
+    const Level &L0 = h->lev[0];
+    const int64_t n = L0.n;
+    const unsigned g = spmm_grid<K>(L0);
+    BArgs a{};
+    a.x = W.p;
+    a.y = W.q;
+    a.partials = W.part;
+    blk_spmv<K>(h, L0, BE_DOT, a, s, g);
+    launch_pdl(k_blk_reduce, 1, 256, s, (const double *)W.part, (int)g, K, 1, W.sc, (int)S_PQ, 0, 0);
+    launch_pdl(k_blk_xr<K>, BLK_RED, 256, s, n, (const double *)W.p, (const double *)W.q, W.x, W.r,
+               (const double *)W.sc, W.part);
+    launch_pdl(k_blk_reduce, 1, 256, s, (const double *)W.part, BLK_RED, K, 1, W.sc, (int)S_RR, 0, 0);
+    h->cur.launches += 3;
+}
+template <int K>
+__global__ void k_blk_copy_cols(int64_t n, const double *__restrict__ src, double *__restrict__ dst,
+                                const double *__restrict__ sc) {
+    pdl_begin();  // columns with sc[S_TMP] != 0
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * K; t += (int64_t)gridDim.x * blockDim.x)
+        if (sc[16 * (t % K) + S_TMP] != 0.0) dst[t] = src[t];
+}
+
+template <int K>
+static void solve_block_k(lap_hierarchy *h, int k, const double *B, double *X, double tol, int32_t *iters,
+                          double *relres, int *conv, cudaStream_t s) {
+    BlockWork &W = *block_work<K>(h, s);
+    const Level &L0 = h->lev[0];
+    const int64_t n = L0.n;
+    const int maxit = h->p.max_iters;
+    double *hs = W.hsc;
+    auto pull = [&]() {
+        LAP_CUDA(cudaMemcpyAsync(hs, W.sc, 8 * 16 * K, cudaMemcpyDeviceToHost, s));
+        LAP_CUDA(cudaStreamSynchronize(s));
+    };
+    auto push = [&]() { LAP_CUDA(cudaMemcpyAsync(W.sc, hs, 8 * 16 * K, cudaMemcpyHostToDevice, s)); };
+    // b' = Pi b per column, projected; x = 0 ; r = b
+    launch_pdl(k_blk_in<K>, beg(n * K), 256, s, n, k, (const int64_t *)h->cmap, B, W.b);
+    h->cur.launches++;
+    blk_sums<K, 1>(h, W, W.b, nullptr, S_TMP, 0, 0, s);
+    launch_pdl(k_blk_sub_mean<K>, beg(n * K), 256, s, n, W.b, (const double *)W.sc, (int)S_TMP);
+    h->cur.launches++;
+    blk_sums<K, 1>(h, W, W.b, W.b, S_BB, 0, 0, s);
+    LAP_CUDA(cudaMemsetAsync(W.x, 0, 8 * (size_t)K * n, s));
+    LAP_CUDA(cudaMemcpyAsync(W.r, W.b, 8 * (size_t)K * n, cudaMemcpyDeviceToDevice, s));
+    pull();
+    std::vector<double> bn(K);
+    int nactive = 0;
+    for (int c = 0; c < K; c++) {
+        bn[c] = std::sqrt(hs[16 * c + S_BB]);
+        const bool act = c < k && bn[c] > 0.0;
+        hs[16 * c + S_ACTIVE] = act ? 1.0 : 0.0;
+        if (c < k) iters[c] = 0;
+        nactive += act;
+    }
+    push();
+    int it = 0;
+    if (nactive) {
+        blk_precond<K>(h, W, true, s);
+        for (it = 1; it <= maxit; it++) {
+            blk_spmv_part<K>(h, W, s);
+            pull();
+            bool check = false;
+            for (int c = 0; c < K; c++)
+                if (hs[16 * c + S_ACTIVE] != 0.0 && std::sqrt(hs[16 * c + S_RR]) / bn[c] <= tol) check = true;
+            if (check) {  // O-R30: confirm with the true residual b - L x (into z: free until the next V-cycle)
+                BArgs t{};
+                t.x = W.x;
+                t.b = W.b;
+                t.y = W.z;
+                blk_spmv<K>(h, L0, BE_RESID, t, s, spmm_grid<K>(L0));
+                blk_sums<K, 1>(h, W, W.z, W.z, S_TRUE, 0, 0, s);
+                pull();
+                bool any_bad = false;
+                for (int c = 0; c < K; c++) {
+                    hs[16 * c + S_TMP] = 0.0;
+                    if (hs[16 * c + S_ACTIVE] == 0.0 || !(std::sqrt(hs[16 * c + S_RR]) / bn[c] <= tol)) continue;
+                    if (std::sqrt(hs[16 * c + S_TRUE]) / bn[c] <= tol) {
+                        hs[16 * c + S_ACTIVE] = 0.0;  // converged: frozen from here on
+                        iters[c] = it;
+                        nactive--;
+                    } else {
+                        hs[16 * c + S_TMP] = 1.0;  // restart this column from its true residual
+                        any_bad = true;
+                    }
+                }
+                push();
+                if (any_bad) {
+                    launch_pdl(k_blk_copy_cols<K>, beg(n * K), 256, s, n, (const double *)W.z, W.r, (const double *)W.sc);
+                    h->cur.launches++;
+                }
+            }
+            if (nactive == 0 || it == maxit) break;
+            blk_precond<K>(h, W, false, s);
+            LAP_CHECK_LAUNCH();
+        }
+    }
+    *conv = nactive == 0 ? 1 : 0;
+    for (int c = 0; c < k; c++)
+        if (hs[16 * c + S_ACTIVE] != 0.0) iters[c] = it < maxit ? it : maxit;
+    // x -= mean x (per column, in k_blk_out) ; true relative residuals
+    blk_sums<K, 1>(h, W, W.x, nullptr, S_SUMZ, 0, 0, s);
+    BArgs t{};
+    t.x = W.x;
+    t.b = W.b;
+    t.y = W.z;
+    blk_spmv<K>(h, L0, BE_RESID, t, s, spmm_grid<K>(L0));
+    blk_sums<K, 1>(h, W, W.z, W.z, S_TRUE, 0, 0, s);
+    launch_pdl(k_blk_out<K>, beg(n * k), 256, s, n, k, (const int64_t *)h->cmap, (const double *)W.x,
+               (const double *)W.sc, X);
+    h->cur.launches++;
+    pull();
+    for (int c = 0; c < k; c++) relres[c] = bn[c] > 0.0 ? std::sqrt(hs[16 * c + S_TRUE]) / bn[c] : 0.0;
+}
+
+// k right-hand sides (1 <= k <= 8), device buffers in the caller's layout: B, X n x k column-major
+void solve_block(lap_hierarchy *h, int k, const double *B, double *X, double tol, int32_t *iters, double *relres,
+                 int *conv, cudaStream_t s) {
+    if (k <= 2) solve_block_k<2>(h, k, B, X, tol, iters, relres, conv, s);
+    else if (k <= 4) solve_block_k<4>(h, k, B, X, tol, iters, relres, conv, s);
+    else solve_block_k<8>(h, k, B, X, tol, iters, relres, conv, s);
+}
+
+}  // namespace lap

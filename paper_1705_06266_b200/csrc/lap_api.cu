@@ -393,6 +393,7 @@ void lap_free(lap_hierarchy *h) {
     lap::free_dist(h);
     lap::free_pcg(h);
     lap::free_ktail(h, s);
+    lap::free_block(h);
     for (auto &L : h->lev) lap::free_level(L, s);
     void *ps[] = {h->perm, h->cmap, h->pb, h->px, h->pr, h->pz, h->pp, h->pq, h->scal, h->partials, h->stage_in,
                   h->stage_out};
@@ -452,6 +453,43 @@ lap_status lap_solve(lap_hierarchy *h, const double *b, double *x, double tol, i
     h->stats.spmv_bytes = h->cur.bytes;
     if (iters) *iters = it;
     if (rel_residual) *rel_residual = rr;
+    return conv ? LAP_OK : LAP_ENOCONV;
+    LAP_API_END
+}
+
+lap_status lap_solve_block(lap_hierarchy *h, int32_t k, const double *B, double *X, double tol, int32_t *iters,
+                           double *rel_residual, void *stream) {
+    if (!h || !B || !X || !iters || !rel_residual || k < 1 || k > 8 || h->dist) {
+        lap::set_error("lap_solve_block: invalid arguments (1 <= k <= 8, single-GPU hierarchy)");
+        return LAP_EINVAL;
+    }
+    LAP_API_BEGIN
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t n = h->n0;
+    cudaEvent_t e0, e1;
+    LAP_CUDA(cudaEventCreate(&e0));
+    LAP_CUDA(cudaEventCreate(&e1));
+    h->cur = lap::Stats{};
+    const bool bdev = lap::is_device_ptr(B), xdev = lap::is_device_ptr(X);
+    lap::DBuf<double> bin, xout;
+    if (!bdev) bin.alloc(n * k, s);
+    if (!xdev) xout.alloc(n * k, s);
+    LAP_CUDA(cudaEventRecord(e0, s));
+    if (!bdev) LAP_CUDA(cudaMemcpyAsync(bin.p, B, 8 * (size_t)(n * k), cudaMemcpyHostToDevice, s));
+    int conv = 0;
+    lap::solve_block(h, k, bdev ? B : bin.p, xdev ? X : xout.p, tol > 0 ? tol : h->p.tol, iters, rel_residual, &conv,
+                     s);
+    if (!xdev) LAP_CUDA(cudaMemcpyAsync(X, xout.p, 8 * (size_t)(n * k), cudaMemcpyDeviceToHost, s));
+    LAP_CUDA(cudaEventRecord(e1, s));
+    LAP_CUDA(cudaStreamSynchronize(s));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    h->stats.solve_ms = ms;
+    h->stats.kernel_launches = h->cur.launches;
+    h->stats.spmv_edges = h->cur.edges;
+    h->stats.spmv_bytes = h->cur.bytes;
     return conv ? LAP_OK : LAP_ENOCONV;
     LAP_API_END
 }

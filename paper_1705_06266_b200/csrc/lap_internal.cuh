@@ -202,7 +202,8 @@ struct lap_hierarchy {
     cudaGraphExec_t pcg_start = nullptr, pcg_resume = nullptr;
     void *pcg_counts = nullptr;
     int dtail_level = -1;          // level whose V-cycle is the dense operator lev[].dense (tail.cu)
-    void *ktail = nullptr;         // K-cycle below a small level as one single-CTA program (ktail.cu)
+    void *ktail = nullptr;         // K-cycle below a small level as one cluster program (ktail.cu)
+    std::vector<void *> blk;       // block (many right-hand sides) workspaces per width (block.cu)
     // multi-GPU shards (dist.cu), NULL for a single-GPU hierarchy
     void *dist = nullptr;
     void *dist_owned = nullptr;
@@ -248,6 +249,9 @@ void kcycle_level(lap_hierarchy *h, int l, bool with_fcg, cudaStream_t s);  // N
 void build_ktail(lap_hierarchy *h, cudaStream_t s);                          // N2 (ktail.cu)
 void free_ktail(lap_hierarchy *h, cudaStream_t s);
 bool ktail_launch(lap_hierarchy *h, int l, bool pre0_done, cudaStream_t s);
+void solve_block(lap_hierarchy *h, int k, const double *B, double *X, double tol, int32_t *iters, double *relres,
+                 int *conv, cudaStream_t s);                                   // N4 (block.cu)
+void free_block(lap_hierarchy *h);
 // multi-GPU (dist.cu)
 void build_dist(lap_hierarchy *h, lap_comm *c, cudaStream_t s);
 void free_dist(lap_hierarchy *h);

@@ -51,7 +51,7 @@ class lap_stats(ctypes.Structure):
 EXPORTS = [
     "lap_params_default", "lap_last_error", "lap_version", "lap_setup", "lap_solve", "lap_free",
     "lap_num_levels", "lap_level_info", "lap_level_export", "lap_level_strength", "lap_coarse_pinv",
-    "lap_perm", "lap_spmv", "lap_vcycle", "lap_kcycle", "lap_get_stats", "lap_bench_op",
+    "lap_perm", "lap_spmv", "lap_vcycle", "lap_kcycle", "lap_solve_block", "lap_get_stats", "lap_bench_op",
     "lap_nccl_unique_id", "lap_comm_create", "lap_comm_create_virtual", "lap_comm_info", "lap_comm_free",
     "lap_setup_dist", "lap_dist_index",
 ]
@@ -80,6 +80,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "lap_spmv": (ctypes.c_int, [P, i32, P, P, P]),
         "lap_vcycle": (ctypes.c_int, [P, P, P, P]),
         "lap_kcycle": (ctypes.c_int, [P, i32, i32, P, P, P]),
+        "lap_solve_block": (ctypes.c_int, [P, i32, P, P, ctypes.c_double, P, P, P]),
         "lap_get_stats": (ctypes.c_int, [P, ctypes.POINTER(lap_stats)]),
         "lap_bench_op": (ctypes.c_int, [P, i32, i32, i32, P, P, pdbl, pi64]),
         "lap_nccl_unique_id": (ctypes.c_int, [P]),
@@ -225,6 +226,21 @@ class Hierarchy:
         rc = _check(lib().lap_solve(self._h, _ptr(b), _ptr(x), tol, ctypes.byref(it), ctypes.byref(rr),
                                     _stream(stream)), allow=(LAP_ENOCONV,))
         return x, int(it.value), float(rr.value), rc
+
+    def solve_block(self, B, X=None, tol: float = 0.0, stream=None):
+        """k right-hand sides at once (N4): B is (k, n) -- row j = right-hand
+        side j, i.e. n x k column-major -- numpy or a torch CUDA tensor.
+        Returns X (k, n), iters[k], rel_residual[k], status."""
+        if not hasattr(B, "data_ptr"):
+            B = np.ascontiguousarray(B, np.float64)
+        k = B.shape[0]
+        if X is None:
+            X = np.zeros((k, self.n)) if not hasattr(B, "data_ptr") else B.new_zeros((k, self.n))
+        it = np.zeros(k, np.int32)
+        rr = np.zeros(k, np.float64)
+        rc = _check(lib().lap_solve_block(self._h, k, _ptr(B), _ptr(X), tol, _ptr(it), _ptr(rr), _stream(stream)),
+                    allow=(LAP_ENOCONV,))
+        return X, it, rr, rc
 
     # ---- introspection
     @property
