@@ -69,15 +69,24 @@ struct BArgs {
     double *partials;  // BE_DOT: [K][grid]
 };
 
-// y = epilogue(L X) for a block of K columns.  Short rows (SELL-32 slices,
-// coalesced index/weight loads, a thread per row); rows longer than
-// SHORT_MAX a warp per row over the CSR (lane-strided, shuffle tree).
+struct BChunks {  // the level's LCHUNK chunks of its long rows (storage.cu), K partials per chunk
+    int64_t nchunks;
+    const int32_t *crow, *cidx, *cslot;
+    int32_t *ccnt;
+    double *cpart;  // [nchunks][K]
+};
+
+// y = epilogue(L X) for a block of K columns, ONE launch: SELL-32 slices of
+// the short rows (coalesced index/weight loads, a thread per row), then the
+// LCHUNK-entry warp chunks of the long rows (lane-strided, shuffle tree, K
+// chunk partials, the last-arriving chunk of a row sums them in chunk order
+// -- the single-vector kernel's scheme, solve.cu chunk_reduce).
 template <int EPI, int K>
 __global__ void __launch_bounds__(256) k_blk_spmv(int64_t nslices, int64_t nshort, int64_t n,
                                                   const int64_t *__restrict__ sp, const int32_t *__restrict__ ec,
                                                   const double *__restrict__ ew, const int64_t *__restrict__ rp,
                                                   const int32_t *__restrict__ col, const double *__restrict__ w,
-                                                  const double *__restrict__ d, BArgs a) {
+                                                  const double *__restrict__ d, BChunks R, BArgs a) {
     pdl_begin();
     __shared__ double sh[8];
     const int lane = threadIdx.x & 31;
@@ -108,28 +117,44 @@ __global__ void __launch_bounds__(256) k_blk_spmv(int64_t nslices, int64_t nshor
             }
         }
     };
-    const int64_t nlong = n - nshort;
-    for (int64_t t = warp; t < nslices + nlong; t += nwarps) {
+    for (int64_t t = warp; t < nslices + R.nchunks; t += nwarps) {
         if (t < nslices) {
             const int64_t i = t * 32 + lane, beg = sp[t], end = sp[t + 1];
             const int width = (int)((end - beg) >> 5);
             double ax[K];
 #pragma unroll
             for (int c = 0; c < K; c++) ax[c] = 0.0;
-            for (int q = 0; q < width; q++) {
-                const int32_t j = __ldg(&ec[beg + (int64_t)q * 32 + lane]);
-                const double wv = __ldg(&ew[beg + (int64_t)q * 32 + lane]);
-                const Vk<K> xj = ldk<K>(a.x + (int64_t)j * K);
+            constexpr int NB = K <= 4 ? 4 : 2;  // padded columns per batch: indices first, then the gathers
+            for (int q = 0; q < width; q += NB) {
+                int32_t j[NB];
+                double wv[NB];
 #pragma unroll
-                for (int c = 0; c < K; c++) ax[c] += wv * xj.v[c];
+                for (int u = 0; u < NB; u++) {
+                    j[u] = 0;
+                    wv[u] = 0.0;
+                    if (q + u < width) {
+                        j[u] = __ldg(&ec[beg + (int64_t)(q + u) * 32 + lane]);
+                        wv[u] = __ldg(&ew[beg + (int64_t)(q + u) * 32 + lane]);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < NB; u++) {
+                    if (q + u < width) {
+                        const Vk<K> xj = ldk<K>(a.x + (int64_t)j[u] * K);
+#pragma unroll
+                        for (int c = 0; c < K; c++) ax[c] += wv[u] * xj.v[c];
+                    }
+                }
             }
             if (i < nshort) epi(i, ax);
         } else {
-            const int64_t i = nshort + (t - nslices);
+            const int64_t ch = t - nslices;
+            const int64_t i = R.crow[ch], j = R.cidx[ch];
+            const int64_t rb = rp[i], re = rp[i + 1], b0 = rb + j * LCHUNK, e0 = min(re, b0 + LCHUNK);
             double ax[K];
 #pragma unroll
             for (int c = 0; c < K; c++) ax[c] = 0.0;
-            for (int64_t q = rp[i] + lane; q < rp[i + 1]; q += 32) {
+            for (int64_t q = b0 + lane; q < e0; q += 32) {
                 const double wv = __ldg(&w[q]);
                 const Vk<K> xj = ldk<K>(a.x + (int64_t)__ldg(&col[q]) * K);
 #pragma unroll
@@ -138,7 +163,33 @@ __global__ void __launch_bounds__(256) k_blk_spmv(int64_t nslices, int64_t nshor
 #pragma unroll
             for (int c = 0; c < K; c++)
                 for (int o = 16; o > 0; o >>= 1) ax[c] += __shfl_xor_sync(0xffffffffu, ax[c], o);
-            if (lane == 0) epi(i, ax);
+            const int slot = R.cslot[ch];
+            if (slot < 0) {  // the whole row in one chunk
+                if (lane == 0) epi(i, ax);
+                continue;
+            }
+            const int nch = (int)((re - rb + LCHUNK - 1) / LCHUNK);
+            int last = 0;
+            if (lane == 0) {
+#pragma unroll
+                for (int c = 0; c < K; c++) R.cpart[ch * K + c] = ax[c];
+                __threadfence();
+                last = atomicAdd(&R.ccnt[slot], 1) == nch - 1;
+            }
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (!last) continue;
+            __threadfence();
+            if (lane == 0) {  // chunk order, per column
+                const int64_t c0 = ch - j;
+                double s2[K];
+#pragma unroll
+                for (int c = 0; c < K; c++) s2[c] = 0.0;
+                for (int q = 0; q < nch; q++)
+#pragma unroll
+                    for (int c = 0; c < K; c++) s2[c] += __ldcg(&R.cpart[(c0 + q) * K + c]);
+                R.ccnt[slot] = 0;
+                epi(i, s2);
+            }
         }
     }
     if (EPI == BE_DOT) {
@@ -373,6 +424,7 @@ __global__ void k_blk_sub_mean(int64_t n, double *__restrict__ v, const double *
 struct BlockWork {  // per (hierarchy, K)
     int K = 0;
     std::vector<double *> lb, lx, lx2, lt, lr, ldv;  // per level, n_l x K
+    std::vector<double *> lcpart;                     // per level, K partials per long-row chunk
     double *b = nullptr, *x = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr;
     double *sc = nullptr, *part = nullptr;
     double *hsc = nullptr;  // pinned host copy of the scalars
@@ -383,12 +435,13 @@ struct BlockWork {  // per (hierarchy, K)
 static inline unsigned beg(int64_t n) { return grid_for(n, 256, 148 * 8); }
 
 template <int K>
-static void blk_spmv(lap_hierarchy *h, const Level &L, int epi, const BArgs &a, cudaStream_t s, unsigned grid) {
-    const int64_t nlong = L.n - L.c_end[0];
+static void blk_spmv(lap_hierarchy *h, const Level &L, double *cpart, int epi, const BArgs &a, cudaStream_t s,
+                     unsigned grid) {
+    BChunks R{L.nchunks, L.chunk_row, L.chunk_idx, L.chunk_slot, L.chunk_cnt, cpart};
 #define BLK_LAUNCH(E)                                                                                             \
     launch_pdl(k_blk_spmv<E, K>, grid, 256, s, L.nslices, L.c_end[0], L.n, (const int64_t *)L.slice_ptr,         \
                (const int32_t *)L.ell_col, (const double *)L.ell_w, (const int64_t *)L.srp,                       \
-               (const int32_t *)L.scol, (const double *)L.sw, (const double *)L.sd, a)
+               (const int32_t *)L.scol, (const double *)L.sw, (const double *)L.sd, R, a)
     switch (epi) {
         case BE_DOT: BLK_LAUNCH(BE_DOT); break;
         case BE_RESID: BLK_LAUNCH(BE_RESID); break;
@@ -396,14 +449,13 @@ static void blk_spmv(lap_hierarchy *h, const Level &L, int epi, const BArgs &a, 
         default: BLK_LAUNCH(BE_CHEB0); break;
     }
 #undef BLK_LAUNCH
-    (void)nlong;
     h->cur.launches++;
     h->cur.edges += L.nnz * K;
     h->cur.bytes += 12 * L.nnz + (int64_t)(8 * K) * L.nnz + (int64_t)(40 * K) * L.n;
 }
 template <int K>
 static unsigned spmm_grid(const Level &L) {
-    return grid_for((L.nslices + (L.n - L.c_end[0])) * 32, 256, 148 * 8);
+    return grid_for((L.nslices + L.nchunks) * 32, 256, 148 * 8);
 }
 
 // V-cycle on K columns (solve.cu cycle_rec, V mode, per-level kernels)
@@ -444,13 +496,13 @@ static void blk_vcycle(lap_hierarchy *h, BlockWork &W, int l, const double *b, d
         a.c2 = 2.0 * rho / delta;
         a.x = cur;
         a.y = alt;
-        blk_spmv<K>(h, L, BE_CHEB, a, s, g);
+        blk_spmv<K>(h, L, W.lcpart[l], BE_CHEB, a, s, g);
         std::swap(cur, alt);
         rho_old = rho;
     }
     a.x = cur;
     a.y = W.lr[l];
-    blk_spmv<K>(h, L, BE_RESID, a, s, g);
+    blk_spmv<K>(h, L, W.lcpart[l], BE_RESID, a, s, g);
     launch_pdl(k_blk_restrict<K>, beg(L.m * K), 256, s, L.m, (const int64_t *)L.mem_ptr, (const int32_t *)L.members,
                (const double *)W.lr[l], cb);
     blk_vcycle<K>(h, W, l + 1, cb, cx, s);
@@ -464,12 +516,12 @@ static void blk_vcycle(lap_hierarchy *h, BlockWork &W, int l, const double *b, d
         if (k == 0) {
             a.c1 = 0.0;
             a.c2 = 1.0 / theta;
-            blk_spmv<K>(h, L, BE_CHEB0, a, s, g);
+            blk_spmv<K>(h, L, W.lcpart[l], BE_CHEB0, a, s, g);
         } else {
             double rho = 1.0 / (2.0 * sigma - rho_old);
             a.c1 = rho * rho_old;
             a.c2 = 2.0 * rho / delta;
-            blk_spmv<K>(h, L, BE_CHEB, a, s, g);
+            blk_spmv<K>(h, L, W.lcpart[l], BE_CHEB, a, s, g);
             rho_old = rho;
         }
         if (k < Kd - 1) std::swap(cur, alt);
@@ -491,6 +543,7 @@ static BlockWork *block_work(lap_hierarchy *h, cudaStream_t s) {
         W->lt.push_back((double *)dalloc(bytes, s));
         W->lr.push_back((double *)dalloc(bytes, s));
         W->ldv.push_back((double *)dalloc(bytes, s));
+        W->lcpart.push_back((double *)dalloc(8 * (size_t)K * (size_t)(L.nchunks > 0 ? L.nchunks : 1), s));
     }
     const size_t b0 = 8 * (size_t)K * (size_t)h->lev[0].n;
     double **vs[] = {&W->b, &W->x, &W->r, &W->z, &W->p, &W->q};
@@ -523,7 +576,7 @@ void free_block(lap_hierarchy *h) {
     for (void *p : h->blk) {
         BlockWork *W = (BlockWork *)p;
         if (W->vgraph) cudaGraphExecDestroy(W->vgraph);
-        for (auto *v : {&W->lb, &W->lx, &W->lx2, &W->lt, &W->lr, &W->ldv})
+        for (auto *v : {&W->lb, &W->lx, &W->lx2, &W->lt, &W->lr, &W->ldv, &W->lcpart})
             for (double *q : *v) dfree(q, nullptr);
         for (double *q : {W->b, W->x, W->r, W->z, W->p, W->q, W->sc, W->part}) dfree(q, nullptr);
         if (W->hsc) cudaFreeHost(W->hsc);
@@ -573,7 +626,7 @@ static void blk_spmv_part(lap_hierarchy *h, BlockWork &W, cudaStream_t s) {
     a.x = W.p;
     a.y = W.q;
     a.partials = W.part;
-    blk_spmv<K>(h, L0, BE_DOT, a, s, g);
+    blk_spmv<K>(h, L0, W.lcpart[0], BE_DOT, a, s, g);
     launch_pdl(k_blk_reduce, 1, 256, s, (const double *)W.part, (int)g, K, 1, W.sc, (int)S_PQ, 0, 0);
     launch_pdl(k_blk_xr<K>, BLK_RED, 256, s, n, (const double *)W.p, (const double *)W.q, W.x, W.r,
                (const double *)W.sc, W.part);
@@ -635,7 +688,7 @@ static void solve_block_k(lap_hierarchy *h, int k, const double *B, double *X, d
                 t.x = W.x;
                 t.b = W.b;
                 t.y = W.z;
-                blk_spmv<K>(h, L0, BE_RESID, t, s, spmm_grid<K>(L0));
+                blk_spmv<K>(h, L0, W.lcpart[0], BE_RESID, t, s, spmm_grid<K>(L0));
                 blk_sums<K, 1>(h, W, W.z, W.z, S_TRUE, 0, 0, s);
                 pull();
                 bool any_bad = false;
@@ -671,7 +724,7 @@ static void solve_block_k(lap_hierarchy *h, int k, const double *B, double *X, d
     t.x = W.x;
     t.b = W.b;
     t.y = W.z;
-    blk_spmv<K>(h, L0, BE_RESID, t, s, spmm_grid<K>(L0));
+    blk_spmv<K>(h, L0, W.lcpart[0], BE_RESID, t, s, spmm_grid<K>(L0));
     blk_sums<K, 1>(h, W, W.z, W.z, S_TRUE, 0, 0, s);
     launch_pdl(k_blk_out<K>, beg(n * k), 256, s, n, k, (const int64_t *)h->cmap, (const double *)W.x,
                (const double *)W.sc, X);
