@@ -43,9 +43,15 @@ struct Vk {
     double v[K];
 };
 template <int K>
-__device__ __forceinline__ Vk<K> ldk(const double *p) {  // K contiguous doubles (16-byte aligned rows)
+__device__ __forceinline__ Vk<K> ldk(const double *p) {  // K contiguous doubles (8K-byte aligned rows)
     Vk<K> r;
-    if (K % 2 == 0) {
+    if (K % 4 == 0) {  // 256-bit loads (LDG.E.ENL2.256 on sm_100): one request per 32 bytes
+#pragma unroll
+        for (int c = 0; c < K; c += 4)
+            asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                : "=d"(r.v[c]), "=d"(r.v[c + 1]), "=d"(r.v[c + 2]), "=d"(r.v[c + 3])
+                : "l"(p + c));
+    } else if (K % 2 == 0) {
 #pragma unroll
         for (int c = 0; c < K; c += 2) {
             double2 t = __ldg((const double2 *)(p + c));
@@ -57,6 +63,17 @@ __device__ __forceinline__ Vk<K> ldk(const double *p) {  // K contiguous doubles
         for (int c = 0; c < K; c++) r.v[c] = __ldg(p + c);
     }
     return r;
+}
+
+template <int K>
+__device__ __forceinline__ void stk(double *p, const Vk<K> &v) {
+    if (K % 2 == 0) {
+#pragma unroll
+        for (int c = 0; c < K; c += 2) *(double2 *)(p + c) = make_double2(v.v[c], v.v[c + 1]);
+    } else {
+#pragma unroll
+        for (int c = 0; c < K; c++) p[c] = v.v[c];
+    }
 }
 
 enum { BE_DOT = 0, BE_RESID = 1, BE_CHEB = 2, BE_CHEB0 = 3 };
@@ -95,27 +112,31 @@ __global__ void __launch_bounds__(256) k_blk_spmv(int64_t nslices, int64_t nshor
     double dacc[K];
 #pragma unroll
     for (int c = 0; c < K; c++) dacc[c] = 0.0;
+    // row epilogue: the K values of a row are contiguous -> 16-byte vector loads / stores
     auto epi = [&](int64_t i, const double *ax) {
         const double di = d[i];
         const Vk<K> xi = ldk<K>(a.x + i * K);
+        Vk<K> bi, dvi, yo, dvo;
+        if (EPI != BE_DOT) bi = ldk<K>(a.b + i * K);
+        if (EPI == BE_CHEB) dvi = ldk<K>(a.dv + i * K);
 #pragma unroll
         for (int c = 0; c < K; c++) {
             const double lx = di * xi.v[c] - ax[c];
             if (EPI == BE_DOT) {
-                a.y[i * K + c] = lx;
+                yo.v[c] = lx;
                 dacc[c] += xi.v[c] * lx;
             } else if (EPI == BE_RESID) {
-                a.y[i * K + c] = a.b[i * K + c] - lx;
+                yo.v[c] = bi.v[c] - lx;
             } else if (EPI == BE_CHEB) {
-                double v = a.c1 * a.dv[i * K + c] + a.c2 * ((a.b[i * K + c] - lx) / di);
-                a.dv[i * K + c] = v;
-                a.y[i * K + c] = xi.v[c] + v;
+                dvo.v[c] = a.c1 * dvi.v[c] + a.c2 * ((bi.v[c] - lx) / di);
+                yo.v[c] = xi.v[c] + dvo.v[c];
             } else {  // BE_CHEB0
-                double v = a.c2 * ((a.b[i * K + c] - lx) / di);
-                a.dv[i * K + c] = v;
-                a.y[i * K + c] = xi.v[c] + v;
+                dvo.v[c] = a.c2 * ((bi.v[c] - lx) / di);
+                yo.v[c] = xi.v[c] + dvo.v[c];
             }
         }
+        stk<K>(a.y + i * K, yo);
+        if (EPI == BE_CHEB || EPI == BE_CHEB0) stk<K>(a.dv + i * K, dvo);
     };
     for (int64_t t = warp; t < nslices + R.nchunks; t += nwarps) {
         if (t < nslices) {
@@ -124,7 +145,7 @@ __global__ void __launch_bounds__(256) k_blk_spmv(int64_t nslices, int64_t nshor
             double ax[K];
 #pragma unroll
             for (int c = 0; c < K; c++) ax[c] = 0.0;
-            constexpr int NB = K <= 4 ? 4 : 2;  // padded columns per batch: indices first, then the gathers
+            constexpr int NB = 4;  // padded columns per batch: indices first, then the gathers
             for (int q = 0; q < width; q += NB) {
                 int32_t j[NB];
                 double wv[NB];
