@@ -147,6 +147,7 @@ void finalize_solve_structures(lap_hierarchy *h, cudaStream_t s) {
     LAP_CUDA(cudaMemsetAsync(h->scal, 0, 8 * 16, s));
     int64_t np = std::max<int64_t>(1024, spmv_partial_slots(h->lev[0]));
     for (auto &L : h->lev) np = std::max<int64_t>(np, 2 * spmv_partial_slots(L));  // E_FCG: two dots
+    np = std::max<int64_t>(np, 3 * spmv_partial_slots(h->lev[0]));                  // E_CHEBZ: three sums
     if (np > h->npartials) {
         dfree(h->partials, s);
         h->partials = (double *)dalloc(8 * np, s);

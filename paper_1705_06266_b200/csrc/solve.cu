@@ -28,9 +28,10 @@ struct Csr {
 // ------------------------------------------------------------------ epilogues
 // Ax = sum_j w_ij x_j ; (L x)_i = d_i x_i - Ax  (L = D - A)
 enum { E_SPMV = EPI_SPMV, E_DOT = EPI_SPMV_DOT, E_RESID = EPI_RESID, E_CHEB = EPI_CHEB, E_LZ = EPI_LANCZOS, E_CHEB0 = 5,
-       E_FCG = 6 };  // E_FCG: y = L x with x.y and x.b (K-cycle inner FCG: p.q and p.r in one pass)
-struct Dacc {  // per-thread dot accumulators of the E_DOT / E_LZ / E_FCG epilogues
-    double a = 0.0, b = 0.0;
+       E_FCG = 6,     // y = L x with x.y and x.b (K-cycle inner FCG: p.q and p.r in one pass)
+       E_CHEBZ = 7 }; // E_CHEB whose output is the PCG's z = V(r) (b = r): also sum z, r.z, sum r (O-S8)
+struct Dacc {  // per-thread dot accumulators of the E_DOT / E_LZ / E_FCG / E_CHEBZ epilogues
+    double a = 0.0, b = 0.0, c = 0.0;
 };
 
 template <int EPI>
@@ -48,11 +49,18 @@ __device__ __forceinline__ void apply_epi(int64_t i, double ax, const Csr &A, co
         dacc.b += xi * a.b[i];
     } else if (EPI == E_RESID) {
         a.y[i] = a.b[i] - lx;
-    } else if (EPI == E_CHEB) {  // dv = c1 dv + c2 D^-1 (b - L x); x_out = x + dv   (O-S6)
-        double r = a.b[i] - lx;
+    } else if (EPI == E_CHEB || EPI == E_CHEBZ) {  // dv = c1 dv + c2 D^-1 (b - L x); x_out = x + dv   (O-S6)
+        const double bi = a.b[i];
+        double r = bi - lx;
         double dv = a.c1 * a.dv[i] + a.c2 * (r / A.d[i]);
         a.dv[i] = dv;
-        a.y[i] = xi + dv;
+        const double y = xi + dv;
+        a.y[i] = y;
+        if (EPI == E_CHEBZ) {
+            dacc.a += y;
+            dacc.b += bi * y;
+            dacc.c += bi;
+        }
     } else if (EPI == E_CHEB0) {  // first step from a nonzero x: dv = D^-1 r / theta
         double r = a.b[i] - lx;
         double dv = a.c2 * (r / A.d[i]);
@@ -112,8 +120,8 @@ __device__ __forceinline__ void sell_slice(int64_t sl, int lane, int64_t nrows, 
     if (live) {
         xi = a.x[i];
         di = A.d[i];
-        if (EPI == E_RESID || EPI == E_CHEB || EPI == E_CHEB0 || EPI == E_FCG) bi = a.b[i];
-        if (EPI == E_CHEB) dvi = a.dv[i];
+        if (EPI == E_RESID || EPI == E_CHEB || EPI == E_CHEB0 || EPI == E_FCG || EPI == E_CHEBZ) bi = a.b[i];
+        if (EPI == E_CHEB || EPI == E_CHEBZ) dvi = a.dv[i];
     }
     // batches of 8 padded columns: all 16 index/weight loads of a batch are
     // issued before the 8 dependent x gathers (memory-level parallelism for
@@ -151,10 +159,16 @@ __device__ __forceinline__ void sell_slice(int64_t sl, int lane, int64_t nrows, 
             dacc.b += xi * bi;
         } else if (EPI == E_RESID) {
             a.y[i] = bi - lx;
-        } else if (EPI == E_CHEB) {
+        } else if (EPI == E_CHEB || EPI == E_CHEBZ) {
             double dv = a.c1 * dvi + a.c2 * ((bi - lx) / di);
             a.dv[i] = dv;
-            a.y[i] = xi + dv;
+            const double y = xi + dv;
+            a.y[i] = y;
+            if (EPI == E_CHEBZ) {
+                dacc.a += y;
+                dacc.b += bi * y;
+                dacc.c += bi;
+            }
         } else if (EPI == E_CHEB0) {
             double dv = a.c2 * ((bi - lx) / di);
             a.dv[i] = dv;
@@ -261,9 +275,16 @@ __global__ void __launch_bounds__(256, NB == 8 ? 4 : 5) k_spmv(int64_t nslices, 
         double r = block_sum(dacc.a, sh);
         if (threadIdx.x == 0) partials[blockIdx.x] = r;
     }
-    if (EPI == E_FCG) {  // second dot in partials[gridDim.x + block]
-        double r = block_sum(dacc.b, sh);
-        if (threadIdx.x == 0) partials[gridDim.x + blockIdx.x] = r;
+    if (EPI == E_FCG || EPI == E_CHEBZ) {  // second dot in partials[gridDim.x + block]
+        double r = block_sum(EPI == E_CHEBZ ? dacc.a : dacc.b, sh);
+        if (threadIdx.x == 0) partials[(EPI == E_CHEBZ ? 0 : 1) * gridDim.x + blockIdx.x] = r;
+    }
+    if (EPI == E_CHEBZ) {  // (sum z, r.z, sum r) in the k_pcg_zsums layout
+        double r1 = block_sum(dacc.b, sh), r2 = block_sum(dacc.c, sh);
+        if (threadIdx.x == 0) {
+            partials[gridDim.x + blockIdx.x] = r1;
+            partials[2 * gridDim.x + blockIdx.x] = r2;
+        }
     }
 }
 
@@ -297,9 +318,16 @@ __global__ void __launch_bounds__(1024, 1) k_spmv_smem(int64_t n, int64_t nslice
         double r = block_sum(dacc.a, sh);
         if (threadIdx.x == 0) partials[blockIdx.x] = r;
     }
-    if (EPI == E_FCG) {  // second dot in partials[gridDim.x + block]
-        double r = block_sum(dacc.b, sh);
-        if (threadIdx.x == 0) partials[gridDim.x + blockIdx.x] = r;
+    if (EPI == E_FCG || EPI == E_CHEBZ) {  // second dot in partials[gridDim.x + block]
+        double r = block_sum(EPI == E_CHEBZ ? dacc.a : dacc.b, sh);
+        if (threadIdx.x == 0) partials[(EPI == E_CHEBZ ? 0 : 1) * gridDim.x + blockIdx.x] = r;
+    }
+    if (EPI == E_CHEBZ) {  // (sum z, r.z, sum r) in the k_pcg_zsums layout
+        double r1 = block_sum(dacc.b, sh), r2 = block_sum(dacc.c, sh);
+        if (threadIdx.x == 0) {
+            partials[gridDim.x + blockIdx.x] = r1;
+            partials[2 * gridDim.x + blockIdx.x] = r2;
+        }
     }
 }
 
@@ -359,10 +387,11 @@ void spmv_level(lap_hierarchy *h, const Level &L, EpiKind kind, const EpiArgs &a
         case E_CHEB: spmv_dispatch<E_CHEB>(h, L, a, s); break;
         case E_CHEB0: spmv_dispatch<E_CHEB0>(h, L, a, s); break;
         case E_FCG: spmv_dispatch<E_FCG>(h, L, a, s); break;
+        case E_CHEBZ: spmv_dispatch<E_CHEBZ>(h, L, a, s); break;
         default: throw Error{LAP_EINVAL, "bad epilogue"};
     }
-    int64_t extra = (kind == EPI_RESID) ? 8 : (kind == EPI_CHEB) ? 24 : (kind == (EpiKind)E_CHEB0) ? 16
-                    : (kind == (EpiKind)E_FCG) ? 8 : 0;
+    int64_t extra = (kind == EPI_RESID) ? 8 : (kind == EPI_CHEB || kind == (EpiKind)E_CHEBZ) ? 24
+                    : (kind == (EpiKind)E_CHEB0) ? 16 : (kind == (EpiKind)E_FCG) ? 8 : 0;
     h->cur.edges += L.nnz;
     h->cur.bytes += 12 * L.nnz + (32 + extra) * L.n;
 }
@@ -535,10 +564,22 @@ static void kcoarse(lap_hierarchy *h, int l, cudaStream_t s, bool pre0_done);
 
 // One cycle at level l: x = V(l, b) (kc = false, O-S7) or x = K(l, b)
 // (kc = true, N2: the coarse problem below each level goes to kcoarse).
+static bool zsums_enabled() {  // LAP_FUSE_ZSUMS=0: separate k_pcg_zsums pass
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("LAP_FUSE_ZSUMS");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 // pre0_done: the caller's restriction already formed this (aggregation)
 // level's pre-smoothing step 0
-static void cycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, cudaStream_t s, bool kc,
-                      bool pre0_done = false) {
+// zsums: the caller is the PCG (b = r, xout = z): the last post-smoothing
+// step also emits the (sum z, r.z, sum r) partials of k_pcg_zsums into
+// h->partials (E_CHEBZ); returns whether it did.
+static bool cycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, cudaStream_t s, bool kc,
+                      bool pre0_done = false, bool zsums = false) {
     Level &L = h->lev[l];
     int64_t n = L.n;
     if (!kc && l == h->dtail_level && L.dense && b == L.b && xout == L.x) {  // (the K-cycle is not linear)  // V(l, b) = M_l b (tail.cu)
@@ -546,13 +587,13 @@ static void cycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, cu
         h->cur.launches++;
         h->cur.bytes += 8 * n * n + 16 * n;
         LAP_CHECK_LAUNCH();
-        return;
+        return false;
     }
     if (L.kind == KIND_COARSEST) {
         launch_pdl(k_coarse_gemv, grid_for(n * 32, 256, 148), 256, s, n, L.pinv_s, b, xout);
         h->cur.launches++;
         LAP_CHECK_LAUNCH();
-        return;
+        return false;
     }
     Level &C = h->lev[l + 1];
     if (L.kind == KIND_ELIM) {
@@ -577,7 +618,7 @@ static void cycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, cu
         h->cur.launches++;
         h->cur.bytes += 16 * n + 24 * (n - nc) * 4;
         LAP_CHECK_LAUNCH();
-        return;
+        return false;
     }
     // aggregation level: degree-K Chebyshev in D^-1 L on [lo, hi] * lambda (O-S6)
     const int K = h->p.cheby_degree;
@@ -638,11 +679,14 @@ static void cycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, cu
             double rho = 1.0 / (2.0 * sigma - rho_old);
             a.c1 = rho * rho_old;
             a.c2 = 2.0 * rho / delta;
-            spmv_level(h, L, EPI_CHEB, a, s);
+            const bool z = zsums && k == K - 1;
+            a.partials = z ? h->partials : nullptr;
+            spmv_level(h, L, z ? (EpiKind)E_CHEBZ : EPI_CHEB, a, s);
             rho_old = rho;
         }
         if (k < K - 1) std::swap(cur, alt);
     }
+    return zsums && K >= 2;
 }
 
 void vcycle(lap_hierarchy *h, int l, cudaStream_t s) {
@@ -923,14 +967,23 @@ static void pcg_precond_part(lap_hierarchy *h, bool first, bool inline_vcycle, c
         reduce_partials(h, h->partials, RED_BLOCKS, sc + 0, s);
         return;
     }
-    if (inline_vcycle) vcycle_apply(h, h->pr, h->pz, s);
+    // inline (captured) V-cycle: its last level-0 Chebyshev step also emits the
+    // z-sums (E_CHEBZ), saving the k_pcg_zsums pass over z and r
+    bool zdone = false;
+    if (inline_vcycle) zdone = cycle_rec(h, 0, h->pr, h->pz, s, false, false, zsums_enabled());
     else launch_vcycle(h, s);
-    launch_pdl(k_pcg_zsums, RED_BLOCKS, 256, s, n, (const double *)h->pz, (const double *)h->pr, h->partials);
-    launch_pdl(k_pcg_zfinish, 1, 256, s, n, (const double *)h->partials, (int)RED_BLOCKS, sc, first ? 1 : 0);
+    if (!zdone) {
+        launch_pdl(k_pcg_zsums, RED_BLOCKS, 256, s, n, (const double *)h->pz, (const double *)h->pr, h->partials);
+        h->cur.launches++;
+    }
+    const int np = zdone ? (int)spmv_partial_slots(L0) : (int)RED_BLOCKS;
+    launch_pdl(k_pcg_zfinish, 1, 256, s, n, (const double *)h->partials, np, sc, first ? 1 : 0);
     launch_pdl(k_pcg_p2, eg(n), 256, s, n, (const double *)h->pz, h->pp, (const double *)sc, first ? 1 : 0);
-    h->cur.launches += 3;
+    h->cur.launches += 2;
 }
 // q = L p ; pq = p.q ; x += alpha p ; r -= alpha q ; rr = r.r   (H1 fused with H7)
+// (Forming the next V-cycle's level-0 step 0 inside k_pcg_xr as r is produced
+// measured 0.7 ms slower per cfg 2 solve: DESIGN.md §7.)
 static void pcg_spmv_part(lap_hierarchy *h, cudaStream_t s) {
     Level &L0 = h->lev[0];
     int64_t n = L0.n;
