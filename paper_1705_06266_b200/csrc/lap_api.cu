@@ -145,7 +145,7 @@ void finalize_solve_structures(lap_hierarchy *h, cudaStream_t s) {
     for (double **v : vecs) *v = (double *)dalloc(8 * (n0 > 0 ? n0 : 1), s);
     h->scal = (double *)dalloc(8 * 16, s);
     LAP_CUDA(cudaMemsetAsync(h->scal, 0, 8 * 16, s));
-    int64_t np = std::max<int64_t>(1024, spmv_partial_slots(h->lev[0]));
+    int64_t np = std::max<int64_t>(148 * 8, spmv_partial_slots(h->lev[0]));  // >= XR_BLOCKS (solve.cu)
     for (auto &L : h->lev) np = std::max<int64_t>(np, 2 * spmv_partial_slots(L));  // E_FCG: two dots
     np = std::max<int64_t>(np, 3 * spmv_partial_slots(h->lev[0]));                  // E_CHEBZ: three sums
     if (np > h->npartials) {
@@ -165,7 +165,8 @@ static void free_level(Level &L, cudaStream_t s) {
                   L.chunk_part, L.ell_col16, L.scol16,
                   L.agg_s, L.mem_ptr, L.members, L.cid_s, L.flist, L.ct_ptr_s, L.ct_f_s, L.ct_coef_s, L.fmap_s,
                   L.ct_crow, L.ct_cidx, L.ct_cslot, L.ct_ccnt, L.ct_cpart,
-                  L.pinv_s, L.dense, L.b, L.x, L.x2, L.t, L.r, L.dv, L.kp, L.kq, L.kz, L.kr, L.ksc};
+                  L.pinv_s, L.dense, L.dense_part, L.dense_cnt, L.b, L.x, L.x2, L.t, L.r, L.dv, L.kp, L.kq, L.kz,
+                  L.kr, L.ksc};
     for (void *p : ps) dfree(p, s);
 }
 

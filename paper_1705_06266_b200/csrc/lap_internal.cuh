@@ -163,6 +163,8 @@ struct Level {
     int32_t *fmap_s = nullptr;      // elim: coarse storage index of a C storage row, -1 for F
     double *pinv_s = nullptr;       // coarsest: L^+ in storage order
     double *dense = nullptr;        // dense-tail level: M = [V(l, e_j)] (n x n, column-major; tail.cu)
+    double *dense_part = nullptr;   // dense-tail GEMV: split partials, per-tile arrival counters
+    int *dense_cnt = nullptr;
     // Chebyshev constants (O-S6), host
     double cheb_theta = 0, cheb_delta = 0, cheb_sigma = 0;
     // solve work vectors (storage order, length n >= 1)

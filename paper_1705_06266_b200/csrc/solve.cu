@@ -398,6 +398,7 @@ void spmv_level(lap_hierarchy *h, const Level &L, EpiKind kind, const EpiArgs &a
 
 // ------------------------------------------------------------------ reductions
 constexpr int RED_BLOCKS = 296;  // fixed: deterministic two-pass reductions
+constexpr int XR_BLOCKS = 148 * 8;  // k_pcg_xr: 48 B/row streamed -- 296 blocks reached ~2.8 TB/s only
 
 __global__ void __launch_bounds__(256) k_dot_partial(int64_t n, const double *__restrict__ a,
                                                      const double *__restrict__ b, double *__restrict__ part) {
@@ -461,19 +462,22 @@ __device__ __forceinline__ void put_b(int64_t k, double s, double *__restrict__ 
     }
 }
 // r_c[a] = sum over members of a (ascending) of r_i; 8 lanes per aggregate
+// G lanes per aggregate (G = 1 for the ~3-4 member aggregates of grids -- 8
+// lanes left most idle --, up to 8 for large ones; restrict_group below)
+template <int G>
 __global__ void __launch_bounds__(256) k_restrict(int64_t m, const int64_t *__restrict__ mp,
                                                   const int32_t *__restrict__ mem, const double *__restrict__ r,
                                                   double *__restrict__ rc, Pre0 p0) {
     pdl_begin();
-    const int lane = threadIdx.x & 31, sub = lane & 7, grp = lane >> 3;
+    const int lane = threadIdx.x & 31, sub = lane & (G - 1), grp = lane / G;
     int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t base = warp * 4; base < m; base += nwarps * 4) {
+    for (int64_t base = warp * (32 / G); base < m; base += nwarps * (32 / G)) {
         int64_t a = base + grp;
         double acc = 0.0;
         if (a < m)
-            for (int64_t k = mp[a] + sub; k < mp[a + 1]; k += 8) acc += r[mem[k]];
-        for (int o = 4; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            for (int64_t k = mp[a] + sub; k < mp[a + 1]; k += G) acc += r[mem[k]];
+        for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         if (sub == 0 && a < m) put_b(a, acc, rc, p0);
     }
 }
@@ -656,7 +660,17 @@ static bool cycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, cu
         p0.x = C.x2;
         p0.dv = C.dv;
     }
-    launch_pdl(k_restrict, grid_for(L.m * 8, 256, 148 * 8), 256, s, L.m, L.mem_ptr, L.members, L.r, C.b, p0);
+    {  // lanes per aggregate from the mean aggregate size n/m; 8 where hub rows exist (aggregates
+       // of hubs have up to degree + 1 members: a few lanes would serialise them)
+        const int64_t avg = (n + L.m - 1) / std::max<int64_t>(1, L.m);
+        // (small levels are latency-bound: 8 lanes keep a member's loads in parallel)
+        const int G = (L.nchunks > 0 || L.m < 65536) ? 8 : avg <= 4 ? 1 : avg <= 8 ? 2 : avg <= 16 ? 4 : 8;
+        const unsigned rg = grid_for(L.m * G, 256, 148 * 8);
+        if (G == 1) launch_pdl(k_restrict<1>, rg, 256, s, L.m, L.mem_ptr, L.members, L.r, C.b, p0);
+        else if (G == 2) launch_pdl(k_restrict<2>, rg, 256, s, L.m, L.mem_ptr, L.members, L.r, C.b, p0);
+        else if (G == 4) launch_pdl(k_restrict<4>, rg, 256, s, L.m, L.mem_ptr, L.members, L.r, C.b, p0);
+        else launch_pdl(k_restrict<8>, rg, 256, s, L.m, L.mem_ptr, L.members, L.r, C.b, p0);
+    }
     h->cur.launches++;
     h->cur.bytes += 16 * n + 8 * L.m;
     if (kc) kcoarse(h, l + 1, s, fuse0);
@@ -994,10 +1008,11 @@ static void pcg_spmv_part(lap_hierarchy *h, cudaStream_t s) {
     a.partials = h->partials;
     spmv_level(h, L0, EPI_SPMV_DOT, a, s);
     reduce_partials(h, h->partials, spmv_partial_slots(L0), sc + 1, s);
-    launch_pdl(k_pcg_xr, RED_BLOCKS, 256, s, n, (const double *)h->pp, (const double *)h->pq, h->px, h->pr,
+    const unsigned xg = grid_for(n, 256, XR_BLOCKS);  // fixed per hierarchy: deterministic
+    launch_pdl(k_pcg_xr, xg, 256, s, n, (const double *)h->pp, (const double *)h->pq, h->px, h->pr,
                (const double *)sc, h->partials);
     h->cur.launches++;
-    reduce_partials(h, h->partials, RED_BLOCKS, sc + 2, s);
+    reduce_partials(h, h->partials, xg, sc + 2, s);
 }
 
 // ---- the PCG loop as one resident CUDA graph (WHILE conditional node)

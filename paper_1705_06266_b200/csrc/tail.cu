@@ -113,31 +113,73 @@ __global__ void k_b_coarse(int64_t n, int64_t k, const double *__restrict__ P, c
     }
 }
 
-// x = M b with M column-major n x n: a block owns 32 consecutive rows (lane =
-// row, coalesced 256-byte reads of each column), its 32 warps split the
-// columns, and the warp partials are summed in a fixed order in shared memory.
-__global__ void __launch_bounds__(1024) k_dense_gemv(int64_t n, const double *__restrict__ M,
-                                                     const double *__restrict__ b, double *__restrict__ x) {
+// x = M b with M column-major n x n (the 49 MB operator of cfg 2's tail is
+// streamed from HBM every V-cycle).  Grid = (row tiles of 32) x (DG_SPLIT
+// column ranges): a block's 8 warps stride over its column range (lane = row,
+// coalesced 256-byte reads, 4 columns in flight per warp), the warp partials
+// are summed in warp order in shared memory, the split partial goes to
+// part[split][row], and the LAST block of a row tile to arrive (per-tile
+// counter) sums the DG_SPLIT partials in split order: deterministic, and
+// ~600 blocks over all SMs instead of one 1024-thread block per 32 rows
+// (78 blocks on cfg 2: 1.9 TB/s).
+template <int NW>  // warps per block: 32 for unsplit small operators, 8 for the split ones
+__global__ void __launch_bounds__(NW * 32) k_dense_gemv(int64_t n, const double *__restrict__ M,
+                                                        const double *__restrict__ b, double *__restrict__ x,
+                                                        double *__restrict__ part, int *__restrict__ cnt) {
     pdl_begin();
-    __shared__ double part[32][33];
+    __shared__ double wp[NW][33];
+    __shared__ int last;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    constexpr int nw = NW;
     const int64_t i = (int64_t)blockIdx.x * 32 + lane;
+    const int nsplit = gridDim.y, sp = blockIdx.y;
+    const int64_t cb = n * sp / nsplit, ce = n * (sp + 1) / nsplit;
     double acc = 0.0;
     if (i < n) {
-        int64_t c = wid;
-        for (; c + 96 < n; c += 128) {
-            double m0 = M[c * n + i], m1 = M[(c + 32) * n + i], m2 = M[(c + 64) * n + i], m3 = M[(c + 96) * n + i];
-            acc += m0 * b[c] + m1 * b[c + 32] + m2 * b[c + 64] + m3 * b[c + 96];
+        int64_t c = cb + wid;
+        for (; c + 7 * nw < ce; c += 8 * nw) {  // 8 columns in flight per warp
+            double m[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) m[u] = __ldg(&M[(c + u * nw) * n + i]);
+#pragma unroll
+            for (int u = 0; u < 8; u++) acc += m[u] * b[c + u * nw];
         }
-        for (; c < n; c += 32) acc += M[c * n + i] * b[c];
+        for (; c < ce; c += nw) acc += __ldg(&M[c * n + i]) * b[c];
     }
-    part[wid][lane] = acc;
+    wp[wid][lane] = acc;
     __syncthreads();
+    if (nsplit == 1) {  // small operators: no split, no combine
+        if (wid == 0) {
+            double s = 0.0;
+            for (int q = 0; q < nw; q++) s += wp[q][lane];
+            if (i < n) x[i] = s;
+        }
+        return;
+    }
     if (wid == 0) {
         double s = 0.0;
-        for (int q = 0; q < 32; q++) s += part[q][lane];
-        if (i < n) x[i] = s;
+        for (int q = 0; q < nw; q++) s += wp[q][lane];
+        if (i < n) part[(int64_t)sp * n + i] = s;
+        __threadfence();
     }
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&cnt[blockIdx.x], 1) == nsplit - 1;
+    __syncthreads();
+    if (!last) return;
+    if (wid == 0) {
+        __threadfence();
+        double s = 0.0;
+        for (int q = 0; q < nsplit; q++) s += (i < n) ? __ldcg(&part[(int64_t)q * n + i]) : 0.0;
+        if (i < n) x[i] = s;
+        if (lane == 0) cnt[blockIdx.x] = 0;
+    }
+}
+
+static unsigned dense_splits(int64_t n) {  // ~4 blocks of 256 per SM in total, >= 256 columns per split
+    if (n < 1536) return 1;  // latency-bound: the split combine costs more than it saves
+    const int64_t tiles = (n + 31) / 32;
+    int64_t sp = (4 * 148 + tiles - 1) / tiles;
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(sp, n / 256));
 }
 
 static inline unsigned bg(int64_t total) { return grid_for(total, 256, 148 * 16); }
@@ -231,6 +273,9 @@ void build_dense_tail(lap_hierarchy *h, cudaStream_t s) {
     }
     Level &T = h->lev[t];
     T.dense = (double *)dalloc(sizeof(double) * (size_t)(k * k), s);
+    T.dense_part = (double *)dalloc(sizeof(double) * (size_t)k * dense_splits(k), s);
+    T.dense_cnt = (int *)dalloc(sizeof(int) * (size_t)((k + 31) / 32), s);
+    LAP_CUDA(cudaMemsetAsync(T.dense_cnt, 0, sizeof(int) * (size_t)((k + 31) / 32), s));
     try {
         k_b_identity<<<bg(k * k), 256, 0, s>>>(k, W[t].b);
         vcycle_batched(h, t, k, W, W[t].b, T.dense, s);
@@ -244,7 +289,23 @@ void build_dense_tail(lap_hierarchy *h, cudaStream_t s) {
 }
 
 void launch_dense_gemv(const Level &L, const double *b, double *x, cudaStream_t s) {
-    launch_pdl(k_dense_gemv, (unsigned)((L.n + 31) / 32), 1024, s, L.n, (const double *)L.dense, b, x);
+    const unsigned tiles = (unsigned)((L.n + 31) / 32);
+    cudaLaunchConfig_t cfg = {};
+    const unsigned sp = dense_splits(L.n);
+    cfg.gridDim = dim3(tiles, sp);
+    cfg.blockDim = dim3(sp == 1 ? 1024 : 256);  // unsplit small operators: 32 warps share a tile's columns
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    if (sp == 1)
+        LAP_CUDA(cudaLaunchKernelEx(&cfg, k_dense_gemv<32>, L.n, (const double *)L.dense, b, x, L.dense_part,
+                                    L.dense_cnt));
+    else
+        LAP_CUDA(cudaLaunchKernelEx(&cfg, k_dense_gemv<8>, L.n, (const double *)L.dense, b, x, L.dense_part,
+                                    L.dense_cnt));
 }
 
 }  // namespace lap
