@@ -59,7 +59,12 @@ def host_cores():
 
 # ---------------------------------------------------------------- clocks
 class Clocks:
-    """nvidia-smi sampler during the timed region (B200_PROFILING.md recipe)."""
+    """Clock / throttle-reason sampler during the timed region (B200_PROFILING.md
+    recipe).  In-process NVML (the library nvidia-smi reads; same clocks.sm,
+    clocks.max.sm and clocks_event_reasons fields) every 200 ms from a thread:
+    a polling `nvidia-smi -lms` child measurably slowed the timed steps (~4 ms
+    of 86 ms on cfg 2, driver calls contending with the CUDA stream).  Falls
+    back to `nvidia-smi -lms 200` when pynvml is missing."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -70,18 +75,49 @@ class Clocks:
         self.p = None
         self.enabled = enabled
 
+    def _nvml_loop(self, nv, hdl):
+        names = [("hw_slowdown", nv.nvmlClocksEventReasonHwSlowdown),
+                 ("hw_thermal_slowdown", nv.nvmlClocksEventReasonHwThermalSlowdown),
+                 ("sw_thermal_slowdown", nv.nvmlClocksEventReasonSwThermalSlowdown),
+                 ("sw_power_cap", nv.nvmlClocksEventReasonSwPowerCap)]
+        mx = nv.nvmlDeviceGetMaxClockInfo(hdl, nv.NVML_CLOCK_SM)
+        while not self._stop.wait(0.2 if self.lines else 0.02):
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(hdl, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(hdl)
+            except Exception:
+                break
+            act = ["Active" if r & bit else "Not Active" for _, bit in names]
+            self.lines.append(", ".join([str(self.idx), str(sm), str(mx), "0", hex(r)] + act))
+
     def __enter__(self):
+        self.lines = []
         if not self.enabled:
             return self
         try:
+            import threading
+            import pynvml as nv
+            nv.nvmlInit()
+            hdl = nv.nvmlDeviceGetHandleByIndex(self.idx)
+            self._stop = threading.Event()
+            self._t = threading.Thread(target=self._nvml_loop, args=(nv, hdl), daemon=True)
+            self._t.start()
+            return self
+        except Exception:
+            self._t = None
+        try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.p = None
         return self
 
     def __exit__(self, *a):
+        if getattr(self, "_t", None) is not None:
+            self._stop.set()
+            self._t.join(timeout=5)
+            return
         self.lines = []
         if self.p is not None:
             self.p.terminate()
@@ -108,7 +144,8 @@ class Clocks:
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "sampler": "nvml" if getattr(self, "_t", None) is not None else "nvidia-smi"}
 
 
 # ---------------------------------------------------------------- edge model
