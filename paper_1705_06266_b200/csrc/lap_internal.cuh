@@ -140,6 +140,7 @@ struct Level {
     bool sell_sorted = false;       // short rows degree-sorted
     bool smem_x = false;            // small dense-ish level: k_spmv_smem (x in shared memory, 16-bit columns)
     int spmv_nb = 8;                // SELL batch width of k_spmv (8, or 4 for mid-size levels)
+    int spmv_vec = 0;               // > 0: k_spmv_vec, G lanes per row over the CSR (solve.cu)
     uint16_t *ell_col16 = nullptr;  // smem_x: 16-bit copies of ell_col / scol
     uint16_t *scol16 = nullptr;
     int64_t nchunks = 0;            // LCHUNK chunks over the long rows [c_end[0], n)

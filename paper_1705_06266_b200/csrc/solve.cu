@@ -345,6 +345,7 @@ static int num_sms() {
 // fixed launch geometry per level (deterministic partial slots for E_DOT)
 static unsigned spmv_grid(const Level &L) {
     if (L.smem_x) return (unsigned)num_sms();
+    if (L.spmv_vec) return grid_for(L.n * L.spmv_vec, 256, (int64_t)num_sms() * 8);
     int64_t items = L.nslices + L.nchunks;
     // one resident wave: 4 CTAs of 256 per SM at 64 registers (NB 8), 5 at NB 4 (48 registers)
     return grid_for(items * 32, 256, (int64_t)num_sms() * (L.spmv_nb == 8 ? 4 : 5));
@@ -352,9 +353,56 @@ static unsigned spmv_grid(const Level &L) {
 
 int64_t spmv_partial_slots(const Level &L) { return spmv_grid(L); }
 
+// G lanes per row over the storage CSR (levels without long rows); the same
+// epilogues as k_spmv via apply_epi
+template <int EPI, int G>
+__global__ void __launch_bounds__(256) k_spmv_vec(int64_t n, Csr A, EpiArgs a, double *__restrict__ partials) {
+    pdl_begin();
+    __shared__ double sh[8];
+    const int lane = threadIdx.x & 31, sub = lane & (G - 1);
+    const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+    const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
+    Dacc dacc;
+    for (int64_t base = grp - (grp % (32 / G)); base < n; base += ngrp) {  // a warp's groups move together
+        const int64_t i = base + (grp % (32 / G));
+        double ax = 0.0;
+        if (i < n) {
+            const int64_t q1 = A.rp[i + 1];
+            for (int64_t q = A.rp[i] + sub; q < q1; q += G) ax += __ldg(&A.w[q]) * a.x[__ldg(&A.col[q])];
+        }
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) ax += __shfl_xor_sync(0xffffffffu, ax, o);
+        if (sub == 0 && i < n) apply_epi<EPI>(i, ax, A, a, dacc);
+    }
+    if (EPI == E_DOT || EPI == E_LZ || EPI == E_FCG) {
+        double r = block_sum(dacc.a, sh);
+        if (threadIdx.x == 0) partials[blockIdx.x] = r;
+    }
+    if (EPI == E_FCG || EPI == E_CHEBZ) {
+        double r = block_sum(EPI == E_CHEBZ ? dacc.a : dacc.b, sh);
+        if (threadIdx.x == 0) partials[(EPI == E_CHEBZ ? 0 : 1) * gridDim.x + blockIdx.x] = r;
+    }
+    if (EPI == E_CHEBZ) {
+        double r1 = block_sum(dacc.b, sh), r2 = block_sum(dacc.c, sh);
+        if (threadIdx.x == 0) {
+            partials[gridDim.x + blockIdx.x] = r1;
+            partials[2 * gridDim.x + blockIdx.x] = r2;
+        }
+    }
+}
+
 template <int EPI>
 static void spmv_dispatch(lap_hierarchy *h, const Level &L, const EpiArgs &a, cudaStream_t s) {
     Csr A{L.srp, L.scol, L.sw, L.sd};
+    if (L.spmv_vec) {
+        EpiArgs b2 = a;
+        if (L.spmv_vec == 4) launch_pdl(k_spmv_vec<EPI, 4>, spmv_grid(L), 256, s, L.n, A, b2, a.partials);
+        else if (L.spmv_vec == 8) launch_pdl(k_spmv_vec<EPI, 8>, spmv_grid(L), 256, s, L.n, A, b2, a.partials);
+        else launch_pdl(k_spmv_vec<EPI, 16>, spmv_grid(L), 256, s, L.n, A, b2, a.partials);
+        h->cur.launches++;
+        LAP_CHECK_LAUNCH();
+        return;
+    }
     LongRows R{L.nchunks, L.chunk_row, L.chunk_idx, L.chunk_slot, L.chunk_part, L.chunk_cnt};
     if (L.smem_x) {
         static bool attr_set = false;
