@@ -353,7 +353,8 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
         if (e) L.spmv_nb = L.nnz <= atoll(e) ? 4 : 8;
         else L.spmv_nb = (L.nnz >= NB4_MIN_NNZ && L.nnz <= 8 * n) ? 4 : 8;
     }
-    // small levels without long rows: 8 lanes per row over the CSR (k_spmv_vec) --
+    // small levels without long rows: 8 (n <= 64K) or 4 (n <= 128K) lanes per row over
+    // the CSR (k_spmv_vec) --
     // a row's ~15 gathers in one dependent round instead of two SELL batches, and
     // 8x the CTAs: cfg 2 level 6 (14.5K rows) 6.6 -> 3.8 us per SpMV, level 5
     // 7.2 -> 3.6 us; on large levels SELL stays faster (level 2: 26.6 vs 65 us per
@@ -361,7 +362,7 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
     // without long rows (experiments).
     {
         const char *e = getenv("LAP_SPMV_VEC");
-        const int G = e ? atoi(e) : (n <= 65536 ? 8 : 0);
+        const int G = e ? atoi(e) : (n <= 65536 ? 8 : n <= 131072 ? 4 : 0);
         L.spmv_vec = (G == 4 || G == 8 || G == 16) && l > 0 && n == L.c_end[0] && !L.smem_x ? G : 0;
     }
     // long rows: LCHUNK-entry warp work items (solve.cu k_spmv)
