@@ -224,9 +224,10 @@ def test_storage_layout_validated_in_debug_mode(P):
 
 
 @pytest.mark.parametrize("env", [{"LAP_DENSE_TAIL": "0"}, {"LAP_PDL": "0"}, {"LAP_FUSE_TRANSFERS": "0"},
-                                 {"LAP_FUSE_ZSUMS": "0"},
+                                 {"LAP_FUSE_ZSUMS": "0"}, {"LAP_SPMV_VEC": "0"}, {"LAP_SPMV_VEC": "16"},
                                  {"LAP_DENSE_TAIL": "0", "LAP_PDL": "0", "LAP_FUSE_TRANSFERS": "0", "LAP_FUSE_ZSUMS": "0"}],
-                         ids=["no-dense-tail", "no-pdl", "no-fused-transfers", "no-fused-zsums", "none"])
+                         ids=["no-dense-tail", "no-pdl", "no-fused-transfers", "no-fused-zsums", "sell-only",
+                              "vec16-everywhere", "none"])
 def test_solve_path_switches(P, env):
     """The alternative solve paths (per-level kernels instead of the dense
     tail operator, launches without programmatic dependent launch) give the
