@@ -229,6 +229,46 @@ static void capture_vcycle(lap_hierarchy *h) {
     h->cur = save;
 }
 
+// Stream-ordered pool warm-up: the pool's physical memory only grows when a
+// request does not fit its free chunks, and growing it (mapping GBs) stalls a
+// setup by 30-90 ms at cfg 4 sizes.  Before each setup, make sure the pool
+// holds one chunk as large as the biggest setup peak seen so far in this
+// process (+10%): allocate it once and free it back to the pool.
+static size_t g_peak = 0;
+void pool_warm(cudaStream_t s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+    uint64_t zero = 0, reserved = 0, used = 0;
+    if (g_peak) {
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+        const size_t want = g_peak + g_peak / 10;
+        if (reserved < used + want) {
+            void *p = nullptr;
+            if (cudaMallocAsync(&p, want, s) == cudaSuccess) cudaFreeAsync(p, s);
+            else cudaGetLastError();
+        }
+    }
+    // the setup's own high-water mark (not the warm-up block's): reset after the warm-up
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &zero);
+}
+void pool_note_peak() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+    uint64_t hi = 0;
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &hi);
+    if (hi > g_peak) g_peak = hi;
+    if (getenv("LAP_SETUP_TRACE")) {
+        uint64_t reserved = 0;
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+        fprintf(stderr, "[lap setup] pool: peak used %.2f GB, reserved %.2f GB\n", hi / 1e9, reserved / 1e9);
+    }
+}
+
 static bool is_device_ptr(const void *p) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -315,6 +355,7 @@ lap_status lap_setup(const lap_graph *g, const lap_params *pp, void *stream, lap
     try {
         LAP_CUDA(cudaEventCreate(&e0));
         LAP_CUDA(cudaEventCreate(&e1));
+        lap::pool_warm(s);
         LAP_CUDA(cudaEventRecord(e0, s));
         h->cur = lap::Stats{};
         int64_t kl0 = lap::g_kl;
@@ -332,6 +373,7 @@ lap_status lap_setup(const lap_graph *g, const lap_params *pp, void *stream, lap
         h->stats.kernel_launches = h->cur.launches + (lap::g_kl - kl0);
         h->stats.spmv_edges = h->cur.edges;
         h->stats.spmv_bytes = h->cur.bytes;
+        lap::pool_note_peak();
         if (p.use_graphs) {
             lap::capture_vcycle(h);
             lap::capture_pcg(h);
