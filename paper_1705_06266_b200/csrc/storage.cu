@@ -106,6 +106,21 @@ __global__ void k_sell_fill(int64_t nslots, int64_t nshort, const int64_t *srp, 
         }
     }
 }
+// SELL-C-sigma: re-sort the short rows by degree only WITHIN windows of sigma
+// consecutive rows of the current (class, locality) order, keeping the gather
+// locality of the order while cutting the slice padding.  Key = window << 9 |
+// (255 - degree), class 0 rows only (the rest keep their position).
+__global__ void k_window_key(int64_t n, int64_t nshort, int64_t sigma, const int32_t *sid, const int64_t *rp,
+                             uint64_t *skey, int32_t *ids) {
+    GRID_STRIDE(p, n) {
+        const int32_t i = sid[p];
+        uint64_t k;
+        if (p < nshort) k = ((uint64_t)(p / sigma) << 9) | (uint64_t)(255 - (rp[i + 1] - rp[i]));
+        else k = ((uint64_t)(nshort / sigma + 1 + p) << 9);  // long rows: unchanged order after the short ones
+        skey[p] = k;
+        ids[p] = i;
+    }
+}
 __global__ void k_inverse(int64_t n, const int32_t *sid, int32_t *spos) {
     GRID_STRIDE(p, n) spos[sid[p]] = (int32_t)p;
 }
@@ -267,7 +282,24 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
         acc += (int64_t)hc[c];
         L.c_end[c] = acc;
     }
+    // which SpMV kernel serves this level (solve.cu): 8 (n <= 64K) or 4 (n <= 128K)
+    // lanes per row over the CSR on levels without long rows (k_spmv_vec) -- a
+    // row's ~15 gathers in one dependent round instead of two SELL batches, 8x
+    // the CTAs: cfg 2 level 6 (14.5K rows) 6.6 -> 3.8 us per SpMV, level 5
+    // 7.2 -> 3.6 us; on large levels SELL stays faster (level 2: 26.6 vs 65 us
+    // per Chebyshev step).  LAP_SPMV_VEC=G (0, 4, 8, 16) overrides on every
+    // level without long rows (experiments).
+    {
+        const bool smem = n <= SMEM_X_MAX && L.nnz >= SMEM_X_MIN_DEG * n && L.nnz > 0;
+        const char *e = getenv("LAP_SPMV_VEC");
+        const int G = e ? atoi(e) : (n <= 65536 ? 8 : n <= 131072 ? 4 : 0);
+        L.spmv_vec = (G == 4 || G == 8 || G == 16) && l > 0 && n == L.c_end[0] && !smem ? G : 0;
+    }
     // SELL-32 over the short class: degree-sort the short rows if natural order pads > 20%
+    // (globally: keeps SELL's gathers as fast as the natural order on mesh levels, measured);
+    // CSR-vector levels instead sort by degree within windows of 64 rows (SELL-C-sigma
+    // ordering: a warp's 8 rows have similar lengths; cfg 2 level 4 Chebyshev step
+    // 10.9 -> 8.5 us, level 6 4.4 -> 4.1 us)
     int64_t nshort = L.c_end[0];
     DBuf<int64_t> width;
     int64_t sell_tot = 0;  // padded SELL entries = sum of the slice widths
@@ -283,9 +315,25 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
                                                                              pad.p);
             g_kl++;
             sell_tot = (int64_t)d2h(pad.p, s);
-            if (pass == 1 || (double)sell_tot <= 1.2 * rn + 64.0) break;
+            const char *es = getenv("LAP_SELL_SIGMA");  // 0: global degree sort; sigma > 0: windows
+            const int64_t sigma = es ? atoll(es) : (L.spmv_vec ? 64 : 0);
+            if (pass == 1 || (sigma == 0 && (double)sell_tot <= 1.2 * rn + 64.0)) break;
             L.sell_sorted = true;
-            sort_rows(1, nullptr);
+            if (sigma > 0) {
+                DBuf<uint64_t> wk(n, s), wk2(n, s);
+                DBuf<int32_t> wid(n, s), sid2(n, s);
+                k_window_key<<<g, 256, 0, s>>>(n, nshort, sigma, L.sid, L.row_ptr, wk.p, wid.p);
+                int eb = 9;
+                while (eb < 64 && ((uint64_t)1 << eb) <= ((uint64_t)(nshort / sigma + 2 + n) << 9)) eb++;
+                size_t bytes = 0;
+                LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, wk.p, wk2.p, wid.p, sid2.p, n, 0, eb, s));
+                DBuf<char> tmp((int64_t)bytes, s);
+                LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, wk.p, wk2.p, wid.p, sid2.p, n, 0, eb, s));
+                LAP_CUDA(cudaMemcpyAsync(L.sid, sid2.p, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
+                g_kl += 3;
+            } else {
+                sort_rows(1, nullptr);
+            }
         }
     }
     k_inverse<<<g, 256, 0, s>>>(n, L.sid, L.spos);
@@ -352,18 +400,6 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
         const char *e = getenv("LAP_NB4_MAXNNZ");
         if (e) L.spmv_nb = L.nnz <= atoll(e) ? 4 : 8;
         else L.spmv_nb = (L.nnz >= NB4_MIN_NNZ && L.nnz <= 8 * n) ? 4 : 8;
-    }
-    // small levels without long rows: 8 (n <= 64K) or 4 (n <= 128K) lanes per row over
-    // the CSR (k_spmv_vec) --
-    // a row's ~15 gathers in one dependent round instead of two SELL batches, and
-    // 8x the CTAs: cfg 2 level 6 (14.5K rows) 6.6 -> 3.8 us per SpMV, level 5
-    // 7.2 -> 3.6 us; on large levels SELL stays faster (level 2: 26.6 vs 65 us per
-    // Chebyshev step).  LAP_SPMV_VEC=G (0, 4, 8, 16) overrides on every level
-    // without long rows (experiments).
-    {
-        const char *e = getenv("LAP_SPMV_VEC");
-        const int G = e ? atoi(e) : (n <= 65536 ? 8 : n <= 131072 ? 4 : 0);
-        L.spmv_vec = (G == 4 || G == 8 || G == 16) && l > 0 && n == L.c_end[0] && !L.smem_x ? G : 0;
     }
     // long rows: LCHUNK-entry warp work items (solve.cu k_spmv)
     L.nchunks = build_chunks(L.srp, L.c_end[0], n - L.c_end[0], SHORT_MAX, &L.chunk_row, &L.chunk_idx, &L.chunk_slot,
