@@ -89,3 +89,19 @@ def test_block_invalid(P):
     h = P.Hierarchy(g)
     with pytest.raises(P.LapError):
         h.solve_block(np.zeros((9, g.n)))
+
+
+def test_block_max_iters_and_tolerance(P):
+    """max_iters reached -> LAP_ENOCONV with every column's iteration count at
+    the cap and its residual above tol (as lap_solve reports it); a looser
+    tolerance stops each column at the oracle's iteration count for it."""
+    g = lapgen.grid2d(64, 64)
+    B = _rhs(g.n, 3, seed=21)
+    X, it, rr, rc = P.Hierarchy(g, max_iters=4).solve_block(B)
+    assert rc == P.LAP_ENOCONV and np.all(it == 4) and np.all(rr > 1e-8)
+    ho = oracle.Hierarchy(g)
+    X, it, rr, rc = P.Hierarchy(g).solve_block(B, tol=1e-5)
+    assert rc == 0 and np.all(rr <= 1e-5)
+    for j in range(3):
+        _, ito, _, _ = ho.solve(B[j], tol=1e-5)
+        assert abs(int(it[j]) - ito) <= 1, (j, it[j], ito)

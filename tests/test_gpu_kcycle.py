@@ -145,3 +145,22 @@ def test_kcycle_tail_program_is_one_launch(P):
     assert rc == 0 and rr <= 1e-8
     # per outer iteration: level-0 cycle (elimination: restrict + tail + prolong) + FCG vector ops
     assert st["kernel_launches"] <= 20 * (it + 2), (st["kernel_launches"], it)
+
+
+@pytest.mark.parametrize("kw", [dict(kcycle_inner=1), dict(kcycle_inner=3), dict(elim_enable=0),
+                                dict(cheby_degree=3)], ids=["inner1", "inner3", "no-elim", "cheb3"])
+def test_kcycle_parameters_match_oracle(P, kw):
+    """The K-cycle under other parameter choices (inner FCG iterations,
+    no elimination levels, degree-3 smoothing) against the oracle with the
+    same parameters."""
+    for g in [lapgen.grid2d(120, 90), lapgen.rmat(12)]:
+        h = P.Hierarchy(g, cycle=1, **kw)
+        ho = oracle.Hierarchy(g, cycle=1, **kw)
+        r = np.random.default_rng(3).standard_normal(g.n)
+        r -= r.mean()
+        z, zo = h.kcycle(0, r), ho.kcycle(0, r)
+        assert _close(z, zo, 1e-9), np.abs(z - zo).max() / np.abs(zo).max()
+        b = lapgen.rhs(g.n, seed=6)
+        x, it, rr, rc = h.solve(b)
+        xo, ito, _, rco = ho.solve(b)
+        assert rc == 0 and rco == 0 and rr <= 1e-8 and abs(it - ito) <= 1, (it, ito, rr)
