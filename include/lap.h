@@ -113,7 +113,8 @@ lap_status lap_setup(const lap_graph *g, const lap_params *p, void *cuda_stream,
                      lap_hierarchy **out);
 
 /* Solve L x = b to relative residual tol (<= 0: use params.tol) with PCG +
- * V-cycle (O-S8).  b, x: length n in the caller's
+ * V-cycle (O-S8), or FCG(1) + K-cycle when the hierarchy
+ * was built with params.cycle = 1.  b, x: length n in the caller's
  * numbering.  A copy of b is projected to mean zero; x is returned mean-zero.
  * *iters = number of L p products; *rel_residual = ||b - L x|| / ||b||
  * recomputed at the end.  b = const -> x = 0, iters = 0, LAP_OK.

@@ -17,7 +17,9 @@
  * Parity-unpinned functions (no external truth beyond invariants, SURVEY
  * O-P16): the aggregates / F sets / coarse operators produced for the five
  * BASELINE.json configs as a whole.  Every building block below is pinned by
- * tests/test_oracle_*.py (brute force, closed forms, SPEC worked examples).
+ * tests/test_oracle_*.py (brute force, closed forms, SPEC worked examples);
+ * the K-cycle (orc_kcycle / orc_kcoarse, N2) by the FCG Gram-system identity
+ * and the V-cycle/PCG special cases (tests/test_oracle_kcycle.py).
  */
 #ifndef LAP_ORACLE_H
 #define LAP_ORACLE_H
