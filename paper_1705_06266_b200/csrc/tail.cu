@@ -36,26 +36,44 @@ __global__ void k_b_cheb_first(int64_t n, int64_t k, const double *__restrict__ 
     }
 }
 // the SpMV epilogues of solve.cu (E_CHEB = 3, E_RESID = 2, E_CHEB0 = 5), column by column
+// A thread owns row i of BC consecutive columns: each matrix entry is loaded
+// once for BC gathers (the matrix was re-read once per column: ~1 GB of L2
+// traffic per pass on cfg 2's 2486-column tail); per column, the row sum and
+// the epilogue are the single-column ones.
+constexpr int BC = 4;
 template <int EPI>
 __global__ void k_b_spmv(int64_t n, int64_t k, const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
                          const double *__restrict__ w, const double *__restrict__ d, const double *__restrict__ X,
                          double *__restrict__ Y, const double *__restrict__ B, double *__restrict__ DV, double c1,
                          double c2) {
-    FOR_ELEM(e, n * k) {
-        const int64_t i = e % n, c0 = e - i;
-        double ax = 0.0;
-        for (int64_t q = rp[i]; q < rp[i + 1]; q++) ax += w[q] * X[c0 + col[q]];
-        const double xi = X[e], lx = d[i] * xi - ax;
-        if (EPI == 2) {
-            Y[e] = B[e] - lx;
-        } else if (EPI == 3) {
-            double dv = c1 * DV[e] + c2 * ((B[e] - lx) / d[i]);
-            DV[e] = dv;
-            Y[e] = xi + dv;
-        } else {
-            double dv = c2 * ((B[e] - lx) / d[i]);
-            DV[e] = dv;
-            Y[e] = xi + dv;
+    const int64_t ngrp = (k + BC - 1) / BC;
+    FOR_ELEM(e0, n * ngrp) {
+        const int64_t i = e0 % n, cb = (e0 / n) * BC;
+        const int nc = (int)min((int64_t)BC, k - cb);
+        double ax[BC] = {0.0, 0.0, 0.0, 0.0};
+        for (int64_t q = rp[i]; q < rp[i + 1]; q++) {
+            const double wq = w[q];
+            const int64_t j = col[q];
+#pragma unroll
+            for (int u = 0; u < BC; u++)
+                if (u < nc) ax[u] += wq * X[(cb + u) * n + j];
+        }
+#pragma unroll
+        for (int u = 0; u < BC; u++) {
+            if (u >= nc) break;
+            const int64_t e = (cb + u) * n + i;
+            const double xi = X[e], lx = d[i] * xi - ax[u];
+            if (EPI == 2) {
+                Y[e] = B[e] - lx;
+            } else if (EPI == 3) {
+                double dv = c1 * DV[e] + c2 * ((B[e] - lx) / d[i]);
+                DV[e] = dv;
+                Y[e] = xi + dv;
+            } else {
+                double dv = c2 * ((B[e] - lx) / d[i]);
+                DV[e] = dv;
+                Y[e] = xi + dv;
+            }
         }
     }
 }
@@ -216,12 +234,12 @@ static void vcycle_batched(lap_hierarchy *h, int l, int64_t k, std::vector<BWork
     double rho_old = 1.0 / sigma;
     for (int q = 1; q < K; q++) {
         double rho = 1.0 / (2.0 * sigma - rho_old);
-        k_b_spmv<3><<<bg(n * k), 256, 0, s>>>(n, k, L.srp, L.scol, L.sw, L.sd, cur, alt, B, w.dv, rho * rho_old,
+        k_b_spmv<3><<<bg(n * ((k + BC - 1) / BC)), 256, 0, s>>>(n, k, L.srp, L.scol, L.sw, L.sd, cur, alt, B, w.dv, rho * rho_old,
                                                 2.0 * rho / delta);
         std::swap(cur, alt);
         rho_old = rho;
     }
-    k_b_spmv<2><<<bg(n * k), 256, 0, s>>>(n, k, L.srp, L.scol, L.sw, L.sd, cur, w.r, B, w.dv, 0.0, 0.0);
+    k_b_spmv<2><<<bg(n * ((k + BC - 1) / BC)), 256, 0, s>>>(n, k, L.srp, L.scol, L.sw, L.sd, cur, w.r, B, w.dv, 0.0, 0.0);
     k_b_restrict<<<bg(L.m * k), 256, 0, s>>>(L.m, n, k, L.mem_ptr, L.members, w.r, WC.b);
     vcycle_batched(h, l + 1, k, W, WC.b, WC.x, s);
     k_b_prolong<<<bg(n * k), 256, 0, s>>>(n, L.m, k, L.agg_s, WC.x, cur);
@@ -229,10 +247,10 @@ static void vcycle_batched(lap_hierarchy *h, int l, int64_t k, std::vector<BWork
     for (int q = 0; q < K; q++) {
         double *dst = (q == K - 1) ? Xout : alt;
         if (q == 0) {
-            k_b_spmv<5><<<bg(n * k), 256, 0, s>>>(n, k, L.srp, L.scol, L.sw, L.sd, cur, dst, B, w.dv, 0.0, 1.0 / theta);
+            k_b_spmv<5><<<bg(n * ((k + BC - 1) / BC)), 256, 0, s>>>(n, k, L.srp, L.scol, L.sw, L.sd, cur, dst, B, w.dv, 0.0, 1.0 / theta);
         } else {
             double rho = 1.0 / (2.0 * sigma - rho_old);
-            k_b_spmv<3><<<bg(n * k), 256, 0, s>>>(n, k, L.srp, L.scol, L.sw, L.sd, cur, dst, B, w.dv, rho * rho_old,
+            k_b_spmv<3><<<bg(n * ((k + BC - 1) / BC)), 256, 0, s>>>(n, k, L.srp, L.scol, L.sw, L.sd, cur, dst, B, w.dv, rho * rho_old,
                                                     2.0 * rho / delta);
             rho_old = rho;
         }
