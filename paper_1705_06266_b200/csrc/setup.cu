@@ -113,21 +113,22 @@ __global__ void k_rowof(int64_t n, const int64_t *__restrict__ row_ptr, int32_t 
 // by (col, row), must equal the CSR list in (row, col) order entry for entry.
 // An exact check with one radix sort instead of a binary search per entry
 // (which serialises on hub rows).
-template <int G>
+template <int G, class IT>  // IT: entry index type (int32 below 2^31 entries: 4 sort bytes less per entry)
 __global__ void k_sym_keys(int64_t n, int cbits, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                           int32_t *__restrict__ rowof, uint64_t *__restrict__ tkey, int64_t *__restrict__ idx) {
+                           int32_t *__restrict__ rowof, uint64_t *__restrict__ tkey, IT *__restrict__ idx) {
     GROUP_LOOP_BEGIN(G, n)
     if (live)
         for (int64_t k = row_ptr[i] + gl; k < row_ptr[i + 1]; k += G) {
             rowof[k] = (int32_t)i;
             tkey[k] = ((uint64_t)(uint32_t)col[k] << cbits) | (uint64_t)i;
-            idx[k] = k;
+            idx[k] = (IT)k;
         }
     GROUP_LOOP_END
 }
+template <class IT>
 __global__ void k_sym_check(int64_t nnz, int cbits, const int32_t *__restrict__ rowof, const int32_t *__restrict__ col,
                             const double *__restrict__ w, const uint64_t *__restrict__ tkey,
-                            const int64_t *__restrict__ idx, int *flag) {
+                            const IT *__restrict__ idx, int *flag) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nnz; t += (int64_t)gridDim.x * blockDim.x) {
         uint64_t want = ((uint64_t)(uint32_t)rowof[t] << cbits) | (uint64_t)(uint32_t)col[t];
         bool bad = tkey[t] != want;
@@ -136,14 +137,28 @@ __global__ void k_sym_check(int64_t nnz, int cbits, const int32_t *__restrict__ 
     }
 }
 
-static bool is_symmetric(int64_t n, int64_t nnz, const int64_t *rp, const int32_t *col, const double *w,
-                         cudaStream_t s) {
-    if (nnz == 0) return true;
+template <class IT>
+static bool is_symmetric_t(int64_t n, int64_t nnz, const int64_t *rp, const int32_t *col, const double *w,
+                           cudaStream_t s) {
     DBuf<int32_t> rowof(nnz, s);
     DBuf<uint64_t> k1(nnz, s), k2(nnz, s);
-    DBuf<int64_t> i1(nnz, s), i2(nnz, s);
+    DBuf<IT> i1(nnz, s), i2(nnz, s);
     const int cbits = bitlen_u64((uint64_t)n);  // columns are validated < n before this check
-    LAUNCH_G(group_size(n, nnz), k_sym_keys, n, s, n, cbits, rp, col, rowof.p, k1.p, i1.p);
+#define SYM_KEYS(GG) k_sym_keys<GG, IT>
+    {
+        const int G = group_size(n, nnz);
+        const unsigned gr = grid_for(n * G, 256, 148 * 16);
+        switch (G) {
+            case 1: SYM_KEYS(1)<<<gr, 256, 0, s>>>(n, cbits, rp, col, rowof.p, k1.p, i1.p); break;
+            case 2: SYM_KEYS(2)<<<gr, 256, 0, s>>>(n, cbits, rp, col, rowof.p, k1.p, i1.p); break;
+            case 4: SYM_KEYS(4)<<<gr, 256, 0, s>>>(n, cbits, rp, col, rowof.p, k1.p, i1.p); break;
+            case 8: SYM_KEYS(8)<<<gr, 256, 0, s>>>(n, cbits, rp, col, rowof.p, k1.p, i1.p); break;
+            case 16: SYM_KEYS(16)<<<gr, 256, 0, s>>>(n, cbits, rp, col, rowof.p, k1.p, i1.p); break;
+            default: SYM_KEYS(32)<<<gr, 256, 0, s>>>(n, cbits, rp, col, rowof.p, k1.p, i1.p); break;
+        }
+        ++g_kl;
+    }
+#undef SYM_KEYS
     size_t bytes = 0;
     int end_bit = 2 * cbits;
     LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k1.p, k2.p, i1.p, i2.p, nnz, 0, end_bit, s));
@@ -151,9 +166,16 @@ static bool is_symmetric(int64_t n, int64_t nnz, const int64_t *rp, const int32_
     LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, k1.p, k2.p, i1.p, i2.p, nnz, 0, end_bit, s)); ++g_kl;
     DBuf<int> flag(1, s);
     LAP_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
-    k_sym_check<<<grid_for(nnz, 256, 148 * 16), 256, 0, s>>>(nnz, cbits, rowof.p, col, w, k2.p, i2.p, flag.p); ++g_kl;
+    k_sym_check<IT><<<grid_for(nnz, 256, 148 * 16), 256, 0, s>>>(nnz, cbits, rowof.p, col, w, k2.p, i2.p, flag.p);
+    ++g_kl;
     LAP_CHECK_LAUNCH();
     return d2h_scalar(flag.p, s) == 0;
+}
+static bool is_symmetric(int64_t n, int64_t nnz, const int64_t *rp, const int32_t *col, const double *w,
+                         cudaStream_t s) {
+    if (nnz == 0) return true;
+    return nnz < ((int64_t)1 << 31) ? is_symmetric_t<int32_t>(n, nnz, rp, col, w, s)
+                                    : is_symmetric_t<int64_t>(n, nnz, rp, col, w, s);
 }
 
 // ---- connectivity: lock-free union-find (parents only ever decrease) ----

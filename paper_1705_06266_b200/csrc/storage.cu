@@ -54,15 +54,16 @@ __global__ void k_key_elim(int64_t nc, const int32_t *cid, const int32_t *fspos,
 __device__ __forceinline__ int deg_class(int64_t dg) {
     return dg <= SHORT_MAX ? 0 : dg <= 1024 ? 1 : dg <= HUB_CHUNK ? 2 : 3;
 }
-// sort key: [63:62] degree class, [61:54] 255 - degree (short rows, only if
-// degree-sorted), [53:0] locality key
+// sort key: [40:39] degree class, [38:31] 255 - degree (short rows, only if
+// degree-sorted), [30:0] locality key (< n < 2^31)
 __global__ void k_class_key(int64_t n, const int64_t *rp, const uint64_t *key, uint64_t *skey, int32_t *ids,
                             unsigned long long *cnt, int by_degree) {
     GRID_STRIDE(i, n) {
         int64_t dg = rp[i + 1] - rp[i];
         int c = deg_class(dg);
-        uint64_t k = key[i] | (((uint64_t)c) << 62);
-        if (by_degree && c == 0) k |= ((uint64_t)(255 - dg)) << 54;
+        // 41 key bits: 6 radix passes instead of 8
+        uint64_t k = key[i] | (((uint64_t)c) << 39);
+        if (by_degree && c == 0) k |= ((uint64_t)(255 - dg)) << 31;
         skey[i] = k;
         ids[i] = (int32_t)i;
         if (cnt) {  // warp-aggregated class counts (one atomic per class per warp, not per row)
@@ -267,9 +268,9 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
     auto sort_rows = [&](int by_degree, unsigned long long *counts) {
         k_class_key<<<g, 256, 0, s>>>(n, L.row_ptr, key.p, skey.p, ids.p, counts, by_degree);
         size_t bytes = 0;
-        LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, skey.p, key2.p, ids.p, L.sid, n, 0, 64, s));
+        LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, skey.p, key2.p, ids.p, L.sid, n, 0, 41, s));
         DBuf<char> tmp((int64_t)bytes, s);
-        LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, skey.p, key2.p, ids.p, L.sid, n, 0, 64, s));
+        LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, skey.p, key2.p, ids.p, L.sid, n, 0, 41, s));
         g_kl += 3;
         LAP_CHECK_LAUNCH();
     };
