@@ -231,9 +231,9 @@ static void capture_vcycle(lap_hierarchy *h) {
 
 // Stream-ordered pool warm-up: the pool's physical memory only grows when a
 // request does not fit its free chunks, and growing it (mapping GBs) stalls a
-// setup by 30-90 ms at cfg 4 sizes.  Before each setup, make sure the pool
-// holds one chunk as large as the biggest setup peak seen so far in this
-// process (+10%): allocate it once and free it back to the pool.
+// setup by 30-500 ms at cfg 4 sizes.  Before each setup, make sure the pool
+// holds one chunk twice as large as the biggest setup peak seen so far in this
+// process: allocate it once and free it back to the pool.
 static size_t g_peak = 0;
 void pool_warm(cudaStream_t s) {
     int dev = 0;
@@ -244,7 +244,7 @@ void pool_warm(cudaStream_t s) {
     if (g_peak) {
         cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
         cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
-        const size_t want = g_peak + g_peak / 10;
+        const size_t want = 2 * g_peak;  // headroom against fragmentation (1.1x still grew now and then)
         if (reserved < used + want) {
             void *p = nullptr;
             if (cudaMallocAsync(&p, want, s) == cudaSuccess) cudaFreeAsync(p, s);
