@@ -712,7 +712,12 @@ static bool cycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, cu
        // of hubs have up to degree + 1 members: a few lanes would serialise them)
         const int64_t avg = (n + L.m - 1) / std::max<int64_t>(1, L.m);
         // (small levels are latency-bound: 8 lanes keep a member's loads in parallel)
-        const int G = (L.nchunks > 0 || L.m < 65536) ? 8 : avg <= 4 ? 1 : avg <= 8 ? 2 : avg <= 16 ? 4 : 8;
+        static const int Gforce = [] {  // LAP_RESTRICT_G=1|2|4|8 (experiments)
+            const char *e = getenv("LAP_RESTRICT_G");
+            return e ? atoi(e) : 0;
+        }();
+        const int G = Gforce ? Gforce
+                             : (L.nchunks > 0 || L.m < 65536) ? 8 : avg <= 4 ? 1 : avg <= 8 ? 2 : avg <= 16 ? 4 : 8;
         const unsigned rg = grid_for(L.m * G, 256, 148 * 8);
         if (G == 1) launch_pdl(k_restrict<1>, rg, 256, s, L.m, L.mem_ptr, L.members, L.r, C.b, p0);
         else if (G == 2) launch_pdl(k_restrict<2>, rg, 256, s, L.m, L.mem_ptr, L.members, L.r, C.b, p0);
