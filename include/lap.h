@@ -124,6 +124,14 @@ lap_status lap_solve(lap_hierarchy *h, const double *b, double *x, double tol,
 
 void lap_free(lap_hierarchy *h);   /* NULL-safe */
 
+/* Device memory: liblap allocates from a stream-ordered pool of its own (never
+ * the device's default pool, so PyTorch's caching allocator and NCCL are not
+ * starved).  When the last live hierarchy is freed the pool is trimmed down to
+ * `bytes` of reservation (default 0: everything goes back to the device).  A
+ * caller that runs setups in a loop may retain the reservation (e.g. 2^40) to
+ * avoid re-mapping gigabytes at every setup; lap_pool_retain(0) releases it. */
+void lap_pool_retain(uint64_t bytes);
+
 /* ---- introspection (host output buffers sized from lap_level_info) ------ */
 lap_status lap_num_levels(const lap_hierarchy *h, int32_t *nlev);
 /* kind: 0 aggregation, 1 elimination, 2 coarsest.  lambda_hat only for kind 0. */
@@ -196,6 +204,18 @@ lap_status lap_setup_dist(const lap_graph *g, const lap_params *p, lap_comm *c, 
  * (block-cyclic in blocks of 256 rows); *piece_size = padded piece length. */
 lap_status lap_dist_index(int64_t n, int32_t nranks, int64_t m, const int64_t *rows, int64_t *dist,
                           int64_t *piece_size);
+
+/* Test hook: the method's counter-based random streams (SURVEY O-S11, O-R17,
+ * O-R7/O-R33, O-S6), evaluated on the device by the same functions the setup
+ * kernels use, copied to the HOST buffer `out`:
+ *   which = 0: out[i] = h(i) = mix64(i XOR salt_2)          (uint64, n)
+ *   which = 1: out[4i+k] = X0[i,k] of (level, attempt)      (double, 4n)
+ *   which = 2: out[i] = Lanczos start v_i of `level`, before normalisation
+ *              (2 u01(mix64(mix64(salt_4 XOR 2 level) XOR i)) - 1; double, n) P:643
+ *   which = 3: out[i] = mix64(i)                            (uint64, n)
+ * LAP_EINVAL for a bad `which` / negative sizes. */
+lap_status lap_random_stream(int32_t which, uint64_t seed, int32_t level, int32_t attempt, int64_t n, void *out,
+                             void *cuda_stream);
 
 /* ---- counters for the benchmark ----------------------------------------- */
 typedef struct {

@@ -91,6 +91,8 @@ def lib():
             "orc_galerkin": (i64, [i64, P, P, P, P, i64, P, P, P, P]),
             "orc_lanczos": (dbl, [i64, P, P, P, P, u64, i32, i32, P, P, P]),
             "orc_tridiag_max_eig": (dbl, [i32, P, P]),
+            "orc_lanczos_start": (None, [i64, u64, i32, P]),
+            "orc_elim_hash": (u64, [u64, u64]),
             "orc_coarse_pinv": (ctypes.c_int, [i64, P, P, P, P, P]),
             "orc_chebyshev": (None, [i64, P, P, P, P, dbl, dbl, dbl, i32, P, P, i32]),
             "orc_setup": (ctypes.c_int, [i64, P, P, P, P, ctypes.POINTER(P)]),
@@ -252,6 +254,18 @@ def lanczos(n, row_ptr, col, w, d, seed=0, level=0, steps=10):
     lam = lib().orc_lanczos(n, _p(_c(row_ptr, np.int64)), _p(_c(col, np.int32)), _p(_c(w, np.float64)),
                             _p(_c(d, np.float64)), seed, level, steps, _p(al), _p(be), ctypes.byref(k))
     return lam, al[:k.value], be[:k.value]
+
+
+def lanczos_start(n, seed=0, level=0):
+    """Unnormalised Lanczos start vector of level `level` (O-S6, reading R-U')."""
+    v = np.zeros(n)
+    lib().orc_lanczos_start(n, seed, level, _p(v))
+    return v
+
+
+def elim_hash(j: int, seed: int = 0) -> int:
+    """h(j) = mix64(j XOR salt_2) (O-R17)."""
+    return lib().orc_elim_hash(j, seed)
 
 
 def tridiag_max_eig(alpha, beta):

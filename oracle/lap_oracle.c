@@ -276,21 +276,22 @@ void orc_spmv(int64_t n, const int64_t *row_ptr, const int32_t *col, const doubl
  * hash(j) = mix64(j XOR salt_2) (O-R17), or hash_override[j] in tests.
  * Non-candidates are skipped instead of mapped to the infinity sentinel
  * (O-R18).  Returns |F|. */
+uint64_t orc_elim_hash(uint64_t j, uint64_t seed) { return orc_mix64(j ^ orc_salt(seed, 2)); }
+
 int64_t orc_elim_select(int64_t n, const int64_t *row_ptr, const int32_t *col,
                         int32_t max_degree, uint64_t seed, const uint64_t *hash_override,
                         uint8_t *F) {
-    uint64_t s2 = orc_salt(seed, 2);
     int64_t nF = 0;
     for (int64_t i = 0; i < n; i++) {
         F[i] = 0;
         if (row_ptr[i + 1] - row_ptr[i] > max_degree) continue;      /* not a candidate */
         /* z_i = oplus over the closed neighbourhood of candidates */
         int64_t zj = i;
-        uint64_t zh = hash_override ? hash_override[i] : orc_mix64((uint64_t)i ^ s2);
+        uint64_t zh = hash_override ? hash_override[i] : orc_elim_hash((uint64_t)i, seed);
         for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; k++) {
             int64_t j = col[k];
             if (row_ptr[j + 1] - row_ptr[j] > max_degree) continue;  /* otimes -> empty */
-            uint64_t hj = hash_override ? hash_override[j] : orc_mix64((uint64_t)j ^ s2);
+            uint64_t hj = hash_override ? hash_override[j] : orc_elim_hash((uint64_t)j, seed);
             if (hj < zh || (hj == zh && j < zj)) { zh = hj; zj = j; }
         }
         if (zj == i) { F[i] = 1; nF++; }                              /* line 430 */
@@ -671,33 +672,70 @@ double orc_tridiag_max_eig(int32_t k, const double *alpha, const double *beta) {
     return hi;
 }
 
-/* start u_i = 2 U'(l,i) - 1, U'(l,i) = u01(mix64(mix64(salt_4 XOR 2l) XOR i)),
- * normalised; no reorthogonalisation; stop when beta_j <= 1e-14 |alpha_j|. */
+/* Lanczos start vector before normalisation (O-S6, reading R-U' of DESIGN.md):
+ *   v_i = 2 U'(l,i) - 1,  U'(l,i) = u01(mix64(mix64(salt_4 XOR 2l) XOR i)). */
+void orc_lanczos_start(int64_t n, uint64_t seed, int32_t level, double *v) {
+    uint64_t base = orc_mix64(orc_salt(seed, 4) ^ (uint64_t)(2 * level));
+    for (int64_t i = 0; i < n; i++) v[i] = 2.0 * u01(orc_mix64(base ^ (uint64_t)i)) - 1.0;
+}
+
+/* exponent of an exact bound: every |t| < 2^(e(m)+1) for |t| <= m (m finite);
+ * m = 0 -> a sentinel far below any term (all terms are then exactly 0). */
+static int32_t ebound(double m) { return m > 0.0 ? orc_ilogb(m) : -1000; }
+
+/* 10 Lanczos steps on B = D^-1/2 L D^-1/2 (O-R3, O-S6), no
+ * reorthogonalisation, stop when beta_j <= 1e-14 |alpha_j|.  Every sum is a
+ * CanonSum (O-S11; reading R-lambda of DESIGN.md: O-R23 extended to lambda-hat,
+ * so lambda-hat is a deterministic function of the level, bit-identical on
+ * the GPU), with these exact exponent bounds (|v_i| < 2 always: v = y / ||y||):
+ *   ||v0||^2 : terms v_i^2 <= 1                          e_max = 1,  K = n
+ *   (L u)_i  : s_i = CanonSum_j fl(w_ij u_j), |u| < 2 max(rs)
+ *                                    e_max = e(max w) + e(max rs) + 3,  K = nnz
+ *   alpha    : terms fl(y_i v_i), |.| < 2^(e(max|y|)+1) * 2 e_max = e(max|y|) + 2, K = n
+ *   beta^2   : y' = fl(y - fl(alpha v)), |y'| < 2^(max(e(max|y|)+1, e(alpha)+2)+1)
+ *              (+1 for the rounding)   e_max = 2 (max(e(max|y|)+1, e(alpha)+2) + 2), K = n
+ * Each scalar step is one IEEE rounding:
+ *   rs_i = fl(1 / fl(sqrt(d_i))), u_i = fl(rs_i v_i),
+ *   y_i = fl(fl(rs_i fl(fl(d_i u_i) - s_i)) - fl(beta_prev vp_i)),
+ *   v_i = fl(y_i / beta). */
 double orc_lanczos(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *w,
                    const double *d, uint64_t seed, int32_t level, int32_t steps,
                    double *alpha_out, double *beta_out, int32_t *k_out) {
+    int64_t nnz = row_ptr[n];
     double *v = malloc(sizeof(double) * (size_t)n), *vp = calloc((size_t)n, sizeof(double));
     double *u = malloc(sizeof(double) * (size_t)n), *y = malloc(sizeof(double) * (size_t)n);
-    double *rs = malloc(sizeof(double) * (size_t)n);
+    double *rs = malloc(sizeof(double) * (size_t)n), *t = malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    int64_t maxdeg = 0;
+    for (int64_t i = 0; i < n; i++)
+        if (row_ptr[i + 1] - row_ptr[i] > maxdeg) maxdeg = row_ptr[i + 1] - row_ptr[i];
+    double *tr = malloc(sizeof(double) * (size_t)(maxdeg + 1));
     double alpha[64], beta[64];
-    uint64_t base = orc_mix64(orc_salt(seed, 4) ^ (uint64_t)(2 * level));
-    for (int64_t i = 0; i < n; i++) { v[i] = 2.0 * u01(orc_mix64(base ^ (uint64_t)i)) - 1.0; rs[i] = 1.0 / sqrt(d[i]); }
-    double nv = 0.0;
-    for (int64_t i = 0; i < n; i++) nv += v[i] * v[i];
-    nv = sqrt(nv);
-    for (int64_t i = 0; i < n; i++) v[i] /= nv;
+    orc_lanczos_start(n, seed, level, v);
+    for (int64_t i = 0; i < n; i++) rs[i] = 1.0 / sqrt(d[i]);
+    for (int64_t i = 0; i < n; i++) t[i] = v[i] * v[i];
+    double nv = sqrt(orc_canon_sum(t, n, 1, n));
+    for (int64_t i = 0; i < n; i++) v[i] = v[i] / nv;
+    const int32_t e_spmv = ebound(max_abs(w, nnz)) + ebound(max_abs(rs, n)) + 3;
     int32_t k = 0;
     double bprev = 0.0;
     for (int32_t j = 0; j < steps; j++) {
         for (int64_t i = 0; i < n; i++) u[i] = rs[i] * v[i];
-        orc_spmv(n, row_ptr, col, w, d, u, y);                      /* y = L D^-1/2 v */
-        for (int64_t i = 0; i < n; i++) y[i] = rs[i] * y[i] - bprev * vp[i];
-        double a = 0.0;
-        for (int64_t i = 0; i < n; i++) a += y[i] * v[i];
-        for (int64_t i = 0; i < n; i++) y[i] -= a * v[i];
-        double b = 0.0;
-        for (int64_t i = 0; i < n; i++) b += y[i] * y[i];
-        b = sqrt(b);
+        for (int64_t i = 0; i < n; i++) {                            /* y = D^-1/2 L D^-1/2 v - beta vp */
+            int64_t c = 0;
+            for (int64_t q = row_ptr[i]; q < row_ptr[i + 1]; q++) tr[c++] = w[q] * u[col[q]];
+            double si = orc_canon_sum(tr, c, e_spmv, nnz);
+            double li = d[i] * u[i] - si;
+            double bv = bprev * vp[i];
+            y[i] = rs[i] * li - bv;
+        }
+        int32_t ey = ebound(max_abs(y, n));
+        for (int64_t i = 0; i < n; i++) t[i] = y[i] * v[i];
+        double a = orc_canon_sum(t, n, ey + 2, n);
+        for (int64_t i = 0; i < n; i++) { double av = a * v[i]; y[i] = y[i] - av; }
+        int32_t ea = ebound(fabs(a));
+        int32_t eb = 2 * ((ey + 1 > ea + 2 ? ey + 1 : ea + 2) + 2);
+        for (int64_t i = 0; i < n; i++) t[i] = y[i] * y[i];
+        double b = sqrt(orc_canon_sum(t, n, eb, n));
         alpha[k] = a;
         beta[k] = b;
         k++;
@@ -709,7 +747,7 @@ double orc_lanczos(int64_t n, const int64_t *row_ptr, const int32_t *col, const 
     if (alpha_out) memcpy(alpha_out, alpha, sizeof(double) * (size_t)k);
     if (beta_out) memcpy(beta_out, beta, sizeof(double) * (size_t)k);
     if (k_out) *k_out = k;
-    free(v); free(vp); free(u); free(y); free(rs);
+    free(v); free(vp); free(u); free(y); free(rs); free(t); free(tr);
     return lam;
 }
 

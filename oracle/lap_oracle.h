@@ -104,6 +104,8 @@ void orc_row_sums(int64_t n, const int64_t *row_ptr, const double *w, double *d)
 /* --- primitives (each pinned in tests) ------------------------------------ */
 void orc_spmv(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *w,
               const double *d, const double *x, double *y);
+/* h(j) = mix64(j XOR salt_2) (O-R17) */
+uint64_t orc_elim_hash(uint64_t j, uint64_t seed);
 int64_t orc_elim_select(int64_t n, const int64_t *row_ptr, const int32_t *col,
                         int32_t max_degree, uint64_t seed, const uint64_t *hash_override,
                         uint8_t *F);
@@ -133,6 +135,7 @@ int64_t orc_galerkin(int64_t n, const int64_t *row_ptr, const int32_t *col, cons
 double orc_lanczos(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *w,
                    const double *d, uint64_t seed, int32_t level, int32_t steps,
                    double *alpha_out, double *beta_out, int32_t *k_out);
+void orc_lanczos_start(int64_t n, uint64_t seed, int32_t level, double *v /* n, unnormalised */);
 double orc_tridiag_max_eig(int32_t k, const double *alpha, const double *beta);
 int  orc_coarse_pinv(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *w,
                      const double *d, double *pinv);

@@ -47,23 +47,48 @@ bool pdl_enabled() {
     return v == 1;
 }
 
-static bool g_pool_init = false;
-void *dalloc(size_t bytes, cudaStream_t s) {
-    if (!g_pool_init) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-        g_pool_init = true;
+// liblap's own stream-ordered pool, one per device (never the device's default
+// pool: memory a pool holds is invisible to other allocators of the process --
+// PyTorch's caching allocator, NCCL -- so the library keeps its reservation in
+// a pool of its own and trims it when the last hierarchy is freed).
+static cudaMemPool_t g_pool[64];
+static bool g_pool_ok[64];
+static int g_live = 0;  // hierarchies alive (lap_setup .. lap_free)
+static uint64_t g_retain = 0;  // bytes the pool keeps reserved when idle (lap_pool_retain)
+cudaMemPool_t lib_pool() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) throw Error{LAP_ECUDA, "device ordinal out of range"};
+    if (!g_pool_ok[dev]) {
+        cudaMemPoolProps pr;
+        std::memset(&pr, 0, sizeof(pr));
+        pr.allocType = cudaMemAllocationTypePinned;
+        pr.handleTypes = cudaMemHandleTypeNone;
+        pr.location.type = cudaMemLocationTypeDevice;
+        pr.location.id = dev;
+        cudaError_t e = cudaMemPoolCreate(&g_pool[dev], &pr);
+        if (e != cudaSuccess) throw Error{LAP_ECUDA, std::string("cudaMemPoolCreate: ") + cudaGetErrorString(e)};
+        uint64_t thr = UINT64_MAX;  // keep freed memory reserved between setups (no re-mapping stalls)
+        cudaMemPoolSetAttribute(g_pool[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+        g_pool_ok[dev] = true;
     }
+    return g_pool[dev];
+}
+void live_add(int d) { g_live += d; }
+// return the pool's reservation to the device once no hierarchy is alive
+void pool_trim_if_idle() {
+    if (g_live > 0) return;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && g_pool_ok[dev]) cudaMemPoolTrimTo(g_pool[dev], (size_t)g_retain);
+}
+void *dalloc(size_t bytes, cudaStream_t s) {
+    cudaMemPool_t pool = lib_pool();
     void *p = nullptr;
-    cudaError_t e = cudaMallocAsync(&p, bytes ? bytes : 1, s);
+    cudaError_t e = cudaMallocFromPoolAsync(&p, bytes ? bytes : 1, pool, s);
     if (e != cudaSuccess)
         throw Error{e == cudaErrorMemoryAllocation ? LAP_ENOMEM : LAP_ECUDA,
-                    std::string("cudaMallocAsync: ") + cudaGetErrorString(e)};
+                    std::string("cudaMallocFromPoolAsync: ") + cudaGetErrorString(e)};
     static int poison = -1;  // LAP_POISON=1: fill new allocations with NaN bytes (tests)
     if (poison < 0) {
         const char *v = getenv("LAP_POISON");
@@ -236,18 +261,21 @@ static void capture_vcycle(lap_hierarchy *h) {
 // process: allocate it once and free it back to the pool.
 static size_t g_peak = 0;
 void pool_warm(cudaStream_t s) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+    cudaMemPool_t pool = lib_pool();
     uint64_t zero = 0, reserved = 0, used = 0;
     if (g_peak) {
         cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
         cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
-        const size_t want = 2 * g_peak;  // headroom against fragmentation (1.1x still grew now and then)
-        if (reserved < used + want) {
+        size_t want = 2 * g_peak;  // headroom against fragmentation (1.1x still grew now and then)
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+            // never reserve beyond what the device has free (leave 5% for other allocators)
+            const size_t cap = (size_t)((double)(fr + (reserved - used)) * 0.95);
+            want = std::min(want, cap);
+        }
+        if (want > 0 && reserved < used + want) {
             void *p = nullptr;
-            if (cudaMallocAsync(&p, want, s) == cudaSuccess) cudaFreeAsync(p, s);
+            if (cudaMallocFromPoolAsync(&p, want, pool, s) == cudaSuccess) cudaFreeAsync(p, s);
             else cudaGetLastError();
         }
     }
@@ -255,10 +283,7 @@ void pool_warm(cudaStream_t s) {
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &zero);
 }
 void pool_note_peak() {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+    cudaMemPool_t pool = lib_pool();
     uint64_t hi = 0;
     cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &hi);
     if (hi > g_peak) g_peak = hi;
@@ -330,6 +355,23 @@ void lap_params_default(lap_params *p) {
 }
 
 const char *lap_last_error(void) { return lap::g_err.c_str(); }
+
+lap_status lap_random_stream(int32_t which, uint64_t seed, int32_t level, int32_t attempt, int64_t n, void *out,
+                             void *stream) {
+    if (which < 0 || which > 3 || n < 0 || level < 0 || attempt < 0 || (n > 0 && !out)) {
+        lap::set_error("lap_random_stream: invalid arguments");
+        return LAP_EINVAL;
+    }
+    LAP_API_BEGIN
+    if (n > 0) lap::random_stream(which, seed, level, attempt, n, out, (cudaStream_t)stream);
+    return LAP_OK;
+    LAP_API_END
+}
+
+void lap_pool_retain(uint64_t bytes) {
+    lap::g_retain = bytes;
+    lap::pool_trim_if_idle();
+}
 const char *lap_version(void) { return "liblap 0.1 (sm_100a)"; }
 
 lap_status lap_setup(const lap_graph *g, const lap_params *pp, void *stream, lap_hierarchy **out) {
@@ -349,6 +391,7 @@ lap_status lap_setup(const lap_graph *g, const lap_params *pp, void *stream, lap
     }
     cudaStream_t s = (cudaStream_t)stream;
     lap_hierarchy *h = new lap_hierarchy();
+    lap::live_add(1);
     h->p = p;
     cudaGetDevice(&h->device);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -446,6 +489,8 @@ void lap_free(lap_hierarchy *h) {
     cudaStreamSynchronize(s);
     lap::vc_forget(h);
     delete h;
+    lap::live_add(-1);
+    lap::pool_trim_if_idle();
 }
 
 lap_status lap_solve(lap_hierarchy *h, const double *b, double *x, double tol, int32_t *iters, double *rel_residual,

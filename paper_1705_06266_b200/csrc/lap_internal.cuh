@@ -255,6 +255,7 @@ bool ktail_launch(lap_hierarchy *h, int l, bool pre0_done, cudaStream_t s);
 void solve_block(lap_hierarchy *h, int k, const double *B, double *X, double tol, int32_t *iters, double *relres,
                  int *conv, cudaStream_t s);                                   // N4 (block.cu)
 void free_block(lap_hierarchy *h);
+void random_stream(int which, uint64_t seed, int level, int attempt, int64_t n, void *out, cudaStream_t s);
 // multi-GPU (dist.cu)
 void build_dist(lap_hierarchy *h, lap_comm *c, cudaStream_t s);
 void free_dist(lap_hierarchy *h);

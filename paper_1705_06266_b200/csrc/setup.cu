@@ -83,13 +83,20 @@ static double max_abs(const double *v, int64_t n, cudaStream_t s) {
 // O-S0 validation: warp per row
 // =========================================================================
 
+// pass 1 of the validation touches row_ptr only: monotone and within
+// [0, nnz], so that pass 2 never reads col/w out of bounds
+__global__ void k_validate_rowptr(int64_t n, int64_t nnz, const int64_t *__restrict__ row_ptr, int *flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = row_ptr[i], e = row_ptr[i + 1];
+        if (a < 0 || e < a || e > nnz) atomicOr(flag, 1);
+    }
+}
 template <int G>
 __global__ void k_validate(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                            const double *__restrict__ w, int *flag) {
     GROUP_LOOP_BEGIN(G, n)
     if (live) {
         int64_t a = row_ptr[i], e = row_ptr[i + 1];
-        if (gl == 0 && e < a) atomicOr(flag, 1);
         for (int64_t k = a + gl; k < e; k += G) {
             int32_t j = col[k];
             bool bad = (j < 0) || (j >= n) || (j == i) || (k > a && col[k - 1] >= j);
@@ -498,6 +505,9 @@ __global__ void k_relabel_emit(int64_t n, const int64_t *__restrict__ row_ptr, c
 // O-S2 elimination (Alg. 2; O-R17..O-R22) and Schur
 // =========================================================================
 
+// h(j) = mix64(j XOR salt_2) (O-R17)
+__device__ __forceinline__ uint64_t elim_hash(int64_t j, uint64_t salt2) { return mix64((uint64_t)j ^ salt2); }
+
 __global__ void k_elim_select(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
                               int maxdeg, uint64_t salt2, uint8_t *__restrict__ F, unsigned long long *nF) {
     int64_t cnt = 0;
@@ -505,12 +515,12 @@ __global__ void k_elim_select(int64_t n, const int64_t *__restrict__ row_ptr, co
         int64_t a = row_ptr[i], e = row_ptr[i + 1];
         uint8_t f = 0;
         if (e - a <= maxdeg) {                       // candidate (O-R19)
-            uint64_t bh = mix64((uint64_t)i ^ salt2);
+            uint64_t bh = elim_hash(i, salt2);
             int64_t bj = i;
             for (int64_t k = a; k < e; k++) {         // oplus_elim over the closed neighbourhood
                 int64_t j = col[k];
                 if (row_ptr[j + 1] - row_ptr[j] > maxdeg) continue;
-                uint64_t hj = mix64((uint64_t)j ^ salt2);
+                uint64_t hj = elim_hash(j, salt2);
                 if (hj < bh || (hj == bh && j < bj)) { bh = hj; bj = j; }
             }
             f = (bj == i);
@@ -971,93 +981,202 @@ __global__ void __launch_bounds__(256) k_gal_emit(int64_t n, int64_t nnz, const 
 // O-S6 lambda-hat: Lanczos on D^-1/2 L D^-1/2 (O-R3)
 // =========================================================================
 
-// start vector u_i = 2 U'(l,i) - 1 of logical vertex i, laid out in storage order
-__global__ void k_lz_init(int64_t n, uint64_t base, const int32_t *sid, const double *sd, double *v, double *rs) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
-        v[p] = 2.0 * unit_from(mix64(base ^ (uint64_t)sid[p])) - 1.0;
-        rs[p] = 1.0 / sqrt(sd[p]);
-    }
+// lambda-hat is computed with canonical sums (reading R-lambda of DESIGN.md:
+// O-R23 extended to the Lanczos SpMV and dots), on the logical CSR, so it is a
+// deterministic function of the level and bit-identical to the oracle's
+// orc_lanczos.  Exponent bounds (every |term| < 2^e_max, computed from exact
+// maxima; |v_i| < 2 since v = y / ||y||):
+//   ||v0||^2 : e_max = 1                                  K = n
+//   (L u)_i  : e_max = e(max w) + e(max rs) + 3           K = nnz
+//   alpha    : e_max = e(max|y|) + 2                      K = n
+//   beta^2   : e_max = 2 (max(e(max|y|)+1, e(alpha)+2) + 2)   K = n
+// e(m) = ilogb(m) for m > 0, else -1000.  One step = four launches:
+//   A  v_prev = v, v = fl(y / beta), u = fl(rs v)  (+ records alpha, beta of the
+//      previous step and the breakdown test beta <= 1e-14 |alpha|)
+//   B  y = fl(fl(rs fl(fl(d u) - s)) - fl(beta_prev v_prev)), s = CanonSum_j fl(w u_j); max |y|
+//   C  alpha = CanonSum fl(y v)
+//   D  y = fl(y - fl(alpha v)), beta^2 = CanonSum fl(y y)
+// Exact int128 accumulators are global (two 64-bit atomics with carry).
+struct LzState {
+    I128 acc_a, acc_b;          // alpha and beta^2 accumulators
+    unsigned long long maxy;    // bit pattern of max |y|
+    double alpha, bprev;
+    int elo_b;                  // E_lo of the beta^2 instance being read by pass A
+    int stop, k;
+};
+__device__ __forceinline__ int ebound_dev(double m) { return m > 0.0 ? ilogb(m) : -1000; }
+__device__ __forceinline__ void atomic_add_i128(I128 *acc, i128 v) {
+    const unsigned long long lo = (unsigned long long)(u128)v;
+    const unsigned long long hi = (unsigned long long)((u128)v >> 64);
+    const unsigned long long old = atomicAdd(&acc->lo, lo);
+    const unsigned long long carry = (old + lo < old) ? 1ULL : 0ULL;
+    atomicAdd((unsigned long long *)&acc->hi, hi + carry);
 }
-__global__ void k_scale_by(int64_t n, double *v, const double *nrm2) {
-    double f = 1.0 / sqrt(*nrm2);
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) v[i] *= f;
-}
-__global__ void k_hadamard(int64_t n, const double *a, const double *b, double *o) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) o[i] = a[i] * b[i];
-}
-// One Lanczos step is three launches: the SpMV with the E_LZ epilogue
-// (y = rs o (L u) - beta_prev v_prev and the partials of alpha = y.v), then
-// k_lz_mid (every block re-reduces the alpha partials in a fixed order,
-// y -= alpha v, partials of |y|^2), then k_lz_end (every block re-reduces
-// |y|^2, block 0 records alpha, beta and the breakdown test, all blocks
-// advance v_prev = v, v = y / beta, u = rs o v).  Scalars (device):
-// sc[0] alpha, sc[2] beta, sc[3] stopped, sc[4] beta_prev.
-__device__ __forceinline__ double fixed_sum(const double *__restrict__ part, int64_t np, double *sh) {
-    double acc = 0.0;
-    for (int64_t i = threadIdx.x; i < np; i += blockDim.x) acc += part[i];
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    __syncthreads();
-    if (lane == 0) sh[wid] = acc;
+// block-wide exact int128 sum, added once per block into *acc
+__device__ __forceinline__ void block_add_i128(I128 *acc, i128 v) {
+    __shared__ I128 sh[32];
+    v = warp_sum_i128(v);
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) sh[wid] = to_I128(v);
     __syncthreads();
     if (wid == 0) {
-        double r = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0.0;
-        for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-        if (lane == 0) sh[32] = r;
+        i128 t = lane < (int)(blockDim.x >> 5) ? from_I128(sh[lane]) : (i128)0;
+        t = warp_sum_i128(t);
+        if (lane == 0 && t != 0) atomic_add_i128(acc, t);
     }
-    __syncthreads();
-    return sh[32];
 }
-__global__ void __launch_bounds__(256) k_lz_mid(int64_t n, const double *__restrict__ part1, int64_t np1,
-                                                double *__restrict__ y, const double *__restrict__ v, double *sc,
-                                                double *__restrict__ part2) {
-    __shared__ double sh[33];
-    const double stopped = sc[3];
-    double alpha = fixed_sum(part1, np1, sh);
-    if (stopped != 0.0) return;
-    if (blockIdx.x == 0 && threadIdx.x == 0) sc[0] = alpha;
-    double acc = 0.0;
+__device__ __forceinline__ double lz_start_value(uint64_t base, int64_t i) {
+    return __dsub_rn(__dmul_rn(2.0, unit_from(mix64(base ^ (uint64_t)i))), 1.0);
+}
+// y = the unnormalised start vector, rs = fl(1 / fl(sqrt(d))), acc_b += q(y^2)
+__global__ void k_lzc_init(int64_t n, uint64_t base, const double *__restrict__ d, double *__restrict__ y,
+                           double *__restrict__ rs, double *__restrict__ vp, LzState *st, int elo) {
+    i128 acc = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        double t = y[i] - alpha * v[i];
-        y[i] = t;
-        acc += t * t;
+        const double v = lz_start_value(base, i);
+        y[i] = v;
+        vp[i] = 0.0;
+        rs[i] = __ddiv_rn(1.0, __dsqrt_rn(d[i]));
+        acc += canon_q(__dmul_rn(v, v), elo);
     }
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        double r = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
-        for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-        if (threadIdx.x == 0) part2[blockIdx.x] = r;
-    }
+    block_add_i128(&st->acc_b, acc);
 }
-__global__ void __launch_bounds__(256) k_lz_end(int64_t n, const double *__restrict__ part2, int64_t np2,
-                                                const double *__restrict__ y, double *__restrict__ v,
-                                                double *__restrict__ vp, double *__restrict__ u,
-                                                const double *__restrict__ rs, double *sc, double *alpha_rec,
-                                                double *beta_rec, int *k) {
-    __shared__ double sh[33];
-    const double stopped = sc[3];
-    double b2 = fixed_sum(part2, np2, sh);
-    if (stopped != 0.0) return;
-    const double a = sc[0], b = sqrt(b2);
-    const bool stop = b <= 1e-14 * fabs(a);
+// pass A (also the final record-only pass after the last step)
+__global__ void __launch_bounds__(256) k_lzc_next(int64_t n, int first, int record_only, const double *__restrict__ y,
+                                                  double *__restrict__ v, double *__restrict__ vp,
+                                                  double *__restrict__ u, const double *__restrict__ rs, LzState *st,
+                                                  double *alpha_rec, double *beta_rec) {
+    if (st->stop) return;
+    const double b = __dsqrt_rn(canon_result(from_I128(st->acc_b), st->elo_b));
+    bool stop = false;
+    if (!first) {
+        const double a = st->alpha;
+        stop = b <= __dmul_rn(1e-14, fabs(a));
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            alpha_rec[st->k] = a;
+            beta_rec[st->k] = b;
+        }
+    }
+    __syncthreads();  // every block has read st before block 0 updates it
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        alpha_rec[*k] = a;
-        beta_rec[*k] = b;
-        *k += 1;
-        sc[2] = b;
-        sc[4] = b;
-        if (stop) sc[3] = 1.0;
+        if (!first) st->k += 1;
+        if (stop) st->stop = 1;
+        st->bprev = first ? 0.0 : b;
+        st->acc_a.lo = 0;
+        st->acc_a.hi = 0;
+        st->maxy = 0;
     }
-    if (stop) return;
+    if (stop || record_only) return;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        double vi = v[i], vn = y[i] / b;
-        vp[i] = vi;
+        const double vn = __ddiv_rn(y[i], b);
+        if (!first) vp[i] = v[i];
         v[i] = vn;
-        u[i] = rs[i] * vn;
+        u[i] = __dmul_rn(rs[i], vn);
     }
+}
+__device__ __forceinline__ void lzc_row_epilogue(int64_t i, double sk, const double *__restrict__ d,
+                                                 const double *__restrict__ u, const double *__restrict__ rs,
+                                                 const double *__restrict__ vp, double bprev, double *__restrict__ y,
+                                                 unsigned long long *maxy) {
+    const double li = __dsub_rn(__dmul_rn(d[i], u[i]), sk);
+    const double yi = __dsub_rn(__dmul_rn(rs[i], li), __dmul_rn(bprev, vp[i]));
+    y[i] = yi;
+    atomicMax(maxy, (unsigned long long)__double_as_longlong(fabs(yi)));
+}
+// pass B, rows up to SETUP_LONG entries (G lanes per row)
+template <int G>
+__global__ void k_lzc_spmv(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                           const double *__restrict__ w, const double *__restrict__ d, const double *__restrict__ u,
+                           const double *__restrict__ rs, const double *__restrict__ vp, int elo, LzState *st,
+                           double *__restrict__ y) {
+    if (st->stop) return;
+    const double bprev = st->bprev;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->acc_b.lo = 0;  // read by pass A only; pass A of this step has finished
+        st->acc_b.hi = 0;
+    }
+    GROUP_LOOP_BEGIN(G, n)
+        i128 a = 0;
+        const int64_t kb0 = live ? row_ptr[i] : 0, ke0 = live ? row_ptr[i + 1] : 0;
+        const bool skip = ke0 - kb0 > SETUP_LONG;  // long rows: k_lzc_chunk
+        const int64_t kb = skip ? 0 : kb0, ke = skip ? 0 : ke0;
+        for (int64_t k = kb + gl; k < ke; k += G) a += canon_q(__dmul_rn(w[k], u[col[k]]), elo);
+        a = grp_sum_i128<G>(a);
+        if (live && !skip && gl == 0) lzc_row_epilogue(i, canon_result(a, elo), d, u, rs, vp, bprev, y, &st->maxy);
+    GROUP_LOOP_END
+}
+// pass B, rows longer than SETUP_LONG: LCHUNK warp chunks, the last chunk of a
+// row to arrive adds the row's exact partials and applies the epilogue
+__global__ void k_lzc_chunk(int64_t nchunks, const int32_t *__restrict__ crow, const int32_t *__restrict__ cidx,
+                            const int32_t *__restrict__ cslot, int32_t *__restrict__ ccnt, I128 *__restrict__ part,
+                            const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                            const double *__restrict__ w, const double *__restrict__ d, const double *__restrict__ u,
+                            const double *__restrict__ rs, const double *__restrict__ vp, int elo, LzState *st,
+                            double *__restrict__ y) {
+    if (st->stop) return;
+    const double bprev = st->bprev;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = warp; c < nchunks; c += nwarps) {
+        const int64_t i = crow[c], j = cidx[c], rb = row_ptr[i], re = row_ptr[i + 1];
+        const int64_t b = rb + j * LCHUNK, e = min(re, b + LCHUNK);
+        i128 a = 0;
+        for (int64_t k = b + lane; k < e; k += 32) a += canon_q(__dmul_rn(w[k], u[col[k]]), elo);
+        a = warp_sum_i128(a);
+        const int nch = (int)((re - rb + LCHUNK - 1) / LCHUNK);
+        int last = 0;
+        if (lane == 0) {
+            part[c] = to_I128(a);
+            __threadfence();
+            last = atomicAdd(&ccnt[cslot[c]], 1) == nch - 1;
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (!last) continue;
+        __threadfence();
+        if (lane == 0) {
+            i128 t = 0;
+            for (int64_t q = c - j; q < c - j + nch; q++) {
+                I128 pv;
+                pv.lo = __ldcg(&part[q].lo);
+                pv.hi = __ldcg(&part[q].hi);
+                t += from_I128(pv);
+            }
+            lzc_row_epilogue(i, canon_result(t, elo), d, u, rs, vp, bprev, y, &st->maxy);
+            ccnt[cslot[c]] = 0;
+        }
+    }
+}
+// pass C: acc_a += q(fl(y v))
+__global__ void __launch_bounds__(256) k_lzc_alpha(int64_t n, const double *__restrict__ y,
+                                                   const double *__restrict__ v, LzState *st) {
+    if (st->stop) return;
+    const int ey = ebound_dev(__longlong_as_double((long long)st->maxy));
+    const int elo = canon_elo(ey + 2, n);
+    i128 acc = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        acc += canon_q(__dmul_rn(y[i], v[i]), elo);
+    block_add_i128(&st->acc_a, acc);
+}
+// pass D: alpha, y -= alpha v, acc_b += q(y^2)
+__global__ void __launch_bounds__(256) k_lzc_update(int64_t n, double *__restrict__ y, const double *__restrict__ v,
+                                                    LzState *st) {
+    if (st->stop) return;
+    const int ey = ebound_dev(__longlong_as_double((long long)st->maxy));
+    const double a = canon_result(from_I128(st->acc_a), canon_elo(ey + 2, n));
+    const int ea = ebound_dev(fabs(a));
+    const int elo = canon_elo(2 * ((ey + 1 > ea + 2 ? ey + 1 : ea + 2) + 2), n);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->alpha = a;
+        st->elo_b = elo;
+    }
+    i128 acc = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double yi = __dsub_rn(y[i], __dmul_rn(a, v[i]));
+        y[i] = yi;
+        acc += canon_q(__dmul_rn(yi, yi), elo);
+    }
+    block_add_i128(&st->acc_b, acc);
 }
 // largest eigenvalue of the k x k tridiagonal by Sturm bisection (one thread)
 __global__ void k_tridiag_max(const double *alpha, const double *beta, const int *kp, double *out) {
@@ -1086,36 +1205,53 @@ __global__ void k_tridiag_max(const double *alpha, const double *beta, const int
 }
 
 static double lanczos(lap_hierarchy *h, Level &L, int l, cudaStream_t s) {
-    int64_t n = L.n;
-    int steps = h->p.lanczos_steps;
-    const int64_t np1 = spmv_partial_slots(L), np2 = 296;
-    DBuf<double> v(n, s), vp(n, s), y(n, s), u(n, s), rs(n, s), sc(8, s), al(64, s), be(64, s), lam(1, s),
-        p1(np1, s), p2(np2, s);
-    DBuf<int> k(1, s);
-    LAP_CUDA(cudaMemsetAsync(vp.p, 0, sizeof(double) * n, s));
-    LAP_CUDA(cudaMemsetAsync(sc.p, 0, sizeof(double) * 8, s));
-    LAP_CUDA(cudaMemsetAsync(k.p, 0, sizeof(int), s));
-    uint64_t base = mix64(salt_of(h->p.seed, 4) ^ (uint64_t)(2 * l));
-    unsigned g = grid_for(n, 256, 148 * 8);
-    k_lz_init<<<g, 256, 0, s>>>(n, base, L.sid, L.sd, v.p, rs.p); ++g_kl;
-    dot(h, v.p, v.p, n, sc.p + 5, s);
-    k_scale_by<<<g, 256, 0, s>>>(n, v.p, sc.p + 5); ++g_kl;
-    k_hadamard<<<g, 256, 0, s>>>(n, rs.p, v.p, u.p); ++g_kl;
+    const int64_t n = L.n, nnz = L.nnz;
+    const int steps = h->p.lanczos_steps;
+    DBuf<double> v(n, s), vp(n, s), y(n, s), u(n, s), rs(n, s), al(64, s), be(64, s), lam(1, s);
+    DBuf<LzState> st(1, s);
+    DBuf<int> kk(1, s);
+    LzState st0;
+    std::memset(&st0, 0, sizeof(st0));
+    st0.elo_b = canon_elo(1, n);
+    LAP_CUDA(cudaMemcpyAsync(st.p, &st0, sizeof(st0), cudaMemcpyHostToDevice, s));
+    const uint64_t base = mix64(salt_of(h->p.seed, 4) ^ (uint64_t)(2 * l));
+    const unsigned g = grid_for(n, 256, 148 * 8);
+    k_lzc_init<<<g, 256, 0, s>>>(n, base, L.d, y.p, rs.p, vp.p, st.p, st0.elo_b); ++g_kl;
+    LAP_CHECK_LAUNCH();
+    const int e_spmv = (L.maxw > 0.0 ? ilogb(L.maxw) : -1000) + [&] {
+        const double mr = max_abs(rs.p, n, s);
+        return mr > 0.0 ? ilogb(mr) : -1000;
+    }() + 3;
+    const int elo_spmv = canon_elo(e_spmv, nnz);
+    const int G = group_size(n, nnz, L.c_end[0] == L.n);
+    int32_t *lc_row = nullptr, *lc_idx = nullptr, *lc_slot = nullptr, *lc_cnt = nullptr;
+    double *lc_dummy = nullptr;
+    const int64_t nlc = L.c_end[0] == L.n ? 0
+                        : build_chunks(L.row_ptr, 0, n, SETUP_LONG, &lc_row, &lc_idx, &lc_slot, &lc_dummy, &lc_cnt, s);
+    struct FreeLc {
+        void *p[5];
+        cudaStream_t s;
+        ~FreeLc() {
+            for (void *q : p) dfree(q, s);
+        }
+    } free_lc{{lc_row, lc_idx, lc_slot, lc_cnt, lc_dummy}, s};
+    DBuf<I128> lc_part(nlc > 0 ? nlc : 1, s);
     for (int j = 0; j < steps && j < 64; j++) {
-        EpiArgs a;
-        a.x = u.p;
-        a.y = y.p;
-        a.rs = rs.p;
-        a.v = v.p;
-        a.vp = vp.p;
-        a.lz = sc.p;
-        a.partials = p1.p;
-        spmv_level(h, L, EPI_LANCZOS, a, s);
-        k_lz_mid<<<np2, 256, 0, s>>>(n, p1.p, np1, y.p, v.p, sc.p, p2.p); ++g_kl;
-        k_lz_end<<<np2, 256, 0, s>>>(n, p2.p, np2, y.p, v.p, vp.p, u.p, rs.p, sc.p, al.p, be.p, k.p); ++g_kl;
+        k_lzc_next<<<g, 256, 0, s>>>(n, j == 0, 0, y.p, v.p, vp.p, u.p, rs.p, st.p, al.p, be.p); ++g_kl;
+        LAUNCH_G(G, k_lzc_spmv, n, s, n, L.row_ptr, L.col, L.w, L.d, u.p, rs.p, vp.p, elo_spmv, st.p, y.p);
+        if (nlc > 0) {
+            k_lzc_chunk<<<grid_for(nlc * 32, 256, 148 * 16), 256, 0, s>>>(nlc, lc_row, lc_idx, lc_slot, lc_cnt,
+                                                                          lc_part.p, L.row_ptr, L.col, L.w, L.d, u.p,
+                                                                          rs.p, vp.p, elo_spmv, st.p, y.p);
+            ++g_kl;
+        }
+        k_lzc_alpha<<<g, 256, 0, s>>>(n, y.p, v.p, st.p); ++g_kl;
+        k_lzc_update<<<g, 256, 0, s>>>(n, y.p, v.p, st.p); ++g_kl;
         LAP_CHECK_LAUNCH();
     }
-    k_tridiag_max<<<1, 1, 0, s>>>(al.p, be.p, k.p, lam.p); ++g_kl;
+    k_lzc_next<<<g, 256, 0, s>>>(n, 0, 1, y.p, v.p, vp.p, u.p, rs.p, st.p, al.p, be.p); ++g_kl;  // record the last step
+    LAP_CUDA(cudaMemcpyAsync(kk.p, &st.p->k, sizeof(int), cudaMemcpyDeviceToDevice, s));
+    k_tridiag_max<<<1, 1, 0, s>>>(al.p, be.p, kk.p, lam.p); ++g_kl;
     LAP_CHECK_LAUNCH();
     h->cur.edges += (int64_t)steps * L.nnz;
     return d2h_scalar(lam.p, s);
@@ -1447,6 +1583,8 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
         nnz = d2h_scalar(g->row_ptr + n, s);
     } else {
         nnz = g->row_ptr[n];
+        if (g->row_ptr[0] != 0 || nnz < 0 || nnz >= (int64_t)1 << 40)
+            throw Error{LAP_EGRAPH, "row_ptr[0] != 0 or row_ptr[n] outside [0, 2^40)"};
         rp_in.alloc(n + 1, s);
         col_in.alloc(nnz, s);
         h2d(rp_in.p, g->row_ptr, n + 1, s);
@@ -1459,6 +1597,7 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
         col = col_in.p;
         w = g->w ? w_in.p : nullptr;
     }
+    if (nnz < 0) throw Error{LAP_EGRAPH, "row_ptr[n] < 0"};
     if (nnz >= (int64_t)1 << 40 || n >= ((int64_t)1 << 31) - 1) throw Error{LAP_EINVAL, "graph too large"};
     // --- O-S0 validate
     {
@@ -1467,6 +1606,9 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
         if (n > 0) {
             int64_t first = d2h_scalar(rp, s);
             if (first != 0) throw Error{LAP_EGRAPH, "row_ptr[0] != 0"};
+            k_validate_rowptr<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(n, nnz, rp, flag.p); ++g_kl;
+            LAP_CHECK_LAUNCH();
+            if (d2h_scalar(flag.p, s)) throw Error{LAP_EGRAPH, "row_ptr is not monotone within [0, nnz]"};
             LAUNCH_G(group_size(n, nnz), k_validate, n, s, n, rp, col, w, flag.p);
             LAP_CHECK_LAUNCH();
         }
@@ -1563,6 +1705,33 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
     }
     coarse_pinv(h->lev.back(), s);
     tr.mark("coarsest pinv", (int)h->lev.size() - 1);
+}
+
+// ---- test hook (lap_random_stream): the method's counter-based streams, by the
+// same device functions the setup kernels use
+__global__ void k_probe_hash(int64_t n, uint64_t salt2, uint64_t *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = elim_hash(i, salt2);
+}
+__global__ void k_probe_mix(int64_t n, uint64_t *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = mix64((uint64_t)i);
+}
+__global__ void k_probe_lz(int64_t n, uint64_t base, double *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = lz_start_value(base, i);
+}
+void random_stream(int which, uint64_t seed, int level, int attempt, int64_t n, void *out, cudaStream_t s) {
+    const int64_t cnt = which == 1 ? 4 * n : n;
+    DBuf<uint64_t> buf(cnt, s);
+    const unsigned g = grid_for(cnt, 256, 148 * 8);
+    if (which == 0) k_probe_hash<<<g, 256, 0, s>>>(n, salt_of(seed, 2), buf.p);
+    else if (which == 1) k_tv_init<<<g, 256, 0, s>>>(n, mix64(salt_of(seed, 3) ^ (uint64_t)(2 * level + attempt)), (double *)buf.p);
+    else if (which == 2) k_probe_lz<<<g, 256, 0, s>>>(n, mix64(salt_of(seed, 4) ^ (uint64_t)(2 * level)), (double *)buf.p);
+    else k_probe_mix<<<g, 256, 0, s>>>(n, buf.p);
+    LAP_CHECK_LAUNCH();
+    LAP_CUDA(cudaMemcpyAsync(out, buf.p, 8 * (size_t)cnt, cudaMemcpyDeviceToHost, s));
+    LAP_CUDA(cudaStreamSynchronize(s));
 }
 
 }  // namespace lap

@@ -712,9 +712,10 @@ static bool cycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, cu
        // of hubs have up to degree + 1 members: a few lanes would serialise them)
         const int64_t avg = (n + L.m - 1) / std::max<int64_t>(1, L.m);
         // (small levels are latency-bound: 8 lanes keep a member's loads in parallel)
-        static const int Gforce = [] {  // LAP_RESTRICT_G=1|2|4|8 (experiments)
+        static const int Gforce = [] {  // LAP_RESTRICT_G=1|2|4|8 (experiments); anything else: default rule
             const char *e = getenv("LAP_RESTRICT_G");
-            return e ? atoi(e) : 0;
+            const int v = e ? atoi(e) : 0;
+            return (v == 1 || v == 2 || v == 4 || v == 8) ? v : 0;
         }();
         const int G = Gforce ? Gforce
                              : (L.nchunks > 0 || L.m < 65536) ? 8 : avg <= 4 ? 1 : avg <= 8 ? 2 : avg <= 16 ? 4 : 8;

@@ -53,7 +53,7 @@ EXPORTS = [
     "lap_num_levels", "lap_level_info", "lap_level_export", "lap_level_strength", "lap_coarse_pinv",
     "lap_perm", "lap_spmv", "lap_vcycle", "lap_kcycle", "lap_solve_block", "lap_get_stats", "lap_bench_op",
     "lap_nccl_unique_id", "lap_comm_create", "lap_comm_create_virtual", "lap_comm_info", "lap_comm_free",
-    "lap_setup_dist", "lap_dist_index",
+    "lap_setup_dist", "lap_dist_index", "lap_pool_retain", "lap_random_stream",
 ]
 
 
@@ -90,6 +90,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "lap_comm_free": (None, [P]),
         "lap_setup_dist": (ctypes.c_int, [ctypes.POINTER(lap_graph), ctypes.POINTER(lap_params), P, P, ctypes.POINTER(P)]),
         "lap_dist_index": (ctypes.c_int, [i64, i32, i64, P, P, pi64]),
+        "lap_pool_retain": (None, [ctypes.c_uint64]),
+        "lap_random_stream": (ctypes.c_int, [i32, ctypes.c_uint64, i32, i32, i64, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -123,12 +125,54 @@ def _ptr(a):
     return ctypes.c_void_p(a.ctypes.data)
 
 
+_TORCH_DT = {np.float64: "torch.float64", np.int64: "torch.int64", np.int32: "torch.int32"}
+
+
+def _arg(a, n: int, dt, name: str, out: bool = False):
+    """Validate one array argument before its pointer crosses the ABI: the C
+    side reads / writes exactly n elements of dtype dt, contiguously.  numpy
+    inputs are converted (a copy if needed); numpy outputs and torch tensors
+    must already match -- a mismatch raises ValueError instead of letting the
+    library over-read host memory or fault on the device."""
+    if hasattr(a, "data_ptr"):  # torch tensor (CUDA or CPU)
+        if str(a.dtype) != _TORCH_DT[dt]:
+            raise ValueError(f"{name}: dtype {a.dtype}, expected {_TORCH_DT[dt]}")
+        if not a.is_contiguous():
+            raise ValueError(f"{name}: tensor is not contiguous")
+        if a.numel() != n:
+            raise ValueError(f"{name}: {a.numel()} elements, expected {n}")
+        return a
+    if out:
+        if not (isinstance(a, np.ndarray) and a.dtype == dt and a.flags.c_contiguous and a.flags.writeable):
+            raise ValueError(f"{name}: output must be a writeable C-contiguous {np.dtype(dt).name} array")
+        if a.size != n:
+            raise ValueError(f"{name}: {a.size} elements, expected {n}")
+        return a
+    a = np.ascontiguousarray(a, dt)
+    if a.size != n:
+        raise ValueError(f"{name}: {a.size} elements, expected {n}")
+    return a
+
+
 def _stream(stream):
     if stream is None:
         return None
     if hasattr(stream, "cuda_stream"):
         return ctypes.c_void_p(stream.cuda_stream)
     return ctypes.c_void_p(int(stream))
+
+
+def random_stream(which: int, n: int, seed: int = 0, level: int = 0, attempt: int = 0, stream=None) -> np.ndarray:
+    """lap_random_stream (test hook): 0 = h(i) (uint64), 1 = X0 rows (n x 4),
+    2 = Lanczos start vector (unnormalised), 3 = mix64(i) (uint64)."""
+    out = np.zeros(4 * n if which == 1 else n, np.uint64 if which in (0, 3) else np.float64)
+    _check(lib().lap_random_stream(which, seed, level, attempt, n, _ptr(out), _stream(stream)))
+    return out.reshape(n, 4) if which == 1 else out
+
+
+def pool_retain(nbytes: int) -> None:
+    """lap_pool_retain: bytes of pool reservation kept when no hierarchy is alive."""
+    lib().lap_pool_retain(int(nbytes))
 
 
 def lap_params_default(**kw) -> lap_params:
@@ -189,11 +233,16 @@ class Hierarchy:
     def __init__(self, graph, params: lap_params | None = None, stream=None, comm: "Comm | None" = None, **kw):
         self.params = params if params is not None else lap_params_default(**kw)
         dev = hasattr(graph.row_ptr, "data_ptr") and getattr(graph.row_ptr, "is_cuda", False)
-        if not dev:
-            self._keep = (np.ascontiguousarray(graph.row_ptr, np.int64), np.ascontiguousarray(graph.col, np.int32),
-                          None if graph.w is None else np.ascontiguousarray(graph.w, np.float64))
-        else:
-            self._keep = (graph.row_ptr, graph.col, graph.w)
+        n = int(graph.n)
+        if n < 1:
+            raise ValueError("graph.n must be >= 1")
+        rp = _arg(graph.row_ptr, n + 1, np.int64, "row_ptr")
+        nnz = int(rp[-1])  # one device read for a CUDA tensor
+        if dev and not (getattr(graph.col, "is_cuda", False) and (graph.w is None or getattr(graph.w, "is_cuda", False))):
+            raise ValueError("row_ptr, col and w must all be CUDA tensors or all host arrays")
+        col = _arg(graph.col, nnz, np.int32, "col")
+        w = None if graph.w is None else _arg(graph.w, nnz, np.float64, "w")
+        self._keep = (rp, col, w)
         g = lap_graph(int(graph.n), _ptr(self._keep[0]), _ptr(self._keep[1]), _ptr(self._keep[2]), 1 if dev else 0)
         self._h = ctypes.c_void_p()
         self.comm = comm
@@ -204,7 +253,7 @@ class Hierarchy:
                                       ctypes.byref(self._h))
         self.status = _check(rc, allow=(LAP_ESTALL,))
         self._keep = None
-        self.n = int(graph.n)
+        self.n = n
 
     def close(self):
         if getattr(self, "_h", None):
@@ -221,6 +270,8 @@ class Hierarchy:
     def solve(self, b, x=None, tol: float = 0.0, stream=None):
         if x is None:
             x = np.zeros(self.n) if not hasattr(b, "data_ptr") else b.new_zeros(self.n)
+        b = _arg(b, self.n, np.float64, "b")
+        x = _arg(x, self.n, np.float64, "x", out=True)
         it = ctypes.c_int32(0)
         rr = ctypes.c_double(0.0)
         rc = _check(lib().lap_solve(self._h, _ptr(b), _ptr(x), tol, ctypes.byref(it), ctypes.byref(rr),
@@ -233,9 +284,13 @@ class Hierarchy:
         Returns X (k, n), iters[k], rel_residual[k], status."""
         if not hasattr(B, "data_ptr"):
             B = np.ascontiguousarray(B, np.float64)
+        if B.ndim != 2 or B.shape[1] != self.n:
+            raise ValueError(f"B: shape {tuple(B.shape)}, expected (k, {self.n})")
         k = B.shape[0]
         if X is None:
             X = np.zeros((k, self.n)) if not hasattr(B, "data_ptr") else B.new_zeros((k, self.n))
+        B = _arg(B, k * self.n, np.float64, "B")
+        X = _arg(X, k * self.n, np.float64, "X", out=True)
         it = np.zeros(k, np.int32)
         rr = np.zeros(k, np.float64)
         rc = _check(lib().lap_solve_block(self._h, k, _ptr(B), _ptr(X), tol, _ptr(it), _ptr(rr), _stream(stream)),
@@ -287,22 +342,30 @@ class Hierarchy:
         return p
 
     def spmv(self, l: int, x, y=None, stream=None):
+        n = self.level_info(l)[1]
         if y is None:
-            y = np.zeros(len(x)) if not hasattr(x, "data_ptr") else x.new_zeros(len(x))
+            y = np.zeros(n) if not hasattr(x, "data_ptr") else x.new_zeros(n)
+        x = _arg(x, n, np.float64, "x")
+        y = _arg(y, n, np.float64, "y", out=True)
         _check(lib().lap_spmv(self._h, l, _ptr(x), _ptr(y), _stream(stream)))
         return y
 
     def vcycle(self, r, z=None, stream=None):
         if z is None:
-            z = np.zeros(len(r)) if not hasattr(r, "data_ptr") else r.new_zeros(len(r))
+            z = np.zeros(self.n) if not hasattr(r, "data_ptr") else r.new_zeros(self.n)
+        r = _arg(r, self.n, np.float64, "r")
+        z = _arg(z, self.n, np.float64, "z", out=True)
         _check(lib().lap_vcycle(self._h, _ptr(r), _ptr(z), _stream(stream)))
         return z
 
     def kcycle(self, l: int, r, with_fcg: bool = False, z=None, stream=None):
         """z = K(l, r) on level l's internal numbering (N2); with_fcg: the
         level's inner FCG iterations around it (oracle.Hierarchy.kcoarse)."""
+        n = self.level_info(l)[1]
         if z is None:
-            z = np.zeros(len(r)) if not hasattr(r, "data_ptr") else r.new_zeros(len(r))
+            z = np.zeros(n) if not hasattr(r, "data_ptr") else r.new_zeros(n)
+        r = _arg(r, n, np.float64, "r")
+        z = _arg(z, n, np.float64, "z", out=True)
         _check(lib().lap_kcycle(self._h, l, 1 if with_fcg else 0, _ptr(r), _ptr(z), _stream(stream)))
         return z
 
