@@ -29,7 +29,7 @@ def build(force: bool = False) -> str:
     newest = max(os.path.getmtime(_SRC), os.path.getmtime(_HDR))
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < newest:
         tmp = _SO + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-std=gnu11", "-O2", "-ffp-contract=off", "-fno-fast-math",
+        subprocess.check_call(["gcc", "-std=gnu11", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp",
                                "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _SO)
     return _SO
@@ -70,6 +70,8 @@ def lib():
         i64, i32, u64, dbl = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, ctypes.c_double
         sig = {
             "orc_params_default": (None, [P]),
+            "orc_set_threads": (None, [i32]),
+            "orc_get_threads": (i32, []),
             "orc_mix64": (u64, [u64]),
             "orc_salt": (u64, [u64, u64]),
             "orc_mix64_inverse": (u64, [u64]),
@@ -129,6 +131,15 @@ def default_params(**kw) -> Params:
 
 
 # ---------------------------------------------------------------- primitives
+
+def set_threads(t: int) -> None:
+    """OpenMP threads of the oracle; results are bitwise independent of it."""
+    lib().orc_set_threads(int(t))
+
+
+def get_threads() -> int:
+    return int(lib().orc_get_threads())
+
 
 def mix64(z: int) -> int:
     return lib().orc_mix64(z & 0xFFFFFFFFFFFFFFFF)

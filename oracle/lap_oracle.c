@@ -1,9 +1,15 @@
 /*
  * oracle/lap_oracle.c -- CPU ORACLE (TEST INFRASTRUCTURE ONLY; see header).
  *
- * Plain single-threaded C99 + GCC __int128, compiled with -ffp-contract=off
- * so every floating operation below is one IEEE-754 round-to-nearest-even
- * operation in the order written.  Each function cites the PAPER.md (P:)
+ * Plain C99 + GCC __int128, compiled with -ffp-contract=off so every
+ * floating operation below is one IEEE-754 round-to-nearest-even operation in
+ * the order written.  Optional OpenMP ("all host cores ...
+ * bitwise identical to the 1-thread run"): only loops whose iterations are
+ * independent (one row, one entry, one aggregate each) are parallel; integer
+ * counters are atomic; every floating sum keeps one fixed order whatever the
+ * thread count (per-row / per-aggregate loops in ascending index order, dot
+ * products in fixed 4096-element chunks, CanonSums exact).  The result does
+ * not depend on the number of threads (tests/test_oracle_threads.py).  Each function cites the PAPER.md (P:)
  * passage it follows and the SURVEY.md §8(c) reading (O-Rxx / O-Sxx) that
  * resolves what the paper leaves open.
  *
@@ -16,6 +22,25 @@
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* number of OpenMP threads the oracle uses (1 without OpenMP) */
+void orc_set_threads(int32_t t) {
+#ifdef _OPENMP
+    omp_set_num_threads(t > 0 ? t : 1);
+#else
+    (void)t;
+#endif
+}
+int32_t orc_get_threads(void) {
+#ifdef _OPENMP
+    return (int32_t)omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
 
 typedef __int128 i128;
 typedef unsigned __int128 u128;
@@ -168,11 +193,31 @@ double orc_canon_sum(const double *t, int64_t cnt, int32_t e_max, int64_t K) {
 
 static double max_abs(const double *v, int64_t n) {
     double m = 0.0;
+    #pragma omp parallel for reduction(max:m) schedule(static)
     for (int64_t i = 0; i < n; i++) {
         double a = fabs(v[i]);
         if (a > m) m = a;
     }
     return m;
+}
+
+/* CanonSum of fl(a_i * b_i) (b = NULL: of a_i) over a long vector; the int128
+ * sum is exact, so the thread partials may be added in any order. */
+static double canon_dot(const double *a, const double *b, int64_t n, int32_t e_max, int64_t K) {
+    int32_t E_lo = orc_canon_elo(e_max, K);
+    i128 Q = 0;
+    #pragma omp parallel
+    {
+        i128 q = 0;
+        #pragma omp for schedule(static)
+        for (int64_t i = 0; i < n; i++) {
+            double t = b ? a[i] * b[i] : a[i];
+            q += canon_quant(t, E_lo);
+        }
+        #pragma omp critical
+        Q += q;
+    }
+    return canon_to_double(Q, E_lo);
 }
 
 /* ======================================================================== */
@@ -249,6 +294,7 @@ void orc_random_perm(int64_t n, uint64_t seed, int64_t *perm) {
 void orc_row_sums(int64_t n, const int64_t *row_ptr, const double *w, double *d) {
     int64_t nnz = row_ptr[n];
     int32_t e_max = orc_ilogb(max_abs(w, nnz)) + 1;
+    #pragma omp parallel for schedule(dynamic, 1024)
     for (int64_t i = 0; i < n; i++)
         d[i] = orc_canon_sum(w + row_ptr[i], row_ptr[i + 1] - row_ptr[i], e_max, nnz);
 }
@@ -259,6 +305,7 @@ void orc_row_sums(int64_t n, const int64_t *row_ptr, const double *w, double *d)
 
 void orc_spmv(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *w,
               const double *d, const double *x, double *y) {
+    #pragma omp parallel for schedule(dynamic, 1024)
     for (int64_t i = 0; i < n; i++) {
         double s = 0.0;
         for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; k++) s += w[k] * x[col[k]];
@@ -282,6 +329,7 @@ int64_t orc_elim_select(int64_t n, const int64_t *row_ptr, const int32_t *col,
                         int32_t max_degree, uint64_t seed, const uint64_t *hash_override,
                         uint8_t *F) {
     int64_t nF = 0;
+    #pragma omp parallel for reduction(+:nF) schedule(dynamic, 4096)
     for (int64_t i = 0; i < n; i++) {
         F[i] = 0;
         if (row_ptr[i + 1] - row_ptr[i] > max_degree) continue;      /* not a candidate */
@@ -374,33 +422,47 @@ int64_t orc_schur(int64_t n, const int64_t *row_ptr, const int32_t *col, const d
     int32_t e_max = orc_ilogb(max_abs(w, nnz)) + 1;
     int64_t K = 4 * nnz;
     int64_t mx = orc_schur_count(n, row_ptr, col, F);
-    term_t *buf = malloc(sizeof(term_t) * (size_t)(mx + 1));
-    double *tv = malloc(sizeof(double) * (size_t)(mx + 1));
-    int64_t out = 0;
-    int64_t a = 0;
-    if (nrow_ptr) nrow_ptr[0] = 0;
-    for (int64_t i = 0; i < n; i++) {
-        if (F[i]) continue;
-        int64_t cnt = schur_row_terms(row_ptr, col, w, d, F, fmap, i, buf);
-        qsort(buf, (size_t)cnt, sizeof(term_t), cmp_term);
-        int64_t s = 0;
-        while (s < cnt) {
-            int64_t e = s;
-            while (e < cnt && buf[e].c == buf[s].c) { tv[e - s] = buf[e].v; e++; }
-            if (ncol) {
-                ncol[out] = buf[s].c;
-                nw[out] = orc_canon_sum(tv, e - s, e_max, K);
+    int64_t *cid = malloc(sizeof(int64_t) * (size_t)(nc + 1));       /* C row a -> fine vertex */
+    for (int64_t i = 0; i < n; i++) if (!F[i]) cid[fmap[i]] = i;
+    int64_t *rl = calloc((size_t)(nc + 1), sizeof(int64_t));          /* row lengths of the new level */
+    for (int pass = 0; pass < 2; pass++) {
+        if (pass == 1 && !ncol) break;
+        #pragma omp parallel
+        {
+            term_t *buf = malloc(sizeof(term_t) * (size_t)(mx + 1));
+            double *tv = malloc(sizeof(double) * (size_t)(mx + 1));
+            #pragma omp for schedule(dynamic, 256)
+            for (int64_t a = 0; a < nc; a++) {
+                int64_t i = cid[a];
+                int64_t cnt = schur_row_terms(row_ptr, col, w, d, F, fmap, i, buf);
+                qsort(buf, (size_t)cnt, sizeof(term_t), cmp_term);
+                int64_t out = pass ? nrow_ptr[a] : 0, s = 0;
+                while (s < cnt) {
+                    int64_t e = s;
+                    while (e < cnt && buf[e].c == buf[s].c) { tv[e - s] = buf[e].v; e++; }
+                    if (pass) {
+                        ncol[out] = buf[s].c;
+                        nw[out] = orc_canon_sum(tv, e - s, e_max, K);
+                    }
+                    out++;
+                    s = e;
+                }
+                if (!pass) rl[a] = out;
             }
-            out++;
-            s = e;
+            free(buf);
+            free(tv);
         }
-        a++;
-        if (nrow_ptr) nrow_ptr[a] = out;
+        if (pass == 0 && nrow_ptr) {
+            nrow_ptr[0] = 0;
+            for (int64_t a = 0; a < nc; a++) nrow_ptr[a + 1] = nrow_ptr[a] + rl[a];
+        }
     }
-    free(buf);
-    free(tv);
+    int64_t tot = 0;
+    for (int64_t a = 0; a < nc; a++) tot += rl[a];
+    free(cid);
+    free(rl);
     if (ncol && nd) orc_row_sums(nc, nrow_ptr, nw, nd);
-    return out;
+    return tot;
 }
 
 /* ======================================================================== */
@@ -434,26 +496,32 @@ void orc_test_vectors_from(int64_t n, const int64_t *row_ptr, const int32_t *col
         if (row_ptr[i + 1] - row_ptr[i] > maxdeg) maxdeg = row_ptr[i + 1] - row_ptr[i];
     double *t = malloc(sizeof(double) * (size_t)(maxdeg + 1));
     int32_t ew = orc_ilogb(max_abs(w, nnz));
+    free(t);
     for (int sw = 0; sw < sweeps; sw++) {
         double mx = max_abs(X, 4 * n);
         int32_t e_max = (mx > 0.0) ? ew + orc_ilogb(mx) + 2 : ew + 1;
-        for (int64_t i = 0; i < n; i++) {
-            for (int k = 0; k < 4; k++) {
-                int64_t c = 0;
-                for (int64_t q = row_ptr[i]; q < row_ptr[i + 1]; q++) t[c++] = w[q] * X[4 * (int64_t)col[q] + k];
-                double s = orc_canon_sum(t, c, e_max, nnz);
-                double xi = X[4 * i + k];
-                double dx = d[i] * xi;
-                double rr = dx - s;
-                double qq = rr / d[i];
-                double om = omega * qq;
-                Xn[4 * i + k] = xi - om;
+        #pragma omp parallel
+        {
+            double *tt = malloc(sizeof(double) * (size_t)(maxdeg + 1));
+            #pragma omp for schedule(dynamic, 1024)
+            for (int64_t i = 0; i < n; i++) {
+                for (int k = 0; k < 4; k++) {
+                    int64_t c = 0;
+                    for (int64_t q = row_ptr[i]; q < row_ptr[i + 1]; q++) tt[c++] = w[q] * X[4 * (int64_t)col[q] + k];
+                    double s = orc_canon_sum(tt, c, e_max, nnz);
+                    double xi = X[4 * i + k];
+                    double dx = d[i] * xi;
+                    double rr = dx - s;
+                    double qq = rr / d[i];
+                    double om = omega * qq;
+                    Xn[4 * i + k] = xi - om;
+                }
             }
+            free(tt);
         }
         memcpy(X, Xn, sizeof(double) * 4 * (size_t)n);
     }
     free(Xn);
-    free(t);
 }
 
 void orc_test_vectors(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *w,
@@ -479,6 +547,7 @@ static double dot4(const double *a, const double *b) {
 
 void orc_affinity(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *X,
                   int32_t power, double *C) {
+    #pragma omp parallel for schedule(dynamic, 1024)
     for (int64_t i = 0; i < n; i++) {
         double ni = dot4(X + 4 * i, X + 4 * i);
         for (int64_t q = row_ptr[i]; q < row_ptr[i + 1]; q++) {
@@ -500,11 +569,13 @@ void orc_affinity(int64_t n, const int64_t *row_ptr, const int32_t *col, const d
 void orc_normalize_strength(int64_t n, const int64_t *row_ptr, const int32_t *col,
                             const double *C, double *S) {
     double *M = malloc(sizeof(double) * (size_t)n);
+    #pragma omp parallel for schedule(dynamic, 1024)
     for (int64_t i = 0; i < n; i++) {
         double m = 0.0;
         for (int64_t q = row_ptr[i]; q < row_ptr[i + 1]; q++) if (C[q] > m) m = C[q];
         M[i] = m;
     }
+    #pragma omp parallel for schedule(dynamic, 1024)
     for (int64_t i = 0; i < n; i++)
         for (int64_t q = row_ptr[i]; q < row_ptr[i + 1]; q++) {
             double den = M[i] > M[col[q]] ? M[i] : M[col[q]];
@@ -540,6 +611,7 @@ int64_t orc_aggregate(int64_t n, const int64_t *row_ptr, const int32_t *col, con
         double filt = ldexp(1.0, -t);
         memcpy(nst, st, (size_t)n);
         memcpy(nidx, idx, sizeof(int32_t) * (size_t)n);
+        #pragma omp parallel for schedule(dynamic, 1024)
         for (int64_t i = 0; i < n; i++) {
             if (st[i] != ST_UNDECIDED) continue;
             int br = -1; double bs = 0.0; int64_t bj = -1;
@@ -553,7 +625,10 @@ int64_t orc_aggregate(int64_t n, const int64_t *row_ptr, const int32_t *col, con
             }
             if (bj < 0) continue;
             if (br == ST_SEED) { nst[i] = ST_DECIDED; nidx[i] = (int32_t)bj; }
-            else votes[bj] += 1;
+            else {
+                #pragma omp atomic
+                votes[bj] += 1;                                 /* integer: exact in any order */
+            }
         }
         for (int64_t i = 0; i < n; i++)
             if (nst[i] == ST_UNDECIDED && votes[i] >= threshold) nst[i] = ST_SEED;
@@ -583,42 +658,74 @@ static int64_t galerkin_impl(int64_t n, const int64_t *row_ptr, const int32_t *c
                              const int32_t *agg, int64_t m, int64_t *crow_ptr, int32_t *ccol,
                              double *cw, double *cd) {
     int64_t nnz = row_ptr[n];
-    /* bucket fine entries by coarse row a */
+    /* bucket fine entries by coarse row a (the order inside a bucket is
+     * irrelevant: the row is sorted by coarse column and every entry is a
+     * CanonSum, which does not depend on the order of its terms) */
     int64_t *cnt = calloc((size_t)(m + 1), sizeof(int64_t));
+    #pragma omp parallel for schedule(dynamic, 1024)
     for (int64_t i = 0; i < n; i++)
         for (int64_t q = row_ptr[i]; q < row_ptr[i + 1]; q++)
-            if (agg[i] != agg[col[q]]) cnt[agg[i] + 1]++;
+            if (agg[i] != agg[col[q]]) {
+                #pragma omp atomic
+                cnt[agg[i] + 1]++;
+            }
     for (int64_t a = 0; a < m; a++) cnt[a + 1] += cnt[a];
     int64_t tot = cnt[m];
     term_t *buf = malloc(sizeof(term_t) * (size_t)(tot + 1));
     int64_t *fill = malloc(sizeof(int64_t) * (size_t)(m + 1));
     memcpy(fill, cnt, sizeof(int64_t) * (size_t)(m + 1));
+    #pragma omp parallel for schedule(dynamic, 1024)
     for (int64_t i = 0; i < n; i++)
         for (int64_t q = row_ptr[i]; q < row_ptr[i + 1]; q++) {
             int32_t a = agg[i], b = agg[col[q]];
-            if (a != b) { buf[fill[a]].c = b; buf[fill[a]].v = w[q]; fill[a]++; }
+            if (a != b) {
+                int64_t pos;
+                #pragma omp atomic capture
+                pos = fill[a]++;
+                buf[pos].c = b;
+                buf[pos].v = w[q];
+            }
         }
     int32_t e_max = orc_ilogb(max_abs(w, nnz)) + 1;
     int64_t mxrow = 0;
     for (int64_t a = 0; a < m; a++) if (cnt[a + 1] - cnt[a] > mxrow) mxrow = cnt[a + 1] - cnt[a];
-    double *tv = malloc(sizeof(double) * (size_t)(mxrow + 1));
-    int64_t out = 0;
-    if (crow_ptr) crow_ptr[0] = 0;
-    for (int64_t a = 0; a < m; a++) {
+    int64_t *rl = calloc((size_t)(m + 1), sizeof(int64_t));
+    #pragma omp parallel for schedule(dynamic, 256)
+    for (int64_t a = 0; a < m; a++) {                              /* sort each coarse row, count distinct */
         term_t *r = buf + cnt[a];
         int64_t len = cnt[a + 1] - cnt[a];
         qsort(r, (size_t)len, sizeof(term_t), cmp_term);
-        int64_t s = 0;
-        while (s < len) {
-            int64_t e = s;
-            while (e < len && r[e].c == r[s].c) { tv[e - s] = r[e].v; e++; }
-            if (ccol) { ccol[out] = r[s].c; cw[out] = orc_canon_sum(tv, e - s, e_max, nnz); }
-            out++;
-            s = e;
-        }
-        if (crow_ptr) crow_ptr[a + 1] = out;
+        int64_t u = 0;
+        for (int64_t e = 0; e < len; e++) if (e == 0 || r[e].c != r[e - 1].c) u++;
+        rl[a] = u;
     }
-    free(cnt); free(buf); free(fill); free(tv);
+    int64_t out = 0;
+    for (int64_t a = 0; a < m; a++) out += rl[a];
+    if (crow_ptr) {
+        crow_ptr[0] = 0;
+        for (int64_t a = 0; a < m; a++) crow_ptr[a + 1] = crow_ptr[a] + rl[a];
+    }
+    if (ccol) {
+        #pragma omp parallel
+        {
+            double *tv = malloc(sizeof(double) * (size_t)(mxrow + 1));
+            #pragma omp for schedule(dynamic, 256)
+            for (int64_t a = 0; a < m; a++) {
+                term_t *r = buf + cnt[a];
+                int64_t len = cnt[a + 1] - cnt[a], o = crow_ptr[a], s = 0;
+                while (s < len) {
+                    int64_t e = s;
+                    while (e < len && r[e].c == r[s].c) { tv[e - s] = r[e].v; e++; }
+                    ccol[o] = r[s].c;
+                    cw[o] = orc_canon_sum(tv, e - s, e_max, nnz);
+                    o++;
+                    s = e;
+                }
+            }
+            free(tv);
+        }
+    }
+    free(cnt); free(buf); free(fill); free(rl);
     if (ccol && cd) orc_row_sums(m, crow_ptr, cw, cd);
     return out;
 }
@@ -708,38 +815,45 @@ double orc_lanczos(int64_t n, const int64_t *row_ptr, const int32_t *col, const 
     int64_t maxdeg = 0;
     for (int64_t i = 0; i < n; i++)
         if (row_ptr[i + 1] - row_ptr[i] > maxdeg) maxdeg = row_ptr[i + 1] - row_ptr[i];
-    double *tr = malloc(sizeof(double) * (size_t)(maxdeg + 1));
     double alpha[64], beta[64];
     orc_lanczos_start(n, seed, level, v);
+    #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; i++) rs[i] = 1.0 / sqrt(d[i]);
-    for (int64_t i = 0; i < n; i++) t[i] = v[i] * v[i];
-    double nv = sqrt(orc_canon_sum(t, n, 1, n));
+    double nv = sqrt(canon_dot(v, v, n, 1, n));
+    #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; i++) v[i] = v[i] / nv;
     const int32_t e_spmv = ebound(max_abs(w, nnz)) + ebound(max_abs(rs, n)) + 3;
     int32_t k = 0;
     double bprev = 0.0;
     for (int32_t j = 0; j < steps; j++) {
+        #pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < n; i++) u[i] = rs[i] * v[i];
-        for (int64_t i = 0; i < n; i++) {                            /* y = D^-1/2 L D^-1/2 v - beta vp */
-            int64_t c = 0;
-            for (int64_t q = row_ptr[i]; q < row_ptr[i + 1]; q++) tr[c++] = w[q] * u[col[q]];
-            double si = orc_canon_sum(tr, c, e_spmv, nnz);
-            double li = d[i] * u[i] - si;
-            double bv = bprev * vp[i];
-            y[i] = rs[i] * li - bv;
+        #pragma omp parallel
+        {
+            double *tr = malloc(sizeof(double) * (size_t)(maxdeg + 1));
+            #pragma omp for schedule(dynamic, 1024)
+            for (int64_t i = 0; i < n; i++) {                        /* y = D^-1/2 L D^-1/2 v - beta vp */
+                int64_t c = 0;
+                for (int64_t q = row_ptr[i]; q < row_ptr[i + 1]; q++) tr[c++] = w[q] * u[col[q]];
+                double si = orc_canon_sum(tr, c, e_spmv, nnz);
+                double li = d[i] * u[i] - si;
+                double bv = bprev * vp[i];
+                y[i] = rs[i] * li - bv;
+            }
+            free(tr);
         }
         int32_t ey = ebound(max_abs(y, n));
-        for (int64_t i = 0; i < n; i++) t[i] = y[i] * v[i];
-        double a = orc_canon_sum(t, n, ey + 2, n);
+        double a = canon_dot(y, v, n, ey + 2, n);
+        #pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < n; i++) { double av = a * v[i]; y[i] = y[i] - av; }
         int32_t ea = ebound(fabs(a));
         int32_t eb = 2 * ((ey + 1 > ea + 2 ? ey + 1 : ea + 2) + 2);
-        for (int64_t i = 0; i < n; i++) t[i] = y[i] * y[i];
-        double b = sqrt(orc_canon_sum(t, n, eb, n));
+        double b = sqrt(canon_dot(y, y, n, eb, n));
         alpha[k] = a;
         beta[k] = b;
         k++;
         if (b <= 1e-14 * fabs(a)) break;
+        #pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < n; i++) { vp[i] = v[i]; v[i] = y[i] / b; }
         bprev = b;
     }
@@ -747,7 +861,7 @@ double orc_lanczos(int64_t n, const int64_t *row_ptr, const int32_t *col, const 
     if (alpha_out) memcpy(alpha_out, alpha, sizeof(double) * (size_t)k);
     if (beta_out) memcpy(beta_out, beta, sizeof(double) * (size_t)k);
     if (k_out) *k_out = k;
-    free(v); free(vp); free(u); free(y); free(rs); free(t); free(tr);
+    free(v); free(vp); free(u); free(y); free(rs); free(t);
     return lam;
 }
 
@@ -828,14 +942,23 @@ void orc_chebyshev(int64_t n, const int64_t *row_ptr, const int32_t *col, const 
     double sigma = theta / delta, rho_old = 1.0 / sigma;
     double *r = malloc(sizeof(double) * (size_t)n), *dv = malloc(sizeof(double) * (size_t)n);
     if (x_is_zero) { for (int64_t i = 0; i < n; i++) { x[i] = 0.0; r[i] = b[i]; } }
-    else { orc_spmv(n, row_ptr, col, w, d, x, r); for (int64_t i = 0; i < n; i++) r[i] = b[i] - r[i]; }
+    else {
+        orc_spmv(n, row_ptr, col, w, d, x, r);
+        #pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < n; i++) r[i] = b[i] - r[i];
+    }
+    #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; i++) { dv[i] = r[i] / d[i] / theta; x[i] += dv[i]; }
     for (int32_t k = 1; k < degree; k++) {
         orc_spmv(n, row_ptr, col, w, d, x, r);
-        for (int64_t i = 0; i < n; i++) r[i] = b[i] - r[i];
         double rho = 1.0 / (2.0 * sigma - rho_old);
         double c1 = rho * rho_old, c2 = 2.0 * rho / delta;
-        for (int64_t i = 0; i < n; i++) { dv[i] = c1 * dv[i] + c2 * (r[i] / d[i]); x[i] += dv[i]; }
+        #pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < n; i++) {
+            r[i] = b[i] - r[i];
+            dv[i] = c1 * dv[i] + c2 * (r[i] / d[i]);
+            x[i] += dv[i];
+        }
         rho_old = rho;
     }
     free(r); free(dv);
@@ -848,6 +971,7 @@ void orc_chebyshev(int64_t n, const int64_t *row_ptr, const int32_t *col, const 
 static void level_free(orc_level *L) {
     free(L->row_ptr); free(L->col); free(L->w); free(L->d);
     free(L->agg); free(L->S); free(L->fmap); free(L->pinv);
+    free(L->mem_ptr); free(L->members); free(L->ct_ptr); free(L->ct_q); free(L->ct_f);
     memset(L, 0, sizeof(*L));
 }
 
@@ -973,6 +1097,41 @@ int orc_setup(int64_t n, const int64_t *row_ptr, const int32_t *col, const doubl
         l++;
     }
     h->nlev = l + 1;
+    for (int32_t t = 0; t < l; t++) {                  /* transfer lists (ascending fine index) */
+        orc_level *T = &h->lev[t];
+        if (T->kind == ORC_AGG) {
+            T->mem_ptr = calloc((size_t)(T->m + 1), sizeof(int64_t));
+            T->members = malloc(sizeof(int32_t) * (size_t)(T->n + 1));
+            for (int64_t i = 0; i < T->n; i++) T->mem_ptr[T->agg[i] + 1]++;
+            for (int64_t a = 0; a < T->m; a++) T->mem_ptr[a + 1] += T->mem_ptr[a];
+            int64_t *cur = malloc(sizeof(int64_t) * (size_t)(T->m + 1));
+            memcpy(cur, T->mem_ptr, sizeof(int64_t) * (size_t)(T->m + 1));
+            for (int64_t i = 0; i < T->n; i++) T->members[cur[T->agg[i]]++] = (int32_t)i;
+            free(cur);
+        } else if (T->kind == ORC_ELIM) {
+            int64_t nc = h->lev[t + 1].n, tot = 0;
+            T->ct_ptr = calloc((size_t)(nc + 1), sizeof(int64_t));
+            for (int64_t f = 0; f < T->n; f++) {
+                if (T->fmap[f] >= 0) continue;
+                for (int64_t q = T->row_ptr[f]; q < T->row_ptr[f + 1]; q++) { T->ct_ptr[T->fmap[T->col[q]] + 1]++; tot++; }
+            }
+            for (int64_t c = 0; c < nc; c++) T->ct_ptr[c + 1] += T->ct_ptr[c];
+            T->ct_q = malloc(sizeof(int64_t) * (size_t)(tot + 1));
+            T->ct_f = malloc(sizeof(int32_t) * (size_t)(tot + 1));
+            int64_t *cur = malloc(sizeof(int64_t) * (size_t)(nc + 1));
+            memcpy(cur, T->ct_ptr, sizeof(int64_t) * (size_t)(nc + 1));
+            for (int64_t f = 0; f < T->n; f++) {
+                if (T->fmap[f] >= 0) continue;
+                for (int64_t q = T->row_ptr[f]; q < T->row_ptr[f + 1]; q++) {
+                    int64_t c = T->fmap[T->col[q]];
+                    T->ct_q[cur[c]] = q;
+                    T->ct_f[cur[c]] = (int32_t)f;
+                    cur[c]++;
+                }
+            }
+            free(cur);
+        }
+    }
     orc_level *Lc = &h->lev[l];
     Lc->pinv = malloc(sizeof(double) * (size_t)(Lc->n * Lc->n));
     rc = orc_coarse_pinv(Lc->n, Lc->row_ptr, Lc->col, Lc->w, Lc->d, Lc->pinv);
@@ -989,10 +1148,43 @@ const orc_level *orc_get_level(const orc_hier *h, int32_t l) { return &h->lev[l]
 /* the exact additive 2-level transfer of P:463-477 (no smoothing)    */
 /* ======================================================================== */
 
+/* b' = P^T b on an elimination level:
+ *   b'_idx(c) = b_c + sum_{f~c} fl(w_fc / d_f) b_f, the f in ascending order */
+static void elim_restrict(const orc_level *L, int64_t nc, const double *b, double *bc) {
+    #pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < L->n; i++) if (L->fmap[i] >= 0) bc[L->fmap[i]] = b[i];
+    #pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t c = 0; c < nc; c++)
+        for (int64_t t = L->ct_ptr[c]; t < L->ct_ptr[c + 1]; t++) {
+            int64_t f = L->ct_f[t], q = L->ct_q[t];
+            bc[c] += (L->w[q] / L->d[f]) * b[f];
+        }
+}
+/* x = P x' + F-smoother: x_c = x'_idx(c); x_f = (b_f + sum w_fc x'_idx(c)) / d_f */
+static void elim_prolong(const orc_level *L, const double *b, const double *xc, double *x) {
+    #pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t i = 0; i < L->n; i++) {
+        if (L->fmap[i] >= 0) { x[i] = xc[L->fmap[i]]; continue; }
+        double s = b[i];
+        for (int64_t q = L->row_ptr[i]; q < L->row_ptr[i + 1]; q++) s += L->w[q] * xc[L->fmap[L->col[q]]];
+        x[i] = s / L->d[i];
+    }
+}
+/* r_c[a] = sum_{agg_i = a} r_i, the members in ascending order */
+static void agg_restrict(const orc_level *L, const double *r, double *rc) {
+    #pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t a = 0; a < L->m; a++) {
+        double s = 0.0;
+        for (int64_t t = L->mem_ptr[a]; t < L->mem_ptr[a + 1]; t++) s += r[L->members[t]];
+        rc[a] = s;
+    }
+}
+
 void orc_vcycle(const orc_hier *h, int32_t l, const double *b, double *x) {
     const orc_level *L = &h->lev[l];
     int64_t n = L->n;
     if (L->kind == ORC_COARSEST) {                   /* x = L_c^+ (b - mean b) */
+        #pragma omp parallel for schedule(static) if (n > 64)
         for (int64_t i = 0; i < n; i++) {
             double s = 0.0;
             for (int64_t j = 0; j < n; j++) s += L->pinv[i * n + j] * b[j];
@@ -1004,20 +1196,10 @@ void orc_vcycle(const orc_hier *h, int32_t l, const double *b, double *x) {
         int64_t nc = h->lev[l + 1].n;
         double *bc = malloc(sizeof(double) * (size_t)(nc + 1)), *xc = malloc(sizeof(double) * (size_t)(nc + 1));
         /* b' = P^T b:  b'_idx(c) = b_c + sum_{f~c} (w_fc/d_f) b_f */
-        for (int64_t i = 0; i < n; i++) if (L->fmap[i] >= 0) bc[L->fmap[i]] = b[i];
-        for (int64_t f = 0; f < n; f++) {
-            if (L->fmap[f] >= 0) continue;
-            for (int64_t q = L->row_ptr[f]; q < L->row_ptr[f + 1]; q++)
-                bc[L->fmap[L->col[q]]] += (L->w[q] / L->d[f]) * b[f];
-        }
+        elim_restrict(L, nc, b, bc);
         orc_vcycle(h, l + 1, bc, xc);
         /* x = P x' + Fsmooth(b): x_c = x'_idx(c); x_f = (b_f + sum w_fc x'_idx(c)) / d_f */
-        for (int64_t i = 0; i < n; i++) {
-            if (L->fmap[i] >= 0) { x[i] = xc[L->fmap[i]]; continue; }
-            double s = b[i];
-            for (int64_t q = L->row_ptr[i]; q < L->row_ptr[i + 1]; q++) s += L->w[q] * xc[L->fmap[L->col[q]]];
-            x[i] = s / L->d[i];
-        }
+        elim_prolong(L, b, xc, x);
         free(bc); free(xc);
         return;
     }
@@ -1029,20 +1211,40 @@ void orc_vcycle(const orc_hier *h, int32_t l, const double *b, double *x) {
     orc_chebyshev(n, L->row_ptr, L->col, L->w, L->d, L->lambda, p->cheby_lo, p->cheby_hi,
                   p->cheby_degree, b, x, 1);                                 /* pre-smooth from 0 */
     orc_spmv(n, L->row_ptr, L->col, L->w, L->d, x, r);
+    #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; i++) r[i] = b[i] - r[i];                      /* residual */
-    for (int64_t i = 0; i < n; i++) rc[L->agg[i]] += r[i];                   /* R r */
+    agg_restrict(L, r, rc);                                                  /* R r */
     orc_vcycle(h, l + 1, rc, xc);                                            /* coarse */
+    #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; i++) x[i] += xc[L->agg[i]];                   /* x += P x_c */
     orc_chebyshev(n, L->row_ptr, L->col, L->w, L->d, L->lambda, p->cheby_lo, p->cheby_hi,
                   p->cheby_degree, b, x, 0);                                 /* post-smooth */
     free(r); free(rc); free(xc);
 }
 
-static double dotp(const double *a, const double *b, int64_t n) {
+/* Solve-phase dot products and sums in fixed 4096-element chunks: each chunk
+ * summed left to right, then the chunk sums left to right (SURVEY §8(d) M5:
+ * the same rounding for any number of threads; the solve phase's parity is by
+ * tolerance, O-S11).  b = NULL: sum of a. */
+#define ORC_CHUNK 4096
+static double chunked_sum(const double *a, const double *b, int64_t n) {
+    int64_t nc = (n + ORC_CHUNK - 1) / ORC_CHUNK;
+    double stackp[64];
+    double *part = nc <= 64 ? stackp : malloc(sizeof(double) * (size_t)nc);
+    #pragma omp parallel for schedule(static) if (nc > 4)
+    for (int64_t c = 0; c < nc; c++) {
+        int64_t e = (c + 1) * ORC_CHUNK < n ? (c + 1) * ORC_CHUNK : n;
+        double s = 0.0;
+        if (b) for (int64_t i = c * ORC_CHUNK; i < e; i++) s += a[i] * b[i];
+        else for (int64_t i = c * ORC_CHUNK; i < e; i++) s += a[i];
+        part[c] = s;
+    }
     double s = 0.0;
-    for (int64_t i = 0; i < n; i++) s += a[i] * b[i];
+    for (int64_t c = 0; c < nc; c++) s += part[c];
+    if (part != stackp) free(part);
     return s;
 }
+static double dotp(const double *a, const double *b, int64_t n) { return chunked_sum(a, b, n); }
 
 /* ======================================================================== */
 /* N2 K-cycle (Notay & Vassilevski's recursive Krylov cycle):     */
@@ -1059,19 +1261,9 @@ void orc_kcycle(const orc_hier *h, int32_t l, const double *b, double *x) {
     if (L->kind == ORC_ELIM) {
         int64_t nc = h->lev[l + 1].n;
         double *bc = malloc(sizeof(double) * (size_t)(nc + 1)), *xc = malloc(sizeof(double) * (size_t)(nc + 1));
-        for (int64_t i = 0; i < n; i++) if (L->fmap[i] >= 0) bc[L->fmap[i]] = b[i];
-        for (int64_t f = 0; f < n; f++) {
-            if (L->fmap[f] >= 0) continue;
-            for (int64_t q = L->row_ptr[f]; q < L->row_ptr[f + 1]; q++)
-                bc[L->fmap[L->col[q]]] += (L->w[q] / L->d[f]) * b[f];
-        }
+        elim_restrict(L, nc, b, bc);
         orc_kcoarse(h, l + 1, bc, xc);                                       /* coarse problem */
-        for (int64_t i = 0; i < n; i++) {
-            if (L->fmap[i] >= 0) { x[i] = xc[L->fmap[i]]; continue; }
-            double s = b[i];
-            for (int64_t q = L->row_ptr[i]; q < L->row_ptr[i + 1]; q++) s += L->w[q] * xc[L->fmap[L->col[q]]];
-            x[i] = s / L->d[i];
-        }
+        elim_prolong(L, b, xc, x);
         free(bc); free(xc);
         return;
     }
@@ -1082,9 +1274,11 @@ void orc_kcycle(const orc_hier *h, int32_t l, const double *b, double *x) {
     orc_chebyshev(n, L->row_ptr, L->col, L->w, L->d, L->lambda, p->cheby_lo, p->cheby_hi,
                   p->cheby_degree, b, x, 1);                                 /* pre-smooth from 0 */
     orc_spmv(n, L->row_ptr, L->col, L->w, L->d, x, r);
+    #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; i++) r[i] = b[i] - r[i];                      /* residual */
-    for (int64_t i = 0; i < n; i++) rc[L->agg[i]] += r[i];                   /* R r */
+    agg_restrict(L, r, rc);                                                  /* R r */
     orc_kcoarse(h, l + 1, rc, xc);                                           /* coarse problem */
+    #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; i++) x[i] += xc[L->agg[i]];                   /* x += P x_c */
     orc_chebyshev(n, L->row_ptr, L->col, L->w, L->d, L->lambda, p->cheby_lo, p->cheby_hi,
                   p->cheby_degree, b, x, 0);                                 /* post-smooth */
@@ -1127,9 +1321,9 @@ void orc_kcoarse(const orc_hier *h, int32_t l, const double *b, double *x) {
 /* ======================================================================== */
 
 static void project_mean(double *v, int64_t n) {
-    double s = 0.0;
-    for (int64_t i = 0; i < n; i++) s += v[i];
+    double s = chunked_sum(v, NULL, n);
     s /= (double)n;
+    #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < n; i++) v[i] -= s;
 }
 
@@ -1184,6 +1378,7 @@ int orc_solve(const orc_hier *h, const double *b_in, double *x_out, double tol,
     for (k = 1; k <= max_iters; k++) {
         orc_spmv(n, L0->row_ptr, L0->col, L0->w, L0->d, pv, q);
         double alpha = rho / dotp(pv, q, n);
+        #pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < n; i++) { x[i] += alpha * pv[i]; r[i] -= alpha * q[i]; }
         if (sqrt(dotp(r, r, n)) / bn <= tol) {                               /* O-R30 */
             orc_spmv(n, L0->row_ptr, L0->col, L0->w, L0->d, x, q);
@@ -1195,6 +1390,7 @@ int orc_solve(const orc_hier *h, const double *b_in, double *x_out, double tol,
         project_mean(z, n);                                                  /* O-R29 */
         double rho2 = dotp(r, z, n);
         double beta = rho2 / rho;
+        #pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < n; i++) pv[i] = z[i] + beta * pv[i];
         rho = rho2;
     }

@@ -75,6 +75,13 @@ typedef struct {
     int32_t *fmap;           /* n: C -> coarse index >= 0; F -> -1-fslot */
     /* coarsest */
     double  *pinv;           /* n*n row-major L^+                       */
+    /* transfer lists (derived at the end of setup; fix the summation order
+     * of R r and P^T b to ascending fine index, whatever the thread count) */
+    int64_t *mem_ptr;        /* agg: m+1, members of aggregate a ascending */
+    int32_t *members;        /* agg: n                                  */
+    int64_t *ct_ptr;         /* elim: nc+1, F neighbours of C vertex c ascending */
+    int64_t *ct_q;           /* elim: entry index q of (f, c) in row f  */
+    int32_t *ct_f;           /* elim: the F vertex f                    */
 } orc_level;
 
 typedef struct {
@@ -87,6 +94,8 @@ typedef struct {
 } orc_hier;
 
 void     orc_params_default(orc_params *p);
+void     orc_set_threads(int32_t t);   /* OpenMP threads (results do not depend on it) */
+int32_t  orc_get_threads(void);
 
 /* --- canonical arithmetic (O-S11) ---------------------------------------- */
 uint64_t orc_mix64(uint64_t z);
