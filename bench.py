@@ -7,18 +7,26 @@ aggregation hierarchy, Galerkin, lambda-hat, coarsest L^+) followed by
 lap_solve (PCG + V-cycle to 1e-8 relative residual), both through the C ABI
 of liblap.so.
 
-metric  = SpMV edges/s: nonzeros of L traversed by all SpMV-shaped passes of
-          the step (setup semiring SpMVs + every solve-phase L_l application),
-          per second of device time (max over ranks).  BASELINE.json names
-          "V-cycle SpMV edges/s & HBM GB/s vs roofline; time to 1e-8 relative
-          residual": the line also carries the solve-only V-cycle edges/s,
-          time_to_1e8_ms, the setup time and the roofline of the dominant
-          kernel (fused Chebyshev/Jacobi SpMV, H2).
-workload (N=1) = BASELINE.json configs[1]: 3D 7-point grid 128^3, log-uniform
-          weights in [1e-3, 1] (the other configs are parity-test cases).
-
---impl reference runs the CPU oracle (oracle/, the paper's method as plain C)
-on a bounded sample of the same workload on the host cores.
+metric  = BASELINE.json's "V-cycle SpMV edges/s & HBM GB/s vs roofline; time
+          to 1e-8 relative residual".  value = the solve's SpMV edges (SURVEY
+          M2: per V-cycle sum over aggregation levels of 4 nnz_off(L_l), plus
+          the PCG's fine products q = L p and residuals) divided by the WHOLE
+          step's device time (setup + solve, max over ranks).  The setup's own
+          semiring SpMVs are not counted as edges.  The same line carries the
+          solve-only and V-cycle-only edges/s (M2), the V-cycle and dominant-
+          kernel GB/s against the measured HBM roofline AND against the
+          measured random-gather ceiling (M3), time to 1e-8, setup time.
+workload (N=1) = BASELINE.json configs[3] (cfg 4: Barabasi-Albert n=4,194,304,
+          m=8, w~U[0.5,2]), the largest single-GPU config; --config k picks
+          another (cfg 5 = R-MAT s26).
+cpu_baseline = the CPU oracle (oracle/, OpenMP over all host cores, bitwise
+          identical to 1 thread) on the SAME input: one setup + one solve,
+          the same edges/time formula; plus fine-SpMV medians at 1 thread and
+          at all threads, and the host CPU model.
+--impl reference = the oracle on the same input and host cores; its step is
+          one PCG solve on a hierarchy it sets up once (setup timed and
+          reported, not repeated per step: a full oracle setup of cfg 4 takes
+          ~30 s on 16 cores).
 """
 from __future__ import annotations
 
@@ -37,7 +45,8 @@ import numpy as np  # noqa: E402
 
 import lapgen  # noqa: E402
 
-CFG = 2
+CFG = 4
+METRIC = "V-cycle SpMV edges/s & HBM GB/s vs roofline; time to 1e-8 relative residual"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
 GRIDS = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}  # pr x pc process grids
 
@@ -55,6 +64,16 @@ def host_cores():
         return len(os.sched_getaffinity(0))
     except Exception:
         return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                return l.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 # ---------------------------------------------------------------- clocks
@@ -148,30 +167,6 @@ class Clocks:
                 "sampler": "nvml" if getattr(self, "_t", None) is not None else "nvidia-smi"}
 
 
-# ---------------------------------------------------------------- edge model
-def pass_counts(levels, iters, vcycles, params):
-    """SpMV-shaped passes of one setup + solve (same accounting as liblap's
-    lap_stats): nonzeros of L traversed."""
-    K = params.get("cheby_degree", 2)
-    setup = solve = 0
-    prev_elim = False
-    for i, L in enumerate(levels):
-        kind, nnz = L["kind"], L["nnz"]
-        if kind == 2:
-            break
-        if kind == 1:
-            setup += 2 * nnz                       # Alg. 2 select + Schur build
-            prev_elim = True
-            continue
-        if not prev_elim:
-            setup += nnz                           # rejected elimination attempt
-        setup += nnz * (params.get("lanczos_steps", 10) + 3 + 2 + 10 + 1)  # Lanczos, sweeps, C/S, votes, Galerkin
-        solve += vcycles * nnz * (2 * K)           # (K-1) pre + resid + K post
-        prev_elim = False
-    solve += (iters + 2) * levels[0]["nnz"]        # PCG q = L p, true residuals
-    return setup, solve
-
-
 # ---------------------------------------------------------------- GPU arm
 def level_table(h):
     """Per-level sizes for the work accounting (host copies, outside timing)."""
@@ -190,6 +185,15 @@ def level_table(h):
     return out
 
 
+def gather_ceiling(P, n, stream, reps=5):
+    """M3 second ceiling: random 8-byte gathers from an x of n doubles with the
+    SpMV's 12 B/entry streams (lap_bench_gather, 2^26 gathers)."""
+    m = 1 << 26
+    t = float(np.median(P.bench_gather(max(1, n), m, reps, stream=stream)))
+    gps = m / (t * 1e-3)
+    return {"x_bytes": 8 * n, "gathers_per_s": gps, "spmv_equiv_gbs": 12.0 * gps / 1e9}
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -205,6 +209,7 @@ def run_gpu(args):
         dist.init_process_group("nccl", init_method="env://")
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(device=dev)
+    P.pool_retain(1 << 40)  # keep liblap's pool reserved across the steps (no re-mapping per setup)
     # sharded solve (G1) over a pr x pc grid for N > 1 (or --shard at N = 1): the
     # library's own NCCL communicators; torch.distributed only broadcasts the id
     comm = None
@@ -218,6 +223,7 @@ def run_gpu(args):
 
     g = lapgen.config(args.config)
     b = lapgen.rhs(g.n)
+    K = 2  # cheby_degree (the paper's)
     # inputs resident in HBM
     rp_d = torch.from_numpy(g.row_ptr).to(dev)
     col_d = torch.from_numpy(g.col).to(dev)
@@ -236,6 +242,8 @@ def run_gpu(args):
         n = g.n
         row_ptr, col, w = rp_h.numpy(), col_h.numpy(), w_h.numpy()
 
+    levels = None
+
     def step(graph, bb, xx):
         w0 = time.perf_counter()
         h = P.Hierarchy(graph, stream=stream, comm=comm)
@@ -246,12 +254,14 @@ def run_gpu(args):
         st = h.stats()
         out = dict(iters=it, relres=rr, rc=rc, setup_ms=st0["setup_ms"], solve_ms=st["solve_ms"],
                    launches=st0["kernel_launches"] + st["kernel_launches"], vcycles=st["vcycles"],
-                   solve_edges=st["spmv_edges"], wall_setup_ms=1e3 * (w1 - w0), wall_solve_ms=1e3 * (w2 - w1))
+                   wall_setup_ms=1e3 * (w1 - w0), wall_solve_ms=1e3 * (w2 - w1))
         return h, out
 
     with torch.cuda.stream(stream):
-        for _ in range(args.warmup):
+        for i in range(args.warmup):
             h, r = step(gd, b_d, x_d)
+            if levels is None:
+                levels = level_table(h)
             h.close()
         torch.cuda.synchronize()
         if world > 1:
@@ -273,13 +283,34 @@ def run_gpu(args):
         total_ms = t0.elapsed_time(t1)
         if world > 1:
             dist.barrier()
-        # ---- per-operation timing on the same stream, after the timed region (M2, M4)
+        # ---- per-operation timing on the same stream, after the timed region (M2, M3, M4)
         hs = P.Hierarchy(gd, stream=stream)
-        levels = level_table(hs)
+        if levels is None:
+            levels = level_table(hs)
         lv = hs.first_agg_level()
         t_cheb, bytes_cheb, _ = hs.bench_op(1, lv, 50, stream=stream)          # dominant kernel (H2)
         t_spmv, bytes_spmv, e_spmv = hs.bench_op(0, 0, 100, stream=stream)    # fine SpMV (H1)
         t_vc, bytes_vc, e_vc = hs.bench_op(2, 0, 20, stream=stream)           # V-cycle (H16)
+        per_level = []
+        ceil_cache = {}
+        for l, L in enumerate(levels):
+            if L["kind"] == 2 or L["nnz"] == 0:
+                continue
+            ts, bs, es = hs.bench_op(0, l, 30, stream=stream)
+            ent = {"level": l, "kind": L["kind"], "n": L["n"], "nnz": L["nnz"],
+                   "spmv_us": float(np.median(ts)) * 1e3, "spmv_gbs": bs / (float(np.median(ts)) * 1e-3) / 1e9}
+            if L["kind"] == 0:
+                tc, bc, _ = hs.bench_op(1, l, 30, stream=stream)
+                ent["cheb_us"] = float(np.median(tc)) * 1e3
+                ent["cheb_gbs"] = bc / (float(np.median(tc)) * 1e-3) / 1e9
+            if L["n"] >= 100000:  # the gather ceiling is meaningful for levels larger than L1 reach
+                key = L["n"]
+                if key not in ceil_cache:
+                    ceil_cache[key] = gather_ceiling(P, L["n"], stream)
+                c = ceil_cache[key]
+                ent["gather_ceiling_us"] = L["nnz"] / c["gathers_per_s"] * 1e6
+                ent["spmv_frac_of_gather_ceiling"] = ent["gather_ceiling_us"] / ent["spmv_us"]
+            per_level.append(ent)
         solve_ms = []
         for _ in range(5):
             _, it_s, rr_s, _ = hs.solve(b_d, x_d, stream=stream)
@@ -301,20 +332,6 @@ def run_gpu(args):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    last = runs[-1]
-    setup_edges, solve_edges = pass_counts(levels, last["iters"], last["vcycles"], {})
-    edges = setup_edges + solve_edges
-    pk, pk_src = peaks()
-    hbm = float(pk.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
-    ms_k = float(np.mean(t_cheb))
-    achieved = bytes_cheb / (ms_k * 1e-3) / 1e9
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tf):
-        try:
-            traffic = json.load(open(tf)).get(f"cfg{args.config}", {}).get("cheb_bytes_per_launch")
-        except Exception:
-            traffic = None
     clocks = clk.summary()
     if rank != 0:
         if comm is not None:
@@ -322,31 +339,54 @@ def run_gpu(args):
         if world > 1:
             dist.destroy_process_group()
         return
-    # M2 metrics
+    last = runs[-1]
+    step_edges = [MX.solve_spmv_edges(levels, r["iters"], r["vcycles"], K) for r in runs]
+    edges = float(np.mean(step_edges))
+    pk, pk_src = peaks()
+    hbm = float(pk.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
+    ms_k = float(np.mean(t_cheb))
+    achieved = bytes_cheb / (ms_k * 1e-3) / 1e9
+    Ld = levels[lv]
+    gc = gather_ceiling(P, Ld["n"], stream)
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(f"cfg{args.config}", {}).get("cheb_bytes_per_launch")
+        except Exception:
+            traffic = None
     nnz0 = levels[0]["nnz"]
     sp_med = float(np.median(t_spmv))
     vc_med = float(np.median(t_vc))
-    vc_edges = sum(4 * L["nnz"] for L in levels if L["kind"] == 0)
+    vc_edges = MX.vcycle_spmv_edges(levels, K)
     t_solve = float(np.median(solve_ms))
     work = MX.solve_work(levels, last["iters"], last["vcycles"])
     dr = last["relres"]
+    setup_med = float(np.median([r["setup_ms"] for r in runs]))
+    solve_med = float(np.median([r["solve_ms"] for r in runs]))
     m2 = {
         "fine_spmv": {"edges_per_s": nnz0 / (sp_med * 1e-3), "gbs": bytes_spmv / (sp_med * 1e-3) / 1e9,
                       "us_median_of_100": sp_med * 1e3,
                       "frac_measured": bytes_spmv / (sp_med * 1e-3) / 1e9 / hbm,
                       "frac_8000": bytes_spmv / (sp_med * 1e-3) / 1e9 / 8000.0},
-        "vcycle": {"edges_per_s": vc_edges / (vc_med * 1e-3), "gbs": bytes_vc / (vc_med * 1e-3) / 1e9,
-                   "us_median_of_20": vc_med * 1e3, "frac_measured": bytes_vc / (vc_med * 1e-3) / 1e9 / hbm},
+        "vcycle": {"edges_per_s": vc_edges / (vc_med * 1e-3), "edges_per_vcycle": vc_edges,
+                   "gbs_method_bytes": bytes_vc / (vc_med * 1e-3) / 1e9, "bytes_per_vcycle": bytes_vc,
+                   "us_median_of_20": vc_med * 1e3, "frac_measured": bytes_vc / (vc_med * 1e-3) / 1e9 / hbm,
+                   "bytes_note": "method bytes of every level's kernels (SURVEY M3); the dense-tail GEMV is booked "
+                                 "with the bytes of the sub-cycle it replaces, not its own 8 n_t^2"},
+        "solve_only_edges_per_s": edges / (solve_med * 1e-3),
         "time_to_1e8_ms_median_of_5": t_solve, "iters": last["iters"], "true_rel_residual": dr,
-        "setup_ms_median": float(np.median([r["setup_ms"] for r in runs])),
+        "setup_ms_median": setup_med,
         "work_units": work, "wda": MX.wda(work, dr) if 0 < dr < 1 else None,
         "tda_ms": MX.tda(t_solve, dr) if 0 < dr < 1 else None,
         "operator_complexity": sum(L["n"] + L["nnz"] for L in levels) / (levels[0]["n"] + nnz0),
+        "per_level": per_level,
     }
-    cpu = cpu_baseline(args) if (world == 1 and not args.no_cpu) else None
+    cpu = cpu_baseline(args, g, b) if (world == 1 and not args.no_cpu) else None
     h2d = g.row_ptr.nbytes + g.col.nbytes + g.w.nbytes + b.nbytes
+    e2e_med = statistics.median(e2e_ms)
     line = {
-        "metric": "SpMV edges/s over one setup + PCG/V-cycle solve to 1e-8 rel. residual",
+        "metric": METRIC,
         "value": world * edges / (ms * 1e-3),
         "unit": "edges/s",
         "n_gpus": world,
@@ -362,21 +402,32 @@ def run_gpu(args):
                    "parallelism": ("single GPU" if comm is None else
                                    f"2D edge partition {grid[0]}x{grid[1]} of the fine levels (NCCL), coarse levels replicated"),
                    "l2": "inputs > L2: the level-0 CSR + SELL copy exceed the 126 MB L2; every SpMV re-streams them",
-                   "levels": [[L["kind"], L["n"], L["nnz"]] for L in levels]},
+                   "levels": [[L["kind"], L["n"], L["nnz"]] for L in levels],
+                   "value_definition": "solve-phase SpMV edges (M2: V-cycles x sum_agg 4 nnz_l + (iters+2) nnz_0) "
+                                       "per second of the whole step (setup + solve)"},
         "iters": last["iters"], "rel_residual": dr,
         "time_to_1e8_ms": t_solve,
-        "setup_ms": m2["setup_ms_median"],
+        "setup_ms": setup_med,
+        "solve_ms": solve_med,
         "vcycle_edges_per_s": m2["vcycle"]["edges_per_s"],
-        "setup_edges": setup_edges, "solve_edges": solve_edges,
+        "vcycle_gbs": m2["vcycle"]["gbs_method_bytes"],
         "m2": m2,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic,
                      "kernel": f"fused Chebyshev/Jacobi SpMV step (H2, k_spmv<E_CHEB>) on level {lv}",
                      "bytes_per_launch": bytes_cheb, "ms_per_launch": ms_k,
-                     "timing": "CUDA events on the solve stream, 50 back-to-back launches, same process, after the timed region",
-                     "frac_of_8000": achieved / 8000.0, "peak_source": pk_src},
-        "e2e": {"value": edges / (statistics.median(e2e_ms) * 1e-3), "unit": "edges/s",
-                "ms": statistics.median(e2e_ms), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": b.nbytes},
+                     "timing": "CUDA events on the solve stream, 50 launches in one graph, same process, after the timed region",
+                     "frac_of_8000": achieved / 8000.0, "peak_source": pk_src,
+                     "second_ceiling": {
+                         "bound": "L1TEX/L2 request rate of random 8-byte x gathers (SURVEY M3)",
+                         "gathers_per_s": gc["gathers_per_s"], "spmv_equiv_gbs": gc["spmv_equiv_gbs"],
+                         "spmv_equiv_frac_of_hbm": gc["spmv_equiv_gbs"] / hbm,
+                         "kernel_us_at_ceiling": Ld["nnz"] / gc["gathers_per_s"] * 1e6,
+                         "kernel_frac_of_ceiling": (Ld["nnz"] / gc["gathers_per_s"]) / (ms_k * 1e-3),
+                         "how": "lap_bench_gather: 2^26 uniform random gathers from an x of the level's size, "
+                                "with int32 col + fp64 w streamed"}},
+        "e2e": {"value": edges / (e2e_med * 1e-3), "unit": "edges/s",
+                "ms": e2e_med, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": b.nbytes},
         "gpu_launches": int(sum(r["launches"] for r in runs)),
         "step_breakdown_ms": {k: float(np.median([r[k] for r in runs])) for k in
                               ["setup_ms", "solve_ms", "wall_setup_ms", "wall_solve_ms", "wall_free_ms"]},
@@ -391,57 +442,93 @@ def run_gpu(args):
 
 
 # ---------------------------------------------------------------- CPU oracle arm
-def oracle_sample(budget_s: float):
-    """Same workload family at a bounded size: 3D 7-point grid side s with the
-    cfg-2 weight distribution (the full 128^3 oracle run takes ~2 min)."""
-    side = 48 if budget_s < 15 else 64
-    return side, lapgen.grid3d(side, True, 1, f"grid3d_{side}")
+def oracle_levels(h):
+    out = []
+    for L in h.levels():
+        d = {"kind": L.kind, "n": L.n, "nnz": L.nnz}
+        out.append(d)
+    return out
 
 
-def run_oracle_once(g):
+def oracle_spmv_median(g, threads, reps=10):
     import oracle
-    b = lapgen.rhs(g.n)
+    oracle.set_threads(threads)
+    d = oracle.row_sums(g.n, g.row_ptr, g.w)
+    x = np.random.default_rng(0).standard_normal(g.n)
+    rp = np.ascontiguousarray(g.row_ptr, np.int64)
+    col = np.ascontiguousarray(g.col, np.int32)
+    w = np.ascontiguousarray(g.w, np.float64)
+    ts = []
+    for _ in range(reps):
+        t = time.perf_counter()
+        oracle.spmv(g.n, rp, col, w, d, x)
+        ts.append(time.perf_counter() - t)
+    return float(np.median(ts))
+
+
+def cpu_baseline(args, g, b):
+    """The oracle as it stands, all host cores (OpenMP, bitwise = 1 thread),
+    on the same input: one setup + one solve, the GPU line's formula."""
+    import oracle
+    from paper_1705_06266_b200 import metrics as MX
+    cores = host_cores()
+    oracle.set_threads(cores)
     t0 = time.perf_counter()
     h = oracle.Hierarchy(g)
+    t1 = time.perf_counter()
     x, it, rr, rc = h.solve(b)
-    dt = time.perf_counter() - t0
-    levels = [dict(kind=L.kind, n=L.n, nnz=L.nnz) for L in h.levels()]
-    nv = it + 1
-    setup_e, solve_e = pass_counts(levels, it, nv, {})
-    return dt, setup_e + solve_e, it, rr
-
-
-def cpu_baseline(args):
-    side, g = oracle_sample(20.0)
-    dt, edges, it, rr = run_oracle_once(g)
-    return {"value": edges / dt, "unit": "edges/s", "cores": 1, "kind": "oracle",
-            "sample": f"one full oracle setup + solve to 1e-8 on a {side}^3 3D grid (cfg-2 weights), "
-                      f"{dt:.1f} s, {it} iters; oracle is single-threaded"}
+    t2 = time.perf_counter()
+    levels = oracle_levels(h)
+    edges = MX.solve_spmv_edges(levels, it, it)
+    sp1 = oracle_spmv_median(g, 1)
+    spn = oracle_spmv_median(g, cores)
+    oracle.set_threads(cores)
+    return {"value": edges / (t2 - t0), "unit": "edges/s", "cores": cores, "kind": "oracle",
+            "sample": f"the full {lapgen.CONFIG_NAMES[args.config]} input: one oracle setup ({t1 - t0:.1f} s) + one "
+                      f"PCG solve to 1e-8 ({t2 - t1:.1f} s, {it} iters) on {cores} OpenMP threads; same edges/time "
+                      f"formula as the GPU value",
+            "setup_s": t1 - t0, "solve_s": t2 - t1, "iters": it, "rel_residual": rr,
+            "solve_only_edges_per_s": edges / (t2 - t1),
+            "fine_spmv_median_of_10": {"threads_1_s": sp1, f"threads_{cores}_s": spn,
+                                       "edges_per_s_1": g.nnz / sp1, f"edges_per_s_{cores}": g.nnz / spn},
+            "cpu": cpu_model()}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    budget = 150.0 / max(1, args.steps + args.warmup)
-    side, g = oracle_sample(budget)
+    import oracle
+    from paper_1705_06266_b200 import metrics as MX
+    cores = host_cores()
+    oracle.set_threads(cores)
+    g = lapgen.config(args.config)
+    b = lapgen.rhs(g.n)
+    t0 = time.perf_counter()
+    h = oracle.Hierarchy(g)
+    setup_s = time.perf_counter() - t0
+    levels = oracle_levels(h)
     for _ in range(args.warmup):
-        run_oracle_once(g)
-    tot_t, tot_e = 0.0, 0
+        h.solve(b)
+    tot_t, tot_e, it = 0.0, 0, 0
     for _ in range(args.steps):
-        dt, e, it, rr = run_oracle_once(g)
-        tot_t += dt
-        tot_e += e
+        t = time.perf_counter()
+        x, it, rr, rc = h.solve(b)
+        tot_t += time.perf_counter() - t
+        tot_e += MX.solve_spmv_edges(levels, it, it)
     v = tot_e / tot_t
+    sample = (f"{lapgen.CONFIG_NAMES[args.config]}, full size; step = one oracle PCG solve to 1e-8 ({it} iters) "
+              f"on a hierarchy set up once ({setup_s:.1f} s, not per step) with {cores} OpenMP threads")
     emit({
         "impl": "reference",
-        "metric": "SpMV edges/s over one setup + PCG/V-cycle solve to 1e-8 rel. residual",
+        "metric": METRIC,
         "value": v, "unit": "edges/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (lapgen, seeded)",
-        "config": {"workload": lapgen.CONFIG_NAMES[args.config], "sample": f"{side}^3 3D grid, cfg-2 weights"},
-        "cpu_baseline": {"value": v, "unit": "edges/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{side}^3 3D 7-pt grid, log-uniform w; full setup + solve per step"},
+        "config": {"workload": lapgen.CONFIG_NAMES[args.config], "n": g.n, "nnz_off": g.nnz, "sample": sample},
+        "setup_s": setup_s,
+        "cpu_baseline": {"value": v, "unit": "edges/s", "cores": cores, "kind": "oracle", "sample": sample,
+                         "cpu": cpu_model()},
         "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     })
 

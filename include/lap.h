@@ -244,6 +244,13 @@ lap_status lap_get_stats(const lap_hierarchy *h, lap_stats *s);
 lap_status lap_bench_op(lap_hierarchy *h, int32_t which, int32_t l, int32_t reps, void *cuda_stream,
                         double *ms, double *bytes, int64_t *edges);
 
+/* The M3 "second ceiling": CUDA-event time (ms[reps], host) of
+ * one kernel doing m random 8-byte gathers x[col[k]] from an x of nx doubles
+ * (uniform counter-hash columns, no locality) with the SpMV's col (int32) and
+ * w (fp64) streams -- the SpMV of a random-ordered power-law level without its
+ * epilogue.  Allocates its own buffers; 1 <= nx < 2^31. */
+lap_status lap_bench_gather(int64_t nx, int64_t m, int32_t reps, void *cuda_stream, double *ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -25,7 +25,8 @@ UNITS = {"setup.cu": ["-fmad=false", "-prec-div=true", "-prec-sqrt=true"],
          "dist.cu": [],
          "tail.cu": [],
          "ktail.cu": [],
-         "block.cu": []}
+         "block.cu": [],
+         "bench_hooks.cu": []}
 
 
 def _sources():

@@ -54,6 +54,7 @@ EXPORTS = [
     "lap_perm", "lap_spmv", "lap_vcycle", "lap_kcycle", "lap_solve_block", "lap_get_stats", "lap_bench_op",
     "lap_nccl_unique_id", "lap_comm_create", "lap_comm_create_virtual", "lap_comm_info", "lap_comm_free",
     "lap_setup_dist", "lap_dist_index", "lap_pool_retain", "lap_random_stream",
+    "lap_bench_gather",
 ]
 
 
@@ -92,6 +93,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "lap_dist_index": (ctypes.c_int, [i64, i32, i64, P, P, pi64]),
         "lap_pool_retain": (None, [ctypes.c_uint64]),
         "lap_random_stream": (ctypes.c_int, [i32, ctypes.c_uint64, i32, i32, i64, P, P]),
+        "lap_bench_gather": (ctypes.c_int, [i64, i64, i32, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -168,6 +170,13 @@ def random_stream(which: int, n: int, seed: int = 0, level: int = 0, attempt: in
     out = np.zeros(4 * n if which == 1 else n, np.uint64 if which in (0, 3) else np.float64)
     _check(lib().lap_random_stream(which, seed, level, attempt, n, _ptr(out), _stream(stream)))
     return out.reshape(n, 4) if which == 1 else out
+
+
+def bench_gather(nx: int, m: int = 1 << 26, reps: int = 5, stream=None) -> np.ndarray:
+    """lap_bench_gather: ms per launch of m random gathers from an nx-double x."""
+    ms = np.zeros(reps)
+    _check(lib().lap_bench_gather(int(nx), int(m), int(reps), _stream(stream), _ptr(ms)))
+    return ms
 
 
 def pool_retain(nbytes: int) -> None:

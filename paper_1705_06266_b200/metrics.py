@@ -62,3 +62,16 @@ def tda(time_s: float, dr: float) -> float:
     if not (dr > 0.0) or dr >= 1.0:
         raise ValueError("no residual reduction: TDA undefined")
     return -time_s / math.log10(dr)
+
+
+def vcycle_spmv_edges(levels, cheby_degree: int = 2) -> int:
+    """SpMV edges of one V-cycle = sum over aggregation levels of
+    2K nnz_off(L_l) ((K-1) pre + 1 residual + K post smoother SpMVs; 4 nnz
+    for the paper's degree K = 2)."""
+    return sum(2 * cheby_degree * L["nnz"] for L in levels if L["kind"] == AGG)
+
+
+def solve_spmv_edges(levels, iters: int, vcycles: int, cheby_degree: int = 2) -> int:
+    """SpMV edges of one PCG solve (O-S8): `vcycles` V-cycles, `iters` fine
+    products q = L p, the true-residual confirmation and the final residual."""
+    return vcycles * vcycle_spmv_edges(levels, cheby_degree) + (iters + 2) * levels[0]["nnz"]
