@@ -97,6 +97,14 @@ typedef struct {
                                  single-GPU only                               */
     int32_t kcycle_inner;     /* 2: FCG iterations per aggregation level below
                                  the finest (paper: "a number of")      */
+    int32_t elim_rounds;      /* 1: at most this many elimination levels in a
+                                 row before an aggregation level ("we can run
+                                 low-degree elimination multiple times in a
+                                 row"; one is the paper's choice)   */
+    int32_t keep_logical;     /* -1: release a level's logical CSR once its solve
+                                 storage exists when nnz >= 2^28 (cfg 5 memory);
+                                 1: always keep (lap_level_export needs it);
+                                 0: always release                             */
 } lap_params;
 
 typedef struct lap_hierarchy lap_hierarchy;
@@ -139,9 +147,18 @@ lap_status lap_level_info(const lap_hierarchy *h, int32_t l, int32_t *kind, int6
                           int64_t *nnz_off, double *lambda_hat);
 /* Copies level l to host arrays (any may be NULL): row_ptr[n+1], col[nnz],
  * w[nnz], d[n], map[n] = agg[] (kind 0) or fmap[] (kind 1: coarse index for
- * C vertices, -1-slot for F vertices). */
+ * C vertices, -1-slot for F vertices).  LAP_EINVAL if row_ptr/col/w are asked
+ * for and the level's logical CSR was released (params.keep_logical); use
+ * lap_level_rows then. */
 lap_status lap_level_export(const lap_hierarchy *h, int32_t l, int64_t *row_ptr, int32_t *col,
                             double *w, double *d, int32_t *map);
+/* Rows rows[0..k) of level l's logical CSR (ascending columns, the logical
+ * numbering the oracle sees), rebuilt from the solve storage, so it works also
+ * when the logical copy was released.  Two calls: with col == NULL only
+ * row_ptr[k+1] (host, exclusive offsets) is filled; then col/w (host,
+ * row_ptr[k] entries).  Parity hook for graphs too big to export whole. */
+lap_status lap_level_rows(const lap_hierarchy *h, int32_t l, int64_t k, const int64_t *rows, int64_t *row_ptr,
+                          int32_t *col, double *w);
 /* Strength S[nnz] of aggregation level l (requires params.keep_strength). */
 lap_status lap_level_strength(const lap_hierarchy *h, int32_t l, double *S);
 /* Coarsest pseudo-inverse, n*n row-major (host buffer). */

@@ -72,6 +72,11 @@ def _L():
         _lib.gen_rmat.restype = None
         _lib.gen_rmat.argtypes = [ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
                                   ctypes.c_double, ctypes.c_uint64, P, P]
+        _lib.gen_rmat_lcc_build.restype = ctypes.c_void_p
+        _lib.gen_rmat_lcc_build.argtypes = [ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                            ctypes.c_double, ctypes.c_uint64, P, P]
+        _lib.gen_rmat_lcc_fetch.restype = None
+        _lib.gen_rmat_lcc_fetch.argtypes = [ctypes.c_void_p, P, P]
         _lib.gen_csr_from_edges.restype = None
         _lib.gen_csr_from_edges.argtypes = [ctypes.c_int64, ctypes.c_int64, P, P, P, P, P, P]
     return _lib
@@ -178,9 +183,10 @@ def rmat(scale: int = 20, edge_factor: int = 16, abcd=(0.57, 0.19, 0.19, 0.05),
     return largest_component(g)
 
 
-def rmat_large(scale: int = 26, edge_factor: int = 16, abcd=(0.57, 0.19, 0.19, 0.05),
-               seed: int = 0, name: str = "") -> Graph:
-    """R-MAT with the counter-based C generator (configs[4]; scale 26)."""
+def rmat_large_reference(scale: int, edge_factor: int = 16, abcd=(0.57, 0.19, 0.19, 0.05),
+                         seed: int = 0, name: str = "") -> Graph:
+    """R-MAT from the counter-based C edge stream, post-processed in numpy /
+    scipy (small scales: the check of rmat_large's C pipeline)."""
     a, b, c, _ = abcd
     ne = edge_factor << scale
     u = np.zeros(ne, dtype=np.int64)
@@ -189,6 +195,24 @@ def rmat_large(scale: int = 26, edge_factor: int = 16, abcd=(0.57, 0.19, 0.19, 0
     u, v = dedup_undirected(u, v)
     g = csr_from_edges(1 << scale, u, v, None, name or f"rmat_s{scale}")
     return largest_component(g)
+
+
+def rmat_large(scale: int = 26, edge_factor: int = 16, abcd=(0.57, 0.19, 0.19, 0.05),
+               seed: int = 0, name: str = "", unit_weights_array: bool = False) -> Graph:
+    """R-MAT with the counter-based C generator (configs[4]; scale 26): edge
+    stream, dedup, LCC and symmetric CSR all in C/OpenMP (gen_rmat_lcc_build),
+    identical to rmat_large_reference.  Unit weights: w is None (the lap_graph
+    contract's NULL = unit) unless unit_weights_array."""
+    a, b, c, _ = abcd
+    ne = edge_factor << scale
+    n = ctypes.c_int64()
+    nnz = ctypes.c_int64()
+    h = _L().gen_rmat_lcc_build(scale, ne, a, b, c, seed, ctypes.byref(n), ctypes.byref(nnz))
+    row_ptr = np.empty(n.value + 1, np.int64)
+    col = np.empty(nnz.value, np.int32)
+    _L().gen_rmat_lcc_fetch(h, _ptr(row_ptr), _ptr(col))
+    w = np.ones(nnz.value) if unit_weights_array else None
+    return Graph(n.value, row_ptr, col, w, name or f"rmat_s{scale}")
 
 
 def barabasi_albert(n: int = 4194304, m: int = 8, seed: int = 0, wseed: int = 2,

@@ -13,6 +13,9 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 static inline uint64_t gen_sm64(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -150,4 +153,158 @@ void gen_csr_from_edges(int64_t n, int64_t ne, const int64_t *u, const int64_t *
             gen_sort_row(col + row_ptr[i], val + row_ptr[i], len);
         }
     }
+}
+
+/*
+ * R-MAT at scales numpy cannot handle (BASELINE.json configs[4], scale 26,
+ * 2^30 generated edges): the whole pipeline of lapgen.rmat_large in C/OpenMP,
+ * producing the same CSR as gen_rmat + dedup_undirected + csr_from_edges +
+ * largest_component (checked at small scales in tests/test_lapgen.py):
+ *   1. edges from gen_rmat's counter stream, self loops dropped, key =
+ *      (min << 32) | max;
+ *   2. parallel LSD radix sort of the keys, duplicates dropped;
+ *   3. union-find over the unique edges, the largest component kept (ties:
+ *      the smallest root label as numpy's argmax over bincount picks the
+ *      first maximum of the component labels ordered by smallest vertex),
+ *      vertices relabelled by ascending original id;
+ *   4. symmetric CSR, columns ascending, unit weights (w not materialised).
+ * Two calls: gen_rmat_lcc_build() returns a handle with n and nnz; then
+ * gen_rmat_lcc_fetch() copies row_ptr/col out and frees the handle.
+ */
+typedef struct { int64_t n, nnz; int64_t *row_ptr; int32_t *col; } gen_csr_t;
+
+static void gen_radix_sort_u64(uint64_t *a, uint64_t *tmp, int64_t n, int bits) {
+    const int R = 11, B = 1 << R;
+    int nth = 1;
+#ifdef _OPENMP
+    nth = omp_get_max_threads();
+#endif
+    int64_t *hist = (int64_t *)malloc(sizeof(int64_t) * (size_t)B * (size_t)nth);
+    uint64_t *src = a, *dst = tmp;
+    for (int sh = 0; sh < bits; sh += R) {
+        memset(hist, 0, sizeof(int64_t) * (size_t)B * (size_t)nth);
+#pragma omp parallel num_threads(nth)
+        {
+            int t = 0;
+#ifdef _OPENMP
+            t = omp_get_thread_num();
+#endif
+            int64_t lo = n * t / nth, hi = n * (t + 1) / nth;
+            int64_t *h = hist + (size_t)t * B;
+            for (int64_t i = lo; i < hi; i++) h[(src[i] >> sh) & (B - 1)]++;
+#pragma omp barrier
+#pragma omp single
+            {
+                int64_t run = 0;
+                for (int d = 0; d < B; d++)
+                    for (int q = 0; q < nth; q++) {
+                        int64_t c = hist[(size_t)q * B + d];
+                        hist[(size_t)q * B + d] = run;
+                        run += c;
+                    }
+            }
+            for (int64_t i = lo; i < hi; i++) dst[h[(src[i] >> sh) & (B - 1)]++] = src[i];
+        }
+        uint64_t *x = src; src = dst; dst = x;
+    }
+    if (src != a) memcpy(a, src, sizeof(uint64_t) * (size_t)n);
+    free(hist);
+}
+
+static int64_t gen_uf_find(int64_t *p, int64_t x) {
+    while (p[x] != x) { p[x] = p[p[x]]; x = p[x]; }
+    return x;
+}
+
+void *gen_rmat_lcc_build(int32_t scale, int64_t nedges, double a, double b, double c, uint64_t seed,
+                         int64_t *n_out, int64_t *nnz_out) {
+    const int64_t N = (int64_t)1 << scale;
+    uint64_t *key = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)nedges);
+    uint64_t stream = gen_sm64(seed ^ 0x524D4154524D4154ULL); /* same stream as gen_rmat */
+    double ab = a + b, abc = a + b + c;
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < nedges; e++) {
+        int64_t u = 0, v = 0;
+        for (int32_t l = 0; l < scale; l++) {
+            uint64_t r = gen_sm64(stream + (uint64_t)(e * scale + l) * 0x9E3779B97F4A7C15ULL);
+            double x = (double)(r >> 11) * 0x1.0p-53;
+            int ub = 0, vb = 0;
+            if (x < a) { }
+            else if (x < ab) { vb = 1; }
+            else if (x < abc) { ub = 1; }
+            else { ub = 1; vb = 1; }
+            u = (u << 1) | ub;
+            v = (v << 1) | vb;
+        }
+        uint64_t lo = (uint64_t)(u < v ? u : v), hi = (uint64_t)(u < v ? v : u);
+        key[e] = (u == v) ? UINT64_MAX : ((lo << 32) | hi);   /* self loops sort last, dropped below */
+    }
+    uint64_t *tmp = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)nedges);
+    gen_radix_sort_u64(key, tmp, nedges, 64);
+    free(tmp);
+    /* unique, self loops (UINT64_MAX) dropped */
+    int64_t m = 0;
+    for (int64_t e = 0; e < nedges; e++) {
+        if (key[e] == UINT64_MAX) break;
+        if (m == 0 || key[e] != key[m - 1]) key[m++] = key[e];
+    }
+    /* components */
+    int64_t *par = (int64_t *)malloc(sizeof(int64_t) * (size_t)N);
+    for (int64_t i = 0; i < N; i++) par[i] = i;
+    for (int64_t e = 0; e < m; e++) {
+        int64_t x = gen_uf_find(par, (int64_t)(key[e] >> 32)), y = gen_uf_find(par, (int64_t)(key[e] & 0xFFFFFFFFULL));
+        if (x != y) { if (x < y) par[y] = x; else par[x] = y; }   /* root = smallest vertex of the component */
+    }
+    int64_t *size = (int64_t *)calloc((size_t)N, sizeof(int64_t));
+    for (int64_t i = 0; i < N; i++) size[gen_uf_find(par, i)]++;
+    int64_t best = 0;
+    for (int64_t i = 1; i < N; i++) if (size[i] > size[best]) best = i;   /* first maximum: smallest root */
+    free(size);
+    int32_t *nid = (int32_t *)malloc(sizeof(int32_t) * (size_t)N);
+    int64_t n = 0;
+    for (int64_t i = 0; i < N; i++) nid[i] = (par[i] == i ? i : gen_uf_find(par, i)) == best ? (int32_t)n++ : -1;
+    free(par);
+    gen_csr_t *g = (gen_csr_t *)malloc(sizeof(gen_csr_t));
+    g->n = n;
+    g->row_ptr = (int64_t *)calloc((size_t)(n + 1), sizeof(int64_t));
+    for (int64_t e = 0; e < m; e++) {
+        int32_t u = nid[key[e] >> 32], v = nid[key[e] & 0xFFFFFFFFULL];
+        if (u < 0) continue;
+        g->row_ptr[u + 1]++;
+        g->row_ptr[v + 1]++;
+    }
+    for (int64_t i = 0; i < n; i++) g->row_ptr[i + 1] += g->row_ptr[i];
+    g->nnz = g->row_ptr[n];
+    g->col = (int32_t *)malloc(sizeof(int32_t) * (size_t)(g->nnz + 1));
+    /* keys are sorted by (min, max): a row's smaller neighbours (key max = row)
+     * arrive in ascending min, its larger ones (key min = row) in ascending max,
+     * and every smaller one precedes every larger one in key order */
+    int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
+    memcpy(fill, g->row_ptr, sizeof(int64_t) * (size_t)(n + 1));
+    for (int64_t e = 0; e < m; e++) {
+        int32_t u = nid[key[e] >> 32], v = nid[key[e] & 0xFFFFFFFFULL];
+        if (u < 0) continue;
+        g->col[fill[v]++] = u;   /* u < v: a smaller neighbour of v */
+    }
+    /* larger neighbours after the smaller ones: second pass in key order */
+    for (int64_t e = 0; e < m; e++) {
+        int32_t u = nid[key[e] >> 32], v = nid[key[e] & 0xFFFFFFFFULL];
+        if (u < 0) continue;
+        g->col[fill[u]++] = v;
+    }
+    free(fill);
+    free(nid);
+    free(key);
+    *n_out = g->n;
+    *nnz_out = g->nnz;
+    return g;
+}
+
+void gen_rmat_lcc_fetch(void *h, int64_t *row_ptr, int32_t *col) {
+    gen_csr_t *g = (gen_csr_t *)h;
+    memcpy(row_ptr, g->row_ptr, sizeof(int64_t) * (size_t)(g->n + 1));
+    memcpy(col, g->col, sizeof(int32_t) * (size_t)g->nnz);
+    free(g->row_ptr);
+    free(g->col);
+    free(g);
 }

@@ -44,6 +44,7 @@ class Params(ctypes.Structure):
         ("vote_rounds", ctypes.c_int32), ("vote_threshold", ctypes.c_int32), ("coarse_nnz", ctypes.c_int64),
         ("max_levels", ctypes.c_int32), ("seed", ctypes.c_uint64), ("random_order", ctypes.c_int32),
         ("affinity_power", ctypes.c_int32), ("cycle", ctypes.c_int32), ("kcycle_inner", ctypes.c_int32),
+        ("elim_rounds", ctypes.c_int32),
     ]
 
 

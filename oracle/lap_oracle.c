@@ -68,6 +68,7 @@ void orc_params_default(orc_params *p) {
     p->affinity_power = 1;    /* O-R5 */
     p->cycle = 0;             /* V-cycle by default */
     p->kcycle_inner = 2;      /* S:525 / S:562 (paper: "a number of") */
+    p->elim_rounds = 1;       /* "one iteration is sufficient" */
 }
 
 /* ======================================================================== */
@@ -1027,7 +1028,7 @@ int orc_setup(int64_t n, const int64_t *row_ptr, const int32_t *col, const doubl
     }
     orc_row_sums(n, L0->row_ptr, L0->w, L0->d);
 
-    int prev_elim = 0;
+    int elim_run = 0;   /* elimination levels in a row just above (O-R21; P:485-486 elim_rounds) */
     int l = 0;
     for (;;) {
         orc_level *L = &h->lev[l];
@@ -1036,7 +1037,7 @@ int orc_setup(int64_t n, const int64_t *row_ptr, const int32_t *col, const doubl
             L->kind = ORC_COARSEST;
             break;
         }
-        if (p.elim_enable && !prev_elim) {                                     /* O-R21 */
+        if (p.elim_enable && elim_run < p.elim_rounds) {                      /* O-R21 */
             uint8_t *F = malloc((size_t)nl);
             int64_t nF = orc_elim_select(nl, L->row_ptr, L->col, p.elim_max_degree, p.seed, NULL, F);
             if (20 * nF > nl) {                                                /* O-R20 */
@@ -1054,7 +1055,7 @@ int orc_setup(int64_t n, const int64_t *row_ptr, const int32_t *col, const doubl
                 N->d = malloc(sizeof(double) * (size_t)(nc + 1));
                 orc_schur(nl, L->row_ptr, L->col, L->w, L->d, F, L->fmap, N->row_ptr, N->col, N->w, N->d);
                 free(F);
-                prev_elim = 1;
+                elim_run++;
                 l++;
                 continue;
             }
@@ -1093,7 +1094,7 @@ int orc_setup(int64_t n, const int64_t *row_ptr, const int32_t *col, const doubl
         N->w = malloc(sizeof(double) * (size_t)(cn + 1));
         N->d = malloc(sizeof(double) * (size_t)(m + 1));
         orc_galerkin(nl, L->row_ptr, L->col, L->w, L->agg, m, N->row_ptr, N->col, N->w, N->d);
-        prev_elim = 0;
+        elim_run = 0;
         l++;
     }
     h->nlev = l + 1;

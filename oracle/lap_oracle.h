@@ -56,6 +56,7 @@ typedef struct {
     int32_t cycle;           /* 0 V-cycle + PCG (default);
                                 1 K-cycle + FCG (N2)         */
     int32_t kcycle_inner;    /* 2 inner FCG iterations   */
+    int32_t elim_rounds;     /* 1: elimination levels in a row */
 } orc_params;
 
 typedef struct {

@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "lap_internal.cuh"
 
@@ -352,6 +353,8 @@ void lap_params_default(lap_params *p) {
     p->kcycle_inner = 2;
     p->use_graphs = 1;
     p->replicate_nnz = 0;
+    p->elim_rounds = 1;
+    p->keep_logical = -1;
 }
 
 const char *lap_last_error(void) { return lap::g_err.c_str(); }
@@ -385,7 +388,8 @@ lap_status lap_setup(const lap_graph *g, const lap_params *pp, void *stream, lap
     else lap_params_default(&p);
     if (p.n_test_vectors != 4 || p.cheby_degree < 1 || p.tv_sweeps < 0 || p.vote_rounds < 0 ||
         p.lanczos_steps < 1 || p.lanczos_steps > 64 || !(p.cheby_hi > p.cheby_lo) || !(p.cheby_lo > 0) ||
-        p.max_levels < 1 || p.cycle < 0 || p.cycle > 1 || p.kcycle_inner < 1 || p.kcycle_inner > 8) {
+        p.max_levels < 1 || p.cycle < 0 || p.cycle > 1 || p.kcycle_inner < 1 || p.kcycle_inner > 8 ||
+        p.elim_rounds < 1 || p.elim_rounds > 64 || p.keep_logical < -1 || p.keep_logical > 1) {
         lap::set_error("lap_setup: unsupported parameter values");
         return LAP_EINVAL;
     }
@@ -605,6 +609,11 @@ lap_status lap_level_export(const lap_hierarchy *h, int32_t l, int64_t *row_ptr,
     if (!h || l < 0 || l >= (int32_t)h->lev.size()) return LAP_EINVAL;
     LAP_API_BEGIN
     const lap::Level &L = h->lev[l];
+    if (L.logical_released && (row_ptr || col || w)) {
+        lap::set_error("lap_level_export: the logical CSR of this level was released (params.keep_logical); "
+                       "use lap_level_rows");
+        return LAP_EINVAL;
+    }
     if (row_ptr) LAP_CUDA(cudaMemcpy(row_ptr, L.row_ptr, 8 * (L.n + 1), cudaMemcpyDeviceToHost));
     if (col && L.nnz) LAP_CUDA(cudaMemcpy(col, L.col, 4 * L.nnz, cudaMemcpyDeviceToHost));
     if (w && L.nnz) LAP_CUDA(cudaMemcpy(w, L.w, 8 * L.nnz, cudaMemcpyDeviceToHost));
@@ -612,6 +621,46 @@ lap_status lap_level_export(const lap_hierarchy *h, int32_t l, int64_t *row_ptr,
     if (map) {
         if (L.kind == lap::KIND_AGG) LAP_CUDA(cudaMemcpy(map, L.agg, 4 * L.n, cudaMemcpyDeviceToHost));
         else if (L.kind == lap::KIND_ELIM) LAP_CUDA(cudaMemcpy(map, L.fmap, 4 * L.n, cudaMemcpyDeviceToHost));
+    }
+    return LAP_OK;
+    LAP_API_END
+}
+
+lap_status lap_level_rows(const lap_hierarchy *h, int32_t l, int64_t k, const int64_t *rows, int64_t *row_ptr,
+                          int32_t *col, double *w) {
+    if (!h || l < 0 || l >= (int32_t)h->lev.size() || k < 0 || (k > 0 && !rows) || !row_ptr) return LAP_EINVAL;
+    LAP_API_BEGIN
+    const lap::Level &L = h->lev[l];
+    std::vector<int32_t> spos(L.n), sid(L.n);
+    std::vector<int64_t> srp(L.n + 1);
+    LAP_CUDA(cudaMemcpy(spos.data(), L.spos, 4 * L.n, cudaMemcpyDeviceToHost));
+    LAP_CUDA(cudaMemcpy(srp.data(), L.srp, 8 * (L.n + 1), cudaMemcpyDeviceToHost));
+    row_ptr[0] = 0;
+    for (int64_t t = 0; t < k; t++) {
+        if (rows[t] < 0 || rows[t] >= L.n) throw lap::Error{LAP_EINVAL, "lap_level_rows: row out of range"};
+        const int64_t p = spos[rows[t]];
+        row_ptr[t + 1] = row_ptr[t] + (srp[p + 1] - srp[p]);
+    }
+    if (!col) return LAP_OK;
+    LAP_CUDA(cudaMemcpy(sid.data(), L.sid, 4 * L.n, cudaMemcpyDeviceToHost));
+    std::vector<std::pair<int32_t, double>> row;
+    for (int64_t t = 0; t < k; t++) {
+        const int64_t p = spos[rows[t]], a = srp[p], len = srp[p + 1] - a;
+        std::vector<int32_t> c(len);
+        std::vector<double> v(len);
+        if (len) {
+            LAP_CUDA(cudaMemcpy(c.data(), L.scol + a, 4 * len, cudaMemcpyDeviceToHost));
+            LAP_CUDA(cudaMemcpy(v.data(), L.sw + a, 8 * len, cudaMemcpyDeviceToHost));
+        }
+        row.resize(len);
+        for (int64_t q = 0; q < len; q++) row[q] = {sid[c[q]], v[q]};  // storage column -> logical id
+        std::sort(row.begin(), row.end(), [](const std::pair<int32_t, double> &x, const std::pair<int32_t, double> &y) {
+            return x.first < y.first;
+        });
+        for (int64_t q = 0; q < len; q++) {
+            col[row_ptr[t] + q] = row[q].first;
+            if (w) w[row_ptr[t] + q] = row[q].second;
+        }
     }
     return LAP_OK;
     LAP_API_END

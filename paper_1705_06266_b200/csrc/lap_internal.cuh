@@ -110,6 +110,8 @@ struct Level {
     double *w = nullptr;
     double *d = nullptr;
     double maxw = 0.0;
+    int64_t maxdeg = 0;             // longest row (setup kernels' hub handling; known before storage)
+    bool logical_released = false;  // logical row_ptr/col/w freed after storage (params.keep_logical)
     int32_t *rowof = nullptr;       // setup only: row of every stored entry (not owned)
     // aggregation (logical)
     double lambda = 0.0;

@@ -178,9 +178,69 @@ static bool is_symmetric_t(int64_t n, int64_t nnz, const int64_t *rp, const int3
     LAP_CHECK_LAUNCH();
     return d2h_scalar(flag.p, s) == 0;
 }
+// Symmetry without extra memory (large graphs: the sort above needs ~32 B per
+// entry, 67 GB at cfg 5): every stored (i, j) looks i up in row j by binary
+// search (rows are validated ascending) and compares the weight bit patterns.
+// Entry-parallel; a block finds the rows of its 256 entries with two searches.
+__global__ void __launch_bounds__(256) k_sym_search(int64_t n, int64_t nnz, const int64_t *__restrict__ rp,
+                                                    const int32_t *__restrict__ col, const double *__restrict__ w,
+                                                    int *flag) {
+    __shared__ int64_t rlo, rhi;
+    for (int64_t b0 = (int64_t)blockIdx.x * 256; b0 < nnz; b0 += (int64_t)gridDim.x * 256) {
+        const int64_t t = b0 + threadIdx.x;
+        if (threadIdx.x < 2) {
+            const int64_t tt = threadIdx.x == 0 ? b0 : min(nnz, b0 + 256) - 1;
+            rlo = 0;
+            int64_t lo = 0, hi = n - 1;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi + 1) >> 1;
+                if (rp[mid] <= tt) lo = mid;
+                else hi = mid - 1;
+            }
+            if (threadIdx.x == 0) rlo = lo;
+            else rhi = lo;
+        }
+        __syncthreads();
+        if (t < nnz) {
+            int64_t lo = rlo, hi = rhi;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi + 1) >> 1;
+                if (rp[mid] <= t) lo = mid;
+                else hi = mid - 1;
+            }
+            const int64_t i = lo, j = col[t];
+            int64_t a = rp[j], e = rp[j + 1];
+            while (a < e) {
+                const int64_t mid = (a + e) >> 1;
+                if (col[mid] < i) a = mid + 1;
+                else e = mid;
+            }
+            bool ok = a < rp[j + 1] && col[a] == i;
+            if (ok && w) ok = __double_as_longlong(w[a]) == __double_as_longlong(w[t]);
+            if (!ok) atomicOr(flag, 1);
+        }
+        __syncthreads();
+    }
+}
+static bool symcheck_by_search(int64_t nnz) {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("LAP_SYMCHECK");  // "search" / "sort" (tests); default by size
+        v = !e ? -1 : (e[0] == 's' && e[1] == 'e') ? 1 : 0;
+        if (!e) return nnz >= ((int64_t)1 << 28);
+    }
+    return v == 1;
+}
 static bool is_symmetric(int64_t n, int64_t nnz, const int64_t *rp, const int32_t *col, const double *w,
                          cudaStream_t s) {
     if (nnz == 0) return true;
+    if (symcheck_by_search(nnz)) {
+        DBuf<int> flag(1, s);
+        LAP_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+        k_sym_search<<<grid_for(nnz, 256, 148 * 16), 256, 0, s>>>(n, nnz, rp, col, w, flag.p); ++g_kl;
+        LAP_CHECK_LAUNCH();
+        return d2h_scalar(flag.p, s) == 0;
+    }
     return nnz < ((int64_t)1 << 31) ? is_symmetric_t<int32_t>(n, nnz, rp, col, w, s)
                                     : is_symmetric_t<int64_t>(n, nnz, rp, col, w, s);
 }
@@ -469,6 +529,333 @@ static void csr_from_terms(int64_t nrows, int cb, int64_t T, DBuf<uint64_t> &key
 }
 
 // =========================================================================
+// Batched term builder (memory-lean: no global sort of all terms)
+// =========================================================================
+// A coarse (or relabelled) CSR whose entries are CanonSums of terms generated
+// from a fine CSR, built in batches of OUTPUT rows: the terms of rows
+// [o0, o1) are emitted, radix-sorted by (row - o0, col), run-length encoded
+// and canonically summed, and appended; the next batch reuses the buffers.
+// Every output entry is one CanonSum of exactly the method's multiset of terms
+// (O-R23), so batching changes nothing in the result -- only the peak memory
+// (terms of one batch instead of all nnz terms: the cfg 5 Galerkin and Schur
+// products have ~2e9 terms) and the number of key bits each sort touches.
+//
+// Sources, as a "virtual CSR" over the fine rows (virtual row v -> fine row
+// vfine[v] and output row vout[v]; output row o owns virtual rows
+// [ostart[o], ostart[o+1]); vptr = prefix of the fine degrees in virtual order):
+//   SRC_RELABEL  (O-S1): v = new id r, vfine = old row, terms
+//                (r, perm[col], w) -- no duplicates, no sums;
+//   SRC_SCHUR    (O-S2, O-R25): v = C index a, vfine = cid[a];
+//                entry (i,j): j in C -> (a, fmap j, w_ij); j in F -> for every
+//                b != i in N(j): (a, fmap b, fl(fl(w_ij w_jb) / d_j));
+//   SRC_GALERKIN (O-S5): v = member slot (members grouped by
+//                aggregate, ascending), vfine = the member, vout = its
+//                aggregate a; entry (i,j) with agg_j != a -> (a, agg_j, w_ij).
+enum { SRC_RELABEL = 0, SRC_SCHUR = 1, SRC_GALERKIN = 2 };
+struct TermSrc {
+    int kind = 0;
+    const int64_t *rp = nullptr;
+    const int32_t *col = nullptr;
+    const double *w = nullptr;     // NULL: unit weights (RELABEL only)
+    const double *d = nullptr;     // SCHUR: d_f
+    const int32_t *vfine = nullptr;
+    const int32_t *vout = nullptr;  // NULL: vout[v] = v
+    const int64_t *ostart = nullptr;  // NULL: ostart[o] = o
+    const int64_t *vptr = nullptr;
+    const int64_t *perm = nullptr;  // RELABEL
+    const uint8_t *F = nullptr;     // SCHUR
+    const int32_t *fmap = nullptr;  // SCHUR
+    const int32_t *agg = nullptr;   // GALERKIN
+};
+__device__ __forceinline__ int64_t src_ostart(const TermSrc &S, int64_t o) { return S.ostart ? S.ostart[o] : o; }
+__device__ __forceinline__ int64_t src_vout(const TermSrc &S, int64_t v) { return S.vout ? (int64_t)S.vout[v] : v; }
+
+// per virtual row: fine degree (for vptr) and number of terms (upper bound)
+template <int G>
+__global__ void k_src_counts(int64_t nv, TermSrc S, int64_t *__restrict__ vdeg, int64_t *__restrict__ vterms) {
+    GROUP_LOOP_BEGIN(G, nv)
+        int64_t c = 0, dg = 0;
+        if (live) {
+            const int64_t fi = S.vfine[i], a = S.rp[fi], e = S.rp[fi + 1];
+            dg = e - a;
+            if (S.kind == SRC_SCHUR) {
+                for (int64_t k = a + gl; k < e; k += G) {
+                    const int64_t j = S.col[k];
+                    c += S.F[j] ? (S.rp[j + 1] - S.rp[j] - 1) : 1;
+                }
+            } else if (gl == 0) {
+                c = dg;
+            }
+        }
+        c = grp_sum<G>(c);
+        if (live && gl == 0) {
+            vdeg[i] = dg;
+            vterms[i] = c;
+        }
+    GROUP_LOOP_END
+}
+// batch end: the largest o1 <= nout with vcp[ostart[o1]] - vcp[ostart[o0]] <= budget (at least o0 + 1)
+__global__ void k_batch_end(int64_t o0, int64_t nout, int64_t budget, TermSrc S, const int64_t *__restrict__ vcp,
+                            int64_t *out) {
+    const int64_t base = vcp[src_ostart(S, o0)];
+    int64_t lo = o0 + 1, hi = nout;
+    if (vcp[src_ostart(S, lo)] - base > budget) {
+        *out = lo;
+        return;
+    }
+    while (lo < hi) {  // invariant: lo fits
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (vcp[src_ostart(S, mid)] - base <= budget) lo = mid;
+        else hi = mid - 1;
+    }
+    *out = lo;
+}
+// emit the terms of the fine entries [t0, t1) (= the virtual rows [v0, v1)); a
+// block claims its output space with one atomic (block scan of per-entry counts)
+__global__ void __launch_bounds__(256) k_src_emit(TermSrc S, int64_t v0, int64_t v1, int64_t t0, int64_t t1,
+                                                  int64_t o0, int cb, unsigned long long *cursor,
+                                                  uint64_t *__restrict__ keys, double *__restrict__ vals) {
+    typedef cub::BlockScan<int, 256> BS;
+    __shared__ typename BS::TempStorage ts;
+    __shared__ unsigned long long boff;
+    __shared__ int64_t vlo_s, vhi_s;
+    for (int64_t b0 = t0 + (int64_t)blockIdx.x * 256; b0 < t1; b0 += (int64_t)gridDim.x * 256) {
+        const int64_t t = b0 + threadIdx.x;
+        const int64_t blast = min(t1, b0 + 256) - 1;
+        // virtual rows of the block's first and last entries (two searches per block)
+        if (threadIdx.x < 2) {
+            const int64_t tt = threadIdx.x == 0 ? b0 : blast;
+            int64_t lo = v0, hi = v1 - 1;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi + 1) >> 1;
+                if (S.vptr[mid] <= tt) lo = mid;
+                else hi = mid - 1;
+            }
+            if (threadIdx.x == 0) vlo_s = lo;
+            else vhi_s = lo;
+        }
+        __syncthreads();
+        int cnt = 0;
+        int64_t v = 0, i = 0, k = 0, j = 0;
+        if (t < t1) {
+            int64_t lo = vlo_s, hi = vhi_s;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi + 1) >> 1;
+                if (S.vptr[mid] <= t) lo = mid;
+                else hi = mid - 1;
+            }
+            v = lo;
+            i = S.vfine[v];
+            k = S.rp[i] + (t - S.vptr[v]);
+            j = S.col[k];
+            if (S.kind == SRC_RELABEL) cnt = 1;
+            else if (S.kind == SRC_SCHUR) cnt = S.F[j] ? (int)(S.rp[j + 1] - S.rp[j] - 1) : 1;
+            else cnt = (S.agg[j] != S.vout[v]) ? 1 : 0;
+        }
+        int rk, tot;
+        BS(ts).ExclusiveSum(cnt, rk, tot);
+        if (threadIdx.x == 0) boff = tot ? atomicAdd(cursor, (unsigned long long)tot) : 0ULL;
+        __syncthreads();
+        if (cnt > 0) {
+            int64_t p = (int64_t)boff + rk;
+            const uint64_t row = (uint64_t)(src_vout(S, v) - o0) << cb;
+            if (S.kind == SRC_RELABEL) {
+                keys[p] = row | (uint64_t)S.perm[j];
+                vals[p] = S.w ? S.w[k] : 1.0;
+            } else if (S.kind == SRC_GALERKIN) {
+                keys[p] = row | (uint64_t)S.agg[j];
+                vals[p] = S.w[k];
+            } else if (!S.F[j]) {
+                keys[p] = row | (uint64_t)S.fmap[j];
+                vals[p] = S.w[k];
+            } else {  // fill through f = j (O-R25): w_ij = w_ji bitwise, the product commutes
+                const double wf = S.w[k], df = S.d[j];
+                for (int64_t q = S.rp[j]; q < S.rp[j + 1]; q++) {
+                    const int64_t bb = S.col[q];
+                    if (bb == i) continue;
+                    keys[p] = row | (uint64_t)S.fmap[bb];
+                    vals[p] = __ddiv_rn(__dmul_rn(wf, S.w[q]), df);
+                    p++;
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+// row_ptr[o0 + r] = base + first u with (uk[u] >> cb) >= r, r in [0, nr)
+__global__ void k_batch_row_ptr(int64_t nr, int64_t U, const uint64_t *__restrict__ uk, int cb, int64_t base,
+                                int64_t *__restrict__ row_ptr) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nr; r += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t key = ((uint64_t)r) << cb;
+        int64_t lo = 0, hi = U;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (uk[mid] < key) lo = mid + 1;
+            else hi = mid;
+        }
+        row_ptr[r] = base + lo;
+    }
+}
+__global__ void k_set_i64(int64_t *p, int64_t v) { *p = v; }
+
+static int64_t batch_budget_override() {
+    static int64_t v = -1;
+    if (v < 0) {
+        const char *e = getenv("LAP_TERM_BATCH");  // tests: force small batches
+        v = e ? std::max<int64_t>(1, atoll(e)) : 0;
+    }
+    return v;
+}
+
+// Build `out` (nout rows, column bits cb) from the source; CanonSum instance (e_max, K).
+static void csr_from_source(const TermSrc &S0, int64_t nv, int64_t nout, int cb, int e_max, int64_t K, bool combine,
+                            Level &out, cudaStream_t s) {
+    TermSrc S = S0;
+    DBuf<int64_t> vdeg(nv + 1, s), vterm(nv + 1, s), vptr(nv + 1, s), vcp(nv + 1, s);
+    LAP_CUDA(cudaMemsetAsync(vdeg.p + nv, 0, sizeof(int64_t), s));
+    LAP_CUDA(cudaMemsetAsync(vterm.p + nv, 0, sizeof(int64_t), s));
+    if (nv > 0) {
+        LAUNCH_G(S.kind == SRC_SCHUR ? 32 : 1, k_src_counts, nv, s, nv, S, vdeg.p, vterm.p);
+        LAP_CHECK_LAUNCH();
+    }
+    exclusive_scan_i64(vdeg.p, vptr.p, nv + 1, s);
+    exclusive_scan_i64(vterm.p, vcp.p, nv + 1, s);
+    vdeg.release();
+    vterm.release();
+    S.vptr = vptr.p;
+    const int64_t Ttot = d2h_scalar(vcp.p + nv, s);
+    tmark("  terms: counts");
+    // batch budget: ~56 B per term in flight (keys, values, their sort copies, RLE)
+    int64_t budget = batch_budget_override();
+    if (!budget) {
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        budget = std::max<int64_t>((int64_t)1 << 24, std::min<int64_t>((int64_t)1 << 28, (int64_t)(fr / 4 / 64)));
+    }
+    if (Ttot <= budget) {  // one batch: the plain path
+        DBuf<uint64_t> keys(Ttot, s);
+        DBuf<double> vals(Ttot, s);
+        DBuf<unsigned long long> cur(1, s);
+        LAP_CUDA(cudaMemsetAsync(cur.p, 0, 8, s));
+        const int64_t t1 = d2h_scalar(vptr.p + nv, s);
+        if (t1 > 0) {
+            k_src_emit<<<grid_for(t1, 256, 148 * 16), 256, 0, s>>>(S, 0, nv, 0, t1, 0, cb, cur.p, keys.p, vals.p);
+            ++g_kl;
+            LAP_CHECK_LAUNCH();
+        }
+        const int64_t T = (int64_t)d2h_scalar(cur.p, s);
+        tmark("  terms: emit");
+        csr_from_terms(nout, cb, T, keys, vals, e_max, K, combine, out, s);
+        return;
+    }
+    // several batches of output rows
+    out.n = nout;
+    out.row_ptr = (int64_t *)dalloc(sizeof(int64_t) * (size_t)(nout + 1), s);
+    int32_t *ocol = (int32_t *)dalloc(sizeof(int32_t) * (size_t)(Ttot + 1), s);
+    double *ow = (double *)dalloc(sizeof(double) * (size_t)(Ttot + 1), s);
+    const int elo = canon_elo(e_max, K);
+    DBuf<int64_t> o1d(1, s);
+    DBuf<unsigned long long> cur(1, s);
+    int64_t base = 0, o0 = 0;
+    std::vector<int64_t> hv(2);
+    while (o0 < nout) {
+        k_batch_end<<<1, 1, 0, s>>>(o0, nout, budget, S, vcp.p, o1d.p); ++g_kl;
+        const int64_t o1 = d2h_scalar(o1d.p, s);
+        int64_t ov[2] = {o0, o1};
+        int64_t vr[2], tr2[2], cr[2];
+        for (int q = 0; q < 2; q++) {
+            int64_t vv = ov[q];
+            if (S.ostart) LAP_CUDA(cudaMemcpyAsync(&vv, S.ostart + ov[q], 8, cudaMemcpyDeviceToHost, s));
+            LAP_CUDA(cudaStreamSynchronize(s));
+            vr[q] = vv;
+        }
+        for (int q = 0; q < 2; q++) {
+            LAP_CUDA(cudaMemcpyAsync(&tr2[q], vptr.p + vr[q], 8, cudaMemcpyDeviceToHost, s));
+            LAP_CUDA(cudaMemcpyAsync(&cr[q], vcp.p + vr[q], 8, cudaMemcpyDeviceToHost, s));
+        }
+        LAP_CUDA(cudaStreamSynchronize(s));
+        const int64_t Tb = cr[1] - cr[0];
+        DBuf<uint64_t> keys(Tb, s), k2(Tb, s);
+        DBuf<double> vals(Tb, s), v2(Tb, s);
+        LAP_CUDA(cudaMemsetAsync(cur.p, 0, 8, s));
+        if (tr2[1] > tr2[0]) {
+            k_src_emit<<<grid_for(tr2[1] - tr2[0], 256, 148 * 16), 256, 0, s>>>(S, vr[0], vr[1], tr2[0], tr2[1], o0, cb,
+                                                                              cur.p, keys.p, vals.p);
+            ++g_kl;
+            LAP_CHECK_LAUNCH();
+        }
+        const int64_t T = (int64_t)d2h_scalar(cur.p, s);
+        const int end_bit = std::min(64, cb + bitlen_u64((uint64_t)(o1 - o0)));
+        if (T > 0) {
+            size_t bytes = 0;
+            LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, k2.p, vals.p, v2.p, T, 0, end_bit, s));
+            DBuf<char> tmp((int64_t)bytes, s);
+            LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, keys.p, k2.p, vals.p, v2.p, T, 0, end_bit, s));
+            ++g_kl;
+        }
+        keys.release();
+        vals.release();
+        int64_t U = T;
+        if (combine && T > 0) {
+            DBuf<uint64_t> uk(T, s);
+            DBuf<int64_t> cnt(T + 1, s), off(T + 1, s), nu(1, s);
+            size_t bytes = 0;
+            LAP_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, bytes, k2.p, uk.p, cnt.p, nu.p, T, s));
+            DBuf<char> tmp((int64_t)bytes, s);
+            LAP_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.p, bytes, k2.p, uk.p, cnt.p, nu.p, T, s)); ++g_kl;
+            U = d2h_scalar(nu.p, s);
+            LAP_CUDA(cudaMemsetAsync(cnt.p + U, 0, sizeof(int64_t), s));
+            exclusive_scan_i64(cnt.p, off.p, U + 1, s);
+            k_seg_canon<<<grid_for(U, 256, 148 * 16), 256, 0, s>>>(U, off.p, uk.p, v2.p, cb, elo, ocol + base,
+                                                                   ow + base); ++g_kl;
+            DBuf<int64_t> nch(U + 1, s), cfirst(U + 1, s);
+            LAP_CUDA(cudaMemsetAsync(nch.p + U, 0, sizeof(int64_t), s));
+            k_seg_nchunks<<<grid_for(U, 256, 148 * 16), 256, 0, s>>>(U, off.p, nch.p); ++g_kl;
+            exclusive_scan_i64(nch.p, cfirst.p, U + 1, s);
+            const int64_t C = d2h_scalar(cfirst.p + U, s);
+            if (C > 0) {
+                DBuf<int32_t> cseg(C, s);
+                DBuf<I128> part(C, s);
+                k_seg_chunk_map<<<grid_for(U, 256, 148 * 16), 256, 0, s>>>(U, cfirst.p, cseg.p); ++g_kl;
+                k_seg_chunk_sum<<<grid_for(C * 32, 256, 148 * 16), 256, 0, s>>>(C, cseg.p, cfirst.p, off.p, v2.p, elo,
+                                                                              part.p); ++g_kl;
+                k_seg_long_finish<<<grid_for(U, 256, 148 * 16), 256, 0, s>>>(U, cfirst.p, part.p, elo, ow + base); ++g_kl;
+            }
+            k_batch_row_ptr<<<grid_for(o1 - o0, 256, 148 * 8), 256, 0, s>>>(o1 - o0, U, uk.p, cb, base,
+                                                                             out.row_ptr + o0); ++g_kl;
+        } else if (T > 0) {
+            k_decode_cols<<<grid_for(T, 256, 148 * 16), 256, 0, s>>>(T, k2.p, (1ULL << cb) - 1, ocol + base); ++g_kl;
+            LAP_CUDA(cudaMemcpyAsync(ow + base, v2.p, sizeof(double) * (size_t)T, cudaMemcpyDeviceToDevice, s));
+            k_batch_row_ptr<<<grid_for(o1 - o0, 256, 148 * 8), 256, 0, s>>>(o1 - o0, T, k2.p, cb, base,
+                                                                             out.row_ptr + o0); ++g_kl;
+        } else {
+            k_batch_row_ptr<<<grid_for(o1 - o0, 256, 148 * 8), 256, 0, s>>>(o1 - o0, 0, k2.p, cb, base,
+                                                                             out.row_ptr + o0); ++g_kl;
+        }
+        LAP_CHECK_LAUNCH();
+        base += U;
+        o0 = o1;
+    }
+    k_set_i64<<<1, 1, 0, s>>>(out.row_ptr + nout, base); ++g_kl;
+    out.nnz = base;
+    if (base < Ttot - Ttot / 4) {  // shrink the over-allocation (Galerkin: entries inside aggregates vanish)
+        out.col = (int32_t *)dalloc(sizeof(int32_t) * (size_t)(base + 1), s);
+        out.w = (double *)dalloc(sizeof(double) * (size_t)(base + 1), s);
+        LAP_CUDA(cudaMemcpyAsync(out.col, ocol, sizeof(int32_t) * (size_t)base, cudaMemcpyDeviceToDevice, s));
+        LAP_CUDA(cudaMemcpyAsync(out.w, ow, sizeof(double) * (size_t)base, cudaMemcpyDeviceToDevice, s));
+        dfree(ocol, s);
+        dfree(ow, s);
+    } else {
+        out.col = ocol;
+        out.w = ow;
+    }
+    tmark("  terms: batches");
+    out.d = (double *)dalloc(sizeof(double) * (size_t)(nout > 0 ? nout : 1), s);
+    row_sums(nout, out.nnz, out.row_ptr, out.w, out.d, &out.maxw, s);
+    tmark("  terms: row sums");
+}
+
+// =========================================================================
 // O-S1 level 0: random order (O-R31) and relabel
 // =========================================================================
 
@@ -481,6 +868,10 @@ __global__ void k_perm_keys(int64_t n, uint64_t salt, uint64_t *keys, int32_t *i
 __global__ void k_perm_from_order(int64_t n, const int32_t *order, int64_t *perm) {
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
         perm[order[r]] = r;
+}
+__global__ void k_inverse_perm(int64_t n, const int64_t *perm, int32_t *inv) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        inv[perm[i]] = (int32_t)i;
 }
 __global__ void k_identity_i64(int64_t n, int64_t *p) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = i;
@@ -1074,14 +1465,24 @@ __global__ void __launch_bounds__(256) k_lzc_next(int64_t n, int first, int reco
         u[i] = __dmul_rn(rs[i], vn);
     }
 }
-__device__ __forceinline__ void lzc_row_epilogue(int64_t i, double sk, const double *__restrict__ d,
-                                                 const double *__restrict__ u, const double *__restrict__ rs,
-                                                 const double *__restrict__ vp, double bprev, double *__restrict__ y,
-                                                 unsigned long long *maxy) {
+__device__ __forceinline__ double lzc_row_epilogue(int64_t i, double sk, const double *__restrict__ d,
+                                                   const double *__restrict__ u, const double *__restrict__ rs,
+                                                   const double *__restrict__ vp, double bprev,
+                                                   double *__restrict__ y) {
     const double li = __dsub_rn(__dmul_rn(d[i], u[i]), sk);
     const double yi = __dsub_rn(__dmul_rn(rs[i], li), __dmul_rn(bprev, vp[i]));
     y[i] = yi;
-    atomicMax(maxy, (unsigned long long)__double_as_longlong(fabs(yi)));
+    return fabs(yi);
+}
+// max |y| of a warp, one atomic per warp (a single address takes one atomic per
+// row otherwise: 4M serialised atomics on cfg 4 level 0)
+__device__ __forceinline__ void warp_atomic_max(unsigned long long *maxy, double v) {
+    unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, b, o);
+        b = t > b ? t : b;
+    }
+    if ((threadIdx.x & 31) == 0 && b) atomicMax(maxy, b);
 }
 // pass B, rows up to SETUP_LONG entries (G lanes per row)
 template <int G>
@@ -1102,7 +1503,9 @@ __global__ void k_lzc_spmv(int64_t n, const int64_t *__restrict__ row_ptr, const
         const int64_t kb = skip ? 0 : kb0, ke = skip ? 0 : ke0;
         for (int64_t k = kb + gl; k < ke; k += G) a += canon_q(__dmul_rn(w[k], u[col[k]]), elo);
         a = grp_sum_i128<G>(a);
-        if (live && !skip && gl == 0) lzc_row_epilogue(i, canon_result(a, elo), d, u, rs, vp, bprev, y, &st->maxy);
+        double ya = 0.0;
+        if (live && !skip && gl == 0) ya = lzc_row_epilogue(i, canon_result(a, elo), d, u, rs, vp, bprev, y);
+        warp_atomic_max(&st->maxy, ya);
     GROUP_LOOP_END
 }
 // pass B, rows longer than SETUP_LONG: LCHUNK warp chunks, the last chunk of a
@@ -1142,7 +1545,8 @@ __global__ void k_lzc_chunk(int64_t nchunks, const int32_t *__restrict__ crow, c
                 pv.hi = __ldcg(&part[q].hi);
                 t += from_I128(pv);
             }
-            lzc_row_epilogue(i, canon_result(t, elo), d, u, rs, vp, bprev, y, &st->maxy);
+            const double ya = lzc_row_epilogue(i, canon_result(t, elo), d, u, rs, vp, bprev, y);
+            atomicMax(&st->maxy, (unsigned long long)__double_as_longlong(ya));
             ccnt[cslot[c]] = 0;
         }
     }
@@ -1223,10 +1627,10 @@ static double lanczos(lap_hierarchy *h, Level &L, int l, cudaStream_t s) {
         return mr > 0.0 ? ilogb(mr) : -1000;
     }() + 3;
     const int elo_spmv = canon_elo(e_spmv, nnz);
-    const int G = group_size(n, nnz, L.c_end[0] == L.n);
+    const int G = group_size(n, nnz, L.maxdeg <= SHORT_MAX);
     int32_t *lc_row = nullptr, *lc_idx = nullptr, *lc_slot = nullptr, *lc_cnt = nullptr;
     double *lc_dummy = nullptr;
-    const int64_t nlc = L.c_end[0] == L.n ? 0
+    const int64_t nlc = L.maxdeg <= SETUP_LONG ? 0
                         : build_chunks(L.row_ptr, 0, n, SETUP_LONG, &lc_row, &lc_idx, &lc_slot, &lc_dummy, &lc_cnt, s);
     struct FreeLc {
         void *p[5];
@@ -1397,32 +1801,22 @@ static void build_elim_level(lap_hierarchy *h, Level &L, const DBuf<uint8_t> &F,
     L.fid = (int32_t *)dalloc(sizeof(int32_t) * (nF + 1), s);
     k_fmap<<<g, 256, 0, s>>>(n, F.p, cpos.p, fpos.p, L.fmap, L.cid, L.fid); ++g_kl;
     LAP_CHECK_LAUNCH();
-    // terms of the Schur complement: L_CC entries (entry-parallel), fill from the F rows
-    const int G = group_size(n, L.nnz, L.c_end[0] == L.n);
-    DBuf<int64_t> fcnt(nF + 1, s), foff(nF + 1, s);
-    LAP_CUDA(cudaMemsetAsync(fcnt.p, 0, sizeof(int64_t) * (nF + 1), s));
-    k_schur_f_count<<<grid_for(nF, 256, 148 * 16), 256, 0, s>>>(nF, L.fid, L.row_ptr, fcnt.p); ++g_kl;
-    LAP_CHECK_LAUNCH();
-    exclusive_scan_i64(fcnt.p, foff.p, nF + 1, s);
-    int64_t Tf = d2h_scalar(foff.p + nF, s);
-    int cb = bitlen_u64((uint64_t)(nc > 0 ? nc : 1));
-    DBuf<uint64_t> keys(L.nnz + Tf, s);
-    DBuf<double> vals(L.nnz + Tf, s);
-    DBuf<unsigned long long> cur(1, s);
-    LAP_CUDA(cudaMemsetAsync(cur.p, 0, sizeof(unsigned long long), s));
-    if (L.nnz > 0) {
-        k_schur_cc_emit<<<grid_for(L.nnz, 256, 148 * 16), 256, 0, s>>>(n, L.nnz, L.rowof, L.col, L.w, F.p, L.fmap,
-                                                                      cb, cur.p, keys.p, vals.p); ++g_kl;
-        LAP_CHECK_LAUNCH();
+    // the Schur complement, row by row of C (batched terms, CanonSum per entry)
+    {
+        TermSrc S;
+        S.kind = SRC_SCHUR;
+        S.rp = L.row_ptr;
+        S.col = L.col;
+        S.w = L.w;
+        S.d = L.d;
+        S.vfine = L.cid;
+        S.F = F.p;
+        S.fmap = L.fmap;
+        const int cb = bitlen_u64((uint64_t)(nc > 0 ? nc : 1));
+        csr_from_source(S, nc, nc, cb, ilogb_pos(L.maxw) + 1, 4 * L.nnz, true, N, s);
     }
-    int64_t Tcc = (int64_t)d2h_scalar(cur.p, s);
-    int64_t T = Tcc + Tf;
-    k_schur_f_emit<<<grid_for(nF, 256, 148 * 16), 256, 0, s>>>(nF, L.fid, L.row_ptr, L.col, L.w, L.d, L.fmap, foff.p,
-                                                               Tcc, cb, keys.p, vals.p); ++g_kl;
-    LAP_CHECK_LAUNCH();
-    int e_max = ilogb_pos(L.maxw) + 1;
-    csr_from_terms(nc, cb, T, keys, vals, e_max, 4 * L.nnz, true, N, s);
     // transposed L_FC for the restriction P^T b
+    const int G = group_size(n, L.nnz);
     DBuf<int64_t> tc(nc + 1, s);
     LAP_CUDA(cudaMemsetAsync(tc.p, 0, sizeof(int64_t) * (nc + 1), s));
     LAUNCH_G(G, k_ct_count, nc, s, nc, L.cid, L.row_ptr, L.col, F.p, tc.p);
@@ -1441,7 +1835,7 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
     int64_t n = L.n, nnz = L.nnz;
     const lap_params &p = h->p;
     unsigned ge = grid_for(n, 256, 148 * 16);
-    const int G = group_size(n, nnz, L.c_end[0] == L.n);
+    const int G = group_size(n, nnz, L.maxdeg <= SHORT_MAX);
     // test vectors
     DBuf<double> X(4 * n, s), Xn(4 * n, s), M(n, s);
     uint64_t base = mix64(salt_of(p.seed, 3) ^ (uint64_t)(2 * l + attempt));
@@ -1453,7 +1847,7 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
     // long rows (deg > SETUP_LONG): LCHUNK warp chunks (logical CSR)
     int32_t *lc_row = nullptr, *lc_idx = nullptr, *lc_slot = nullptr, *lc_cnt = nullptr;
     double *lc_dummy = nullptr;
-    const int64_t nlc = L.c_end[0] == L.n ? 0
+    const int64_t nlc = L.maxdeg <= SETUP_LONG ? 0
                         : build_chunks(L.row_ptr, 0, n, SETUP_LONG, &lc_row, &lc_idx, &lc_slot, &lc_dummy, &lc_cnt, s);
     struct FreeLc {
         void *p[5];
@@ -1537,27 +1931,100 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
     return d2h_scalar(rid.p + n, s);
 }
 
-static void galerkin(lap_hierarchy *h, Level &L, Level &N, cudaStream_t s) {
-    int64_t n = L.n, m = L.m, nnz = L.nnz;
-    int cb = bitlen_u64((uint64_t)(m > 0 ? m : 1));
-    DBuf<uint64_t> keys(nnz, s);
-    DBuf<double> vals(nnz, s);
-    DBuf<unsigned long long> cur(1, s);
-    LAP_CUDA(cudaMemsetAsync(cur.p, 0, sizeof(unsigned long long), s));
-    if (nnz > 0) {
-        k_gal_emit<<<grid_for(nnz, 256, 148 * 16), 256, 0, s>>>(n, nnz, L.rowof, L.col, L.w, L.agg, cb, cur.p, keys.p,
-                                                                vals.p); ++g_kl;
-        LAP_CHECK_LAUNCH();
+__global__ void k_iota_agg(int64_t n, const int32_t *agg, uint32_t *key, int32_t *ids) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        key[i] = (uint32_t)agg[i];
+        ids[i] = (int32_t)i;
     }
-    int64_t T = (int64_t)d2h_scalar(cur.p, s);
-    tmark("  galerkin emit");
-    csr_from_terms(m, cb, T, keys, vals, ilogb_pos(L.maxw) + 1, L.nnz, true, N, s);
+}
+__global__ void k_mem_ptr(int64_t m, int64_t n, const uint32_t *skey, int64_t *ptr) {
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a <= m; a += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)skey[mid] < a) lo = mid + 1;
+            else hi = mid;
+        }
+        ptr[a] = lo;
+    }
+}
+
+static void galerkin(lap_hierarchy *h, Level &L, Level &N, cudaStream_t s) {
+    const int64_t n = L.n, m = L.m;
+    // members of every aggregate, ascending (stable radix sort by aggregate id)
+    DBuf<uint32_t> k1(n, s), k2(n, s);
+    DBuf<int32_t> ids(n, s), members(n, s);
+    DBuf<int64_t> mem_ptr(m + 1, s);
+    k_iota_agg<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, L.agg, k1.p, ids.p); ++g_kl;
+    {
+        size_t bytes = 0;
+        const int eb = bitlen_u64((uint64_t)(m > 0 ? m : 1));
+        LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k1.p, k2.p, ids.p, members.p, n, 0, eb, s));
+        DBuf<char> tmp((int64_t)bytes, s);
+        LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, k1.p, k2.p, ids.p, members.p, n, 0, eb, s)); ++g_kl;
+    }
+    k_mem_ptr<<<grid_for(m + 1, 256, 148 * 8), 256, 0, s>>>(m, n, k2.p, mem_ptr.p); ++g_kl;
+    LAP_CHECK_LAUNCH();
+    ids.release();
+    k1.release();
+    tmark("  galerkin members");
+    TermSrc S;
+    S.kind = SRC_GALERKIN;
+    S.rp = L.row_ptr;
+    S.col = L.col;
+    S.w = L.w;
+    S.vfine = members.p;
+    S.vout = (const int32_t *)k2.p;  // aggregate of member slot v (sorted keys)
+    S.ostart = mem_ptr.p;
+    S.agg = L.agg;
+    const int cb = bitlen_u64((uint64_t)(m > 0 ? m : 1));
+    csr_from_source(S, n, m, cb, ilogb_pos(L.maxw) + 1, L.nnz, true, N, s);
     h->cur.edges += L.nnz;
 }
 
 // =========================================================================
 // O-S9 hierarchy loop
 // =========================================================================
+
+__global__ void k_max_deg(int64_t n, const int64_t *__restrict__ rp, unsigned long long *out) {
+    unsigned long long m = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long dg = (unsigned long long)(rp[i + 1] - rp[i]);
+        m = dg > m ? dg : m;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, m, o);
+        m = t > m ? t : m;
+    }
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+static int64_t max_degree(int64_t n, const int64_t *rp, cudaStream_t s) {
+    DBuf<unsigned long long> r(1, s);
+    LAP_CUDA(cudaMemsetAsync(r.p, 0, 8, s));
+    if (n > 0) {
+        k_max_deg<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(n, rp, r.p); ++g_kl;
+        LAP_CHECK_LAUNCH();
+    }
+    return (int64_t)d2h_scalar(r.p, s);
+}
+// the level's solve storage; then release the logical CSR of a big level
+// (params.keep_logical: 1 keep, 0 release, -1 release when nnz >= 2^28)
+static void finish_level(lap_hierarchy *h, int l, cudaStream_t s) {
+    Level &L = h->lev[l];
+    build_storage(h, l, s);
+    if (g_tr) g_tr->mark("storage", l);
+    const int kl = h->p.keep_logical;
+    const bool rel = L.kind != KIND_COARSEST && (kl == 0 || (kl < 0 && L.nnz >= ((int64_t)1 << 28)));
+    if (rel) {
+        dfree(L.row_ptr, s);
+        dfree(L.col, s);
+        dfree(L.w, s);
+        L.row_ptr = nullptr;
+        L.col = nullptr;
+        L.w = nullptr;
+        L.logical_released = true;
+    }
+}
 
 void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
     SetupTrace tr(s);
@@ -1641,32 +2108,37 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
     {
         Level &L0 = h->lev[0];
         int cb = bitlen_u64((uint64_t)(n > 0 ? n : 1));
-        DBuf<uint64_t> keys(nnz, s);
-        DBuf<double> vals(nnz, s);
-        if (nnz) {
-            LAUNCH_G(group_size(n, nnz), k_relabel_emit, n, s, n, rp, col, w, h->perm, cb, keys.p, vals.p);
-            LAP_CHECK_LAUNCH();
-        }
-        csr_from_terms(n, cb, nnz, keys, vals, 0, 0, false, L0, s);
+        DBuf<int32_t> inv(n, s);  // old row of new id r
+        k_inverse_perm<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, h->perm, inv.p); ++g_kl;
+        TermSrc S;
+        S.kind = SRC_RELABEL;
+        S.rp = rp;
+        S.col = col;
+        S.w = w;
+        S.vfine = inv.p;
+        S.perm = h->perm;
+        csr_from_source(S, n, n, cb, 0, 0, false, L0, s);
         tr.mark("random order", 0);
     }
     rp_in.release();
     col_in.release();
     w_in.release();
 
-    bool prev_elim = false;
+    // Each level: setup work on its logical CSR, the next level built, then the
+    // level's solve storage (build_storage needs the finer level's storage
+    // order only) and -- for big levels unless params.keep_logical = 1 -- the
+    // logical CSR is released (the solve runs on the storage copy; the
+    // coarsest level keeps it for L^+).
+    int elim_run = 0;  // consecutive elimination levels built just above (O-R21)
     for (int l = 0;; l++) {
         Level &L = h->lev[l];
-        build_storage(h, l, s);
-        tr.mark("storage", l);
-        DBuf<int32_t> rowof(L.nnz, s);  // row of every stored entry (entry-parallel setup kernels)
-        if (L.nnz > 0) LAUNCH_G(group_size(L.n, L.nnz, L.c_end[0] == L.n), k_rowof, L.n, s, L.n, L.row_ptr, rowof.p);
-        L.rowof = rowof.p;
+        L.maxdeg = max_degree(L.n, L.row_ptr, s);
         if (L.n + L.nnz <= p.coarse_nnz || l == p.max_levels - 1 || l == 63) {     // O-R27
             L.kind = KIND_COARSEST;
+            finish_level(h, l, s);
             break;
         }
-        if (p.elim_enable && !prev_elim) {                                          // O-R21
+        if (p.elim_enable && elim_run < p.elim_rounds) {                            // O-R21
             DBuf<uint8_t> F;
             int64_t nF = elim_select(h, L, F, s);
             tr.mark("elim select", l);
@@ -1675,7 +2147,9 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
                 Level &L2 = h->lev[l];
                 build_elim_level(h, L2, F, nF, h->lev[l + 1], s);
                 tr.mark("schur", l);
-                prev_elim = true;
+                F.release();
+                finish_level(h, l, s);
+                elim_run++;
                 continue;
             }
         }
@@ -1683,25 +2157,33 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
         L.kind = KIND_AGG;
         L.lambda = lanczos(h, L, l, s);
         tr.mark("lanczos", l);
-        DBuf<double> S(L.nnz, s);
         int64_t m = L.n;
-        for (int attempt = 0; attempt < 2 && m == L.n; attempt++) m = aggregate_attempt(h, L, l, attempt, S, s);
-        tr.mark("strength+votes", l);
+        {
+            DBuf<int32_t> rowof(L.nnz, s);  // row of every stored entry (entry-parallel strength kernels)
+            if (L.nnz > 0) LAUNCH_G(group_size(L.n, L.nnz, L.maxdeg <= SHORT_MAX), k_rowof, L.n, s, L.n, L.row_ptr, rowof.p);
+            L.rowof = rowof.p;
+            DBuf<double> S(L.nnz, s);
+            for (int attempt = 0; attempt < 2 && m == L.n; attempt++) m = aggregate_attempt(h, L, l, attempt, S, s);
+            tr.mark("strength+votes", l);
+            if (m != L.n && p.keep_strength) L.S = S.take();
+            L.rowof = nullptr;
+        }
         if (m == L.n) {                                                             // stalled twice (O-R28)
             if (L.agg) dfree(L.agg, s);
             L.agg = nullptr;
             L.kind = KIND_COARSEST;
             h->status = LAP_ESTALL;
             if (L.n > 8192) throw Error{LAP_ESTALL, "aggregation stalled on a level with more than 8192 vertices"};
+            finish_level(h, l, s);
             break;
         }
         L.m = m;
-        if (p.keep_strength) L.S = S.take();
         h->lev.emplace_back();
         Level &L2 = h->lev[l];
         galerkin(h, L2, h->lev[l + 1], s);
         tr.mark("galerkin", l);
-        prev_elim = false;
+        finish_level(h, l, s);
+        elim_run = 0;
     }
     coarse_pinv(h->lev.back(), s);
     tr.mark("coarsest pinv", (int)h->lev.size() - 1);

@@ -39,7 +39,8 @@ class lap_params(ctypes.Structure):
         ("vote_threshold", ctypes.c_int32), ("coarse_nnz", ctypes.c_int64), ("max_levels", ctypes.c_int32),
         ("seed", ctypes.c_uint64), ("random_order", ctypes.c_int32), ("affinity_power", ctypes.c_int32),
         ("keep_strength", ctypes.c_int32), ("use_graphs", ctypes.c_int32), ("replicate_nnz", ctypes.c_int64),
-        ("cycle", ctypes.c_int32), ("kcycle_inner", ctypes.c_int32),
+        ("cycle", ctypes.c_int32), ("kcycle_inner", ctypes.c_int32), ("elim_rounds", ctypes.c_int32),
+        ("keep_logical", ctypes.c_int32),
     ]
 
 
@@ -54,7 +55,7 @@ EXPORTS = [
     "lap_perm", "lap_spmv", "lap_vcycle", "lap_kcycle", "lap_solve_block", "lap_get_stats", "lap_bench_op",
     "lap_nccl_unique_id", "lap_comm_create", "lap_comm_create_virtual", "lap_comm_info", "lap_comm_free",
     "lap_setup_dist", "lap_dist_index", "lap_pool_retain", "lap_random_stream",
-    "lap_bench_gather",
+    "lap_bench_gather", "lap_level_rows",
 ]
 
 
@@ -94,6 +95,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "lap_pool_retain": (None, [ctypes.c_uint64]),
         "lap_random_stream": (ctypes.c_int, [i32, ctypes.c_uint64, i32, i32, i64, P, P]),
         "lap_bench_gather": (ctypes.c_int, [i64, i64, i32, P, P]),
+        "lap_level_rows": (ctypes.c_int, [P, i32, i64, P, P, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -338,6 +340,17 @@ class Hierarchy:
             _check(lib().lap_coarse_pinv(self._h, _ptr(P)))
             out["pinv"] = P.reshape(n, n)
         return out
+
+    def level_rows(self, l: int, rows):
+        """Rows of level l's logical CSR rebuilt from the solve storage
+        (lap_level_rows): returns (row_ptr[k+1], col, w)."""
+        rows = np.ascontiguousarray(rows, np.int64)
+        rp = np.zeros(len(rows) + 1, np.int64)
+        _check(lib().lap_level_rows(self._h, l, len(rows), _ptr(rows), _ptr(rp), None, None))
+        col = np.zeros(max(1, int(rp[-1])), np.int32)
+        w = np.zeros(max(1, int(rp[-1])), np.float64)
+        _check(lib().lap_level_rows(self._h, l, len(rows), _ptr(rows), _ptr(rp), _ptr(col), _ptr(w)))
+        return rp, col[:rp[-1]], w[:rp[-1]]
 
     def strength(self, l: int) -> np.ndarray:
         _, n, z, _ = self.level_info(l)

@@ -167,9 +167,10 @@ def test_device_graph_and_determinism(P):
 
 
 @pytest.mark.parametrize("kw", [dict(random_order=0), dict(affinity_power=2), dict(seed=5),
-                                dict(elim_enable=0), dict(cheby_degree=3), dict(use_graphs=0)])
+                                dict(elim_enable=0), dict(cheby_degree=3), dict(use_graphs=0),
+                                dict(elim_rounds=3)])
 def test_parameter_variants(P, kw):
-    g = lapgen.rmat(11)
+    g = lapgen.path(5000) if "elim_rounds" in kw else lapgen.rmat(11)  # path: consecutive elimination levels
     h = P.Hierarchy(g, **kw)
     okw = {k: v for k, v in kw.items() if k != "use_graphs"}
     ho = oracle.Hierarchy(g, **okw)
@@ -281,3 +282,42 @@ def test_fused_transfers_bitwise(P, tmp_path):
         assert r.returncode == 0, r.stderr[-2000:]
         res.append(np.load(f))
     assert res[0].tobytes() == res[1].tobytes()
+
+
+def test_memory_lean_paths_bit_exact(P):
+    """The memory-lean setup paths give the oracle's hierarchy bit for bit:
+    terms built in many small batches of output rows (LAP_TERM_BATCH), the
+    search-based symmetry check (LAP_SYMCHECK=search), and released logical
+    copies (keep_logical = 0) read back through lap_level_rows."""
+    import os
+    import subprocess
+    import sys
+    code = ("import numpy as np, lapgen, oracle, paper_1705_06266_b200 as P\n"
+            "for g in [lapgen.rmat(12), lapgen.barabasi_albert(6000, 8), lapgen.grid3d(14), lapgen.star(9000)]:\n"
+            "    ho = oracle.Hierarchy(g)\n"
+            "    h = P.Hierarchy(g)\n"
+            "    assert h.nlev == ho.nlev\n"
+            "    for l in range(ho.nlev):\n"
+            "        a, o = h.level(l), ho.level(l)\n"
+            "        assert (a['n'], a['nnz']) == (o.n, o.nnz)\n"
+            "        assert np.array_equal(a['col'], o.col) and a['w'].tobytes() == o.w.tobytes() and a['d'].tobytes() == o.d.tobytes(), l\n"
+            "        assert np.float64(a['lam']).tobytes() == np.float64(o.lam).tobytes()\n"
+            "    hr = P.Hierarchy(g, keep_logical=0)\n"
+            "    for l in range(ho.nlev):\n"
+            "        o = ho.level(l)\n"
+            "        rows = np.arange(o.n)\n"
+            "        rp, col, w = hr.level_rows(l, rows)\n"
+            "        assert np.array_equal(rp, o.row_ptr) and np.array_equal(col, o.col) and w.tobytes() == o.w.tobytes(), l\n"
+            "    b = lapgen.rhs(g.n); x, it, rr, rc = hr.solve(b); xo, ito, _, _ = ho.solve(b)\n"
+            "    assert rc == 0 and rr <= 1e-8 and abs(it - ito) <= 1\n"
+            "bad = lapgen.Graph(3, np.array([0, 1, 3, 4]), np.array([1, 0, 2, 1], np.int32), np.array([1.0, np.nextafter(1.0, 2.0), 2.0, 2.0]))\n"
+            "try:\n"
+            "    P.Hierarchy(bad); raise SystemExit('accepted an asymmetric graph')\n"
+            "except P.LapError as e:\n"
+            "    assert e.code == P.LAP_EGRAPH\n"
+            "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for env in [{"LAP_TERM_BATCH": "3000"}, {"LAP_SYMCHECK": "search"}, {"LAP_TERM_BATCH": "100000", "LAP_SYMCHECK": "search"}]:
+        e = dict(os.environ, **env)
+        r = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, timeout=900, cwd=root)
+        assert r.returncode == 0 and "ok" in r.stdout, (env, r.stderr[-3000:])

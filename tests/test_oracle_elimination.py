@@ -122,3 +122,26 @@ def test_elimination_vcycle_is_exact_on_p3():
     x = h.vcycle(0, b)
     xs = np.linalg.pinv(dense_L(lapgen.path(3))) @ b
     assert np.allclose(x - x.mean(), xs, atol=1e-14)
+
+
+def test_elim_rounds_consecutive_levels():
+    """P:485-486: "we can run low-degree elimination multiple times in a row";
+    elim_rounds = r allows up to r elimination levels in a row (default 1)."""
+    g = lapgen.path(3000)
+    for r in (1, 2, 4):
+        h = oracle.Hierarchy(g, elim_rounds=r)
+        kinds = [L.kind for L in h.levels()]
+        run = best = 0
+        for k in kinds:
+            run = run + 1 if k == oracle.ELIM else 0
+            best = max(best, run)
+        assert best <= r
+        if r > 1:
+            assert best >= 2, kinds          # a path keeps passing the 5% gate
+        x, it, rr, rc = h.solve(lapgen.rhs(g.n))
+        assert rc == 0 and rr <= 1e-8
+    # an elimination-only hierarchy down to the coarsest is an exact solver: one iteration
+    h = oracle.Hierarchy(lapgen.path(200), elim_rounds=40)
+    assert all(L.kind != oracle.AGG for L in h.levels())
+    x, it, rr, rc = h.solve(lapgen.rhs(200))
+    assert it == 1 and rr <= 1e-12

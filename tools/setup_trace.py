@@ -10,6 +10,7 @@ g = lapgen.config(k)
 dev = torch.device("cuda", 0)
 gd = lapgen.Graph(g.n, torch.from_numpy(g.row_ptr).to(dev), torch.from_numpy(g.col).to(dev), torch.from_numpy(g.w).to(dev))
 st = torch.cuda.Stream()
+P.pool_retain(1 << 40)
 for name, strm in [("torch stream", st), ("default stream", None)]:
     for rep in range(4):
         torch.cuda.synchronize()
