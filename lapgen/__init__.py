@@ -290,15 +290,16 @@ def config(k: int) -> Graph:
     if k >= 2 and os.path.exists(fn):
         try:
             z = np.load(fn)
-            return Graph(int(z["n"]), z["row_ptr"], z["col"], z["w"], str(z["name"]))
+            w = z["w"] if z["w"].size else None  # cfg 5: unit weights are not materialised
+            return Graph(int(z["n"]), z["row_ptr"], z["col"], w, str(z["name"]))
         except Exception:
             pass
     g = makers[k]()
-    if k >= 2 and k <= 4:
+    if k >= 2:
         try:
             os.makedirs(cache, exist_ok=True)
             tmp = fn + f".tmp{os.getpid()}.npz"
-            np.savez(tmp, n=g.n, row_ptr=g.row_ptr, col=g.col, w=g.w, name=g.name)
+            np.savez(tmp, n=g.n, row_ptr=g.row_ptr, col=g.col, w=g.w if g.w is not None else np.zeros(0), name=g.name)
             os.replace(tmp, fn)
         except OSError:
             pass

@@ -82,6 +82,7 @@ def lib():
             "orc_validate": (ctypes.c_int, [i64, P, P, P]),
             "orc_random_perm": (None, [i64, u64, P]),
             "orc_row_sums": (None, [i64, P, P, P]),
+            "orc_relabel": (None, [i64, P, P, P, P, P, P, P]),
             "orc_spmv": (None, [i64, P, P, P, P, P, P]),
             "orc_elim_select": (i64, [i64, P, P, i32, u64, P, P]),
             "orc_schur": (i64, [i64, P, P, P, P, P, P, P, P, P, P]),
@@ -176,6 +177,17 @@ def random_perm(n: int, seed: int = 0) -> np.ndarray:
     perm = np.zeros(n, dtype=np.int64)
     lib().orc_random_perm(n, seed, _p(perm))
     return perm
+
+
+def relabel(g, perm):
+    """O-S1: Pi L Pi^T of graph g (w None = unit) -> (row_ptr, col, w)."""
+    rp = np.zeros(g.n + 1, np.int64)
+    col = np.zeros(max(1, g.nnz), np.int32)
+    w = np.zeros(max(1, g.nnz), np.float64)
+    ww = None if g.w is None else _c(g.w, np.float64)
+    lib().orc_relabel(g.n, _p(_c(g.row_ptr, np.int64)), _p(_c(g.col, np.int32)), _p(ww), _p(_c(perm, np.int64)),
+                      _p(rp), _p(col), _p(w))
+    return rp, col[:g.nnz], w[:g.nnz]
 
 
 def row_sums(n, row_ptr, w) -> np.ndarray:
@@ -333,7 +345,7 @@ class Hierarchy:
     def __init__(self, g, params: Params | None = None, **kw):
         self.params = params if params is not None else default_params(**kw)
         self._h = ctypes.c_void_p()
-        w = _c(g.w, np.float64)
+        w = None if g.w is None else _c(g.w, np.float64)
         self._keep = (_c(g.row_ptr, np.int64), _c(g.col, np.int32), w)
         self.status = lib().orc_setup(g.n, _p(self._keep[0]), _p(self._keep[1]), _p(self._keep[2]),
                                       ctypes.byref(self.params), ctypes.byref(self._h))
@@ -376,6 +388,28 @@ class Hierarchy:
 
     def levels(self):
         return [self.level(l) for l in range(self.nlev)]
+
+    def level_view(self, l: int) -> LevelData:
+        """level(l) without copies: numpy views into the oracle's memory, valid
+        while this Hierarchy is alive (cfg 5 levels hold ~25 GB each)."""
+        L = lib().orc_get_level(self._h, l).contents
+        n, z = L.n, L.nnz
+
+        def v(ptr, cnt, dt):
+            if cnt <= 0 or not ptr:
+                return np.zeros(0, dtype=dt)
+            return np.ctypeslib.as_array(ptr, shape=(cnt,))
+        ld = LevelData(L.kind, n, z, v(L.row_ptr, n + 1, np.int64), v(L.col, z, np.int32), v(L.w, z, np.float64),
+                       v(L.d, n, np.float64))
+        if L.kind == AGG:
+            ld.lam, ld.m = L.lam, L.m
+            ld.agg = v(L.agg, n, np.int32)
+        elif L.kind == ELIM:
+            ld.nF = L.nF
+            ld.fmap = v(L.fmap, n, np.int32)
+        else:
+            ld.pinv = v(L.pinv, n * n, np.float64).reshape(n, n)
+        return ld
 
     def vcycle(self, l: int, b) -> np.ndarray:
         n = self.level(l).n

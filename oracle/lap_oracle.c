@@ -239,19 +239,22 @@ static int64_t find_in_row(const int64_t *row_ptr, const int32_t *col, int64_t i
 int orc_validate(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *w) {
     if (n < 1 || !row_ptr) return ORC_EINVAL;
     if (row_ptr[0] != 0) return ORC_EGRAPH;
+    for (int64_t i = 0; i < n; i++) if (row_ptr[i + 1] < row_ptr[i]) return ORC_EGRAPH;
+    int bad = 0;
+    #pragma omp parallel for schedule(dynamic, 1024) reduction(|:bad)
     for (int64_t i = 0; i < n; i++) {
-        if (row_ptr[i + 1] < row_ptr[i]) return ORC_EGRAPH;
-        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; k++) {
+        for (int64_t k = row_ptr[i]; k < row_ptr[i + 1] && !bad; k++) {
             int32_t j = col[k];
-            if (j < 0 || j >= n || j == i) return ORC_EGRAPH;             /* range, self loop */
-            if (k > row_ptr[i] && col[k - 1] >= j) return ORC_EGRAPH;      /* sorted, unique */
+            if (j < 0 || j >= n || j == i) { bad = 1; break; }              /* range, self loop */
+            if (k > row_ptr[i] && col[k - 1] >= j) { bad = 1; break; }       /* sorted, unique */
             double wk = w ? w[k] : 1.0;
-            if (!(wk > 0.0) || !isfinite(wk)) return ORC_EGRAPH;          /* w > 0 */
+            if (!(wk > 0.0) || !isfinite(wk)) { bad = 1; break; }           /* w > 0 */
             int64_t t = find_in_row(row_ptr, col, j, (int32_t)i);
-            if (t < 0) return ORC_EGRAPH;                                 /* symmetric pattern */
-            if (w && memcmp(&w[t], &wk, 8) != 0) return ORC_EGRAPH;       /* w_ij == w_ji bitwise */
+            if (t < 0) { bad = 1; break; }                                  /* symmetric pattern */
+            if (w && memcmp(&w[t], &wk, 8) != 0) { bad = 1; break; }        /* w_ij == w_ji bitwise */
         }
     }
+    if (bad) return ORC_EGRAPH;
     /* connectivity by BFS ("we assume that the graph G is connected") */
     int64_t *queue = malloc(sizeof(int64_t) * (size_t)n);
     uint8_t *seen = calloc((size_t)n, 1);
@@ -983,6 +986,35 @@ void orc_free(orc_hier *h) {
     free(h);
 }
 
+/* O-S1: the relabelled level 0, Pi L Pi^T: new row r = old row
+ * inv[r], columns perm[col] in ascending order; w = NULL means unit weights.
+ * out_row_ptr[n+1], out_col/out_w[nnz]. */
+void orc_relabel(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *w, const int64_t *perm,
+                 int64_t *out_row_ptr, int32_t *out_col, double *out_w) {
+    int64_t *inv = malloc(sizeof(int64_t) * (size_t)n);
+    for (int64_t i = 0; i < n; i++) inv[perm[i]] = i;
+    out_row_ptr[0] = 0;
+    for (int64_t r = 0; r < n; r++) out_row_ptr[r + 1] = out_row_ptr[r] + (row_ptr[inv[r] + 1] - row_ptr[inv[r]]);
+    int64_t mx = 0;
+    for (int64_t i = 0; i < n; i++) if (row_ptr[i + 1] - row_ptr[i] > mx) mx = row_ptr[i + 1] - row_ptr[i];
+    #pragma omp parallel
+    {
+        term_t *tmp = malloc(sizeof(term_t) * (size_t)(mx + 1));
+        #pragma omp for schedule(dynamic, 1024)
+        for (int64_t r = 0; r < n; r++) {
+            int64_t i = inv[r], len = row_ptr[i + 1] - row_ptr[i];
+            for (int64_t k = 0; k < len; k++) {
+                tmp[k].c = (int32_t)perm[col[row_ptr[i] + k]];
+                tmp[k].v = w ? w[row_ptr[i] + k] : 1.0;
+            }
+            qsort(tmp, (size_t)len, sizeof(term_t), cmp_term);
+            for (int64_t k = 0; k < len; k++) { out_col[out_row_ptr[r] + k] = tmp[k].c; out_w[out_row_ptr[r] + k] = tmp[k].v; }
+        }
+        free(tmp);
+    }
+    free(inv);
+}
+
 int orc_setup(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *w,
               const orc_params *pp, orc_hier **out) {
     *out = NULL;
@@ -1005,27 +1037,7 @@ int orc_setup(int64_t n, const int64_t *row_ptr, const int32_t *col, const doubl
     L0->col = malloc(sizeof(int32_t) * (size_t)(nnz + 1));
     L0->w = malloc(sizeof(double) * (size_t)(nnz + 1));
     L0->d = malloc(sizeof(double) * (size_t)n);
-    {
-        int64_t *inv = malloc(sizeof(int64_t) * (size_t)n);
-        for (int64_t i = 0; i < n; i++) inv[h->perm[i]] = i;
-        for (int64_t r = 0; r < n; r++) L0->row_ptr[r + 1] = L0->row_ptr[r] + (row_ptr[inv[r] + 1] - row_ptr[inv[r]]);
-        term_t *tmp = malloc(sizeof(term_t) * (size_t)(n > 0 ? 1 : 1));
-        int64_t mx = 0;
-        for (int64_t i = 0; i < n; i++) if (row_ptr[i + 1] - row_ptr[i] > mx) mx = row_ptr[i + 1] - row_ptr[i];
-        free(tmp);
-        tmp = malloc(sizeof(term_t) * (size_t)(mx + 1));
-        for (int64_t r = 0; r < n; r++) {
-            int64_t i = inv[r], len = row_ptr[i + 1] - row_ptr[i];
-            for (int64_t k = 0; k < len; k++) {
-                tmp[k].c = (int32_t)h->perm[col[row_ptr[i] + k]];
-                tmp[k].v = w ? w[row_ptr[i] + k] : 1.0;
-            }
-            qsort(tmp, (size_t)len, sizeof(term_t), cmp_term);
-            for (int64_t k = 0; k < len; k++) { L0->col[L0->row_ptr[r] + k] = tmp[k].c; L0->w[L0->row_ptr[r] + k] = tmp[k].v; }
-        }
-        free(tmp);
-        free(inv);
-    }
+    orc_relabel(n, row_ptr, col, w, h->perm, L0->row_ptr, L0->col, L0->w);
     orc_row_sums(n, L0->row_ptr, L0->w, L0->d);
 
     int elim_run = 0;   /* elimination levels in a row just above (O-R21; P:485-486 elim_rounds) */

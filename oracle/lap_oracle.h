@@ -110,6 +110,8 @@ int32_t  orc_ilogb(double x);
 int  orc_validate(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *w);
 void orc_random_perm(int64_t n, uint64_t seed, int64_t *perm);
 void orc_row_sums(int64_t n, const int64_t *row_ptr, const double *w, double *d);
+void orc_relabel(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *w, const int64_t *perm,
+                 int64_t *out_row_ptr, int32_t *out_col, double *out_w);
 
 /* --- primitives (each pinned in tests) ------------------------------------ */
 void orc_spmv(int64_t n, const int64_t *row_ptr, const int32_t *col, const double *w,

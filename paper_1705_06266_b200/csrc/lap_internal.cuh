@@ -42,6 +42,7 @@ bool debug_sync();
 // ---------------------------------------------------------------- memory
 // Stream-ordered device allocation (cudaMallocAsync pool).
 void *dalloc(size_t bytes, cudaStream_t s);
+cudaMemPool_t lib_pool();
 void dfree(void *p, cudaStream_t s);
 
 template <class T>

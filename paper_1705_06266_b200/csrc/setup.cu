@@ -324,7 +324,9 @@ struct SetupTrace {
         if (!on) return;
         cudaStreamSynchronize(s);
         double t = now();
-        fprintf(stderr, "[lap setup] level %2d %-18s %9.3f ms\n", l, what, t - t0);
+        uint64_t rsv = 0;
+        cudaMemPoolGetAttribute(lib_pool(), cudaMemPoolAttrReservedMemCurrent, &rsv);
+        fprintf(stderr, "[lap setup] level %2d %-18s %9.3f ms  (pool %.2f GB)\n", l, what, t - t0, rsv / 1e9);
         t0 = t;
     }
 };

@@ -134,14 +134,34 @@ __global__ void k_storage_deg(int64_t n, const int32_t *sid, const int64_t *rp, 
     }
 }
 // copy logical row sid[p] into storage row p, columns translated; entry-
-// parallel over the storage entries (hub rows do not serialise)
-__global__ void k_storage_fill(int64_t n, int64_t nnz, const int32_t *sid, const int32_t *spos, const int64_t *rp,
-                               const int32_t *col, const double *w, const int64_t *srp, int32_t *scol, double *sw) {
-    GRID_STRIDE(t, nnz) {
-        int64_t p = row_of(srp, n, t);
-        int64_t src = rp[sid[p]] + (t - srp[p]);
-        scol[t] = spos[col[src]];
-        sw[t] = w[src];
+// parallel over the storage entries (hub rows do not serialise).  A block's
+// 256 entries span few rows: two full searches per block bound the rows, the
+// per-entry search runs inside that range (cfg 5 level 0: 2.1e9 entries)
+__global__ void __launch_bounds__(256) k_storage_fill(int64_t n, int64_t nnz, const int32_t *sid, const int32_t *spos,
+                                                      const int64_t *rp, const int32_t *col, const double *w,
+                                                      const int64_t *srp, int32_t *scol, double *sw) {
+    __shared__ int64_t plo, phi;
+    for (int64_t b0 = (int64_t)blockIdx.x * 256; b0 < nnz; b0 += (int64_t)gridDim.x * 256) {
+        if (threadIdx.x < 2) {
+            const int64_t tt = threadIdx.x == 0 ? b0 : min(nnz, b0 + 256) - 1;
+            const int64_t r = row_of(srp, n, tt);
+            if (threadIdx.x == 0) plo = r;
+            else phi = r;
+        }
+        __syncthreads();
+        const int64_t t = b0 + threadIdx.x;
+        if (t < nnz) {
+            int64_t lo = plo, hi = phi;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi + 1) >> 1;
+                if (srp[mid] <= t) lo = mid;
+                else hi = mid - 1;
+            }
+            const int64_t src = rp[sid[lo]] + (t - srp[lo]);
+            scol[t] = spos[col[src]];
+            sw[t] = w ? w[src] : 1.0;
+        }
+        __syncthreads();
     }
 }
 __global__ void k_to_u16(int64_t m, const int32_t *in, uint16_t *out) {
@@ -353,22 +373,31 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
         k_storage_fill<<<grid_for(L.nnz, 256, 148 * 16), 256, 0, s>>>(n, L.nnz, L.sid, L.spos, L.row_ptr, L.col, L.w,
                                                                       L.srp, L.scol, L.sw);
         g_kl++;
-        // each storage row in ascending STORAGE column order: the u-th column of
-        // consecutive rows of a SELL slice then point the same way (-z, -y, -x, +x,
-        // ... on a grid-like level), so one gather instruction touches few lines
-        // instead of one line per lane (the L1 tag rate bounds these gathers)
-        if (L.nnz < ((int64_t)1 << 31) && n < ((int64_t)1 << 31) && !getenv_flag_off("LAP_SORT_ROWS")) {
-            DBuf<int32_t> c2(L.nnz, s);
-            DBuf<double> w2(L.nnz, s);
+        // each SHORT storage row (the SELL class, rows [0, c_end[0]) of the storage
+        // order) in ascending STORAGE column order: the u-th column of consecutive
+        // rows of a SELL slice then point the same way (-z, -y, -x, +x, ... on a
+        // grid-like level), so one gather instruction touches few lines instead of
+        // one line per lane (the L1 tag rate bounds these gathers).  Long rows are
+        // read in 32-entry warp chunks, where the order buys nothing: they keep
+        // the logical order (no sort and no double buffer over ~all entries of a
+        // power-law level: cfg 5 level 0 storage 2.1 s -> see DESIGN.md)
+        // long rows are sorted too (gather locality of dense-ish rows) unless the
+        // level is served by the column-tiled kernel or is huge (the sort would
+        // cost more setup than it saves: cfg 5 level 1, 2.1e9 entries)
+        const int64_t short_nnz = L.nnz < ((int64_t)1 << 28) ? L.nnz : (nshort > 0 ? d2h(L.srp + nshort, s) : 0);
+        const int64_t nsorted = L.nnz < ((int64_t)1 << 28) ? n : nshort;
+        if (short_nnz > 0 && short_nnz < ((int64_t)1 << 31) && !getenv_flag_off("LAP_SORT_ROWS")) {
+            DBuf<int32_t> c2(short_nnz, s);
+            DBuf<double> w2(short_nnz, s);
             size_t bytes = 0;
-            LAP_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, bytes, L.scol, c2.p, L.sw, w2.p, (int)L.nnz, (int)n,
-                                                         L.srp, L.srp + 1, s));
+            LAP_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, bytes, L.scol, c2.p, L.sw, w2.p, (int)short_nnz,
+                                                         (int)nsorted, L.srp, L.srp + 1, s));
             DBuf<char> tmp((int64_t)bytes, s);
-            LAP_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp.p, bytes, L.scol, c2.p, L.sw, w2.p, (int)L.nnz, (int)n,
-                                                         L.srp, L.srp + 1, s));
+            LAP_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp.p, bytes, L.scol, c2.p, L.sw, w2.p, (int)short_nnz,
+                                                         (int)nsorted, L.srp, L.srp + 1, s));
             g_kl++;
-            std::swap(L.scol, c2.p);
-            std::swap(L.sw, w2.p);
+            LAP_CUDA(cudaMemcpyAsync(L.scol, c2.p, sizeof(int32_t) * short_nnz, cudaMemcpyDeviceToDevice, s));
+            LAP_CUDA(cudaMemcpyAsync(L.sw, w2.p, sizeof(double) * short_nnz, cudaMemcpyDeviceToDevice, s));
         }
     }
     // SELL-32 slices of the short class

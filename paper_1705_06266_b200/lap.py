@@ -341,6 +341,15 @@ class Hierarchy:
             out["pinv"] = P.reshape(n, n)
         return out
 
+    def level_maps(self, l: int):
+        """(d, map) of level l (map = agg or fmap; None for the coarsest) --
+        available also when the logical CSR was released."""
+        kind, n, z, lam = self.level_info(l)
+        d = np.zeros(max(n, 1), np.float64)
+        mp = np.zeros(max(n, 1), np.int32)
+        _check(lib().lap_level_export(self._h, l, None, None, None, _ptr(d), _ptr(mp)))
+        return d[:n], (mp[:n] if kind != KIND_COARSEST else None)
+
     def level_rows(self, l: int, rows):
         """Rows of level l's logical CSR rebuilt from the solve storage
         (lap_level_rows): returns (row_ptr[k+1], col, w)."""

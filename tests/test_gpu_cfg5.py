@@ -1,0 +1,128 @@
+"""cfg 5 (BASELINE.json configs[4]: R-MAT scale 26, edge factor 16, LCC, unit
+weights; ~32.8M vertices, ~2.1e9 stored entries) end to end on ONE B200.
+
+Default (-m gpu): generation (C/OpenMP, lapgen.rmat_large), lap_setup +
+lap_solve on the device, the TRUE relative residual recomputed on the host
+from the input graph, level 0 checked against its definition Pi L Pi^T on
+sampled rows (Pi = the oracle's random order, O-S1), and every level's SpMV
+checked per entry (O-P2 bound) on sampled rows against those rows.
+
+LAP_TEST_CFG5_ORACLE=1 adds the full CPU oracle (OpenMP, all host cores,
+bitwise = 1 thread; ~10 min, ~120 GB host RAM) and compares the whole
+hierarchy: perm, every level's d / agg / fmap / lambda-hat bit-exactly, the
+CSR of every level bit-exactly (whole when the GPU kept the logical copy,
+else 20000 sampled + the 200 longest rows via lap_level_rows), and the solve
+iterations within +-1.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import lapgen
+import oracle
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def cfg5():
+    import paper_1705_06266_b200 as P
+    g = lapgen.config(5)
+    dev = torch.device("cuda", 0)
+    gd = lapgen.Graph(g.n, torch.from_numpy(g.row_ptr).to(dev), torch.from_numpy(g.col).to(dev), None)
+    h = P.Hierarchy(gd)
+    del gd
+    torch.cuda.empty_cache()
+    return g, h
+
+
+def _sample_rows(n, rp, k, seed):
+    rng = np.random.default_rng(seed)
+    rows = rng.choice(n, min(n, k), replace=False)
+    longest = np.argsort(np.diff(rp))[-200:]
+    return np.unique(np.concatenate([rows, longest]))
+
+
+def test_cfg5_solve_true_residual(cfg5):
+    from scipy.sparse import csr_matrix
+    g, h = cfg5
+    b = lapgen.rhs(g.n)
+    x, it, rr, rc = h.solve(torch.from_numpy(b).cuda())
+    x = x.cpu().numpy()
+    assert rc == 0 and rr <= 1e-8, (rc, rr, it)
+    A = csr_matrix((np.ones(g.nnz), g.col, g.row_ptr), shape=(g.n, g.n))
+    deg = np.diff(g.row_ptr).astype(np.float64)
+    bb = b - b.mean()
+    r = bb - (deg * x - A @ x)
+    true = np.linalg.norm(r) / np.linalg.norm(bb)
+    assert true <= 1.01e-8, true
+    assert abs(x.mean()) <= 1e-10 * np.abs(x).max()
+
+
+def test_cfg5_level0_is_pi_l_pi(cfg5):
+    g, h = cfg5
+    perm = oracle.random_perm(g.n, 0)
+    assert np.array_equal(h.perm(), perm)
+    inv = np.empty(g.n, np.int64)
+    inv[perm] = np.arange(g.n)
+    rows = _sample_rows(g.n, g.row_ptr, 20000, 5)
+    rp, col, w = h.level_rows(0, rows)
+    for t, r in enumerate(rows):
+        i = inv[r]
+        want = np.sort(perm[g.col[g.row_ptr[i]:g.row_ptr[i + 1]]])
+        assert np.array_equal(col[rp[t]:rp[t + 1]], want), r
+    assert np.all(w == 1.0)
+    d, _ = h.level_maps(0)
+    assert np.array_equal(d[rows], np.diff(g.row_ptr)[inv[rows]].astype(np.float64))
+
+
+def test_cfg5_spmv_every_level_sampled_rows(cfg5):
+    g, h = cfg5
+    rng = np.random.default_rng(7)
+    for l in range(h.nlev):
+        kind, n, nnz, _ = h.level_info(l)
+        x = rng.standard_normal(n)
+        y = h.spmv(l, torch.from_numpy(x).cuda()).cpu().numpy()
+        d, _ = h.level_maps(l)
+        rows = _sample_rows(n, np.zeros(n + 1, np.int64), 5000, l) if n > 5000 else np.arange(n)
+        rp, col, w = h.level_rows(l, rows)
+        for t, i in enumerate(rows):
+            c, ww = col[rp[t]:rp[t + 1]], w[rp[t]:rp[t + 1]]
+            yo = d[i] * x[i] - np.sum(ww * x[c])
+            bound = 1e-12 * (abs(d[i] * x[i]) + np.sum(np.abs(ww * x[c])))
+            assert abs(y[i] - yo) <= bound + 1e-300, (l, i, y[i], yo)
+
+
+@pytest.mark.skipif(os.environ.get("LAP_TEST_CFG5_ORACLE") != "1", reason="full cfg-5 oracle: set LAP_TEST_CFG5_ORACLE=1")
+def test_cfg5_full_oracle_hierarchy(cfg5):
+    g, h = cfg5
+    cores = len(os.sched_getaffinity(0))
+    oracle.set_threads(cores)
+    ho = oracle.Hierarchy(g)
+    assert h.nlev == ho.nlev
+    assert np.array_equal(h.perm(), ho.perm())
+    for l in range(ho.nlev):
+        o = ho.level_view(l)
+        kind, n, nnz, lam = h.level_info(l)
+        assert (kind, n, nnz) == (o.kind, o.n, o.nnz), l
+        d, mp = h.level_maps(l)
+        assert d.tobytes() == o.d.tobytes(), l
+        if o.kind == oracle.AGG:
+            assert np.array_equal(mp, o.agg), l
+            assert np.float64(lam).tobytes() == np.float64(o.lam).tobytes(), l
+        elif o.kind == oracle.ELIM:
+            assert np.array_equal(mp, o.fmap), l
+        rows = np.arange(o.n) if o.nnz < (1 << 26) else _sample_rows(o.n, o.row_ptr, 20000, 11 + l)
+        rp, col, w = h.level_rows(l, rows)
+        orp = o.row_ptr
+        for t, i in enumerate(rows):
+            assert np.array_equal(col[rp[t]:rp[t + 1]], o.col[orp[i]:orp[i + 1]]), (l, i)
+            assert w[rp[t]:rp[t + 1]].tobytes() == o.w[orp[i]:orp[i + 1]].tobytes(), (l, i)
+    b = lapgen.rhs(g.n)
+    x, it, rr, rc = h.solve(torch.from_numpy(b).cuda())
+    xo, ito, rro, rco = ho.solve(b)
+    assert rc == 0 and rr <= 1e-8 and abs(it - ito) <= 1, (it, ito, rr)
+    x = x.cpu().numpy()
+    assert np.abs(x - xo).max() <= 1e-6 * np.abs(xo).max()
