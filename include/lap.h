@@ -132,6 +132,24 @@ lap_status lap_solve(lap_hierarchy *h, const double *b, double *x, double tol,
 
 void lap_free(lap_hierarchy *h);   /* NULL-safe */
 
+/* A hierarchy given as files (SURVEY §8(b) interchange format; the CPU oracle
+ * writes it, oracle.Hierarchy.export): the solve then runs on exactly those
+ * operators, maps and lambda-hats (parity isolation; checkpoint / resume of a
+ * setup).  Directory layout, little-endian raw arrays + flat JSON:
+ *   meta.json            {"format": "lap-hierarchy-v1", "nlev": L, "n0": n, ...}
+ *   perm.i64             n: internal (level-0) id of caller vertex i (Pi_rand)
+ *   L<l>/meta.json       {"kind": 0 agg | 1 elim | 2 coarsest, "n", "nnz",
+ *                         "lambda" and "m" (kind 0)}
+ *   L<l>/row_ptr.i64 (n+1), col.i32 (nnz), w.f64 (nnz), d.f64 (n)
+ *   L<l>/agg.i32 (kind 0) | fmap.i32 (kind 1: C -> order-preserving coarse id,
+ *                         F -> -1 - slot, slots ascending) | coarse_pinv.f64
+ *                         (kind 2, n*n row-major L^+)
+ * Sizes are checked against meta.json and the level chain (n_{l+1} = m or
+ * n - |F|; the last level, and only it, is the coarsest); any mismatch or
+ * unreadable file -> LAP_EINVAL.  p: solve parameters (cheby_lo/hi, cycle,
+ * use_graphs, tol, max_iters); the setup parameters are not used. */
+lap_status lap_import_hierarchy(const char *dir, const lap_params *p, void *cuda_stream, lap_hierarchy **out);
+
 /* Device memory: liblap allocates from a stream-ordered pool of its own (never
  * the device's default pool, so PyTorch's caching allocator and NCCL are not
  * starved).  When the last live hierarchy is freed the pool is trimmed down to

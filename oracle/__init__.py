@@ -9,6 +9,7 @@ computes.
 from __future__ import annotations
 
 import ctypes
+import json
 import os
 import subprocess
 from dataclasses import dataclass, field
@@ -410,6 +411,40 @@ class Hierarchy:
         else:
             ld.pinv = v(L.pinv, n * n, np.float64).reshape(n, n)
         return ld
+
+    def export(self, path: str) -> None:
+        """Write the hierarchy in the interchange format (SURVEY §8(b);
+        include/lap.h lap_import_hierarchy): meta.json, perm.i64, and per level
+        L<l>/meta.json, row_ptr.i64, col.i32, w.f64, d.f64 and agg.i32 /
+        fmap.i32 / coarse_pinv.f64 (little-endian raw arrays)."""
+        os.makedirs(path, exist_ok=True)
+        p = self.params
+        meta = {"format": "lap-hierarchy-v1", "producer": "oracle/lap_oracle.c", "nlev": self.nlev, "n0": self.n,
+                "params": {f: getattr(p, f) for f, _ in p._fields_}}
+        with open(os.path.join(path, "meta.json"), "w") as f:
+            json.dump(meta, f)
+        self.perm().astype("<i8").tofile(os.path.join(path, "perm.i64"))
+        for l in range(self.nlev):
+            L = self.level_view(l)
+            d = os.path.join(path, f"L{l}")
+            os.makedirs(d, exist_ok=True)
+            lm = {"kind": L.kind, "n": L.n, "nnz": L.nnz}
+            if L.kind == AGG:
+                lm.update(**{"lambda": float(L.lam), "m": int(L.m)})
+            elif L.kind == ELIM:
+                lm["nF"] = int(L.nF)
+            with open(os.path.join(d, "meta.json"), "w") as f:
+                json.dump(lm, f)
+            L.row_ptr.astype("<i8").tofile(os.path.join(d, "row_ptr.i64"))
+            L.col.astype("<i4").tofile(os.path.join(d, "col.i32"))
+            L.w.astype("<f8").tofile(os.path.join(d, "w.f64"))
+            L.d.astype("<f8").tofile(os.path.join(d, "d.f64"))
+            if L.kind == AGG:
+                L.agg.astype("<i4").tofile(os.path.join(d, "agg.i32"))
+            elif L.kind == ELIM:
+                L.fmap.astype("<i4").tofile(os.path.join(d, "fmap.i32"))
+            else:
+                L.pinv.astype("<f8").tofile(os.path.join(d, "coarse_pinv.f64"))
 
     def vcycle(self, l: int, b) -> np.ndarray:
         n = self.level(l).n

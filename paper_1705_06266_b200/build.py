@@ -26,7 +26,8 @@ UNITS = {"setup.cu": ["-fmad=false", "-prec-div=true", "-prec-sqrt=true"],
          "tail.cu": [],
          "ktail.cu": [],
          "block.cu": [],
-         "bench_hooks.cu": []}
+         "bench_hooks.cu": [],
+         "xt.cu": []}
 
 
 def _sources():

@@ -188,7 +188,7 @@ void finalize_solve_structures(lap_hierarchy *h, cudaStream_t s) {
 static void free_level(Level &L, cudaStream_t s) {
     void *ps[] = {L.row_ptr, L.col, L.w, L.d, L.agg, L.S, L.fmap, L.cid, L.fid, L.ct_ptr, L.ct_f, L.ct_coef,
                   L.pinv, L.sid, L.spos, L.srp, L.scol, L.sw, L.sd, L.slice_ptr, L.ell_col, L.ell_w, L.chunk_row, L.chunk_idx, L.chunk_slot, L.chunk_cnt,
-                  L.chunk_part, L.ell_col16, L.scol16,
+                  L.chunk_part, L.ell_col16, L.scol16, L.xt_rb, L.xt_seg, L.xt_wo, L.xt_rc, L.xt_w,
                   L.agg_s, L.mem_ptr, L.members, L.cid_s, L.flist, L.ct_ptr_s, L.ct_f_s, L.ct_coef_s, L.fmap_s,
                   L.ct_crow, L.ct_cidx, L.ct_cslot, L.ct_ccnt, L.ct_cpart,
                   L.pinv_s, L.dense, L.dense_part, L.dense_cnt, L.b, L.x, L.x2, L.t, L.r, L.dv, L.kp, L.kq, L.kz,
@@ -377,12 +377,29 @@ void lap_pool_retain(uint64_t bytes) {
 }
 const char *lap_version(void) { return "liblap 0.1 (sm_100a)"; }
 
+static lap_status setup_common(const lap_graph *g, const char *dir, const lap_params *pp, void *stream,
+                               lap_hierarchy **out);
+
 lap_status lap_setup(const lap_graph *g, const lap_params *pp, void *stream, lap_hierarchy **out) {
     if (out) *out = nullptr;
     if (!g || !out || g->n < 1 || !g->row_ptr || (g->row_ptr && !g->col && g->n > 1)) {
         lap::set_error("lap_setup: invalid arguments");
         return LAP_EINVAL;
     }
+    return setup_common(g, nullptr, pp, stream, out);
+}
+
+lap_status lap_import_hierarchy(const char *dir, const lap_params *pp, void *stream, lap_hierarchy **out) {
+    if (out) *out = nullptr;
+    if (!dir || !out) {
+        lap::set_error("lap_import_hierarchy: invalid arguments");
+        return LAP_EINVAL;
+    }
+    return setup_common(nullptr, dir, pp, stream, out);
+}
+
+static lap_status setup_common(const lap_graph *g, const char *dir, const lap_params *pp, void *stream,
+                               lap_hierarchy **out) {
     lap_params p;
     if (pp) p = *pp;
     else lap_params_default(&p);
@@ -408,7 +425,8 @@ lap_status lap_setup(const lap_graph *g, const lap_params *pp, void *stream, lap
         int64_t kl0 = lap::g_kl;
         h->npartials = 1024;  // reduction scratch used during setup (Lanczos dots)
         h->partials = (double *)lap::dalloc(8 * h->npartials, s);
-        lap::build_hierarchy(h, g, s);
+        if (g) lap::build_hierarchy(h, g, s);
+        else lap::import_hierarchy(h, dir, s);
         lap::finalize_solve_structures(h, s);
         lap::build_dense_tail(h, s);
         lap::build_ktail(h, s);

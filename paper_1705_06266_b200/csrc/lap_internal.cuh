@@ -152,6 +152,15 @@ struct Level {
     int32_t *chunk_slot = nullptr;  // chunk -> arrival counter slot (-1: one-chunk row)
     int32_t *chunk_cnt = nullptr;   // n - c_end[0] arrival counters (kept at 0 between launches)
     double *chunk_part = nullptr;
+    // column-tiled "x-stationary" layout (xt.cu): dense-ish levels too big for x
+    // in shared memory; a CTA owns a row block and sweeps x tile by tile
+    bool xt = false;
+    int xt_nb = 0, xt_T = 0, xt_W = 0, xt_rmax = 0;  // row blocks, tiles, tile width (doubles), max rows per block
+    int64_t *xt_rb = nullptr;       // nb+1 storage-row boundaries of the row blocks
+    int64_t *xt_seg = nullptr;      // nb*T+1 start of segment (block, tile) (global entry index)
+    int32_t *xt_wo = nullptr;       // nb*T*(XT_NW+1) warp offsets inside each segment
+    uint32_t *xt_rc = nullptr;      // nnz: (local row << 16) | local column
+    double *xt_w = nullptr;         // nnz
     // transfer maps in storage space
     int32_t *agg_s = nullptr;       // agg: coarse storage index of each fine storage row
     int64_t *mem_ptr = nullptr;     // agg: coarse storage index -> members (m+1)
@@ -223,6 +232,7 @@ namespace lap {
 // ---------------------------------------------------------------- kernels (host launchers)
 // setup (setup.cu)
 void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s);
+void import_hierarchy(lap_hierarchy *h, const char *dir, cudaStream_t s);
 void finalize_solve_structures(lap_hierarchy *h, cudaStream_t s);
 
 // solve (solve.cu)
@@ -241,6 +251,10 @@ void spmv_level(lap_hierarchy *h, const Level &L, EpiKind kind, const EpiArgs &a
 // storage (storage.cu)
 void build_storage(lap_hierarchy *h, int l, cudaStream_t s);
 void build_transfers(lap_hierarchy *h, cudaStream_t s);
+// column-tiled SpMV layout (xt.cu)
+constexpr int XT_NW = 16;             // warps per CTA (512 threads)
+bool xt_eligible(const Level &L, int l);
+void build_xt(Level &L, cudaStream_t s);
 // LCHUNK work items over the rows [row0, row0+nrows) of a CSR longer than minlen
 int64_t build_chunks(const int64_t *rp, int64_t row0, int64_t nrows, int64_t minlen, int32_t **crow, int32_t **cidx,
                      int32_t **cslot, double **cpart, int32_t **ccnt, cudaStream_t s);

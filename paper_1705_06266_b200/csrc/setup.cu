@@ -13,7 +13,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <ctime>
+#include <string>
+#include <vector>
 
 #include "canon.cuh"
 #include "lap_internal.cuh"
@@ -1786,6 +1789,7 @@ static int64_t elim_select(lap_hierarchy *h, Level &L, DBuf<uint8_t> &F, cudaStr
     return (int64_t)d2h_scalar(nF.p, s);
 }
 
+static void build_ct_lists(Level &L, const uint8_t *Fp, int64_t nc, cudaStream_t s);
 static void build_elim_level(lap_hierarchy *h, Level &L, const DBuf<uint8_t> &F, int64_t nF, Level &N,
                              cudaStream_t s) {
     int64_t n = L.n, nc = n - nF;
@@ -1817,8 +1821,16 @@ static void build_elim_level(lap_hierarchy *h, Level &L, const DBuf<uint8_t> &F,
         const int cb = bitlen_u64((uint64_t)(nc > 0 ? nc : 1));
         csr_from_source(S, nc, nc, cb, ilogb_pos(L.maxw) + 1, 4 * L.nnz, true, N, s);
     }
-    // transposed L_FC for the restriction P^T b
+    build_ct_lists(L, F.p, nc, s);
+    h->cur.edges += L.nnz;
+}
+
+// transposed L_FC for the restriction P^T b: per C vertex its F neighbours and
+// w_fc / d_f (logical numbering)
+static void build_ct_lists(Level &L, const uint8_t *Fp, int64_t nc, cudaStream_t s) {
+    const int64_t n = L.n;
     const int G = group_size(n, L.nnz);
+    struct { const uint8_t *p; } F{Fp};
     DBuf<int64_t> tc(nc + 1, s);
     LAP_CUDA(cudaMemsetAsync(tc.p, 0, sizeof(int64_t) * (nc + 1), s));
     LAUNCH_G(G, k_ct_count, nc, s, nc, L.cid, L.row_ptr, L.col, F.p, tc.p);
@@ -1829,7 +1841,6 @@ static void build_elim_level(lap_hierarchy *h, Level &L, const DBuf<uint8_t> &F,
     L.ct_coef = (double *)dalloc(sizeof(double) * (TT + 1), s);
     LAUNCH_G(G, k_ct_fill, nc, s, nc, L.cid, L.row_ptr, L.col, L.w, L.d, F.p, L.ct_ptr, L.ct_f, L.ct_coef);
     LAP_CHECK_LAUNCH();
-    h->cur.edges += L.nnz;
 }
 
 // strength + voting for one attempt; returns m, fills L.agg
@@ -2215,6 +2226,152 @@ void random_stream(int which, uint64_t seed, int level, int attempt, int64_t n, 
     else k_probe_mix<<<g, 256, 0, s>>>(n, buf.p);
     LAP_CHECK_LAUNCH();
     LAP_CUDA(cudaMemcpyAsync(out, buf.p, 8 * (size_t)cnt, cudaMemcpyDeviceToHost, s));
+    LAP_CUDA(cudaStreamSynchronize(s));
+}
+
+// =========================================================================
+// lap_import_hierarchy: a hierarchy given as files (SURVEY §8(b) interchange
+// format, written by the oracle's export): the GPU solve runs on exactly the
+// operators, maps and lambda-hat of another implementation.
+// =========================================================================
+static std::string read_text(const std::string &fn) {
+    FILE *f = fopen(fn.c_str(), "rb");
+    if (!f) throw Error{LAP_EINVAL, "import: cannot open " + fn};
+    std::string t;
+    char buf[4096];
+    size_t k;
+    while ((k = fread(buf, 1, sizeof(buf), f)) > 0) t.append(buf, k);
+    fclose(f);
+    return t;
+}
+// the number after "key": in a flat JSON object
+static double json_num(const std::string &js, const char *key, bool required, double dflt = 0.0) {
+    const std::string k = std::string("\"") + key + "\"";
+    size_t p = js.find(k);
+    if (p == std::string::npos) {
+        if (required) throw Error{LAP_EINVAL, std::string("import: meta.json lacks ") + key};
+        return dflt;
+    }
+    p = js.find(':', p + k.size());
+    if (p == std::string::npos) throw Error{LAP_EINVAL, std::string("import: bad value of ") + key};
+    const char *c = js.c_str() + p + 1;
+    char *end = nullptr;
+    const double v = strtod(c, &end);
+    if (end == c) throw Error{LAP_EINVAL, std::string("import: bad value of ") + key};
+    return v;
+}
+template <class T>
+static std::vector<T> read_raw(const std::string &fn, int64_t count) {
+    FILE *f = fopen(fn.c_str(), "rb");
+    if (!f) throw Error{LAP_EINVAL, "import: cannot open " + fn};
+    fseek(f, 0, SEEK_END);
+    const long long sz = ftell(f);
+    fseek(f, 0, SEEK_SET);
+    if (sz != (long long)(count * (int64_t)sizeof(T))) {
+        fclose(f);
+        throw Error{LAP_EINVAL, "import: " + fn + " has " + std::to_string(sz) + " bytes, expected " +
+                                    std::to_string(count * (int64_t)sizeof(T))};
+    }
+    std::vector<T> v((size_t)count);
+    if (count > 0 && fread(v.data(), sizeof(T), (size_t)count, f) != (size_t)count) {
+        fclose(f);
+        throw Error{LAP_EINVAL, "import: short read of " + fn};
+    }
+    fclose(f);
+    return v;
+}
+template <class T>
+static T *to_dev(const std::vector<T> &v, cudaStream_t s) {
+    T *p = (T *)dalloc(sizeof(T) * (v.size() ? v.size() : 1), s);
+    if (!v.empty()) h2d(p, v.data(), (int64_t)v.size(), s);
+    return p;
+}
+__global__ void k_fmap_split(int64_t n, const int32_t *fmap, int32_t *cid, int32_t *fid, uint8_t *F) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t f = fmap[i];
+        F[i] = f < 0;
+        if (f < 0) fid[-1 - f] = (int32_t)i;
+        else cid[f] = (int32_t)i;
+    }
+}
+
+void import_hierarchy(lap_hierarchy *h, const char *dir, cudaStream_t s) {
+    const std::string D(dir);
+    const std::string meta = read_text(D + "/meta.json");
+    if (meta.find("lap-hierarchy-v1") == std::string::npos) throw Error{LAP_EINVAL, "import: not a lap-hierarchy-v1 directory"};
+    const int nlev = (int)json_num(meta, "nlev", true);
+    const int64_t n0 = (int64_t)json_num(meta, "n0", true);
+    if (nlev < 1 || nlev > 64 || n0 < 1 || n0 >= ((int64_t)1 << 31)) throw Error{LAP_EINVAL, "import: bad nlev / n0"};
+    h->n0 = n0;
+    {
+        std::vector<int64_t> perm = read_raw<int64_t>(D + "/perm.i64", n0);
+        std::vector<char> seen((size_t)n0, 0);
+        for (int64_t i = 0; i < n0; i++) {
+            if (perm[i] < 0 || perm[i] >= n0 || seen[perm[i]]) throw Error{LAP_EINVAL, "import: perm is not a permutation"};
+            seen[perm[i]] = 1;
+        }
+        h->perm = to_dev(perm, s);
+    }
+    h->lev.clear();
+    h->lev.reserve(64);
+    int64_t expect_n = n0;
+    for (int l = 0; l < nlev; l++) {
+        const std::string P = D + "/L" + std::to_string(l);
+        const std::string lm = read_text(P + "/meta.json");
+        h->lev.emplace_back();
+        Level &L = h->lev.back();
+        L.kind = (int)json_num(lm, "kind", true);
+        L.n = (int64_t)json_num(lm, "n", true);
+        L.nnz = (int64_t)json_num(lm, "nnz", true);
+        if (L.kind < 0 || L.kind > 2 || L.n != expect_n || L.nnz < 0 || (L.kind == KIND_COARSEST) != (l == nlev - 1))
+            throw Error{LAP_EINVAL, "import: level " + std::to_string(l) + " has an inconsistent kind or size"};
+        std::vector<int64_t> rp = read_raw<int64_t>(P + "/row_ptr.i64", L.n + 1);
+        if (rp[0] != 0 || rp[L.n] != L.nnz) throw Error{LAP_EINVAL, "import: bad row_ptr at level " + std::to_string(l)};
+        for (int64_t i = 0; i < L.n; i++)
+            if (rp[i + 1] < rp[i]) throw Error{LAP_EINVAL, "import: row_ptr not monotone"};
+        std::vector<int32_t> col = read_raw<int32_t>(P + "/col.i32", L.nnz);
+        for (int64_t k = 0; k < L.nnz; k++)
+            if (col[k] < 0 || col[k] >= L.n) throw Error{LAP_EINVAL, "import: column out of range"};
+        L.row_ptr = to_dev(rp, s);
+        L.col = to_dev(col, s);
+        L.w = to_dev(read_raw<double>(P + "/w.f64", L.nnz), s);
+        L.d = to_dev(read_raw<double>(P + "/d.f64", L.n), s);
+        L.maxw = max_abs(L.w, L.nnz, s);
+        L.maxdeg = max_degree(L.n, L.row_ptr, s);
+        if (L.kind == KIND_AGG) {
+            L.lambda = json_num(lm, "lambda", true);
+            L.m = (int64_t)json_num(lm, "m", true);
+            std::vector<int32_t> agg = read_raw<int32_t>(P + "/agg.i32", L.n);
+            for (int64_t i = 0; i < L.n; i++)
+                if (agg[i] < 0 || agg[i] >= L.m) throw Error{LAP_EINVAL, "import: aggregate id out of range"};
+            L.agg = to_dev(agg, s);
+            expect_n = L.m;
+        } else if (L.kind == KIND_ELIM) {
+            std::vector<int32_t> fmap = read_raw<int32_t>(P + "/fmap.i32", L.n);
+            int64_t nF = 0, nc = 0;
+            for (int64_t i = 0; i < L.n; i++) {
+                if (fmap[i] < 0) {
+                    if (-1 - fmap[i] != nF) throw Error{LAP_EINVAL, "import: F slots not in ascending order"};
+                    nF++;
+                } else {
+                    if (fmap[i] != nc) throw Error{LAP_EINVAL, "import: C numbering not order-preserving"};
+                    nc++;
+                }
+            }
+            L.nF = nF;
+            L.fmap = to_dev(fmap, s);
+            L.cid = (int32_t *)dalloc(sizeof(int32_t) * (size_t)(nc + 1), s);
+            L.fid = (int32_t *)dalloc(sizeof(int32_t) * (size_t)(nF + 1), s);
+            DBuf<uint8_t> F(L.n, s);
+            k_fmap_split<<<grid_for(L.n, 256, 148 * 8), 256, 0, s>>>(L.n, L.fmap, L.cid, L.fid, F.p); ++g_kl;
+            LAP_CHECK_LAUNCH();
+            build_ct_lists(L, F.p, nc, s);
+            expect_n = nc;
+        } else {
+            L.pinv = to_dev(read_raw<double>(P + "/coarse_pinv.f64", L.n * L.n), s);
+        }
+    }
+    for (int l = 0; l < nlev; l++) build_storage(h, l, s);
     LAP_CUDA(cudaStreamSynchronize(s));
 }
 

@@ -331,6 +331,125 @@ __global__ void __launch_bounds__(1024, 1) k_spmv_smem(int64_t n, int64_t nslice
     }
 }
 
+// Column-tiled ("x-stationary") SpMV of a dense-ish level (xt.cu has the
+// layout and the rationale): CTA = row block, tiles of x streamed through
+// shared memory by TMA bulk copies (double-buffered, mbarrier completion),
+// warps own row ranges and accumulate segmented warp sums into shared y.
+struct XtArgs {
+    int nb, T, W, rmax;
+    int64_t n;
+    const int64_t *__restrict__ rb;
+    const int64_t *__restrict__ seg;
+    const int32_t *__restrict__ wo;
+    const uint32_t *__restrict__ rc;
+    const double *__restrict__ w;
+};
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+// one thread: x[t W .. t W + cnt) (cnt even, 16-byte aligned) -> dst, completion on bar
+__device__ __forceinline__ void xt_issue(double *dst, const double *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the buffer's previous readers are done (WAR)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+template <int EPI>
+__global__ void __launch_bounds__(XT_NW * 32, 1) k_spmv_xt(XtArgs X, Csr A, EpiArgs a, double *__restrict__ partials) {
+    extern __shared__ __align__(16) double xsm[];
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ double sh[32];
+    pdl_begin();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double *xs[2] = {xsm, xsm + X.W};
+    double *ys = xsm + 2 * X.W;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t par[2] = {0u, 0u};
+    Dacc dacc;
+    const double *__restrict__ xg = a.x;
+    auto issue = [&](int t, int buf) {
+        const int64_t c0 = (int64_t)t * X.W;
+        const int64_t cnt = min((int64_t)X.W, X.n - c0) & ~(int64_t)1;  // an odd last element is read from global
+        if (cnt > 0) xt_issue(xs[buf], xg + c0, (uint32_t)(cnt * 8), &bar[buf]);
+        else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar[buf])) : "memory");
+    };
+    for (int b = blockIdx.x; b < X.nb; b += gridDim.x) {
+        const int64_t r0 = X.rb[b], nr = X.rb[b + 1] - r0;
+        for (int64_t i = tid; i < nr; i += blockDim.x) ys[i] = 0.0;
+        if (tid == 0) {
+            issue(0, 0);
+            if (X.T > 1) issue(1, 1);
+        }
+        __syncthreads();
+        for (int t = 0; t < X.T; t++) {
+            const int buf = t & 1;
+            mbar_wait(&bar[buf], par[buf]);
+            par[buf] ^= 1u;
+            const double *__restrict__ xt = xs[buf];
+            const int64_t c0 = (int64_t)t * X.W;
+            const int64_t tl = min((int64_t)X.W, X.n - c0), tle = tl & ~(int64_t)1;
+            const int64_t sb = ((int64_t)b * X.T + t);
+            const int64_t s0 = X.seg[sb];
+            const int32_t *wo = X.wo + sb * (XT_NW + 1);
+            const int64_t e0 = s0 + wo[warp], e1 = s0 + wo[warp + 1];
+            for (int64_t e = e0; e < e1; e += 32) {
+                const int64_t q = e + lane;
+                const bool valid = q < e1;
+                const uint32_t rcw = valid ? __ldcs(X.rc + q) : 0xFFFF0000u;
+                const int r = (int)(rcw >> 16), c = (int)(rcw & 0xFFFF);
+                double v = 0.0;
+                if (valid) v = __ldcs(X.w + q) * (c < tle ? xt[c] : xg[c0 + c]);
+                // segmented inclusive scan over runs of equal local rows (ascending in the warp's range)
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double tv = __shfl_up_sync(0xffffffffu, v, o);
+                    const int tr = __shfl_up_sync(0xffffffffu, r, o);
+                    if (lane >= o && tr == r) v += tv;
+                }
+                const int rn = __shfl_down_sync(0xffffffffu, r, 1);
+                if (valid && (lane == 31 || rn != r)) ys[r] += v;
+            }
+            __syncthreads();  // tile consumed, y updates visible
+            if (tid == 0 && t + 2 < X.T) issue(t + 2, buf);
+        }
+        for (int64_t i = tid; i < nr; i += blockDim.x) apply_epi<EPI>(r0 + i, ys[i], A, a, dacc);
+        __syncthreads();
+    }
+    if (EPI == E_DOT || EPI == E_LZ || EPI == E_FCG) {
+        double r = block_sum(dacc.a, sh);
+        if (threadIdx.x == 0) partials[blockIdx.x] = r;
+    }
+    if (EPI == E_FCG || EPI == E_CHEBZ) {
+        double r = block_sum(EPI == E_CHEBZ ? dacc.a : dacc.b, sh);
+        if (threadIdx.x == 0) partials[(EPI == E_CHEBZ ? 0 : 1) * gridDim.x + blockIdx.x] = r;
+    }
+    if (EPI == E_CHEBZ) {
+        double r1 = block_sum(dacc.b, sh), r2 = block_sum(dacc.c, sh);
+        if (threadIdx.x == 0) {
+            partials[gridDim.x + blockIdx.x] = r1;
+            partials[2 * gridDim.x + blockIdx.x] = r2;
+        }
+    }
+}
+
 static int num_sms() {
     static int v = 0;
     if (!v) {
@@ -345,6 +464,7 @@ static int num_sms() {
 // fixed launch geometry per level (deterministic partial slots for E_DOT)
 static unsigned spmv_grid(const Level &L) {
     if (L.smem_x) return (unsigned)num_sms();
+    if (L.xt) return (unsigned)std::min(L.xt_nb, num_sms());
     if (L.spmv_vec) return grid_for(L.n * L.spmv_vec, 256, (int64_t)num_sms() * 8);
     int64_t items = L.nslices + L.nchunks;
     // one resident wave: 4 CTAs of 256 per SM at 64 registers (NB 8), 5 at NB 4 (48 registers)
@@ -404,6 +524,19 @@ static void spmv_dispatch(lap_hierarchy *h, const Level &L, const EpiArgs &a, cu
         return;
     }
     LongRows R{L.nchunks, L.chunk_row, L.chunk_idx, L.chunk_slot, L.chunk_part, L.chunk_cnt};
+    if (L.xt && ((uintptr_t)a.x & 15) == 0) {  // (the bulk copy needs a 16-byte aligned x; level vectors are)
+        static bool attr_set = false;
+        const size_t smem = 8 * (size_t)(2 * L.xt_W + L.xt_rmax);
+        if (!attr_set) {
+            LAP_CUDA(cudaFuncSetAttribute(k_spmv_xt<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+            attr_set = true;
+        }
+        XtArgs X{L.xt_nb, L.xt_T, L.xt_W, L.xt_rmax, L.n, L.xt_rb, L.xt_seg, L.xt_wo, L.xt_rc, L.xt_w};
+        launch_pdl_smem(k_spmv_xt<EPI>, spmv_grid(L), XT_NW * 32, smem, s, X, A, a, a.partials);
+        h->cur.launches++;
+        LAP_CHECK_LAUNCH();
+        return;
+    }
     if (L.smem_x) {
         static bool attr_set = false;
         if (!attr_set) {

@@ -435,6 +435,8 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
     L.nchunks = build_chunks(L.srp, L.c_end[0], n - L.c_end[0], SHORT_MAX, &L.chunk_row, &L.chunk_idx, &L.chunk_slot,
                              &L.chunk_part, &L.chunk_cnt, s);
     LAP_CHECK_LAUNCH();
+    // dense-ish level too big for x in shared memory: the column-tiled layout (xt.cu)
+    if (xt_eligible(L, l)) build_xt(L, s);
 }
 
 // ---------------------------------------------------------------- transfer maps

@@ -55,7 +55,7 @@ EXPORTS = [
     "lap_perm", "lap_spmv", "lap_vcycle", "lap_kcycle", "lap_solve_block", "lap_get_stats", "lap_bench_op",
     "lap_nccl_unique_id", "lap_comm_create", "lap_comm_create_virtual", "lap_comm_info", "lap_comm_free",
     "lap_setup_dist", "lap_dist_index", "lap_pool_retain", "lap_random_stream",
-    "lap_bench_gather", "lap_level_rows",
+    "lap_bench_gather", "lap_level_rows", "lap_import_hierarchy",
 ]
 
 
@@ -96,6 +96,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "lap_random_stream": (ctypes.c_int, [i32, ctypes.c_uint64, i32, i32, i64, P, P]),
         "lap_bench_gather": (ctypes.c_int, [i64, i64, i32, P, P]),
         "lap_level_rows": (ctypes.c_int, [P, i32, i64, P, P, P, P]),
+        "lap_import_hierarchy": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(lap_params), P, ctypes.POINTER(P)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -265,6 +266,20 @@ class Hierarchy:
         self.status = _check(rc, allow=(LAP_ESTALL,))
         self._keep = None
         self.n = n
+
+    @classmethod
+    def import_dir(cls, path: str, params: lap_params | None = None, stream=None, **kw) -> "Hierarchy":
+        """lap_import_hierarchy: a hierarchy from the interchange directory."""
+        self = cls.__new__(cls)
+        self.params = params if params is not None else lap_params_default(**kw)
+        self._h = ctypes.c_void_p()
+        self.comm = None
+        self._keep = None
+        rc = lib().lap_import_hierarchy(os.fsencode(path), ctypes.byref(self.params), _stream(stream),
+                                        ctypes.byref(self._h))
+        self.status = _check(rc, allow=(LAP_ESTALL,))
+        self.n = self.level_info(0)[1]
+        return self
 
     def close(self):
         if getattr(self, "_h", None):

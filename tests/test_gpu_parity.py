@@ -231,9 +231,11 @@ def test_storage_layout_validated_in_debug_mode(P):
 
 @pytest.mark.parametrize("env", [{"LAP_DENSE_TAIL": "0"}, {"LAP_PDL": "0"}, {"LAP_FUSE_TRANSFERS": "0"},
                                  {"LAP_FUSE_ZSUMS": "0"}, {"LAP_SPMV_VEC": "0"}, {"LAP_SPMV_VEC": "16"},
-                                 {"LAP_DENSE_TAIL": "0", "LAP_PDL": "0", "LAP_FUSE_TRANSFERS": "0", "LAP_FUSE_ZSUMS": "0"}],
+                                 {"LAP_DENSE_TAIL": "0", "LAP_PDL": "0", "LAP_FUSE_TRANSFERS": "0", "LAP_FUSE_ZSUMS": "0"},
+                                 {"LAP_XT": "force", "LAP_XT_W": "64"}, {"LAP_XT": "force", "LAP_XT_W": "1000", "LAP_XT_NB": "300"},
+                                 {"LAP_XT": "0"}],
                          ids=["no-dense-tail", "no-pdl", "no-fused-transfers", "no-fused-zsums", "sell-only",
-                              "vec16-everywhere", "none"])
+                              "vec16-everywhere", "none", "xt-forced-w64", "xt-forced-nb300", "no-xt"])
 def test_solve_path_switches(P, env):
     """The alternative solve paths (per-level kernels instead of the dense
     tail operator, launches without programmatic dependent launch) give the
@@ -321,3 +323,38 @@ def test_memory_lean_paths_bit_exact(P):
         e = dict(os.environ, **env)
         r = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, timeout=900, cwd=root)
         assert r.returncode == 0 and "ok" in r.stdout, (env, r.stderr[-3000:])
+
+
+@pytest.mark.parametrize("env", [{"LAP_XT": "force", "LAP_XT_W": "64"},
+                                 {"LAP_XT": "force", "LAP_XT_W": "2", "LAP_XT_NB": "3"},
+                                 {"LAP_XT": "force", "LAP_XT_W": "1000", "LAP_XT_NB": "300"},
+                                 {"LAP_XT": "force", "LAP_XT_W": "777"}],
+                         ids=["w64", "w2-nb3", "w1000-nb300", "w777-odd-tiles"])
+def test_column_tiled_spmv_per_entry(P, env):
+    """The column-tiled (x-stationary) SpMV (xt.cu), forced on every level with
+    a few hundred rows, with tiny tiles (many tiles, odd tile lengths), few or
+    many row blocks: every entry of L_l x within the O-P2 bound of the oracle,
+    every epilogue through the V-cycle and solve."""
+    import os
+    import subprocess
+    import sys
+    code = ("import numpy as np, lapgen, oracle, paper_1705_06266_b200 as P\n"
+            "from tests.test_gpu_parity import spmv_bound\n"
+            "for g in [lapgen.rmat(12), lapgen.barabasi_albert(6000, 8), lapgen.random_connected(3000, 60000, 3)]:\n"
+            "    h = P.Hierarchy(g); ho = oracle.Hierarchy(g)\n"
+            "    rng = np.random.default_rng(0)\n"
+            "    for l in range(ho.nlev):\n"
+            "        o = ho.level(l); x = rng.standard_normal(o.n)\n"
+            "        y = h.spmv(l, x); yo = oracle.spmv(o.n, o.row_ptr, o.col, o.w, o.d, x)\n"
+            "        assert np.all(np.abs(y - yo) <= spmv_bound(o.row_ptr, o.col, o.w, o.d, x) + 1e-300), l\n"
+            "    r = rng.standard_normal(g.n); r -= r.mean()\n"
+            "    z = h.vcycle(r); zo = ho.vcycle(0, r)\n"
+            "    assert np.abs(z - zo).max() <= 1e-9 * np.abs(zo).max()\n"
+            "    b = lapgen.rhs(g.n); x, it, rr, rc = h.solve(b); xo, ito, _, _ = ho.solve(b)\n"
+            "    assert rc == 0 and rr <= 1e-8 and abs(it - ito) <= 1, (it, ito, rr)\n"
+            "    x2, it2, _, _ = h.solve(b); assert it2 == it and x2.tobytes() == x.tobytes()\n"
+            "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, timeout=900, cwd=root)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
