@@ -1032,6 +1032,21 @@ __global__ void k_tv_init(int64_t n, uint64_t base, double *X) {
         X[t] = __dsub_rn(__dmul_rn(2.0, unit_from(mix64(base ^ (uint64_t)t))), 1.0);
 }
 
+// X0 in the storage order: Xs[4p+k] = X0[sid[p], k] (the counter is the logical id, O-R7/O-R33)
+__global__ void k_tv_init_s(int64_t n, uint64_t base, const int32_t *__restrict__ sid, double *__restrict__ X) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < 4 * n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = t >> 2, k = t & 3;
+        const uint64_t c = 4 * (uint64_t)sid[p] + (uint64_t)k;
+        X[t] = __dsub_rn(__dmul_rn(2.0, unit_from(mix64(base ^ c))), 1.0);
+    }
+}
+__global__ void k_tv_unpermute(int64_t n, const int32_t *__restrict__ sid, const double *__restrict__ Xs,
+                               double *__restrict__ X) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < 4 * n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = t >> 2, k = t & 3;
+        X[4 * (int64_t)sid[p] + k] = Xs[t];
+    }
+}
 // E_lo of a sweep's CanonSum instance from the bit pattern of max |x| (O-S11)
 __global__ void k_tv_elo(const unsigned long long *mxbits, int ew, int64_t K, int *elo) {
     double mx = __longlong_as_double((long long)*mxbits);
@@ -1556,6 +1571,165 @@ __global__ void k_lzc_chunk(int64_t nchunks, const int32_t *__restrict__ crow, c
         }
     }
 }
+// ---- canonical SpMV over the SOLVE STORAGE (SELL slices | long-row chunks):
+// the same order-independent CanonSum per row as the logical-CSR kernels above,
+// but in the storage order (locality of the caller's numbering, coalesced
+// SELL loads, hub rows in 1024-entry warp chunks): NC = 1 (Lanczos, x = u) or
+// 4 (test-vector sweep, x = the n x 4 block).  Any order gives the same bits.
+enum { CS_LANCZOS = 0, CS_SWEEP = 1 };
+struct CStore {
+    int64_t nslices, nshort, nchunks;
+    const int64_t *__restrict__ slice_ptr;
+    const int32_t *__restrict__ ell_col;
+    const double *__restrict__ ell_w;
+    const int64_t *__restrict__ srp;
+    const int32_t *__restrict__ scol;
+    const double *__restrict__ sw;
+    const double *__restrict__ sd;
+    const int32_t *__restrict__ crow, *__restrict__ cidx, *__restrict__ cslot;
+    int32_t *__restrict__ ccnt;
+    I128 *__restrict__ cpart;  // NC per chunk
+};
+struct CSweep {  // CS_SWEEP: x_new = x - omega ((d x - s) / d), per column
+    const double *__restrict__ X;
+    double *__restrict__ Xn;
+    const int *__restrict__ elo_p;
+    double omega;
+};
+template <int NC>
+__device__ __forceinline__ void cs_gather(const double *__restrict__ x, int64_t c, double wk, int elo, i128 *acc) {
+    if (NC == 1) {
+        acc[0] += canon_q(__dmul_rn(wk, x[c]), elo);
+    } else {
+        const double2 *xj = reinterpret_cast<const double2 *>(x + 4 * c);
+        const double2 u = xj[0], v = xj[1];
+        acc[0] += canon_q(__dmul_rn(wk, u.x), elo);
+        acc[1] += canon_q(__dmul_rn(wk, u.y), elo);
+        acc[2] += canon_q(__dmul_rn(wk, v.x), elo);
+        acc[3] += canon_q(__dmul_rn(wk, v.y), elo);
+    }
+}
+template <int NC, int MODE>
+__device__ __forceinline__ double cs_epilogue(int64_t p, const i128 *acc, int elo, const CStore &C,
+                                              const double *__restrict__ u, const double *__restrict__ rs,
+                                              const double *__restrict__ vp, double bprev, double *__restrict__ y,
+                                              const CSweep &W) {
+    if (MODE == CS_LANCZOS) return lzc_row_epilogue(p, canon_result(acc[0], elo), C.sd, u, rs, vp, bprev, y);
+    const double di = C.sd[p];
+#pragma unroll
+    for (int k = 0; k < NC; k++) {
+        const double sk = canon_result(acc[k], elo), xi = W.X[4 * p + k];
+        const double r = __dsub_rn(__dmul_rn(di, xi), sk);
+        W.Xn[4 * p + k] = __dsub_rn(xi, __dmul_rn(W.omega, __ddiv_rn(r, di)));
+    }
+    return 0.0;
+}
+template <int NC, int MODE>
+__global__ void __launch_bounds__(256) k_cspmv_store(CStore C, const double *__restrict__ x, const double *__restrict__ rs,
+                                                     const double *__restrict__ vp, int elo_fixed, LzState *st,
+                                                     double *__restrict__ y, CSweep W) {
+    if (MODE == CS_LANCZOS && st->stop) return;
+    const double bprev = MODE == CS_LANCZOS ? st->bprev : 0.0;
+    const int elo = MODE == CS_LANCZOS ? elo_fixed : *W.elo_p;
+    if (MODE == CS_LANCZOS && blockIdx.x == 0 && threadIdx.x == 0) {
+        st->acc_b.lo = 0;  // read by pass A only; pass A of this step has finished
+        st->acc_b.hi = 0;
+    }
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nitems = C.nslices + C.nchunks;
+    for (int64_t t = warp; t < nitems; t += nwarps) {
+        if (t < C.nslices) {  // SELL-32 slice: a thread per row, 8 independent loads per batch
+            const int64_t p = t * 32 + lane, beg = C.slice_ptr[t];
+            const int width = (int)((C.slice_ptr[t + 1] - beg) >> 5);
+            i128 acc[NC];
+#pragma unroll
+            for (int k = 0; k < NC; k++) acc[k] = 0;
+            for (int q = 0; q < width; q += 8) {
+                int cc[8];
+                double wv[8];
+#pragma unroll
+                for (int uu = 0; uu < 8; uu++) {
+                    cc[uu] = 0;
+                    wv[uu] = 0.0;
+                    if (q + uu < width) {
+                        cc[uu] = __ldg(&C.ell_col[beg + (int64_t)(q + uu) * 32 + lane]);
+                        wv[uu] = __ldg(&C.ell_w[beg + (int64_t)(q + uu) * 32 + lane]);
+                    }
+                }
+#pragma unroll
+                for (int uu = 0; uu < 8; uu++)
+                    if (q + uu < width) cs_gather<NC>(x, cc[uu], wv[uu], elo, acc);
+            }
+            double ya = 0.0;
+            if (p < C.nshort) ya = cs_epilogue<NC, MODE>(p, acc, elo, C, x, rs, vp, bprev, y, W);
+            if (MODE == CS_LANCZOS) warp_atomic_max(&st->maxy, ya);
+        } else {  // a 1024-entry chunk of a long row: warp-wide, int128 partials combined by the last arrival
+            const int64_t c = t - C.nslices;
+            const int64_t p = C.crow[c], j = C.cidx[c], rb = C.srp[p], re = C.srp[p + 1];
+            const int64_t b = rb + j * LCHUNK, e = min(re, b + LCHUNK);
+            i128 acc[NC];
+#pragma unroll
+            for (int k = 0; k < NC; k++) acc[k] = 0;
+            for (int64_t k = b + lane; k < e; k += 32) cs_gather<NC>(x, __ldg(&C.scol[k]), __ldg(&C.sw[k]), elo, acc);
+#pragma unroll
+            for (int k = 0; k < NC; k++) acc[k] = warp_sum_i128(acc[k]);
+            const int slot = C.cslot[c];
+            bool fin = slot < 0;
+            if (!fin) {
+                const int nch = (int)((re - rb + LCHUNK - 1) / LCHUNK);
+                int last = 0;
+                if (lane == 0) {
+                    for (int k = 0; k < NC; k++) C.cpart[NC * c + k] = to_I128(acc[k]);
+                    __threadfence();
+                    last = atomicAdd(&C.ccnt[slot], 1) == nch - 1;
+                }
+                last = __shfl_sync(0xffffffffu, last, 0);
+                if (last) {
+                    __threadfence();
+                    if (lane == 0) {
+                        for (int k = 0; k < NC; k++) acc[k] = 0;
+                        for (int64_t q = c - j; q < c - j + nch; q++)
+                            for (int k = 0; k < NC; k++) {
+                                I128 pv;
+                                pv.lo = __ldcg(&C.cpart[NC * q + k].lo);
+                                pv.hi = __ldcg(&C.cpart[NC * q + k].hi);
+                                acc[k] += from_I128(pv);
+                            }
+                        C.ccnt[slot] = 0;
+                    }
+                    fin = true;
+                }
+            }
+            if (fin && lane == 0) {
+                const double ya = cs_epilogue<NC, MODE>(p, acc, elo, C, x, rs, vp, bprev, y, W);
+                if (MODE == CS_LANCZOS) atomicMax(&st->maxy, (unsigned long long)__double_as_longlong(ya));
+            }
+        }
+    }
+}
+static CStore cstore_of(const Level &L, I128 *cpart) {
+    CStore C;
+    C.nslices = L.nslices;
+    C.nshort = L.c_end[0];
+    C.nchunks = L.nchunks;
+    C.slice_ptr = L.slice_ptr;
+    C.ell_col = L.ell_col;
+    C.ell_w = L.ell_w;
+    C.srp = L.srp;
+    C.scol = L.scol;
+    C.sw = L.sw;
+    C.sd = L.sd;
+    C.crow = L.chunk_row;
+    C.cidx = L.chunk_idx;
+    C.cslot = L.chunk_slot;
+    C.ccnt = L.chunk_cnt;
+    C.cpart = cpart;
+    return C;
+}
+static unsigned cstore_grid(const Level &L) { return grid_for((L.nslices + L.nchunks) * 32, 256, 148 * 8); }
+
 // pass C: acc_a += q(fl(y v))
 __global__ void __launch_bounds__(256) k_lzc_alpha(int64_t n, const double *__restrict__ y,
                                                    const double *__restrict__ v, LzState *st) {
@@ -1613,47 +1787,49 @@ __global__ void k_tridiag_max(const double *alpha, const double *beta, const int
     *out = hi;
 }
 
+// start vector and rs in the storage order (p holds logical vertex sid[p])
+__global__ void k_lzc_init_s(int64_t n, uint64_t base, const int32_t *__restrict__ sid, const double *__restrict__ sd,
+                             double *__restrict__ y, double *__restrict__ rs, double *__restrict__ vp, LzState *st,
+                             int elo) {
+    i128 acc = 0;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        const double v = lz_start_value(base, sid[p]);
+        y[p] = v;
+        vp[p] = 0.0;
+        rs[p] = __ddiv_rn(1.0, __dsqrt_rn(sd[p]));
+        acc += canon_q(__dmul_rn(v, v), elo);
+    }
+    block_add_i128(&st->acc_b, acc);
+}
+
+// lambda-hat on the level's solve storage (built before this is called): the
+// Lanczos vectors live in the storage order; every sum is a CanonSum, so the
+// order changes no bit (the tridiagonal equals the oracle's).
 static double lanczos(lap_hierarchy *h, Level &L, int l, cudaStream_t s) {
     const int64_t n = L.n, nnz = L.nnz;
     const int steps = h->p.lanczos_steps;
     DBuf<double> v(n, s), vp(n, s), y(n, s), u(n, s), rs(n, s), al(64, s), be(64, s), lam(1, s);
     DBuf<LzState> st(1, s);
     DBuf<int> kk(1, s);
+    DBuf<I128> cpart(L.nchunks > 0 ? L.nchunks : 1, s);
     LzState st0;
     std::memset(&st0, 0, sizeof(st0));
     st0.elo_b = canon_elo(1, n);
     LAP_CUDA(cudaMemcpyAsync(st.p, &st0, sizeof(st0), cudaMemcpyHostToDevice, s));
     const uint64_t base = mix64(salt_of(h->p.seed, 4) ^ (uint64_t)(2 * l));
     const unsigned g = grid_for(n, 256, 148 * 8);
-    k_lzc_init<<<g, 256, 0, s>>>(n, base, L.d, y.p, rs.p, vp.p, st.p, st0.elo_b); ++g_kl;
+    k_lzc_init_s<<<g, 256, 0, s>>>(n, base, L.sid, L.sd, y.p, rs.p, vp.p, st.p, st0.elo_b); ++g_kl;
     LAP_CHECK_LAUNCH();
     const int e_spmv = (L.maxw > 0.0 ? ilogb(L.maxw) : -1000) + [&] {
         const double mr = max_abs(rs.p, n, s);
         return mr > 0.0 ? ilogb(mr) : -1000;
     }() + 3;
     const int elo_spmv = canon_elo(e_spmv, nnz);
-    const int G = group_size(n, nnz, L.maxdeg <= SHORT_MAX);
-    int32_t *lc_row = nullptr, *lc_idx = nullptr, *lc_slot = nullptr, *lc_cnt = nullptr;
-    double *lc_dummy = nullptr;
-    const int64_t nlc = L.maxdeg <= SETUP_LONG ? 0
-                        : build_chunks(L.row_ptr, 0, n, SETUP_LONG, &lc_row, &lc_idx, &lc_slot, &lc_dummy, &lc_cnt, s);
-    struct FreeLc {
-        void *p[5];
-        cudaStream_t s;
-        ~FreeLc() {
-            for (void *q : p) dfree(q, s);
-        }
-    } free_lc{{lc_row, lc_idx, lc_slot, lc_cnt, lc_dummy}, s};
-    DBuf<I128> lc_part(nlc > 0 ? nlc : 1, s);
+    const CStore C = cstore_of(L, cpart.p);
+    const CSweep W{};
     for (int j = 0; j < steps && j < 64; j++) {
         k_lzc_next<<<g, 256, 0, s>>>(n, j == 0, 0, y.p, v.p, vp.p, u.p, rs.p, st.p, al.p, be.p); ++g_kl;
-        LAUNCH_G(G, k_lzc_spmv, n, s, n, L.row_ptr, L.col, L.w, L.d, u.p, rs.p, vp.p, elo_spmv, st.p, y.p);
-        if (nlc > 0) {
-            k_lzc_chunk<<<grid_for(nlc * 32, 256, 148 * 16), 256, 0, s>>>(nlc, lc_row, lc_idx, lc_slot, lc_cnt,
-                                                                          lc_part.p, L.row_ptr, L.col, L.w, L.d, u.p,
-                                                                          rs.p, vp.p, elo_spmv, st.p, y.p);
-            ++g_kl;
-        }
+        k_cspmv_store<1, CS_LANCZOS><<<cstore_grid(L), 256, 0, s>>>(C, u.p, rs.p, vp.p, elo_spmv, st.p, y.p, W); ++g_kl;
         k_lzc_alpha<<<g, 256, 0, s>>>(n, y.p, v.p, st.p); ++g_kl;
         k_lzc_update<<<g, 256, 0, s>>>(n, y.p, v.p, st.p); ++g_kl;
         LAP_CHECK_LAUNCH();
@@ -1849,10 +2025,11 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
     const lap_params &p = h->p;
     unsigned ge = grid_for(n, 256, 148 * 16);
     const int G = group_size(n, nnz, L.maxdeg <= SHORT_MAX);
-    // test vectors
+    // test vectors: swept on the solve storage (canonical sums:
+    // the order is free), then laid out in the logical order for the affinity
     DBuf<double> X(4 * n, s), Xn(4 * n, s), M(n, s);
     uint64_t base = mix64(salt_of(p.seed, 3) ^ (uint64_t)(2 * l + attempt));
-    k_tv_init<<<grid_for(4 * n, 256, 148 * 16), 256, 0, s>>>(n, base, X.p); ++g_kl;
+    k_tv_init_s<<<grid_for(4 * n, 256, 148 * 16), 256, 0, s>>>(n, base, L.sid, X.p); ++g_kl;
     LAP_CHECK_LAUNCH();
     int ew = ilogb_pos(L.maxw);
     DBuf<unsigned long long> mxb(1, s);
@@ -1869,24 +2046,24 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
             for (void *q : p) dfree(q, s);
         }
     } free_lc{{lc_row, lc_idx, lc_slot, lc_cnt, lc_dummy}, s};
-    DBuf<I128> lc_part(4 * (nlc > 0 ? nlc : 1), s);
+    DBuf<I128> cpart(4 * (L.nchunks > 0 ? L.nchunks : 1), s);
     for (int sw = 0; sw < p.tv_sweeps; sw++) {
         // CanonSum instance of this sweep: e_max from the exact max |x| (O-S11), computed on
         // the device (no host round trip)
         LAP_CUDA(cudaMemsetAsync(mxb.p, 0, sizeof(unsigned long long), s));
         k_max_abs<<<grid_for(4 * n, 256, 148 * 8), 256, 0, s>>>(X.p, 4 * n, mxb.p); ++g_kl;
         k_tv_elo<<<1, 1, 0, s>>>(mxb.p, ew, nnz, elo.p); ++g_kl;
-        LAUNCH_G(G, k_tv_sweep, n, s, n, L.row_ptr, L.col, L.w, L.d, (const int *)elo.p, p.tv_omega, X.p, Xn.p);
-        if (nlc > 0) {
-            k_tv_chunk<<<grid_for(nlc * 32, 256, 148 * 16), 256, 0, s>>>(nlc, lc_row, lc_idx, lc_slot, lc_cnt, lc_part.p,
-                                                                         L.row_ptr, L.col, L.w, L.d, elo.p,
-                                                                         p.tv_omega, X.p, Xn.p);
-            ++g_kl;
-        }
+        const CSweep W{X.p, Xn.p, elo.p, p.tv_omega};
+        k_cspmv_store<4, CS_SWEEP><<<cstore_grid(L), 256, 0, s>>>(CStore(cstore_of(L, cpart.p)), X.p, nullptr, nullptr,
+                                                                  0, nullptr, nullptr, W);
+        ++g_kl;
         LAP_CHECK_LAUNCH();
         std::swap(X.p, Xn.p);
         h->cur.edges += nnz;
     }
+    // storage order -> logical order (Xn is free)
+    k_tv_unpermute<<<grid_for(4 * n, 256, 148 * 16), 256, 0, s>>>(n, L.sid, X.p, Xn.p); ++g_kl;
+    std::swap(X.p, Xn.p);
     tmark("  test vectors");
     // affinity + normalisation
     if (nlc > 0) LAP_CUDA(cudaMemsetAsync(M.p, 0, sizeof(double) * n, s));
@@ -2020,12 +2197,17 @@ static int64_t max_degree(int64_t n, const int64_t *rp, cudaStream_t s) {
     }
     return (int64_t)d2h_scalar(r.p, s);
 }
-// the level's solve storage; then release the logical CSR of a big level
-// (params.keep_logical: 1 keep, 0 release, -1 release when nnz >= 2^28)
+static void release_logical(lap_hierarchy *h, int l, cudaStream_t s);
+// the level's solve storage (built after the level below it), then release
 static void finish_level(lap_hierarchy *h, int l, cudaStream_t s) {
-    Level &L = h->lev[l];
     build_storage(h, l, s);
     if (g_tr) g_tr->mark("storage", l);
+    release_logical(h, l, s);
+}
+// release the logical CSR of a big level once its storage exists
+// (params.keep_logical: 1 keep, 0 release, -1 release when nnz >= 2^28)
+static void release_logical(lap_hierarchy *h, int l, cudaStream_t s) {
+    Level &L = h->lev[l];
     const int kl = h->p.keep_logical;
     const bool rel = L.kind != KIND_COARSEST && (kl == 0 || (kl < 0 && L.nnz >= ((int64_t)1 << 28)));
     if (rel) {
@@ -2166,8 +2348,10 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
                 continue;
             }
         }
-        // aggregation level
+        // aggregation level: its storage first (Lanczos and the test-vector sweeps run on it)
         L.kind = KIND_AGG;
+        build_storage(h, l, s);
+        tr.mark("storage", l);
         L.lambda = lanczos(h, L, l, s);
         tr.mark("lanczos", l);
         int64_t m = L.n;
@@ -2187,7 +2371,6 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
             L.kind = KIND_COARSEST;
             h->status = LAP_ESTALL;
             if (L.n > 8192) throw Error{LAP_ESTALL, "aggregation stalled on a level with more than 8192 vertices"};
-            finish_level(h, l, s);
             break;
         }
         L.m = m;
@@ -2195,7 +2378,7 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
         Level &L2 = h->lev[l];
         galerkin(h, L2, h->lev[l + 1], s);
         tr.mark("galerkin", l);
-        finish_level(h, l, s);
+        release_logical(h, l, s);
         elim_run = 0;
     }
     coarse_pinv(h->lev.back(), s);

@@ -1,7 +1,8 @@
 """cfg 5 (BASELINE.json configs[4]: R-MAT scale 26, edge factor 16, LCC, unit
 weights; ~32.8M vertices, ~2.1e9 stored entries) end to end on ONE B200.
 
-Default (-m gpu): generation (C/OpenMP, lapgen.rmat_large), lap_setup +
+With LAP_TEST_CFG5=1 (kept out of the default -m gpu run for its ~10 min):
+generation (C/OpenMP, lapgen.rmat_large), lap_setup +
 lap_solve on the device, the TRUE relative residual recomputed on the host
 from the input graph, level 0 checked against its definition Pi L Pi^T on
 sampled rows (Pi = the oracle's random order, O-S1), and every level's SpMV
@@ -22,7 +23,9 @@ import pytest
 import lapgen
 import oracle
 
-pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+pytestmark = [pytest.mark.gpu, pytest.mark.slow,
+              pytest.mark.skipif(os.environ.get("LAP_TEST_CFG5") != "1",
+                                 reason="cfg 5 (~10 min: generation of 2.1e9 entries, host residual): LAP_TEST_CFG5=1")]
 torch = pytest.importorskip("torch")
 
 
