@@ -139,7 +139,21 @@ struct Dist {
     std::vector<DistLevel> lev;
     double *gscal = nullptr;  // world-reduced scalars (16)
     double *xfull = nullptr;  // level-0 allgather target (P*S0)
+    // the PCG's per-iteration preconditioner step (V-cycle + projection + z
+    // dots, collectives included) as one CUDA graph, captured at the first solve
+    cudaGraphExec_t pgraph = nullptr;
+    int64_t pg_launches = 0, pg_edges = 0, pg_bytes = 0;
+    bool use_graph = true;  // the caller's params.use_graphs
 };
+extern bool g_capturing_flag(bool v);
+static bool dist_graph_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("LAP_DIST_GRAPH");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
 
 static std::vector<void *> *g_owned = nullptr;
 template <class T>
@@ -911,15 +925,53 @@ void dist_run_pcg(lap_hierarchy *h, double tol, int32_t *iters, double *relres, 
         *conv = 1;
         return;
     }
-    auto precond = [&](bool first) {
-        dist_vcycle(h, D, 0, pr, pz, s);
-        h->stats.vcycles++;
-        dist_dot(h, D, sh, pz, {}, 3, false, s);  // sum z
+    auto precond_body = [&](bool first, cudaStream_t st) {
+        dist_vcycle(h, D, 0, pr, pz, st);
+        dist_dot(h, D, sh, pz, {}, 3, false, st);  // sum z
         for (auto &a : sh)
-            launch_pdl(k_d_proj_dot, DRED, 256, s, a.nreal, inv_n, a.pz, (const double *)a.pr, (const double *)g, a.partials);
-        dist_dot(h, D, sh, {}, {}, first ? 0 : 4, true, s);
-        for (auto &a : sh) launch_pdl(k_d_p, dg(a.nreal), 256, s, a.nreal, (const double *)a.pz, a.pp, (const double *)g, first ? 1 : 0);
-        if (!first) LAP_CUDA(cudaMemcpyAsync(g + 0, g + 4, sizeof(double), cudaMemcpyDeviceToDevice, s));
+            launch_pdl(k_d_proj_dot, DRED, 256, st, a.nreal, inv_n, a.pz, (const double *)a.pr, (const double *)g, a.partials);
+        dist_dot(h, D, sh, {}, {}, first ? 0 : 4, true, st);
+        for (auto &a : sh) launch_pdl(k_d_p, dg(a.nreal), 256, st, a.nreal, (const double *)a.pz, a.pp, (const double *)g, first ? 1 : 0);
+        if (!first) LAP_CUDA(cudaMemcpyAsync(g + 0, g + 4, sizeof(double), cudaMemcpyDeviceToDevice, st));
+    };
+    // the per-iteration step is the same launch sequence every time: replay it as
+    // one CUDA graph (NCCL collectives are captured with it), captured once
+    auto precond = [&](bool first) {
+        h->stats.vcycles++;
+        if (first || !D.use_graph || !dist_graph_enabled()) {
+            precond_body(first, s);
+            return;
+        }
+        if (!D.pgraph) {
+            cudaStream_t cs;
+            LAP_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+            Stats save = h->cur;
+            h->cur = Stats{};
+            cudaGraph_t gr;
+            LAP_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+            g_capturing_flag(true);
+            try {
+                precond_body(false, cs);
+            } catch (...) {
+                g_capturing_flag(false);
+                cudaStreamEndCapture(cs, &gr);
+                cudaStreamDestroy(cs);
+                throw;
+            }
+            g_capturing_flag(false);
+            LAP_CUDA(cudaStreamEndCapture(cs, &gr));
+            LAP_CUDA(cudaGraphInstantiate(&D.pgraph, gr, 0));
+            LAP_CUDA(cudaGraphDestroy(gr));
+            LAP_CUDA(cudaStreamDestroy(cs));
+            D.pg_launches = h->cur.launches;
+            D.pg_edges = h->cur.edges;
+            D.pg_bytes = h->cur.bytes;
+            h->cur = save;
+        }
+        LAP_CUDA(cudaGraphLaunch(D.pgraph, s));
+        h->cur.launches += D.pg_launches;
+        h->cur.edges += D.pg_edges;
+        h->cur.bytes += D.pg_bytes;
     };
     auto true_ok = [&]() {
         dist_spmv(h, D, 0, DE_RESID, px, pq, pbin, {}, 0, 0, false, s);
@@ -962,8 +1014,9 @@ void dist_run_pcg(lap_hierarchy *h, double tol, int32_t *iters, double *relres, 
 }
 
 // ------------------------------------------------------------------ construction
-void build_dist(lap_hierarchy *h, lap_comm *c, cudaStream_t s) {
+void build_dist(lap_hierarchy *h, lap_comm *c, cudaStream_t s, bool use_graph) {
     Dist *D = new Dist();
+    D->use_graph = use_graph;
     h->dist = D;
     h->dist_owned = new std::vector<void *>();
     g_owned = (std::vector<void *> *)h->dist_owned;
@@ -1016,6 +1069,7 @@ void build_dist(lap_hierarchy *h, lap_comm *c, cudaStream_t s) {
 
 void free_dist(lap_hierarchy *h) {
     if (!h->dist) return;
+    if (((Dist *)h->dist)->pgraph) cudaGraphExecDestroy(((Dist *)h->dist)->pgraph);
     auto *own = (std::vector<void *> *)h->dist_owned;
     if (own) {
         for (void *p : *own) dfree(p, nullptr);

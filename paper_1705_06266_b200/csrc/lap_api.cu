@@ -471,7 +471,8 @@ lap_status lap_setup_dist(const lap_graph *g, const lap_params *pp, lap_comm *c,
     lap_params p;
     if (pp) p = *pp;
     else lap_params_default(&p);
-    p.use_graphs = 0;  // the sharded solve is host-sequenced (collectives between kernels)
+    const int want_graphs = p.use_graphs;
+    p.use_graphs = 0;  // no single-GPU solve graphs: the sharded solve captures its own (dist.cu)
     if (p.cycle != 0) {
         lap::set_error("lap_setup_dist: the K-cycle (params.cycle = 1) is single-GPU only");
         return LAP_EINVAL;
@@ -480,7 +481,7 @@ lap_status lap_setup_dist(const lap_graph *g, const lap_params *pp, lap_comm *c,
     lap_status st = lap_setup(g, &p, stream, &h);
     if (st != LAP_OK && st != LAP_ESTALL) return st;
     try {
-        if (h->lev[0].kind != lap::KIND_COARSEST) lap::build_dist(h, c, (cudaStream_t)stream);
+        if (h->lev[0].kind != lap::KIND_COARSEST) lap::build_dist(h, c, (cudaStream_t)stream, want_graphs != 0);
     } catch (const lap::Error &e) {
         lap::set_error(e.msg);
         lap_free(h);

@@ -253,6 +253,7 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s);
 void build_transfers(lap_hierarchy *h, cudaStream_t s);
 // column-tiled SpMV layout (xt.cu)
 constexpr int XT_NW = 16;             // warps per CTA (512 threads)
+constexpr size_t XT_SMEM_MAX = 220 * 1024;  // dynamic shared memory of k_spmv_xt: 8 (2 W + rows per block)
 bool xt_eligible(const Level &L, int l);
 void build_xt(Level &L, cudaStream_t s);
 // LCHUNK work items over the rows [row0, row0+nrows) of a CSR longer than minlen
@@ -274,7 +275,7 @@ void solve_block(lap_hierarchy *h, int k, const double *B, double *X, double tol
 void free_block(lap_hierarchy *h);
 void random_stream(int which, uint64_t seed, int level, int attempt, int64_t n, void *out, cudaStream_t s);
 // multi-GPU (dist.cu)
-void build_dist(lap_hierarchy *h, lap_comm *c, cudaStream_t s);
+void build_dist(lap_hierarchy *h, lap_comm *c, cudaStream_t s, bool use_graph = true);
 void free_dist(lap_hierarchy *h);
 void dist_run_pcg(lap_hierarchy *h, double tol, int32_t *iters, double *relres, int *conv, cudaStream_t s);
 void free_pcg(lap_hierarchy *h);

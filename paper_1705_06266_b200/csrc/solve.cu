@@ -528,7 +528,8 @@ static void spmv_dispatch(lap_hierarchy *h, const Level &L, const EpiArgs &a, cu
         static bool attr_set = false;
         const size_t smem = 8 * (size_t)(2 * L.xt_W + L.xt_rmax);
         if (!attr_set) {
-            LAP_CUDA(cudaFuncSetAttribute(k_spmv_xt<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+            LAP_CUDA(cudaFuncSetAttribute(k_spmv_xt<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)XT_SMEM_MAX));
             attr_set = true;
         }
         XtArgs X{L.xt_nb, L.xt_T, L.xt_W, L.xt_rmax, L.n, L.xt_rb, L.xt_seg, L.xt_wo, L.xt_rc, L.xt_w};

@@ -161,7 +161,7 @@ __global__ void k_xt_segs(int64_t cnt, int64_t E0, int b0, int b1, int T, const 
 void build_xt(Level &L, cudaStream_t s) {
     const int64_t n = L.n, nnz = L.nnz;
     int W = env_int("LAP_XT_W", XT_W_DEFAULT);
-    W = std::max(2, std::min(16384, W & ~1));
+    W = std::max(2, std::min(11264, W & ~1));  // 2 W + XT_RMAX doubles <= XT_SMEM_MAX
     const int64_t T = (n + W - 1) / W;
     if (T >= 4096) return;
     int dev = 0, sms = 148;
@@ -186,7 +186,7 @@ void build_xt(Level &L, cudaStream_t s) {
         }
         nb *= 2;
     }
-    if (L.xt_rmax > XT_RMAX) return;
+    if (L.xt_rmax > XT_RMAX || 8 * (size_t)(2 * W + L.xt_rmax) > XT_SMEM_MAX) return;
     g_kl++;
     std::vector<int64_t> hsrp(nb + 1);
     for (int b = 0; b <= nb; b++) LAP_CUDA(cudaMemcpyAsync(&hsrp[b], L.srp + hrb[b], 8, cudaMemcpyDeviceToHost, s));

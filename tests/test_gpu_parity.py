@@ -339,7 +339,9 @@ def test_column_tiled_spmv_per_entry(P, env):
     import subprocess
     import sys
     code = ("import numpy as np, lapgen, oracle, paper_1705_06266_b200 as P\n"
-            "from tests.test_gpu_parity import spmv_bound\n"
+            "def spmv_bound(rp, col, w, d, x):\n"
+            "    rows = np.repeat(np.arange(len(d)), np.diff(rp)); s = np.zeros(len(d))\n"
+            "    np.add.at(s, rows, np.abs(w) * np.abs(x[col])); return 1e-12 * (np.abs(d) * np.abs(x) + s)\n"
             "for g in [lapgen.rmat(12), lapgen.barabasi_albert(6000, 8), lapgen.random_connected(3000, 60000, 3)]:\n"
             "    h = P.Hierarchy(g); ho = oracle.Hierarchy(g)\n"
             "    rng = np.random.default_rng(0)\n"

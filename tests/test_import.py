@@ -53,9 +53,10 @@ def test_import_oracle_hierarchy_solves_like_oracle(tmp_path, mk):
     xo, ito, rro, rco = ho.solve(b)
     assert rc == 0 and rr <= 1e-8 and abs(it - ito) <= 1, (it, ito, rr)
     assert np.abs(x - xo).max() <= 1e-6 * np.abs(xo).max()
-    # the GPU's own setup builds the same hierarchy, so the two solves are bit-identical
+    # the GPU's own setup builds the same operators and maps; only the coarsest
+    # L^+ differs in rounding (the oracle grounds + Cholesky, the GPU Gauss-Jordan)
     xb, itb, _, _ = hb.solve(b)
-    assert itb == it and xb.tobytes() == x.tobytes()
+    assert abs(itb - it) <= 1 and np.abs(xb - x).max() <= 1e-9 * np.abs(x).max()
 
 
 @pytest.mark.gpu
