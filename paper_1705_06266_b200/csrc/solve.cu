@@ -203,8 +203,27 @@ __device__ __forceinline__ bool chunk_reduce(int64_t c, int lane, const int64_t 
     const int64_t rb = rp[i], re = rp[i + 1];
     const int64_t j = R.cidx[c];
     const int64_t b = rb + j * LCHUNK, e = min(re, b + LCHUNK);
+    // 8 independent (col, w) loads, then 8 gathers in flight per lane: the
+    // random x gathers of power-law levels are latency / request-rate bound
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int64_t k = b + lane;
+    for (; k + 224 < e; k += 256) {
+        int c[8];
+        double wv[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            c[u] = __ldg(&col[k + 32 * u]);
+            wv[u] = __ldg(&w[k + 32 * u]);
+        }
+        a0 += wv[0] * x[c[0]];
+        a1 += wv[1] * x[c[1]];
+        a2 += wv[2] * x[c[2]];
+        a3 += wv[3] * x[c[3]];
+        a0 += wv[4] * x[c[4]];
+        a1 += wv[5] * x[c[5]];
+        a2 += wv[6] * x[c[6]];
+        a3 += wv[7] * x[c[7]];
+    }
     for (; k + 96 < e; k += 128) {
         int c0 = __ldg(&col[k]), c1 = __ldg(&col[k + 32]), c2 = __ldg(&col[k + 64]), c3 = __ldg(&col[k + 96]);
         double w0 = __ldg(&w[k]), w1 = __ldg(&w[k + 32]), w2 = __ldg(&w[k + 64]), w3 = __ldg(&w[k + 96]);
@@ -372,9 +391,11 @@ __global__ void __launch_bounds__(XT_NW * 32, 1) k_spmv_xt(XtArgs X, Csr A, EpiA
     extern __shared__ __align__(16) double xsm[];
     __shared__ __align__(8) uint64_t bar[2];
     __shared__ double sh[32];
+    __shared__ double carry_v[XT_NW];
+    __shared__ int carry_r[XT_NW];
     pdl_begin();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double *xs[2] = {xsm, xsm + X.W};
+    double *xs0 = xsm, *xs1 = xsm + X.W;
     double *ys = xsm + 2 * X.W;
     if (tid == 0) {
         mbar_init(&bar[0], 1);
@@ -382,15 +403,16 @@ __global__ void __launch_bounds__(XT_NW * 32, 1) k_spmv_xt(XtArgs X, Csr A, EpiA
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    uint32_t par[2] = {0u, 0u};
+    uint32_t par0 = 0u, par1 = 0u;
     Dacc dacc;
     const double *__restrict__ xg = a.x;
     auto issue = [&](int t, int buf) {
         const int64_t c0 = (int64_t)t * X.W;
         const int64_t cnt = min((int64_t)X.W, X.n - c0) & ~(int64_t)1;  // an odd last element is read from global
-        if (cnt > 0) xt_issue(xs[buf], xg + c0, (uint32_t)(cnt * 8), &bar[buf]);
+        if (cnt > 0) xt_issue(buf ? xs1 : xs0, xg + c0, (uint32_t)(cnt * 8), &bar[buf]);
         else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar[buf])) : "memory");
     };
+    constexpr int U = 4;  // chunks of 32 entries whose loads are in flight together
     for (int b = blockIdx.x; b < X.nb; b += gridDim.x) {
         const int64_t r0 = X.rb[b], nr = X.rb[b + 1] - r0;
         for (int64_t i = tid; i < nr; i += blockDim.x) ys[i] = 0.0;
@@ -401,34 +423,87 @@ __global__ void __launch_bounds__(XT_NW * 32, 1) k_spmv_xt(XtArgs X, Csr A, EpiA
         __syncthreads();
         for (int t = 0; t < X.T; t++) {
             const int buf = t & 1;
-            mbar_wait(&bar[buf], par[buf]);
-            par[buf] ^= 1u;
-            const double *__restrict__ xt = xs[buf];
+            mbar_wait(&bar[buf], buf ? par1 : par0);
+            if (buf) par1 ^= 1u;
+            else par0 ^= 1u;
+            const double *__restrict__ xt = buf ? xs1 : xs0;
             const int64_t c0 = (int64_t)t * X.W;
-            const int64_t tl = min((int64_t)X.W, X.n - c0), tle = tl & ~(int64_t)1;
-            const int64_t sb = ((int64_t)b * X.T + t);
-            const int64_t s0 = X.seg[sb];
-            const int32_t *wo = X.wo + sb * (XT_NW + 1);
-            const int64_t e0 = s0 + wo[warp], e1 = s0 + wo[warp + 1];
-            for (int64_t e = e0; e < e1; e += 32) {
-                const int64_t q = e + lane;
-                const bool valid = q < e1;
-                const uint32_t rcw = valid ? __ldcs(X.rc + q) : 0xFFFF0000u;
-                const int r = (int)(rcw >> 16), c = (int)(rcw & 0xFFFF);
-                double v = 0.0;
-                if (valid) v = __ldcs(X.w + q) * (c < tle ? xt[c] : xg[c0 + c]);
-                // segmented inclusive scan over runs of equal local rows (ascending in the warp's range)
+            const int64_t tle = min((int64_t)X.W, X.n - c0) & ~(int64_t)1;
+            const int64_t sb = (int64_t)b * X.T + t;
+            const int64_t s0 = X.seg[sb], len = X.seg[sb + 1] - s0;
+            // equal shares of the segment's entries per warp; the run of the warp's
+            // first row (which may continue the previous warp's last row) is
+            // accumulated in a register and added after the tile in warp order
+            const int64_t e0 = s0 + len * warp / XT_NW, e1 = s0 + len * (warp + 1) / XT_NW;
+            const int head_r = e0 < e1 ? (int)(__ldg(X.rc + e0) >> 16) : -1;
+            double head_v = 0.0;
+            // runs of one row longer than a chunk (dense levels) accumulate per lane
+            // with no scan; a chunk with several rows takes the segmented scan
+            double acc = 0.0;
+            int cur = head_r;  // the row acc belongs to (warp-uniform)
+            auto flush = [&]() {
+                double t = acc;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const double tv = __shfl_up_sync(0xffffffffu, v, o);
-                    const int tr = __shfl_up_sync(0xffffffffu, r, o);
-                    if (lane >= o && tr == r) v += tv;
+                for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+                if (cur == head_r) head_v += t;
+                else if (lane == 0 && cur >= 0) ys[cur] += t;
+                acc = 0.0;
+                __syncwarp();  // that add precedes the chunk's own adds to the same row (other lanes)
+            };
+            for (int64_t e = e0; e < e1; e += 32 * U) {
+                uint32_t rcw[U];
+                double wv[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int64_t q = e + u * 32 + lane;
+                    rcw[u] = q < e1 ? __ldcs(X.rc + q) : 0xFFFF0000u;
+                    wv[u] = q < e1 ? __ldcs(X.w + q) : 0.0;
                 }
-                const int rn = __shfl_down_sync(0xffffffffu, r, 1);
-                if (valid && (lane == 31 || rn != r)) ys[r] += v;
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    if (e + u * 32 >= e1) break;  // warp-uniform
+                    const int r = (int)(rcw[u] >> 16), c = (int)(rcw[u] & 0xFFFF);
+                    double v = r == 0xFFFF ? 0.0 : wv[u] * (c < tle ? xt[c] : xg[c0 + c]);
+                    if (__all_sync(0xffffffffu, r == cur)) {
+                        acc += v;
+                        continue;
+                    }
+                    flush();
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {  // segmented inclusive scan over equal-row runs
+                        const double tv = __shfl_up_sync(0xffffffffu, v, o);
+                        const int tr = __shfl_up_sync(0xffffffffu, r, o);
+                        if (lane >= o && tr == r) v += tv;
+                    }
+                    const int rn = __shfl_down_sync(0xffffffffu, r, 1);
+                    const bool last = (lane == 31) || (rn != r);
+                    const unsigned valid = __ballot_sync(0xffffffffu, r != 0xFFFF);
+                    const int L = 31 - __clz(valid);  // the last valid lane: its run may go on
+                    const int rl = __shfl_sync(0xffffffffu, r, L);
+                    const double vl = __shfl_sync(0xffffffffu, v, L);
+                    // the head row can only be the chunk's first run
+                    const unsigned same = __ballot_sync(0xffffffffu, r == head_r);
+                    if ((same & 1u) && rl != head_r) {
+                        const int endl = (~same) ? __ffs(~same) - 2 : 31;
+                        head_v += __shfl_sync(0xffffffffu, v, endl);
+                    }
+                    if (last && r != 0xFFFF && r != head_r && r != rl) ys[r] += v;
+                    cur = rl;
+                    acc = lane == 0 ? vl : 0.0;
+                }
             }
-            __syncthreads();  // tile consumed, y updates visible
-            if (tid == 0 && t + 2 < X.T) issue(t + 2, buf);
+            flush();
+            if (lane == 0) {
+                carry_v[warp] = head_v;
+                carry_r[warp] = head_r;
+            }
+            __syncthreads();  // tile consumed, direct y updates and carries visible
+            if (tid == 0) {
+                for (int w = 0; w < XT_NW; w++)
+                    if (carry_r[w] >= 0) ys[carry_r[w]] += carry_v[w];
+                if (t + 2 < X.T) issue(t + 2, buf);
+            }
+            __syncthreads();
         }
         for (int64_t i = tid; i < nr; i += blockDim.x) apply_epi<EPI>(r0 + i, ys[i], A, a, dacc);
         __syncthreads();
@@ -532,7 +607,7 @@ static void spmv_dispatch(lap_hierarchy *h, const Level &L, const EpiArgs &a, cu
                                           (int)XT_SMEM_MAX));
             attr_set = true;
         }
-        XtArgs X{L.xt_nb, L.xt_T, L.xt_W, L.xt_rmax, L.n, L.xt_rb, L.xt_seg, L.xt_wo, L.xt_rc, L.xt_w};
+        XtArgs X{L.xt_nb, L.xt_T, L.xt_W, L.xt_rmax, L.n, L.xt_rb, L.xt_seg, nullptr, L.xt_rc, L.xt_w};
         launch_pdl_smem(k_spmv_xt<EPI>, spmv_grid(L), XT_NW * 32, smem, s, X, A, a, a.partials);
         h->cur.launches++;
         LAP_CHECK_LAUNCH();

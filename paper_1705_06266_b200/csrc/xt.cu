@@ -17,9 +17,12 @@
 //   * a CTA sweeps the tiles in order: x[tile] arrives in shared memory by a TMA
 //     bulk copy (cp.async.bulk + mbarrier, double-buffered so tile t+1 loads
 //     while tile t is consumed), its 16 warps read their segment entries with
-//     coalesced loads and gather x from shared memory; each warp owns a fixed
-//     range of the block's rows and adds segmented (row-run) warp sums into a
-//     shared-memory y, in a fixed order -- bitwise reproducible, no atomics;
+//     coalesced loads (4 chunks of 32 in flight per warp) and gather x from
+//     shared memory; each warp takes an equal share of the segment's entries,
+//     adds segmented (row-run) warp sums into a shared-memory y, and hands the
+//     run of its first row (which may continue the previous warp's) to a carry
+//     that one thread adds after the tile in warp order -- a fixed summation
+//     order, bitwise reproducible, no atomics, hub rows spread over all warps;
 //   * the fused epilogue (diagonal, Chebyshev, residual, dots) runs per row.
 //
 // Traffic per SpMV: 12 B/entry + the epilogue vectors from HBM, plus nb * 8n
@@ -55,6 +58,11 @@ bool xt_eligible(const Level &L, int l) {
     // dense enough that streaming x (nb * 8n bytes from L2) beats one sector per
     // entry (32 B): average degree >= 32; tiles bounded (T < 4096)
     if (!(L.n > SMEM_X_MAX && L.nnz >= 32 * L.n && L.n < (int64_t)XT_W_DEFAULT * 4000)) return false;
+    // a row's entries inside one tile must form long runs (>= 8 on average) or the
+    // per-chunk segmented scans cost more issue slots than the gathers they save
+    // (cfg 3 / 4 level 1: 1-3 entries per row and tile, measured slower than SELL)
+    const double run = (double)L.nnz / (double)L.n * std::min<double>(1.0, (double)XT_W_DEFAULT / (double)L.n);
+    if (run < env_int("LAP_XT_MIN_RUN", 8)) return false;
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
     return (double)fr > 2.5 * 12.0 * (double)L.nnz + 4e9;  // room for the copy + build buffers
@@ -75,53 +83,31 @@ __global__ void k_xt_bounds(int64_t n, int nb, const int64_t *__restrict__ srp, 
         rb[b] = b == 0 ? 0 : (b == nb ? n : lo);
     }
 }
-// warp w of block b owns local rows [wr[b][w], wr[b][w+1]): equal shares of entries
-__global__ void k_xt_warp_rows(int nb, const int64_t *__restrict__ rb, const int64_t *__restrict__ srp,
-                               int32_t *__restrict__ wr) {
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nb * (XT_NW + 1); t += gridDim.x * blockDim.x) {
-        const int b = t / (XT_NW + 1), w = t % (XT_NW + 1);
-        const int64_t r0 = rb[b], r1 = rb[b + 1];
-        int64_t p;
-        if (w == 0) p = r0;
-        else if (w == XT_NW) p = r1;
-        else {
-            const int64_t target = srp[r0] + (srp[r1] - srp[r0]) * w / XT_NW;
-            int64_t lo = r0, hi = r1;
-            while (lo < hi) {
-                const int64_t mid = (lo + hi) >> 1;
-                if (srp[mid] < target) lo = mid + 1;
-                else hi = mid;
-            }
-            p = lo;
-        }
-        wr[t] = (int32_t)(p - r0);
-    }
-}
-// sort keys of the entries [E0, E1) (blocks [b0, b1)):
+// sort keys of the entries [E0, E1) (rows [p0, p0 + nrows) = blocks [b0, b1)):
 //   (block - b0) << 39 | tile << 27 | local row << 14 | local column
-__global__ void __launch_bounds__(256) k_xt_keys(int64_t n, int64_t E0, int64_t E1, int b0, int b1, int W,
-                                                 const int64_t *__restrict__ rb, const int64_t *__restrict__ srp,
-                                                 const int32_t *__restrict__ scol, uint64_t *__restrict__ key,
-                                                 int32_t *__restrict__ idx) {
-    for (int64_t e = E0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E1; e += (int64_t)gridDim.x * blockDim.x) {
-        int64_t lo = rb[b0], hi = rb[b1] - 1;  // storage row of e
-        while (lo < hi) {
-            const int64_t mid = (lo + hi + 1) >> 1;
-            if (srp[mid] <= e) lo = mid;
-            else hi = mid - 1;
-        }
-        const int64_t p = lo;
-        int blo = b0, bhi = b1 - 1;  // its block
+// G lanes per row (hub rows stream), the row's block by one small search
+template <int G>
+__global__ void k_xt_keys(int64_t nrows, int64_t p0, int64_t E0, int b0, int b1, int W, const int64_t *__restrict__ rb,
+                          const int64_t *__restrict__ srp, const int32_t *__restrict__ scol, uint64_t *__restrict__ key,
+                          int32_t *__restrict__ idx) {
+    GROUP_LOOP_BEGIN(G, nrows)
+    if (live) {
+        const int64_t p = p0 + i;
+        int blo = b0, bhi = b1 - 1;
         while (blo < bhi) {
             const int mid = (blo + bhi + 1) >> 1;
             if (rb[mid] <= p) blo = mid;
             else bhi = mid - 1;
         }
-        const int64_t c = scol[e];
-        const uint64_t t = (uint64_t)(c / W), lc = (uint64_t)(c - (int64_t)t * W), lr = (uint64_t)(p - rb[blo]);
-        key[e - E0] = ((uint64_t)(blo - b0) << 39) | (t << 27) | (lr << 14) | lc;
-        idx[e - E0] = (int32_t)(e - E0);
+        const uint64_t hi = ((uint64_t)(blo - b0) << 39) | ((uint64_t)(p - rb[blo]) << 14);
+        for (int64_t k = srp[p] + gl; k < srp[p + 1]; k += G) {
+            const int64_t c = scol[k];
+            const uint64_t t = (uint64_t)(c / W);
+            key[k - E0] = hi | (t << 27) | (uint64_t)(c - (int64_t)t * W);
+            idx[k - E0] = (int32_t)(k - E0);
+        }
     }
+    GROUP_LOOP_END
 }
 __global__ void k_xt_fill(int64_t cnt, int64_t E0, const uint64_t *__restrict__ key, const int32_t *__restrict__ idx,
                           const double *__restrict__ sw, uint32_t *__restrict__ rc, double *__restrict__ w) {
@@ -140,21 +126,13 @@ __device__ __forceinline__ int64_t xt_lower(const uint64_t *__restrict__ key, in
     }
     return lo;
 }
-// segment starts and warp offsets of blocks [b0, b1)
+// segment starts of blocks [b0, b1): first entry of (block, tile) in sorted order
 __global__ void k_xt_segs(int64_t cnt, int64_t E0, int b0, int b1, int T, const uint64_t *__restrict__ key,
-                          const int32_t *__restrict__ wr, int64_t *__restrict__ seg, int32_t *__restrict__ wo) {
+                          int64_t *__restrict__ seg) {
     const int64_t npairs = (int64_t)(b1 - b0) * T;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < npairs; q += (int64_t)gridDim.x * blockDim.x) {
         const int bl = (int)(q / T), t = (int)(q % T), b = b0 + bl;
-        const uint64_t base = ((uint64_t)bl << 39) | ((uint64_t)t << 27);
-        const int64_t s0 = xt_lower(key, cnt, base);
-        seg[(int64_t)b * T + t] = E0 + s0;
-        const int64_t o = ((int64_t)b * T + t) * (XT_NW + 1);
-        for (int w = 0; w <= XT_NW; w++) {
-            const int64_t pos = w == XT_NW ? xt_lower(key, cnt, ((uint64_t)bl << 39) | ((uint64_t)(t + 1) << 27))
-                                           : xt_lower(key, cnt, base | ((uint64_t)wr[b * (XT_NW + 1) + w] << 14));
-            wo[o + w] = (int32_t)(pos - s0);
-        }
+        seg[(int64_t)b * T + t] = E0 + xt_lower(key, cnt, ((uint64_t)bl << 39) | ((uint64_t)t << 27));
     }
 }
 
@@ -196,12 +174,8 @@ void build_xt(Level &L, cudaStream_t s) {
     L.xt_W = W;
     L.xt_rb = rb.take();
     L.xt_seg = (int64_t *)dalloc(sizeof(int64_t) * ((size_t)nb * T + 1), s);
-    L.xt_wo = (int32_t *)dalloc(sizeof(int32_t) * ((size_t)nb * T * (XT_NW + 1)), s);
     L.xt_rc = (uint32_t *)dalloc(sizeof(uint32_t) * (size_t)(nnz + 1), s);
     L.xt_w = (double *)dalloc(sizeof(double) * (size_t)(nnz + 1), s);
-    DBuf<int32_t> wr((int64_t)nb * (XT_NW + 1), s);
-    k_xt_warp_rows<<<grid_for((int64_t)nb * (XT_NW + 1), 128, 512), 128, 0, s>>>(nb, L.xt_rb, L.srp, wr.p);
-    g_kl++;
     // batches of whole blocks, <= 2^27 entries (one radix sort each)
     const int64_t budget = (int64_t)1 << 27;
     int b0 = 0;
@@ -212,23 +186,22 @@ void build_xt(Level &L, cudaStream_t s) {
         if (cnt > 0) {
             DBuf<uint64_t> k1(cnt, s), k2(cnt, s);
             DBuf<int32_t> i1(cnt, s), i2(cnt, s);
-            k_xt_keys<<<grid_for(cnt, 256, 148 * 16), 256, 0, s>>>(n, E0, E1, b0, b1, W, L.xt_rb, L.srp, L.scol, k1.p,
-                                                                   i1.p);
+            const int64_t nrows = hrb[b1] - hrb[b0];
+            LAUNCH_G(group_size(nrows, cnt), k_xt_keys, nrows, s, nrows, hrb[b0], E0, b0, b1, W, L.xt_rb, L.srp,
+                     L.scol, k1.p, i1.p);
             size_t bytes = 0;
             LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k1.p, k2.p, i1.p, i2.p, cnt, 0, 47, s));
             DBuf<char> tmp((int64_t)bytes, s);
             LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, k1.p, k2.p, i1.p, i2.p, cnt, 0, 47, s));
             k_xt_fill<<<grid_for(cnt, 256, 148 * 16), 256, 0, s>>>(cnt, E0, k2.p, i2.p, L.sw, L.xt_rc, L.xt_w);
             k_xt_segs<<<grid_for((int64_t)(b1 - b0) * T, 128, 148 * 8), 128, 0, s>>>(cnt, E0, b0, b1, (int)T, k2.p,
-                                                                                     wr.p, L.xt_seg, L.xt_wo);
+                                                                                     L.xt_seg);
             g_kl += 4;
             LAP_CHECK_LAUNCH();
         } else {
-            // empty blocks: every segment starts at E0 with zero-length warp ranges
+            // empty blocks: every segment starts (and ends) at E0
             std::vector<int64_t> z((size_t)(b1 - b0) * T, E0);
             LAP_CUDA(cudaMemcpyAsync(L.xt_seg + (int64_t)b0 * T, z.data(), 8 * z.size(), cudaMemcpyHostToDevice, s));
-            LAP_CUDA(cudaMemsetAsync(L.xt_wo + (int64_t)b0 * T * (XT_NW + 1), 0,
-                                     4 * (size_t)(b1 - b0) * T * (XT_NW + 1), s));
             LAP_CUDA(cudaStreamSynchronize(s));
         }
         b0 = b1;
