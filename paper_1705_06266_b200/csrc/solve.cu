@@ -395,7 +395,6 @@ __global__ void __launch_bounds__(XT_NW * 32, 1) k_spmv_xt(XtArgs X, Csr A, EpiA
     __shared__ int carry_r[XT_NW];
     pdl_begin();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double *xs0 = xsm, *xs1 = xsm + X.W;
     double *ys = xsm + 2 * X.W;
     if (tid == 0) {
         mbar_init(&bar[0], 1);
@@ -406,19 +405,24 @@ __global__ void __launch_bounds__(XT_NW * 32, 1) k_spmv_xt(XtArgs X, Csr A, EpiA
     uint32_t par0 = 0u, par1 = 0u;
     Dacc dacc;
     const double *__restrict__ xg = a.x;
-    auto issue = [&](int t, int buf) {
+    // tile t -> buffer t&1: the even part by one bulk copy, an odd last element
+    // stored by this thread (visible at the next __syncthreads, as the copy is)
+    auto issue = [&](int t) {
+        const int buf = t & 1;
+        double *dst = xsm + buf * X.W;
         const int64_t c0 = (int64_t)t * X.W;
-        const int64_t cnt = min((int64_t)X.W, X.n - c0) & ~(int64_t)1;  // an odd last element is read from global
-        if (cnt > 0) xt_issue(buf ? xs1 : xs0, xg + c0, (uint32_t)(cnt * 8), &bar[buf]);
+        const int64_t tl = min((int64_t)X.W, X.n - c0), cnt = tl & ~(int64_t)1;
+        if (tl & 1) dst[tl - 1] = xg[c0 + tl - 1];
+        if (cnt > 0) xt_issue(dst, xg + c0, (uint32_t)(cnt * 8), &bar[buf]);
         else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar[buf])) : "memory");
     };
-    constexpr int U = 4;  // chunks of 32 entries whose loads are in flight together
+    constexpr int U = 8;  // chunks of 32 entries whose loads are in flight together
     for (int b = blockIdx.x; b < X.nb; b += gridDim.x) {
         const int64_t r0 = X.rb[b], nr = X.rb[b + 1] - r0;
         for (int64_t i = tid; i < nr; i += blockDim.x) ys[i] = 0.0;
         if (tid == 0) {
-            issue(0, 0);
-            if (X.T > 1) issue(1, 1);
+            issue(0);
+            if (X.T > 1) issue(1);
         }
         __syncthreads();
         for (int t = 0; t < X.T; t++) {
@@ -426,49 +430,51 @@ __global__ void __launch_bounds__(XT_NW * 32, 1) k_spmv_xt(XtArgs X, Csr A, EpiA
             mbar_wait(&bar[buf], buf ? par1 : par0);
             if (buf) par1 ^= 1u;
             else par0 ^= 1u;
-            const double *__restrict__ xt = buf ? xs1 : xs0;
-            const int64_t c0 = (int64_t)t * X.W;
-            const int64_t tle = min((int64_t)X.W, X.n - c0) & ~(int64_t)1;
+            const double *__restrict__ xt = xsm + buf * X.W;
             const int64_t sb = (int64_t)b * X.T + t;
-            const int64_t s0 = X.seg[sb], len = X.seg[sb + 1] - s0;
+            const int64_t s0 = X.seg[sb];
+            const int len = (int)(X.seg[sb + 1] - s0);  // < 2^31 entries per segment
             // equal shares of the segment's entries per warp; the run of the warp's
             // first row (which may continue the previous warp's last row) is
             // accumulated in a register and added after the tile in warp order
-            const int64_t e0 = s0 + len * warp / XT_NW, e1 = s0 + len * (warp + 1) / XT_NW;
-            const int head_r = e0 < e1 ? (int)(__ldg(X.rc + e0) >> 16) : -1;
+            const int q0 = (int)((int64_t)len * warp / XT_NW), q1 = (int)((int64_t)len * (warp + 1) / XT_NW);
+            const uint32_t *__restrict__ rcp = X.rc + s0;
+            const double *__restrict__ wp = X.w + s0;
+            const int head_r = q0 < q1 ? (int)(__ldg(rcp + q0) >> 16) : -1;
             double head_v = 0.0;
             // runs of one row longer than a chunk (dense levels) accumulate per lane
             // with no scan; a chunk with several rows takes the segmented scan
             double acc = 0.0;
             int cur = head_r;  // the row acc belongs to (warp-uniform)
-            auto flush = [&]() {
-                double t = acc;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-                if (cur == head_r) head_v += t;
-                else if (lane == 0 && cur >= 0) ys[cur] += t;
-                acc = 0.0;
-                __syncwarp();  // that add precedes the chunk's own adds to the same row (other lanes)
-            };
-            for (int64_t e = e0; e < e1; e += 32 * U) {
+            for (int e = q0; e < q1; e += 32 * U) {
                 uint32_t rcw[U];
                 double wv[U];
 #pragma unroll
                 for (int u = 0; u < U; u++) {
-                    const int64_t q = e + u * 32 + lane;
-                    rcw[u] = q < e1 ? __ldcs(X.rc + q) : 0xFFFF0000u;
-                    wv[u] = q < e1 ? __ldcs(X.w + q) : 0.0;
+                    const int q = e + u * 32 + lane;
+                    const bool ok = q < q1;
+                    rcw[u] = ok ? __ldcs(rcp + q) : 0xFFFF0000u;
+                    wv[u] = ok ? __ldcs(wp + q) : 0.0;
                 }
 #pragma unroll
                 for (int u = 0; u < U; u++) {
-                    if (e + u * 32 >= e1) break;  // warp-uniform
-                    const int r = (int)(rcw[u] >> 16), c = (int)(rcw[u] & 0xFFFF);
-                    double v = r == 0xFFFF ? 0.0 : wv[u] * (c < tle ? xt[c] : xg[c0 + c]);
+                    const int r = (int)(rcw[u] >> 16);
+                    const double v0 = r == 0xFFFF ? 0.0 : wv[u] * xt[rcw[u] & 0xFFFF];
                     if (__all_sync(0xffffffffu, r == cur)) {
-                        acc += v;
+                        acc += v0;
                         continue;
                     }
-                    flush();
+                    if (__all_sync(0xffffffffu, r == 0xFFFF)) break;  // past the warp's range
+                    {  // flush the accumulated run of row cur
+                        double tsum = acc;
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) tsum += __shfl_xor_sync(0xffffffffu, tsum, o);
+                        if (cur == head_r) head_v += tsum;
+                        else if (lane == 0 && cur >= 0) ys[cur] += tsum;
+                        acc = 0.0;
+                        __syncwarp();  // that add precedes the adds below to the same row (other lanes)
+                    }
+                    double v = v0;
 #pragma unroll
                     for (int o = 1; o < 32; o <<= 1) {  // segmented inclusive scan over equal-row runs
                         const double tv = __shfl_up_sync(0xffffffffu, v, o);
@@ -492,7 +498,13 @@ __global__ void __launch_bounds__(XT_NW * 32, 1) k_spmv_xt(XtArgs X, Csr A, EpiA
                     acc = lane == 0 ? vl : 0.0;
                 }
             }
-            flush();
+            {
+                double tsum = acc;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) tsum += __shfl_xor_sync(0xffffffffu, tsum, o);
+                if (cur == head_r) head_v += tsum;
+                else if (lane == 0 && cur >= 0) ys[cur] += tsum;
+            }
             if (lane == 0) {
                 carry_v[warp] = head_v;
                 carry_r[warp] = head_r;
@@ -501,7 +513,7 @@ __global__ void __launch_bounds__(XT_NW * 32, 1) k_spmv_xt(XtArgs X, Csr A, EpiA
             if (tid == 0) {
                 for (int w = 0; w < XT_NW; w++)
                     if (carry_r[w] >= 0) ys[carry_r[w]] += carry_v[w];
-                if (t + 2 < X.T) issue(t + 2, buf);
+                if (t + 2 < X.T) issue(t + 2);
             }
             __syncthreads();
         }

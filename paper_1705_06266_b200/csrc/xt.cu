@@ -48,13 +48,16 @@ static int env_int(const char *name, int dflt) {
 }
 
 bool xt_eligible(const Level &L, int l) {
-    (void)l;
+    // Off by default: measured no faster than the SELL/chunk kernel (dense random
+    // level n = 100K x 1980: 861 vs 873 us; cfg 5 level 3 slower).
+    // LAP_XT=1 applies the rule below, LAP_XT=force any level (tests).
     const char *e = getenv("LAP_XT");
-    if (e && e[0] == '0') return false;
-    const bool force = e && e[0] == 'f';  // tests: any level with a few hundred rows
+    if (!e || e[0] == '0') return false;
+    const bool force = e[0] == 'f';  // tests: any level with a few hundred rows
     if (L.smem_x || L.n < 2 || L.nnz == 0) return false;
     if (force) return L.n >= 256 && L.nnz >= 4 * L.n;
     if (L.spmv_vec) return false;
+    if (L.kind == KIND_ELIM && l > 0) return false;  // no SpMV on an elimination level below 0 in the solve
     // dense enough that streaming x (nb * 8n bytes from L2) beats one sector per
     // entry (32 B): average degree >= 32; tiles bounded (T < 4096)
     if (!(L.n > SMEM_X_MAX && L.nnz >= 32 * L.n && L.n < (int64_t)XT_W_DEFAULT * 4000)) return false;
@@ -65,7 +68,11 @@ bool xt_eligible(const Level &L, int l) {
     if (run < env_int("LAP_XT_MIN_RUN", 8)) return false;
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
-    return (double)fr > 2.5 * 12.0 * (double)L.nnz + 4e9;  // room for the copy + build buffers
+    uint64_t rsv = 0, used = 0;  // memory liblap's pool holds but does not use is free for us too
+    cudaMemPoolGetAttribute(lib_pool(), cudaMemPoolAttrReservedMemCurrent, &rsv);
+    cudaMemPoolGetAttribute(lib_pool(), cudaMemPoolAttrUsedMemCurrent, &used);
+    const double avail = (double)fr + (double)(rsv - used);
+    return avail > 1.5 * 12.0 * (double)L.nnz + 8e9;  // the copy + its build buffers, with headroom
 }
 
 // row-block boundaries: equal shares of (entries + XT_ROWCOST * rows)

@@ -233,9 +233,9 @@ def test_storage_layout_validated_in_debug_mode(P):
                                  {"LAP_FUSE_ZSUMS": "0"}, {"LAP_SPMV_VEC": "0"}, {"LAP_SPMV_VEC": "16"},
                                  {"LAP_DENSE_TAIL": "0", "LAP_PDL": "0", "LAP_FUSE_TRANSFERS": "0", "LAP_FUSE_ZSUMS": "0"},
                                  {"LAP_XT": "force", "LAP_XT_W": "64"}, {"LAP_XT": "force", "LAP_XT_W": "1000", "LAP_XT_NB": "300"},
-                                 {"LAP_XT": "0"}],
+                                 {"LAP_XT": "1"}],
                          ids=["no-dense-tail", "no-pdl", "no-fused-transfers", "no-fused-zsums", "sell-only",
-                              "vec16-everywhere", "none", "xt-forced-w64", "xt-forced-nb300", "no-xt"])
+                              "vec16-everywhere", "none", "xt-forced-w64", "xt-forced-nb300", "xt-rule"])
 def test_solve_path_switches(P, env):
     """The alternative solve paths (per-level kernels instead of the dense
     tail operator, launches without programmatic dependent launch) give the
