@@ -261,6 +261,19 @@ static void capture_vcycle(lap_hierarchy *h) {
 // holds one chunk twice as large as the biggest setup peak seen so far in this
 // process: allocate it once and free it back to the pool.
 static size_t g_peak = 0;
+// device memory total (cached) minus what liblap's pool has in use: a free-memory
+// estimate for batch sizing that avoids cudaMemGetInfo on the setup path (that
+// call measured 0.5-29 ms, at random -- the source of the setup-time outliers)
+size_t device_free_estimate() {
+    static size_t total = 0;
+    if (!total) {
+        size_t fr = 0;
+        if (cudaMemGetInfo(&fr, &total) != cudaSuccess) total = (size_t)80 << 30;
+    }
+    uint64_t used = 0;
+    cudaMemPoolGetAttribute(lib_pool(), cudaMemPoolAttrUsedMemCurrent, &used);
+    return total > used ? total - (size_t)used : 0;
+}
 void pool_warm(cudaStream_t s) {
     cudaMemPool_t pool = lib_pool();
     uint64_t zero = 0, reserved = 0, used = 0;
@@ -269,7 +282,8 @@ void pool_warm(cudaStream_t s) {
         cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
         size_t want = 2 * g_peak;  // headroom against fragmentation (1.1x still grew now and then)
         size_t fr = 0, tot = 0;
-        if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+        // (cudaMemGetInfo only when the pool must grow: it is slow at random)
+        if (reserved < used + want && cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
             // never reserve beyond what the device has free (leave 5% for other allocators)
             const size_t cap = (size_t)((double)(fr + (reserved - used)) * 0.95);
             want = std::min(want, cap);
@@ -288,7 +302,7 @@ void pool_note_peak() {
     uint64_t hi = 0;
     cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &hi);
     if (hi > g_peak) g_peak = hi;
-    if (getenv("LAP_SETUP_TRACE")) {
+    if (getenv("LAP_SETUP_TRACE") || getenv("LAP_POOL_TRACE")) {
         uint64_t reserved = 0;
         cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
         fprintf(stderr, "[lap setup] pool: peak used %.2f GB, reserved %.2f GB\n", hi / 1e9, reserved / 1e9);

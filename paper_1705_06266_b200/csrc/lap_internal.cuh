@@ -250,6 +250,20 @@ struct EpiArgs {
 void spmv_level(lap_hierarchy *h, const Level &L, EpiKind kind, const EpiArgs &a, cudaStream_t s);
 // storage (storage.cu)
 void build_storage(lap_hierarchy *h, int l, cudaStream_t s);
+size_t device_free_estimate();  // lap_api.cu
+void trace_mark(const char *what);  // LAP_SETUP_TRACE phase mark (setup.cu)
+// every row of a CSR sorted by column (distinct columns < 2^cbits): kin/vin -> kout/vout
+void sort_rows(int64_t n, const int64_t *rp, int64_t nnz, int cbits, const int32_t *kin, const double *vin,
+               int32_t *kout, double *vout, cudaStream_t s);
+// P A P^T with sorted rows: new row p = old row sid[p], column c -> spos[c]; writes srp (n+1),
+// scol / sw (nnz); w NULL = unit weights
+void permute_csr(int64_t n, int64_t nnz, const int32_t *sid, const int32_t *spos, const int64_t *rp,
+                 const int32_t *col, const double *w, int64_t *srp, int32_t *scol, double *sw, bool sort_cols,
+                 int64_t maxlen, cudaStream_t s);
+// the same rows sorted into scol / sw with srp already built; maxlen bounds the row length
+void permute_sorted_rows(int64_t n, int64_t nnz, const int32_t *sid, const int32_t *spos, const int64_t *rp,
+                         const int32_t *col, const double *w, const int64_t *srp, int32_t *scol, double *sw,
+                         int64_t maxlen, cudaStream_t s);
 void build_transfers(lap_hierarchy *h, cudaStream_t s);
 // column-tiled SpMV layout (xt.cu)
 constexpr int XT_NW = 16;             // warps per CTA (512 threads)

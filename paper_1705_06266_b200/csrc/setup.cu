@@ -308,8 +308,27 @@ static bool is_connected(int64_t n, int64_t nnz, const int64_t *row_ptr, const i
 // phase to stderr (diagnostics only; changes the timing it reports on).
 struct SetupTrace {
     bool on = false;
+    int mode = 0;  // 1: synchronise per phase; 2: events per phase, no synchronisation, printed at the end
     double t0 = 0;
     cudaStream_t s = nullptr;
+    struct M {
+        std::string what;
+        int l;
+        cudaEvent_t e;
+        double host;
+    };
+    std::vector<M> marks;
+    ~SetupTrace() {
+        if (mode != 2 || marks.empty()) return;
+        cudaStreamSynchronize(s);
+        for (size_t i = 1; i < marks.size(); i++) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, marks[i - 1].e, marks[i].e);
+            fprintf(stderr, "[lap trace2] level %2d %-30s gpu %8.3f ms host %8.3f ms\n", marks[i].l, marks[i].what.c_str(),
+                    ms, marks[i].host - marks[i - 1].host);
+        }
+        for (auto &m : marks) cudaEventDestroy(m.e);
+    }
     static double now() {
         timespec ts;
         clock_gettime(CLOCK_MONOTONIC, &ts);
@@ -317,14 +336,23 @@ struct SetupTrace {
     }
     explicit SetupTrace(cudaStream_t st) : s(st) {
         const char *e = getenv("LAP_SETUP_TRACE");
-        on = e && e[0] == '1';
-        if (on) {
+        mode = e ? (e[0] == '1' ? 1 : e[0] == '2' ? 2 : 0) : 0;
+        on = mode != 0;
+        if (mode == 1) {
             cudaStreamSynchronize(s);
             t0 = now();
         }
+        if (mode == 2) mark("start", -1);
     }
     void mark(const char *what, int l) {
         if (!on) return;
+        if (mode == 2) {
+            M m{what, l, nullptr, now()};
+            cudaEventCreate(&m.e);
+            cudaEventRecord(m.e, s);
+            marks.push_back(m);
+            return;
+        }
         cudaStreamSynchronize(s);
         double t = now();
         uint64_t rsv = 0;
@@ -338,6 +366,7 @@ static SetupTrace *g_tr = nullptr;
 static void tmark(const char *what) {
     if (g_tr) g_tr->mark(what, -1);
 }
+void trace_mark(const char *what) { tmark(what); }
 
 // =========================================================================
 // generic: sorted (row,col) terms -> CSR with canonical sums
@@ -733,16 +762,20 @@ static void csr_from_source(const TermSrc &S0, int64_t nv, int64_t nout, int cb,
     // batch budget: ~56 B per term in flight (keys, values, their sort copies, RLE)
     int64_t budget = batch_budget_override();
     if (!budget) {
-        size_t fr = 0, tot = 0;
-        cudaMemGetInfo(&fr, &tot);
+        // free-memory estimate without cudaMemGetInfo (measured: 0.5-29 ms per call,
+        // randomly -- the setup-time outliers): device total minus what liblap's
+        // pool holds in use (other allocators of the process are not seen)
+        const size_t fr = device_free_estimate();
         budget = std::max<int64_t>((int64_t)1 << 24, std::min<int64_t>((int64_t)1 << 28, (int64_t)(fr / 4 / 64)));
     }
+    tmark("  terms: budget");
     if (Ttot <= budget) {  // one batch: the plain path
         DBuf<uint64_t> keys(Ttot, s);
         DBuf<double> vals(Ttot, s);
         DBuf<unsigned long long> cur(1, s);
         LAP_CUDA(cudaMemsetAsync(cur.p, 0, 8, s));
         const int64_t t1 = d2h_scalar(vptr.p + nv, s);
+        tmark("  terms: alloc");
         if (t1 > 0) {
             k_src_emit<<<grid_for(t1, 256, 148 * 16), 256, 0, s>>>(S, 0, nv, 0, t1, 0, cb, cur.p, keys.p, vals.p);
             ++g_kl;
@@ -877,6 +910,10 @@ __global__ void k_perm_from_order(int64_t n, const int32_t *order, int64_t *perm
 __global__ void k_inverse_perm(int64_t n, const int64_t *perm, int32_t *inv) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         inv[perm[i]] = (int32_t)i;
+}
+__global__ void k_perm_to_i32(int64_t n, const int64_t *perm, int32_t *p32) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p32[i] = (int32_t)perm[i];
 }
 __global__ void k_identity_i64(int64_t n, int64_t *p) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = i;
@@ -1624,11 +1661,22 @@ __device__ __forceinline__ double cs_epilogue(int64_t p, const i128 *acc, int el
     }
     return 0.0;
 }
-template <int NC, int MODE>
-__global__ void __launch_bounds__(256) k_cspmv_store(CStore C, const double *__restrict__ x, const double *__restrict__ rs,
-                                                     const double *__restrict__ vp, int elo_fixed, LzState *st,
-                                                     double *__restrict__ y, CSweep W) {
+// XS: the whole x staged in shared memory first (small dense-ish levels, as
+// the solve's k_spmv_smem: random gathers from a ~100 KB x are bound by the L1
+// tag rate); one 1024-thread CTA per SM
+template <int NC, int MODE, bool XS = false>
+__global__ void __launch_bounds__(XS ? 1024 : 256) k_cspmv_store(CStore C, const double *__restrict__ x0,
+                                                                 const double *__restrict__ rs,
+                                                                 const double *__restrict__ vp, int elo_fixed,
+                                                                 LzState *st, double *__restrict__ y, CSweep W,
+                                                                 int64_t nx) {
+    extern __shared__ double xs_dyn[];
     if (MODE == CS_LANCZOS && st->stop) return;
+    if (XS) {
+        for (int64_t i = threadIdx.x; i < nx; i += blockDim.x) xs_dyn[i] = x0[i];
+        __syncthreads();
+    }
+    const double *__restrict__ x = XS ? xs_dyn : x0;
     const double bprev = MODE == CS_LANCZOS ? st->bprev : 0.0;
     const int elo = MODE == CS_LANCZOS ? elo_fixed : *W.elo_p;
     if (MODE == CS_LANCZOS && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1787,6 +1835,16 @@ __global__ void k_tridiag_max(const double *alpha, const double *beta, const int
     *out = hi;
 }
 
+static int num_sms_dev() {
+    static int v = 0;
+    if (!v) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        if (v <= 0) v = 148;
+    }
+    return v;
+}
 // start vector and rs in the storage order (p holds logical vertex sid[p])
 __global__ void k_lzc_init_s(int64_t n, uint64_t base, const int32_t *__restrict__ sid, const double *__restrict__ sd,
                              double *__restrict__ y, double *__restrict__ rs, double *__restrict__ vp, LzState *st,
@@ -1827,9 +1885,21 @@ static double lanczos(lap_hierarchy *h, Level &L, int l, cudaStream_t s) {
     const int elo_spmv = canon_elo(e_spmv, nnz);
     const CStore C = cstore_of(L, cpart.p);
     const CSweep W{};
+    const bool xs = L.smem_x && n <= SMEM_X_MAX;
+    if (xs) {
+        static bool attr = false;
+        if (!attr) {
+            LAP_CUDA(cudaFuncSetAttribute(k_cspmv_store<1, CS_LANCZOS, true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * SMEM_X_MAX)));
+            attr = true;
+        }
+    }
     for (int j = 0; j < steps && j < 64; j++) {
         k_lzc_next<<<g, 256, 0, s>>>(n, j == 0, 0, y.p, v.p, vp.p, u.p, rs.p, st.p, al.p, be.p); ++g_kl;
-        k_cspmv_store<1, CS_LANCZOS><<<cstore_grid(L), 256, 0, s>>>(C, u.p, rs.p, vp.p, elo_spmv, st.p, y.p, W); ++g_kl;
+        if (xs) k_cspmv_store<1, CS_LANCZOS, true><<<num_sms_dev(), 1024, 8 * n, s>>>(C, u.p, rs.p, vp.p, elo_spmv, st.p,
+                                                                                       y.p, W, n);
+        else k_cspmv_store<1, CS_LANCZOS><<<cstore_grid(L), 256, 0, s>>>(C, u.p, rs.p, vp.p, elo_spmv, st.p, y.p, W, 0);
+        ++g_kl;
         k_lzc_alpha<<<g, 256, 0, s>>>(n, y.p, v.p, st.p); ++g_kl;
         k_lzc_update<<<g, 256, 0, s>>>(n, y.p, v.p, st.p); ++g_kl;
         LAP_CHECK_LAUNCH();
@@ -2055,7 +2125,7 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
         k_tv_elo<<<1, 1, 0, s>>>(mxb.p, ew, nnz, elo.p); ++g_kl;
         const CSweep W{X.p, Xn.p, elo.p, p.tv_omega};
         k_cspmv_store<4, CS_SWEEP><<<cstore_grid(L), 256, 0, s>>>(CStore(cstore_of(L, cpart.p)), X.p, nullptr, nullptr,
-                                                                  0, nullptr, nullptr, W);
+                                                                  0, nullptr, nullptr, W, 0);
         ++g_kl;
         LAP_CHECK_LAUNCH();
         std::swap(X.p, Xn.p);
@@ -2305,6 +2375,23 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
         int cb = bitlen_u64((uint64_t)(n > 0 ? n : 1));
         DBuf<int32_t> inv(n, s);  // old row of new id r
         k_inverse_perm<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, h->perm, inv.p); ++g_kl;
+        if (nnz < ((int64_t)1 << 28)) {
+            // P L P^T directly: row r = old row inv[r], columns perm[c], each row
+            // sorted in registers / shared memory (no duplicates, nothing to sum)
+            DBuf<int32_t> p32(n, s);
+            k_perm_to_i32<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, h->perm, p32.p); ++g_kl;
+            L0.n = n;
+            L0.nnz = nnz;
+            L0.row_ptr = (int64_t *)dalloc(sizeof(int64_t) * (size_t)(n + 1), s);
+            L0.col = (int32_t *)dalloc(sizeof(int32_t) * (size_t)(nnz + 1), s);
+            L0.w = (double *)dalloc(sizeof(double) * (size_t)(nnz + 1), s);
+            permute_csr(n, nnz, inv.p, p32.p, rp, col, w, L0.row_ptr, L0.col, L0.w, true, INT64_MAX, s);
+            tmark("  relabel: permute + row sorts");
+            L0.d = (double *)dalloc(sizeof(double) * (size_t)(n > 0 ? n : 1), s);
+            row_sums(n, nnz, L0.row_ptr, L0.w, L0.d, &L0.maxw, s);
+            tmark("  terms: row sums");
+            tr.mark("random order", 0);
+        } else {
         TermSrc S;
         S.kind = SRC_RELABEL;
         S.rp = rp;
@@ -2314,6 +2401,7 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
         S.perm = h->perm;
         csr_from_source(S, n, n, cb, 0, 0, false, L0, s);
         tr.mark("random order", 0);
+        }
     }
     rp_in.release();
     col_in.release();

@@ -273,7 +273,9 @@ __device__ __forceinline__ void long_chunk(int64_t c, int lane, const Csr &A, co
 
 // NB = SELL columns per batch: 8 (64 registers, 4 CTAs of 256 per SM) or 4 (48, 5 CTAs) for the
 // big levels, 4 (more resident warps, shorter per-warp slice chains) for mid-size ones
-template <int EPI, int NB>
+// LONG = 0: a level without long rows (grids, coarse mesh levels) -- the chunk
+// path is compiled out, so its registers do not constrain the SELL loop
+template <int EPI, int NB, int LONG>
 __global__ void __launch_bounds__(256, NB == 8 ? 4 : 5) k_spmv(int64_t nslices, int64_t nshort,
                                                              const int64_t *__restrict__ sp,
                                                              const int32_t *__restrict__ ec,
@@ -287,7 +289,7 @@ __global__ void __launch_bounds__(256, NB == 8 ? 4 : 5) k_spmv(int64_t nslices, 
     const int64_t nitems = nslices + R.nchunks;
     Dacc dacc;
     for (int64_t t = warp; t < nitems; t += nwarps) {
-        if (t < nslices) sell_slice<EPI, int32_t, NB>(t, lane, nshort, sp, ec, ew, A, a, a.x, dacc);
+        if (!LONG || t < nslices) sell_slice<EPI, int32_t, NB>(t, lane, nshort, sp, ec, ew, A, a, a.x, dacc);
         else long_chunk<EPI>(t - nslices, lane, A, A.col, R, a, a.x, dacc);
     }
     if (EPI == E_DOT || EPI == E_LZ || EPI == E_FCG) {
@@ -636,12 +638,17 @@ static void spmv_dispatch(lap_hierarchy *h, const Level &L, const EpiArgs &a, cu
                         (const int64_t *)L.slice_ptr, (const uint16_t *)L.ell_col16, (const double *)L.ell_w, A,
                         (const uint16_t *)L.scol16, R, a, a.partials);
     } else {
-        if (L.spmv_nb == 8)
-            launch_pdl(k_spmv<EPI, 8>, spmv_grid(L), 256, s, L.nslices, L.c_end[0], (const int64_t *)L.slice_ptr,
-                       (const int32_t *)L.ell_col, (const double *)L.ell_w, A, R, a, a.partials);
-        else
-            launch_pdl(k_spmv<EPI, 4>, spmv_grid(L), 256, s, L.nslices, L.c_end[0], (const int64_t *)L.slice_ptr,
-                       (const int32_t *)L.ell_col, (const double *)L.ell_w, A, R, a, a.partials);
+#define LAP_SPMV_LAUNCH(NBV, LV)                                                                               \
+    launch_pdl(k_spmv<EPI, NBV, LV>, spmv_grid(L), 256, s, L.nslices, L.c_end[0], (const int64_t *)L.slice_ptr, \
+               (const int32_t *)L.ell_col, (const double *)L.ell_w, A, R, a, a.partials)
+        if (L.nchunks > 0) {
+            if (L.spmv_nb == 8) LAP_SPMV_LAUNCH(8, 1);
+            else LAP_SPMV_LAUNCH(4, 1);
+        } else {
+            if (L.spmv_nb == 8) LAP_SPMV_LAUNCH(8, 0);
+            else LAP_SPMV_LAUNCH(4, 0);
+        }
+#undef LAP_SPMV_LAUNCH
     }
     h->cur.launches++;
     LAP_CHECK_LAUNCH();

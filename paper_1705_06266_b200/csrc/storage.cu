@@ -20,6 +20,7 @@
 #include <string>
 #include <vector>
 
+#include "canon.cuh"
 #include "lap_internal.cuh"
 
 namespace lap {
@@ -188,6 +189,233 @@ __global__ void k_chunk_fill(int64_t nrows, int64_t row0, const int64_t *first, 
     }
 }
 
+// ---------------------------------------------------------------- per-row sorts
+// Every row of a CSR sorted by column (rows independent, columns of a row
+// distinct), by row length class:
+//   <= 32 entries (most rows of every level): one THREAD per row, fused with
+//        the permutation -- the row's (column << 8 | slot) words are loaded
+//        straight from the source row into registers, sorted by a bitonic
+//        network with compile-time indices (no shuffles, no shared memory),
+//        and the weights gathered by slot on the way out;
+//   33..64: one warp per row, bitonic network over two registers per lane;
+//   65..256 / 257..2048: a block radix sort in shared memory (64 x 4 / 256 x 8);
+//   > 2048 (hubs): cub's segmented sort over a list of just those rows.
+// Replaces one device-wide segmented sort of every row (cfg 4: ~5 ms per
+// launch, three per setup) and the emit + 64-bit-key radix sort of the
+// level-0 relabel.
+constexpr int ROWSORT_MED = 2048;  // 256 threads x 8 entries
+constexpr int ROWSORT_SMALL = 256;  // 64 threads x 4 entries
+template <int N>
+__device__ __forceinline__ void reg_bitonic(uint64_t (&a)[N]) {
+#pragma unroll
+    for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+            for (int i = 0; i < N; i++) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const uint64_t x = a[i], y = a[l];
+                    const uint64_t mn = x < y ? x : y, mx = x < y ? y : x;
+                    if ((i & k) == 0) a[i] = mn, a[l] = mx;
+                    else a[i] = mx, a[l] = mn;
+                }
+            }
+        }
+    }
+}
+// rows with LO <= len <= N of P A P^T (new row p = old row sid[p], column c -> spos[c])
+template <int N, int LO>
+__global__ void __launch_bounds__(256) k_perm_sort_thread(int64_t n, const int32_t *__restrict__ sid,
+                                                          const int32_t *__restrict__ spos,
+                                                          const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                                                          const double *__restrict__ w, const int64_t *__restrict__ srp,
+                                                          int32_t *__restrict__ kout, double *__restrict__ vout) {
+    GRID_STRIDE(p, n) {
+        const int64_t o = srp[p];
+        const int64_t len = srp[p + 1] - o;
+        if (len < LO || len > N) continue;
+        const int64_t a0 = rp[sid[p]];
+        uint64_t a[N];
+#pragma unroll
+        for (int q = 0; q < N; q++)
+            a[q] = q < len ? ((uint64_t)(uint32_t)spos[col[a0 + q]] << 8) | (uint64_t)q : ~0ULL;
+        reg_bitonic<N>(a);
+#pragma unroll
+        for (int q = 0; q < N; q++) {
+            if (q < len) {
+                kout[o + q] = (int32_t)(a[q] >> 8);
+                vout[o + q] = w ? w[a0 + (int64_t)(a[q] & 255u)] : 1.0;
+            }
+        }
+    }
+}
+// rows longer than minlen copied (columns translated) into the scratch at their output positions; warp per row
+__global__ void __launch_bounds__(256) k_perm_fill_long(int64_t n, int64_t minlen, const int32_t *__restrict__ sid,
+                                                        const int32_t *__restrict__ spos, const int64_t *__restrict__ rp,
+                                                        const int32_t *__restrict__ col, const double *__restrict__ w,
+                                                        const int64_t *__restrict__ srp, int32_t *__restrict__ kt,
+                                                        double *__restrict__ vt) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t p = warp; p < n; p += nwarps) {
+        const int64_t o = srp[p], len = srp[p + 1] - o;
+        if (len <= minlen) continue;
+        const int64_t a0 = rp[sid[p]];
+        for (int64_t q = lane; q < len; q += 32) {
+            kt[o + q] = spos[col[a0 + q]];
+            vt[o + q] = w ? w[a0 + q] : 1.0;
+        }
+    }
+}
+template <int NH>
+__device__ __forceinline__ void warp_bitonic(int (&k)[2], double (&v)[2], int lane) {
+#pragma unroll
+    for (int kk = 2; kk <= 32 * NH; kk <<= 1) {
+#pragma unroll
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            if (j == 32) {  // partner in this lane's other register (kk = 64: ascending)
+                if (k[1] < k[0]) {
+                    const int tk = k[0];
+                    const double tv = v[0];
+                    k[0] = k[1], v[0] = v[1];
+                    k[1] = tk, v[1] = tv;
+                }
+                continue;
+            }
+#pragma unroll
+            for (int hh = 0; hh < NH; hh++) {
+                const int ok = __shfl_xor_sync(0xffffffffu, k[hh], j);
+                const double ov = __shfl_xor_sync(0xffffffffu, v[hh], j);
+                const int i = hh * 32 + lane;
+                const bool asc = (i & kk) == 0, lower = (lane & j) == 0;
+                const bool take = (asc == lower) ? (ok < k[hh]) : (ok > k[hh]);
+                if (take) k[hh] = ok, v[hh] = ov;
+            }
+        }
+    }
+}
+// rows with minlen < len <= 64
+__global__ void __launch_bounds__(256) k_rowsort_warp(int64_t n, int64_t minlen, const int64_t *__restrict__ rp,
+                                                      const int32_t *__restrict__ kin, const double *__restrict__ vin,
+                                                      int32_t *__restrict__ kout, double *__restrict__ vout) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < n; r += nwarps) {
+        const int64_t a = rp[r];
+        const int64_t len0 = rp[r + 1] - a;
+        if (len0 > 64 || len0 <= minlen) continue;
+        const int len = (int)len0;
+        int k[2];
+        double v[2];
+#pragma unroll
+        for (int hh = 0; hh < 2; hh++) {
+            const int q = hh * 32 + lane;
+            k[hh] = q < len ? kin[a + q] : INT_MAX;
+            v[hh] = q < len ? vin[a + q] : 0.0;
+        }
+        if (len > 32) warp_bitonic<2>(k, v, lane);
+        else if (len > 1) warp_bitonic<1>(k, v, lane);
+#pragma unroll
+        for (int hh = 0; hh < 2; hh++) {
+            const int q = hh * 32 + lane;
+            if (q < len) kout[a + q] = k[hh], vout[a + q] = v[hh];
+        }
+    }
+}
+__global__ void k_rowsort_lists(int64_t n, const int64_t *__restrict__ rp, int32_t *sml, int32_t *med, int32_t *lng,
+                                int *cnt) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t len = rp[r + 1] - rp[r];
+        if (len > ROWSORT_MED) lng[atomicAdd(&cnt[2], 1)] = (int32_t)r;  // order free: rows are independent
+        else if (len > ROWSORT_SMALL) med[atomicAdd(&cnt[1], 1)] = (int32_t)r;
+        else if (len > 64) sml[atomicAdd(&cnt[0], 1)] = (int32_t)r;
+    }
+}
+template <int NT, int IPT>
+__global__ void __launch_bounds__(NT) k_rowsort_block(int64_t m, const int32_t *__restrict__ list,
+                                                      const int64_t *__restrict__ rp, int cbits,
+                                                      const int32_t *__restrict__ kin, const double *__restrict__ vin,
+                                                      int32_t *__restrict__ kout, double *__restrict__ vout) {
+    typedef cub::BlockRadixSort<uint32_t, NT, IPT, double> BRS;
+    __shared__ typename BRS::TempStorage ts;
+    for (int64_t t = blockIdx.x; t < m; t += gridDim.x) {
+        const int64_t r = list[t], a = rp[r];
+        const int len = (int)(rp[r + 1] - a);
+        uint32_t k[IPT];
+        double v[IPT];
+#pragma unroll
+        for (int u = 0; u < IPT; u++) {  // blocked arrangement: thread t holds entries IPT t .. IPT t + IPT - 1
+            const int q = threadIdx.x * IPT + u;
+            k[u] = q < len ? (uint32_t)kin[a + q] : 0xFFFFFFFFu;
+            v[u] = q < len ? vin[a + q] : 0.0;
+        }
+        BRS(ts).Sort(k, v, 0, cbits < 32 ? cbits + 1 : 32);  // (padding 0xFFFFFFFF still sorts last)
+#pragma unroll
+        for (int u = 0; u < IPT; u++) {
+            const int q = threadIdx.x * IPT + u;
+            if (q < len) kout[a + q] = (int32_t)k[u], vout[a + q] = v[u];
+        }
+        __syncthreads();
+    }
+}
+__global__ void k_seg_bounds(int64_t m, const int32_t *__restrict__ list, const int64_t *__restrict__ rp,
+                             int64_t *__restrict__ beg, int64_t *__restrict__ end) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x) {
+        beg[t] = rp[list[t]];
+        end[t] = rp[list[t] + 1];
+    }
+}
+
+// rows of length > minlen (minlen >= 32) sorted: kin/vin -> kout/vout
+static void sort_rows_min(int64_t n, const int64_t *rp, int64_t nnz, int cbits, int64_t minlen, const int32_t *kin,
+                          const double *vin, int32_t *kout, double *vout, cudaStream_t s) {
+    if (n <= 0 || nnz <= 0) return;
+    DBuf<int32_t> sml(n, s), med(n, s), lng(n, s);
+    DBuf<int> cnt(3, s);
+    LAP_CUDA(cudaMemsetAsync(cnt.p, 0, 3 * sizeof(int), s));
+    k_rowsort_lists<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(n, rp, sml.p, med.p, lng.p, cnt.p);
+    k_rowsort_warp<<<grid_for(n * 32, 256, 148 * 8), 256, 0, s>>>(n, minlen, rp, kin, vin, kout, vout);
+    g_kl += 2;
+    trace_mark("    rowsort: lists + warp rows");
+    int hc[3];
+    LAP_CUDA(cudaMemcpyAsync(hc, cnt.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
+    LAP_CUDA(cudaStreamSynchronize(s));
+    if (hc[0] > 0) {
+        k_rowsort_block<64, 4><<<grid_for(hc[0], 1, 148 * 16), 64, 0, s>>>(hc[0], sml.p, rp, cbits, kin, vin, kout, vout);
+        g_kl++;
+    }
+    if (hc[1] > 0) {
+        k_rowsort_block<256, 8><<<grid_for(hc[1], 1, 148 * 4), 256, 0, s>>>(hc[1], med.p, rp, cbits, kin, vin, kout,
+                                                                           vout);
+        g_kl++;
+    }
+    trace_mark("    rowsort: block rows");
+    if (hc[2] > 0) {
+        if (nnz >= ((int64_t)1 << 31)) throw Error{LAP_EINVAL, "sort_rows: rows longer than 2048 entries in a CSR of >= 2^31 entries"};
+        DBuf<int64_t> beg(hc[2], s), end(hc[2], s);
+        k_seg_bounds<<<grid_for(hc[2], 256, 148 * 4), 256, 0, s>>>(hc[2], lng.p, rp, beg.p, end.p);
+        size_t bytes = 0;
+        LAP_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, (int)nnz, hc[2], beg.p, end.p,
+                                                     s));
+        DBuf<char> tmp((int64_t)bytes, s);
+        LAP_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp.p, bytes, kin, kout, vin, vout, (int)nnz, hc[2], beg.p, end.p, s));
+        g_kl += 2;
+        trace_mark("    rowsort: long rows (cub)");
+    }
+    LAP_CHECK_LAUNCH();
+}
+
+void sort_rows(int64_t n, const int64_t *rp, int64_t nnz, int cbits, const int32_t *kin, const double *vin,
+               int32_t *kout, double *vout, cudaStream_t s) {
+    if (n <= 0 || nnz <= 0) return;
+    k_rowsort_warp<<<grid_for(n * 32, 256, 148 * 8), 256, 0, s>>>(n, -1, rp, kin, vin, kout, vout);
+    g_kl++;
+    sort_rows_min(n, rp, nnz, cbits, 64, kin, vin, kout, vout, s);
+}
+
 template <class T>
 static void scan_excl(const T *in, T *out, int64_t n, cudaStream_t s) {
     size_t bytes = 0;
@@ -218,6 +446,49 @@ int64_t build_chunks(const int64_t *rp, int64_t row0, int64_t nrows, int64_t min
     }
     LAP_CHECK_LAUNCH();
     return nch;
+}
+
+__global__ void k_perm_deg(int64_t n, const int32_t *sid, const int64_t *rp, int64_t *deg) {
+    GRID_STRIDE(p, n) deg[p] = rp[sid[p] + 1] - rp[sid[p]];
+}
+void permute_csr(int64_t n, int64_t nnz, const int32_t *sid, const int32_t *spos, const int64_t *rp,
+                 const int32_t *col, const double *w, int64_t *srp, int32_t *scol, double *sw, bool sort_cols,
+                 int64_t maxlen, cudaStream_t s) {
+    DBuf<int64_t> deg(n + 1, s);
+    LAP_CUDA(cudaMemsetAsync(deg.p + n, 0, sizeof(int64_t), s));
+    if (n > 0) {
+        k_perm_deg<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(n, sid, rp, deg.p);
+        g_kl++;
+    }
+    scan_excl(deg.p, srp, n + 1, s);
+    if (nnz <= 0) return;
+    if (!sort_cols) {
+        k_storage_fill<<<grid_for(nnz, 256, 148 * 16), 256, 0, s>>>(n, nnz, sid, spos, rp, col, w, srp, scol, sw);
+        g_kl++;
+        LAP_CHECK_LAUNCH();
+        return;
+    }
+    permute_sorted_rows(n, nnz, sid, spos, rp, col, w, srp, scol, sw, maxlen, s);
+}
+// the rows of P A P^T sorted, srp given
+void permute_sorted_rows(int64_t n, int64_t nnz, const int32_t *sid, const int32_t *spos, const int64_t *rp,
+                         const int32_t *col, const double *w, const int64_t *srp, int32_t *scol, double *sw,
+                         int64_t maxlen, cudaStream_t s) {
+    if (n <= 0 || nnz <= 0) return;
+    // rows of <= 32 entries: permuted and sorted in one thread's registers
+    k_perm_sort_thread<16, 0><<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(n, sid, spos, rp, col, w, srp, scol, sw);
+    k_perm_sort_thread<32, 17><<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(n, sid, spos, rp, col, w, srp, scol, sw);
+    g_kl += 2;
+    trace_mark("    permute: short rows sorted");
+    if (maxlen > 32) {  // longer rows: copied into a scratch at their positions, then sorted by length class
+        DBuf<int32_t> c2(nnz, s);
+        DBuf<double> w2(nnz, s);
+        k_perm_fill_long<<<grid_for(n * 32, 256, 148 * 8), 256, 0, s>>>(n, 32, sid, spos, rp, col, w, srp, c2.p, w2.p);
+        g_kl++;
+        trace_mark("    permute: long rows filled");
+        sort_rows_min(n, srp, nnz, bitlen_u64((uint64_t)n), 32, c2.p, w2.p, scol, sw, s);
+    }
+    LAP_CHECK_LAUNCH();
 }
 
 // LAP_DEBUG_SYNC=1: host-side consistency check of a level's storage layout
@@ -285,7 +556,7 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
     DBuf<uint64_t> skey(n, s);
     L.sid = (int32_t *)dalloc(sizeof(int32_t) * n, s);
     L.spos = (int32_t *)dalloc(sizeof(int32_t) * n, s);
-    auto sort_rows = [&](int by_degree, unsigned long long *counts) {
+    auto order_rows = [&](int by_degree, unsigned long long *counts) {
         k_class_key<<<g, 256, 0, s>>>(n, L.row_ptr, key.p, skey.p, ids.p, counts, by_degree);
         size_t bytes = 0;
         LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, skey.p, key2.p, ids.p, L.sid, n, 0, 41, s));
@@ -294,7 +565,8 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
         g_kl += 3;
         LAP_CHECK_LAUNCH();
     };
-    sort_rows(0, cnt.p);
+    order_rows(0, cnt.p);
+    trace_mark("    storage: row order");
     unsigned long long hc[NCLASS + 1];
     LAP_CUDA(cudaMemcpyAsync(hc, cnt.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
     LAP_CUDA(cudaStreamSynchronize(s));
@@ -353,12 +625,13 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
                 LAP_CUDA(cudaMemcpyAsync(L.sid, sid2.p, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
                 g_kl += 3;
             } else {
-                sort_rows(1, nullptr);
+                order_rows(1, nullptr);
             }
         }
     }
     k_inverse<<<g, 256, 0, s>>>(n, L.sid, L.spos);
     g_kl++;
+    trace_mark("    storage: slices + inverse");
     // storage CSR
     DBuf<int64_t> deg(n + 1, s);
     LAP_CUDA(cudaMemsetAsync(deg.p + n, 0, sizeof(int64_t), s));
@@ -370,36 +643,34 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
     L.scol = (int32_t *)dalloc(sizeof(int32_t) * (L.nnz + 1), s);
     L.sw = (double *)dalloc(sizeof(double) * (L.nnz + 1), s);
     if (L.nnz) {
-        k_storage_fill<<<grid_for(L.nnz, 256, 148 * 16), 256, 0, s>>>(n, L.nnz, L.sid, L.spos, L.row_ptr, L.col, L.w,
-                                                                      L.srp, L.scol, L.sw);
-        g_kl++;
-        // each SHORT storage row (the SELL class, rows [0, c_end[0]) of the storage
-        // order) in ascending STORAGE column order: the u-th column of consecutive
-        // rows of a SELL slice then point the same way (-z, -y, -x, +x, ... on a
-        // grid-like level), so one gather instruction touches few lines instead of
-        // one line per lane (the L1 tag rate bounds these gathers).  Long rows are
-        // read in 32-entry warp chunks, where the order buys nothing: they keep
-        // the logical order (no sort and no double buffer over ~all entries of a
-        // power-law level: cfg 5 level 0 storage 2.1 s -> see DESIGN.md)
-        // long rows are sorted too (gather locality of dense-ish rows) unless the
-        // level is served by the column-tiled kernel or is huge (the sort would
-        // cost more setup than it saves: cfg 5 level 1, 2.1e9 entries)
-        const int64_t short_nnz = L.nnz < ((int64_t)1 << 28) ? L.nnz : (nshort > 0 ? d2h(L.srp + nshort, s) : 0);
-        const int64_t nsorted = L.nnz < ((int64_t)1 << 28) ? n : nshort;
-        if (short_nnz > 0 && short_nnz < ((int64_t)1 << 31) && !getenv_flag_off("LAP_SORT_ROWS")) {
-            DBuf<int32_t> c2(short_nnz, s);
-            DBuf<double> w2(short_nnz, s);
-            size_t bytes = 0;
-            LAP_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, bytes, L.scol, c2.p, L.sw, w2.p, (int)short_nnz,
-                                                         (int)nsorted, L.srp, L.srp + 1, s));
-            DBuf<char> tmp((int64_t)bytes, s);
-            LAP_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp.p, bytes, L.scol, c2.p, L.sw, w2.p, (int)short_nnz,
-                                                         (int)nsorted, L.srp, L.srp + 1, s));
+        // each storage row in ascending STORAGE column order: the u-th column of
+        // consecutive rows of a SELL slice then point the same way (-z, -y, -x,
+        // +x, ... on a grid-like level), so one gather instruction touches few
+        // lines instead of one line per lane (the L1 tag rate bounds these
+        // gathers); long rows too (gather locality of dense-ish rows), except on
+        // huge levels (>= 2^28 entries, cfg 5), where only the short rows are
+        // sorted (no double buffer over ~all entries of a power-law level)
+        const bool sort_on = !getenv_flag_off("LAP_SORT_ROWS");
+        const int cbits = bitlen_u64((uint64_t)n);
+        if (sort_on && L.nnz < ((int64_t)1 << 28)) {
+            permute_sorted_rows(n, L.nnz, L.sid, L.spos, L.row_ptr, L.col, L.w, L.srp, L.scol, L.sw,
+                                L.maxdeg > 0 ? L.maxdeg : INT64_MAX, s);
+        } else {
+            k_storage_fill<<<grid_for(L.nnz, 256, 148 * 16), 256, 0, s>>>(n, L.nnz, L.sid, L.spos, L.row_ptr, L.col,
+                                                                          L.w, L.srp, L.scol, L.sw);
             g_kl++;
-            LAP_CUDA(cudaMemcpyAsync(L.scol, c2.p, sizeof(int32_t) * short_nnz, cudaMemcpyDeviceToDevice, s));
-            LAP_CUDA(cudaMemcpyAsync(L.sw, w2.p, sizeof(double) * short_nnz, cudaMemcpyDeviceToDevice, s));
+            const int64_t short_nnz = nshort > 0 ? d2h(L.srp + nshort, s) : 0;
+            if (sort_on && short_nnz > 0) {
+                DBuf<int32_t> c2(short_nnz, s);
+                DBuf<double> w2(short_nnz, s);
+                sort_rows(nshort, L.srp, short_nnz, cbits, L.scol, L.sw, c2.p, w2.p, s);
+                LAP_CUDA(cudaMemcpyAsync(L.scol, c2.p, sizeof(int32_t) * short_nnz, cudaMemcpyDeviceToDevice, s));
+                LAP_CUDA(cudaMemcpyAsync(L.sw, w2.p, sizeof(double) * short_nnz, cudaMemcpyDeviceToDevice, s));
+            }
         }
+        LAP_CHECK_LAUNCH();
     }
+    trace_mark("    storage: csr fill + row sorts");
     // SELL-32 slices of the short class
     if (nshort > 0) {
         L.slice_ptr = (int64_t *)dalloc(sizeof(int64_t) * (L.nslices + 1), s);
@@ -411,6 +682,7 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
                                                                     L.ell_w);
         g_kl++;
     }
+    trace_mark("    storage: sell fill");
     if (debug_sync()) validate_storage(L, s);
     // small dense-ish level: 16-bit column copies for the shared-memory-x SpMV
     if (n <= SMEM_X_MAX && L.nnz >= SMEM_X_MIN_DEG * n && L.nnz > 0) {
