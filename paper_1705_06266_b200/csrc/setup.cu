@@ -94,9 +94,22 @@ __global__ void k_validate_rowptr(int64_t n, int64_t nnz, const int64_t *__restr
         if (a < 0 || e < a || e > nnz) atomicOr(flag, 1);
     }
 }
+// Symmetry fingerprint (hsum != NULL): two independent 64-bit multiset hashes,
+// sum over entries of h(i, j, bits(w)) - h(j, i, bits(w)) mod 2^64.  A symmetric
+// matrix has the same multiset of (i, j, w) and (j, i, w) tuples, so both sums
+// are 0; an asymmetric one leaves a nonzero sum except with probability ~2^-128
+// (a pseudo-random collision of both hashes).  Integer additions mod 2^64:
+// order-free, so the atomics are deterministic.
+__device__ __forceinline__ uint64_t sym_h1(uint64_t a, uint64_t b, uint64_t mw) {
+    return mix64((a * 0x9E3779B97F4A7C15ULL + b * 0xD1B54A32D192ED03ULL) ^ mw);
+}
+__device__ __forceinline__ uint64_t sym_h2(uint64_t a, uint64_t b, uint64_t mw) {
+    return mix64(mix64(a ^ 0x5851F42D4C957F2DULL) + (b ^ mw));
+}
 template <int G>
 __global__ void k_validate(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                           const double *__restrict__ w, int *flag) {
+                           const double *__restrict__ w, int *flag, unsigned long long *hsum) {
+    uint64_t s1 = 0, s2 = 0;
     GROUP_LOOP_BEGIN(G, n)
     if (live) {
         int64_t a = row_ptr[i], e = row_ptr[i + 1];
@@ -106,9 +119,26 @@ __global__ void k_validate(int64_t n, const int64_t *__restrict__ row_ptr, const
             double wk = w ? w[k] : 1.0;
             bad |= !(wk > 0.0) || !isfinite(wk);
             if (bad) atomicOr(flag, 1);
+            if (hsum) {
+                const uint64_t wb = (uint64_t)__double_as_longlong(wk);
+                const uint64_t m1 = mix64(wb), m2 = mix64(wb ^ 0x2545F4914F6CDD1DULL);
+                s1 += sym_h1((uint64_t)i, (uint64_t)j, m1) - sym_h1((uint64_t)j, (uint64_t)i, m1);
+                s2 += sym_h2((uint64_t)i, (uint64_t)j, m2) - sym_h2((uint64_t)j, (uint64_t)i, m2);
+            }
         }
     }
     GROUP_LOOP_END
+    if (hsum) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+            s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        }
+        if ((threadIdx.x & 31) == 0 && (s1 | s2)) {
+            atomicAdd(&hsum[0], (unsigned long long)s1);
+            atomicAdd(&hsum[1], (unsigned long long)s2);
+        }
+    }
 }
 
 template <int G>
@@ -225,14 +255,19 @@ __global__ void __launch_bounds__(256) k_sym_search(int64_t n, int64_t nnz, cons
         __syncthreads();
     }
 }
-static bool symcheck_by_search(int64_t nnz) {
+// LAP_SYMCHECK = "hash" (default: the fingerprint computed by k_validate),
+// "sort" (exact: one radix sort of the transposed entries), "search" (exact:
+// a binary search per entry, no extra memory)
+static int symcheck_mode() {
     static int v = -1;
     if (v < 0) {
-        const char *e = getenv("LAP_SYMCHECK");  // "search" / "sort" (tests); default by size
-        v = !e ? -1 : (e[0] == 's' && e[1] == 'e') ? 1 : 0;
-        if (!e) return nnz >= ((int64_t)1 << 28);
+        const char *e = getenv("LAP_SYMCHECK");
+        v = !e ? 0 : (e[0] == 's' && e[1] == 'e') ? 2 : (e[0] == 's' && e[1] == 'o') ? 1 : 0;
     }
-    return v == 1;
+    return v;
+}
+static bool symcheck_by_search(int64_t nnz) {
+    return symcheck_mode() == 2 || (symcheck_mode() == 1 && nnz >= ((int64_t)1 << 28));
 }
 static bool is_symmetric(int64_t n, int64_t nnz, const int64_t *rp, const int32_t *col, const double *w,
                          cudaStream_t s) {
@@ -485,27 +520,15 @@ static void row_sums(int64_t n, int64_t nnz, const int64_t *row_ptr, const doubl
     }
 }
 
-// Build a level's CSR from unsorted (key=(row<<cb)|col, value) terms whose
-// duplicates are combined by CanonSum with instance (e_max, K).
-static void csr_from_terms(int64_t nrows, int cb, int64_t T, DBuf<uint64_t> &keys, DBuf<double> &vals,
-                           int e_max, int64_t K, bool combine, Level &out, cudaStream_t s) {
-    int rb = bitlen_u64((uint64_t)(nrows > 0 ? nrows : 1));
-    int end_bit = std::min(64, cb + rb);
-    DBuf<uint64_t> k2(T, s);
-    DBuf<double> v2(T, s);
-    if (T > 0) {
-        size_t bytes = 0;
-        LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, k2.p, vals.p, v2.p, T, 0, end_bit, s));
-        DBuf<char> tmp((int64_t)bytes, s);
-        LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, keys.p, k2.p, vals.p, v2.p, T, 0, end_bit, s)); ++g_kl;
-    }
-    keys.release();
-    vals.release();
-    tmark("  terms: sort");
-    int64_t U = T;
+// The combine step of csr_from_terms on terms already sorted by (row << cb | col):
+// duplicates of a key are one segment; each segment's CanonSum (instance e_max, K)
+// is formed directly from the fp64 terms.
+static void csr_combine_sorted(int64_t nrows, int cb, int64_t T, DBuf<uint64_t> &k2, DBuf<double> &v2, int e_max,
+                               int64_t K, Level &out, cudaStream_t s) {
+    int64_t U = 0;
     out.n = nrows;
     out.row_ptr = (int64_t *)dalloc(sizeof(int64_t) * (size_t)(nrows + 1), s);
-    if (combine && T > 0) {
+    if (T > 0) {
         // duplicates of a key are one segment of the sorted terms: run-length
         // encode the keys, then each segment's CanonSum is formed directly from
         // the fp64 terms (thread per short segment, warp per long one)
@@ -547,16 +570,49 @@ static void csr_from_terms(int64_t nrows, int cb, int64_t T, DBuf<uint64_t> &key
         k_row_ptr_from_keys<<<grid_for(nrows + 1, 256, 148 * 16), 256, 0, s>>>(nrows, U, uk.p, cb, out.row_ptr); ++g_kl;
         LAP_CHECK_LAUNCH();
     } else {
-        out.nnz = T;
-        out.col = (int32_t *)dalloc(sizeof(int32_t) * (size_t)(T + 1), s);
-        out.w = v2.take();
-        if (T > 0) {
-            k_decode_cols<<<grid_for(T, 256, 148 * 16), 256, 0, s>>>(T, k2.p, (1ULL << cb) - 1, out.col); ++g_kl;
-            LAP_CHECK_LAUNCH();
-        }
-        k_row_ptr_from_keys<<<grid_for(nrows + 1, 256, 148 * 16), 256, 0, s>>>(nrows, T, k2.p, cb, out.row_ptr); ++g_kl;
+        out.nnz = 0;
+        out.col = (int32_t *)dalloc(sizeof(int32_t), s);
+        out.w = (double *)dalloc(sizeof(double), s);
+        k_row_ptr_from_keys<<<grid_for(nrows + 1, 256, 148 * 16), 256, 0, s>>>(nrows, 0, k2.p, cb, out.row_ptr); ++g_kl;
+    }
+    (void)U;
+    out.d = (double *)dalloc(sizeof(double) * (size_t)(nrows > 0 ? nrows : 1), s);
+    row_sums(nrows, out.nnz, out.row_ptr, out.w, out.d, &out.maxw, s);
+    tmark("  terms: row sums");
+}
+
+// Build a level's CSR from unsorted (key=(row<<cb)|col, value) terms whose
+// duplicates are combined by CanonSum with instance (e_max, K).
+static void csr_from_terms(int64_t nrows, int cb, int64_t T, DBuf<uint64_t> &keys, DBuf<double> &vals,
+                           int e_max, int64_t K, bool combine, Level &out, cudaStream_t s) {
+    int rb = bitlen_u64((uint64_t)(nrows > 0 ? nrows : 1));
+    int end_bit = std::min(64, cb + rb);
+    DBuf<uint64_t> k2(T, s);
+    DBuf<double> v2(T, s);
+    if (T > 0) {
+        size_t bytes = 0;
+        LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, k2.p, vals.p, v2.p, T, 0, end_bit, s));
+        DBuf<char> tmp((int64_t)bytes, s);
+        LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, keys.p, k2.p, vals.p, v2.p, T, 0, end_bit, s)); ++g_kl;
+    }
+    keys.release();
+    vals.release();
+    tmark("  terms: sort");
+    if (combine) {
+        csr_combine_sorted(nrows, cb, T, k2, v2, e_max, K, out, s);
+        return;
+    }
+    out.n = nrows;
+    out.row_ptr = (int64_t *)dalloc(sizeof(int64_t) * (size_t)(nrows + 1), s);
+    out.nnz = T;
+    out.col = (int32_t *)dalloc(sizeof(int32_t) * (size_t)(T + 1), s);
+    out.w = v2.take();
+    if (T > 0) {
+        k_decode_cols<<<grid_for(T, 256, 148 * 16), 256, 0, s>>>(T, k2.p, (1ULL << cb) - 1, out.col); ++g_kl;
         LAP_CHECK_LAUNCH();
     }
+    k_row_ptr_from_keys<<<grid_for(nrows + 1, 256, 148 * 16), 256, 0, s>>>(nrows, T, k2.p, cb, out.row_ptr); ++g_kl;
+    LAP_CHECK_LAUNCH();
     out.d = (double *)dalloc(sizeof(double) * (size_t)(nrows > 0 ? nrows : 1), s);
     row_sums(nrows, out.nnz, out.row_ptr, out.w, out.d, &out.maxw, s);
     tmark("  terms: row sums");
@@ -2209,6 +2265,104 @@ __global__ void k_mem_ptr(int64_t m, int64_t n, const uint32_t *skey, int64_t *p
     }
 }
 
+// ---- aggregate-ordered Galerkin (N3: "a matrix-matrix product
+// that exploits the special structure of R and P"): the members of every
+// aggregate are consecutive member slots, so emitting the fine entries slot
+// by slot (self-terms agg_j == a dropped, positions by a prefix sum of the
+// per-slot counts -- deterministic, no atomics) leaves the terms of coarse row
+// a contiguous; only each row's terms need sorting by agg_j (per-row sorts by
+// length class, sort_rows), not one device-wide 64-bit-key radix sort of all
+// terms.  Each (a, b) entry is then one CanonSum of exactly the method's
+// multiset of terms (O-R23): bit-identical to the global-sort path.
+template <int G>
+__global__ void k_gal_slot_cnt(int64_t ns, const int32_t *__restrict__ members, const uint32_t *__restrict__ slot_agg,
+                               const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                               const int32_t *__restrict__ agg, int64_t *__restrict__ cnt) {
+    GROUP_LOOP_BEGIN(G, ns)
+    int64_t c = 0;
+    int32_t fi = 0, a = 0;
+    if (live) {
+        fi = members[i];
+        a = (int32_t)slot_agg[i];
+        for (int64_t k = rp[fi] + gl; k < rp[fi + 1]; k += G) c += agg[col[k]] != a;
+    }
+    c = grp_sum<G>(c);
+    if (live && gl == 0) cnt[i] = c;
+    GROUP_LOOP_END
+}
+template <int G>
+__global__ void k_gal_slot_emit(int64_t ns, const int32_t *__restrict__ members, const uint32_t *__restrict__ slot_agg,
+                                const int64_t *__restrict__ rp, const int32_t *__restrict__ col,
+                                const double *__restrict__ w, const int32_t *__restrict__ agg,
+                                const int64_t *__restrict__ pv, int32_t *__restrict__ tk, double *__restrict__ tv) {
+    GROUP_LOOP_BEGIN(G, ns)
+    int64_t kb = 0, ke = 0, o = 0;
+    int32_t a = 0;
+    if (live) {
+        const int32_t fi = members[i];
+        a = (int32_t)slot_agg[i];
+        kb = rp[fi];
+        ke = rp[fi + 1];
+        o = pv[i];
+    }
+    GROUP_COMPACT_ROW(G, kb, ke, o, agg[col[k]] != a, (tk[p] = agg[col[k]], tv[p] = w[k]))
+    GROUP_LOOP_END
+}
+__global__ void k_gal_row_ptr(int64_t m, const int64_t *__restrict__ mem_ptr, const int64_t *__restrict__ pv,
+                              int64_t *__restrict__ pa) {
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a <= m; a += (int64_t)gridDim.x * blockDim.x)
+        pa[a] = pv[mem_ptr[a]];
+}
+template <int G>
+__global__ void k_gal_keys(int64_t m, const int64_t *__restrict__ pa, const int32_t *__restrict__ sk, int cb,
+                           uint64_t *__restrict__ key) {
+    GROUP_LOOP_BEGIN(G, m)
+    if (live)
+        for (int64_t k = pa[i] + gl; k < pa[i + 1]; k += G) key[k] = ((uint64_t)i << cb) | (uint64_t)(uint32_t)sk[k];
+    GROUP_LOOP_END
+}
+constexpr int64_t GAL_ORDERED_MAX_AVG = 256;  // terms per coarse row (average) for the ordered Galerkin
+static bool gal_fast_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("LAP_GAL_FAST");  // 0: the batched global-sort path (tests, experiments)
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+static void csr_combine_sorted(int64_t nrows, int cb, int64_t T, DBuf<uint64_t> &k2, DBuf<double> &v2, int e_max,
+                               int64_t K, Level &out, cudaStream_t s);
+static void galerkin_fast(lap_hierarchy *h, Level &L, Level &N, const int32_t *members, const uint32_t *slot_agg,
+                          const int64_t *mem_ptr, cudaStream_t s) {
+    const int64_t n = L.n, m = L.m;
+    const int cb = bitlen_u64((uint64_t)(m > 0 ? m : 1));
+    const int G = group_size(n, L.nnz, L.maxdeg <= SHORT_MAX);
+    DBuf<int64_t> cnt(n + 1, s), pv(n + 1, s), pa(m + 1, s);
+    LAP_CUDA(cudaMemsetAsync(cnt.p + n, 0, sizeof(int64_t), s));
+    LAUNCH_G(G, k_gal_slot_cnt, n, s, n, members, slot_agg, L.row_ptr, L.col, L.agg, cnt.p);
+    exclusive_scan_i64(cnt.p, pv.p, n + 1, s);
+    const int64_t T = d2h_scalar(pv.p + n, s);
+    DBuf<int32_t> tk(T + 1, s);
+    DBuf<double> tv(T + 1, s);
+    LAUNCH_G(G, k_gal_slot_emit, n, s, n, members, slot_agg, L.row_ptr, L.col, L.w, L.agg, pv.p, tk.p, tv.p);
+    k_gal_row_ptr<<<grid_for(m + 1, 256, 148 * 8), 256, 0, s>>>(m, mem_ptr, pv.p, pa.p); ++g_kl;
+    LAP_CHECK_LAUNCH();
+    cnt.release();
+    pv.release();
+    tmark("  galerkin: ordered emit");
+    DBuf<int32_t> sk(T + 1, s);
+    DBuf<double> sv(T + 1, s);
+    sort_rows(m, pa.p, T, cb, tk.p, tv.p, sk.p, sv.p, s);
+    tk.release();
+    tv.release();
+    tmark("  galerkin: row sorts");
+    DBuf<uint64_t> key(T + 1, s);
+    if (T > 0) LAUNCH_G(group_size(m, T), k_gal_keys, m, s, m, pa.p, sk.p, cb, key.p);
+    LAP_CHECK_LAUNCH();
+    sk.release();
+    csr_combine_sorted(m, cb, T, key, sv, ilogb_pos(L.maxw) + 1, L.nnz, N, s);
+}
+
 static void galerkin(lap_hierarchy *h, Level &L, Level &N, cudaStream_t s) {
     const int64_t n = L.n, m = L.m;
     // members of every aggregate, ascending (stable radix sort by aggregate id)
@@ -2238,7 +2392,12 @@ static void galerkin(lap_hierarchy *h, Level &L, Level &N, cudaStream_t s) {
     S.ostart = mem_ptr.p;
     S.agg = L.agg;
     const int cb = bitlen_u64((uint64_t)(m > 0 ? m : 1));
-    csr_from_source(S, n, m, cb, ilogb_pos(L.maxw) + 1, L.nnz, true, N, s);
+    // the ordered path pays off when coarse rows are short (per-row sorts); dense
+    // coarse levels (thousands of terms per row: cfg 3/4 below level 0) keep the
+    // one device-wide radix sort
+    if (gal_fast_enabled() && L.nnz < ((int64_t)1 << 28) && L.nnz <= GAL_ORDERED_MAX_AVG * m)
+        galerkin_fast(h, L, N, members.p, k2.p, mem_ptr.p, s);
+    else csr_from_source(S, n, m, cb, ilogb_pos(L.maxw) + 1, L.nnz, true, N, s);
     h->cur.edges += L.nnz;
 }
 
@@ -2334,6 +2493,7 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
     // --- O-S0 validate
     {
         DBuf<int> flag(1, s);
+        DBuf<unsigned long long> hsum(2, s);
         LAP_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
         if (n > 0) {
             int64_t first = d2h_scalar(rp, s);
@@ -2341,12 +2501,22 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
             k_validate_rowptr<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(n, nnz, rp, flag.p); ++g_kl;
             LAP_CHECK_LAUNCH();
             if (d2h_scalar(flag.p, s)) throw Error{LAP_EGRAPH, "row_ptr is not monotone within [0, nnz]"};
-            LAUNCH_G(group_size(n, nnz), k_validate, n, s, n, rp, col, w, flag.p);
+            LAP_CUDA(cudaMemsetAsync(hsum.p, 0, 2 * sizeof(unsigned long long), s));
+            LAUNCH_G(group_size(n, nnz), k_validate, n, s, n, rp, col, w, flag.p, symcheck_mode() == 0 ? hsum.p : nullptr);
             LAP_CHECK_LAUNCH();
         }
         if (d2h_scalar(flag.p, s)) throw Error{LAP_EGRAPH, "graph is not a valid symmetric positive-weight adjacency"};
         tr.mark("validate", 0);
-        if (!is_symmetric(n, nnz, rp, col, w, s)) throw Error{LAP_EGRAPH, "graph is not symmetric (w_ij != w_ji)"};
+        if (symcheck_mode() == 0) {
+            unsigned long long hh[2] = {0, 0};
+            if (n > 0) {
+                LAP_CUDA(cudaMemcpyAsync(hh, hsum.p, sizeof(hh), cudaMemcpyDeviceToHost, s));
+                LAP_CUDA(cudaStreamSynchronize(s));
+            }
+            if (hh[0] | hh[1]) throw Error{LAP_EGRAPH, "graph is not symmetric (w_ij != w_ji)"};
+        } else if (!is_symmetric(n, nnz, rp, col, w, s)) {
+            throw Error{LAP_EGRAPH, "graph is not symmetric (w_ij != w_ji)"};
+        }
         tr.mark("symmetry", 0);
         if (!is_connected(n, nnz, rp, col, s)) throw Error{LAP_EDISCONNECTED, "graph is disconnected"};
         tr.mark("connectivity", 0);

@@ -189,6 +189,15 @@ __global__ void k_chunk_fill(int64_t nrows, int64_t row0, const int64_t *first, 
     }
 }
 
+template <class T>
+static void scan_excl(const T *in, T *out, int64_t n, cudaStream_t s) {
+    size_t bytes = 0;
+    LAP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s));
+    DBuf<char> tmp((int64_t)bytes, s);
+    LAP_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, in, out, n, s));
+    g_kl += 2;
+}
+
 // ---------------------------------------------------------------- per-row sorts
 // Every row of a CSR sorted by column (rows independent, columns of a row
 // distinct), by row length class:
@@ -205,6 +214,7 @@ __global__ void k_chunk_fill(int64_t nrows, int64_t row0, const int64_t *first, 
 // level-0 relabel.
 constexpr int ROWSORT_MED = 2048;  // 256 threads x 8 entries
 constexpr int ROWSORT_SMALL = 256;  // 64 threads x 4 entries
+constexpr int ROWSORT_SEG_AVG = 16384;  // long rows: cub segmented sort up to this average length
 template <int N>
 __device__ __forceinline__ void reg_bitonic(uint64_t (&a)[N]) {
 #pragma unroll
@@ -369,6 +379,40 @@ __global__ void k_seg_bounds(int64_t m, const int32_t *__restrict__ list, const 
     }
 }
 
+__global__ void k_seg_len(int64_t m, const int64_t *__restrict__ beg, const int64_t *__restrict__ end,
+                          int64_t *__restrict__ len) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x)
+        len[t] = end[t] - beg[t];
+}
+__global__ void k_long_gather(int64_t B, const int64_t *__restrict__ beg, const int64_t *__restrict__ loff, int cbits,
+                              const int32_t *__restrict__ kin, const double *__restrict__ vin, uint64_t *__restrict__ k1,
+                              double *__restrict__ v1) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = warp; r < B; r += nwarps) {
+        const int64_t a = beg[r], o = loff[r], len = loff[r + 1] - o;
+        for (int64_t q = lane; q < len; q += 32) {
+            k1[o + q] = ((uint64_t)r << cbits) | (uint64_t)(uint32_t)kin[a + q];
+            v1[o + q] = vin[a + q];
+        }
+    }
+}
+__global__ void k_long_scatter(int64_t B, const int64_t *__restrict__ beg, const int64_t *__restrict__ loff, int cbits,
+                               const uint64_t *__restrict__ k2, const double *__restrict__ v2, int32_t *__restrict__ kout,
+                               double *__restrict__ vout) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t mask = (1ULL << cbits) - 1;
+    for (int64_t r = warp; r < B; r += nwarps) {
+        const int64_t a = beg[r], o = loff[r], len = loff[r + 1] - o;
+        for (int64_t q = lane; q < len; q += 32) {
+            kout[a + q] = (int32_t)(k2[o + q] & mask);
+            vout[a + q] = v2[o + q];
+        }
+    }
+}
 // rows of length > minlen (minlen >= 32) sorted: kin/vin -> kout/vout
 static void sort_rows_min(int64_t n, const int64_t *rp, int64_t nnz, int cbits, int64_t minlen, const int32_t *kin,
                           const double *vin, int32_t *kout, double *vout, cudaStream_t s) {
@@ -394,16 +438,41 @@ static void sort_rows_min(int64_t n, const int64_t *rp, int64_t nnz, int cbits, 
     }
     trace_mark("    rowsort: block rows");
     if (hc[2] > 0) {
-        if (nnz >= ((int64_t)1 << 31)) throw Error{LAP_EINVAL, "sort_rows: rows longer than 2048 entries in a CSR of >= 2^31 entries"};
-        DBuf<int64_t> beg(hc[2], s), end(hc[2], s);
-        k_seg_bounds<<<grid_for(hc[2], 256, 148 * 4), 256, 0, s>>>(hc[2], lng.p, rp, beg.p, end.p);
-        size_t bytes = 0;
-        LAP_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, (int)nnz, hc[2], beg.p, end.p,
-                                                     s));
-        DBuf<char> tmp((int64_t)bytes, s);
-        LAP_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp.p, bytes, kin, kout, vin, vout, (int)nnz, hc[2], beg.p, end.p, s));
-        g_kl += 2;
-        trace_mark("    rowsort: long rows (cub)");
+        // rows longer than ROWSORT_MED (hubs, dense coarse rows): cub's segmented
+        // sort over just those rows; when they are few and huge (cub gives a
+        // segment to one block), ONE device-wide radix sort of their entries
+        // keyed (list index << cbits | column) instead
+        const int64_t B = hc[2];
+        DBuf<int64_t> beg(B + 1, s), end(B + 1, s), len(B + 1, s), loff(B + 1, s);
+        k_seg_bounds<<<grid_for(B, 256, 148 * 4), 256, 0, s>>>(B, lng.p, rp, beg.p, end.p);
+        k_seg_len<<<grid_for(B, 256, 148 * 4), 256, 0, s>>>(B, beg.p, end.p, len.p);
+        LAP_CUDA(cudaMemsetAsync(len.p + B, 0, sizeof(int64_t), s));
+        scan_excl(len.p, loff.p, B + 1, s);
+        const int64_t Tl = d2h(loff.p + B, s);
+        if (Tl <= (int64_t)ROWSORT_SEG_AVG * B && nnz < ((int64_t)1 << 31)) {
+            size_t bytes = 0;
+            LAP_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, (int)nnz, (int)B, beg.p,
+                                                         end.p, s));
+            DBuf<char> tmp((int64_t)bytes, s);
+            LAP_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp.p, bytes, kin, kout, vin, vout, (int)nnz, (int)B, beg.p,
+                                                         end.p, s));
+            g_kl += 4;
+            trace_mark("    rowsort: long rows (cub segmented)");
+        } else {
+            DBuf<uint64_t> k1(Tl, s), k2(Tl, s);
+            DBuf<double> v1(Tl, s), v2(Tl, s);
+            k_long_gather<<<grid_for(B * 32, 256, 148 * 8), 256, 0, s>>>(B, beg.p, loff.p, cbits, kin, vin, k1.p, v1.p);
+            size_t bytes = 0;
+            int lb = 1;
+            while (lb < 40 && ((int64_t)1 << lb) <= B) lb++;
+            const int end_bit = std::min(64, cbits + lb);
+            LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k1.p, k2.p, v1.p, v2.p, Tl, 0, end_bit, s));
+            DBuf<char> tmp((int64_t)bytes, s);
+            LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, k1.p, k2.p, v1.p, v2.p, Tl, 0, end_bit, s));
+            k_long_scatter<<<grid_for(B * 32, 256, 148 * 8), 256, 0, s>>>(B, beg.p, loff.p, cbits, k2.p, v2.p, kout, vout);
+            g_kl += 5;
+            trace_mark("    rowsort: long rows (global radix)");
+        }
     }
     LAP_CHECK_LAUNCH();
 }
@@ -416,14 +485,6 @@ void sort_rows(int64_t n, const int64_t *rp, int64_t nnz, int cbits, const int32
     sort_rows_min(n, rp, nnz, cbits, 64, kin, vin, kout, vout, s);
 }
 
-template <class T>
-static void scan_excl(const T *in, T *out, int64_t n, cudaStream_t s) {
-    size_t bytes = 0;
-    LAP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s));
-    DBuf<char> tmp((int64_t)bytes, s);
-    LAP_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, in, out, n, s));
-    g_kl += 2;
-}
 
 int64_t build_chunks(const int64_t *rp, int64_t row0, int64_t nrows, int64_t minlen, int32_t **crow,
                             int32_t **cidx, int32_t **cslot, double **cpart, int32_t **ccnt, cudaStream_t s) {

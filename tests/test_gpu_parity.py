@@ -123,6 +123,49 @@ def test_degenerate_inputs(P):
     assert np.allclose(x, [0.5, -0.5])
 
 
+@pytest.mark.parametrize("mode", ["hash", "sort", "search"])
+def test_symmetry_check_modes(mode):
+    """The three symmetry checks (LAP_SYMCHECK: the default multiset
+    fingerprint computed by k_validate, the exact transposed sort, the exact
+    per-entry search) accept symmetric graphs and reject asymmetric ones: a
+    one-ulp weight change, a missing reverse entry, weights swapped between two
+    edges (w_ij = w_kl = a, w_ji = w_lk = b), on a random weighted graph."""
+    import os
+    import subprocess
+    import sys
+    code = ("import numpy as np, lapgen, paper_1705_06266_b200 as P\n"
+            "g = lapgen.barabasi_albert(3000, 4)\n"
+            "h = P.Hierarchy(g); assert h.nlev >= 2\n"
+            "rp, col, w = g.row_ptr.copy(), g.col.copy(), g.w.copy()\n"
+            "def rev(i, j):\n"
+            "    return rp[j] + int(np.searchsorted(col[rp[j]:rp[j + 1]], i))\n"
+            "def bad(rp2, col2, w2):\n"
+            "    try:\n"
+            "        P.Hierarchy(lapgen.Graph(len(rp2) - 1, rp2, col2, w2)); return False\n"
+            "    except P.LapError as e:\n"
+            "        return e.code == P.LAP_EGRAPH\n"
+            "rng = np.random.default_rng(7)\n"
+            "for t in range(5):\n"
+            "    k = int(rng.integers(len(col))); w2 = w.copy(); w2[k] = np.nextafter(w2[k], 9.0)\n"
+            "    assert bad(rp, col, w2), 'ulp'\n"
+            "    i = int(np.searchsorted(rp, k, side='right') - 1); j = int(col[k]); k2 = rev(i, j)\n"
+            "    assert k2 != k and col[k2] == i\n"
+            "    w3 = w.copy(); w3[k], w3[k2] = 1.0, 2.0\n"
+            "    k3 = int(rng.integers(len(col))); i3 = int(np.searchsorted(rp, k3, side='right') - 1); j3 = int(col[k3])\n"
+            "    k4 = rev(i3, j3)\n"
+            "    if len({k, k2, k3, k4}) == 4:\n"
+            "        w3[k3], w3[k4] = 1.0, 2.0  # (i,j,1) (j,i,2) (i3,j3,1) (j3,i3,2): swapped, still asymmetric\n"
+            "        assert bad(rp, col, w3), 'swap'\n"
+            "    keep = np.ones(len(col), bool); keep[k2] = False\n"
+            "    rp4 = rp.copy(); rp4[j + 1:] -= 1\n"
+            "    assert bad(rp4, col[keep], w[keep]), 'missing'\n"
+            "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = dict(os.environ, LAP_SYMCHECK=mode)
+    r = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+
+
 def test_invalid_graphs_rejected(P):
     bad_sym = lapgen.Graph(2, np.array([0, 1, 1]), np.array([1], np.int32), np.array([1.0]))
     with pytest.raises(P.LapError) as e:
@@ -287,9 +330,11 @@ def test_fused_transfers_bitwise(P, tmp_path):
 
 
 def test_memory_lean_paths_bit_exact(P):
-    """The memory-lean setup paths give the oracle's hierarchy bit for bit:
-    terms built in many small batches of output rows (LAP_TERM_BATCH), the
-    search-based symmetry check (LAP_SYMCHECK=search), and released logical
+    """The memory-lean and alternative setup paths give the oracle's hierarchy
+    bit for bit: terms built in many small batches of output rows
+    (LAP_TERM_BATCH; with the shared-memory Galerkin only its hub rows take
+    that path), the global-sort Galerkin (LAP_GAL_FAST=0), the exact
+    search- / sort-based symmetry checks (LAP_SYMCHECK), and released logical
     copies (keep_logical = 0) read back through lap_level_rows."""
     import os
     import subprocess
@@ -319,7 +364,8 @@ def test_memory_lean_paths_bit_exact(P):
             "    assert e.code == P.LAP_EGRAPH\n"
             "print('ok')\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    for env in [{"LAP_TERM_BATCH": "3000"}, {"LAP_SYMCHECK": "search"}, {"LAP_TERM_BATCH": "100000", "LAP_SYMCHECK": "search"}]:
+    for env in [{"LAP_TERM_BATCH": "3000"}, {"LAP_SYMCHECK": "search"}, {"LAP_TERM_BATCH": "100000", "LAP_SYMCHECK": "search"},
+                {"LAP_GAL_FAST": "0", "LAP_SYMCHECK": "sort"}, {"LAP_GAL_FAST": "0", "LAP_TERM_BATCH": "3000"}]:
         e = dict(os.environ, **env)
         r = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, timeout=900, cwd=root)
         assert r.returncode == 0 and "ok" in r.stdout, (env, r.stderr[-3000:])
