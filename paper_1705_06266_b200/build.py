@@ -43,14 +43,24 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     objdir = os.path.join(HERE, "_build")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
+    headers = [f for f in _sources() if not f.endswith(".cu")]
+    hdr_time = max(os.path.getmtime(f) for f in headers)
+    jobs, objs = [], []
     for unit, extra in UNITS.items():
+        src = os.path.join(CSRC, unit)
         obj = os.path.join(objdir, unit.replace(".cu", ".o"))
-        cmd = [nvcc, *ARCH, *COMMON, *extra, "-c", os.path.join(CSRC, unit), "-o", obj]
+        objs.append(obj)
+        if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(src), hdr_time):
+            jobs.append([nvcc, *ARCH, *COMMON, *extra, "-c", src, "-o", obj])
+    # translation units compile independently: in parallel
+    from concurrent.futures import ThreadPoolExecutor
+    def run(cmd):
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)
-        objs.append(obj)
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        for f in [ex.submit(run, c) for c in jobs]:
+            f.result()
     tmp = SO + f".tmp{os.getpid()}"
     subprocess.check_call([nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-lnccl"])
     os.replace(tmp, SO)

@@ -222,6 +222,125 @@ __global__ void __launch_bounds__(256) k_blk_spmv(int64_t nslices, int64_t nshor
     }
 }
 
+// The same SpMM for K = 16 / 32 columns with the LANES owning the columns
+// (K lanes per row, 32 / K rows of a slice at a time): a register array of K
+// accumulators per thread and K-wide vector gathers would spill, while here
+// every x_j gather is ONE coalesced K*8-byte warp access (4 / 8 sectors, all
+// bytes used) and each thread keeps one accumulator.  A row's index and
+// weight loads are warp-uniform (broadcast; the slice's 128-byte col line
+// serves its 32 rows from L1); padded SELL slots (w = 0) skip their gather.
+// Per column the products are added in the row's slot order, as in the
+// narrow kernel; chunk partials are combined in chunk order.
+template <int EPI, int K>
+__global__ void __launch_bounds__(256) k_blk_spmv_wide(int64_t nslices, int64_t nshort, int64_t n,
+                                                       const int64_t *__restrict__ sp, const int32_t *__restrict__ ec,
+                                                       const double *__restrict__ ew, const int64_t *__restrict__ rp,
+                                                       const int32_t *__restrict__ col, const double *__restrict__ w,
+                                                       const double *__restrict__ d, BChunks R, BArgs a) {
+    static_assert(K == 16 || K == 32, "wide SpMM: K = 16 or 32");
+    constexpr int RPW = 32 / K;  // rows of a slice per warp pass
+    pdl_begin();
+    __shared__ double shd[8][32];
+    const int lane = threadIdx.x & 31, c = lane & (K - 1), sub = lane / K;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double dacc = 0.0;
+    auto epi = [&](int64_t i, double ax) {  // column c of row i
+        const double di = d[i], xi = a.x[i * K + c];
+        const double lx = di * xi - ax;
+        if (EPI == BE_DOT) {
+            a.y[i * K + c] = lx;
+            dacc += xi * lx;
+        } else if (EPI == BE_RESID) {
+            a.y[i * K + c] = a.b[i * K + c] - lx;
+        } else {
+            const double r = (a.b[i * K + c] - lx) / di;
+            const double dvo = EPI == BE_CHEB ? a.c1 * a.dv[i * K + c] + a.c2 * r : a.c2 * r;
+            a.dv[i * K + c] = dvo;
+            a.y[i * K + c] = xi + dvo;
+        }
+    };
+    for (int64_t t = warp; t < nslices + R.nchunks; t += nwarps) {
+        if (t < nslices) {
+            const int64_t beg = sp[t];
+            const int width = (int)((sp[t + 1] - beg) >> 5);
+            for (int r0 = 0; r0 < 32; r0 += RPW) {
+                const int r = r0 + sub;
+                const int64_t i = t * 32 + r;
+                double ax = 0.0;
+                for (int q = 0; q < width; q += 8) {
+                    int32_t jj[8];
+                    double wv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; u++) {
+                        jj[u] = 0;
+                        wv[u] = 0.0;
+                        if (q + u < width) {
+                            jj[u] = __ldg(&ec[beg + (int64_t)(q + u) * 32 + r]);
+                            wv[u] = __ldg(&ew[beg + (int64_t)(q + u) * 32 + r]);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; u++)
+                        if (wv[u] != 0.0) ax += wv[u] * __ldg(a.x + (int64_t)jj[u] * K + c);
+                }
+                if (i < nshort) epi(i, ax);
+            }
+        } else {
+            const int64_t ch = t - nslices;
+            const int64_t i = R.crow[ch], j = R.cidx[ch];
+            const int64_t rb = rp[i], re = rp[i + 1], b0 = rb + j * LCHUNK, e0 = min(re, b0 + LCHUNK);
+            double ax = 0.0;
+            for (int64_t q0 = b0; q0 < e0; q0 += 32) {
+                const int cnt = (int)min((int64_t)32, e0 - q0);
+                const int32_t cl = lane < cnt ? __ldg(&col[q0 + lane]) : 0;
+                const double wl = lane < cnt ? __ldg(&w[q0 + lane]) : 0.0;
+#pragma unroll
+                for (int v = 0; v < 32 / RPW; v++) {  // entry v * RPW + sub of this batch
+                    const int u = v * RPW + sub;
+                    const int32_t jj = __shfl_sync(0xffffffffu, cl, u);
+                    const double ww = __shfl_sync(0xffffffffu, wl, u);
+                    if (u < cnt) ax += ww * __ldg(a.x + (int64_t)jj * K + c);
+                }
+            }
+            if (RPW == 2) ax += __shfl_xor_sync(0xffffffffu, ax, 16);
+            const int slot = R.cslot[ch];
+            if (slot < 0) {  // the whole row in one chunk
+                if (lane < K) epi(i, ax);
+                continue;
+            }
+            const int nch = (int)((re - rb + LCHUNK - 1) / LCHUNK);
+            if (lane < K) R.cpart[ch * K + c] = ax;
+            __threadfence();
+            __syncwarp();
+            int last = 0;
+            if (lane == 0) last = atomicAdd(&R.ccnt[slot], 1) == nch - 1;
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (!last) continue;
+            __threadfence();
+            if (lane < K) {  // chunk order, per column
+                const int64_t c0 = ch - j;
+                double s2 = 0.0;
+                for (int q = 0; q < nch; q++) s2 += __ldcg(&R.cpart[(c0 + q) * K + c]);
+                epi(i, s2);
+            }
+            __syncwarp();
+            if (lane == 0) R.ccnt[slot] = 0;
+        }
+    }
+    if (EPI == BE_DOT) {
+        if (RPW == 2) dacc += __shfl_xor_sync(0xffffffffu, dacc, 16);
+        const int wid = threadIdx.x >> 5;
+        if (lane < K) shd[wid][c] = dacc;
+        __syncthreads();
+        if (threadIdx.x < K) {
+            double r = 0.0;
+            for (int q = 0; q < (int)(blockDim.x >> 5); q++) r += shd[q][threadIdx.x];
+            a.partials[threadIdx.x * gridDim.x + blockIdx.x] = r;
+        }
+    }
+}
+
 template <int K>
 __global__ void k_blk_cheb_first(int64_t n, const double *__restrict__ b, const double *__restrict__ d,
                                  double inv_theta, double *__restrict__ x, double *__restrict__ dv) {
@@ -413,6 +532,67 @@ __global__ void __launch_bounds__(256) k_blk_xr(int64_t n, const double *__restr
         if (threadIdx.x == 0) part[c * gridDim.x + blockIdx.x] = t;
     }
 }
+// K >= 16: the same sums and update with a thread per ELEMENT of the n x K
+// block (coalesced; the grid stride is a multiple of K, so a thread always
+// serves column threadIdx.x % K) and a fixed-order per-column combine of the
+// block's 256 / K threads -- a register array of K (or 3K) partials per thread
+// would hold 100-250 registers
+template <int K>
+__device__ __forceinline__ double blk_col_sum(double v, double *sh) {  // -> threads 0..K-1: column sums
+    __syncthreads();
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (threadIdx.x < K)
+        for (int q = threadIdx.x; q < (int)blockDim.x; q += K) r += sh[q];
+    return r;
+}
+template <int K, int NS>
+__global__ void __launch_bounds__(256) k_blk_sums_w(int64_t n, const double *__restrict__ a0,
+                                                    const double *__restrict__ a1, const double *__restrict__ a2,
+                                                    double *__restrict__ part) {
+    pdl_begin();
+    __shared__ double sh[256];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * K; t += (int64_t)gridDim.x * blockDim.x) {
+        const double x0 = a0[t], x1 = a1 ? a1[t] : 1.0;
+        if (NS == 1) {
+            s0 += x0 * x1;
+        } else {
+            s0 += x0;
+            s1 += x0 * x1;
+            s2 += x1;
+        }
+    }
+    const int c = threadIdx.x;
+    double r = blk_col_sum<K>(s0, sh);
+    if (c < K) part[(NS * c) * gridDim.x + blockIdx.x] = r;
+    if (NS == 3) {
+        r = blk_col_sum<K>(s1, sh);
+        if (c < K) part[(NS * c + 1) * gridDim.x + blockIdx.x] = r;
+        r = blk_col_sum<K>(s2, sh);
+        if (c < K) part[(NS * c + 2) * gridDim.x + blockIdx.x] = r;
+    }
+}
+template <int K>
+__global__ void __launch_bounds__(256) k_blk_xr_w(int64_t n, const double *__restrict__ p,
+                                                  const double *__restrict__ q, double *__restrict__ x,
+                                                  double *__restrict__ r, const double *__restrict__ sc,
+                                                  double *__restrict__ part) {
+    pdl_begin();
+    __shared__ double sh[256];
+    const double *s = sc + 16 * (threadIdx.x % K);
+    const double alpha = (s[4] != 0.0 && s[1] != 0.0) ? s[0] / s[1] : 0.0;
+    double acc = 0.0;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * K; t += (int64_t)gridDim.x * blockDim.x) {
+        x[t] += alpha * p[t];
+        const double ri = r[t] - alpha * q[t];
+        r[t] = ri;
+        acc += ri * ri;
+    }
+    const double v = blk_col_sum<K>(acc, sh);
+    if (threadIdx.x < K) part[threadIdx.x * gridDim.x + blockIdx.x] = v;
+}
 // caller layout (n x k column-major, caller numbering) <-> block layout (storage order, row-major n x K)
 template <int K>
 __global__ void k_blk_in(int64_t n, int k, const int64_t *__restrict__ cmap, const double *__restrict__ B,
@@ -460,7 +640,8 @@ static void blk_spmv(lap_hierarchy *h, const Level &L, double *cpart, int epi, c
                      unsigned grid) {
     BChunks R{L.nchunks, L.chunk_row, L.chunk_idx, L.chunk_slot, L.chunk_cnt, cpart};
 #define BLK_LAUNCH(E)                                                                                             \
-    launch_pdl(k_blk_spmv<E, K>, grid, 256, s, L.nslices, L.c_end[0], L.n, (const int64_t *)L.slice_ptr,         \
+    launch_pdl(K >= 16 ? k_blk_spmv_wide<E, (K >= 16 ? K : 16)> : k_blk_spmv<E, K>, grid, 256, s, L.nslices,      \
+               L.c_end[0], L.n, (const int64_t *)L.slice_ptr,                                                     \
                (const int32_t *)L.ell_col, (const double *)L.ell_w, (const int64_t *)L.srp,                       \
                (const int32_t *)L.scol, (const double *)L.sw, (const double *)L.sd, R, a)
     switch (epi) {
@@ -622,7 +803,10 @@ template <int K, int NS>
 static void blk_sums(lap_hierarchy *h, BlockWork &W, const double *a0, const double *a1, int s0, int s1, int s2,
                      cudaStream_t s) {
     const int64_t n = h->lev[0].n;
-    launch_pdl(k_blk_sums<K, NS>, BLK_RED, 256, s, n, a0, a1, (const double *)nullptr, W.part);
+    if constexpr (K >= 16)
+        launch_pdl(k_blk_sums_w<K, NS>, BLK_RED, 256, s, n, a0, a1, (const double *)nullptr, W.part);
+    else
+        launch_pdl(k_blk_sums<K, NS>, BLK_RED, 256, s, n, a0, a1, (const double *)nullptr, W.part);
     launch_pdl(k_blk_reduce, 1, 256, s, (const double *)W.part, BLK_RED, NS * K, NS, W.sc, s0, s1, s2);
     h->cur.launches += 2;
 }
@@ -649,7 +833,11 @@ static void blk_spmv_part(lap_hierarchy *h, BlockWork &W, cudaStream_t s) {
     a.partials = W.part;
     blk_spmv<K>(h, L0, W.lcpart[0], BE_DOT, a, s, g);
     launch_pdl(k_blk_reduce, 1, 256, s, (const double *)W.part, (int)g, K, 1, W.sc, (int)S_PQ, 0, 0);
-    launch_pdl(k_blk_xr<K>, BLK_RED, 256, s, n, (const double *)W.p, (const double *)W.q, W.x, W.r,
+    if constexpr (K >= 16)
+        launch_pdl(k_blk_xr_w<K>, BLK_RED, 256, s, n, (const double *)W.p, (const double *)W.q, W.x, W.r,
+                   (const double *)W.sc, W.part);
+    else
+        launch_pdl(k_blk_xr<K>, BLK_RED, 256, s, n, (const double *)W.p, (const double *)W.q, W.x, W.r,
                (const double *)W.sc, W.part);
     launch_pdl(k_blk_reduce, 1, 256, s, (const double *)W.part, BLK_RED, K, 1, W.sc, (int)S_RR, 0, 0);
     h->cur.launches += 3;
@@ -754,12 +942,14 @@ static void solve_block_k(lap_hierarchy *h, int k, const double *B, double *X, d
     for (int c = 0; c < k; c++) relres[c] = bn[c] > 0.0 ? std::sqrt(hs[16 * c + S_TRUE]) / bn[c] : 0.0;
 }
 
-// k right-hand sides (1 <= k <= 8), device buffers in the caller's layout: B, X n x k column-major
+// k right-hand sides (1 <= k <= 32), device buffers in the caller's layout: B, X n x k column-major
 void solve_block(lap_hierarchy *h, int k, const double *B, double *X, double tol, int32_t *iters, double *relres,
                  int *conv, cudaStream_t s) {
     if (k <= 2) solve_block_k<2>(h, k, B, X, tol, iters, relres, conv, s);
     else if (k <= 4) solve_block_k<4>(h, k, B, X, tol, iters, relres, conv, s);
-    else solve_block_k<8>(h, k, B, X, tol, iters, relres, conv, s);
+    else if (k <= 8) solve_block_k<8>(h, k, B, X, tol, iters, relres, conv, s);
+    else if (k <= 16) solve_block_k<16>(h, k, B, X, tol, iters, relres, conv, s);
+    else solve_block_k<32>(h, k, B, X, tol, iters, relres, conv, s);
 }
 
 }  // namespace lap

@@ -585,8 +585,8 @@ lap_status lap_solve(lap_hierarchy *h, const double *b, double *x, double tol, i
 
 lap_status lap_solve_block(lap_hierarchy *h, int32_t k, const double *B, double *X, double tol, int32_t *iters,
                            double *rel_residual, void *stream) {
-    if (!h || !B || !X || !iters || !rel_residual || k < 1 || k > 8 || h->dist) {
-        lap::set_error("lap_solve_block: invalid arguments (1 <= k <= 8, single-GPU hierarchy)");
+    if (!h || !B || !X || !iters || !rel_residual || k < 1 || k > 32 || h->dist) {
+        lap::set_error("lap_solve_block: invalid arguments (1 <= k <= 32, single-GPU hierarchy)");
         return LAP_EINVAL;
     }
     LAP_API_BEGIN

@@ -24,7 +24,7 @@ for cfg in want:
     t1 = statistics.median(ms1[1:])
     print(json.dumps({"cfg": cfg, "k": 1, "api": "lap_solve", "solve_ms": t1, "iters": it1,
                       "edges_rhs_per_s": e1 / (t1 * 1e-3)}), flush=True)
-    for k in (2, 4, 8):
+    for k in [int(v) for v in os.environ.get("BLOCK_KS", "2,4,8").split(",")]:
         B = torch.from_numpy(np.stack([lapgen.rhs(g.n, seed=j) for j in range(k)])).to(dev)
         X = torch.zeros_like(B)
         ms = []
