@@ -176,11 +176,10 @@ def level_table(h):
         L = {"kind": kind, "n": n, "nnz": nnz, "lambda": lam}
         if kind == 0 and l + 1 < h.nlev:
             L["m"] = h.level_info(l + 1)[1]
-        if kind == 1:
-            lv = h.level(l)
-            deg = np.diff(lv["row_ptr"])
-            L["nF"] = int((lv["fmap"] < 0).sum())
-            L["nnz_fc"] = int(deg[lv["fmap"] < 0].sum())
+        if kind == 1:  # works when the logical CSR was released too (cfg 5)
+            frows = np.flatnonzero(h.level_map(l) < 0)
+            L["nF"] = int(len(frows))
+            L["nnz_fc"] = int(h.level_degrees(l, frows).sum())
         out.append(L)
     return out
 

@@ -239,6 +239,16 @@ lap_status lap_setup_dist(const lap_graph *g, const lap_params *p, lap_comm *c, 
 /* Host-only (no GPU needed): the piece map of a sharded level with n rows over
  * nranks pieces: dist[t] = piece * piece_size + slot of storage row rows[t]
  * (block-cyclic in blocks of 256 rows); *piece_size = padded piece length. */
+/* SURVEY N1 (distributed setup): lap_setup_dist splits every
+ * coarse-operator term build (Galerkin R L P, Schur complement, relabel of a
+ * big graph) by output rows over the communicator's ranks, each range
+ * holding about 1/P of the terms, and gathers the ranges on every rank (the
+ * result is the single-GPU operator bit for bit).  This is the split rule,
+ * host-only: cum[0..nout] = terms of the output rows before row o
+ * (non-decreasing); bounds[0..nranks]: rank r builds rows [bounds[r],
+ * bounds[r+1]), bounds[r] = the first o with cum[o] * nranks >= r * cum[nout].
+ * LAP_EINVAL on a decreasing or negative cum. */
+lap_status lap_setup_split(int64_t nout, const int64_t *cum, int32_t nranks, int64_t *bounds);
 lap_status lap_dist_index(int64_t n, int32_t nranks, int64_t m, const int64_t *rows, int64_t *dist,
                           int64_t *piece_size);
 

@@ -32,6 +32,16 @@ __host__ __device__ __forceinline__ double unit_from(uint64_t u) {
     return (double)(u >> 11) * 0x1.0p-53;
 }
 
+__host__ __device__ __forceinline__ double __longlong_as_double_hd(long long b) {
+#ifdef __CUDA_ARCH__
+    return __longlong_as_double(b);
+#else
+    double d;
+    __builtin_memcpy(&d, &b, sizeof d);
+    return d;
+#endif
+}
+
 __host__ __device__ __forceinline__ int bitlen_u64(uint64_t k) {
 #ifdef __CUDA_ARCH__
     return 64 - __clzll((long long)k);
@@ -57,6 +67,21 @@ __device__ __forceinline__ i128 canon_q(double t, int elo) {
     if (fabs(sc) < 9007199254740992.0) return (i128)__double2ll_rn(sc);  // |s| < 2^53: RNE to an integer
     const double hi = floor(sc * 0x1p-64);
     const double lo = sc - hi * 0x1p64;                                   // exact, in [0, 2^64)
+    return (i128)__double2ll_rz(hi) * ((i128)1 << 64) + (i128)__double2ull_rz(lo);
+}
+
+// 2^-elo when it is a normal double (every realistic instance), else 0: the
+// hot kernels then scale by ONE multiplication -- the correctly rounded
+// product t * 2^-elo is exactly scalbn(t, -elo) -- instead of scalbn's
+// special-case sequence
+__host__ __device__ __forceinline__ double canon_scale(int elo) {
+    return (-elo >= -1022 && -elo <= 1023) ? __longlong_as_double_hd((long long)(1023 - elo) << 52) : 0.0;
+}
+__device__ __forceinline__ i128 canon_q_s(double t, double s2, int elo) {
+    const double sc = s2 != 0.0 ? t * s2 : scalbn(t, -elo);
+    if (fabs(sc) < 9007199254740992.0) return (i128)__double2ll_rn(sc);
+    const double hi = floor(sc * 0x1p-64);
+    const double lo = sc - hi * 0x1p64;
     return (i128)__double2ll_rz(hi) * ((i128)1 << 64) + (i128)__double2ull_rz(lo);
 }
 

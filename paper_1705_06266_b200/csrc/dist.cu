@@ -1082,6 +1082,115 @@ void free_dist(lap_hierarchy *h) {
 
 }  // namespace lap
 
+namespace lap {
+
+// ------------------------------------------------------------------ distributed setup
+// The coarse-operator term builds (Galerkin R L P, the Schur complement, the
+// level-0 relabel of a big graph) are split by output rows over the ranks of
+// the setup communicator (setup.cu build_split); here the ranges are gathered
+// into the whole operator on every rank: per root rank, an ncclBroadcast of its
+// rows' row_ptr / col / w pieces (grouped: NCCL has no allgatherv), then the
+// row_ptr pieces are shifted by their entry offsets.  On a virtual grid (one
+// process) the pieces are device copies.  Only discrete data and final CanonSum
+// values move: the result is the single-GPU operator bit for bit.
+static thread_local lap_comm *g_setup_comm = nullptr;
+
+SetupCommScope::SetupCommScope(lap_comm *c) { g_setup_comm = c; }
+SetupCommScope::~SetupCommScope() { g_setup_comm = nullptr; }
+
+int setup_nranks() { return g_setup_comm ? g_setup_comm->P : 1; }
+std::vector<int> setup_local_ranks() {
+    std::vector<int> r;
+    if (!g_setup_comm) {
+        r.push_back(0);
+    } else if (g_setup_comm->virt) {
+        for (int q = 0; q < g_setup_comm->P; q++) r.push_back(q);
+    } else {
+        r.push_back(g_setup_comm->rank);
+    }
+    return r;
+}
+__global__ void k_shift_rows(int64_t nr, const int64_t *__restrict__ in, int64_t off, int64_t *__restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nr; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in[i] + off;
+}
+__global__ void k_shift_rows_inplace(int64_t nr, int64_t *__restrict__ v, int64_t off) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nr; i += (int64_t)gridDim.x * blockDim.x)
+        v[i] += off;
+}
+void setup_gather(std::vector<Level> &pieces, const std::vector<int> &mine, const std::vector<int64_t> &bounds,
+                  Level &out, cudaStream_t s) {
+    const int P = (int)bounds.size() - 1;
+    const int64_t nout = bounds[P];
+    std::vector<int64_t> cnt(P, 0);
+    lap_comm *c = g_setup_comm;
+    const bool nccl = c && !c->virt && P > 1;
+    if (nccl) {  // entry counts of every rank's range
+        int64_t *dc = (int64_t *)dalloc(8 * (size_t)(P + 1), s);
+        LAP_CUDA(cudaMemcpyAsync(dc + P, &pieces[0].nnz, 8, cudaMemcpyHostToDevice, s));
+        NCCL_CHECK(ncclAllGather(dc + P, dc, 1, ncclInt64, c->world, s));
+        LAP_CUDA(cudaMemcpyAsync(cnt.data(), dc, 8 * P, cudaMemcpyDeviceToHost, s));
+        LAP_CUDA(cudaStreamSynchronize(s));
+        dfree(dc, s);
+    } else {
+        for (size_t q = 0; q < mine.size(); q++) cnt[mine[q]] = pieces[q].nnz;
+    }
+    std::vector<int64_t> off(P + 1, 0);
+    for (int r = 0; r < P; r++) off[r + 1] = off[r] + cnt[r];
+    out.n = nout;
+    out.nnz = off[P];
+    out.row_ptr = (int64_t *)dalloc(sizeof(int64_t) * (size_t)(nout + 1), s);
+    out.col = (int32_t *)dalloc(sizeof(int32_t) * (size_t)(out.nnz + 1), s);
+    out.w = (double *)dalloc(sizeof(double) * (size_t)(out.nnz + 1), s);
+    if (nccl) {
+        const Level &me = pieces[0];
+        NCCL_CHECK(ncclGroupStart());
+        for (int r = 0; r < P; r++) {
+            const bool root = r == c->rank;
+            const int64_t nr = bounds[r + 1] - bounds[r];
+            if (nr > 0)
+                NCCL_CHECK(ncclBroadcast(root ? (const void *)me.row_ptr : nullptr, out.row_ptr + bounds[r], (size_t)nr,
+                                         ncclInt64, r, c->world, s));
+            if (cnt[r] > 0) {
+                NCCL_CHECK(ncclBroadcast(root ? (const void *)me.col : nullptr, out.col + off[r], (size_t)cnt[r],
+                                         ncclInt32, r, c->world, s));
+                NCCL_CHECK(ncclBroadcast(root ? (const void *)me.w : nullptr, out.w + off[r], (size_t)cnt[r],
+                                         ncclFloat64, r, c->world, s));
+            }
+        }
+        NCCL_CHECK(ncclGroupEnd());
+        for (int r = 1; r < P; r++) {
+            const int64_t nr = bounds[r + 1] - bounds[r];
+            if (nr > 0 && off[r])
+                k_shift_rows_inplace<<<dg(nr), 256, 0, s>>>(nr, out.row_ptr + bounds[r], off[r]);
+        }
+    } else {
+        for (size_t q = 0; q < mine.size(); q++) {
+            const int r = mine[q];
+            const Level &pc = pieces[q];
+            const int64_t nr = bounds[r + 1] - bounds[r];
+            if (nr > 0) k_shift_rows<<<dg(nr), 256, 0, s>>>(nr, pc.row_ptr, off[r], out.row_ptr + bounds[r]);
+            if (cnt[r] > 0) {
+                LAP_CUDA(cudaMemcpyAsync(out.col + off[r], pc.col, 4 * (size_t)cnt[r], cudaMemcpyDeviceToDevice, s));
+                LAP_CUDA(cudaMemcpyAsync(out.w + off[r], pc.w, 8 * (size_t)cnt[r], cudaMemcpyDeviceToDevice, s));
+            }
+        }
+    }
+    LAP_CHECK_LAUNCH();
+    const int64_t tot = out.nnz;
+    LAP_CUDA(cudaMemcpyAsync(out.row_ptr + nout, &tot, 8, cudaMemcpyHostToDevice, s));
+    LAP_CUDA(cudaStreamSynchronize(s));  // (the host value above) before the pieces go
+    for (Level &pc : pieces) {
+        dfree(pc.row_ptr, s);
+        dfree(pc.col, s);
+        dfree(pc.w, s);
+        pc.row_ptr = nullptr;
+        pc.col = nullptr;
+        pc.w = nullptr;
+    }
+}
+}  // namespace lap
+
 // ------------------------------------------------------------------ C ABI (multi-GPU)
 extern "C" {
 
@@ -1170,6 +1279,14 @@ lap_status lap_dist_index(int64_t n, int32_t nranks, int64_t m, const int64_t *r
         if (rows[t] < 0 || rows[t] >= n) return LAP_EINVAL;
         dist[t] = pm.dist_of(rows[t]);
     }
+    return LAP_OK;
+}
+
+lap_status lap_setup_split(int64_t nout, const int64_t *cum, int32_t nranks, int64_t *bounds) {
+    if (nout < 0 || !cum || !bounds || nranks < 1) return LAP_EINVAL;
+    for (int64_t o = 0; o < nout; o++)
+        if (cum[o + 1] < cum[o] || cum[o] < 0) return LAP_EINVAL;
+    for (int r = 0; r <= nranks; r++) bounds[r] = lap::split_bound(r, nranks, nout, [&](int64_t o) { return cum[o]; });
     return LAP_OK;
 }
 

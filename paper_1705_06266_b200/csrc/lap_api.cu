@@ -492,7 +492,11 @@ lap_status lap_setup_dist(const lap_graph *g, const lap_params *pp, lap_comm *c,
         return LAP_EINVAL;
     }
     lap_hierarchy *h = nullptr;
-    lap_status st = lap_setup(g, &p, stream, &h);
+    lap_status st;
+    {
+        lap::SetupCommScope scope(c);  // the coarse-operator term builds split over the ranks
+        st = lap_setup(g, &p, stream, &h);
+    }
     if (st != LAP_OK && st != LAP_ESTALL) return st;
     try {
         if (h->lev[0].kind != lap::KIND_COARSEST) lap::build_dist(h, c, (cudaStream_t)stream, want_graphs != 0);

@@ -143,6 +143,8 @@ struct Level {
     bool sell_sorted = false;       // short rows degree-sorted
     bool smem_x = false;            // small dense-ish level: k_spmv_smem (x in shared memory, 16-bit columns)
     int spmv_nb = 8;                // SELL batch width of k_spmv (8, or 4 for mid-size levels)
+    bool unit = false;              // every stored weight is 1 (level 0 of a unit-weight graph): the
+                                    // solve SpMV reads the pattern only, 4 instead of 12 B per entry (N4)
     int spmv_vec = 0;               // > 0: k_spmv_vec, G lanes per row over the CSR (solve.cu)
     uint16_t *ell_col16 = nullptr;  // smem_x: 16-bit copies of ell_col / scol
     uint16_t *scol16 = nullptr;
@@ -228,6 +230,37 @@ struct lap_hierarchy {
 };
 
 namespace lap {
+
+// ---------------------------------------------------------------- distributed setup (dist.cu)
+// The communicator of the setup in progress (lap_setup_dist), else none: the
+// coarse-operator term builds are then split over its ranks (setup.cu
+// build_split) and gathered here.
+int setup_nranks();                   // 1 without a setup communicator
+std::vector<int> setup_local_ranks(); // ranks this process builds: {rank} (NCCL) or 0..P-1 (virtual grid)
+// pieces[q] = rows [bounds[r], bounds[r+1]) of the operator for r = mine[q]
+// (local row_ptr from 0); out <- the whole operator's row_ptr / col / w / nnz
+void setup_gather(std::vector<Level> &pieces, const std::vector<int> &mine, const std::vector<int64_t> &bounds,
+                  Level &out, cudaStream_t s);
+// the split rule of a term build over P ranks (device: setup.cu k_split_bounds;
+// host: lap_setup_split): bounds[r] = the first output row o with
+// cum(o) * P >= r * cum(nout), cum(o) = terms of the rows before o
+template <class Cum>
+__host__ __device__ inline int64_t split_bound(int r, int P, int64_t nout, Cum cum) {
+    if (r <= 0) return 0;
+    if (r >= P) return nout;
+    const __int128 want = (__int128)r * cum(nout);
+    int64_t lo = 0, hi = nout;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((__int128)cum(mid) * P >= want) hi = mid;
+        else lo = mid + 1;
+    }
+    return lo;
+}
+struct SetupCommScope {  // lap_setup_dist: the setup runs under this communicator
+    explicit SetupCommScope(lap_comm *c);
+    ~SetupCommScope();
+};
 
 // ---------------------------------------------------------------- kernels (host launchers)
 // setup (setup.cu)

@@ -524,7 +524,7 @@ static void row_sums(int64_t n, int64_t nnz, const int64_t *row_ptr, const doubl
 // duplicates of a key are one segment; each segment's CanonSum (instance e_max, K)
 // is formed directly from the fp64 terms.
 static void csr_combine_sorted(int64_t nrows, int cb, int64_t T, DBuf<uint64_t> &k2, DBuf<double> &v2, int e_max,
-                               int64_t K, Level &out, cudaStream_t s) {
+                               int64_t K, Level &out, cudaStream_t s, bool sums) {
     int64_t U = 0;
     out.n = nrows;
     out.row_ptr = (int64_t *)dalloc(sizeof(int64_t) * (size_t)(nrows + 1), s);
@@ -576,6 +576,7 @@ static void csr_combine_sorted(int64_t nrows, int cb, int64_t T, DBuf<uint64_t> 
         k_row_ptr_from_keys<<<grid_for(nrows + 1, 256, 148 * 16), 256, 0, s>>>(nrows, 0, k2.p, cb, out.row_ptr); ++g_kl;
     }
     (void)U;
+    if (!sums) return;  // a piece of a split build: the diagonal comes from the gathered rows
     out.d = (double *)dalloc(sizeof(double) * (size_t)(nrows > 0 ? nrows : 1), s);
     row_sums(nrows, out.nnz, out.row_ptr, out.w, out.d, &out.maxw, s);
     tmark("  terms: row sums");
@@ -584,7 +585,7 @@ static void csr_combine_sorted(int64_t nrows, int cb, int64_t T, DBuf<uint64_t> 
 // Build a level's CSR from unsorted (key=(row<<cb)|col, value) terms whose
 // duplicates are combined by CanonSum with instance (e_max, K).
 static void csr_from_terms(int64_t nrows, int cb, int64_t T, DBuf<uint64_t> &keys, DBuf<double> &vals,
-                           int e_max, int64_t K, bool combine, Level &out, cudaStream_t s) {
+                           int e_max, int64_t K, bool combine, Level &out, cudaStream_t s, bool sums = true) {
     int rb = bitlen_u64((uint64_t)(nrows > 0 ? nrows : 1));
     int end_bit = std::min(64, cb + rb);
     DBuf<uint64_t> k2(T, s);
@@ -599,7 +600,7 @@ static void csr_from_terms(int64_t nrows, int cb, int64_t T, DBuf<uint64_t> &key
     vals.release();
     tmark("  terms: sort");
     if (combine) {
-        csr_combine_sorted(nrows, cb, T, k2, v2, e_max, K, out, s);
+        csr_combine_sorted(nrows, cb, T, k2, v2, e_max, K, out, s, sums);
         return;
     }
     out.n = nrows;
@@ -613,6 +614,7 @@ static void csr_from_terms(int64_t nrows, int cb, int64_t T, DBuf<uint64_t> &key
     }
     k_row_ptr_from_keys<<<grid_for(nrows + 1, 256, 148 * 16), 256, 0, s>>>(nrows, T, k2.p, cb, out.row_ptr); ++g_kl;
     LAP_CHECK_LAUNCH();
+    if (!sums) return;
     out.d = (double *)dalloc(sizeof(double) * (size_t)(nrows > 0 ? nrows : 1), s);
     row_sums(nrows, out.nnz, out.row_ptr, out.w, out.d, &out.maxw, s);
     tmark("  terms: row sums");
@@ -788,13 +790,189 @@ __global__ void k_batch_row_ptr(int64_t nr, int64_t U, const uint64_t *__restric
 }
 __global__ void k_set_i64(int64_t *p, int64_t v) { *p = v; }
 
-static int64_t batch_budget_override() {
-    static int64_t v = -1;
-    if (v < 0) {
-        const char *e = getenv("LAP_TERM_BATCH");  // tests: force small batches
-        v = e ? std::max<int64_t>(1, atoll(e)) : 0;
+static int64_t batch_budget_override() {  // read per product (tests switch it inside one process)
+    const char *e = getenv("LAP_TERM_BATCH");  // tests: force small batches
+    return e ? std::max<int64_t>(1, atoll(e)) : 0;
+}
+
+// output rows [olo, ohi) of the source -> `out` (ohi - olo rows, local row_ptr
+// from 0, no diagonal): terms emitted, sorted and CanonSum-combined in batches
+// of at most `budget` terms (S.vptr = fine-entry prefix, vcp = term prefix, both
+// over the virtual rows)
+static void csr_source_range(const TermSrc &S, const int64_t *vcp, int64_t olo, int64_t ohi, int cb, int e_max,
+                             int64_t K, bool combine, int64_t budget, Level &out, cudaStream_t s) {
+    const int64_t nr = ohi - olo;
+    auto vrow = [&](int64_t o) {  // first virtual row of output row o
+        int64_t vv = o;
+        if (S.ostart) {
+            LAP_CUDA(cudaMemcpyAsync(&vv, S.ostart + o, 8, cudaMemcpyDeviceToHost, s));
+            LAP_CUDA(cudaStreamSynchronize(s));
+        }
+        return vv;
+    };
+    auto at = [&](const int64_t *p, int64_t v) { return d2h_scalar(p + v, s); };
+    const int64_t vlo = vrow(olo), vhi = vrow(ohi);
+    const int64_t Tr = at(vcp, vhi) - at(vcp, vlo);
+    if (Tr <= budget) {  // one batch: the plain path
+        DBuf<uint64_t> keys(Tr, s);
+        DBuf<double> vals(Tr, s);
+        DBuf<unsigned long long> cur(1, s);
+        LAP_CUDA(cudaMemsetAsync(cur.p, 0, 8, s));
+        const int64_t t0 = at(S.vptr, vlo), t1 = at(S.vptr, vhi);
+        tmark("  terms: alloc");
+        if (t1 > t0) {
+            k_src_emit<<<grid_for(t1 - t0, 256, 148 * 16), 256, 0, s>>>(S, vlo, vhi, t0, t1, olo, cb, cur.p, keys.p,
+                                                                       vals.p);
+            ++g_kl;
+            LAP_CHECK_LAUNCH();
+        }
+        const int64_t T = (int64_t)d2h_scalar(cur.p, s);
+        tmark("  terms: emit");
+        csr_from_terms(nr, cb, T, keys, vals, e_max, K, combine, out, s, false);
+        return;
     }
-    return v;
+    // several batches of output rows
+    out.n = nr;
+    out.row_ptr = (int64_t *)dalloc(sizeof(int64_t) * (size_t)(nr + 1), s);
+    int32_t *ocol = (int32_t *)dalloc(sizeof(int32_t) * (size_t)(Tr + 1), s);
+    double *ow = (double *)dalloc(sizeof(double) * (size_t)(Tr + 1), s);
+    const int elo = canon_elo(e_max, K);
+    DBuf<int64_t> o1d(1, s);
+    DBuf<unsigned long long> cur(1, s);
+    int64_t base = 0, o0 = olo;
+    while (o0 < ohi) {
+        k_batch_end<<<1, 1, 0, s>>>(o0, ohi, budget, S, vcp, o1d.p); ++g_kl;
+        const int64_t o1 = d2h_scalar(o1d.p, s);
+        int64_t vr[2] = {vrow(o0), vrow(o1)}, tr2[2], cr[2];
+        for (int q = 0; q < 2; q++) {
+            LAP_CUDA(cudaMemcpyAsync(&tr2[q], S.vptr + vr[q], 8, cudaMemcpyDeviceToHost, s));
+            LAP_CUDA(cudaMemcpyAsync(&cr[q], vcp + vr[q], 8, cudaMemcpyDeviceToHost, s));
+        }
+        LAP_CUDA(cudaStreamSynchronize(s));
+        const int64_t Tb = cr[1] - cr[0];
+        DBuf<uint64_t> keys(Tb, s), k2(Tb, s);
+        DBuf<double> vals(Tb, s), v2(Tb, s);
+        LAP_CUDA(cudaMemsetAsync(cur.p, 0, 8, s));
+        if (tr2[1] > tr2[0]) {
+            k_src_emit<<<grid_for(tr2[1] - tr2[0], 256, 148 * 16), 256, 0, s>>>(S, vr[0], vr[1], tr2[0], tr2[1], o0, cb,
+                                                                              cur.p, keys.p, vals.p);
+            ++g_kl;
+            LAP_CHECK_LAUNCH();
+        }
+        const int64_t T = (int64_t)d2h_scalar(cur.p, s);
+        const int end_bit = std::min(64, cb + bitlen_u64((uint64_t)(o1 - o0)));
+        if (T > 0) {
+            size_t bytes = 0;
+            LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, k2.p, vals.p, v2.p, T, 0, end_bit, s));
+            DBuf<char> tmp((int64_t)bytes, s);
+            LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, keys.p, k2.p, vals.p, v2.p, T, 0, end_bit, s));
+            ++g_kl;
+        }
+        keys.release();
+        vals.release();
+        int64_t U = T;
+        int64_t *rpo = out.row_ptr + (o0 - olo);
+        if (combine && T > 0) {
+            DBuf<uint64_t> uk(T, s);
+            DBuf<int64_t> cnt(T + 1, s), off(T + 1, s), nu(1, s);
+            size_t bytes = 0;
+            LAP_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, bytes, k2.p, uk.p, cnt.p, nu.p, T, s));
+            DBuf<char> tmp((int64_t)bytes, s);
+            LAP_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.p, bytes, k2.p, uk.p, cnt.p, nu.p, T, s)); ++g_kl;
+            U = d2h_scalar(nu.p, s);
+            LAP_CUDA(cudaMemsetAsync(cnt.p + U, 0, sizeof(int64_t), s));
+            exclusive_scan_i64(cnt.p, off.p, U + 1, s);
+            k_seg_canon<<<grid_for(U, 256, 148 * 16), 256, 0, s>>>(U, off.p, uk.p, v2.p, cb, elo, ocol + base,
+                                                                   ow + base); ++g_kl;
+            DBuf<int64_t> nch(U + 1, s), cfirst(U + 1, s);
+            LAP_CUDA(cudaMemsetAsync(nch.p + U, 0, sizeof(int64_t), s));
+            k_seg_nchunks<<<grid_for(U, 256, 148 * 16), 256, 0, s>>>(U, off.p, nch.p); ++g_kl;
+            exclusive_scan_i64(nch.p, cfirst.p, U + 1, s);
+            const int64_t C = d2h_scalar(cfirst.p + U, s);
+            if (C > 0) {
+                DBuf<int32_t> cseg(C, s);
+                DBuf<I128> part(C, s);
+                k_seg_chunk_map<<<grid_for(U, 256, 148 * 16), 256, 0, s>>>(U, cfirst.p, cseg.p); ++g_kl;
+                k_seg_chunk_sum<<<grid_for(C * 32, 256, 148 * 16), 256, 0, s>>>(C, cseg.p, cfirst.p, off.p, v2.p, elo,
+                                                                              part.p); ++g_kl;
+                k_seg_long_finish<<<grid_for(U, 256, 148 * 16), 256, 0, s>>>(U, cfirst.p, part.p, elo, ow + base); ++g_kl;
+            }
+            k_batch_row_ptr<<<grid_for(o1 - o0, 256, 148 * 8), 256, 0, s>>>(o1 - o0, U, uk.p, cb, base, rpo); ++g_kl;
+        } else if (T > 0) {
+            k_decode_cols<<<grid_for(T, 256, 148 * 16), 256, 0, s>>>(T, k2.p, (1ULL << cb) - 1, ocol + base); ++g_kl;
+            LAP_CUDA(cudaMemcpyAsync(ow + base, v2.p, sizeof(double) * (size_t)T, cudaMemcpyDeviceToDevice, s));
+            k_batch_row_ptr<<<grid_for(o1 - o0, 256, 148 * 8), 256, 0, s>>>(o1 - o0, T, k2.p, cb, base, rpo); ++g_kl;
+        } else {
+            k_batch_row_ptr<<<grid_for(o1 - o0, 256, 148 * 8), 256, 0, s>>>(o1 - o0, 0, k2.p, cb, base, rpo); ++g_kl;
+        }
+        LAP_CHECK_LAUNCH();
+        base += U;
+        o0 = o1;
+    }
+    k_set_i64<<<1, 1, 0, s>>>(out.row_ptr + nr, base); ++g_kl;
+    out.nnz = base;
+    if (base < Tr - Tr / 4) {  // shrink the over-allocation (Galerkin: entries inside aggregates vanish)
+        out.col = (int32_t *)dalloc(sizeof(int32_t) * (size_t)(base + 1), s);
+        out.w = (double *)dalloc(sizeof(double) * (size_t)(base + 1), s);
+        LAP_CUDA(cudaMemcpyAsync(out.col, ocol, sizeof(int32_t) * (size_t)base, cudaMemcpyDeviceToDevice, s));
+        LAP_CUDA(cudaMemcpyAsync(out.w, ow, sizeof(double) * (size_t)base, cudaMemcpyDeviceToDevice, s));
+        dfree(ocol, s);
+        dfree(ow, s);
+    } else {
+        out.col = ocol;
+        out.w = ow;
+    }
+    tmark("  terms: batches");
+}
+
+// ---- the term build of a coarse operator split over the setup
+// ranks.  Output rows are cut into P ranges of equal term counts
+// (split_bounds); each rank builds the CSR of its range exactly as one GPU
+// would (every entry is one CanonSum of its whole multiset of terms with the
+// level's global instance (e_max, K): no partial sums cross ranks), the ranges
+// are gathered into the full operator on every rank (dist.cu setup_gather:
+// NCCL broadcasts per root, or device copies on a virtual grid) and the
+// diagonal is formed from the gathered rows.  The hierarchy is therefore the
+// single-GPU one bit for bit; per-rank term memory and term work divide by P.
+static int64_t dsetup_min_terms() {
+    const char *e = getenv("LAP_DSETUP_MIN");  // tests: 0 forces the split on tiny graphs
+    return e ? atoll(e) : ((int64_t)1 << 22);
+}
+// bounds[r] = the first output row o with cum(o) * P >= r * total, cum(o) =
+// terms of the output rows before o (cum[o] = vcp[ostart[o]]); bounds[0] = 0,
+// bounds[P] = nout -- the same rule as lap_setup_split (host)
+__global__ void k_split_bounds(int64_t nout, int P, const int64_t *__restrict__ vcp,
+                               const int64_t *__restrict__ ostart, int64_t *__restrict__ bounds) {
+    const int r = threadIdx.x;
+    if (r > P) return;
+    bounds[r] = split_bound(r, P, nout, [&](int64_t o) { return vcp[ostart ? ostart[o] : o]; });
+}
+static std::vector<int64_t> split_bounds(int64_t nout, int P, const int64_t *vcp, const int64_t *ostart,
+                                         cudaStream_t s) {
+    DBuf<int64_t> b(P + 1, s);
+    k_split_bounds<<<1, 64, 0, s>>>(nout, P, vcp, ostart, b.p); ++g_kl;
+    LAP_CHECK_LAUNCH();
+    std::vector<int64_t> hb(P + 1);
+    LAP_CUDA(cudaMemcpyAsync(hb.data(), b.p, 8 * (P + 1), cudaMemcpyDeviceToHost, s));
+    LAP_CUDA(cudaStreamSynchronize(s));
+    return hb;
+}
+// run build(lo, hi, piece) for this process's ranges and gather the full operator
+template <class F>
+static void build_split(int64_t nout, const std::vector<int64_t> &bounds, Level &out, cudaStream_t s, F build) {
+    const int P = (int)bounds.size() - 1;
+    std::vector<Level> pieces;
+    std::vector<int> mine = setup_local_ranks();
+    for (int r : mine) {
+        pieces.emplace_back();
+        build(bounds[r], bounds[r + 1], pieces.back());
+    }
+    setup_gather(pieces, mine, bounds, out, s);
+    (void)P;
+    out.n = nout;
+    out.d = (double *)dalloc(sizeof(double) * (size_t)(nout > 0 ? nout : 1), s);
+    row_sums(nout, out.nnz, out.row_ptr, out.w, out.d, &out.maxw, s);
+    tmark("  terms: gathered + row sums");
 }
 
 // Build `out` (nout rows, column bits cb) from the source; CanonSum instance (e_max, K).
@@ -825,125 +1003,15 @@ static void csr_from_source(const TermSrc &S0, int64_t nv, int64_t nout, int cb,
         budget = std::max<int64_t>((int64_t)1 << 24, std::min<int64_t>((int64_t)1 << 28, (int64_t)(fr / 4 / 64)));
     }
     tmark("  terms: budget");
-    if (Ttot <= budget) {  // one batch: the plain path
-        DBuf<uint64_t> keys(Ttot, s);
-        DBuf<double> vals(Ttot, s);
-        DBuf<unsigned long long> cur(1, s);
-        LAP_CUDA(cudaMemsetAsync(cur.p, 0, 8, s));
-        const int64_t t1 = d2h_scalar(vptr.p + nv, s);
-        tmark("  terms: alloc");
-        if (t1 > 0) {
-            k_src_emit<<<grid_for(t1, 256, 148 * 16), 256, 0, s>>>(S, 0, nv, 0, t1, 0, cb, cur.p, keys.p, vals.p);
-            ++g_kl;
-            LAP_CHECK_LAUNCH();
-        }
-        const int64_t T = (int64_t)d2h_scalar(cur.p, s);
-        tmark("  terms: emit");
-        csr_from_terms(nout, cb, T, keys, vals, e_max, K, combine, out, s);
+    const int P = setup_nranks();
+    if (P > 1 && Ttot >= dsetup_min_terms()) {
+        const std::vector<int64_t> bounds = split_bounds(nout, P, vcp.p, S.ostart, s);
+        build_split(nout, bounds, out, s, [&](int64_t lo, int64_t hi, Level &piece) {
+            csr_source_range(S, vcp.p, lo, hi, cb, e_max, K, combine, budget, piece, s);
+        });
         return;
     }
-    // several batches of output rows
-    out.n = nout;
-    out.row_ptr = (int64_t *)dalloc(sizeof(int64_t) * (size_t)(nout + 1), s);
-    int32_t *ocol = (int32_t *)dalloc(sizeof(int32_t) * (size_t)(Ttot + 1), s);
-    double *ow = (double *)dalloc(sizeof(double) * (size_t)(Ttot + 1), s);
-    const int elo = canon_elo(e_max, K);
-    DBuf<int64_t> o1d(1, s);
-    DBuf<unsigned long long> cur(1, s);
-    int64_t base = 0, o0 = 0;
-    std::vector<int64_t> hv(2);
-    while (o0 < nout) {
-        k_batch_end<<<1, 1, 0, s>>>(o0, nout, budget, S, vcp.p, o1d.p); ++g_kl;
-        const int64_t o1 = d2h_scalar(o1d.p, s);
-        int64_t ov[2] = {o0, o1};
-        int64_t vr[2], tr2[2], cr[2];
-        for (int q = 0; q < 2; q++) {
-            int64_t vv = ov[q];
-            if (S.ostart) LAP_CUDA(cudaMemcpyAsync(&vv, S.ostart + ov[q], 8, cudaMemcpyDeviceToHost, s));
-            LAP_CUDA(cudaStreamSynchronize(s));
-            vr[q] = vv;
-        }
-        for (int q = 0; q < 2; q++) {
-            LAP_CUDA(cudaMemcpyAsync(&tr2[q], vptr.p + vr[q], 8, cudaMemcpyDeviceToHost, s));
-            LAP_CUDA(cudaMemcpyAsync(&cr[q], vcp.p + vr[q], 8, cudaMemcpyDeviceToHost, s));
-        }
-        LAP_CUDA(cudaStreamSynchronize(s));
-        const int64_t Tb = cr[1] - cr[0];
-        DBuf<uint64_t> keys(Tb, s), k2(Tb, s);
-        DBuf<double> vals(Tb, s), v2(Tb, s);
-        LAP_CUDA(cudaMemsetAsync(cur.p, 0, 8, s));
-        if (tr2[1] > tr2[0]) {
-            k_src_emit<<<grid_for(tr2[1] - tr2[0], 256, 148 * 16), 256, 0, s>>>(S, vr[0], vr[1], tr2[0], tr2[1], o0, cb,
-                                                                              cur.p, keys.p, vals.p);
-            ++g_kl;
-            LAP_CHECK_LAUNCH();
-        }
-        const int64_t T = (int64_t)d2h_scalar(cur.p, s);
-        const int end_bit = std::min(64, cb + bitlen_u64((uint64_t)(o1 - o0)));
-        if (T > 0) {
-            size_t bytes = 0;
-            LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, k2.p, vals.p, v2.p, T, 0, end_bit, s));
-            DBuf<char> tmp((int64_t)bytes, s);
-            LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, keys.p, k2.p, vals.p, v2.p, T, 0, end_bit, s));
-            ++g_kl;
-        }
-        keys.release();
-        vals.release();
-        int64_t U = T;
-        if (combine && T > 0) {
-            DBuf<uint64_t> uk(T, s);
-            DBuf<int64_t> cnt(T + 1, s), off(T + 1, s), nu(1, s);
-            size_t bytes = 0;
-            LAP_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, bytes, k2.p, uk.p, cnt.p, nu.p, T, s));
-            DBuf<char> tmp((int64_t)bytes, s);
-            LAP_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.p, bytes, k2.p, uk.p, cnt.p, nu.p, T, s)); ++g_kl;
-            U = d2h_scalar(nu.p, s);
-            LAP_CUDA(cudaMemsetAsync(cnt.p + U, 0, sizeof(int64_t), s));
-            exclusive_scan_i64(cnt.p, off.p, U + 1, s);
-            k_seg_canon<<<grid_for(U, 256, 148 * 16), 256, 0, s>>>(U, off.p, uk.p, v2.p, cb, elo, ocol + base,
-                                                                   ow + base); ++g_kl;
-            DBuf<int64_t> nch(U + 1, s), cfirst(U + 1, s);
-            LAP_CUDA(cudaMemsetAsync(nch.p + U, 0, sizeof(int64_t), s));
-            k_seg_nchunks<<<grid_for(U, 256, 148 * 16), 256, 0, s>>>(U, off.p, nch.p); ++g_kl;
-            exclusive_scan_i64(nch.p, cfirst.p, U + 1, s);
-            const int64_t C = d2h_scalar(cfirst.p + U, s);
-            if (C > 0) {
-                DBuf<int32_t> cseg(C, s);
-                DBuf<I128> part(C, s);
-                k_seg_chunk_map<<<grid_for(U, 256, 148 * 16), 256, 0, s>>>(U, cfirst.p, cseg.p); ++g_kl;
-                k_seg_chunk_sum<<<grid_for(C * 32, 256, 148 * 16), 256, 0, s>>>(C, cseg.p, cfirst.p, off.p, v2.p, elo,
-                                                                              part.p); ++g_kl;
-                k_seg_long_finish<<<grid_for(U, 256, 148 * 16), 256, 0, s>>>(U, cfirst.p, part.p, elo, ow + base); ++g_kl;
-            }
-            k_batch_row_ptr<<<grid_for(o1 - o0, 256, 148 * 8), 256, 0, s>>>(o1 - o0, U, uk.p, cb, base,
-                                                                             out.row_ptr + o0); ++g_kl;
-        } else if (T > 0) {
-            k_decode_cols<<<grid_for(T, 256, 148 * 16), 256, 0, s>>>(T, k2.p, (1ULL << cb) - 1, ocol + base); ++g_kl;
-            LAP_CUDA(cudaMemcpyAsync(ow + base, v2.p, sizeof(double) * (size_t)T, cudaMemcpyDeviceToDevice, s));
-            k_batch_row_ptr<<<grid_for(o1 - o0, 256, 148 * 8), 256, 0, s>>>(o1 - o0, T, k2.p, cb, base,
-                                                                             out.row_ptr + o0); ++g_kl;
-        } else {
-            k_batch_row_ptr<<<grid_for(o1 - o0, 256, 148 * 8), 256, 0, s>>>(o1 - o0, 0, k2.p, cb, base,
-                                                                             out.row_ptr + o0); ++g_kl;
-        }
-        LAP_CHECK_LAUNCH();
-        base += U;
-        o0 = o1;
-    }
-    k_set_i64<<<1, 1, 0, s>>>(out.row_ptr + nout, base); ++g_kl;
-    out.nnz = base;
-    if (base < Ttot - Ttot / 4) {  // shrink the over-allocation (Galerkin: entries inside aggregates vanish)
-        out.col = (int32_t *)dalloc(sizeof(int32_t) * (size_t)(base + 1), s);
-        out.w = (double *)dalloc(sizeof(double) * (size_t)(base + 1), s);
-        LAP_CUDA(cudaMemcpyAsync(out.col, ocol, sizeof(int32_t) * (size_t)base, cudaMemcpyDeviceToDevice, s));
-        LAP_CUDA(cudaMemcpyAsync(out.w, ow, sizeof(double) * (size_t)base, cudaMemcpyDeviceToDevice, s));
-        dfree(ocol, s);
-        dfree(ow, s);
-    } else {
-        out.col = ocol;
-        out.w = ow;
-    }
-    tmark("  terms: batches");
+    csr_source_range(S, vcp.p, 0, nout, cb, e_max, K, combine, budget, out, s);
     out.d = (double *)dalloc(sizeof(double) * (size_t)(nout > 0 ? nout : 1), s);
     row_sums(nout, out.nnz, out.row_ptr, out.w, out.d, &out.maxw, s);
     tmark("  terms: row sums");
@@ -1292,18 +1360,31 @@ __global__ void k_affinity(int64_t n, const int64_t *__restrict__ row_ptr, const
         const int64_t kb0 = live ? row_ptr[i] : 0, ke0 = live ? row_ptr[i + 1] : 0;
         const bool skip = ke0 - kb0 > SETUP_LONG;  // long rows: k_affinity_long
         const int64_t kb = skip ? 0 : kb0, ke = skip ? 0 : ke0;
-        for (int64_t k = kb + gl; k < ke; k += G) {
-            int64_t j = col[k];
-            const double2 *xj2 = reinterpret_cast<const double2 *>(X + 4 * j);  // 32-byte aligned rows
-            const double2 u0 = xj2[0], u1 = xj2[1];
-            double xj[4] = {u0.x, u0.y, u1.x, u1.y};
-            double nj = dot4_rn(xj, xj);
-            double g = dot4_rn(xi, xj);
-            double num = __dmul_rn(g, g);
-            double den = power == 2 ? __dmul_rn(__dmul_rn(ni, ni), __dmul_rn(nj, nj)) : __dmul_rn(ni, nj);
-            double c = den > 0.0 ? __ddiv_rn(num, den) : 0.0;
-            C[k] = c;
-            mx = c > mx ? c : mx;
+        // 4 column loads, then 4 independent 32-byte gathers of X_j in flight per lane
+        for (int64_t k0 = kb + gl; k0 < ke; k0 += 4 * G) {
+            int64_t jj[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) jj[u] = k0 + u * G < ke ? col[k0 + u * G] : 0;
+            double2 u0[4], u1[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const double2 *xj2 = reinterpret_cast<const double2 *>(X + 4 * jj[u]);  // 32-byte aligned rows
+                u0[u] = xj2[0];
+                u1[u] = xj2[1];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int64_t k = k0 + u * G;
+                if (k >= ke) break;
+                double xj[4] = {u0[u].x, u0[u].y, u1[u].x, u1[u].y};
+                double nj = dot4_rn(xj, xj);
+                double g = dot4_rn(xi, xj);
+                double num = __dmul_rn(g, g);
+                double den = power == 2 ? __dmul_rn(__dmul_rn(ni, ni), __dmul_rn(nj, nj)) : __dmul_rn(ni, nj);
+                double c = den > 0.0 ? __ddiv_rn(num, den) : 0.0;
+                C[k] = c;
+                mx = c > mx ? c : mx;
+            }
         }
         for (int o = G / 2; o > 0; o >>= 1) {
             double t = __shfl_xor_sync(0xffffffffu, mx, o);
@@ -1344,19 +1425,34 @@ __global__ void k_vote_round(int64_t n, const int64_t *__restrict__ row_ptr, con
                              const int32_t *__restrict__ idx, int8_t *__restrict__ nst, int32_t *__restrict__ nidx,
                              int32_t *__restrict__ votes) {
     GROUP_LOOP_BEGIN(G, n)
-        const bool lng = live && row_ptr[i + 1] - row_ptr[i] > SETUP_LONG;  // k_vote_long_*
-        const bool act = live && !lng && st[i] == ST_UND;  // only Undecided act (O-R9)
+        const int sti = live ? st[i] : ST_DEC;
+        const int64_t kb0 = sti == ST_UND ? row_ptr[i] : 0, ke0 = sti == ST_UND ? row_ptr[i + 1] : 0;
+        const bool lng = ke0 - kb0 > SETUP_LONG;  // k_vote_long_*
+        const bool act = sti == ST_UND && !lng;    // only Undecided act (O-R9)
         int br = -1;
         double bs = 0.0;
         int32_t bj = 0x7fffffff;
-        const int64_t kb = act ? row_ptr[i] : 0, ke = act ? row_ptr[i + 1] : 0;
-        for (int64_t k = kb + gl; k < ke; k += G) {
-            double sv = S[k];
-            if (sv == 0.0 || sv < filt) continue;           // filter 2^-t, w != 0 (O-R13)
-            int32_t j = col[k];
-            int r = st[j];
-            if (r == ST_DEC) continue;                      // (O-R12)
-            if (r > br || (r == br && (sv > bs || (sv == bs && j < bj)))) { br = r; bs = sv; bj = j; }
+        const int64_t kb = act ? kb0 : 0, ke = act ? ke0 : 0;
+        // 4 (S, col) loads, then the passing entries' state gathers, in flight together
+        for (int64_t k0 = kb + gl; k0 < ke; k0 += 4 * G) {
+            double sv[4];
+            int32_t jj[4];
+            int rr[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int64_t k = k0 + u * G;
+                sv[u] = k < ke ? S[k] : 0.0;
+                jj[u] = k < ke ? col[k] : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++)   // filter 2^-t, w != 0 (O-R13)
+                rr[u] = (sv[u] == 0.0 || sv[u] < filt) ? ST_DEC : (int)st[jj[u]];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int r = rr[u];
+                if (r == ST_DEC) continue;                  // (O-R12)
+                if (r > br || (r == br && (sv[u] > bs || (sv[u] == bs && jj[u] < bj)))) { br = r; bs = sv[u]; bj = jj[u]; }
+            }
         }
         for (int o = G / 2; o > 0; o >>= 1) {               // group arg-max under (rank, S, -j)
             int r2 = __shfl_xor_sync(0xffffffffu, br, o);
@@ -1366,7 +1462,7 @@ __global__ void k_vote_round(int64_t n, const int64_t *__restrict__ row_ptr, con
         }
         if (live && !lng && gl == 0) {  // every row writes its next state (no round-start copy needed)
             bool dec = act && br == ST_SEED;
-            nst[i] = dec ? (int8_t)ST_DEC : st[i];
+            nst[i] = dec ? (int8_t)ST_DEC : (int8_t)sti;
             nidx[i] = dec ? bj : idx[i];
             if (act && br == ST_UND) atomicAdd(&votes[bj], 1);
         }
@@ -1690,17 +1786,38 @@ struct CSweep {  // CS_SWEEP: x_new = x - omega ((d x - s) / d), per column
     double omega;
 };
 template <int NC>
-__device__ __forceinline__ void cs_gather(const double *__restrict__ x, int64_t c, double wk, int elo, i128 *acc) {
+__device__ __forceinline__ void cs_gather(const double *__restrict__ x, int64_t c, double wk, int elo, double s2,
+                                          i128 *acc) {
     if (NC == 1) {
-        acc[0] += canon_q(__dmul_rn(wk, x[c]), elo);
+        acc[0] += canon_q_s(__dmul_rn(wk, x[c]), s2, elo);
     } else {
         const double2 *xj = reinterpret_cast<const double2 *>(x + 4 * c);
         const double2 u = xj[0], v = xj[1];
-        acc[0] += canon_q(__dmul_rn(wk, u.x), elo);
-        acc[1] += canon_q(__dmul_rn(wk, u.y), elo);
-        acc[2] += canon_q(__dmul_rn(wk, v.x), elo);
-        acc[3] += canon_q(__dmul_rn(wk, v.y), elo);
+        acc[0] += canon_q_s(__dmul_rn(wk, u.x), s2, elo);
+        acc[1] += canon_q_s(__dmul_rn(wk, u.y), s2, elo);
+        acc[2] += canon_q_s(__dmul_rn(wk, v.x), s2, elo);
+        acc[3] += canon_q_s(__dmul_rn(wk, v.y), s2, elo);
     }
+}
+// NC x-values of column c (the gather half of cs_gather, issued ahead of the sums)
+template <int NC>
+struct CsX {
+    double v[NC];
+};
+template <int NC>
+__device__ __forceinline__ CsX<NC> cs_load(const double *__restrict__ x, int64_t c) {
+    CsX<NC> r;
+    if (NC == 1) {
+        r.v[0] = x[c];
+    } else {
+        const double2 *xj = reinterpret_cast<const double2 *>(x + 4 * c);
+        const double2 u = xj[0], v = xj[1];
+        r.v[0] = u.x;
+        r.v[1] = u.y;
+        r.v[2] = v.x;
+        r.v[3] = v.y;
+    }
+    return r;
 }
 template <int NC, int MODE>
 __device__ __forceinline__ double cs_epilogue(int64_t p, const i128 *acc, int elo, const CStore &C,
@@ -1720,8 +1837,10 @@ __device__ __forceinline__ double cs_epilogue(int64_t p, const i128 *acc, int el
 // XS: the whole x staged in shared memory first (small dense-ish levels, as
 // the solve's k_spmv_smem: random gathers from a ~100 KB x are bound by the L1
 // tag rate); one 1024-thread CTA per SM
+// (occupancy: 78 / 128 registers left 35 % / 25 % of the warps resident and the
+// gathers latency-bound, ncu profiles/r02; the bounds cap them at 64 / 80)
 template <int NC, int MODE, bool XS = false>
-__global__ void __launch_bounds__(XS ? 1024 : 256) k_cspmv_store(CStore C, const double *__restrict__ x0,
+__global__ void __launch_bounds__(XS ? 1024 : 256, XS ? 1 : (NC == 1 ? 4 : 3)) k_cspmv_store(CStore C, const double *__restrict__ x0,
                                                                  const double *__restrict__ rs,
                                                                  const double *__restrict__ vp, int elo_fixed,
                                                                  LzState *st, double *__restrict__ y, CSweep W,
@@ -1735,6 +1854,7 @@ __global__ void __launch_bounds__(XS ? 1024 : 256) k_cspmv_store(CStore C, const
     const double *__restrict__ x = XS ? xs_dyn : x0;
     const double bprev = MODE == CS_LANCZOS ? st->bprev : 0.0;
     const int elo = MODE == CS_LANCZOS ? elo_fixed : *W.elo_p;
+    const double s2 = canon_scale(elo);
     if (MODE == CS_LANCZOS && blockIdx.x == 0 && threadIdx.x == 0) {
         st->acc_b.lo = 0;  // read by pass A only; pass A of this step has finished
         st->acc_b.hi = 0;
@@ -1764,7 +1884,7 @@ __global__ void __launch_bounds__(XS ? 1024 : 256) k_cspmv_store(CStore C, const
                 }
 #pragma unroll
                 for (int uu = 0; uu < 8; uu++)
-                    if (q + uu < width) cs_gather<NC>(x, cc[uu], wv[uu], elo, acc);
+                    if (q + uu < width) cs_gather<NC>(x, cc[uu], wv[uu], elo, s2, acc);
             }
             double ya = 0.0;
             if (p < C.nshort) ya = cs_epilogue<NC, MODE>(p, acc, elo, C, x, rs, vp, bprev, y, W);
@@ -1776,7 +1896,28 @@ __global__ void __launch_bounds__(XS ? 1024 : 256) k_cspmv_store(CStore C, const
             i128 acc[NC];
 #pragma unroll
             for (int k = 0; k < NC; k++) acc[k] = 0;
-            for (int64_t k = b + lane; k < e; k += 32) cs_gather<NC>(x, __ldg(&C.scol[k]), __ldg(&C.sw[k]), elo, acc);
+            // 8 (col, w) loads and then 8 gathers in flight per lane (long rows of
+            // aggregated levels carry most entries; the sum is order-free)
+            constexpr int U = NC == 1 ? 8 : 4;
+            for (int64_t k0 = b + lane; k0 < e; k0 += 32 * U) {
+                int32_t cc[U];
+                double wv[U];
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const int64_t k = k0 + 32 * u;
+                    cc[u] = k < e ? __ldg(&C.scol[k]) : 0;
+                    wv[u] = k < e ? __ldg(&C.sw[k]) : 0.0;
+                }
+                CsX<NC> xv[U];
+#pragma unroll
+                for (int u = 0; u < U; u++)
+                    if (k0 + 32 * u < e) xv[u] = cs_load<NC>(x, cc[u]);
+#pragma unroll
+                for (int u = 0; u < U; u++)
+                    if (k0 + 32 * u < e)
+#pragma unroll
+                        for (int kk = 0; kk < NC; kk++) acc[kk] += canon_q_s(__dmul_rn(wv[u], xv[u].v[kk]), s2, elo);
+            }
 #pragma unroll
             for (int k = 0; k < NC; k++) acc[k] = warp_sum_i128(acc[k]);
             const int slot = C.cslot[c];
@@ -1952,9 +2093,11 @@ static double lanczos(lap_hierarchy *h, Level &L, int l, cudaStream_t s) {
     }
     for (int j = 0; j < steps && j < 64; j++) {
         k_lzc_next<<<g, 256, 0, s>>>(n, j == 0, 0, y.p, v.p, vp.p, u.p, rs.p, st.p, al.p, be.p); ++g_kl;
-        if (xs) k_cspmv_store<1, CS_LANCZOS, true><<<num_sms_dev(), 1024, 8 * n, s>>>(C, u.p, rs.p, vp.p, elo_spmv, st.p,
-                                                                                       y.p, W, n);
-        else k_cspmv_store<1, CS_LANCZOS><<<cstore_grid(L), 256, 0, s>>>(C, u.p, rs.p, vp.p, elo_spmv, st.p, y.p, W, 0);
+        if (xs)
+            k_cspmv_store<1, CS_LANCZOS, true><<<num_sms_dev(), 1024, 8 * n, s>>>(C, u.p, rs.p, vp.p, elo_spmv, st.p,
+                                                                                  y.p, W, n);
+        else
+            k_cspmv_store<1, CS_LANCZOS><<<cstore_grid(L), 256, 0, s>>>(C, u.p, rs.p, vp.p, elo_spmv, st.p, y.p, W, 0);
         ++g_kl;
         k_lzc_alpha<<<g, 256, 0, s>>>(n, y.p, v.p, st.p); ++g_kl;
         k_lzc_update<<<g, 256, 0, s>>>(n, y.p, v.p, st.p); ++g_kl;
@@ -2151,6 +2294,13 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
     const lap_params &p = h->p;
     unsigned ge = grid_for(n, 256, 148 * 16);
     const int G = group_size(n, nnz, L.maxdeg <= SHORT_MAX);
+    // lanes per row of the affinity / vote passes (LAP_AFF_G / LAP_VOTE_G: experiments)
+    auto env_g = [&](const char *name) {
+        const char *e = getenv(name);
+        const int v = e ? atoi(e) : 0;
+        return (v == 1 || v == 2 || v == 4 || v == 8 || v == 16 || v == 32) ? v : G;
+    };
+    const int Ga = env_g("LAP_AFF_G"), Gv = env_g("LAP_VOTE_G");
     // test vectors: swept on the solve storage (canonical sums:
     // the order is free), then laid out in the logical order for the affinity
     DBuf<double> X(4 * n, s), Xn(4 * n, s), M(n, s);
@@ -2180,8 +2330,8 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
         k_max_abs<<<grid_for(4 * n, 256, 148 * 8), 256, 0, s>>>(X.p, 4 * n, mxb.p); ++g_kl;
         k_tv_elo<<<1, 1, 0, s>>>(mxb.p, ew, nnz, elo.p); ++g_kl;
         const CSweep W{X.p, Xn.p, elo.p, p.tv_omega};
-        k_cspmv_store<4, CS_SWEEP><<<cstore_grid(L), 256, 0, s>>>(CStore(cstore_of(L, cpart.p)), X.p, nullptr, nullptr,
-                                                                  0, nullptr, nullptr, W, 0);
+        k_cspmv_store<4, CS_SWEEP><<<cstore_grid(L), 256, 0, s>>>(CStore(cstore_of(L, cpart.p)), X.p, nullptr,
+                                                                  nullptr, 0, nullptr, nullptr, W, 0);
         ++g_kl;
         LAP_CHECK_LAUNCH();
         std::swap(X.p, Xn.p);
@@ -2193,7 +2343,7 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
     tmark("  test vectors");
     // affinity + normalisation
     if (nlc > 0) LAP_CUDA(cudaMemsetAsync(M.p, 0, sizeof(double) * n, s));
-    LAUNCH_G(G, k_affinity, n, s, n, L.row_ptr, L.col, X.p, p.affinity_power, S.p, M.p);
+    LAUNCH_G(Ga, k_affinity, n, s, n, L.row_ptr, L.col, X.p, p.affinity_power, S.p, M.p);
     if (nlc > 0) {
         k_affinity_long<<<grid_for(nlc * 32, 256, 148 * 16), 256, 0, s>>>(nlc, lc_row, lc_idx, L.row_ptr, L.col, X.p,
                                                                           p.affinity_power, S.p,
@@ -2219,7 +2369,7 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
     }
     for (int t = 1; t <= p.vote_rounds; t++) {
         double filt = ldexp(1.0, -t);
-        LAUNCH_G(G, k_vote_round, n, s, n, L.row_ptr, L.col, S.p, filt, st.p, idx.p, nst.p, nidx.p, votes.p);
+        LAUNCH_G(Gv, k_vote_round, n, s, n, L.row_ptr, L.col, S.p, filt, st.p, idx.p, nst.p, nidx.p, votes.p);
         if (nlc > 0) {
             const unsigned gc = grid_for(nlc * 32, 256, 148 * 16);
             k_vote_long_max<<<gc, 256, 0, s>>>(nlc, lc_row, lc_idx, L.row_ptr, L.col, S.p, filt, st.p, vbest.p);
@@ -2308,11 +2458,6 @@ __global__ void k_gal_slot_emit(int64_t ns, const int32_t *__restrict__ members,
     GROUP_COMPACT_ROW(G, kb, ke, o, agg[col[k]] != a, (tk[p] = agg[col[k]], tv[p] = w[k]))
     GROUP_LOOP_END
 }
-__global__ void k_gal_row_ptr(int64_t m, const int64_t *__restrict__ mem_ptr, const int64_t *__restrict__ pv,
-                              int64_t *__restrict__ pa) {
-    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a <= m; a += (int64_t)gridDim.x * blockDim.x)
-        pa[a] = pv[mem_ptr[a]];
-}
 template <int G>
 __global__ void k_gal_keys(int64_t m, const int64_t *__restrict__ pa, const int32_t *__restrict__ sk, int cb,
                            uint64_t *__restrict__ key) {
@@ -2322,45 +2467,72 @@ __global__ void k_gal_keys(int64_t m, const int64_t *__restrict__ pa, const int3
     GROUP_LOOP_END
 }
 constexpr int64_t GAL_ORDERED_MAX_AVG = 256;  // terms per coarse row (average) for the ordered Galerkin
-static bool gal_fast_enabled() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("LAP_GAL_FAST");  // 0: the batched global-sort path (tests, experiments)
-        v = (e && e[0] == '0') ? 0 : 1;
-    }
-    return v == 1;
+static bool gal_fast_enabled() {  // read per level (tests switch it inside one process)
+    const char *e = getenv("LAP_GAL_FAST");  // 0: the batched global-sort path (tests, experiments)
+    return !(e && e[0] == '0');
 }
 static void csr_combine_sorted(int64_t nrows, int cb, int64_t T, DBuf<uint64_t> &k2, DBuf<double> &v2, int e_max,
-                               int64_t K, Level &out, cudaStream_t s);
+                               int64_t K, Level &out, cudaStream_t s, bool sums);
+// local prefix of a slot range: pl[v] = pv[s0 + v] - pv[s0], v in [0, ns]
+__global__ void k_sub_prefix(int64_t ns, const int64_t *__restrict__ pv, int64_t *__restrict__ pl) {
+    const int64_t b = pv[0];
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= ns; v += (int64_t)gridDim.x * blockDim.x)
+        pl[v] = pv[v] - b;
+}
+// row pointers of the coarse rows [alo, ahi): pa[a] = pl[mem_ptr[alo + a] - s0]
+__global__ void k_gal_row_ptr_r(int64_t mr, const int64_t *__restrict__ mem_ptr, int64_t s0,
+                                const int64_t *__restrict__ pl, int64_t *__restrict__ pa) {
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a <= mr; a += (int64_t)gridDim.x * blockDim.x)
+        pa[a] = pl[mem_ptr[a] - s0];
+}
 static void galerkin_fast(lap_hierarchy *h, Level &L, Level &N, const int32_t *members, const uint32_t *slot_agg,
                           const int64_t *mem_ptr, cudaStream_t s) {
     const int64_t n = L.n, m = L.m;
     const int cb = bitlen_u64((uint64_t)(m > 0 ? m : 1));
     const int G = group_size(n, L.nnz, L.maxdeg <= SHORT_MAX);
-    DBuf<int64_t> cnt(n + 1, s), pv(n + 1, s), pa(m + 1, s);
+    const int e_max = ilogb_pos(L.maxw) + 1;
+    DBuf<int64_t> cnt(n + 1, s), pv(n + 1, s);
     LAP_CUDA(cudaMemsetAsync(cnt.p + n, 0, sizeof(int64_t), s));
     LAUNCH_G(G, k_gal_slot_cnt, n, s, n, members, slot_agg, L.row_ptr, L.col, L.agg, cnt.p);
     exclusive_scan_i64(cnt.p, pv.p, n + 1, s);
-    const int64_t T = d2h_scalar(pv.p + n, s);
-    DBuf<int32_t> tk(T + 1, s);
-    DBuf<double> tv(T + 1, s);
-    LAUNCH_G(G, k_gal_slot_emit, n, s, n, members, slot_agg, L.row_ptr, L.col, L.w, L.agg, pv.p, tk.p, tv.p);
-    k_gal_row_ptr<<<grid_for(m + 1, 256, 148 * 8), 256, 0, s>>>(m, mem_ptr, pv.p, pa.p); ++g_kl;
-    LAP_CHECK_LAUNCH();
     cnt.release();
-    pv.release();
-    tmark("  galerkin: ordered emit");
-    DBuf<int32_t> sk(T + 1, s);
-    DBuf<double> sv(T + 1, s);
-    sort_rows(m, pa.p, T, cb, tk.p, tv.p, sk.p, sv.p, s);
-    tk.release();
-    tv.release();
-    tmark("  galerkin: row sorts");
-    DBuf<uint64_t> key(T + 1, s);
-    if (T > 0) LAUNCH_G(group_size(m, T), k_gal_keys, m, s, m, pa.p, sk.p, cb, key.p);
-    LAP_CHECK_LAUNCH();
-    sk.release();
-    csr_combine_sorted(m, cb, T, key, sv, ilogb_pos(L.maxw) + 1, L.nnz, N, s);
+    const int64_t Ttot = d2h_scalar(pv.p + n, s);
+    // coarse rows [alo, ahi) -> out (local rows, no diagonal)
+    auto range = [&](int64_t alo, int64_t ahi, Level &out) {
+        const int64_t mr = ahi - alo;
+        const int64_t s0 = d2h_scalar(mem_ptr + alo, s), s1 = d2h_scalar(mem_ptr + ahi, s), ns = s1 - s0;
+        DBuf<int64_t> pl(ns + 1, s), pa(mr + 1, s);
+        k_sub_prefix<<<grid_for(ns + 1, 256, 148 * 8), 256, 0, s>>>(ns, pv.p + s0, pl.p); ++g_kl;
+        const int64_t T = d2h_scalar(pl.p + ns, s);
+        DBuf<int32_t> tk(T + 1, s);
+        DBuf<double> tv(T + 1, s);
+        if (ns > 0) LAUNCH_G(G, k_gal_slot_emit, ns, s, ns, members + s0, slot_agg + s0, L.row_ptr, L.col, L.w, L.agg,
+                             pl.p, tk.p, tv.p);
+        k_gal_row_ptr_r<<<grid_for(mr + 1, 256, 148 * 8), 256, 0, s>>>(mr, mem_ptr + alo, s0, pl.p, pa.p); ++g_kl;
+        LAP_CHECK_LAUNCH();
+        pl.release();
+        tmark("  galerkin: ordered emit");
+        DBuf<int32_t> sk(T + 1, s);
+        DBuf<double> sv(T + 1, s);
+        sort_rows(mr, pa.p, T, cb, tk.p, tv.p, sk.p, sv.p, s);
+        tk.release();
+        tv.release();
+        tmark("  galerkin: row sorts");
+        DBuf<uint64_t> key(T + 1, s);
+        if (T > 0) LAUNCH_G(group_size(mr, T), k_gal_keys, mr, s, mr, pa.p, sk.p, cb, key.p);
+        LAP_CHECK_LAUNCH();
+        sk.release();
+        csr_combine_sorted(mr, cb, T, key, sv, e_max, L.nnz, out, s, false);
+    };
+    const int P = setup_nranks();
+    if (P > 1 && Ttot >= dsetup_min_terms()) {
+        build_split(m, split_bounds(m, P, pv.p, mem_ptr, s), N, s, range);
+        return;
+    }
+    range(0, m, N);
+    N.d = (double *)dalloc(sizeof(double) * (size_t)(m > 0 ? m : 1), s);
+    row_sums(m, N.nnz, N.row_ptr, N.w, N.d, &N.maxw, s);
+    tmark("  terms: row sums");
 }
 
 static void galerkin(lap_hierarchy *h, Level &L, Level &N, cudaStream_t s) {
@@ -2545,7 +2717,8 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
         int cb = bitlen_u64((uint64_t)(n > 0 ? n : 1));
         DBuf<int32_t> inv(n, s);  // old row of new id r
         k_inverse_perm<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, h->perm, inv.p); ++g_kl;
-        if (nnz < ((int64_t)1 << 28)) {
+        const char *fr = getenv("LAP_RELABEL_TERMS");  // tests: the term-build relabel of big graphs
+        if (nnz < ((int64_t)1 << 28) && !(fr && fr[0] == '1')) {
             // P L P^T directly: row r = old row inv[r], columns perm[c], each row
             // sorted in registers / shared memory (no duplicates, nothing to sum)
             DBuf<int32_t> p32(n, s);

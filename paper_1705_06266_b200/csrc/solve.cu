@@ -109,7 +109,7 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
 // coarse levels are load balanced, and no class runs alone on a partly idle
 // GPU.  No fp64 atomics: per-chunk sums and the in-order combine are fixed, so
 // results are bitwise reproducible run to run.
-template <int EPI, class CT, int NB = 8>
+template <int EPI, class CT, int NB = 8, bool UNIT = false>
 __device__ __forceinline__ void sell_slice(int64_t sl, int lane, int64_t nrows, const int64_t *__restrict__ sp,
                                            const CT *__restrict__ ec, const double *__restrict__ ew, const Csr &A,
                                            const EpiArgs &a, const double *__restrict__ xg, Dacc &dacc) {
@@ -136,13 +136,21 @@ __device__ __forceinline__ void sell_slice(int64_t sl, int lane, int64_t nrows, 
             c[u] = 0;
             if (q + u < width) {
                 c[u] = __ldg(&ec[beg + (int64_t)(q + u) * 32 + lane]);
-                wv[u] = __ldg(&ew[beg + (int64_t)(q + u) * 32 + lane]);
+                // UNIT: pattern only; a padding slot holds the row's own index (never a
+                // real entry: no self loops) and is skipped -- 1.0 * x_j = x_j, the same bits
+                if (UNIT) wv[u] = c[u] != (int)i ? 1.0 : 0.0;
+                else wv[u] = __ldg(&ew[beg + (int64_t)(q + u) * 32 + lane]);
             }
         }
 #pragma unroll
         for (int u = 0; u < NB; u += 2) {
-            if (q + u < width) acc0 += wv[u] * xg[c[u]];
-            if (q + u + 1 < width) acc1 += wv[u + 1] * xg[c[u + 1]];
+            if (UNIT) {
+                if (q + u < width && wv[u] != 0.0) acc0 += xg[c[u]];
+                if (q + u + 1 < width && wv[u + 1] != 0.0) acc1 += xg[c[u + 1]];
+            } else {
+                if (q + u < width) acc0 += wv[u] * xg[c[u]];
+                if (q + u + 1 < width) acc1 += wv[u + 1] * xg[c[u + 1]];
+            }
         }
     }
     if (live) {
@@ -194,7 +202,7 @@ struct LongRows {
 // lane) iff this warp must finish the row: either the row is a single chunk,
 // or this warp is the last of the row's chunks to arrive, in which case the
 // row's partials are summed in chunk order.  *sum is valid on lane 0.
-template <class CT>
+template <class CT, bool UNIT = false>
 __device__ __forceinline__ bool chunk_reduce(int64_t c, int lane, const int64_t *__restrict__ rp,
                                              const CT *__restrict__ col, const double *__restrict__ w,
                                              const double *__restrict__ x, const LongRows &R, int64_t &row,
@@ -213,7 +221,7 @@ __device__ __forceinline__ bool chunk_reduce(int64_t c, int lane, const int64_t 
 #pragma unroll
         for (int u = 0; u < 8; u++) {
             c[u] = __ldg(&col[k + 32 * u]);
-            wv[u] = __ldg(&w[k + 32 * u]);
+            wv[u] = UNIT ? 1.0 : __ldg(&w[k + 32 * u]);
         }
         a0 += wv[0] * x[c[0]];
         a1 += wv[1] * x[c[1]];
@@ -226,13 +234,14 @@ __device__ __forceinline__ bool chunk_reduce(int64_t c, int lane, const int64_t 
     }
     for (; k + 96 < e; k += 128) {
         int c0 = __ldg(&col[k]), c1 = __ldg(&col[k + 32]), c2 = __ldg(&col[k + 64]), c3 = __ldg(&col[k + 96]);
-        double w0 = __ldg(&w[k]), w1 = __ldg(&w[k + 32]), w2 = __ldg(&w[k + 64]), w3 = __ldg(&w[k + 96]);
+        double w0 = UNIT ? 1.0 : __ldg(&w[k]), w1 = UNIT ? 1.0 : __ldg(&w[k + 32]),
+               w2 = UNIT ? 1.0 : __ldg(&w[k + 64]), w3 = UNIT ? 1.0 : __ldg(&w[k + 96]);
         a0 += w0 * x[c0];
         a1 += w1 * x[c1];
         a2 += w2 * x[c2];
         a3 += w3 * x[c3];
     }
-    for (; k < e; k += 32) a0 += __ldg(&w[k]) * x[__ldg(&col[k])];
+    for (; k < e; k += 32) a0 += (UNIT ? 1.0 : __ldg(&w[k])) * x[__ldg(&col[k])];
     double acc = (a0 + a1) + (a2 + a3);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -262,20 +271,21 @@ __device__ __forceinline__ bool chunk_reduce(int64_t c, int lane, const int64_t 
     return true;
 }
 
-template <int EPI, class CT>
+template <int EPI, class CT, bool UNIT = false>
 __device__ __forceinline__ void long_chunk(int64_t c, int lane, const Csr &A, const CT *__restrict__ col,
                                            const LongRows &R, const EpiArgs &a, const double *__restrict__ xg,
                                            Dacc &dacc) {
     int64_t i;
     double ax;
-    if (chunk_reduce(c, lane, A.rp, col, A.w, xg, R, i, ax) && lane == 0) apply_epi<EPI>(i, ax, A, a, dacc);
+    if (chunk_reduce<CT, UNIT>(c, lane, A.rp, col, A.w, xg, R, i, ax) && lane == 0) apply_epi<EPI>(i, ax, A, a, dacc);
 }
 
 // NB = SELL columns per batch: 8 (64 registers, 4 CTAs of 256 per SM) or 4 (48, 5 CTAs) for the
 // big levels, 4 (more resident warps, shorter per-warp slice chains) for mid-size ones
 // LONG = 0: a level without long rows (grids, coarse mesh levels) -- the chunk
 // path is compiled out, so its registers do not constrain the SELL loop
-template <int EPI, int NB, int LONG>
+// UNIT: pattern-only level (unit weights, N4): ew / A.w are not read
+template <int EPI, int NB, int LONG, bool UNIT = false>
 __global__ void __launch_bounds__(256, NB == 8 ? 4 : 5) k_spmv(int64_t nslices, int64_t nshort,
                                                              const int64_t *__restrict__ sp,
                                                              const int32_t *__restrict__ ec,
@@ -289,8 +299,8 @@ __global__ void __launch_bounds__(256, NB == 8 ? 4 : 5) k_spmv(int64_t nslices, 
     const int64_t nitems = nslices + R.nchunks;
     Dacc dacc;
     for (int64_t t = warp; t < nitems; t += nwarps) {
-        if (!LONG || t < nslices) sell_slice<EPI, int32_t, NB>(t, lane, nshort, sp, ec, ew, A, a, a.x, dacc);
-        else long_chunk<EPI>(t - nslices, lane, A, A.col, R, a, a.x, dacc);
+        if (!LONG || t < nslices) sell_slice<EPI, int32_t, NB, UNIT>(t, lane, nshort, sp, ec, ew, A, a, a.x, dacc);
+        else long_chunk<EPI, int32_t, UNIT>(t - nslices, lane, A, A.col, R, a, a.x, dacc);
     }
     if (EPI == E_DOT || EPI == E_LZ || EPI == E_FCG) {
         double r = block_sum(dacc.a, sh);
@@ -641,7 +651,14 @@ static void spmv_dispatch(lap_hierarchy *h, const Level &L, const EpiArgs &a, cu
 #define LAP_SPMV_LAUNCH(NBV, LV)                                                                               \
     launch_pdl(k_spmv<EPI, NBV, LV>, spmv_grid(L), 256, s, L.nslices, L.c_end[0], (const int64_t *)L.slice_ptr, \
                (const int32_t *)L.ell_col, (const double *)L.ell_w, A, R, a, a.partials)
-        if (L.nchunks > 0) {
+#define LAP_SPMV_LAUNCH_U(NBV)                                                                                 \
+    launch_pdl(k_spmv<EPI, NBV, 1, true>, spmv_grid(L), 256, s, L.nslices, L.c_end[0],                        \
+               (const int64_t *)L.slice_ptr, (const int32_t *)L.ell_col, (const double *)L.ell_w, A, R, a,     \
+               a.partials)
+        if (L.unit) {  // pattern only (the LONG variant also serves a level without long rows)
+            if (L.spmv_nb == 8) LAP_SPMV_LAUNCH_U(8);
+            else LAP_SPMV_LAUNCH_U(4);
+        } else if (L.nchunks > 0) {
             if (L.spmv_nb == 8) LAP_SPMV_LAUNCH(8, 1);
             else LAP_SPMV_LAUNCH(4, 1);
         } else {
@@ -649,6 +666,7 @@ static void spmv_dispatch(lap_hierarchy *h, const Level &L, const EpiArgs &a, cu
             else LAP_SPMV_LAUNCH(4, 0);
         }
 #undef LAP_SPMV_LAUNCH
+#undef LAP_SPMV_LAUNCH_U
     }
     h->cur.launches++;
     LAP_CHECK_LAUNCH();
@@ -669,7 +687,7 @@ void spmv_level(lap_hierarchy *h, const Level &L, EpiKind kind, const EpiArgs &a
     int64_t extra = (kind == EPI_RESID) ? 8 : (kind == EPI_CHEB || kind == (EpiKind)E_CHEBZ) ? 24
                     : (kind == (EpiKind)E_CHEB0) ? 16 : (kind == (EpiKind)E_FCG) ? 8 : 0;
     h->cur.edges += L.nnz;
-    h->cur.bytes += 12 * L.nnz + (32 + extra) * L.n;
+    h->cur.bytes += (L.unit && !L.spmv_vec && !L.xt && !L.smem_x ? 4 : 12) * L.nnz + (32 + extra) * L.n;
 }
 
 // ------------------------------------------------------------------ reductions

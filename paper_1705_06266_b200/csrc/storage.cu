@@ -593,6 +593,12 @@ static void validate_storage(const Level &L, cudaStream_t s) {
     }
 }
 
+__global__ void k_flag_not_one(int64_t m, const double *__restrict__ w, int *flag) {
+    GRID_STRIDE(k, m) {
+        if (w[k] != 1.0) *flag = 1;
+    }
+}
+
 void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
     Level &L = h->lev[l];
     int64_t n = L.n;
@@ -763,6 +769,19 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
         const char *e = getenv("LAP_NB4_MAXNNZ");
         if (e) L.spmv_nb = L.nnz <= atoll(e) ? 4 : 8;
         else L.spmv_nb = (L.nnz >= NB4_MIN_NNZ && L.nnz <= 8 * n) ? 4 : 8;
+    }
+    // pattern-only solve SpMV on a unit-weight level 0: the
+    // weights stay stored (setup kernels, exports) but k_spmv does not read them
+    // (1.0 * x_j = x_j: the same bits); LAP_UNIT=0 turns it off
+    if (l == 0 && L.nnz > 0) {
+        const char *e = getenv("LAP_UNIT");
+        if (!(e && e[0] == '0')) {
+            DBuf<int> flag(1, s);
+            LAP_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+            k_flag_not_one<<<grid_for(L.nnz, 256, 148 * 8), 256, 0, s>>>(L.nnz, L.sw, flag.p);
+            g_kl++;
+            L.unit = d2h(flag.p, s) == 0;
+        }
     }
     // long rows: LCHUNK-entry warp work items (solve.cu k_spmv)
     L.nchunks = build_chunks(L.srp, L.c_end[0], n - L.c_end[0], SHORT_MAX, &L.chunk_row, &L.chunk_idx, &L.chunk_slot,

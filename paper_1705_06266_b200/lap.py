@@ -55,7 +55,7 @@ EXPORTS = [
     "lap_perm", "lap_spmv", "lap_vcycle", "lap_kcycle", "lap_solve_block", "lap_get_stats", "lap_bench_op",
     "lap_nccl_unique_id", "lap_comm_create", "lap_comm_create_virtual", "lap_comm_info", "lap_comm_free",
     "lap_setup_dist", "lap_dist_index", "lap_pool_retain", "lap_random_stream",
-    "lap_bench_gather", "lap_level_rows", "lap_import_hierarchy",
+    "lap_bench_gather", "lap_level_rows", "lap_import_hierarchy", "lap_setup_split",
 ]
 
 
@@ -92,6 +92,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
         "lap_comm_free": (None, [P]),
         "lap_setup_dist": (ctypes.c_int, [ctypes.POINTER(lap_graph), ctypes.POINTER(lap_params), P, P, ctypes.POINTER(P)]),
         "lap_dist_index": (ctypes.c_int, [i64, i32, i64, P, P, pi64]),
+        "lap_setup_split": (ctypes.c_int, [i64, P, i32, P]),
         "lap_pool_retain": (None, [ctypes.c_uint64]),
         "lap_random_stream": (ctypes.c_int, [i32, ctypes.c_uint64, i32, i32, i64, P, P]),
         "lap_bench_gather": (ctypes.c_int, [i64, i64, i32, P, P]),
@@ -238,6 +239,15 @@ def dist_index(n: int, nranks: int, rows) -> tuple:
     return out, S.value
 
 
+def setup_split(cum, nranks: int) -> np.ndarray:
+    """Host-only split rule of the distributed setup's term builds
+    (lap_setup_split): cum[0..nout] term prefix -> bounds[0..nranks]."""
+    cum = np.ascontiguousarray(cum, np.int64)
+    out = np.zeros(nranks + 1, np.int64)
+    _check(lib().lap_setup_split(len(cum) - 1, _ptr(cum), nranks, _ptr(out)))
+    return out
+
+
 class Hierarchy:
     """lap_setup(graph, params) -> hierarchy ; .solve(b) -> (x, iters, residual).
     With comm=Comm(...), lap_setup_dist: the fine levels are sharded over the grid."""
@@ -364,6 +374,22 @@ class Hierarchy:
         mp = np.zeros(max(n, 1), np.int32)
         _check(lib().lap_level_export(self._h, l, None, None, None, _ptr(d), _ptr(mp)))
         return d[:n], (mp[:n] if kind != KIND_COARSEST else None)
+
+    def level_map(self, l: int) -> np.ndarray:
+        """agg (aggregation level) or fmap (elimination level) of level l in the
+        logical numbering; available also when the logical CSR was released."""
+        _, n, _, _ = self.level_info(l)
+        mp = np.zeros(max(n, 1), np.int32)
+        _check(lib().lap_level_export(self._h, l, None, None, None, None, _ptr(mp)))
+        return mp[:n]
+
+    def level_degrees(self, l: int, rows) -> np.ndarray:
+        """Stored entries of the given logical rows of level l (lap_level_rows
+        without the column / weight copies)."""
+        rows = np.ascontiguousarray(rows, np.int64)
+        rp = np.zeros(len(rows) + 1, np.int64)
+        _check(lib().lap_level_rows(self._h, l, len(rows), _ptr(rows), _ptr(rp), None, None))
+        return np.diff(rp)
 
     def level_rows(self, l: int, rows):
         """Rows of level l's logical CSR rebuilt from the solve storage

@@ -130,3 +130,104 @@ def test_2d_exchange_reproduces_global_spmv_gloo(pr, pc):
     for rank, err, padchk in res:
         assert err <= 1e-12, (rank, err)
         assert padchk >= 0, "pads of the reduce-scattered y must be exactly 0"
+
+
+# ---------------------------------------------------------------- distributed setup
+def _galerkin_row_terms(lv):
+    """terms of each coarse row of R L P: fine entries (i, j) with
+    agg_i = a != agg_j -- the counts the library's split balances."""
+    rows = np.repeat(np.arange(lv.n), np.diff(lv.row_ptr))
+    a, b = lv.agg[rows], lv.agg[lv.col]
+    return np.bincount(a[a != b], minlength=int(lv.agg.max()) + 1)
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+def test_setup_split_rule(P):
+    """lap_setup_split: a partition of the output rows into P contiguous ranges
+    with nearly equal term counts (each range's terms within one row's terms of
+    total / P), and bit-equal to the rule written out here."""
+    L = _lib()
+    import oracle
+    for g in [lapgen.rmat(12), lapgen.barabasi_albert(3000, 6), lapgen.grid2d(60, 50)]:
+        ho = oracle.Hierarchy(g)
+        lv = next(ho.level(l) for l in range(ho.nlev) if ho.level(l).kind == oracle.AGG)
+        t = _galerkin_row_terms(lv)
+        cum = np.concatenate([[0], np.cumsum(t)])
+        b = L.setup_split(cum, P)
+        assert b[0] == 0 and b[-1] == len(t) and np.all(np.diff(b) >= 0)
+        ref = [0] + [int(np.searchsorted(cum * P, r * cum[-1], side="left")) for r in range(1, P)] + [len(t)]
+        assert list(b) == ref
+        loads = cum[b[1:]] - cum[b[:-1]]
+        assert loads.max() <= cum[-1] / P + t.max()
+    with pytest.raises(L.LapError):
+        L.setup_split(np.array([0, 5, 3]), 2)
+
+
+def _split_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        L = _lib()
+        g = lapgen.barabasi_albert(4000, 7)
+        ho = oracle.Hierarchy(g)
+        la = next(l for l in range(ho.nlev) if ho.level(l).kind == oracle.AGG)
+        lv, co = ho.level(la), ho.level(la + 1)
+        cum = np.concatenate([[0], np.cumsum(_galerkin_row_terms(lv))])
+        b = L.setup_split(cum, world)
+        lo, hi = int(b[rank]), int(b[rank + 1])
+        # this rank's rows of R L P (stand-in for its device build): local row_ptr from 0
+        rp = co.row_ptr[lo:hi + 1] - co.row_ptr[lo]
+        col = co.col[co.row_ptr[lo]:co.row_ptr[hi]]
+        w = co.w[co.row_ptr[lo]:co.row_ptr[hi]]
+        # setup_gather: entry counts of every rank, offsets, one broadcast per root
+        cnt = torch.zeros(world, dtype=torch.int64)
+        dist.all_gather(list(cnt.chunk(world)), torch.tensor([len(col)], dtype=torch.int64))
+        off = np.concatenate([[0], np.cumsum(cnt.numpy())])
+        n_out, nnz = int(b[-1]), int(off[-1])
+        row_ptr = torch.zeros(n_out + 1, dtype=torch.int64)
+        col_all = torch.zeros(nnz, dtype=torch.int32)
+        w_all = torch.zeros(nnz, dtype=torch.float64)
+        for r in range(world):
+            a0, a1 = int(b[r]), int(b[r + 1])
+            seg = torch.from_numpy(rp[:-1].copy()) if r == rank else torch.zeros(a1 - a0, dtype=torch.int64)
+            dist.broadcast(seg, src=r)
+            row_ptr[a0:a1] = seg + int(off[r])           # shifted by the root's entry offset
+            c = torch.from_numpy(col.copy()) if r == rank else torch.zeros(int(cnt[r]), dtype=torch.int32)
+            v = torch.from_numpy(w.copy()) if r == rank else torch.zeros(int(cnt[r]), dtype=torch.float64)
+            dist.broadcast(c, src=r)
+            dist.broadcast(v, src=r)
+            col_all[int(off[r]):int(off[r + 1])] = c
+            w_all[int(off[r]):int(off[r + 1])] = v
+        row_ptr[n_out] = nnz
+        ok = (np.array_equal(row_ptr.numpy(), co.row_ptr) and np.array_equal(col_all.numpy(), co.col)
+              and w_all.numpy().tobytes() == co.w.tobytes())
+        q.put((rank, bool(ok), hi - lo))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_setup_split_gather_gloo(world):
+    """N1 host logic with torch.distributed 'gloo' (world 2 and 4): every rank
+    takes its row range from lap_setup_split, contributes those rows of the
+    coarse operator with a local row_ptr, and the gather of dist.cu
+    setup_gather (entry counts all-gathered, one broadcast per root, row_ptr
+    pieces shifted by the root's entry offset) rebuilds the whole operator
+    bit for bit on every rank."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_split_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _ in res), res
+    assert sum(nr for _, _, nr in res) > 0

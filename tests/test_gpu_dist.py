@@ -141,3 +141,58 @@ def test_sharded_pcg_graph_replays_eager_bitwise(P):
         res.append(np.load(fn))
         os.remove(fn)
     assert res[0].tobytes() == res[1].tobytes()
+
+
+def _level_bits(h, l):
+    lv = h.level(l)
+    out = [lv["kind"], lv["n"], lv["nnz"], lv["row_ptr"].tobytes(), lv["col"].tobytes(), lv["w"].tobytes(),
+           lv["d"].tobytes()]
+    for key in ("agg", "fmap"):
+        if key in lv:
+            out.append(lv[key].tobytes())
+    return out
+
+
+@pytest.mark.parametrize("gname", ["rmat12", "ba3000", "grid3d_14", "star20000"])
+@pytest.mark.parametrize("grid", [(1, 2), (2, 2), (2, 3), (2, 4)], ids=["1x2", "2x2", "2x3", "2x4"])
+@pytest.mark.parametrize("gal_fast", ["1", "0"], ids=["ordered", "batched"])
+def test_distributed_setup_bit_identical(P, gname, grid, gal_fast, monkeypatch):
+    """with a setup communicator the coarse-operator term builds
+    (Galerkin -- ordered and batched paths --, Schur complement) are split by
+    output rows over the ranks and gathered; every entry is still one CanonSum
+    of its whole multiset with the level's global instance, so the hierarchy
+    (every level's CSR, diagonal, aggregates / F sets, lambda-hat) equals the
+    single-GPU one bit for bit.  LAP_DSETUP_MIN=0 splits every product."""
+    g = GRAPHS[gname]()
+    monkeypatch.setenv("LAP_GAL_FAST", gal_fast)
+    h1 = P.Hierarchy(g)
+    monkeypatch.setenv("LAP_DSETUP_MIN", "0")
+    comm = P.Comm(*grid)
+    hd = P.Hierarchy(g, comm=comm)
+    assert hd.nlev == h1.nlev
+    for l in range(h1.nlev - 1):
+        assert _level_bits(hd, l) == _level_bits(h1, l), l
+        assert hd.level_info(l) == h1.level_info(l), l
+    b = lapgen.rhs(g.n, seed=2)
+    x1, it1, _, _ = h1.solve(b)
+    xd, itd, rrd, rc = hd.solve(b)
+    assert rc == 0 and rrd <= 1e-8 and abs(itd - it1) <= 1
+    hd.close()
+    comm.close()
+
+
+def test_distributed_setup_big_relabel(P, monkeypatch):
+    """The level-0 relabel of a graph above 2^28 entries is a split term build
+    too (forced here on a small graph, LAP_RELABEL_TERMS=1), with small
+    batches inside every rank's range (LAP_TERM_BATCH)."""
+    g = lapgen.rmat(13)
+    monkeypatch.setenv("LAP_TERM_BATCH", "3000")
+    monkeypatch.setenv("LAP_RELABEL_TERMS", "1")
+    h1 = P.Hierarchy(g)
+    monkeypatch.setenv("LAP_DSETUP_MIN", "0")
+    comm = P.Comm(2, 2)
+    hd = P.Hierarchy(g, comm=comm)
+    for l in range(h1.nlev - 1):
+        assert _level_bits(hd, l) == _level_bits(h1, l), l
+    hd.close()
+    comm.close()

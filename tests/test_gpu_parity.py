@@ -406,3 +406,34 @@ def test_column_tiled_spmv_per_entry(P, env):
     e = dict(os.environ, **env)
     r = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, timeout=900, cwd=root)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("mk", [lambda: lapgen.rmat(16), lambda: lapgen.grid2d(420, 420),
+                                lambda: lapgen.star(30000)], ids=["rmat16", "grid420", "star30000"])
+def test_pattern_only_level0(P, mk, monkeypatch):
+    """Unit-weight level 0: the solve SpMV reads the pattern
+    only (4 B per entry, padding slots recognised by their own-row index).
+    1.0 * x_j = x_j, so the SpMV, the V-cycle and the whole solve are
+    bit-identical to the weighted kernel (LAP_UNIT=0), the SpMV is within the
+    O-P2 bound of the oracle, and the library books 4 B per stored entry."""
+    g = mk()
+    g = lapgen.Graph(g.n, g.row_ptr, g.col, np.ones(g.nnz))
+    monkeypatch.setenv("LAP_UNIT", "0")
+    hw = P.Hierarchy(g)
+    monkeypatch.delenv("LAP_UNIT")
+    hu = P.Hierarchy(g)
+    x = np.random.default_rng(3).standard_normal(g.n)
+    yu, yw = hu.spmv(0, x), hw.spmv(0, x)
+    assert yu.tobytes() == yw.tobytes()
+    lv = hu.level(0)
+    ref = oracle.spmv(lv["n"], lv["row_ptr"], lv["col"], lv["w"], lv["d"], x)
+    assert np.all(np.abs(yu - ref) <= spmv_bound(lv["row_ptr"], lv["col"], lv["w"], lv["d"], x))
+    b = lapgen.rhs(g.n)
+    xu, itu, rru, _ = hu.solve(b)
+    xw, itw, rrw, _ = hw.solve(b)
+    assert itu == itw and xu.tobytes() == xw.tobytes() and rru <= 1e-8
+    _, bu, eu = hu.bench_op(0, 0, 2)
+    _, bw, ew = hw.bench_op(0, 0, 2)
+    nnz = lv["nnz"]
+    if lv["n"] > 131072 or np.diff(lv["row_ptr"]).max() > 64:  # big enough for k_spmv (not the small-level kernels)
+        assert bw - bu == 8 * nnz, (bw, bu, nnz)
