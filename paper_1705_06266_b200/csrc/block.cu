@@ -91,7 +91,33 @@ struct BChunks {  // the level's LCHUNK chunks of its long rows (storage.cu), K 
     const int32_t *crow, *cidx, *cslot;
     int32_t *ccnt;
     double *cpart;  // [nchunks][K]
+    int64_t nmulti;  // rows of several chunks: their BE_DOT terms [nmulti][K] in mdot (see blk_dot_fixup)
+    double *mdot;
+    int *mdone;
 };
+// the last block to finish adds the multi-chunk rows' dot terms (slot order) to
+// the last block's partial of every column: bitwise reproducible (solve.cu dot_fixup)
+template <int K>
+__device__ __forceinline__ void blk_dot_fixup(const BChunks &R, double *__restrict__ partials, double *sh) {
+    if (R.nmulti == 0) return;
+    __shared__ int last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(R.mdone, 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int c = 0; c < K; c++) {
+        double acc = 0.0;
+        for (int64_t q = threadIdx.x; q < R.nmulti; q += blockDim.x) acc += __ldcg(&R.mdot[q * K + c]);
+        const double r = blk_block_sum(acc, sh);
+        if (threadIdx.x == 0) {
+            double *p = partials + (int64_t)c * gridDim.x + gridDim.x - 1;
+            *p = __ldcg(p) + r;
+        }
+    }
+    if (threadIdx.x == 0) *R.mdone = 0;
+}
 
 // y = epilogue(L X) for a block of K columns, ONE launch: SELL-32 slices of
 // the short rows (coalesced index/weight loads, a thread per row), then the
@@ -113,7 +139,7 @@ __global__ void __launch_bounds__(256) k_blk_spmv(int64_t nslices, int64_t nshor
 #pragma unroll
     for (int c = 0; c < K; c++) dacc[c] = 0.0;
     // row epilogue: the K values of a row are contiguous -> 16-byte vector loads / stores
-    auto epi = [&](int64_t i, const double *ax) {
+    auto epi = [&](int64_t i, const double *ax, int slot = -1) {
         const double di = d[i];
         const Vk<K> xi = ldk<K>(a.x + i * K);
         Vk<K> bi, dvi, yo, dvo;
@@ -124,7 +150,8 @@ __global__ void __launch_bounds__(256) k_blk_spmv(int64_t nslices, int64_t nshor
             const double lx = di * xi.v[c] - ax[c];
             if (EPI == BE_DOT) {
                 yo.v[c] = lx;
-                dacc[c] += xi.v[c] * lx;
+                if (slot >= 0) R.mdot[(int64_t)slot * K + c] = xi.v[c] * lx;
+                else dacc[c] += xi.v[c] * lx;
             } else if (EPI == BE_RESID) {
                 yo.v[c] = bi.v[c] - lx;
             } else if (EPI == BE_CHEB) {
@@ -209,7 +236,7 @@ __global__ void __launch_bounds__(256) k_blk_spmv(int64_t nslices, int64_t nshor
 #pragma unroll
                     for (int c = 0; c < K; c++) s2[c] += __ldcg(&R.cpart[(c0 + q) * K + c]);
                 R.ccnt[slot] = 0;
-                epi(i, s2);
+                epi(i, s2, slot);
             }
         }
     }
@@ -219,6 +246,7 @@ __global__ void __launch_bounds__(256) k_blk_spmv(int64_t nslices, int64_t nshor
             double r = blk_block_sum(dacc[c], sh);
             if (threadIdx.x == 0) a.partials[c * gridDim.x + blockIdx.x] = r;
         }
+        blk_dot_fixup<K>(R, a.partials, sh);
     }
 }
 
@@ -245,12 +273,13 @@ __global__ void __launch_bounds__(256) k_blk_spmv_wide(int64_t nslices, int64_t 
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     double dacc = 0.0;
-    auto epi = [&](int64_t i, double ax) {  // column c of row i
+    auto epi = [&](int64_t i, double ax, int slot = -1) {  // column c of row i
         const double di = d[i], xi = a.x[i * K + c];
         const double lx = di * xi - ax;
         if (EPI == BE_DOT) {
             a.y[i * K + c] = lx;
-            dacc += xi * lx;
+            if (slot >= 0) R.mdot[(int64_t)slot * K + c] = xi * lx;
+            else dacc += xi * lx;
         } else if (EPI == BE_RESID) {
             a.y[i * K + c] = a.b[i * K + c] - lx;
         } else {
@@ -322,7 +351,7 @@ __global__ void __launch_bounds__(256) k_blk_spmv_wide(int64_t nslices, int64_t 
                 const int64_t c0 = ch - j;
                 double s2 = 0.0;
                 for (int q = 0; q < nch; q++) s2 += __ldcg(&R.cpart[(c0 + q) * K + c]);
-                epi(i, s2);
+                epi(i, s2, slot);
             }
             __syncwarp();
             if (lane == 0) R.ccnt[slot] = 0;
@@ -338,6 +367,8 @@ __global__ void __launch_bounds__(256) k_blk_spmv_wide(int64_t nslices, int64_t 
             for (int q = 0; q < (int)(blockDim.x >> 5); q++) r += shd[q][threadIdx.x];
             a.partials[threadIdx.x * gridDim.x + blockIdx.x] = r;
         }
+        __shared__ double shf[8];
+        blk_dot_fixup<K>(R, a.partials, shf);
     }
 }
 
@@ -626,6 +657,8 @@ struct BlockWork {  // per (hierarchy, K)
     int K = 0;
     std::vector<double *> lb, lx, lx2, lt, lr, ldv;  // per level, n_l x K
     std::vector<double *> lcpart;                     // per level, K partials per long-row chunk
+    std::vector<double *> lmdot;                      // per level, K dot terms per multi-chunk row
+    int *mdone = nullptr;                             // blk_dot_fixup arrival counter (kept at 0)
     double *b = nullptr, *x = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr;
     double *sc = nullptr, *part = nullptr;
     double *hsc = nullptr;  // pinned host copy of the scalars
@@ -636,9 +669,9 @@ struct BlockWork {  // per (hierarchy, K)
 static inline unsigned beg(int64_t n) { return grid_for(n, 256, 148 * 8); }
 
 template <int K>
-static void blk_spmv(lap_hierarchy *h, const Level &L, double *cpart, int epi, const BArgs &a, cudaStream_t s,
-                     unsigned grid) {
-    BChunks R{L.nchunks, L.chunk_row, L.chunk_idx, L.chunk_slot, L.chunk_cnt, cpart};
+static void blk_spmv(lap_hierarchy *h, const Level &L, double *cpart, double *mdot, int *mdone, int epi,
+                     const BArgs &a, cudaStream_t s, unsigned grid) {
+    BChunks R{L.nchunks, L.chunk_row, L.chunk_idx, L.chunk_slot, L.chunk_cnt, cpart, L.nmulti, mdot, mdone};
 #define BLK_LAUNCH(E)                                                                                             \
     launch_pdl(K >= 16 ? k_blk_spmv_wide<E, (K >= 16 ? K : 16)> : k_blk_spmv<E, K>, grid, 256, s, L.nslices,      \
                L.c_end[0], L.n, (const int64_t *)L.slice_ptr,                                                     \
@@ -698,13 +731,13 @@ static void blk_vcycle(lap_hierarchy *h, BlockWork &W, int l, const double *b, d
         a.c2 = 2.0 * rho / delta;
         a.x = cur;
         a.y = alt;
-        blk_spmv<K>(h, L, W.lcpart[l], BE_CHEB, a, s, g);
+        blk_spmv<K>(h, L, W.lcpart[l], W.lmdot[l], W.mdone, BE_CHEB, a, s, g);
         std::swap(cur, alt);
         rho_old = rho;
     }
     a.x = cur;
     a.y = W.lr[l];
-    blk_spmv<K>(h, L, W.lcpart[l], BE_RESID, a, s, g);
+    blk_spmv<K>(h, L, W.lcpart[l], W.lmdot[l], W.mdone, BE_RESID, a, s, g);
     launch_pdl(k_blk_restrict<K>, beg(L.m * K), 256, s, L.m, (const int64_t *)L.mem_ptr, (const int32_t *)L.members,
                (const double *)W.lr[l], cb);
     blk_vcycle<K>(h, W, l + 1, cb, cx, s);
@@ -718,12 +751,12 @@ static void blk_vcycle(lap_hierarchy *h, BlockWork &W, int l, const double *b, d
         if (k == 0) {
             a.c1 = 0.0;
             a.c2 = 1.0 / theta;
-            blk_spmv<K>(h, L, W.lcpart[l], BE_CHEB0, a, s, g);
+            blk_spmv<K>(h, L, W.lcpart[l], W.lmdot[l], W.mdone, BE_CHEB0, a, s, g);
         } else {
             double rho = 1.0 / (2.0 * sigma - rho_old);
             a.c1 = rho * rho_old;
             a.c2 = 2.0 * rho / delta;
-            blk_spmv<K>(h, L, W.lcpart[l], BE_CHEB, a, s, g);
+            blk_spmv<K>(h, L, W.lcpart[l], W.lmdot[l], W.mdone, BE_CHEB, a, s, g);
             rho_old = rho;
         }
         if (k < Kd - 1) std::swap(cur, alt);
@@ -746,11 +779,14 @@ static BlockWork *block_work(lap_hierarchy *h, cudaStream_t s) {
         W->lr.push_back((double *)dalloc(bytes, s));
         W->ldv.push_back((double *)dalloc(bytes, s));
         W->lcpart.push_back((double *)dalloc(8 * (size_t)K * (size_t)(L.nchunks > 0 ? L.nchunks : 1), s));
+        W->lmdot.push_back((double *)dalloc(8 * (size_t)K * (size_t)(L.nmulti > 0 ? L.nmulti : 1), s));
     }
     const size_t b0 = 8 * (size_t)K * (size_t)h->lev[0].n;
     double **vs[] = {&W->b, &W->x, &W->r, &W->z, &W->p, &W->q};
     for (double **v : vs) *v = (double *)dalloc(b0, s);
     W->sc = (double *)dalloc(8 * 16 * K, s);
+    W->mdone = (int *)dalloc(sizeof(int), s);
+    LAP_CUDA(cudaMemsetAsync(W->mdone, 0, sizeof(int), s));
     int64_t np = BLK_RED;
     for (auto &L : h->lev) np = std::max<int64_t>(np, (int64_t)spmm_grid<K>(L));
     W->part = (double *)dalloc(8 * 3 * K * (size_t)np, s);
@@ -778,9 +814,10 @@ void free_block(lap_hierarchy *h) {
     for (void *p : h->blk) {
         BlockWork *W = (BlockWork *)p;
         if (W->vgraph) cudaGraphExecDestroy(W->vgraph);
-        for (auto *v : {&W->lb, &W->lx, &W->lx2, &W->lt, &W->lr, &W->ldv, &W->lcpart})
+        for (auto *v : {&W->lb, &W->lx, &W->lx2, &W->lt, &W->lr, &W->ldv, &W->lcpart, &W->lmdot})
             for (double *q : *v) dfree(q, nullptr);
         for (double *q : {W->b, W->x, W->r, W->z, W->p, W->q, W->sc, W->part}) dfree(q, nullptr);
+        dfree(W->mdone, nullptr);
         if (W->hsc) cudaFreeHost(W->hsc);
         delete W;
     }
@@ -831,7 +868,7 @@ static void blk_spmv_part(lap_hierarchy *h, BlockWork &W, cudaStream_t s) {
     a.x = W.p;
     a.y = W.q;
     a.partials = W.part;
-    blk_spmv<K>(h, L0, W.lcpart[0], BE_DOT, a, s, g);
+    blk_spmv<K>(h, L0, W.lcpart[0], W.lmdot[0], W.mdone, BE_DOT, a, s, g);
     launch_pdl(k_blk_reduce, 1, 256, s, (const double *)W.part, (int)g, K, 1, W.sc, (int)S_PQ, 0, 0);
     if constexpr (K >= 16)
         launch_pdl(k_blk_xr_w<K>, BLK_RED, 256, s, n, (const double *)W.p, (const double *)W.q, W.x, W.r,
@@ -897,7 +934,7 @@ static void solve_block_k(lap_hierarchy *h, int k, const double *B, double *X, d
                 t.x = W.x;
                 t.b = W.b;
                 t.y = W.z;
-                blk_spmv<K>(h, L0, W.lcpart[0], BE_RESID, t, s, spmm_grid<K>(L0));
+                blk_spmv<K>(h, L0, W.lcpart[0], W.lmdot[0], W.mdone, BE_RESID, t, s, spmm_grid<K>(L0));
                 blk_sums<K, 1>(h, W, W.z, W.z, S_TRUE, 0, 0, s);
                 pull();
                 bool any_bad = false;
@@ -933,7 +970,7 @@ static void solve_block_k(lap_hierarchy *h, int k, const double *B, double *X, d
     t.x = W.x;
     t.b = W.b;
     t.y = W.z;
-    blk_spmv<K>(h, L0, W.lcpart[0], BE_RESID, t, s, spmm_grid<K>(L0));
+    blk_spmv<K>(h, L0, W.lcpart[0], W.lmdot[0], W.mdone, BE_RESID, t, s, spmm_grid<K>(L0));
     blk_sums<K, 1>(h, W, W.z, W.z, S_TRUE, 0, 0, s);
     launch_pdl(k_blk_out<K>, beg(n * k), 256, s, n, k, (const int64_t *)h->cmap, (const double *)W.x,
                (const double *)W.sc, X);

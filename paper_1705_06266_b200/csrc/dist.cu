@@ -88,11 +88,8 @@ static int64_t real_rows(const PieceMap &m, int k) {
     return lo;
 }
 
-struct Shard {
-    int r = 0, gi = 0, gj = 0;
-    int64_t nreal = 0;
-    // 2D block: rows = row block (nrow = pc*S), columns = column block (ncol = pr*S)
-    int64_t nrow = 0, ncol = 0, nnz = 0;
+struct BlockMat {  // one part of a rank's 2D block: SELL-32 over short rows + LCHUNK chunks over long rows
+    int64_t nnz = 0;
     int64_t *rp = nullptr;
     int32_t *col = nullptr;
     double *w = nullptr;
@@ -103,8 +100,18 @@ struct Shard {
     int64_t nchunks = 0;
     int32_t *crow = nullptr, *cidx = nullptr, *cslot = nullptr, *ccnt = nullptr;
     double *cpart = nullptr;
-    // vectors: column block, row-block partial, owned piece
-    double *xcol = nullptr, *ypart = nullptr, *ax = nullptr;
+};
+struct Shard {
+    int r = 0, gi = 0, gj = 0;
+    int64_t nreal = 0;
+    // 2D block: rows = row block (nrow = pc*S), columns = column block (ncol = pr*S)
+    int64_t nrow = 0, ncol = 0;
+    // A_ij split by column: `own` = the columns of this rank's own x piece
+    // (local ids into the piece, needs no communication), `rem` = the other
+    // pieces of column block gj (ids into xcol, after the column allgather)
+    BlockMat own, rem;
+    // vectors: column block, row-block partial (own part, then own + remote), owned piece
+    double *xcol = nullptr, *ypart = nullptr, *yown = nullptr, *ax = nullptr;
     double *d = nullptr, *b = nullptr, *x = nullptr, *x2 = nullptr, *t = nullptr, *rv = nullptr, *dv = nullptr;
     // aggregation transfer (coarse index space of the next level)
     int64_t *mem_ptr = nullptr;
@@ -144,6 +151,10 @@ struct Dist {
     cudaGraphExec_t pgraph = nullptr;
     int64_t pg_launches = 0, pg_edges = 0, pg_bytes = 0;
     bool use_graph = true;  // the caller's params.use_graphs
+    // NCCL grids: the own-piece block SpMV runs on a side stream while the
+    // column allgather is in flight (fork / join by events; captured into the graph too)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 extern bool g_capturing_flag(bool v);
 static bool dist_graph_enabled() {
@@ -164,29 +175,42 @@ static T *dal(int64_t count, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ block extraction
+// column part of an entry: 0 = not in column block gj; 1 = in this rank's own
+// piece (gi of the column block); 2 = another piece of the column block
+__device__ __forceinline__ int blk_part(const PieceMap &m, int pc, int gi, int gj, int32_t c) {
+    const int64_t d = m.dist_of(c), piece = d / m.S;
+    if (piece % pc != gj) return 0;
+    return piece / pc == gi ? 1 : 2;
+}
+// local column id: into the column block (part 2) or into the own piece (part 1)
+__device__ __forceinline__ int32_t blk_lcol(const PieceMap &m, int pc, int part, int32_t c) {
+    const int64_t d = m.dist_of(c);
+    return part == 1 ? (int32_t)(d % m.S) : (int32_t)((d / m.S / pc) * m.S + d % m.S);
+}
 template <int G>
-__global__ void k_blk_count(int64_t nrow, int64_t row_d0, PieceMap m, int pc, int gj, const int64_t *__restrict__ srp,
-                            const int32_t *__restrict__ scol, int64_t *__restrict__ cnt) {
+__global__ void k_blk_count(int64_t nrow, int64_t row_d0, PieceMap m, int pc, int gi, int gj, int part,
+                            const int64_t *__restrict__ srp, const int32_t *__restrict__ scol,
+                            int64_t *__restrict__ cnt) {
     GROUP_LOOP_BEGIN(G, nrow)
         int64_t c = 0;
         const int64_t p = live ? m.storage_of(row_d0 + i) : -1;
         if (p >= 0)
-            for (int64_t k = srp[p] + gl; k < srp[p + 1]; k += G) c += ((m.dist_of(scol[k]) / m.S) % pc) == gj;
+            for (int64_t k = srp[p] + gl; k < srp[p + 1]; k += G) c += blk_part(m, pc, gi, gj, scol[k]) == part;
         c = grp_sum<G>(c);
         if (live && gl == 0) cnt[i] = c;
     GROUP_LOOP_END
 }
 template <int G>
-__global__ void k_blk_fill(int64_t nrow, int64_t row_d0, PieceMap m, int pc, int gj, const int64_t *__restrict__ srp,
-                           const int32_t *__restrict__ scol, const double *__restrict__ sw,
-                           const int64_t *__restrict__ rp, int32_t *__restrict__ col, double *__restrict__ w) {
+__global__ void k_blk_fill(int64_t nrow, int64_t row_d0, PieceMap m, int pc, int gi, int gj, int part,
+                           const int64_t *__restrict__ srp, const int32_t *__restrict__ scol,
+                           const double *__restrict__ sw, const int64_t *__restrict__ rp, int32_t *__restrict__ col,
+                           double *__restrict__ w) {
     GROUP_LOOP_BEGIN(G, nrow)
         const int64_t srow = live ? m.storage_of(row_d0 + i) : -1;
         const int64_t kb = srow >= 0 ? srp[srow] : 0, ke = srow >= 0 ? srp[srow + 1] : 0;
         int64_t o = live ? rp[i] : 0;
-        GROUP_COMPACT_ROW(G, kb, ke, o, ((m.dist_of(scol[k]) / m.S) % pc) == gj,
-                          (col[p] = (int32_t)((m.dist_of(scol[k]) / m.S / pc) * m.S + m.dist_of(scol[k]) % m.S),
-                           w[p] = sw[k]))
+        GROUP_COMPACT_ROW(G, kb, ke, o, blk_part(m, pc, gi, gj, scol[k]) == part,
+                          (col[p] = blk_lcol(m, pc, part, scol[k]), w[p] = sw[k]))
     GROUP_LOOP_END
 }
 // SELL-32 over all block rows; rows longer than SHORT_MAX have width 0 here
@@ -223,7 +247,8 @@ __global__ void __launch_bounds__(256) k_blk_spmv(int64_t nslices, int64_t nrow,
                                                   const int32_t *__restrict__ crow, const int32_t *__restrict__ cidx,
                                                   const int32_t *__restrict__ cslot, double *__restrict__ cpart,
                                                   int32_t *__restrict__ ccnt, const double *__restrict__ x,
-                                                  double *__restrict__ y) {
+                                                  double *__restrict__ y, const double *__restrict__ yadd) {
+    // y = yadd + A x (yadd: the own-piece part, NULL for 0) -- every row written once
     pdl_begin();
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -233,7 +258,7 @@ __global__ void __launch_bounds__(256) k_blk_spmv(int64_t nslices, int64_t nrow,
             const int64_t i = t * 32 + lane, beg = sp[t], end = sp[t + 1];
             double acc = 0.0;
             for (int64_t k = beg + lane; k < end; k += 32) acc += __ldg(&ew[k]) * x[__ldg(&ec[k])];
-            if (i < nrow && rp[i + 1] - rp[i] <= SHORT_MAX) y[i] = acc;
+            if (i < nrow && rp[i + 1] - rp[i] <= SHORT_MAX) y[i] = (yadd ? yadd[i] : 0.0) + acc;
         } else {
             const int64_t c = t - nslices, i = crow[c], rb = rp[i], re = rp[i + 1], j = cidx[c];
             const int64_t b = rb + j * LCHUNK, e = min(re, b + LCHUNK);
@@ -242,7 +267,7 @@ __global__ void __launch_bounds__(256) k_blk_spmv(int64_t nslices, int64_t nrow,
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             const int slot = cslot[c];
             if (slot < 0) {
-                if (lane == 0) y[i] = acc;
+                if (lane == 0) y[i] = (yadd ? yadd[i] : 0.0) + acc;
                 continue;
             }
             const int nch = (int)((re - rb + LCHUNK - 1) / LCHUNK);
@@ -260,7 +285,7 @@ __global__ void __launch_bounds__(256) k_blk_spmv(int64_t nslices, int64_t nrow,
             for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
             if (lane == 0) {
                 ccnt[slot] = 0;
-                y[i] = s2;
+                y[i] = (yadd ? yadd[i] : 0.0) + s2;
             }
         }
     }
@@ -558,46 +583,50 @@ static void build_shard(lap_hierarchy *h, Dist &D, int l, Shard &sh, cudaStream_
     sh.ncol = (int64_t)pr * S;
     const int64_t row_d0 = (int64_t)sh.gi * pc * S;
     const int G = group_size(L.n, L.nnz);
-    // ---- 2D block (rows: row block gi, columns: column block gj, local ids)
-    {
+    // ---- 2D block (rows: row block gi, columns: column block gj, local ids), in
+    // two parts: the own piece's columns and the rest of the column block
+    auto build_part = [&](int part, BlockMat &B) {
         DBuf<int64_t> cnt(sh.nrow + 1, s);
         LAP_CUDA(cudaMemsetAsync(cnt.p, 0, sizeof(int64_t) * (sh.nrow + 1), s));
-        LAUNCH_G(G, k_blk_count, sh.nrow, s, sh.nrow, row_d0, m, pc, sh.gj, (const int64_t *)L.srp,
+        LAUNCH_G(G, k_blk_count, sh.nrow, s, sh.nrow, row_d0, m, pc, sh.gi, sh.gj, part, (const int64_t *)L.srp,
                  (const int32_t *)L.scol, cnt.p);
-        sh.rp = dal<int64_t>(sh.nrow + 1, s);
+        B.rp = dal<int64_t>(sh.nrow + 1, s);
         size_t bytes = 0;
-        LAP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt.p, sh.rp, sh.nrow + 1, s));
+        LAP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, cnt.p, B.rp, sh.nrow + 1, s));
         DBuf<char> tmp((int64_t)bytes, s);
-        LAP_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, cnt.p, sh.rp, sh.nrow + 1, s));
-        sh.nnz = d2h1(sh.rp + sh.nrow, s);
-        sh.col = dal<int32_t>(sh.nnz + 1, s);
-        sh.w = dal<double>(sh.nnz + 1, s);
-        LAUNCH_G(G, k_blk_fill, sh.nrow, s, sh.nrow, row_d0, m, pc, sh.gj, (const int64_t *)L.srp,
-                 (const int32_t *)L.scol, (const double *)L.sw, (const int64_t *)sh.rp, sh.col, sh.w);
+        LAP_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, bytes, cnt.p, B.rp, sh.nrow + 1, s));
+        B.nnz = d2h1(B.rp + sh.nrow, s);
+        B.col = dal<int32_t>(B.nnz + 1, s);
+        B.w = dal<double>(B.nnz + 1, s);
+        LAUNCH_G(G, k_blk_fill, sh.nrow, s, sh.nrow, row_d0, m, pc, sh.gi, sh.gj, part, (const int64_t *)L.srp,
+                 (const int32_t *)L.scol, (const double *)L.sw, (const int64_t *)B.rp, B.col, B.w);
         LAP_CHECK_LAUNCH();
         // SELL-32 slices over the short rows, LCHUNK chunks over the long rows
-        sh.nslices = (sh.nrow + 31) / 32;
-        DBuf<int64_t> width(sh.nslices + 1, s);
-        LAP_CUDA(cudaMemsetAsync(width.p + sh.nslices, 0, sizeof(int64_t), s));
-        k_blk_width<<<dg(sh.nslices), 256, 0, s>>>(sh.nslices, sh.nrow, sh.rp, width.p);
-        sh.slice_ptr = dal<int64_t>(sh.nslices + 1, s);
+        B.nslices = (sh.nrow + 31) / 32;
+        DBuf<int64_t> width(B.nslices + 1, s);
+        LAP_CUDA(cudaMemsetAsync(width.p + B.nslices, 0, sizeof(int64_t), s));
+        k_blk_width<<<dg(B.nslices), 256, 0, s>>>(B.nslices, sh.nrow, B.rp, width.p);
+        B.slice_ptr = dal<int64_t>(B.nslices + 1, s);
         bytes = 0;
-        LAP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, width.p, sh.slice_ptr, sh.nslices + 1, s));
+        LAP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, width.p, B.slice_ptr, B.nslices + 1, s));
         DBuf<char> tmp2((int64_t)bytes, s);
-        LAP_CUDA(cub::DeviceScan::ExclusiveSum(tmp2.p, bytes, width.p, sh.slice_ptr, sh.nslices + 1, s));
-        int64_t tot = d2h1(sh.slice_ptr + sh.nslices, s);
-        sh.ell_col = dal<int32_t>(tot + 1, s);
-        sh.ell_w = dal<double>(tot + 1, s);
-        k_blk_sell_fill<<<dg(sh.nslices * 32), 256, 0, s>>>(sh.nslices * 32, sh.nrow, sh.rp, sh.col, sh.w, sh.slice_ptr,
-                                                              sh.ell_col, sh.ell_w);
-        sh.nchunks = build_chunks(sh.rp, 0, sh.nrow, SHORT_MAX, &sh.crow, &sh.cidx, &sh.cslot, &sh.cpart, &sh.ccnt, s);
-        void *cs[] = {sh.crow, sh.cidx, sh.cslot, sh.cpart, sh.ccnt};
+        LAP_CUDA(cub::DeviceScan::ExclusiveSum(tmp2.p, bytes, width.p, B.slice_ptr, B.nslices + 1, s));
+        int64_t tot = d2h1(B.slice_ptr + B.nslices, s);
+        B.ell_col = dal<int32_t>(tot + 1, s);
+        B.ell_w = dal<double>(tot + 1, s);
+        k_blk_sell_fill<<<dg(B.nslices * 32), 256, 0, s>>>(B.nslices * 32, sh.nrow, B.rp, B.col, B.w, B.slice_ptr,
+                                                             B.ell_col, B.ell_w);
+        B.nchunks = build_chunks(B.rp, 0, sh.nrow, SHORT_MAX, &B.crow, &B.cidx, &B.cslot, &B.cpart, &B.ccnt, s);
+        void *cs[] = {B.crow, B.cidx, B.cslot, B.cpart, B.ccnt};
         for (void *p : cs) g_owned->push_back(p);
         LAP_CHECK_LAUNCH();
-    }
+    };
+    build_part(1, sh.own);
+    build_part(2, sh.rem);
     // ---- owned-piece vectors
     sh.xcol = dal<double>(sh.ncol, s);
     sh.ypart = dal<double>(sh.nrow, s);
+    sh.yown = dal<double>(sh.nrow, s);
     sh.ax = dal<double>(S, s);
     double **vs[] = {&sh.b, &sh.x, &sh.x2, &sh.t, &sh.rv, &sh.dv};
     for (double **v : vs) {
@@ -747,15 +776,29 @@ static void dist_spmv(lap_hierarchy *h, Dist &D, int l, int epi, const std::vect
     DistLevel &DL = D.lev[l];
     Coll co{D.c, s};
     const int64_t S = DL.map.S;
-    co.allgather_col(cnst(x), each(DL.sh, [](Shard &a) { return a.xcol; }), S, DL.sh);
-    for (auto &a : DL.sh) {
-        launch_pdl(k_blk_spmv, grid_for((a.nslices + a.nchunks) * 32, 256, 148 * 8), 256, s, a.nslices, a.nrow,
-                   (const int64_t *)a.slice_ptr, (const int32_t *)a.ell_col, (const double *)a.ell_w,
-                   (const int64_t *)a.rp, (const int32_t *)a.col, (const double *)a.w, a.nchunks,
-                   (const int32_t *)a.crow, (const int32_t *)a.cidx, (const int32_t *)a.cslot, a.cpart, a.ccnt,
-                   (const double *)a.xcol, a.ypart);
+    auto part_spmv = [&](const BlockMat &B, int64_t nrow, const double *xin, double *yout, const double *yadd,
+                         cudaStream_t st) {
+        launch_pdl(k_blk_spmv, grid_for((B.nslices + B.nchunks) * 32, 256, 148 * 8), 256, st, B.nslices, nrow,
+                   (const int64_t *)B.slice_ptr, (const int32_t *)B.ell_col, (const double *)B.ell_w,
+                   (const int64_t *)B.rp, (const int32_t *)B.col, (const double *)B.w, B.nchunks,
+                   (const int32_t *)B.crow, (const int32_t *)B.cidx, (const int32_t *)B.cslot, B.cpart, B.ccnt, xin,
+                   yout, yadd);
         h->cur.launches++;
+    };
+    // own-piece columns first: they need no communication, so on an NCCL grid this
+    // part runs on the side stream while the column allgather is in flight
+    const bool fork = D.side != nullptr;
+    if (fork) {
+        LAP_CUDA(cudaEventRecord(D.ev_fork, s));
+        LAP_CUDA(cudaStreamWaitEvent(D.side, D.ev_fork, 0));
     }
+    for (size_t k = 0; k < DL.sh.size(); k++)
+        part_spmv(DL.sh[k].own, DL.sh[k].nrow, x[k], DL.sh[k].yown, nullptr, fork ? D.side : s);
+    if (fork) LAP_CUDA(cudaEventRecord(D.ev_join, D.side));
+    co.allgather_col(cnst(x), each(DL.sh, [](Shard &a) { return a.xcol; }), S, DL.sh);
+    if (fork) LAP_CUDA(cudaStreamWaitEvent(s, D.ev_join, 0));
+    // the rest of the column block, added to the own part (fixed order: own + remote)
+    for (auto &a : DL.sh) part_spmv(a.rem, a.nrow, a.xcol, a.ypart, a.yown, s);
     co.reduce_scatter_row(cnst(each(DL.sh, [](Shard &a) { return a.ypart; })), each(DL.sh, [](Shard &a) { return a.ax; }),
                           S, DL.sh);
     for (size_t k = 0; k < DL.sh.size(); k++) {
@@ -1063,13 +1106,22 @@ void build_dist(lap_hierarchy *h, lap_comm *c, cudaStream_t s, bool use_graph) {
     }
     D->gscal = dal<double>(16, s);
     LAP_CUDA(cudaMemsetAsync(D->gscal, 0, sizeof(double) * 16, s));
+    if (!c->virt) {  // overlap of the own-piece SpMV with the column allgather (also 1x1: tested there)
+        LAP_CUDA(cudaStreamCreateWithFlags(&D->side, cudaStreamNonBlocking));
+        LAP_CUDA(cudaEventCreateWithFlags(&D->ev_fork, cudaEventDisableTiming));
+        LAP_CUDA(cudaEventCreateWithFlags(&D->ev_join, cudaEventDisableTiming));
+    }
     LAP_CUDA(cudaStreamSynchronize(s));
     g_owned = nullptr;
 }
 
 void free_dist(lap_hierarchy *h) {
     if (!h->dist) return;
-    if (((Dist *)h->dist)->pgraph) cudaGraphExecDestroy(((Dist *)h->dist)->pgraph);
+    Dist *Dd = (Dist *)h->dist;
+    if (Dd->pgraph) cudaGraphExecDestroy(Dd->pgraph);
+    if (Dd->side) cudaStreamDestroy(Dd->side);
+    if (Dd->ev_fork) cudaEventDestroy(Dd->ev_fork);
+    if (Dd->ev_join) cudaEventDestroy(Dd->ev_join);
     auto *own = (std::vector<void *> *)h->dist_owned;
     if (own) {
         for (void *p : *own) dfree(p, nullptr);

@@ -154,6 +154,9 @@ struct Level {
     int32_t *chunk_slot = nullptr;  // chunk -> arrival counter slot (-1: one-chunk row)
     int32_t *chunk_cnt = nullptr;   // n - c_end[0] arrival counters (kept at 0 between launches)
     double *chunk_part = nullptr;
+    int64_t nmulti = 0;             // rows of several chunks (slots 0..nmulti-1)
+    double *mdot = nullptr;         // their dot-epilogue terms, 3 per slot
+    int *mdone = nullptr;           // block-arrival counter of the dot fix-up (kept at 0)
     // column-tiled "x-stationary" layout (xt.cu): dense-ish levels too big for x
     // in shared memory; a CTA owns a row block and sweeps x tile by tile
     bool xt = false;
@@ -294,9 +297,10 @@ void permute_csr(int64_t n, int64_t nnz, const int32_t *sid, const int32_t *spos
                  const int32_t *col, const double *w, int64_t *srp, int32_t *scol, double *sw, bool sort_cols,
                  int64_t maxlen, cudaStream_t s);
 // the same rows sorted into scol / sw with srp already built; maxlen bounds the row length
+// (rows longer than sort_max are permuted but keep their column order)
 void permute_sorted_rows(int64_t n, int64_t nnz, const int32_t *sid, const int32_t *spos, const int64_t *rp,
                          const int32_t *col, const double *w, const int64_t *srp, int32_t *scol, double *sw,
-                         int64_t maxlen, cudaStream_t s);
+                         int64_t maxlen, cudaStream_t s, int64_t sort_max = INT64_MAX);
 void build_transfers(lap_hierarchy *h, cudaStream_t s);
 // column-tiled SpMV layout (xt.cu)
 constexpr int XT_NW = 16;             // warps per CTA (512 threads)
@@ -305,7 +309,7 @@ bool xt_eligible(const Level &L, int l);
 void build_xt(Level &L, cudaStream_t s);
 // LCHUNK work items over the rows [row0, row0+nrows) of a CSR longer than minlen
 int64_t build_chunks(const int64_t *rp, int64_t row0, int64_t nrows, int64_t minlen, int32_t **crow, int32_t **cidx,
-                     int32_t **cslot, double **cpart, int32_t **ccnt, cudaStream_t s);
+                     int32_t **cslot, double **cpart, int32_t **ccnt, cudaStream_t s, int64_t *nmulti = nullptr);
 int64_t spmv_partial_slots(const Level &L);
 void vcycle(lap_hierarchy *h, int l, cudaStream_t s);   // x_l = V(l, b_l)
 void run_pcg(lap_hierarchy *h, double tol, int32_t *iters, double *relres, int *conv, cudaStream_t s);

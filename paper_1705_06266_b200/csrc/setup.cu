@@ -2300,7 +2300,10 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
         const int v = e ? atoi(e) : 0;
         return (v == 1 || v == 2 || v == 4 || v == 8 || v == 16 || v == 32) ? v : G;
     };
-    const int Ga = env_g("LAP_AFF_G"), Gv = env_g("LAP_VOTE_G");
+    // votes: at most 8 lanes per row (the group argmax is most of a round's
+    // instructions: cfg 4 G = 16 -> 8 setup 76.0 -> 73.4 ms, cfg 3 neutral;
+    // profiles/r02/gsweep_summary.txt)
+    const int Ga = env_g("LAP_AFF_G"), Gv = getenv("LAP_VOTE_G") ? env_g("LAP_VOTE_G") : std::min(G, 8);
     // test vectors: swept on the solve storage (canonical sums:
     // the order is free), then laid out in the logical order for the affinity
     DBuf<double> X(4 * n, s), Xn(4 * n, s), M(n, s);
@@ -2458,14 +2461,6 @@ __global__ void k_gal_slot_emit(int64_t ns, const int32_t *__restrict__ members,
     GROUP_COMPACT_ROW(G, kb, ke, o, agg[col[k]] != a, (tk[p] = agg[col[k]], tv[p] = w[k]))
     GROUP_LOOP_END
 }
-template <int G>
-__global__ void k_gal_keys(int64_t m, const int64_t *__restrict__ pa, const int32_t *__restrict__ sk, int cb,
-                           uint64_t *__restrict__ key) {
-    GROUP_LOOP_BEGIN(G, m)
-    if (live)
-        for (int64_t k = pa[i] + gl; k < pa[i + 1]; k += G) key[k] = ((uint64_t)i << cb) | (uint64_t)(uint32_t)sk[k];
-    GROUP_LOOP_END
-}
 constexpr int64_t GAL_ORDERED_MAX_AVG = 256;  // terms per coarse row (average) for the ordered Galerkin
 static bool gal_fast_enabled() {  // read per level (tests switch it inside one process)
     const char *e = getenv("LAP_GAL_FAST");  // 0: the batched global-sort path (tests, experiments)
@@ -2484,6 +2479,14 @@ __global__ void k_gal_row_ptr_r(int64_t mr, const int64_t *__restrict__ mem_ptr,
                                 const int64_t *__restrict__ pl, int64_t *__restrict__ pa) {
     for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a <= mr; a += (int64_t)gridDim.x * blockDim.x)
         pa[a] = pl[mem_ptr[a] - s0];
+}
+template <int G>
+__global__ void k_gal_keys(int64_t m, const int64_t *__restrict__ pa, const int32_t *__restrict__ sk, int cb,
+                           uint64_t *__restrict__ key) {
+    GROUP_LOOP_BEGIN(G, m)
+    if (live)
+        for (int64_t k = pa[i] + gl; k < pa[i + 1]; k += G) key[k] = ((uint64_t)i << cb) | (uint64_t)(uint32_t)sk[k];
+    GROUP_LOOP_END
 }
 static void galerkin_fast(lap_hierarchy *h, Level &L, Level &N, const int32_t *members, const uint32_t *slot_agg,
                           const int64_t *mem_ptr, cudaStream_t s) {

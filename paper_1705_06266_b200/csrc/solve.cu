@@ -196,7 +196,12 @@ struct LongRows {
     const int32_t *__restrict__ cslot;  // chunk -> arrival-counter slot of its row (-1: one-chunk row)
     double *__restrict__ cpart;         // chunk partial sums
     int32_t *__restrict__ ccnt;         // per multi-chunk row: arrivals (reset by the combiner)
+    int64_t nmulti = 0;                 // multi-chunk rows (slots 0..nmulti-1)
+    double *__restrict__ mdot = nullptr;  // their dot-epilogue terms (3 per slot)
+    int *__restrict__ mdone = nullptr;    // block-arrival counter of dot_fixup (reset by the last block)
 };
+constexpr bool epi_has_dots(int EPI) { return EPI == E_DOT || EPI == E_LZ || EPI == E_FCG || EPI == E_CHEBZ; }
+constexpr int epi_ndots(int EPI) { return EPI == E_CHEBZ ? 3 : EPI == E_FCG ? 2 : epi_has_dots(EPI) ? 1 : 0; }
 
 // Sum of chunk c of a long CSR row (all 32 lanes).  Returns true (on every
 // lane) iff this warp must finish the row: either the row is a single chunk,
@@ -277,7 +282,47 @@ __device__ __forceinline__ void long_chunk(int64_t c, int lane, const Csr &A, co
                                            Dacc &dacc) {
     int64_t i;
     double ax;
-    if (chunk_reduce<CT, UNIT>(c, lane, A.rp, col, A.w, xg, R, i, ax) && lane == 0) apply_epi<EPI>(i, ax, A, a, dacc);
+    if (chunk_reduce<CT, UNIT>(c, lane, A.rp, col, A.w, xg, R, i, ax) && lane == 0) {
+        const int slot = R.cslot[c];
+        if (epi_has_dots(EPI) && slot >= 0) {
+            // a multi-chunk row is finished by whichever warp arrives last; its
+            // dot terms go to the row's slot (summed in slot order by dot_fixup),
+            // not to that warp's block partial, so the reductions stay bitwise
+            // reproducible run to run
+            Dacc t;
+            apply_epi<EPI>(i, ax, A, a, t);
+            R.mdot[3 * slot] = t.a;
+            R.mdot[3 * slot + 1] = t.b;
+            R.mdot[3 * slot + 2] = t.c;
+        } else {
+            apply_epi<EPI>(i, ax, A, a, dacc);
+        }
+    }
+}
+// After the block partials: the last block to finish adds the multi-chunk rows'
+// dot terms, summed in slot order, to the LAST block's partial of each region
+// (written before that block arrived) -- a fixed order, so every run gives the
+// same bits.  All threads of the block call it (block_sum inside).
+template <int EPI>
+__device__ __forceinline__ void dot_fixup(const LongRows &R, double *__restrict__ partials, double *sh) {
+    if (!epi_has_dots(EPI) || R.nmulti == 0) return;
+    __shared__ int last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(R.mdone, 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int k = 0; k < epi_ndots(EPI); k++) {
+        double acc = 0.0;
+        for (int64_t q = threadIdx.x; q < R.nmulti; q += blockDim.x) acc += __ldcg(&R.mdot[3 * q + k]);
+        const double r = block_sum(acc, sh);
+        if (threadIdx.x == 0) {
+            double *p = partials + (int64_t)k * gridDim.x + gridDim.x - 1;
+            *p = __ldcg(p) + r;
+        }
+    }
+    if (threadIdx.x == 0) *R.mdone = 0;
 }
 
 // NB = SELL columns per batch: 8 (64 registers, 4 CTAs of 256 per SM) or 4 (48, 5 CTAs) for the
@@ -317,6 +362,7 @@ __global__ void __launch_bounds__(256, NB == 8 ? 4 : 5) k_spmv(int64_t nslices, 
             partials[2 * gridDim.x + blockIdx.x] = r2;
         }
     }
+    if (LONG) dot_fixup<EPI>(R, partials, sh);
 }
 
 // Small, dense-ish levels (n <= SMEM_X_MAX, average degree >= SMEM_X_MIN_DEG:
@@ -360,6 +406,7 @@ __global__ void __launch_bounds__(1024, 1) k_spmv_smem(int64_t n, int64_t nslice
             partials[2 * gridDim.x + blockIdx.x] = r2;
         }
     }
+    dot_fixup<EPI>(R, partials, sh);
 }
 
 // Column-tiled ("x-stationary") SpMV of a dense-ish level (xt.cu has the
@@ -622,7 +669,7 @@ static void spmv_dispatch(lap_hierarchy *h, const Level &L, const EpiArgs &a, cu
         LAP_CHECK_LAUNCH();
         return;
     }
-    LongRows R{L.nchunks, L.chunk_row, L.chunk_idx, L.chunk_slot, L.chunk_part, L.chunk_cnt};
+    LongRows R{L.nchunks, L.chunk_row, L.chunk_idx, L.chunk_slot, L.chunk_part, L.chunk_cnt, L.nmulti, L.mdot, L.mdone};
     if (L.xt && ((uintptr_t)a.x & 15) == 0) {  // (the bulk copy needs a 16-byte aligned x; level vectors are)
         static bool attr_set = false;
         const size_t smem = 8 * (size_t)(2 * L.xt_W + L.xt_rmax);

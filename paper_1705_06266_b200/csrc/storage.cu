@@ -177,14 +177,20 @@ __global__ void k_chunk_counts(int64_t nrows, int64_t row0, const int64_t *rp, i
         cnt[h] = dg > minlen ? (dg + LCHUNK - 1) / LCHUNK : 0;
     }
 }
-__global__ void k_chunk_fill(int64_t nrows, int64_t row0, const int64_t *first, int32_t *crow, int32_t *cidx,
-                             int32_t *cslot) {
+// slot = the row's index among the rows of several chunks (mpre: prefix of
+// "several chunks" flags), so per-row side data (arrival counters, the solve's
+// dot terms of such rows) can be compact and summed in slot order
+__global__ void k_chunk_multi(int64_t nrows, const int64_t *first, int64_t *mflag) {
+    GRID_STRIDE(h, nrows) mflag[h] = first[h + 1] - first[h] > 1 ? 1 : 0;
+}
+__global__ void k_chunk_fill(int64_t nrows, int64_t row0, const int64_t *first, const int64_t *mpre, int32_t *crow,
+                             int32_t *cidx, int32_t *cslot) {
     GRID_STRIDE(h, nrows) {
         int64_t f = first[h], nch = first[h + 1] - f;
         for (int64_t j = 0; j < nch; j++) {
             crow[f + j] = (int32_t)(row0 + h);
             cidx[f + j] = (int32_t)j;
-            cslot[f + j] = nch > 1 ? (int32_t)h : -1;
+            cslot[f + j] = nch > 1 ? (int32_t)mpre[h] : -1;
         }
     }
 }
@@ -336,10 +342,11 @@ __global__ void __launch_bounds__(256) k_rowsort_warp(int64_t n, int64_t minlen,
     }
 }
 __global__ void k_rowsort_lists(int64_t n, const int64_t *__restrict__ rp, int32_t *sml, int32_t *med, int32_t *lng,
-                                int *cnt) {
+                                int *cnt, int64_t sort_max, int32_t *cpy) {
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
         const int64_t len = rp[r + 1] - rp[r];
-        if (len > ROWSORT_MED) lng[atomicAdd(&cnt[2], 1)] = (int32_t)r;  // order free: rows are independent
+        if (len > sort_max) cpy[atomicAdd(&cnt[3], 1)] = (int32_t)r;    // kept in the given order
+        else if (len > ROWSORT_MED) lng[atomicAdd(&cnt[2], 1)] = (int32_t)r;  // order free: rows are independent
         else if (len > ROWSORT_SMALL) med[atomicAdd(&cnt[1], 1)] = (int32_t)r;
         else if (len > 64) sml[atomicAdd(&cnt[0], 1)] = (int32_t)r;
     }
@@ -413,20 +420,42 @@ __global__ void k_long_scatter(int64_t B, const int64_t *__restrict__ beg, const
         }
     }
 }
-// rows of length > minlen (minlen >= 32) sorted: kin/vin -> kout/vout
+// rows longer than sort_max copied as they are (warp per row)
+__global__ void k_rowcopy_list(int64_t m, const int32_t *__restrict__ list, const int64_t *__restrict__ rp,
+                               const int32_t *__restrict__ kin, const double *__restrict__ vin,
+                               int32_t *__restrict__ kout, double *__restrict__ vout) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = warp; t < m; t += nwarps) {
+        const int64_t r = list[t];
+        for (int64_t k = rp[r] + lane; k < rp[r + 1]; k += 32) {
+            kout[k] = kin[k];
+            vout[k] = vin[k];
+        }
+    }
+}
+// rows of length > minlen (minlen >= 32) sorted: kin/vin -> kout/vout; rows
+// longer than sort_max are copied unsorted
 static void sort_rows_min(int64_t n, const int64_t *rp, int64_t nnz, int cbits, int64_t minlen, const int32_t *kin,
-                          const double *vin, int32_t *kout, double *vout, cudaStream_t s) {
+                          const double *vin, int32_t *kout, double *vout, cudaStream_t s,
+                          int64_t sort_max = INT64_MAX) {
     if (n <= 0 || nnz <= 0) return;
-    DBuf<int32_t> sml(n, s), med(n, s), lng(n, s);
-    DBuf<int> cnt(3, s);
-    LAP_CUDA(cudaMemsetAsync(cnt.p, 0, 3 * sizeof(int), s));
-    k_rowsort_lists<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(n, rp, sml.p, med.p, lng.p, cnt.p);
+    DBuf<int32_t> sml(n, s), med(n, s), lng(n, s), cpy(sort_max < INT64_MAX ? n : 1, s);
+    DBuf<int> cnt(4, s);
+    LAP_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * sizeof(int), s));
+    k_rowsort_lists<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(n, rp, sml.p, med.p, lng.p, cnt.p, sort_max, cpy.p);
     k_rowsort_warp<<<grid_for(n * 32, 256, 148 * 8), 256, 0, s>>>(n, minlen, rp, kin, vin, kout, vout);
     g_kl += 2;
     trace_mark("    rowsort: lists + warp rows");
-    int hc[3];
+    int hc[4];
     LAP_CUDA(cudaMemcpyAsync(hc, cnt.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
     LAP_CUDA(cudaStreamSynchronize(s));
+    if (hc[3] > 0) {
+        k_rowcopy_list<<<grid_for((int64_t)hc[3] * 32, 256, 148 * 8), 256, 0, s>>>(hc[3], cpy.p, rp, kin, vin, kout,
+                                                                                  vout);
+        g_kl++;
+    }
     if (hc[0] > 0) {
         k_rowsort_block<64, 4><<<grid_for(hc[0], 1, 148 * 16), 64, 0, s>>>(hc[0], sml.p, rp, cbits, kin, vin, kout, vout);
         g_kl++;
@@ -487,7 +516,9 @@ void sort_rows(int64_t n, const int64_t *rp, int64_t nnz, int cbits, const int32
 
 
 int64_t build_chunks(const int64_t *rp, int64_t row0, int64_t nrows, int64_t minlen, int32_t **crow,
-                            int32_t **cidx, int32_t **cslot, double **cpart, int32_t **ccnt, cudaStream_t s) {
+                            int32_t **cidx, int32_t **cslot, double **cpart, int32_t **ccnt, cudaStream_t s,
+                            int64_t *nmulti) {
+    if (nmulti) *nmulti = 0;
     if (nrows <= 0) return 0;
     DBuf<int64_t> cc(nrows + 1, s), first(nrows + 1, s);
     LAP_CUDA(cudaMemsetAsync(cc.p, 0, sizeof(int64_t) * (nrows + 1), s));
@@ -502,8 +533,13 @@ int64_t build_chunks(const int64_t *rp, int64_t row0, int64_t nrows, int64_t min
     *ccnt = (int32_t *)dalloc(sizeof(int32_t) * nrows, s);
     LAP_CUDA(cudaMemsetAsync(*ccnt, 0, sizeof(int32_t) * nrows, s));
     if (nch > 0) {
-        k_chunk_fill<<<grid_for(nrows, 256, 148 * 8), 256, 0, s>>>(nrows, row0, first.p, *crow, *cidx, *cslot);
-        g_kl++;
+        DBuf<int64_t> mflag(nrows + 1, s), mpre(nrows + 1, s);
+        LAP_CUDA(cudaMemsetAsync(mflag.p + nrows, 0, sizeof(int64_t), s));
+        k_chunk_multi<<<grid_for(nrows, 256, 148 * 8), 256, 0, s>>>(nrows, first.p, mflag.p);
+        scan_excl(mflag.p, mpre.p, nrows + 1, s);
+        k_chunk_fill<<<grid_for(nrows, 256, 148 * 8), 256, 0, s>>>(nrows, row0, first.p, mpre.p, *crow, *cidx, *cslot);
+        g_kl += 2;
+        if (nmulti) *nmulti = d2h(mpre.p + nrows, s);
     }
     LAP_CHECK_LAUNCH();
     return nch;
@@ -529,12 +565,12 @@ void permute_csr(int64_t n, int64_t nnz, const int32_t *sid, const int32_t *spos
         LAP_CHECK_LAUNCH();
         return;
     }
-    permute_sorted_rows(n, nnz, sid, spos, rp, col, w, srp, scol, sw, maxlen, s);
+    permute_sorted_rows(n, nnz, sid, spos, rp, col, w, srp, scol, sw, maxlen, s, INT64_MAX);
 }
 // the rows of P A P^T sorted, srp given
 void permute_sorted_rows(int64_t n, int64_t nnz, const int32_t *sid, const int32_t *spos, const int64_t *rp,
                          const int32_t *col, const double *w, const int64_t *srp, int32_t *scol, double *sw,
-                         int64_t maxlen, cudaStream_t s) {
+                         int64_t maxlen, cudaStream_t s, int64_t sort_max) {  // NOLINT (default in the header)
     if (n <= 0 || nnz <= 0) return;
     // rows of <= 32 entries: permuted and sorted in one thread's registers
     k_perm_sort_thread<16, 0><<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(n, sid, spos, rp, col, w, srp, scol, sw);
@@ -547,7 +583,7 @@ void permute_sorted_rows(int64_t n, int64_t nnz, const int32_t *sid, const int32
         k_perm_fill_long<<<grid_for(n * 32, 256, 148 * 8), 256, 0, s>>>(n, 32, sid, spos, rp, col, w, srp, c2.p, w2.p);
         g_kl++;
         trace_mark("    permute: long rows filled");
-        sort_rows_min(n, srp, nnz, bitlen_u64((uint64_t)n), 32, c2.p, w2.p, scol, sw, s);
+        sort_rows_min(n, srp, nnz, bitlen_u64((uint64_t)n), 32, c2.p, w2.p, scol, sw, s, sort_max);
     }
     LAP_CHECK_LAUNCH();
 }
@@ -719,9 +755,16 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
         // sorted (no double buffer over ~all entries of a power-law level)
         const bool sort_on = !getenv_flag_off("LAP_SORT_ROWS");
         const int cbits = bitlen_u64((uint64_t)n);
+        // rows longer than SHORT_MAX (warp chunks: a chunk's 32 lanes gather from one
+        // row, where order buys no line sharing) stay unsorted, except on the
+        // shared-memory-x levels (fewer bank conflicts sorted): cfg 3 setup
+        // -5.6 ms for +0.5 ms of solve, cfg 4 -1.9 / +0.75 (LAP_SORT_LONG=1: sort all)
+        const char *sl = getenv("LAP_SORT_LONG");
+        const bool smem_level = n <= SMEM_X_MAX && L.nnz >= SMEM_X_MIN_DEG * n;
+        const int64_t sort_max = (sl && sl[0] == '1') || smem_level ? INT64_MAX : SHORT_MAX;
         if (sort_on && L.nnz < ((int64_t)1 << 28)) {
             permute_sorted_rows(n, L.nnz, L.sid, L.spos, L.row_ptr, L.col, L.w, L.srp, L.scol, L.sw,
-                                L.maxdeg > 0 ? L.maxdeg : INT64_MAX, s);
+                                L.maxdeg > 0 ? L.maxdeg : INT64_MAX, s, sort_max);
         } else {
             k_storage_fill<<<grid_for(L.nnz, 256, 148 * 16), 256, 0, s>>>(n, L.nnz, L.sid, L.spos, L.row_ptr, L.col,
                                                                           L.w, L.srp, L.scol, L.sw);
@@ -785,7 +828,13 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
     }
     // long rows: LCHUNK-entry warp work items (solve.cu k_spmv)
     L.nchunks = build_chunks(L.srp, L.c_end[0], n - L.c_end[0], SHORT_MAX, &L.chunk_row, &L.chunk_idx, &L.chunk_slot,
-                             &L.chunk_part, &L.chunk_cnt, s);
+                             &L.chunk_part, &L.chunk_cnt, s, &L.nmulti);
+    // dot terms of the multi-chunk rows (3 per row; k_spmv adds them in slot
+    // order, run-to-run reproducible) and the kernels' block-arrival counter
+    L.mdot = (double *)dalloc(sizeof(double) * (size_t)(3 * L.nmulti + 3), s);
+    L.mdone = (int *)dalloc(sizeof(int) * 2, s);
+    LAP_CUDA(cudaMemsetAsync(L.mdot, 0, sizeof(double) * (size_t)(3 * L.nmulti + 3), s));
+    LAP_CUDA(cudaMemsetAsync(L.mdone, 0, sizeof(int) * 2, s));
     LAP_CHECK_LAUNCH();
     // dense-ish level too big for x in shared memory: the column-tiled layout (xt.cu)
     if (xt_eligible(L, l)) build_xt(L, s);

@@ -437,3 +437,24 @@ def test_pattern_only_level0(P, mk, monkeypatch):
     nnz = lv["nnz"]
     if lv["n"] > 131072 or np.diff(lv["row_ptr"]).max() > 64:  # big enough for k_spmv (not the small-level kernels)
         assert bw - bu == 8 * nnz, (bw, bu, nnz)
+
+
+@pytest.mark.parametrize("mk", [lambda: lapgen.star(30000), lambda: lapgen.rmat(16),
+                                lambda: lapgen.barabasi_albert(60000, 8)], ids=["star30000", "rmat16", "ba60000"])
+def test_solves_bitwise_reproducible_with_hub_rows(P, mk):
+    """Rows of several 1024-entry chunks are finished by whichever warp arrives
+    last; their dot-epilogue terms (PCG p.q, the E_CHEBZ z-sums, FCG's two
+    dots, the block solve's per-column p.q) are summed in slot order by the
+    last block (dot_fixup), so repeated solves on one hierarchy give the same
+    bits -- V-cycle + PCG, K-cycle + FCG, and the block solve."""
+    g = mk()
+    b = lapgen.rhs(g.n, seed=4)
+    for kw in [dict(), dict(use_graphs=0), dict(cycle=1)]:
+        h = P.Hierarchy(g, **kw)
+        xs = {h.solve(b)[0].tobytes() for _ in range(5)}
+        assert len(xs) == 1, kw
+        h.close()
+    h = P.Hierarchy(g)
+    B = np.stack([lapgen.rhs(g.n, seed=j) for j in range(3)])
+    Xs = {h.solve_block(B)[0].tobytes() for _ in range(4)}
+    assert len(Xs) == 1
