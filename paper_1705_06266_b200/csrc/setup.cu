@@ -2060,13 +2060,19 @@ __global__ void k_lzc_init_s(int64_t n, uint64_t base, const int32_t *__restrict
 // lambda-hat on the level's solve storage (built before this is called): the
 // Lanczos vectors live in the storage order; every sum is a CanonSum, so the
 // order changes no bit (the tridiagonal equals the oracle's).
-static double lanczos(lap_hierarchy *h, Level &L, int l, cudaStream_t s) {
+// Enqueued on its own stream (build_hierarchy): lambda-hat is needed only by
+// the solve, so the Lanczos steps of level l overlap the strength, voting and
+// Galerkin work of levels >= l; it only reads the level's storage and has its
+// own arrival counters; lambda-hat lands in *host_out (pinned) when s gets there.
+static void lanczos(lap_hierarchy *h, Level &L, int l, cudaStream_t s, double *host_out) {
     const int64_t n = L.n, nnz = L.nnz;
     const int steps = h->p.lanczos_steps;
     DBuf<double> v(n, s), vp(n, s), y(n, s), u(n, s), rs(n, s), al(64, s), be(64, s), lam(1, s);
     DBuf<LzState> st(1, s);
     DBuf<int> kk(1, s);
     DBuf<I128> cpart(L.nchunks > 0 ? L.nchunks : 1, s);
+    DBuf<int32_t> ccnt(L.nmulti > 0 ? L.nmulti : 1, s);  // not the sweeps' counters: they may run meanwhile
+    LAP_CUDA(cudaMemsetAsync(ccnt.p, 0, sizeof(int32_t) * (size_t)(L.nmulti > 0 ? L.nmulti : 1), s));
     LzState st0;
     std::memset(&st0, 0, sizeof(st0));
     st0.elo_b = canon_elo(1, n);
@@ -2080,7 +2086,8 @@ static double lanczos(lap_hierarchy *h, Level &L, int l, cudaStream_t s) {
         return mr > 0.0 ? ilogb(mr) : -1000;
     }() + 3;
     const int elo_spmv = canon_elo(e_spmv, nnz);
-    const CStore C = cstore_of(L, cpart.p);
+    CStore C = cstore_of(L, cpart.p);
+    C.ccnt = ccnt.p;
     const CSweep W{};
     const bool xs = L.smem_x && n <= SMEM_X_MAX;
     if (xs) {
@@ -2108,8 +2115,41 @@ static double lanczos(lap_hierarchy *h, Level &L, int l, cudaStream_t s) {
     k_tridiag_max<<<1, 1, 0, s>>>(al.p, be.p, kk.p, lam.p); ++g_kl;
     LAP_CHECK_LAUNCH();
     h->cur.edges += (int64_t)steps * L.nnz;
-    return d2h_scalar(lam.p, s);
+    LAP_CUDA(cudaMemcpyAsync(host_out, lam.p, sizeof(double), cudaMemcpyDeviceToHost, s));
 }
+// the side stream of the Lanczos runs (joined, and its resources released, at
+// the end of the setup or when an error unwinds it)
+struct LanczosStream {
+    cudaStream_t ls = nullptr;
+    cudaEvent_t ev = nullptr;
+    double *lam = nullptr;  // pinned, one per level
+    std::vector<int> levels;
+    void start(int l, cudaStream_t s) {  // after the level's storage is enqueued on s
+        if (!ls) {
+            LAP_CUDA(cudaStreamCreateWithFlags(&ls, cudaStreamNonBlocking));
+            LAP_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            LAP_CUDA(cudaMallocHost(&lam, sizeof(double) * 64));
+        }
+        LAP_CUDA(cudaEventRecord(ev, s));
+        LAP_CUDA(cudaStreamWaitEvent(ls, ev, 0));
+        levels.push_back(l);
+    }
+    void join(lap_hierarchy *h, cudaStream_t s) {  // s continues after every Lanczos run
+        if (!ls) return;
+        LAP_CUDA(cudaStreamSynchronize(ls));
+        for (int l : levels) h->lev[l].lambda = lam[l];
+        LAP_CUDA(cudaEventRecord(ev, ls));
+        LAP_CUDA(cudaStreamWaitEvent(s, ev, 0));
+    }
+    ~LanczosStream() {
+        if (ls) {
+            cudaStreamSynchronize(ls);
+            cudaStreamDestroy(ls);
+            cudaEventDestroy(ev);
+            cudaFreeHost(lam);
+        }
+    }
+};
 
 // =========================================================================
 // O-S10 coarsest pseudo-inverse (O-R26): ground the last vertex,
@@ -2759,6 +2799,10 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
     // logical CSR is released (the solve runs on the storage copy; the
     // coarsest level keeps it for L^+).
     int elim_run = 0;  // consecutive elimination levels built just above (O-R21)
+    LanczosStream lzs;
+    const char *lza = getenv("LAP_LANCZOS_ASYNC");  // 0: in line on the setup stream
+    const bool lz_async = !(lza && lza[0] == '0');
+    double lz_host_v = 0.0, *lz_host = &lz_host_v;
     for (int l = 0;; l++) {
         Level &L = h->lev[l];
         L.maxdeg = max_degree(L.n, L.row_ptr, s);
@@ -2786,7 +2830,14 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
         L.kind = KIND_AGG;
         build_storage(h, l, s);
         tr.mark("storage", l);
-        L.lambda = lanczos(h, L, l, s);
+        if (lz_async) {
+            lzs.start(l, s);
+            lanczos(h, L, l, lzs.ls, lzs.lam + l);
+        } else {
+            lanczos(h, L, l, s, lz_host);
+            LAP_CUDA(cudaStreamSynchronize(s));
+            L.lambda = *lz_host;
+        }
         tr.mark("lanczos", l);
         int64_t m = L.n;
         {
@@ -2817,6 +2868,8 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
     }
     coarse_pinv(h->lev.back(), s);
     tr.mark("coarsest pinv", (int)h->lev.size() - 1);
+    lzs.join(h, s);
+    tr.mark("lanczos join", 0);
 }
 
 // ---- test hook (lap_random_stream): the method's counter-based streams, by the
