@@ -271,17 +271,23 @@ __global__ void __launch_bounds__(256) k_perm_fill_long(int64_t n, int64_t minle
                                                         const int32_t *__restrict__ spos, const int64_t *__restrict__ rp,
                                                         const int32_t *__restrict__ col, const double *__restrict__ w,
                                                         const int64_t *__restrict__ srp, int32_t *__restrict__ kt,
-                                                        double *__restrict__ vt) {
+                                                        double *__restrict__ vt, int64_t maxlen = INT64_MAX,
+                                                        int32_t *__restrict__ kbig = nullptr,
+                                                        double *__restrict__ vbig = nullptr) {
+    // rows of (minlen, maxlen] -> kt / vt (to be sorted); rows longer than maxlen
+    // (left unsorted) straight to kbig / vbig
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t p = warp; p < n; p += nwarps) {
         const int64_t o = srp[p], len = srp[p + 1] - o;
         if (len <= minlen) continue;
+        int32_t *kd = len > maxlen ? kbig : kt;
+        double *vd = len > maxlen ? vbig : vt;
         const int64_t a0 = rp[sid[p]];
         for (int64_t q = lane; q < len; q += 32) {
-            kt[o + q] = spos[col[a0 + q]];
-            vt[o + q] = w ? w[a0 + q] : 1.0;
+            kd[o + q] = spos[col[a0 + q]];
+            vd[o + q] = w ? w[a0 + q] : 1.0;
         }
     }
 }
@@ -439,7 +445,7 @@ __global__ void k_rowcopy_list(int64_t m, const int32_t *__restrict__ list, cons
 // longer than sort_max are copied unsorted
 static void sort_rows_min(int64_t n, const int64_t *rp, int64_t nnz, int cbits, int64_t minlen, const int32_t *kin,
                           const double *vin, int32_t *kout, double *vout, cudaStream_t s,
-                          int64_t sort_max = INT64_MAX) {
+                          int64_t sort_max = INT64_MAX, bool copy_big = true) {
     if (n <= 0 || nnz <= 0) return;
     DBuf<int32_t> sml(n, s), med(n, s), lng(n, s), cpy(sort_max < INT64_MAX ? n : 1, s);
     DBuf<int> cnt(4, s);
@@ -451,7 +457,7 @@ static void sort_rows_min(int64_t n, const int64_t *rp, int64_t nnz, int cbits, 
     int hc[4];
     LAP_CUDA(cudaMemcpyAsync(hc, cnt.p, sizeof(hc), cudaMemcpyDeviceToHost, s));
     LAP_CUDA(cudaStreamSynchronize(s));
-    if (hc[3] > 0) {
+    if (hc[3] > 0 && copy_big) {
         k_rowcopy_list<<<grid_for((int64_t)hc[3] * 32, 256, 148 * 8), 256, 0, s>>>(hc[3], cpy.p, rp, kin, vin, kout,
                                                                                   vout);
         g_kl++;
@@ -580,10 +586,11 @@ void permute_sorted_rows(int64_t n, int64_t nnz, const int32_t *sid, const int32
     if (maxlen > 32) {  // longer rows: copied into a scratch at their positions, then sorted by length class
         DBuf<int32_t> c2(nnz, s);
         DBuf<double> w2(nnz, s);
-        k_perm_fill_long<<<grid_for(n * 32, 256, 148 * 8), 256, 0, s>>>(n, 32, sid, spos, rp, col, w, srp, c2.p, w2.p);
+        k_perm_fill_long<<<grid_for(n * 32, 256, 148 * 8), 256, 0, s>>>(n, 32, sid, spos, rp, col, w, srp, c2.p, w2.p,
+                                                                        sort_max, scol, sw);
         g_kl++;
         trace_mark("    permute: long rows filled");
-        sort_rows_min(n, srp, nnz, bitlen_u64((uint64_t)n), 32, c2.p, w2.p, scol, sw, s, sort_max);
+        sort_rows_min(n, srp, nnz, bitlen_u64((uint64_t)n), 32, c2.p, w2.p, scol, sw, s, sort_max, false);
     }
     LAP_CHECK_LAUNCH();
 }
