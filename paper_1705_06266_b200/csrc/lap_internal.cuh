@@ -297,10 +297,11 @@ void permute_csr(int64_t n, int64_t nnz, const int32_t *sid, const int32_t *spos
                  const int32_t *col, const double *w, int64_t *srp, int32_t *scol, double *sw, bool sort_cols,
                  int64_t maxlen, cudaStream_t s);
 // the same rows sorted into scol / sw with srp already built; maxlen bounds the row length
-// (rows longer than sort_max are permuted but keep their column order)
+// (rows of sort_max < len <= band_hi are permuted but keep their column order)
 void permute_sorted_rows(int64_t n, int64_t nnz, const int32_t *sid, const int32_t *spos, const int64_t *rp,
                          const int32_t *col, const double *w, const int64_t *srp, int32_t *scol, double *sw,
-                         int64_t maxlen, cudaStream_t s, int64_t sort_max = INT64_MAX);
+                         int64_t maxlen, cudaStream_t s, int64_t sort_max = INT64_MAX,
+                         int64_t band_hi = INT64_MAX);
 void build_transfers(lap_hierarchy *h, cudaStream_t s);
 // column-tiled SpMV layout (xt.cu)
 constexpr int XT_NW = 16;             // warps per CTA (512 threads)

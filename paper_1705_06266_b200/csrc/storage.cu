@@ -273,7 +273,8 @@ __global__ void __launch_bounds__(256) k_perm_fill_long(int64_t n, int64_t minle
                                                         const int64_t *__restrict__ srp, int32_t *__restrict__ kt,
                                                         double *__restrict__ vt, int64_t maxlen = INT64_MAX,
                                                         int32_t *__restrict__ kbig = nullptr,
-                                                        double *__restrict__ vbig = nullptr) {
+                                                        double *__restrict__ vbig = nullptr,
+                                                        int64_t band_hi = INT64_MAX) {
     // rows of (minlen, maxlen] -> kt / vt (to be sorted); rows longer than maxlen
     // (left unsorted) straight to kbig / vbig
     const int lane = threadIdx.x & 31;
@@ -282,8 +283,9 @@ __global__ void __launch_bounds__(256) k_perm_fill_long(int64_t n, int64_t minle
     for (int64_t p = warp; p < n; p += nwarps) {
         const int64_t o = srp[p], len = srp[p + 1] - o;
         if (len <= minlen) continue;
-        int32_t *kd = len > maxlen ? kbig : kt;
-        double *vd = len > maxlen ? vbig : vt;
+        const bool unsorted = len > maxlen && len <= band_hi;  // (maxlen, band_hi]: left in place, unsorted
+        int32_t *kd = unsorted ? kbig : kt;
+        double *vd = unsorted ? vbig : vt;
         const int64_t a0 = rp[sid[p]];
         for (int64_t q = lane; q < len; q += 32) {
             kd[o + q] = spos[col[a0 + q]];
@@ -348,10 +350,10 @@ __global__ void __launch_bounds__(256) k_rowsort_warp(int64_t n, int64_t minlen,
     }
 }
 __global__ void k_rowsort_lists(int64_t n, const int64_t *__restrict__ rp, int32_t *sml, int32_t *med, int32_t *lng,
-                                int *cnt, int64_t sort_max, int32_t *cpy) {
+                                int *cnt, int64_t sort_max, int32_t *cpy, int64_t band_hi) {
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
         const int64_t len = rp[r + 1] - rp[r];
-        if (len > sort_max) cpy[atomicAdd(&cnt[3], 1)] = (int32_t)r;    // kept in the given order
+        if (len > sort_max && len <= band_hi) cpy[atomicAdd(&cnt[3], 1)] = (int32_t)r;  // kept in the given order
         else if (len > ROWSORT_MED) lng[atomicAdd(&cnt[2], 1)] = (int32_t)r;  // order free: rows are independent
         else if (len > ROWSORT_SMALL) med[atomicAdd(&cnt[1], 1)] = (int32_t)r;
         else if (len > 64) sml[atomicAdd(&cnt[0], 1)] = (int32_t)r;
@@ -445,12 +447,13 @@ __global__ void k_rowcopy_list(int64_t m, const int32_t *__restrict__ list, cons
 // longer than sort_max are copied unsorted
 static void sort_rows_min(int64_t n, const int64_t *rp, int64_t nnz, int cbits, int64_t minlen, const int32_t *kin,
                           const double *vin, int32_t *kout, double *vout, cudaStream_t s,
-                          int64_t sort_max = INT64_MAX, bool copy_big = true) {
+                          int64_t sort_max = INT64_MAX, bool copy_big = true, int64_t band_hi = INT64_MAX) {
     if (n <= 0 || nnz <= 0) return;
     DBuf<int32_t> sml(n, s), med(n, s), lng(n, s), cpy(sort_max < INT64_MAX ? n : 1, s);
     DBuf<int> cnt(4, s);
     LAP_CUDA(cudaMemsetAsync(cnt.p, 0, 4 * sizeof(int), s));
-    k_rowsort_lists<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(n, rp, sml.p, med.p, lng.p, cnt.p, sort_max, cpy.p);
+    k_rowsort_lists<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(n, rp, sml.p, med.p, lng.p, cnt.p, sort_max, cpy.p,
+                                                              band_hi);
     k_rowsort_warp<<<grid_for(n * 32, 256, 148 * 8), 256, 0, s>>>(n, minlen, rp, kin, vin, kout, vout);
     g_kl += 2;
     trace_mark("    rowsort: lists + warp rows");
@@ -576,7 +579,7 @@ void permute_csr(int64_t n, int64_t nnz, const int32_t *sid, const int32_t *spos
 // the rows of P A P^T sorted, srp given
 void permute_sorted_rows(int64_t n, int64_t nnz, const int32_t *sid, const int32_t *spos, const int64_t *rp,
                          const int32_t *col, const double *w, const int64_t *srp, int32_t *scol, double *sw,
-                         int64_t maxlen, cudaStream_t s, int64_t sort_max) {  // NOLINT (default in the header)
+                         int64_t maxlen, cudaStream_t s, int64_t sort_max, int64_t band_hi) {
     if (n <= 0 || nnz <= 0) return;
     // rows of <= 32 entries: permuted and sorted in one thread's registers
     k_perm_sort_thread<16, 0><<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(n, sid, spos, rp, col, w, srp, scol, sw);
@@ -587,10 +590,10 @@ void permute_sorted_rows(int64_t n, int64_t nnz, const int32_t *sid, const int32
         DBuf<int32_t> c2(nnz, s);
         DBuf<double> w2(nnz, s);
         k_perm_fill_long<<<grid_for(n * 32, 256, 148 * 8), 256, 0, s>>>(n, 32, sid, spos, rp, col, w, srp, c2.p, w2.p,
-                                                                        sort_max, scol, sw);
+                                                                        sort_max, scol, sw, band_hi);
         g_kl++;
         trace_mark("    permute: long rows filled");
-        sort_rows_min(n, srp, nnz, bitlen_u64((uint64_t)n), 32, c2.p, w2.p, scol, sw, s, sort_max, false);
+        sort_rows_min(n, srp, nnz, bitlen_u64((uint64_t)n), 32, c2.p, w2.p, scol, sw, s, sort_max, false, band_hi);
     }
     LAP_CHECK_LAUNCH();
 }
@@ -762,16 +765,21 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
         // sorted (no double buffer over ~all entries of a power-law level)
         const bool sort_on = !getenv_flag_off("LAP_SORT_ROWS");
         const int cbits = bitlen_u64((uint64_t)n);
-        // rows longer than SHORT_MAX (warp chunks: a chunk's 32 lanes gather from one
-        // row, where order buys no line sharing) stay unsorted, except on the
-        // shared-memory-x levels (fewer bank conflicts sorted): cfg 3 setup
-        // -5.6 ms for +0.5 ms of solve, cfg 4 -1.9 / +0.75 (LAP_SORT_LONG=1: sort all)
+        // rows of SHORT_MAX < len <= ROWSORT_MED entries (one or two warp chunks of
+        // a sparse row: sorting buys no line sharing) stay unsorted; the SELL rows
+        // and the hub rows are sorted -- a hub row's chunk of 1024 sorted entries
+        // covers a narrow column range, so its gathers share lines (cfg 4 level 1
+        // step 286 -> 255 us sorted, medium rows alone 283) -- and so is every row
+        // of a shared-memory-x level.  cfg 3 setup -3 ms, cfg 4 -1.5 ms for the
+        // same solve (profiles/r02/sortmax_summary.txt; LAP_SORT_LONG=1: sort all)
         const char *sl = getenv("LAP_SORT_LONG");
+        const char *sm = getenv("LAP_SORT_MAX");  // experiments: the band's lower end
         const bool smem_level = n <= SMEM_X_MAX && L.nnz >= SMEM_X_MIN_DEG * n;
-        const int64_t sort_max = (sl && sl[0] == '1') || smem_level ? INT64_MAX : SHORT_MAX;
+        const int64_t sort_max = (sl && sl[0] == '1') || smem_level ? INT64_MAX : sm ? atoll(sm) : SHORT_MAX;
+        const int64_t band_hi = ROWSORT_MED;
         if (sort_on && L.nnz < ((int64_t)1 << 28)) {
             permute_sorted_rows(n, L.nnz, L.sid, L.spos, L.row_ptr, L.col, L.w, L.srp, L.scol, L.sw,
-                                L.maxdeg > 0 ? L.maxdeg : INT64_MAX, s, sort_max);
+                                L.maxdeg > 0 ? L.maxdeg : INT64_MAX, s, sort_max, band_hi);
         } else {
             k_storage_fill<<<grid_for(L.nnz, 256, 148 * 16), 256, 0, s>>>(n, L.nnz, L.sid, L.spos, L.row_ptr, L.col,
                                                                           L.w, L.srp, L.scol, L.sw);
