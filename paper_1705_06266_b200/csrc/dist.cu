@@ -1151,6 +1151,7 @@ SetupCommScope::SetupCommScope(lap_comm *c) { g_setup_comm = c; }
 SetupCommScope::~SetupCommScope() { g_setup_comm = nullptr; }
 
 int setup_nranks() { return g_setup_comm ? g_setup_comm->P : 1; }
+bool setup_has_comm() { return g_setup_comm != nullptr; }
 std::vector<int> setup_local_ranks() {
     std::vector<int> r;
     if (!g_setup_comm) {
@@ -1176,7 +1177,7 @@ void setup_gather(std::vector<Level> &pieces, const std::vector<int> &mine, cons
     const int64_t nout = bounds[P];
     std::vector<int64_t> cnt(P, 0);
     lap_comm *c = g_setup_comm;
-    const bool nccl = c && !c->virt && P > 1;
+    const bool nccl = c && !c->virt;
     if (nccl) {  // entry counts of every rank's range
         int64_t *dc = (int64_t *)dalloc(8 * (size_t)(P + 1), s);
         LAP_CUDA(cudaMemcpyAsync(dc + P, &pieces[0].nnz, 8, cudaMemcpyHostToDevice, s));

@@ -239,6 +239,7 @@ namespace lap {
 // coarse-operator term builds are then split over its ranks (setup.cu
 // build_split) and gathered here.
 int setup_nranks();                   // 1 without a setup communicator
+bool setup_has_comm();
 std::vector<int> setup_local_ranks(); // ranks this process builds: {rank} (NCCL) or 0..P-1 (virtual grid)
 // pieces[q] = rows [bounds[r], bounds[r+1]) of the operator for r = mine[q]
 // (local row_ptr from 0); out <- the whole operator's row_ptr / col / w / nnz

@@ -938,6 +938,13 @@ static int64_t dsetup_min_terms() {
     const char *e = getenv("LAP_DSETUP_MIN");  // tests: 0 forces the split on tiny graphs
     return e ? atoll(e) : ((int64_t)1 << 22);
 }
+// split this term build? P > 1 and enough terms; with LAP_DSETUP_MIN=0 also a
+// single NCCL rank (its gather path -- count allgather, broadcast, row_ptr
+// shift -- then runs on one GPU: tests)
+static bool dsetup_split(int64_t Ttot) {
+    const int64_t mn = dsetup_min_terms();
+    return (setup_nranks() > 1 || (mn == 0 && setup_has_comm())) && Ttot >= mn;
+}
 // bounds[r] = the first output row o with cum(o) * P >= r * total, cum(o) =
 // terms of the output rows before o (cum[o] = vcp[ostart[o]]); bounds[0] = 0,
 // bounds[P] = nout -- the same rule as lap_setup_split (host)
@@ -1004,7 +1011,7 @@ static void csr_from_source(const TermSrc &S0, int64_t nv, int64_t nout, int cb,
     }
     tmark("  terms: budget");
     const int P = setup_nranks();
-    if (P > 1 && Ttot >= dsetup_min_terms()) {
+    if (dsetup_split(Ttot)) {
         const std::vector<int64_t> bounds = split_bounds(nout, P, vcp.p, S.ostart, s);
         build_split(nout, bounds, out, s, [&](int64_t lo, int64_t hi, Level &piece) {
             csr_source_range(S, vcp.p, lo, hi, cb, e_max, K, combine, budget, piece, s);
@@ -2568,7 +2575,7 @@ static void galerkin_fast(lap_hierarchy *h, Level &L, Level &N, const int32_t *m
         csr_combine_sorted(mr, cb, T, key, sv, e_max, L.nnz, out, s, false);
     };
     const int P = setup_nranks();
-    if (P > 1 && Ttot >= dsetup_min_terms()) {
+    if (dsetup_split(Ttot)) {
         build_split(m, split_bounds(m, P, pv.p, mem_ptr, s), N, s, range);
         return;
     }

@@ -114,6 +114,28 @@ def test_nccl_transport_single_rank(P):
     comm.close()
 
 
+def test_nccl_distributed_setup_single_rank(P, monkeypatch):
+    """The distributed setup's NCCL gather (entry counts all-gathered, one
+    ncclBroadcast per root, row_ptr pieces shifted) on a real 1 x 1 NCCL
+    communicator with every term build forced through it (LAP_DSETUP_MIN=0):
+    the hierarchy equals the single-GPU one bit for bit and the sharded solve
+    (own-piece SpMV on the side stream) converges like it."""
+    g = lapgen.barabasi_albert(4000, 7)
+    h1 = P.Hierarchy(g)
+    monkeypatch.setenv("LAP_DSETUP_MIN", "0")
+    uid = P.Comm.unique_id()
+    comm = P.Comm(1, 1, nccl_id=uid, rank=0)
+    hd = P.Hierarchy(g, comm=comm, replicate_nnz=1)
+    for l in range(h1.nlev - 1):
+        assert _level_bits(hd, l) == _level_bits(h1, l), l
+    b = lapgen.rhs(g.n, seed=3)
+    x1, it1, _, _ = h1.solve(b)
+    xd, itd, rrd, rc = hd.solve(b)
+    assert rc == 0 and rrd <= 1e-8 and abs(itd - it1) <= 1
+    hd.close()
+    comm.close()
+
+
 def test_sharded_pcg_graph_replays_eager_bitwise(P):
     """The sharded PCG replays its per-iteration preconditioner step (V-cycle
     with the collectives, projection, dots) as one captured CUDA graph; the
