@@ -382,6 +382,8 @@ __global__ void k_blk_cheb_first(int64_t n, const double *__restrict__ b, const 
         x[t] = v;
     }
 }
+// a thread per (aggregate, column); aggregates of more than RESTRICT_SHORT
+// members (hubs) are left to k_blk_restrict_big
 template <int K>
 __global__ void k_blk_restrict(int64_t m, const int64_t *__restrict__ mp, const int32_t *__restrict__ mem,
                                const double *__restrict__ r, double *__restrict__ rc) {
@@ -389,9 +391,48 @@ __global__ void k_blk_restrict(int64_t m, const int64_t *__restrict__ mp, const 
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m * K; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t a = t / K;
         const int c = (int)(t - a * K);
+        if (mp[a + 1] - mp[a] > RESTRICT_SHORT) continue;
         double acc = 0.0;
         for (int64_t q = mp[a]; q < mp[a + 1]; q++) acc += r[(int64_t)mem[q] * K + c];
         rc[t] = acc;
+    }
+}
+// hub aggregates: a block per aggregate (the first chunk of each in the level's
+// restriction chunk list), threads strided over its members, column sums by a
+// fixed-order block reduction
+template <int K>
+__global__ void __launch_bounds__(256) k_blk_restrict_big(int64_t nchunks, const int32_t *__restrict__ crow,
+                                                          const int32_t *__restrict__ cidx,
+                                                          const int64_t *__restrict__ mp,
+                                                          const int32_t *__restrict__ mem,
+                                                          const double *__restrict__ r, double *__restrict__ rc) {
+    pdl_begin();
+    __shared__ double sh[8][K];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+        if (cidx[ch] != 0) continue;  // uniform over the block
+        const int64_t a = crow[ch];
+        double acc[K];
+#pragma unroll
+        for (int c = 0; c < K; c++) acc[c] = 0.0;
+        for (int64_t q = mp[a] + threadIdx.x; q < mp[a + 1]; q += blockDim.x) {
+            const double *rr = r + (int64_t)mem[q] * K;
+#pragma unroll
+            for (int c = 0; c < K; c++) acc[c] += rr[c];
+        }
+#pragma unroll
+        for (int c = 0; c < K; c++) {
+            double v = acc[c];
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) sh[wid][c] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < K) {
+            double v = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); w++) v += sh[w][threadIdx.x];
+            rc[a * K + threadIdx.x] = v;
+        }
+        __syncthreads();
     }
 }
 template <int K>
@@ -740,6 +781,12 @@ static void blk_vcycle(lap_hierarchy *h, BlockWork &W, int l, const double *b, d
     blk_spmv<K>(h, L, W.lcpart[l], W.lmdot[l], W.mdone, BE_RESID, a, s, g);
     launch_pdl(k_blk_restrict<K>, beg(L.m * K), 256, s, L.m, (const int64_t *)L.mem_ptr, (const int32_t *)L.members,
                (const double *)W.lr[l], cb);
+    if (L.rs_nchunks > 0) {
+        launch_pdl(k_blk_restrict_big<K>, grid_for(L.rs_nchunks, 1, 148 * 4), 256, s, L.rs_nchunks,
+                   (const int32_t *)L.rs_crow, (const int32_t *)L.rs_cidx, (const int64_t *)L.mem_ptr,
+                   (const int32_t *)L.members, (const double *)W.lr[l], cb);
+        h->cur.launches++;
+    }
     blk_vcycle<K>(h, W, l + 1, cb, cx, s);
     launch_pdl(k_blk_prolong<K>, beg(n * K), 256, s, n, (const int32_t *)L.agg_s, (const double *)cx, cur);
     h->cur.launches += 2;

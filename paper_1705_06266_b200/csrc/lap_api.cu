@@ -192,7 +192,7 @@ static void free_level(Level &L, cudaStream_t s) {
                   L.agg_s, L.mem_ptr, L.members, L.cid_s, L.flist, L.ct_ptr_s, L.ct_f_s, L.ct_coef_s, L.fmap_s,
                   L.ct_crow, L.ct_cidx, L.ct_cslot, L.ct_ccnt, L.ct_cpart,
                   L.pinv_s, L.dense, L.dense_part, L.dense_cnt, L.b, L.x, L.x2, L.t, L.r, L.dv, L.kp, L.kq, L.kz,
-                  L.kr, L.ksc, L.mdot, L.mdone};
+                  L.kr, L.ksc, L.mdot, L.mdone, L.rs_crow, L.rs_cidx, L.rs_cslot, L.rs_ccnt, L.rs_cpart};
     for (void *p : ps) dfree(p, s);
 }
 

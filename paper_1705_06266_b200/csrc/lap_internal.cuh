@@ -96,6 +96,7 @@ constexpr int64_t SHORT_MAX = 64;
 constexpr int64_t HUB_CHUNK = 16384;  // class 2/3 boundary (storage grouping only)
 constexpr int64_t LCHUNK = 1024;      // long-row chunk (entries per warp work item)
 constexpr int64_t SETUP_LONG = 4096;   // setup row kernels: longer rows go to LCHUNK warp chunks
+constexpr int64_t RESTRICT_SHORT = 64;  // restriction: aggregates with more members are chunked
 constexpr int64_t ELIM_SHORT = 32;    // elimination restriction: longer coarse lists are chunked
 constexpr int64_t DTAIL_MAX_N = 3072;  // the V-cycle below the first level this small is one dense operator (tail.cu)
 constexpr int64_t NB4_MIN_NNZ = 4000000;  // SELL batch width 4 for levels this big with avg degree <= 8
@@ -175,6 +176,9 @@ struct Level {
     int64_t *ct_ptr_s = nullptr;    // elim: coarse storage -> F neighbours (storage), coef
     int32_t *ct_f_s = nullptr;
     double *ct_coef_s = nullptr;
+    int64_t rs_nchunks = 0;         // agg: LCHUNK chunks of the aggregates with more than RESTRICT_SHORT members
+    int32_t *rs_crow = nullptr, *rs_cidx = nullptr, *rs_cslot = nullptr, *rs_ccnt = nullptr;
+    double *rs_cpart = nullptr;
     int64_t ct_nchunks = 0;         // elim: LCHUNK chunks of the coarse lists longer than ELIM_SHORT
     int32_t *ct_crow = nullptr, *ct_cidx = nullptr, *ct_cslot = nullptr, *ct_ccnt = nullptr;
     double *ct_cpart = nullptr;

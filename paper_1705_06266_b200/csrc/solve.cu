@@ -805,21 +805,75 @@ __device__ __forceinline__ void put_b(int64_t k, double s, double *__restrict__ 
 // r_c[a] = sum over members of a (ascending) of r_i; 8 lanes per aggregate
 // G lanes per aggregate (G = 1 for the ~3-4 member aggregates of grids -- 8
 // lanes left most idle --, up to 8 for large ones; restrict_group below)
+// Aggregates of more than RESTRICT_SHORT members (a hub with its thousands of
+// neighbours: one lane group would walk them serially -- 218 us of cfg 4's
+// level-0 restriction) are cut into LCHUNK-member warp chunks, 8 loads in
+// flight per lane, partials combined in chunk order by the last arrival (the
+// k_spmv scheme): one launch over [groups of small aggregates | chunks].
 template <int G>
 __global__ void __launch_bounds__(256) k_restrict(int64_t m, const int64_t *__restrict__ mp,
                                                   const int32_t *__restrict__ mem, const double *__restrict__ r,
-                                                  double *__restrict__ rc, Pre0 p0) {
+                                                  double *__restrict__ rc, Pre0 p0, LongRows R) {
     pdl_begin();
     const int lane = threadIdx.x & 31, sub = lane & (G - 1), grp = lane / G;
-    int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t base = warp * (32 / G); base < m; base += nwarps * (32 / G)) {
-        int64_t a = base + grp;
-        double acc = 0.0;
-        if (a < m)
-            for (int64_t k = mp[a] + sub; k < mp[a + 1]; k += G) acc += r[mem[k]];
-        for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (sub == 0 && a < m) put_b(a, acc, rc, p0);
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nsw = (m + 32 / G - 1) / (32 / G);  // warps over the small aggregates
+    for (int64_t t = warp; t < nsw + R.nchunks; t += nwarps) {
+        if (t < nsw) {
+            const int64_t a = t * (32 / G) + grp;
+            double acc = 0.0;
+            bool own = false;
+            if (a < m) {
+                const int64_t kb = mp[a], ke = mp[a + 1];
+                own = ke - kb <= RESTRICT_SHORT;
+                if (own)
+                    for (int64_t k = kb + sub; k < ke; k += G) acc += r[mem[k]];
+            }
+            for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (sub == 0 && own) put_b(a, acc, rc, p0);
+        } else {
+            const int64_t c = t - nsw;
+            const int64_t a = R.crow[c], j = R.cidx[c], kb = mp[a], ke = mp[a + 1];
+            const int64_t b = kb + j * LCHUNK, e = min(ke, b + LCHUNK);
+            double a0 = 0.0, a1 = 0.0;
+            int64_t k = b + lane;
+            for (; k + 224 < e; k += 256) {
+                int32_t q[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) q[u] = mem[k + 32 * u];
+#pragma unroll
+                for (int u = 0; u < 8; u += 2) {
+                    a0 += r[q[u]];
+                    a1 += r[q[u + 1]];
+                }
+            }
+            for (; k < e; k += 32) a0 += r[mem[k]];
+            double acc = a0 + a1;
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            const int slot = R.cslot[c];
+            if (slot < 0) {
+                if (lane == 0) put_b(a, acc, rc, p0);
+                continue;
+            }
+            const int nch = (int)((ke - kb + LCHUNK - 1) / LCHUNK);
+            int last = 0;
+            if (lane == 0) {
+                R.cpart[c] = acc;
+                __threadfence();
+                last = atomicAdd(&R.ccnt[slot], 1) == nch - 1;
+            }
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (!last) continue;
+            __threadfence();
+            double s2 = 0.0;
+            for (int q = lane; q < nch; q += 32) s2 += __ldcg(&R.cpart[c - j + q]);
+            for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+            if (lane == 0) {
+                R.ccnt[slot] = 0;
+                put_b(a, s2, rc, p0);
+            }
+        }
     }
 }
 __global__ void k_prolong(int64_t n, const int32_t *__restrict__ agg, const double *__restrict__ xc,
@@ -1041,11 +1095,12 @@ static bool cycle_rec(lap_hierarchy *h, int l, const double *b, double *xout, cu
         }();
         const int G = Gforce ? Gforce
                              : (L.nchunks > 0 || L.m < 65536) ? 8 : avg <= 4 ? 1 : avg <= 8 ? 2 : avg <= 16 ? 4 : 8;
-        const unsigned rg = grid_for(L.m * G, 256, 148 * 8);
-        if (G == 1) launch_pdl(k_restrict<1>, rg, 256, s, L.m, L.mem_ptr, L.members, L.r, C.b, p0);
-        else if (G == 2) launch_pdl(k_restrict<2>, rg, 256, s, L.m, L.mem_ptr, L.members, L.r, C.b, p0);
-        else if (G == 4) launch_pdl(k_restrict<4>, rg, 256, s, L.m, L.mem_ptr, L.members, L.r, C.b, p0);
-        else launch_pdl(k_restrict<8>, rg, 256, s, L.m, L.mem_ptr, L.members, L.r, C.b, p0);
+        const LongRows RR{L.rs_nchunks, L.rs_crow, L.rs_cidx, L.rs_cslot, L.rs_cpart, L.rs_ccnt};
+        const unsigned rg = grid_for(L.m * G + L.rs_nchunks * 32, 256, 148 * 8);
+        if (G == 1) launch_pdl(k_restrict<1>, rg, 256, s, L.m, L.mem_ptr, L.members, L.r, C.b, p0, RR);
+        else if (G == 2) launch_pdl(k_restrict<2>, rg, 256, s, L.m, L.mem_ptr, L.members, L.r, C.b, p0, RR);
+        else if (G == 4) launch_pdl(k_restrict<4>, rg, 256, s, L.m, L.mem_ptr, L.members, L.r, C.b, p0, RR);
+        else launch_pdl(k_restrict<8>, rg, 256, s, L.m, L.mem_ptr, L.members, L.r, C.b, p0, RR);
     }
     h->cur.launches++;
     h->cur.bytes += 16 * n + 8 * L.m;

@@ -935,6 +935,10 @@ void build_transfers(lap_hierarchy *h, cudaStream_t s) {
             LAP_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, L.agg_s, keys2.p, ids.p, L.members, n, 0, end_bit, s));
             k_lower_bound32<<<grid_for(L.m + 1, 256, 148 * 8), 256, 0, s>>>(L.m, n, keys2.p, L.mem_ptr);
             g_kl += 4;
+            // hub aggregates (a hub and its thousands of neighbours): warp chunks of
+            // LCHUNK members for the restriction (solve.cu k_restrict)
+            L.rs_nchunks = build_chunks(L.mem_ptr, 0, L.m, RESTRICT_SHORT, &L.rs_crow, &L.rs_cidx, &L.rs_cslot,
+                                        &L.rs_cpart, &L.rs_ccnt, s);
         } else if (L.kind == KIND_ELIM) {
             Level &C = h->lev[l + 1];
             int64_t nc = C.n;
