@@ -348,14 +348,23 @@ __global__ void k_d_cheb_first(int64_t nreal, const double *b, const double *d, 
     }
 }
 // coarse-space partial sums of a restriction: out[c] = sum_k coef_k v[slot_k] over the list of c
+// 8 lanes per coarse index (lane-strided, fixed shuffle tree): a hub aggregate's
+// members in this piece do not serialise one thread
 __global__ void __launch_bounds__(256) k_d_gather_sum(int64_t mc, const int64_t *__restrict__ ptr,
                                                       const int32_t *__restrict__ slot, const double *__restrict__ coef,
                                                       const double *__restrict__ v, double *__restrict__ out) {
     pdl_begin();
-    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < mc; c += (int64_t)gridDim.x * blockDim.x) {
+    constexpr int G = 8;
+    const int lane = threadIdx.x & 31, sub = lane & (G - 1);
+    const int64_t grp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+    const int64_t ngrp = ((int64_t)gridDim.x * blockDim.x) / G;
+    for (int64_t base = grp - (grp % (32 / G)); base < mc; base += ngrp) {  // a warp's groups move together
+        const int64_t c = base + (grp % (32 / G));
         double s = 0.0;
-        for (int64_t k = ptr[c]; k < ptr[c + 1]; k++) s += (coef ? coef[k] : 1.0) * v[slot[k]];
-        out[c] = s;
+        if (c < mc)
+            for (int64_t k = ptr[c] + sub; k < ptr[c + 1]; k += G) s += (coef ? coef[k] : 1.0) * v[slot[k]];
+        for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (sub == 0 && c < mc) out[c] = s;
     }
 }
 __global__ void k_d_prolong(int64_t nreal, const int32_t *__restrict__ cmap, const double *__restrict__ xc,
@@ -879,7 +888,7 @@ static void dist_vcycle(lap_hierarchy *h, Dist &D, int l, const std::vector<doub
     if (L.kind == KIND_ELIM) {
         for (size_t k = 0; k < DL.sh.size(); k++) {
             Shard &a = DL.sh[k];
-            launch_pdl(k_d_gather_sum, dg(DL.mc), 256, s, DL.mc, (const int64_t *)a.er_ptr, (const int32_t *)a.er_slot,
+            launch_pdl(k_d_gather_sum, dg(DL.mc * 8), 256, s, DL.mc, (const int64_t *)a.er_ptr, (const int32_t *)a.er_slot,
                        (const double *)a.er_coef, (const double *)b[k], a.cfull);
         }
         dist_restrict_finish(h, D, l, s);
@@ -913,7 +922,7 @@ static void dist_vcycle(lap_hierarchy *h, Dist &D, int l, const std::vector<doub
     dist_spmv(h, D, l, DE_RESID, cur, rv, b, {}, 0, 0, false, s);
     for (size_t k = 0; k < DL.sh.size(); k++) {
         Shard &a = DL.sh[k];
-        launch_pdl(k_d_gather_sum, dg(DL.mc), 256, s, DL.mc, (const int64_t *)a.mem_ptr, (const int32_t *)a.members,
+        launch_pdl(k_d_gather_sum, dg(DL.mc * 8), 256, s, DL.mc, (const int64_t *)a.mem_ptr, (const int32_t *)a.members,
                    (const double *)nullptr, (const double *)rv[k], a.cfull);
     }
     dist_restrict_finish(h, D, l, s);

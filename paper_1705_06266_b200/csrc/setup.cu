@@ -88,11 +88,19 @@ static double max_abs(const double *v, int64_t n, cudaStream_t s) {
 
 // pass 1 of the validation touches row_ptr only: monotone and within
 // [0, nnz], so that pass 2 never reads col/w out of bounds
-__global__ void k_validate_rowptr(int64_t n, int64_t nnz, const int64_t *__restrict__ row_ptr, int *flag) {
+__global__ void k_validate_rowptr(int64_t n, int64_t nnz, const int64_t *__restrict__ row_ptr, int *flag,
+                                  unsigned long long *maxdeg) {
+    unsigned long long md = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t a = row_ptr[i], e = row_ptr[i + 1];
         if (a < 0 || e < a || e > nnz) atomicOr(flag, 1);
+        else md = (unsigned long long)(e - a) > md ? (unsigned long long)(e - a) : md;
     }
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, md, o);
+        md = t > md ? t : md;
+    }
+    if ((threadIdx.x & 31) == 0 && md) atomicMax(maxdeg, md);
 }
 // Symmetry fingerprint (hsum != NULL): two independent 64-bit multiset hashes,
 // sum over entries of h(i, j, bits(w)) - h(j, i, bits(w)) mod 2^64.  A symmetric
@@ -106,39 +114,61 @@ __device__ __forceinline__ uint64_t sym_h1(uint64_t a, uint64_t b, uint64_t mw) 
 __device__ __forceinline__ uint64_t sym_h2(uint64_t a, uint64_t b, uint64_t mw) {
     return mix64(mix64(a ^ 0x5851F42D4C957F2DULL) + (b ^ mw));
 }
+// one stored entry (i, j, w) at position k of row i starting at a
+__device__ __forceinline__ void validate_entry(int64_t n, int64_t i, int64_t a, int64_t k,
+                                               const int32_t *__restrict__ col, const double *__restrict__ w,
+                                               int *flag, bool hash, uint64_t &s1, uint64_t &s2) {
+    const int32_t j = col[k];
+    bool bad = (j < 0) || (j >= n) || (j == i) || (k > a && col[k - 1] >= j);
+    const double wk = w ? w[k] : 1.0;
+    bad |= !(wk > 0.0) || !isfinite(wk);
+    if (bad) atomicOr(flag, 1);
+    if (hash) {
+        const uint64_t wb = (uint64_t)__double_as_longlong(wk);
+        const uint64_t m1 = mix64(wb), m2 = mix64(wb ^ 0x2545F4914F6CDD1DULL);
+        s1 += sym_h1((uint64_t)i, (uint64_t)j, m1) - sym_h1((uint64_t)j, (uint64_t)i, m1);
+        s2 += sym_h2((uint64_t)i, (uint64_t)j, m2) - sym_h2((uint64_t)j, (uint64_t)i, m2);
+    }
+}
+__device__ __forceinline__ void hash_flush(uint64_t s1, uint64_t s2, unsigned long long *hsum) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    if ((threadIdx.x & 31) == 0 && (s1 | s2)) {
+        atomicAdd(&hsum[0], (unsigned long long)s1);
+        atomicAdd(&hsum[1], (unsigned long long)s2);
+    }
+}
+// rows longer than skip_long are left to k_validate_chunks (a hub row of 10^4
+// - 10^6 entries would serialise one lane group: cfg 3's validation tail)
 template <int G>
 __global__ void k_validate(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                           const double *__restrict__ w, int *flag, unsigned long long *hsum) {
+                           const double *__restrict__ w, int *flag, unsigned long long *hsum, int64_t skip_long) {
     uint64_t s1 = 0, s2 = 0;
     GROUP_LOOP_BEGIN(G, n)
     if (live) {
         int64_t a = row_ptr[i], e = row_ptr[i + 1];
-        for (int64_t k = a + gl; k < e; k += G) {
-            int32_t j = col[k];
-            bool bad = (j < 0) || (j >= n) || (j == i) || (k > a && col[k - 1] >= j);
-            double wk = w ? w[k] : 1.0;
-            bad |= !(wk > 0.0) || !isfinite(wk);
-            if (bad) atomicOr(flag, 1);
-            if (hsum) {
-                const uint64_t wb = (uint64_t)__double_as_longlong(wk);
-                const uint64_t m1 = mix64(wb), m2 = mix64(wb ^ 0x2545F4914F6CDD1DULL);
-                s1 += sym_h1((uint64_t)i, (uint64_t)j, m1) - sym_h1((uint64_t)j, (uint64_t)i, m1);
-                s2 += sym_h2((uint64_t)i, (uint64_t)j, m2) - sym_h2((uint64_t)j, (uint64_t)i, m2);
-            }
-        }
+        if (e - a <= skip_long)
+            for (int64_t k = a + gl; k < e; k += G) validate_entry(n, i, a, k, col, w, flag, hsum != nullptr, s1, s2);
     }
     GROUP_LOOP_END
-    if (hsum) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-            s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-        }
-        if ((threadIdx.x & 31) == 0 && (s1 | s2)) {
-            atomicAdd(&hsum[0], (unsigned long long)s1);
-            atomicAdd(&hsum[1], (unsigned long long)s2);
-        }
+    if (hsum) hash_flush(s1, s2, hsum);
+}
+// LCHUNK-entry warp chunks of the long rows (order-free: flags and mod-2^64 sums)
+__global__ void k_validate_chunks(int64_t nch, const int32_t *__restrict__ crow, const int32_t *__restrict__ cidx,
+                                  int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                                  const double *__restrict__ w, int *flag, unsigned long long *hsum) {
+    uint64_t s1 = 0, s2 = 0;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = warp; c < nch; c += nwarps) {
+        const int64_t i = crow[c], a = row_ptr[i], b = a + (int64_t)cidx[c] * LCHUNK, e = min(row_ptr[i + 1], b + LCHUNK);
+        for (int64_t k = b + lane; k < e; k += 32) validate_entry(n, i, a, k, col, w, flag, hsum != nullptr, s1, s2);
     }
+    if (hsum) hash_flush(s1, s2, hsum);
 }
 
 template <int G>
@@ -300,38 +330,63 @@ __device__ __forceinline__ int32_t cc_find(int32_t *p, int32_t v) {
     }
     return cur;
 }
+__device__ __forceinline__ void cc_link(int32_t *p, int32_t i, int32_t j) {
+    if (j < i) return;                         // each undirected edge once
+    int32_t a = cc_find(p, i), b = cc_find(p, j);
+    while (a != b) {
+        if (a < b) {
+            int32_t t = a; a = b; b = t;
+        }
+        int32_t ret = atomicCAS(&p[a], a, b);  // hook the larger root under the smaller
+        if (ret == a) break;
+        a = ret;
+    }
+}
 template <int G>
 __global__ void k_cc_union(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                           int32_t *p) {
+                           int32_t *p, int64_t skip_long) {
     GROUP_LOOP_BEGIN(G, n)
-    if (live) {
-        for (int64_t k = row_ptr[i] + gl; k < row_ptr[i + 1]; k += G) {
-            int32_t j = col[k];
-            if (j < i) continue;                       // each undirected edge once
-            int32_t a = cc_find(p, (int32_t)i), b = cc_find(p, j);
-            while (a != b) {
-                if (a < b) {
-                    int32_t t = a; a = b; b = t;
-                }
-                int32_t ret = atomicCAS(&p[a], a, b);  // hook the larger root under the smaller
-                if (ret == a) break;
-                a = ret;
-            }
-        }
-    }
+    if (live && row_ptr[i + 1] - row_ptr[i] <= skip_long)
+        for (int64_t k = row_ptr[i] + gl; k < row_ptr[i + 1]; k += G) cc_link(p, (int32_t)i, col[k]);
     GROUP_LOOP_END
+}
+__global__ void k_cc_union_chunks(int64_t nch, const int32_t *__restrict__ crow, const int32_t *__restrict__ cidx,
+                                  const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col, int32_t *p) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = warp; c < nch; c += nwarps) {
+        const int64_t i = crow[c], b = row_ptr[i] + (int64_t)cidx[c] * LCHUNK, e = min(row_ptr[i + 1], b + LCHUNK);
+        for (int64_t k = b + lane; k < e; k += 32) cc_link(p, (int32_t)i, col[k]);
+    }
 }
 __global__ void k_cc_count_roots(int64_t n, int32_t *p, unsigned long long *cnt) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         if (cc_find(p, (int32_t)i) == i) atomicAdd(cnt, 1ULL);
 }
 
-static bool is_connected(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col, cudaStream_t s) {
+// the long rows' chunk list of the input graph (validation, connectivity)
+struct InputChunks {
+    int64_t nch = 0;
+    int32_t *crow = nullptr, *cidx = nullptr, *cslot = nullptr, *ccnt = nullptr;
+    double *cpart = nullptr;
+    cudaStream_t s = nullptr;
+    ~InputChunks() {
+        for (void *q : {(void *)crow, (void *)cidx, (void *)cslot, (void *)ccnt, (void *)cpart}) dfree(q, s);
+    }
+};
+static bool is_connected(int64_t n, int64_t nnz, const int64_t *row_ptr, const int32_t *col, cudaStream_t s,
+                         const InputChunks &IC) {
     if (n <= 1) return true;
     DBuf<int32_t> p(n, s);
     unsigned g = grid_for(n, 256, 148 * 16);
     k_cc_init<<<g, 256, 0, s>>>(n, p.p); ++g_kl;
-    LAUNCH_G(group_size(n, nnz), k_cc_union, n, s, n, row_ptr, col, p.p);
+    LAUNCH_G(group_size(n, nnz), k_cc_union, n, s, n, row_ptr, col, p.p, IC.nch > 0 ? SETUP_LONG : INT64_MAX);
+    if (IC.nch > 0) {
+        k_cc_union_chunks<<<grid_for(IC.nch * 32, 256, 148 * 16), 256, 0, s>>>(IC.nch, IC.crow, IC.cidx, row_ptr, col,
+                                                                                p.p);
+        ++g_kl;
+    }
     DBuf<unsigned long long> c(1, s);
     LAP_CUDA(cudaMemsetAsync(c.p, 0, 8, s));
     k_cc_count_roots<<<g, 256, 0, s>>>(n, p.p, c.p); ++g_kl;
@@ -2714,17 +2769,35 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
     if (nnz >= (int64_t)1 << 40 || n >= ((int64_t)1 << 31) - 1) throw Error{LAP_EINVAL, "graph too large"};
     // --- O-S0 validate
     {
+        InputChunks IC;
+        IC.s = s;
         DBuf<int> flag(1, s);
         DBuf<unsigned long long> hsum(2, s);
         LAP_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
         if (n > 0) {
             int64_t first = d2h_scalar(rp, s);
             if (first != 0) throw Error{LAP_EGRAPH, "row_ptr[0] != 0"};
-            k_validate_rowptr<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(n, nnz, rp, flag.p); ++g_kl;
+            DBuf<unsigned long long> mdeg(1, s);
+            LAP_CUDA(cudaMemsetAsync(mdeg.p, 0, sizeof(unsigned long long), s));
+            k_validate_rowptr<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(n, nnz, rp, flag.p, mdeg.p); ++g_kl;
             LAP_CHECK_LAUNCH();
             if (d2h_scalar(flag.p, s)) throw Error{LAP_EGRAPH, "row_ptr is not monotone within [0, nnz]"};
+            const int64_t maxdeg0 = (int64_t)d2h_scalar(mdeg.p, s);
             LAP_CUDA(cudaMemsetAsync(hsum.p, 0, 2 * sizeof(unsigned long long), s));
-            LAUNCH_G(group_size(n, nnz), k_validate, n, s, n, rp, col, w, flag.p, symcheck_mode() == 0 ? hsum.p : nullptr);
+            // rows longer than SETUP_LONG in warp chunks (row_ptr is valid now) when some
+            // row is long enough to be the kernels' tail (cfg 3: validation 2.66 -> 0.97 ms,
+            // connectivity 2.09 -> 0.86; on cfg 4, max degree ~2^14, the chunk list costs
+            // more than it saves)
+            if (maxdeg0 > 8 * SETUP_LONG)
+                IC.nch = build_chunks(rp, 0, n, SETUP_LONG, &IC.crow, &IC.cidx, &IC.cslot, &IC.cpart, &IC.ccnt, s);
+            unsigned long long *hs = symcheck_mode() == 0 ? hsum.p : nullptr;
+            LAUNCH_G(group_size(n, nnz), k_validate, n, s, n, rp, col, w, flag.p, hs,
+                     IC.nch > 0 ? SETUP_LONG : INT64_MAX);
+            if (IC.nch > 0) {
+                k_validate_chunks<<<grid_for(IC.nch * 32, 256, 148 * 16), 256, 0, s>>>(IC.nch, IC.crow, IC.cidx, n, rp,
+                                                                                        col, w, flag.p, hs);
+                ++g_kl;
+            }
             LAP_CHECK_LAUNCH();
         }
         if (d2h_scalar(flag.p, s)) throw Error{LAP_EGRAPH, "graph is not a valid symmetric positive-weight adjacency"};
@@ -2740,7 +2813,7 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
             throw Error{LAP_EGRAPH, "graph is not symmetric (w_ij != w_ji)"};
         }
         tr.mark("symmetry", 0);
-        if (!is_connected(n, nnz, rp, col, s)) throw Error{LAP_EDISCONNECTED, "graph is disconnected"};
+        if (!is_connected(n, nnz, rp, col, s, IC)) throw Error{LAP_EDISCONNECTED, "graph is disconnected"};
         tr.mark("connectivity", 0);
     }
     // --- O-S1 level 0
