@@ -62,28 +62,21 @@ __host__ __device__ __forceinline__ int canon_elo(int e_max, int64_t K) {
 // integer that splits exactly into hi * 2^64 + lo.  Same value as the integer
 // reference canon_q_bits below (and the oracle's), ~10 instructions instead of
 // ~200 (the int128 shift chain made the test-vector sweeps compute-bound).
-__device__ __forceinline__ i128 canon_q(double t, int elo) {
-    const double sc = scalbn(t, -elo);
-    if (fabs(sc) < 9007199254740992.0) return (i128)__double2ll_rn(sc);  // |s| < 2^53: RNE to an integer
-    const double hi = floor(sc * 0x1p-64);
-    const double lo = sc - hi * 0x1p64;                                   // exact, in [0, 2^64)
-    return (i128)__double2ll_rz(hi) * ((i128)1 << 64) + (i128)__double2ull_rz(lo);
-}
-
 // 2^-elo when it is a normal double (every realistic instance), else 0: the
-// hot kernels then scale by ONE multiplication -- the correctly rounded
-// product t * 2^-elo is exactly scalbn(t, -elo) -- instead of scalbn's
-// special-case sequence
+// kernels then scale by ONE multiplication -- the correctly rounded product
+// t * 2^-elo is exactly scalbn(t, -elo) -- instead of scalbn's special-case
+// sequence (the scale is loop-invariant, so it is hoisted out of the loops)
 __host__ __device__ __forceinline__ double canon_scale(int elo) {
     return (-elo >= -1022 && -elo <= 1023) ? __longlong_as_double_hd((long long)(1023 - elo) << 52) : 0.0;
 }
 __device__ __forceinline__ i128 canon_q_s(double t, double s2, int elo) {
     const double sc = s2 != 0.0 ? t * s2 : scalbn(t, -elo);
-    if (fabs(sc) < 9007199254740992.0) return (i128)__double2ll_rn(sc);
+    if (fabs(sc) < 9007199254740992.0) return (i128)__double2ll_rn(sc);  // |s| < 2^53: RNE to an integer
     const double hi = floor(sc * 0x1p-64);
-    const double lo = sc - hi * 0x1p64;
+    const double lo = sc - hi * 0x1p64;                                   // exact, in [0, 2^64)
     return (i128)__double2ll_rz(hi) * ((i128)1 << 64) + (i128)__double2ull_rz(lo);
 }
+__device__ __forceinline__ i128 canon_q(double t, int elo) { return canon_q_s(t, canon_scale(elo), elo); }
 
 // integer reference of canon_q (bit decomposition); kept for the self-check
 __device__ __forceinline__ i128 canon_q_bits(double t, int elo) {
