@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "lap_internal.cuh"
+#include "canon.cuh"
 
 namespace lap {
 void vcycle_apply(lap_hierarchy *h, const double *r, double *z, cudaStream_t s);
@@ -652,8 +653,23 @@ lap_status lap_level_export(const lap_hierarchy *h, int32_t l, int64_t *row_ptr,
         return LAP_EINVAL;
     }
     if (row_ptr) LAP_CUDA(cudaMemcpy(row_ptr, L.row_ptr, 8 * (L.n + 1), cudaMemcpyDeviceToHost));
-    if (col && L.nnz) LAP_CUDA(cudaMemcpy(col, L.col, 4 * L.nnz, cudaMemcpyDeviceToHost));
-    if (w && L.nnz) LAP_CUDA(cudaMemcpy(w, L.w, 8 * L.nnz, cudaMemcpyDeviceToHost));
+    if ((col || w) && L.nnz) {
+        const int32_t *cs = L.col;
+        const double *ws = L.w;
+        lap::DBuf<int32_t> c2;
+        lap::DBuf<double> w2;
+        if (!L.cols_sorted) {  // the logical CSR as the method defines it: each row in ascending column order
+            c2.alloc(L.nnz, nullptr);
+            w2.alloc(L.nnz, nullptr);
+            lap::sort_rows(L.n, L.row_ptr, L.nnz, lap::bitlen_u64((uint64_t)(L.n > 0 ? L.n : 1)), L.col, L.w, c2.p,
+                           w2.p, nullptr);
+            LAP_CUDA(cudaStreamSynchronize(nullptr));
+            cs = c2.p;
+            ws = w2.p;
+        }
+        if (col) LAP_CUDA(cudaMemcpy(col, cs, 4 * L.nnz, cudaMemcpyDeviceToHost));
+        if (w) LAP_CUDA(cudaMemcpy(w, ws, 8 * L.nnz, cudaMemcpyDeviceToHost));
+    }
     if (d) LAP_CUDA(cudaMemcpy(d, L.d, 8 * L.n, cudaMemcpyDeviceToHost));
     if (map) {
         if (L.kind == lap::KIND_AGG) LAP_CUDA(cudaMemcpy(map, L.agg, 4 * L.n, cudaMemcpyDeviceToHost));
@@ -711,7 +727,15 @@ lap_status lap_level_strength(const lap_hierarchy *h, int32_t l, double *S) {
         return LAP_EINVAL;
     }
     LAP_API_BEGIN
-    if (L.nnz) LAP_CUDA(cudaMemcpy(S, L.S, 8 * L.nnz, cudaMemcpyDeviceToHost));
+    if (L.nnz && !L.cols_sorted && L.col) {  // S in the logical entry order of sorted rows (as exported)
+        lap::DBuf<int32_t> c2(L.nnz, nullptr);
+        lap::DBuf<double> s2(L.nnz, nullptr);
+        lap::sort_rows(L.n, L.row_ptr, L.nnz, lap::bitlen_u64((uint64_t)(L.n > 0 ? L.n : 1)), L.col, L.S, c2.p, s2.p,
+                       nullptr);
+        LAP_CUDA(cudaMemcpy(S, s2.p, 8 * L.nnz, cudaMemcpyDeviceToHost));
+    } else if (L.nnz) {
+        LAP_CUDA(cudaMemcpy(S, L.S, 8 * L.nnz, cudaMemcpyDeviceToHost));
+    }
     return LAP_OK;
     LAP_API_END
 }

@@ -114,6 +114,7 @@ struct Level {
     double maxw = 0.0;
     int64_t maxdeg = 0;             // longest row (setup kernels' hub handling; known before storage)
     bool logical_released = false;  // logical row_ptr/col/w freed after storage (params.keep_logical)
+    bool cols_sorted = true;        // logical rows in ascending column order (level 0: not by default)
     int32_t *rowof = nullptr;       // setup only: row of every stored entry (not owned)
     // aggregation (logical)
     double lambda = 0.0;

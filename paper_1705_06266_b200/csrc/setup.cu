@@ -2841,9 +2841,17 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
         DBuf<int32_t> inv(n, s);  // old row of new id r
         k_inverse_perm<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, h->perm, inv.p); ++g_kl;
         const char *fr = getenv("LAP_RELABEL_TERMS");  // tests: the term-build relabel of big graphs
-        if (nnz < ((int64_t)1 << 28) && !(fr && fr[0] == '1')) {
-            // P L P^T directly: row r = old row inv[r], columns perm[c], each row
-            // sorted in registers / shared memory (no duplicates, nothing to sum)
+        const char *fs = getenv("LAP_L0_SORTED");      // 1: level 0 with sorted columns (as round 1)
+        if (!(fr && fr[0] == '1')) {
+            // P L P^T directly: row r = old row inv[r], columns perm[c], no duplicates,
+            // nothing to sum.  The rows keep the caller's column order mapped through
+            // Pi: no setup kernel needs them sorted (every setup reduction is an
+            // order-free CanonSum, an argmax under a total order or a per-entry map;
+            // the ordered Galerkin sorts its coarse rows itself), so the ~4 ms of
+            // per-row sorts are spent only when the level is exported
+            // (lap_level_export sorts a copy).  LAP_L0_SORTED=1 sorts them here.
+            const bool sort0 = fs && fs[0] == '1';
+            L0.cols_sorted = sort0;
             DBuf<int32_t> p32(n, s);
             k_perm_to_i32<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, h->perm, p32.p); ++g_kl;
             L0.n = n;
@@ -2851,7 +2859,7 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
             L0.row_ptr = (int64_t *)dalloc(sizeof(int64_t) * (size_t)(n + 1), s);
             L0.col = (int32_t *)dalloc(sizeof(int32_t) * (size_t)(nnz + 1), s);
             L0.w = (double *)dalloc(sizeof(double) * (size_t)(nnz + 1), s);
-            permute_csr(n, nnz, inv.p, p32.p, rp, col, w, L0.row_ptr, L0.col, L0.w, true, INT64_MAX, s);
+            permute_csr(n, nnz, inv.p, p32.p, rp, col, w, L0.row_ptr, L0.col, L0.w, sort0, INT64_MAX, s);
             tmark("  relabel: permute + row sorts");
             L0.d = (double *)dalloc(sizeof(double) * (size_t)(n > 0 ? n : 1), s);
             row_sums(n, nnz, L0.row_ptr, L0.w, L0.d, &L0.maxw, s);

@@ -366,7 +366,7 @@ def test_memory_lean_paths_bit_exact(P):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     for env in [{"LAP_TERM_BATCH": "3000"}, {"LAP_SYMCHECK": "search"}, {"LAP_TERM_BATCH": "100000", "LAP_SYMCHECK": "search"},
                 {"LAP_GAL_FAST": "0", "LAP_SYMCHECK": "sort"}, {"LAP_GAL_FAST": "0", "LAP_TERM_BATCH": "3000"},
-                {"LAP_LANCZOS_ASYNC": "0", "LAP_SORT_LONG": "1"}]:
+                {"LAP_LANCZOS_ASYNC": "0", "LAP_SORT_LONG": "1", "LAP_L0_SORTED": "1"}]:
         e = dict(os.environ, **env)
         r = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, timeout=900, cwd=root)
         assert r.returncode == 0 and "ok" in r.stdout, (env, r.stderr[-3000:])
