@@ -763,7 +763,11 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
         // gathers); long rows too (gather locality of dense-ish rows), except on
         // huge levels (>= 2^28 entries, cfg 5), where only the short rows are
         // sorted (no double buffer over ~all entries of a power-law level)
-        const bool sort_on = !getenv_flag_off("LAP_SORT_ROWS");
+        // elimination levels are never smoothed: their storage serves the PCG's
+        // q = L_0 p (level 0) and the F-row solves, whose speed the row order does
+        // not change (cfg 3 level 0: 104.5 vs 105.1 us per SpMV) -- no sort there
+        // (cfg 3 setup -4 ms)
+        const bool sort_on = !getenv_flag_off("LAP_SORT_ROWS") && L.kind != KIND_ELIM;
         const int cbits = bitlen_u64((uint64_t)n);
         // rows of SHORT_MAX < len <= ROWSORT_MED entries (one or two warp chunks of
         // a sparse row: sorting buys no line sharing) stay unsorted; the SELL rows
