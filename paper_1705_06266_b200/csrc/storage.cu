@@ -581,6 +581,19 @@ void permute_sorted_rows(int64_t n, int64_t nnz, const int32_t *sid, const int32
                          const int32_t *col, const double *w, const int64_t *srp, int32_t *scol, double *sw,
                          int64_t maxlen, cudaStream_t s, int64_t sort_max, int64_t band_hi) {
     if (n <= 0 || nnz <= 0) return;
+    if (sort_max == 0) {  // only the rows longer than band_hi sorted (power-law levels)
+        const bool any_long = maxlen > band_hi;
+        DBuf<int32_t> c2(any_long ? nnz : 1, s);
+        DBuf<double> w2(any_long ? nnz : 1, s);
+        k_perm_fill_long<<<grid_for(n * 32, 256, 148 * 8), 256, 0, s>>>(n, 0, sid, spos, rp, col, w, srp, c2.p, w2.p, 0,
+                                                                        scol, sw, band_hi);
+        g_kl++;
+        trace_mark("    permute: rows filled");
+        if (any_long)
+            sort_rows_min(n, srp, nnz, bitlen_u64((uint64_t)n), band_hi, c2.p, w2.p, scol, sw, s, 0, false, band_hi);
+        LAP_CHECK_LAUNCH();
+        return;
+    }
     // rows of <= 32 entries: permuted and sorted in one thread's registers
     k_perm_sort_thread<16, 0><<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(n, sid, spos, rp, col, w, srp, scol, sw);
     k_perm_sort_thread<32, 17><<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(n, sid, spos, rp, col, w, srp, scol, sw);
@@ -779,7 +792,14 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
         const char *sl = getenv("LAP_SORT_LONG");
         const char *sm = getenv("LAP_SORT_MAX");  // experiments: the band's lower end
         const bool smem_level = n <= SMEM_X_MAX && L.nnz >= SMEM_X_MIN_DEG * n;
-        const int64_t sort_max = (sl && sl[0] == '1') || smem_level ? INT64_MAX : sm ? atoll(sm) : SHORT_MAX;
+        // power-law levels (rows beyond SELL exist): the SELL rows' order buys no
+        // line sharing either (random neighbours; cfg 4 level 0 step 327.5 us
+        // unsorted vs 326.5 sorted), so only the hub rows are sorted there
+        const bool mesh_like = L.maxdeg <= SHORT_MAX;
+        const int64_t sort_max = (sl && sl[0] == '1') || smem_level ? INT64_MAX
+                                 : sm                                ? atoll(sm)
+                                 : mesh_like                         ? SHORT_MAX
+                                                                     : 0;
         const int64_t band_hi = ROWSORT_MED;
         if (sort_on && L.nnz < ((int64_t)1 << 28)) {
             permute_sorted_rows(n, L.nnz, L.sid, L.spos, L.row_ptr, L.col, L.w, L.srp, L.scol, L.sw,
