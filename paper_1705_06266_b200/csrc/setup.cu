@@ -1862,6 +1862,9 @@ __device__ __forceinline__ void cs_gather(const double *__restrict__ x, int64_t 
     }
 }
 // NC x-values of column c (the gather half of cs_gather, issued ahead of the sums)
+#ifndef CS_SB4
+#define CS_SB4 4
+#endif
 template <int NC>
 struct CsX {
     double v[NC];
@@ -1932,11 +1935,12 @@ __global__ void __launch_bounds__(XS ? 1024 : 256, XS ? 1 : (NC == 1 ? 4 : 3)) k
             i128 acc[NC];
 #pragma unroll
             for (int k = 0; k < NC; k++) acc[k] = 0;
-            for (int q = 0; q < width; q += 8) {
-                int cc[8];
-                double wv[8];
+            constexpr int SB = (NC == 1 || XS) ? 8 : CS_SB4;  // SELL columns per batch (registers: NC = 4 holds 4 x-rows each)
+            for (int q = 0; q < width; q += SB) {
+                int cc[SB];
+                double wv[SB];
 #pragma unroll
-                for (int uu = 0; uu < 8; uu++) {
+                for (int uu = 0; uu < SB; uu++) {
                     cc[uu] = 0;
                     wv[uu] = 0.0;
                     if (q + uu < width) {
@@ -1945,7 +1949,7 @@ __global__ void __launch_bounds__(XS ? 1024 : 256, XS ? 1 : (NC == 1 ? 4 : 3)) k
                     }
                 }
 #pragma unroll
-                for (int uu = 0; uu < 8; uu++)
+                for (int uu = 0; uu < SB; uu++)
                     if (q + uu < width) cs_gather<NC>(x, cc[uu], wv[uu], elo, s2, acc);
             }
             double ya = 0.0;

@@ -568,8 +568,8 @@ void permute_csr(int64_t n, int64_t nnz, const int32_t *sid, const int32_t *spos
     }
     scan_excl(deg.p, srp, n + 1, s);
     if (nnz <= 0) return;
-    if (!sort_cols) {
-        k_storage_fill<<<grid_for(nnz, 256, 148 * 16), 256, 0, s>>>(n, nnz, sid, spos, rp, col, w, srp, scol, sw);
+    if (!sort_cols) {  // warp per row (a row's source entries are contiguous): 2.4 -> 1.2 ms on cfg 4 level 0
+        k_perm_fill_long<<<grid_for(n * 32, 256, 148 * 8), 256, 0, s>>>(n, 0, sid, spos, rp, col, w, srp, scol, sw);
         g_kl++;
         LAP_CHECK_LAUNCH();
         return;
