@@ -15,9 +15,6 @@ for k in 2 3; do timeout 600 python bench.py --config $k --no-cpu --steps 10 --w
 for k in 4 3 2; do timeout 600 python tools/prof_solve.py $k > $O/levels_p$k.txt 2>&1; done
 for k in 4 3 2; do LAP_SETUP_TRACE=2 timeout 600 python tools/setup_trace.py $k > $O/setup_trace$k.log 2>&1; done
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -c 12000 --csv --log-file /tmp/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu > $O/ncu_launch.log 2>&1; gzip -c /tmp/launches.csv > $O/launches_bench_cfg4.csv.gz
-for k in 4 3; do
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"k_spmv<3" -s 2 -c 1 -o /tmp/cheb$k python tools/prof_cheb.py $k 5 > $O/ncu_cheb$k.log 2>&1
-python tools/ncu_summary.py /tmp/cheb$k.ncu-rep > $O/ncu_full_cheb_cfg$k.txt 2>&1
-done
+CFGS="4 3" bash tools/call_ncu_cheb.sh
 timeout 1200 python bench.py --config 5 --no-cpu --steps 3 --warmup 3 > $O/bench_cfg5.json 2> $O/bench_cfg5.err; echo "rc=$?" >> $O/bench_cfg5.err
 du -sh $O
