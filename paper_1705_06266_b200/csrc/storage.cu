@@ -795,12 +795,16 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
         // power-law levels (rows beyond SELL exist): the SELL rows' order buys no
         // line sharing either (random neighbours; cfg 4 level 0 step 327.5 us
         // unsorted vs 326.5 sorted), so only the hub rows are sorted there
+        // shared-memory-x levels gather from shared memory: no line sharing to win
+        // either (cfg 4 level 2 step 80.0 vs 79.8 us, cfg 3 level 3 42.9 vs 42.7) --
+        // nothing sorted there (cfg 4: the 1.5 ms segmented sort of level 2)
         const bool mesh_like = L.maxdeg <= SHORT_MAX;
-        const int64_t sort_max = (sl && sl[0] == '1') || smem_level ? INT64_MAX
-                                 : sm                                ? atoll(sm)
-                                 : mesh_like                         ? SHORT_MAX
-                                                                     : 0;
-        const int64_t band_hi = ROWSORT_MED;
+        const int64_t sort_max = (sl && sl[0] == '1') ? INT64_MAX
+                                 : sm                 ? atoll(sm)
+                                 : smem_level         ? 0
+                                 : mesh_like          ? SHORT_MAX
+                                                      : 0;
+        const int64_t band_hi = smem_level && !(sl && sl[0] == '1') ? INT64_MAX : ROWSORT_MED;
         if (sort_on && L.nnz < ((int64_t)1 << 28)) {
             permute_sorted_rows(n, L.nnz, L.sid, L.spos, L.row_ptr, L.col, L.w, L.srp, L.scol, L.sw,
                                 L.maxdeg > 0 ? L.maxdeg : INT64_MAX, s, sort_max, band_hi);
