@@ -18,6 +18,19 @@
 
 namespace lap {
 
+// matrix streams (col / w, read once per SpMV): no L1 allocation, so L1 keeps
+// the gathered x lines (LAP_STREAM_L1NA build switch; experiments)
+#ifndef LAP_STREAM_L1NA
+#define LAP_STREAM_L1NA 1
+#endif
+template <class T>
+__device__ __forceinline__ T lds(const T *p) {
+#if LAP_STREAM_L1NA
+    return __ldcs(p);
+#else
+    return __ldg(p);
+#endif
+}
 struct Csr {
     const int64_t *__restrict__ rp;
     const int32_t *__restrict__ col;
@@ -135,11 +148,11 @@ __device__ __forceinline__ void sell_slice(int64_t sl, int lane, int64_t nrows, 
         for (int u = 0; u < NB; u++) {
             c[u] = 0;
             if (q + u < width) {
-                c[u] = __ldg(&ec[beg + (int64_t)(q + u) * 32 + lane]);
+                c[u] = lds(&ec[beg + (int64_t)(q + u) * 32 + lane]);
                 // UNIT: pattern only; a padding slot holds the row's own index (never a
                 // real entry: no self loops) and is skipped -- 1.0 * x_j = x_j, the same bits
                 if (UNIT) wv[u] = c[u] != (int)i ? 1.0 : 0.0;
-                else wv[u] = __ldg(&ew[beg + (int64_t)(q + u) * 32 + lane]);
+                else wv[u] = lds(&ew[beg + (int64_t)(q + u) * 32 + lane]);
             }
         }
 #pragma unroll
@@ -225,8 +238,8 @@ __device__ __forceinline__ bool chunk_reduce(int64_t c, int lane, const int64_t 
         double wv[8];
 #pragma unroll
         for (int u = 0; u < 8; u++) {
-            c[u] = __ldg(&col[k + 32 * u]);
-            wv[u] = UNIT ? 1.0 : __ldg(&w[k + 32 * u]);
+            c[u] = lds(&col[k + 32 * u]);
+            wv[u] = UNIT ? 1.0 : lds(&w[k + 32 * u]);
         }
         a0 += wv[0] * x[c[0]];
         a1 += wv[1] * x[c[1]];
@@ -238,15 +251,15 @@ __device__ __forceinline__ bool chunk_reduce(int64_t c, int lane, const int64_t 
         a3 += wv[7] * x[c[7]];
     }
     for (; k + 96 < e; k += 128) {
-        int c0 = __ldg(&col[k]), c1 = __ldg(&col[k + 32]), c2 = __ldg(&col[k + 64]), c3 = __ldg(&col[k + 96]);
-        double w0 = UNIT ? 1.0 : __ldg(&w[k]), w1 = UNIT ? 1.0 : __ldg(&w[k + 32]),
-               w2 = UNIT ? 1.0 : __ldg(&w[k + 64]), w3 = UNIT ? 1.0 : __ldg(&w[k + 96]);
+        int c0 = lds(&col[k]), c1 = lds(&col[k + 32]), c2 = lds(&col[k + 64]), c3 = lds(&col[k + 96]);
+        double w0 = UNIT ? 1.0 : lds(&w[k]), w1 = UNIT ? 1.0 : lds(&w[k + 32]),
+               w2 = UNIT ? 1.0 : lds(&w[k + 64]), w3 = UNIT ? 1.0 : lds(&w[k + 96]);
         a0 += w0 * x[c0];
         a1 += w1 * x[c1];
         a2 += w2 * x[c2];
         a3 += w3 * x[c3];
     }
-    for (; k < e; k += 32) a0 += (UNIT ? 1.0 : __ldg(&w[k])) * x[__ldg(&col[k])];
+    for (; k < e; k += 32) a0 += (UNIT ? 1.0 : lds(&w[k])) * x[lds(&col[k])];
     double acc = (a0 + a1) + (a2 + a3);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);

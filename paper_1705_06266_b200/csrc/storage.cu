@@ -58,12 +58,15 @@ __device__ __forceinline__ int deg_class(int64_t dg) {
 // sort key: [40:39] degree class, [38:31] 255 - degree (short rows, only if
 // degree-sorted), [30:0] locality key (< n < 2^31)
 __global__ void k_class_key(int64_t n, const int64_t *rp, const uint64_t *key, uint64_t *skey, int32_t *ids,
-                            unsigned long long *cnt, int by_degree) {
+                            unsigned long long *cnt, int by_degree, int hub_order) {
     GRID_STRIDE(i, n) {
         int64_t dg = rp[i + 1] - rp[i];
         int c = deg_class(dg);
         // 41 key bits: 6 radix passes instead of 8
-        uint64_t k = key[i] | (((uint64_t)c) << 39);
+        // hub_order: rows beyond SELL by descending degree within their class (the
+        // most referenced x entries contiguous)
+        const uint64_t loc = (hub_order && c > 0) ? (uint64_t)(0x7FFFFFFF - (dg < 0x7FFFFFFF ? dg : 0x7FFFFFFF)) : key[i];
+        uint64_t k = loc | (((uint64_t)c) << 39);
         if (by_degree && c == 0) k |= ((uint64_t)(255 - dg)) << 31;
         skey[i] = k;
         ids[i] = (int32_t)i;
@@ -682,8 +685,10 @@ void build_storage(lap_hierarchy *h, int l, cudaStream_t s) {
     DBuf<uint64_t> skey(n, s);
     L.sid = (int32_t *)dalloc(sizeof(int32_t) * n, s);
     L.spos = (int32_t *)dalloc(sizeof(int32_t) * n, s);
+    const char *ho = getenv("LAP_HUB_ORDER");  // experiments
+    const int hub_order = ho ? atoi(ho) : 0;
     auto order_rows = [&](int by_degree, unsigned long long *counts) {
-        k_class_key<<<g, 256, 0, s>>>(n, L.row_ptr, key.p, skey.p, ids.p, counts, by_degree);
+        k_class_key<<<g, 256, 0, s>>>(n, L.row_ptr, key.p, skey.p, ids.p, counts, by_degree, hub_order);
         size_t bytes = 0;
         LAP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, skey.p, key2.p, ids.p, L.sid, n, 0, 41, s));
         DBuf<char> tmp((int64_t)bytes, s);
