@@ -1426,7 +1426,7 @@ __global__ void k_affinity(int64_t n, const int64_t *__restrict__ row_ptr, const
         for (int64_t k0 = kb + gl; k0 < ke; k0 += 4 * G) {
             int64_t jj[4];
 #pragma unroll
-            for (int u = 0; u < 4; u++) jj[u] = k0 + u * G < ke ? col[k0 + u * G] : 0;
+            for (int u = 0; u < 4; u++) jj[u] = k0 + u * G < ke ? __ldcs(&col[k0 + u * G]) : 0;
             double2 u0[4], u1[4];
 #pragma unroll
             for (int u = 0; u < 4; u++) {
@@ -1503,8 +1503,8 @@ __global__ void k_vote_round(int64_t n, const int64_t *__restrict__ row_ptr, con
 #pragma unroll
             for (int u = 0; u < 4; u++) {
                 const int64_t k = k0 + u * G;
-                sv[u] = k < ke ? S[k] : 0.0;
-                jj[u] = k < ke ? col[k] : 0;
+                sv[u] = k < ke ? __ldcs(&S[k]) : 0.0;  // streams: evict-first (L1 keeps the gathered states)
+                jj[u] = k < ke ? __ldcs(&col[k]) : 0;
             }
 #pragma unroll
             for (int u = 0; u < 4; u++)   // filter 2^-t, w != 0 (O-R13)
@@ -1944,8 +1944,8 @@ __global__ void __launch_bounds__(XS ? 1024 : 256, XS ? 1 : (NC == 1 ? 4 : 3)) k
                     cc[uu] = 0;
                     wv[uu] = 0.0;
                     if (q + uu < width) {
-                        cc[uu] = __ldg(&C.ell_col[beg + (int64_t)(q + uu) * 32 + lane]);
-                        wv[uu] = __ldg(&C.ell_w[beg + (int64_t)(q + uu) * 32 + lane]);
+                        cc[uu] = __ldcs(&C.ell_col[beg + (int64_t)(q + uu) * 32 + lane]);
+                        wv[uu] = __ldcs(&C.ell_w[beg + (int64_t)(q + uu) * 32 + lane]);
                     }
                 }
 #pragma unroll
@@ -1971,8 +1971,8 @@ __global__ void __launch_bounds__(XS ? 1024 : 256, XS ? 1 : (NC == 1 ? 4 : 3)) k
 #pragma unroll
                 for (int u = 0; u < U; u++) {
                     const int64_t k = k0 + 32 * u;
-                    cc[u] = k < e ? __ldg(&C.scol[k]) : 0;
-                    wv[u] = k < e ? __ldg(&C.sw[k]) : 0.0;
+                    cc[u] = k < e ? __ldcs(&C.scol[k]) : 0;
+                    wv[u] = k < e ? __ldcs(&C.sw[k]) : 0.0;
                 }
                 CsX<NC> xv[U];
 #pragma unroll
