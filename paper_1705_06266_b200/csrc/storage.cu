@@ -290,7 +290,22 @@ __global__ void __launch_bounds__(256) k_perm_fill_long(int64_t n, int64_t minle
         int32_t *kd = unsorted ? kbig : kt;
         double *vd = unsorted ? vbig : vt;
         const int64_t a0 = rp[sid[p]];
-        for (int64_t q = lane; q < len; q += 32) {
+        int64_t q = lane;
+        for (; q + 96 < len; q += 128) {  // 4 column loads, then their 4 spos gathers, in flight
+            int32_t c[4];
+            double v[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                c[u] = __ldcs(&col[a0 + q + 32 * u]);
+                v[u] = w ? __ldcs(&w[a0 + q + 32 * u]) : 1.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                kd[o + q + 32 * u] = spos[c[u]];
+                vd[o + q + 32 * u] = v[u];
+            }
+        }
+        for (; q < len; q += 32) {
             kd[o + q] = spos[col[a0 + q]];
             vd[o + q] = w ? w[a0 + q] : 1.0;
         }

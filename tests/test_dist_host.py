@@ -85,12 +85,22 @@ def _worker(rank, world, port, pr, pc, q):
         xd = np.zeros(world * S)
         xd[d] = x
         own = torch.from_numpy(xd[rank * S:(rank + 1) * S].copy())
+        own_x = own.numpy().copy()
         # column allgather (column communicator rank order = grid row order)
         parts = [torch.zeros(S, dtype=torch.float64) for _ in range(pr)]
         dist.all_gather(parts, own, group=cg)
         xcol = torch.cat(parts).numpy()
         ypart = np.zeros(pc * S)
         np.add.at(ypart, lrow, wv * xcol[lcol])
+        # the library's split of A_ij (dist.cu build_part): columns of this rank's
+        # OWN piece (local ids into the piece, usable before the column allgather)
+        # and the rest of the column block; own + remote = the whole block product
+        own = ((dcol[sel] // S) // pc) == gi
+        y_own = np.zeros(pc * S)
+        np.add.at(y_own, lrow[own], wv[own] * own_x[(dcol[sel] % S)[own]])
+        y_rem = np.zeros(pc * S)
+        np.add.at(y_rem, lrow[~own], wv[~own] * xcol[lcol[~own]])
+        assert np.allclose(y_own + y_rem, ypart, rtol=1e-13, atol=1e-13)
         # row reduce-scatter (row communicator rank order = grid column order)
         out = torch.zeros(S, dtype=torch.float64)
         segs = [torch.from_numpy(ypart[j * S:(j + 1) * S].copy()) for j in range(pc)]
