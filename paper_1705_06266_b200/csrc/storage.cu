@@ -296,8 +296,8 @@ __global__ void __launch_bounds__(256) k_perm_fill_long(int64_t n, int64_t minle
             double v[4];
 #pragma unroll
             for (int u = 0; u < 4; u++) {
-                c[u] = __ldcs(&col[a0 + q + 32 * u]);
-                v[u] = w ? __ldcs(&w[a0 + q + 32 * u]) : 1.0;
+                c[u] = col[a0 + q + 32 * u];  // (cached: short rows of neighbouring warps share lines)
+                v[u] = w ? w[a0 + q + 32 * u] : 1.0;
             }
 #pragma unroll
             for (int u = 0; u < 4; u++) {
