@@ -759,9 +759,21 @@ __global__ void k_batch_end(int64_t o0, int64_t nout, int64_t budget, TermSrc S,
 }
 // emit the terms of the fine entries [t0, t1) (= the virtual rows [v0, v1)); a
 // block claims its output space with one atomic (block scan of per-entry counts)
+// rv[t - t0] = the virtual row of fine entry t, t in [vptr[v0], vptr[v1]) (G lanes per row)
+template <int G>
+__global__ void k_src_rowof(int64_t v0, int64_t v1, const int64_t *__restrict__ vptr, int64_t t0,
+                            int32_t *__restrict__ rv) {
+    GROUP_LOOP_BEGIN(G, v1 - v0)
+    if (live) {
+        const int64_t v = v0 + i;
+        for (int64_t t = vptr[v] + gl; t < vptr[v + 1]; t += G) rv[t - t0] = (int32_t)v;
+    }
+    GROUP_LOOP_END
+}
 __global__ void __launch_bounds__(256) k_src_emit(TermSrc S, int64_t v0, int64_t v1, int64_t t0, int64_t t1,
                                                   int64_t o0, int cb, unsigned long long *cursor,
-                                                  uint64_t *__restrict__ keys, double *__restrict__ vals) {
+                                                  uint64_t *__restrict__ keys, double *__restrict__ vals,
+                                                  const int32_t *__restrict__ rv) {
     typedef cub::BlockScan<int, 256> BS;
     __shared__ typename BS::TempStorage ts;
     __shared__ unsigned long long boff;
@@ -769,8 +781,9 @@ __global__ void __launch_bounds__(256) k_src_emit(TermSrc S, int64_t v0, int64_t
     for (int64_t b0 = t0 + (int64_t)blockIdx.x * 256; b0 < t1; b0 += (int64_t)gridDim.x * 256) {
         const int64_t t = b0 + threadIdx.x;
         const int64_t blast = min(t1, b0 + 256) - 1;
-        // virtual rows of the block's first and last entries (two searches per block)
-        if (threadIdx.x < 2) {
+        // virtual rows of the block's first and last entries (two searches per block),
+        // unless the row of every entry is given (rv: no dependent search chains)
+        if (!rv && threadIdx.x < 2) {
             const int64_t tt = threadIdx.x == 0 ? b0 : blast;
             int64_t lo = v0, hi = v1 - 1;
             while (lo < hi) {
@@ -785,13 +798,17 @@ __global__ void __launch_bounds__(256) k_src_emit(TermSrc S, int64_t v0, int64_t
         int cnt = 0;
         int64_t v = 0, i = 0, k = 0, j = 0;
         if (t < t1) {
-            int64_t lo = vlo_s, hi = vhi_s;
-            while (lo < hi) {
-                const int64_t mid = (lo + hi + 1) >> 1;
-                if (S.vptr[mid] <= t) lo = mid;
-                else hi = mid - 1;
+            if (rv) {
+                v = rv[t - t0];
+            } else {
+                int64_t lo = vlo_s, hi = vhi_s;
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi + 1) >> 1;
+                    if (S.vptr[mid] <= t) lo = mid;
+                    else hi = mid - 1;
+                }
+                v = lo;
             }
-            v = lo;
             i = S.vfine[v];
             k = S.rp[i] + (t - S.vptr[v]);
             j = S.col[k];
@@ -876,8 +893,10 @@ static void csr_source_range(const TermSrc &S, const int64_t *vcp, int64_t olo, 
         const int64_t t0 = at(S.vptr, vlo), t1 = at(S.vptr, vhi);
         tmark("  terms: alloc");
         if (t1 > t0) {
+            DBuf<int32_t> rv(t1 - t0, s);
+            LAUNCH_G(8, k_src_rowof, vhi - vlo, s, vlo, vhi, S.vptr, t0, rv.p);
             k_src_emit<<<grid_for(t1 - t0, 256, 148 * 16), 256, 0, s>>>(S, vlo, vhi, t0, t1, olo, cb, cur.p, keys.p,
-                                                                       vals.p);
+                                                                       vals.p, rv.p);
             ++g_kl;
             LAP_CHECK_LAUNCH();
         }
@@ -909,8 +928,10 @@ static void csr_source_range(const TermSrc &S, const int64_t *vcp, int64_t olo, 
         DBuf<double> vals(Tb, s), v2(Tb, s);
         LAP_CUDA(cudaMemsetAsync(cur.p, 0, 8, s));
         if (tr2[1] > tr2[0]) {
+            DBuf<int32_t> rv(tr2[1] - tr2[0], s);
+            LAUNCH_G(8, k_src_rowof, vr[1] - vr[0], s, vr[0], vr[1], S.vptr, tr2[0], rv.p);
             k_src_emit<<<grid_for(tr2[1] - tr2[0], 256, 148 * 16), 256, 0, s>>>(S, vr[0], vr[1], tr2[0], tr2[1], o0, cb,
-                                                                              cur.p, keys.p, vals.p);
+                                                                              cur.p, keys.p, vals.p, rv.p);
             ++g_kl;
             LAP_CHECK_LAUNCH();
         }
@@ -1918,7 +1939,7 @@ __global__ void __launch_bounds__(XS ? 1024 : 256, XS ? 1 : (NC == 1 ? 4 : 3)) k
     }
     const double *__restrict__ x = XS ? xs_dyn : x0;
     const double bprev = MODE == CS_LANCZOS ? st->bprev : 0.0;
-    const int elo = MODE == CS_LANCZOS ? elo_fixed : *W.elo_p;
+    const int elo = W.elo_p ? *W.elo_p : elo_fixed;
     const double s2 = canon_scale(elo);
     if (MODE == CS_LANCZOS && blockIdx.x == 0 && threadIdx.x == 0) {
         st->acc_b.lo = 0;  // read by pass A only; pass A of this step has finished
@@ -2112,6 +2133,7 @@ static int num_sms_dev() {
 __global__ void k_lzc_init_s(int64_t n, uint64_t base, const int32_t *__restrict__ sid, const double *__restrict__ sd,
                              double *__restrict__ y, double *__restrict__ rs, double *__restrict__ vp, LzState *st,
                              int elo) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->elo_b = elo;  // (st zeroed by a memset before)
     i128 acc = 0;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
         const double v = lz_start_value(base, sid[p]);
@@ -2123,6 +2145,12 @@ __global__ void k_lzc_init_s(int64_t n, uint64_t base, const int32_t *__restrict
     block_add_i128(&st->acc_b, acc);
 }
 
+// E_lo of the Lanczos SpMV instance on the device (no host round trip): the
+// exponent bound ilogb(max w) + ilogb(max rs) + 3 of the products w_ij rs_j v_j
+__global__ void k_lz_spmv_elo(const unsigned long long *mxrs, int ew, int64_t nnz, int *elo) {
+    const double mr = __longlong_as_double((long long)*mxrs);
+    *elo = canon_elo(ew + (mr > 0.0 ? ilogb(mr) : -1000) + 3, nnz);
+}
 // lambda-hat on the level's solve storage (built before this is called): the
 // Lanczos vectors live in the storage order; every sum is a CanonSum, so the
 // order changes no bit (the tridiagonal equals the oracle's).
@@ -2139,22 +2167,24 @@ static void lanczos(lap_hierarchy *h, Level &L, int l, cudaStream_t s, double *h
     DBuf<I128> cpart(L.nchunks > 0 ? L.nchunks : 1, s);
     DBuf<int32_t> ccnt(L.nmulti > 0 ? L.nmulti : 1, s);  // not the sweeps' counters: they may run meanwhile
     LAP_CUDA(cudaMemsetAsync(ccnt.p, 0, sizeof(int32_t) * (size_t)(L.nmulti > 0 ? L.nmulti : 1), s));
-    LzState st0;
-    std::memset(&st0, 0, sizeof(st0));
-    st0.elo_b = canon_elo(1, n);
-    LAP_CUDA(cudaMemcpyAsync(st.p, &st0, sizeof(st0), cudaMemcpyHostToDevice, s));
+    // no host synchronisation anywhere below: this runs on the side stream while
+    // the host keeps enqueueing the setup's main work
+    LAP_CUDA(cudaMemsetAsync(st.p, 0, sizeof(LzState), s));
     const uint64_t base = mix64(salt_of(h->p.seed, 4) ^ (uint64_t)(2 * l));
     const unsigned g = grid_for(n, 256, 148 * 8);
-    k_lzc_init_s<<<g, 256, 0, s>>>(n, base, L.sid, L.sd, y.p, rs.p, vp.p, st.p, st0.elo_b); ++g_kl;
+    k_lzc_init_s<<<g, 256, 0, s>>>(n, base, L.sid, L.sd, y.p, rs.p, vp.p, st.p, canon_elo(1, n)); ++g_kl;
     LAP_CHECK_LAUNCH();
-    const int e_spmv = (L.maxw > 0.0 ? ilogb(L.maxw) : -1000) + [&] {
-        const double mr = max_abs(rs.p, n, s);
-        return mr > 0.0 ? ilogb(mr) : -1000;
-    }() + 3;
-    const int elo_spmv = canon_elo(e_spmv, nnz);
+    DBuf<unsigned long long> mxrs(1, s);
+    DBuf<int> elo_d(1, s);
+    LAP_CUDA(cudaMemsetAsync(mxrs.p, 0, sizeof(unsigned long long), s));
+    k_max_abs<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(rs.p, n, mxrs.p); ++g_kl;
+    k_lz_spmv_elo<<<1, 1, 0, s>>>(mxrs.p, L.maxw > 0.0 ? ilogb(L.maxw) : -1000, nnz, elo_d.p); ++g_kl;
+    LAP_CHECK_LAUNCH();
+    const int elo_spmv = 0;  // (read from elo_d by the SpMV)
     CStore C = cstore_of(L, cpart.p);
     C.ccnt = ccnt.p;
-    const CSweep W{};
+    CSweep W{};
+    W.elo_p = elo_d.p;
     const bool xs = L.smem_x && n <= SMEM_X_MAX;
     if (xs) {
         static bool attr = false;
