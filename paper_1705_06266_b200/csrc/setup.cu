@@ -1926,7 +1926,7 @@ __device__ __forceinline__ double cs_epilogue(int64_t p, const i128 *acc, int el
 // (occupancy: 78 / 128 registers left 35 % / 25 % of the warps resident and the
 // gathers latency-bound, ncu profiles/r02; the bounds cap them at 64 / 80)
 template <int NC, int MODE, bool XS = false>
-__global__ void __launch_bounds__(XS ? 1024 : 256, XS ? 1 : (NC == 1 ? 4 : 3)) k_cspmv_store(CStore C, const double *__restrict__ x0,
+__global__ void __launch_bounds__(XS ? 1024 : 256, XS ? 1 : 4) k_cspmv_store(CStore C, const double *__restrict__ x0,
                                                                  const double *__restrict__ rs,
                                                                  const double *__restrict__ vp, int elo_fixed,
                                                                  LzState *st, double *__restrict__ y, CSweep W,
@@ -1985,7 +1985,7 @@ __global__ void __launch_bounds__(XS ? 1024 : 256, XS ? 1 : (NC == 1 ? 4 : 3)) k
             for (int k = 0; k < NC; k++) acc[k] = 0;
             // 8 (col, w) loads and then 8 gathers in flight per lane (long rows of
             // aggregated levels carry most entries; the sum is order-free)
-            constexpr int U = NC == 1 ? 8 : 4;
+            constexpr int U = NC == 1 ? 8 : 2;
             for (int64_t k0 = b + lane; k0 < e; k0 += 32 * U) {
                 int32_t cc[U];
                 double wv[U];
