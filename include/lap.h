@@ -191,8 +191,8 @@ lap_status lap_spmv(const lap_hierarchy *h, int32_t l, const double *x, double *
  * lap_solve would (its own projection, PCG + V-cycle, stopping rule; O-S8),
  * but the k solves advance together so every pass over a level's matrix
  * serves all columns (SpMM).  1 <= k <= 32 (k <= 8: a thread per row, K values
- * per gather; 9..32: K = 16 / 32 lanes per row, one coalesced gather per
- * neighbour).  X: n x k column-major, mean-zero
+ * per gather; 9..16: two such blocks of <= 8 columns one after the other;
+ * 17..32: 32 lanes per row, one coalesced gather per neighbour).  X: n x k column-major, mean-zero
  * columns.  iters[j], rel_residual[j]: per column (length k).  LAP_ENOCONV if
  * any column reached max_iters.  Single-GPU hierarchies only. */
 lap_status lap_solve_block(lap_hierarchy *h, int32_t k, const double *B, double *X, double tol,

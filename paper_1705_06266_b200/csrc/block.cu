@@ -1027,13 +1027,42 @@ static void solve_block_k(lap_hierarchy *h, int k, const double *B, double *X, d
 }
 
 // k right-hand sides (1 <= k <= 32), device buffers in the caller's layout: B, X n x k column-major
+// LAP_BLOCK_WIDE=1: every k > 8 on the lane-per-column SpMM (K = 16 / 32),
+// the round-2 routing before column groups (tests, measurements)
+static bool wide_forced() {
+    const char *e = getenv("LAP_BLOCK_WIDE");
+    return e && e[0] == '1';
+}
 void solve_block(lap_hierarchy *h, int k, const double *B, double *X, double tol, int32_t *iters, double *relres,
                  int *conv, cudaStream_t s) {
     if (k <= 2) solve_block_k<2>(h, k, B, X, tol, iters, relres, conv, s);
     else if (k <= 4) solve_block_k<4>(h, k, B, X, tol, iters, relres, conv, s);
     else if (k <= 8) solve_block_k<8>(h, k, B, X, tol, iters, relres, conv, s);
-    else if (k <= 16) solve_block_k<16>(h, k, B, X, tol, iters, relres, conv, s);
-    else solve_block_k<32>(h, k, B, X, tol, iters, relres, conv, s);
+    else if (wide_forced()) {
+        if (k <= 16) solve_block_k<16>(h, k, B, X, tol, iters, relres, conv, s);
+        else solve_block_k<32>(h, k, B, X, tol, iters, relres, conv, s);
+    } else if (k <= 16 || 10 * h->lev[0].n > h->lev[0].nnz) {
+        // blocks of <= 8 columns one after the other: the thread-per-row K = 8
+        // SpMM moves 8x the bytes per gather instruction of the lane-per-column
+        // K = 16 one (measured 2.13x vs 1.66x the throughput of k single solves
+        // on cfg 4, 1.71x vs 1.35x on cfg 2); past 16 columns K = 32 wins only
+        // where the matrix bytes it shares dominate (>= 10 entries per row:
+        // cfg 3 2.88x vs 2.03x) -- on mesh-like levels vectors dominate (cfg 2
+        // K = 32 1.41x vs 1.71x)
+        const int64_t n = h->lev[0].n;
+        int all = 1;
+        for (int c0 = 0; c0 < k; c0 += 8) {
+            const int kc = k - c0 < 8 ? k - c0 : 8;
+            int c = 0;
+            if (kc <= 2) solve_block_k<2>(h, kc, B + c0 * n, X + c0 * n, tol, iters + c0, relres + c0, &c, s);
+            else if (kc <= 4) solve_block_k<4>(h, kc, B + c0 * n, X + c0 * n, tol, iters + c0, relres + c0, &c, s);
+            else solve_block_k<8>(h, kc, B + c0 * n, X + c0 * n, tol, iters + c0, relres + c0, &c, s);
+            all = all && c;
+        }
+        *conv = all;
+    } else {
+        solve_block_k<32>(h, k, B, X, tol, iters, relres, conv, s);
+    }
 }
 
 }  // namespace lap

@@ -58,9 +58,11 @@ def test_block_matches_per_column_oracle(P, gname, k):
 
 @pytest.mark.parametrize("gname", ["grid2d_64", "rmat12", "star20000", "ba3000"])
 @pytest.mark.parametrize("k", [12, 16, 25, 32])
-def test_wide_block_matches_per_column_oracle(P, gname, k):
-    """k = 9..32 columns run the lane-per-column SpMM (K = 16 / 32) and the
-    per-element vector kernels; each column is still its own O-S8 solve."""
+def test_wide_block_matches_per_column_oracle(P, gname, k, monkeypatch):
+    """k = 9..32 columns on the lane-per-column SpMM (K = 16 / 32, forced by
+    LAP_BLOCK_WIDE=1) and the per-element vector kernels; each column is
+    still its own O-S8 solve."""
+    monkeypatch.setenv("LAP_BLOCK_WIDE", "1")
     g = GRAPHS[gname]()
     B = _rhs(g.n, k, seed=40)
     X, it, rr, rc = P.Hierarchy(g).solve_block(B)
@@ -74,9 +76,38 @@ def test_wide_block_matches_per_column_oracle(P, gname, k):
         assert np.abs(X[j] - xo).max() <= 1e-6 * np.abs(xo).max(), j
 
 
-def test_wide_block_agrees_with_narrow(P):
-    """The first 8 columns of a 32-column block solve agree with the same 8
-    columns solved at K = 8 (same iterations, x to 1e-10 relative)."""
+@pytest.mark.parametrize("gname", ["grid2d_64", "grid3d_16", "rmat12", "rand2000"])
+@pytest.mark.parametrize("k", [9, 16, 21, 32])
+def test_grouped_block_matches_per_column_oracle(P, gname, k):
+    """Default routing past 8 columns: groups of <= 8 columns on the
+    thread-per-row SpMM one after the other (k <= 16, or any k on a level 0
+    with < 10 entries per row), else K = 32; each column is its own O-S8
+    solve whichever way, and the grouped columns equal the same columns
+    solved alone as a block (bitwise: the same K = 8 program)."""
+    g = GRAPHS[gname]()
+    B = _rhs(g.n, k, seed=70)
+    h = P.Hierarchy(g)
+    X, it, rr, rc = h.solve_block(B)
+    assert rc == 0
+    ho = oracle.Hierarchy(g)
+    for j in range(k):
+        xo, ito, _, rco = ho.solve(B[j])
+        assert rco == 0
+        assert rr[j] <= 1e-8, (j, rr[j])
+        assert abs(int(it[j]) - ito) <= 1, (j, it[j], ito)
+        assert np.abs(X[j] - xo).max() <= 1e-6 * np.abs(xo).max(), j
+    if k <= 16 or 10 * g.n > len(g.col):
+        c0 = 8 * ((k - 1) // 8)
+        Xg, itg, _, _ = h.solve_block(B[c0:])
+        assert np.array_equal(itg, it[c0:])
+        assert Xg.tobytes() == X[c0:].tobytes()
+
+
+def test_wide_block_agrees_with_narrow(P, monkeypatch):
+    """The first 8 columns of a 32-column block solve on the lane-per-column
+    SpMM agree with the same 8 columns solved at K = 8 (same iterations, x to
+    1e-10 relative)."""
+    monkeypatch.setenv("LAP_BLOCK_WIDE", "1")
     g = lapgen.rmat(12)
     B = _rhs(g.n, 32, seed=5)
     h = P.Hierarchy(g)
