@@ -1251,6 +1251,37 @@ void setup_gather(std::vector<Level> &pieces, const std::vector<int> &mine, cons
         pc.w = nullptr;
     }
 }
+
+// Row-split setup passes (elimination select, affinity, vote rounds; setup.cu
+// RowSplit): every rank computed bytes [bb[r], bb[r+1]) of buf for its own
+// rows; afterwards every rank holds the whole array.  NCCL: one broadcast per
+// root, grouped, in place (the root's range is already in buf).  Virtual grid
+// or no communicator: every range was computed into the same buffer, nothing
+// moves.  Only exact per-row results move (states, indices, flags, the C_ij
+// and M_i of a row): bit-identical to one GPU.
+bool setup_nccl() { return g_setup_comm && !g_setup_comm->virt; }
+void setup_share(void *buf, const std::vector<int64_t> &bb, cudaStream_t s) {
+    if (!setup_nccl()) return;
+    lap_comm *c = g_setup_comm;
+    const int P = (int)bb.size() - 1;
+    uint8_t *b = (uint8_t *)buf;
+    NCCL_CHECK(ncclGroupStart());
+    for (int r = 0; r < P; r++) {
+        const int64_t cnt = bb[r + 1] - bb[r];
+        if (cnt > 0) NCCL_CHECK(ncclBroadcast(b + bb[r], b + bb[r], (size_t)cnt, ncclUint8, r, c->world, s));
+    }
+    NCCL_CHECK(ncclGroupEnd());
+}
+// K4: the votes of a round = sum over ranks of each rank's own votes
+// (integer sums: exact, order-free); NCCL only
+void setup_sum_i32(const int32_t *in, int32_t *out, int64_t n, cudaStream_t s) {
+    if (!setup_nccl() || n <= 0) return;
+    NCCL_CHECK(ncclAllReduce(in, out, (size_t)n, ncclInt32, ncclSum, g_setup_comm->world, s));
+}
+void setup_sum_u64(unsigned long long *v, int64_t n, cudaStream_t s) {
+    if (!setup_nccl() || n <= 0) return;
+    NCCL_CHECK(ncclAllReduce(v, v, (size_t)n, ncclUint64, ncclSum, g_setup_comm->world, s));
+}
 }  // namespace lap
 
 // ------------------------------------------------------------------ C ABI (multi-GPU)

@@ -250,6 +250,13 @@ std::vector<int> setup_local_ranks(); // ranks this process builds: {rank} (NCCL
 // (local row_ptr from 0); out <- the whole operator's row_ptr / col / w / nnz
 void setup_gather(std::vector<Level> &pieces, const std::vector<int> &mine, const std::vector<int64_t> &bounds,
                   Level &out, cudaStream_t s);
+// row-split setup passes: a real NCCL setup communicator?; bytes [bb[r], bb[r+1])
+// of buf broadcast from rank r to all (in place; no-op without NCCL); integer
+// sums over the ranks (no-op without NCCL)
+bool setup_nccl();
+void setup_share(void *buf, const std::vector<int64_t> &bb, cudaStream_t s);
+void setup_sum_i32(const int32_t *in, int32_t *out, int64_t n, cudaStream_t s);
+void setup_sum_u64(unsigned long long *v, int64_t n, cudaStream_t s);
 // the split rule of a term build over P ranks (device: setup.cu k_split_bounds;
 // host: lap_setup_split): bounds[r] = the first output row o with
 // cum(o) * P >= r * cum(nout), cum(o) = terms of the rows before o
@@ -368,6 +375,17 @@ inline unsigned grid_for(int64_t work, int threads, int64_t cap = 148 * 32) {
         const bool live = i < (n);                                                     \
         (void)live;
 #define GROUP_LOOP_END }
+// the same over rows [r0, r1) (row-split setup passes)
+#define GROUP_LOOP_RANGE_BEGIN(G, r0, r1)                                              \
+    const int lane = threadIdx.x & 31, gl = lane & ((G)-1);                            \
+    (void)gl;                                                                          \
+    const int64_t _gpw = 32 / (G);                                                     \
+    const int64_t _stride = (((int64_t)gridDim.x * blockDim.x) >> 5) * _gpw;           \
+    for (int64_t _base = (r0) + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * _gpw; \
+         _base < (r1); _base += _stride) {                                             \
+        const int64_t i = _base + lane / (G);                                          \
+        const bool live = i < (r1);                                                    \
+        (void)live;
 
 template <int G, class T>
 __device__ __forceinline__ T grp_sum(T v) {

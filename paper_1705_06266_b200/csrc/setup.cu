@@ -1040,6 +1040,50 @@ static std::vector<int64_t> split_bounds(int64_t nout, int P, const int64_t *vcp
     LAP_CUDA(cudaStreamSynchronize(s));
     return hb;
 }
+// ---- the row-parallel passes over a level's logical CSR --
+// elimination select (Alg. 2), affinity and the vote rounds
+// (Alg. 3) -- split by rows over the setup ranks in ranges of equal entry
+// counts (the term builds' rule with cum(o) = row_ptr[o]).  Each rank computes
+// its rows exactly as one GPU does (every per-row result depends only on
+// replicated round-start data), then the rows are shared (setup_share) and the
+// votes summed (K4: integer sums); the hierarchy is the single-GPU one
+// bit for bit, and each rank reads 1/P of the level's entries per pass.
+struct RowSplit {
+    bool on = false;
+    std::vector<int64_t> rb{0, 0}, eb{0, 0};  // row / entry bounds of the P ranges
+    std::vector<int> mine{0};                 // ranges this process computes
+    std::vector<int64_t> bytes(const std::vector<int64_t> &b, int64_t esz) const {
+        std::vector<int64_t> o(b.size());
+        for (size_t r = 0; r < b.size(); r++) o[r] = b[r] * esz;
+        return o;
+    }
+};
+__global__ void k_split_rows(int64_t n, int P, const int64_t *__restrict__ row_ptr, int64_t *__restrict__ out) {
+    const int r = threadIdx.x;
+    if (r > P) return;
+    const int64_t b = split_bound(r, P, n, [&](int64_t o) { return row_ptr[o]; });
+    out[r] = b;
+    out[P + 1 + r] = row_ptr[b];
+}
+static RowSplit row_split(int64_t n, int64_t nnz, const int64_t *row_ptr, cudaStream_t s) {
+    RowSplit R;
+    R.rb = {0, n};
+    R.eb = {0, nnz};
+    if (!dsetup_split(nnz)) return R;
+    const int P = setup_nranks();
+    DBuf<int64_t> b(2 * (P + 1), s);
+    k_split_rows<<<1, 64, 0, s>>>(n, P, row_ptr, b.p); ++g_kl;
+    LAP_CHECK_LAUNCH();
+    std::vector<int64_t> hb(2 * (P + 1));
+    LAP_CUDA(cudaMemcpyAsync(hb.data(), b.p, 8 * hb.size(), cudaMemcpyDeviceToHost, s));
+    LAP_CUDA(cudaStreamSynchronize(s));
+    R.on = true;
+    R.rb.assign(hb.begin(), hb.begin() + P + 1);
+    R.eb.assign(hb.begin() + P + 1, hb.end());
+    R.mine = setup_local_ranks();
+    return R;
+}
+
 // run build(lo, hi, piece) for this process's ranges and gather the full operator
 template <class F>
 static void build_split(int64_t nout, const std::vector<int64_t> &bounds, Level &out, cudaStream_t s, F build) {
@@ -1148,10 +1192,11 @@ __global__ void k_relabel_emit(int64_t n, const int64_t *__restrict__ row_ptr, c
 // h(j) = mix64(j XOR salt_2) (O-R17)
 __device__ __forceinline__ uint64_t elim_hash(int64_t j, uint64_t salt2) { return mix64((uint64_t)j ^ salt2); }
 
-__global__ void k_elim_select(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                              int maxdeg, uint64_t salt2, uint8_t *__restrict__ F, unsigned long long *nF) {
+__global__ void k_elim_select(int64_t r0, int64_t r1, const int64_t *__restrict__ row_ptr,
+                              const int32_t *__restrict__ col, int maxdeg, uint64_t salt2, uint8_t *__restrict__ F,
+                              unsigned long long *nF) {
     int64_t cnt = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t i = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r1; i += (int64_t)gridDim.x * blockDim.x) {
         int64_t a = row_ptr[i], e = row_ptr[i + 1];
         uint8_t f = 0;
         if (e - a <= maxdeg) {                       // candidate (O-R19)
@@ -1410,14 +1455,16 @@ __device__ __forceinline__ double affinity_of(const double *__restrict__ X, int6
 // max M_i as an atomic max of the bit pattern (non-negative doubles order like
 // their bits; max is exact and order-free)
 __global__ void k_affinity_long(int64_t nchunks, const int32_t *__restrict__ crow, const int32_t *__restrict__ cidx,
-                                const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                                const double *__restrict__ X, int power, double *__restrict__ C,
-                                unsigned long long *__restrict__ Mbits) {
+                                int64_t r0, int64_t r1, const int64_t *__restrict__ row_ptr,
+                                const int32_t *__restrict__ col, const double *__restrict__ X, int power,
+                                double *__restrict__ C, unsigned long long *__restrict__ Mbits) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t c = warp; c < nchunks; c += nwarps) {
-        const int64_t i = crow[c], b = row_ptr[i] + (int64_t)cidx[c] * LCHUNK, e = min(row_ptr[i + 1], b + LCHUNK);
+        const int64_t i = crow[c];
+        if (i < r0 || i >= r1) continue;  // another setup rank's row
+        const int64_t b = row_ptr[i] + (int64_t)cidx[c] * LCHUNK, e = min(row_ptr[i + 1], b + LCHUNK);
         double mx = 0.0;
         for (int64_t k = b + lane; k < e; k += 32) {
             double cv = affinity_of(X, i, col[k], power);
@@ -1433,9 +1480,10 @@ __global__ void k_affinity_long(int64_t nchunks, const int32_t *__restrict__ cro
 }
 // C_ij (O-R5) and row max M_i; warp per row
 template <int G>
-__global__ void k_affinity(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                           const double *__restrict__ X, int power, double *__restrict__ C, double *__restrict__ M) {
-    GROUP_LOOP_BEGIN(G, n)
+__global__ void k_affinity(int64_t r0, int64_t r1, const int64_t *__restrict__ row_ptr,
+                           const int32_t *__restrict__ col, const double *__restrict__ X, int power,
+                           double *__restrict__ C, double *__restrict__ M) {
+    GROUP_LOOP_RANGE_BEGIN(G, r0, r1)
         const int64_t ii = live ? i : 0;
         double xi[4] = {X[4 * ii], X[4 * ii + 1], X[4 * ii + 2], X[4 * ii + 3]};
         double ni = dot4_rn(xi, xi);
@@ -1503,11 +1551,11 @@ __global__ void k_vote_init(int64_t n, int8_t *st, int32_t *idx, int32_t *votes)
 // d = S_filt oplus_agg.otimes_agg status for Undecided rows; warp per row.
 // Reads round-start state st/idx, writes nst/nidx and votes.
 template <int G>
-__global__ void k_vote_round(int64_t n, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                             const double *__restrict__ S, double filt, const int8_t *__restrict__ st,
-                             const int32_t *__restrict__ idx, int8_t *__restrict__ nst, int32_t *__restrict__ nidx,
-                             int32_t *__restrict__ votes) {
-    GROUP_LOOP_BEGIN(G, n)
+__global__ void k_vote_round(int64_t r0, int64_t r1, const int64_t *__restrict__ row_ptr,
+                             const int32_t *__restrict__ col, const double *__restrict__ S, double filt,
+                             const int8_t *__restrict__ st, const int32_t *__restrict__ idx, int8_t *__restrict__ nst,
+                             int32_t *__restrict__ nidx, int32_t *__restrict__ votes) {
+    GROUP_LOOP_RANGE_BEGIN(G, r0, r1)
         // state and row bounds loaded together (independent loads: one memory round
         // trip less per row group than loading row_ptr after the state test)
         const int sti = live ? st[i] : ST_DEC;
@@ -1568,15 +1616,15 @@ __device__ __forceinline__ unsigned long long vote_key(const double *__restrict_
     return ((unsigned long long)r << 62) | (unsigned long long)__double_as_longlong(sv);
 }
 __global__ void k_vote_long_max(int64_t nchunks, const int32_t *__restrict__ crow, const int32_t *__restrict__ cidx,
-                                const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
-                                const double *__restrict__ S, double filt, const int8_t *__restrict__ st,
+                                int64_t r0, int64_t r1, const int64_t *__restrict__ row_ptr,
+                                const int32_t *__restrict__ col, const double *__restrict__ S, double filt, const int8_t *__restrict__ st,
                                 unsigned long long *__restrict__ best) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t c = warp; c < nchunks; c += nwarps) {
         const int64_t i = crow[c];
-        if (st[i] != ST_UND) continue;
+        if (i < r0 || i >= r1 || st[i] != ST_UND) continue;
         const int64_t b = row_ptr[i] + (int64_t)cidx[c] * LCHUNK, e = min(row_ptr[i + 1], b + LCHUNK);
         unsigned long long m = 0;
         for (int64_t k = b + lane; k < e; k += 32) {
@@ -1591,7 +1639,8 @@ __global__ void k_vote_long_max(int64_t nchunks, const int32_t *__restrict__ cro
     }
 }
 __global__ void k_vote_long_argj(int64_t nchunks, const int32_t *__restrict__ crow, const int32_t *__restrict__ cidx,
-                                 const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                                 int64_t r0, int64_t r1, const int64_t *__restrict__ row_ptr,
+                                 const int32_t *__restrict__ col,
                                  const double *__restrict__ S, double filt, const int8_t *__restrict__ st,
                                  const unsigned long long *__restrict__ best, int32_t *__restrict__ bestj) {
     const int lane = threadIdx.x & 31;
@@ -1599,7 +1648,7 @@ __global__ void k_vote_long_argj(int64_t nchunks, const int32_t *__restrict__ cr
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t c = warp; c < nchunks; c += nwarps) {
         const int64_t i = crow[c];
-        if (st[i] != ST_UND || best[i] == 0) continue;
+        if (i < r0 || i >= r1 || st[i] != ST_UND || best[i] == 0) continue;
         const unsigned long long bk = best[i];
         const int64_t b = row_ptr[i] + (int64_t)cidx[c] * LCHUNK, e = min(row_ptr[i + 1], b + LCHUNK);
         int32_t jm = 0x7fffffff;
@@ -1610,12 +1659,13 @@ __global__ void k_vote_long_argj(int64_t nchunks, const int32_t *__restrict__ cr
     }
 }
 __global__ void k_vote_long_apply(int64_t nchunks, const int32_t *__restrict__ crow, const int32_t *__restrict__ cidx,
-                                  const int8_t *__restrict__ st, const int32_t *__restrict__ idx,
+                                  int64_t r0, int64_t r1, const int8_t *__restrict__ st, const int32_t *__restrict__ idx,
                                   unsigned long long *__restrict__ best, int32_t *__restrict__ bestj,
                                   int8_t *__restrict__ nst, int32_t *__restrict__ nidx, int32_t *__restrict__ votes) {
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nchunks; c += (int64_t)gridDim.x * blockDim.x) {
         if (cidx[c] != 0) continue;  // once per long row
         const int64_t i = crow[c];
+        if (i < r0 || i >= r1) continue;
         const unsigned long long bk = best[i];
         const int br = bk ? (int)(bk >> 62) : -1;
         const bool act = st[i] == ST_UND;
@@ -1864,6 +1914,9 @@ struct CStore {
     const int32_t *__restrict__ crow, *__restrict__ cidx, *__restrict__ cslot;
     int32_t *__restrict__ ccnt;
     I128 *__restrict__ cpart;  // NC per chunk
+    // the work of one setup rank (SURVEY N1 row-split sweeps): slices [s_lo, s_hi)
+    // and the chunks of the long rows [p_lo, p_hi); cstore_of: everything
+    int64_t s_lo, s_hi, p_lo, p_hi;
 };
 struct CSweep {  // CS_SWEEP: x_new = x - omega ((d x - s) / d), per column
     const double *__restrict__ X;
@@ -1951,11 +2004,13 @@ __global__ void __launch_bounds__(XS ? 1024 : 256, XS ? 1 : 4) k_cspmv_store(CSt
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int64_t nitems = C.nslices + C.nchunks;
+    const int64_t nsl = C.s_hi - C.s_lo;
+    const int64_t nitems = nsl + C.nchunks;
     for (int64_t t = warp; t < nitems; t += nwarps) {
-        if (t < C.nslices) {  // SELL-32 slice: a thread per row, 8 independent loads per batch
-            const int64_t p = t * 32 + lane, beg = C.slice_ptr[t];
-            const int width = (int)((C.slice_ptr[t + 1] - beg) >> 5);
+        if (t < nsl) {  // SELL-32 slice: a thread per row, 8 independent loads per batch
+            const int64_t ts = C.s_lo + t;
+            const int64_t p = ts * 32 + lane, beg = C.slice_ptr[ts];
+            const int width = (int)((C.slice_ptr[ts + 1] - beg) >> 5);
             i128 acc[NC];
 #pragma unroll
             for (int k = 0; k < NC; k++) acc[k] = 0;
@@ -1980,8 +2035,10 @@ __global__ void __launch_bounds__(XS ? 1024 : 256, XS ? 1 : 4) k_cspmv_store(CSt
             if (p < C.nshort) ya = cs_epilogue<NC, MODE>(p, acc, elo, C, x, rs, vp, bprev, y, W);
             if (MODE == CS_LANCZOS) warp_atomic_max(&st->maxy, ya);
         } else {  // a 1024-entry chunk of a long row: warp-wide, int128 partials combined by the last arrival
-            const int64_t c = t - C.nslices;
-            const int64_t p = C.crow[c], j = C.cidx[c], rb = C.srp[p], re = C.srp[p + 1];
+            const int64_t c = t - nsl;
+            const int64_t p = C.crow[c];
+            if (p < C.p_lo || p >= C.p_hi) continue;  // another setup rank's long row (warp-uniform)
+            const int64_t j = C.cidx[c], rb = C.srp[p], re = C.srp[p + 1];
             const int64_t b = rb + j * LCHUNK, e = min(re, b + LCHUNK);
             i128 acc[NC];
 #pragma unroll
@@ -2061,7 +2118,21 @@ static CStore cstore_of(const Level &L, I128 *cpart) {
     C.cslot = L.chunk_slot;
     C.ccnt = L.chunk_cnt;
     C.cpart = cpart;
+    C.s_lo = 0;
+    C.s_hi = L.nslices;
+    C.p_lo = 0;
+    C.p_hi = (int64_t)1 << 62;
     return C;
+}
+// N1: a level's solve storage split over the setup ranks for the test-vector
+// sweeps: slices by entries (cum = slice_ptr), long rows [c_end[0], n) by
+// entries (cum = srp); out = P+1 slice bounds, then P+1 long-row bounds
+__global__ void k_split_store(int64_t nslices, const int64_t *__restrict__ slice_ptr, int64_t nshort, int64_t n,
+                              const int64_t *__restrict__ srp, int P, int64_t *__restrict__ out) {
+    const int r = threadIdx.x;
+    if (r > P) return;
+    out[r] = split_bound(r, P, nslices, [&](int64_t o) { return slice_ptr[o]; });
+    out[P + 1 + r] = nshort + split_bound(r, P, n - nshort, [&](int64_t o) { return srp[nshort + o] - srp[nshort]; });
 }
 static unsigned cstore_grid(const Level &L) { return grid_for((L.nslices + L.nchunks) * 32, 256, 148 * 8); }
 
@@ -2366,9 +2437,18 @@ static int64_t elim_select(lap_hierarchy *h, Level &L, DBuf<uint8_t> &F, cudaStr
     F.alloc(L.n, s);
     DBuf<unsigned long long> nF(1, s);
     LAP_CUDA(cudaMemsetAsync(nF.p, 0, 8, s));
-    k_elim_select<<<grid_for(L.n, 256, 148 * 16), 256, 0, s>>>(L.n, L.row_ptr, L.col, h->p.elim_max_degree,
-                                                                salt_of(h->p.seed, 2), F.p, nF.p); ++g_kl;
+    const RowSplit R = row_split(L.n, L.nnz, L.row_ptr, s);  // N1: rows over the setup ranks
+    for (int r : R.mine) {
+        const int64_t r0 = R.rb[r], r1 = R.rb[r + 1];
+        k_elim_select<<<grid_for(r1 - r0, 256, 148 * 16), 256, 0, s>>>(r0, r1, L.row_ptr, L.col,
+                                                                        h->p.elim_max_degree, salt_of(h->p.seed, 2),
+                                                                        F.p, nF.p); ++g_kl;
+    }
     LAP_CHECK_LAUNCH();
+    if (R.on) {
+        setup_share(F.p, R.rb, s);  // one byte per row
+        setup_sum_u64(nF.p, 1, s);
+    }
     h->cur.edges += L.nnz;
     return (int64_t)d2h_scalar(nF.p, s);
 }
@@ -2465,6 +2545,28 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
         }
     } free_lc{{lc_row, lc_idx, lc_slot, lc_cnt, lc_dummy}, s};
     DBuf<I128> cpart(4 * (L.nchunks > 0 ? L.nchunks : 1), s);
+    // N1: each setup rank sweeps its slices and long rows (ranges of equal entry
+    // counts, k_split_store); the rows' new vectors (32 B each) are shared after
+    // every sweep.  Per-row CanonSums: bit-identical to one GPU.
+    const bool tv_split = dsetup_split(nnz);
+    const int Ps = tv_split ? setup_nranks() : 1;
+    std::vector<int64_t> tsb{0, L.nslices}, tlb{L.c_end[0], n};
+    const std::vector<int> tmine = tv_split ? setup_local_ranks() : std::vector<int>{0};
+    if (tv_split) {
+        DBuf<int64_t> b(2 * (Ps + 1), s);
+        k_split_store<<<1, 64, 0, s>>>(L.nslices, L.slice_ptr, L.c_end[0], n, L.srp, Ps, b.p); ++g_kl;
+        LAP_CHECK_LAUNCH();
+        std::vector<int64_t> hb(2 * (Ps + 1));
+        LAP_CUDA(cudaMemcpyAsync(hb.data(), b.p, 8 * hb.size(), cudaMemcpyDeviceToHost, s));
+        LAP_CUDA(cudaStreamSynchronize(s));
+        tsb.assign(hb.begin(), hb.begin() + Ps + 1);
+        tlb.assign(hb.begin() + Ps + 1, hb.end());
+    }
+    std::vector<int64_t> tb_sell(Ps + 1), tb_long(Ps + 1);  // byte bounds of the shared rows of X
+    for (int r = 0; r <= Ps; r++) {
+        tb_sell[r] = 32 * std::min<int64_t>(32 * tsb[r], L.c_end[0]);
+        tb_long[r] = 32 * tlb[r];
+    }
     for (int sw = 0; sw < p.tv_sweeps; sw++) {
         // CanonSum instance of this sweep: e_max from the exact max |x| (O-S11), computed on
         // the device (no host round trip)
@@ -2472,10 +2574,21 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
         k_max_abs<<<grid_for(4 * n, 256, 148 * 8), 256, 0, s>>>(X.p, 4 * n, mxb.p); ++g_kl;
         k_tv_elo<<<1, 1, 0, s>>>(mxb.p, ew, nnz, elo.p); ++g_kl;
         const CSweep W{X.p, Xn.p, elo.p, p.tv_omega};
-        k_cspmv_store<4, CS_SWEEP><<<cstore_grid(L), 256, 0, s>>>(CStore(cstore_of(L, cpart.p)), X.p, nullptr,
-                                                                  nullptr, 0, nullptr, nullptr, W, 0);
-        ++g_kl;
+        for (int r : tmine) {
+            CStore C = cstore_of(L, cpart.p);
+            C.s_lo = tsb[r];
+            C.s_hi = tsb[r + 1];
+            C.p_lo = tlb[r];
+            C.p_hi = tlb[r + 1];
+            const unsigned gsw = grid_for((C.s_hi - C.s_lo + L.nchunks / Ps + 1) * 32, 256, 148 * 8);
+            k_cspmv_store<4, CS_SWEEP><<<gsw, 256, 0, s>>>(C, X.p, nullptr, nullptr, 0, nullptr, nullptr, W, 0);
+            ++g_kl;
+        }
         LAP_CHECK_LAUNCH();
+        if (tv_split) {
+            setup_share(Xn.p, tb_sell, s);
+            setup_share(Xn.p, tb_long, s);
+        }
         std::swap(X.p, Xn.p);
         h->cur.edges += nnz;
     }
@@ -2483,14 +2596,22 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
     k_tv_unpermute<<<grid_for(4 * n, 256, 148 * 16), 256, 0, s>>>(n, L.sid, X.p, Xn.p); ++g_kl;
     std::swap(X.p, Xn.p);
     tmark("  test vectors");
-    // affinity + normalisation
+    // affinity + normalisation; C_ij and M_i of each setup rank's
+    // rows (N1), shared before the (replicated, entry-parallel) normalisation
+    const RowSplit R = row_split(n, nnz, L.row_ptr, s);
     if (nlc > 0) LAP_CUDA(cudaMemsetAsync(M.p, 0, sizeof(double) * n, s));
-    LAUNCH_G(Ga, k_affinity, n, s, n, L.row_ptr, L.col, X.p, p.affinity_power, S.p, M.p);
-    if (nlc > 0) {
-        k_affinity_long<<<grid_for(nlc * 32, 256, 148 * 16), 256, 0, s>>>(nlc, lc_row, lc_idx, L.row_ptr, L.col, X.p,
-                                                                          p.affinity_power, S.p,
-                                                                          (unsigned long long *)M.p);
-        ++g_kl;
+    for (int r : R.mine) {
+        const int64_t r0 = R.rb[r], r1 = R.rb[r + 1];
+        LAUNCH_G(Ga, k_affinity, r1 - r0, s, r0, r1, L.row_ptr, L.col, X.p, p.affinity_power, S.p, M.p);
+        if (nlc > 0) {
+            k_affinity_long<<<grid_for(nlc * 32, 256, 148 * 16), 256, 0, s>>>(
+                nlc, lc_row, lc_idx, r0, r1, L.row_ptr, L.col, X.p, p.affinity_power, S.p, (unsigned long long *)M.p);
+            ++g_kl;
+        }
+    }
+    if (R.on) {
+        setup_share(S.p, R.bytes(R.eb, 8), s);
+        setup_share(M.p, R.bytes(R.rb, 8), s);
     }
     if (nnz > 0) {
         k_normalize<<<grid_for(nnz, 256, 148 * 16), 256, 0, s>>>(n, nnz, L.rowof, L.col, M.p, S.p);
@@ -2503,6 +2624,12 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
     DBuf<int8_t> st(n, s), nst(n, s);
     DBuf<int32_t> idx(n, s), nidx(n, s), votes(n, s);
     k_vote_init<<<ge, 256, 0, s>>>(n, st.p, idx.p, votes.p); ++g_kl;
+    // N1 over NCCL: this rank's own votes accumulate in vloc, votes = their sum
+    // over the ranks (K4); otherwise every range adds into votes directly
+    const bool vsum = R.on && setup_nccl();
+    DBuf<int32_t> vloc(vsum ? n : 1, s);
+    if (vsum) LAP_CUDA(cudaMemsetAsync(vloc.p, 0, sizeof(int32_t) * n, s));
+    int32_t *vp = vsum ? vloc.p : votes.p;
     DBuf<unsigned long long> vbest(nlc > 0 ? n : 1, s);
     DBuf<int32_t> vbestj(nlc > 0 ? n : 1, s);
     if (nlc > 0) {
@@ -2511,15 +2638,25 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
     }
     for (int t = 1; t <= p.vote_rounds; t++) {
         double filt = ldexp(1.0, -t);
-        LAUNCH_G(Gv, k_vote_round, n, s, n, L.row_ptr, L.col, S.p, filt, st.p, idx.p, nst.p, nidx.p, votes.p);
-        if (nlc > 0) {
-            const unsigned gc = grid_for(nlc * 32, 256, 148 * 16);
-            k_vote_long_max<<<gc, 256, 0, s>>>(nlc, lc_row, lc_idx, L.row_ptr, L.col, S.p, filt, st.p, vbest.p);
-            k_vote_long_argj<<<gc, 256, 0, s>>>(nlc, lc_row, lc_idx, L.row_ptr, L.col, S.p, filt, st.p, vbest.p,
-                                                vbestj.p);
-            k_vote_long_apply<<<grid_for(nlc, 256, 148 * 8), 256, 0, s>>>(nlc, lc_row, lc_idx, st.p, idx.p, vbest.p,
-                                                                          vbestj.p, nst.p, nidx.p, votes.p);
-            g_kl += 3;
+        for (int r : R.mine) {
+            const int64_t r0 = R.rb[r], r1 = R.rb[r + 1];
+            LAUNCH_G(Gv, k_vote_round, r1 - r0, s, r0, r1, L.row_ptr, L.col, S.p, filt, st.p, idx.p, nst.p, nidx.p,
+                     vp);
+            if (nlc > 0) {
+                const unsigned gc = grid_for(nlc * 32, 256, 148 * 16);
+                k_vote_long_max<<<gc, 256, 0, s>>>(nlc, lc_row, lc_idx, r0, r1, L.row_ptr, L.col, S.p, filt, st.p,
+                                                   vbest.p);
+                k_vote_long_argj<<<gc, 256, 0, s>>>(nlc, lc_row, lc_idx, r0, r1, L.row_ptr, L.col, S.p, filt, st.p,
+                                                    vbest.p, vbestj.p);
+                k_vote_long_apply<<<grid_for(nlc, 256, 148 * 8), 256, 0, s>>>(
+                    nlc, lc_row, lc_idx, r0, r1, st.p, idx.p, vbest.p, vbestj.p, nst.p, nidx.p, vp);
+                g_kl += 3;
+            }
+        }
+        if (R.on) {  // the round's new states of every rank's rows, and the summed votes
+            setup_share(nst.p, R.rb, s);
+            setup_share(nidx.p, R.bytes(R.rb, 4), s);
+            if (vsum) setup_sum_i32(vloc.p, votes.p, n, s);
         }
         k_vote_promote<<<ge, 256, 0, s>>>(n, nst.p, votes.p, p.vote_threshold); ++g_kl;
         LAP_CHECK_LAUNCH();

@@ -241,3 +241,93 @@ def test_setup_split_gather_gloo(world):
         assert p.exitcode == 0
     assert all(ok for _, ok, _ in res), res
     assert sum(nr for _, _, nr in res) > 0
+
+
+def _vote_worker(rank, world, port, q):
+    """One setup rank of the row-split vote rounds (setup.cu aggregate_attempt
+    under a setup communicator): its rows of each synchronous round
+    (Alg. 3) from the replicated round-start state, the new states
+    shared by one broadcast per root (dist.cu setup_share), the votes summed
+    over the ranks (K4; dist.cu setup_sum_i32)."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        L = _lib()
+        res = []
+        for g in [lapgen.barabasi_albert(3000, 6), lapgen.rmat(11), lapgen.grid2d(40, 30)]:
+            n, rp, col = g.n, g.row_ptr, g.col
+            d = oracle.row_sums(n, rp, g.w)
+            X = oracle.test_vectors(n, rp, col, g.w, d, seed=0, level=0)
+            S = oracle.normalize_strength(n, rp, col, oracle.affinity(n, rp, col, X))
+            agg_ref, m_ref, st_ref, votes_ref = oracle.aggregate(n, rp, col, S)
+            b = L.setup_split(rp, world)          # rows in ranges of equal entry counts
+            lo, hi = int(b[rank]), int(b[rank + 1])
+            DEC, UND, SEED = 0, 1, 2
+            st = np.full(n, UND, np.int8)
+            idx = np.arange(n, dtype=np.int32)
+            votes = torch.zeros(n, dtype=torch.int32)
+            vloc = torch.zeros(n, dtype=torch.int32)
+            for t in range(1, 11):
+                filt = 2.0 ** -t
+                nst, nidx = st.copy(), idx.copy()
+                for i in range(lo, hi):
+                    if st[i] != UND:
+                        continue
+                    best = None
+                    for k in range(rp[i], rp[i + 1]):
+                        j, s = int(col[k]), S[k]
+                        if s == 0.0 or s < filt or st[j] == DEC:
+                            continue
+                        key = (int(st[j]), s, -j)
+                        if best is None or key > best:
+                            best = key
+                    if best is None:
+                        continue
+                    if best[0] == SEED:
+                        nst[i], nidx[i] = DEC, -best[2]
+                    else:
+                        vloc[-best[2]] += 1
+                ts, ti = torch.from_numpy(nst), torch.from_numpy(nidx)
+                for r in range(world):                # setup_share: one broadcast per root
+                    a0, a1 = int(b[r]), int(b[r + 1])
+                    for buf in (ts, ti):
+                        seg = buf[a0:a1].clone()
+                        dist.broadcast(seg, src=r)
+                        buf[a0:a1] = seg
+                dist.all_reduce(votes.copy_(vloc), op=dist.ReduceOp.SUM)   # setup_sum_i32
+                st, idx = ts.numpy().copy(), ti.numpy().copy()
+                st[(st == UND) & (votes.numpy() >= 8)] = SEED              # k_vote_promote (replicated)
+            root = st != DEC
+            rid = np.cumsum(root) - 1
+            agg = np.where(root, rid, rid[idx]).astype(np.int32)
+            res.append(bool(np.array_equal(agg, agg_ref) and np.array_equal(st, st_ref)
+                            and np.array_equal(votes.numpy(), votes_ref) and int(root.sum()) == m_ref))
+        q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_split_voting_gloo(world):
+    """N1 row-split vote rounds with torch.distributed 'gloo' (world 2 and 3):
+    each rank runs Alg. 3's synchronous rounds on its lap_setup_split row range
+    (split by entries, cum = row_ptr) against the replicated round-start
+    states, the new states are shared by one broadcast per root and the votes
+    summed over the ranks; the aggregates, final states and vote counts equal
+    the oracle's whole-graph aggregation on every rank."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_vote_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(all(ok) for _, ok in res), res

@@ -116,8 +116,9 @@ def test_nccl_transport_single_rank(P):
 
 def test_nccl_distributed_setup_single_rank(P, monkeypatch):
     """The distributed setup's NCCL gather (entry counts all-gathered, one
-    ncclBroadcast per root, row_ptr pieces shifted) on a real 1 x 1 NCCL
-    communicator with every term build forced through it (LAP_DSETUP_MIN=0):
+    ncclBroadcast per root, row_ptr pieces shifted) and the row-split passes'
+    sharing (in-place broadcasts, the vote / F-count allreduces) on a real
+    1 x 1 NCCL communicator with every split forced (LAP_DSETUP_MIN=0):
     the hierarchy equals the single-GPU one bit for bit and the sharded solve
     (own-piece SpMV on the side stream) converges like it."""
     g = lapgen.barabasi_albert(4000, 7)
@@ -181,8 +182,11 @@ def _level_bits(h, l):
 def test_distributed_setup_bit_identical(P, gname, grid, gal_fast, monkeypatch):
     """with a setup communicator the coarse-operator term builds
     (Galerkin -- ordered and batched paths --, Schur complement) are split by
-    output rows over the ranks and gathered; every entry is still one CanonSum
-    of its whole multiset with the level's global instance, so the hierarchy
+    output rows over the ranks and gathered, and the row-parallel passes
+    (elimination select, affinity, the ten vote rounds -- hub rows by chunks
+    included, star20000) run on each rank's row range; every entry is still
+    one CanonSum of its whole multiset with the level's global instance and
+    every per-row result is computed once, so the hierarchy
     (every level's CSR, diagonal, aggregates / F sets, lambda-hat) equals the
     single-GPU one bit for bit.  LAP_DSETUP_MIN=0 splits every product."""
     g = GRAPHS[gname]()
