@@ -1278,6 +1278,12 @@ void setup_sum_i32(const int32_t *in, int32_t *out, int64_t n, cudaStream_t s) {
     if (!setup_nccl() || n <= 0) return;
     NCCL_CHECK(ncclAllReduce(in, out, (size_t)n, ncclInt32, ncclSum, g_setup_comm->world, s));
 }
+// the Lanczos max |y| (bit patterns of non-negative doubles order like the
+// values): an exact max over the ranks; NCCL only
+void setup_max_u64(unsigned long long *v, cudaStream_t s) {
+    if (!setup_nccl()) return;
+    NCCL_CHECK(ncclAllReduce(v, v, 1, ncclUint64, ncclMax, g_setup_comm->world, s));
+}
 void setup_sum_u64(unsigned long long *v, int64_t n, cudaStream_t s) {
     if (!setup_nccl() || n <= 0) return;
     NCCL_CHECK(ncclAllReduce(v, v, (size_t)n, ncclUint64, ncclSum, g_setup_comm->world, s));

@@ -257,6 +257,7 @@ bool setup_nccl();
 void setup_share(void *buf, const std::vector<int64_t> &bb, cudaStream_t s);
 void setup_sum_i32(const int32_t *in, int32_t *out, int64_t n, cudaStream_t s);
 void setup_sum_u64(unsigned long long *v, int64_t n, cudaStream_t s);
+void setup_max_u64(unsigned long long *v, cudaStream_t s);
 // the split rule of a term build over P ranks (device: setup.cu k_split_bounds;
 // host: lap_setup_split): bounds[r] = the first output row o with
 // cum(o) * P >= r * cum(nout), cum(o) = terms of the rows before o

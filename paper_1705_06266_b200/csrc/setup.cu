@@ -2134,6 +2134,52 @@ __global__ void k_split_store(int64_t nslices, const int64_t *__restrict__ slice
     out[r] = split_bound(r, P, nslices, [&](int64_t o) { return slice_ptr[o]; });
     out[P + 1 + r] = nshort + split_bound(r, P, n - nshort, [&](int64_t o) { return srp[nshort + o] - srp[nshort]; });
 }
+struct StoreSplit {
+    bool on = false;
+    int P = 1;
+    std::vector<int64_t> sb, lb;  // slice bounds, long-row (storage row) bounds
+    std::vector<int> mine{0};
+    CStore range(CStore C, int r) const {
+        C.s_lo = sb[r];
+        C.s_hi = sb[r + 1];
+        C.p_lo = lb[r];
+        C.p_hi = lb[r + 1];
+        return C;
+    }
+    unsigned grid(const CStore &C, int64_t nchunks) const {
+        return grid_for((C.s_hi - C.s_lo + nchunks / P + 1) * 32, 256, 148 * 8);
+    }
+    // share rows of a storage-order array of rsz bytes per row: the SELL rows,
+    // then the long rows of every rank
+    void share(void *buf, int64_t rsz, int64_t nshort, cudaStream_t s) const {
+        if (!on) return;
+        std::vector<int64_t> a(P + 1), b(P + 1);
+        for (int r = 0; r <= P; r++) {
+            a[r] = rsz * std::min<int64_t>(32 * sb[r], nshort);
+            b[r] = rsz * lb[r];
+        }
+        setup_share(buf, a, s);
+        setup_share(buf, b, s);
+    }
+};
+static StoreSplit store_split(const Level &L, cudaStream_t s) {
+    StoreSplit T;
+    T.sb = {0, L.nslices};
+    T.lb = {L.c_end[0], L.n};
+    if (!dsetup_split(L.nnz)) return T;
+    T.on = true;
+    T.P = setup_nranks();
+    T.mine = setup_local_ranks();
+    DBuf<int64_t> b(2 * (T.P + 1), s);
+    k_split_store<<<1, 64, 0, s>>>(L.nslices, L.slice_ptr, L.c_end[0], L.n, L.srp, T.P, b.p); ++g_kl;
+    LAP_CHECK_LAUNCH();
+    std::vector<int64_t> hb(2 * (T.P + 1));
+    LAP_CUDA(cudaMemcpyAsync(hb.data(), b.p, 8 * hb.size(), cudaMemcpyDeviceToHost, s));
+    LAP_CUDA(cudaStreamSynchronize(s));
+    T.sb.assign(hb.begin(), hb.begin() + T.P + 1);
+    T.lb.assign(hb.begin() + T.P + 1, hb.end());
+    return T;
+}
 static unsigned cstore_grid(const Level &L) { return grid_for((L.nslices + L.nchunks) * 32, 256, 148 * 8); }
 
 // pass C: acc_a += q(fl(y v))
@@ -2259,7 +2305,12 @@ static void lanczos(lap_hierarchy *h, Level &L, int l, cudaStream_t s, double *h
     C.ccnt = ccnt.p;
     CSweep W{};
     W.elo_p = elo_d.p;
+    // N1: the SpMV of each step split over the setup ranks (rows of y shared,
+    // max |y| combined: an exact max); the dots run on the whole vectors on every
+    // rank.  Only in line on the setup stream (lanczos_in_line), and not on
+    // shared-memory-x levels (small)
     const bool xs = L.smem_x && n <= SMEM_X_MAX;
+    const StoreSplit T = xs ? StoreSplit{} : store_split(L, s);
     if (xs) {
         static bool attr = false;
         if (!attr) {
@@ -2273,9 +2324,19 @@ static void lanczos(lap_hierarchy *h, Level &L, int l, cudaStream_t s, double *h
         if (xs)
             k_cspmv_store<1, CS_LANCZOS, true><<<num_sms_dev(), 1024, 8 * n, s>>>(C, u.p, rs.p, vp.p, elo_spmv, st.p,
                                                                                   y.p, W, n);
-        else
+        else if (!T.on)
             k_cspmv_store<1, CS_LANCZOS><<<cstore_grid(L), 256, 0, s>>>(C, u.p, rs.p, vp.p, elo_spmv, st.p, y.p, W, 0);
+        else
+            for (int r : T.mine) {
+                const CStore Cr = T.range(C, r);
+                k_cspmv_store<1, CS_LANCZOS><<<T.grid(Cr, L.nchunks), 256, 0, s>>>(Cr, u.p, rs.p, vp.p, elo_spmv,
+                                                                                   st.p, y.p, W, 0);
+            }
         ++g_kl;
+        if (T.on) {
+            T.share(y.p, 8, L.c_end[0], s);
+            setup_max_u64(&st.p->maxy, s);
+        }
         k_lzc_alpha<<<g, 256, 0, s>>>(n, y.p, v.p, st.p); ++g_kl;
         k_lzc_update<<<g, 256, 0, s>>>(n, y.p, v.p, st.p); ++g_kl;
         LAP_CHECK_LAUNCH();
@@ -2548,25 +2609,7 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
     // N1: each setup rank sweeps its slices and long rows (ranges of equal entry
     // counts, k_split_store); the rows' new vectors (32 B each) are shared after
     // every sweep.  Per-row CanonSums: bit-identical to one GPU.
-    const bool tv_split = dsetup_split(nnz);
-    const int Ps = tv_split ? setup_nranks() : 1;
-    std::vector<int64_t> tsb{0, L.nslices}, tlb{L.c_end[0], n};
-    const std::vector<int> tmine = tv_split ? setup_local_ranks() : std::vector<int>{0};
-    if (tv_split) {
-        DBuf<int64_t> b(2 * (Ps + 1), s);
-        k_split_store<<<1, 64, 0, s>>>(L.nslices, L.slice_ptr, L.c_end[0], n, L.srp, Ps, b.p); ++g_kl;
-        LAP_CHECK_LAUNCH();
-        std::vector<int64_t> hb(2 * (Ps + 1));
-        LAP_CUDA(cudaMemcpyAsync(hb.data(), b.p, 8 * hb.size(), cudaMemcpyDeviceToHost, s));
-        LAP_CUDA(cudaStreamSynchronize(s));
-        tsb.assign(hb.begin(), hb.begin() + Ps + 1);
-        tlb.assign(hb.begin() + Ps + 1, hb.end());
-    }
-    std::vector<int64_t> tb_sell(Ps + 1), tb_long(Ps + 1);  // byte bounds of the shared rows of X
-    for (int r = 0; r <= Ps; r++) {
-        tb_sell[r] = 32 * std::min<int64_t>(32 * tsb[r], L.c_end[0]);
-        tb_long[r] = 32 * tlb[r];
-    }
+    const StoreSplit T = store_split(L, s);
     for (int sw = 0; sw < p.tv_sweeps; sw++) {
         // CanonSum instance of this sweep: e_max from the exact max |x| (O-S11), computed on
         // the device (no host round trip)
@@ -2574,21 +2617,14 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
         k_max_abs<<<grid_for(4 * n, 256, 148 * 8), 256, 0, s>>>(X.p, 4 * n, mxb.p); ++g_kl;
         k_tv_elo<<<1, 1, 0, s>>>(mxb.p, ew, nnz, elo.p); ++g_kl;
         const CSweep W{X.p, Xn.p, elo.p, p.tv_omega};
-        for (int r : tmine) {
-            CStore C = cstore_of(L, cpart.p);
-            C.s_lo = tsb[r];
-            C.s_hi = tsb[r + 1];
-            C.p_lo = tlb[r];
-            C.p_hi = tlb[r + 1];
-            const unsigned gsw = grid_for((C.s_hi - C.s_lo + L.nchunks / Ps + 1) * 32, 256, 148 * 8);
-            k_cspmv_store<4, CS_SWEEP><<<gsw, 256, 0, s>>>(C, X.p, nullptr, nullptr, 0, nullptr, nullptr, W, 0);
+        for (int r : T.mine) {
+            const CStore C = T.range(cstore_of(L, cpart.p), r);
+            k_cspmv_store<4, CS_SWEEP><<<T.grid(C, L.nchunks), 256, 0, s>>>(C, X.p, nullptr, nullptr, 0, nullptr,
+                                                                            nullptr, W, 0);
             ++g_kl;
         }
         LAP_CHECK_LAUNCH();
-        if (tv_split) {
-            setup_share(Xn.p, tb_sell, s);
-            setup_share(Xn.p, tb_long, s);
-        }
+        T.share(Xn.p, 32, L.c_end[0], s);  // n x 4 doubles
         std::swap(X.p, Xn.p);
         h->cur.edges += nnz;
     }
@@ -3063,7 +3099,9 @@ void build_hierarchy(lap_hierarchy *h, const lap_graph *g, cudaStream_t s) {
     int elim_run = 0;  // consecutive elimination levels built just above (O-R21)
     LanczosStream lzs;
     const char *lza = getenv("LAP_LANCZOS_ASYNC");  // 0: in line on the setup stream
-    const bool lz_async = !(lza && lza[0] == '0');
+    // (under a real NCCL setup communicator the split Lanczos issues collectives:
+    // in line, so that every rank enqueues them in one order on one stream)
+    const bool lz_async = !(lza && lza[0] == '0') && !setup_nccl();
     double lz_host_v = 0.0, *lz_host = &lz_host_v;
     for (int l = 0;; l++) {
         Level &L = h->lev[l];
