@@ -1479,8 +1479,10 @@ __global__ void k_affinity_long(int64_t nchunks, const int32_t *__restrict__ cro
     }
 }
 // C_ij (O-R5) and row max M_i; warp per row
+// (64 registers: 4 CTAs per SM; 78 left 37 % of the warps resident and the
+// 32-byte X gathers latency-bound, ncu profiles/r02)
 template <int G>
-__global__ void k_affinity(int64_t r0, int64_t r1, const int64_t *__restrict__ row_ptr,
+__global__ void __launch_bounds__(256, 4) k_affinity(int64_t r0, int64_t r1, const int64_t *__restrict__ row_ptr,
                            const int32_t *__restrict__ col, const double *__restrict__ X, int power,
                            double *__restrict__ C, double *__restrict__ M) {
     GROUP_LOOP_RANGE_BEGIN(G, r0, r1)
@@ -1548,60 +1550,6 @@ __global__ void k_vote_init(int64_t n, int8_t *st, int32_t *idx, int32_t *votes)
     }
 }
 
-// d = S_filt oplus_agg.otimes_agg status for Undecided rows; warp per row.
-// Reads round-start state st/idx, writes nst/nidx and votes.
-template <int G>
-__global__ void k_vote_round(int64_t r0, int64_t r1, const int64_t *__restrict__ row_ptr,
-                             const int32_t *__restrict__ col, const double *__restrict__ S, double filt,
-                             const int8_t *__restrict__ st, const int32_t *__restrict__ idx, int8_t *__restrict__ nst,
-                             int32_t *__restrict__ nidx, int32_t *__restrict__ votes) {
-    GROUP_LOOP_RANGE_BEGIN(G, r0, r1)
-        // state and row bounds loaded together (independent loads: one memory round
-        // trip less per row group than loading row_ptr after the state test)
-        const int sti = live ? st[i] : ST_DEC;
-        const int64_t rb = live ? row_ptr[i] : 0, re = live ? row_ptr[i + 1] : 0;
-        const int64_t kb0 = sti == ST_UND ? rb : 0, ke0 = sti == ST_UND ? re : 0;
-        const bool lng = ke0 - kb0 > SETUP_LONG;  // k_vote_long_*
-        const bool act = sti == ST_UND && !lng;    // only Undecided act (O-R9)
-        int br = -1;
-        double bs = 0.0;
-        int32_t bj = 0x7fffffff;
-        const int64_t kb = act ? kb0 : 0, ke = act ? ke0 : 0;
-        // 4 (S, col) loads, then the passing entries' state gathers, in flight together
-        for (int64_t k0 = kb + gl; k0 < ke; k0 += 4 * G) {
-            double sv[4];
-            int32_t jj[4];
-            int rr[4];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const int64_t k = k0 + u * G;
-                sv[u] = k < ke ? __ldcs(&S[k]) : 0.0;  // streams: evict-first (L1 keeps the gathered states)
-                jj[u] = k < ke ? __ldcs(&col[k]) : 0;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; u++)   // filter 2^-t, w != 0 (O-R13)
-                rr[u] = (sv[u] == 0.0 || sv[u] < filt) ? ST_DEC : (int)st[jj[u]];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const int r = rr[u];
-                if (r == ST_DEC) continue;                  // (O-R12)
-                if (r > br || (r == br && (sv[u] > bs || (sv[u] == bs && jj[u] < bj)))) { br = r; bs = sv[u]; bj = jj[u]; }
-            }
-        }
-        for (int o = G / 2; o > 0; o >>= 1) {               // group arg-max under (rank, S, -j)
-            int r2 = __shfl_xor_sync(0xffffffffu, br, o);
-            double s2 = __shfl_xor_sync(0xffffffffu, bs, o);
-            int32_t j2 = __shfl_xor_sync(0xffffffffu, bj, o);
-            if (r2 > br || (r2 == br && (s2 > bs || (s2 == bs && j2 < bj)))) { br = r2; bs = s2; bj = j2; }
-        }
-        if (live && !lng && gl == 0) {  // every row writes its next state (no round-start copy needed)
-            bool dec = act && br == ST_SEED;
-            nst[i] = dec ? (int8_t)ST_DEC : (int8_t)sti;
-            nidx[i] = dec ? bj : idx[i];
-            if (act && br == ST_UND) atomicAdd(&votes[bj], 1);
-        }
-    GROUP_LOOP_END
-}
 // Long rows (deg > SETUP_LONG) of a vote round, chunk-parallel: the argmax
 // under (rank(state), S, -j) is an atomic max of key = rank << 62 | bits(S)
 // (S in (0, 1] has bits < 2^62) followed by an atomic min of j over the entries
@@ -1683,9 +1631,99 @@ __global__ void k_vote_long_init(int64_t n, unsigned long long *best, int32_t *b
         bestj[i] = 0x7fffffff;
     }
 }
-__global__ void k_vote_promote(int64_t n, int8_t *nst, const int32_t *votes, int thr) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        if (nst[i] == ST_UND && votes[i] >= thr) nst[i] = ST_SEED;
+// ---- vote rounds over the ACTIVE rows only.  A row leaves Undecided once
+// (Decided by a seed, or promoted to Seed) and never changes again (Alg. 3,
+// O-R9), so each round runs over the rows still Undecided at its start: a
+// list compacted after every round (late rounds of cfg 4 level 0 have a few
+// per cent of the rows left).  The round writes nst / nidx of its listed
+// rows; k_vote_commit then applies the promotion and copies them
+// into st / idx (the rows not listed are final in st), and appends the rows
+// still Undecided to the next list.  Order-free: same states, bit for bit.
+// Levels of short rows (grids: fewer than 10 entries per row on average) keep
+// the plain row order instead (list = nullptr, out = nullptr: every row of
+// [lo, lo + n) each round, non-Undecided rows skipped): there the list's
+// indirection and compaction cost more than the rows they skip.
+// (round 1: list = nullptr, the rows lo, lo + 1, ... themselves)
+__global__ void k_act_init(int64_t lo, int64_t hi, int32_t *__restrict__ cnt) { *cnt = (int32_t)(hi - lo); }
+template <int G>
+__global__ void k_vote_round_list(const int32_t *__restrict__ list, int64_t lo, const int32_t *__restrict__ nact_p,
+                                  const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col,
+                                  const double *__restrict__ S, double filt, const int8_t *__restrict__ st,
+                                  int8_t *__restrict__ nst, int32_t *__restrict__ nidx, int32_t *__restrict__ votes) {
+    const int64_t nact = *nact_p;
+    GROUP_LOOP_BEGIN(G, nact)
+        const int64_t ia = !live ? 0 : list ? list[i] : lo + i;  // a listed row is Undecided at the round's start
+        const int sti = !live ? ST_DEC : list ? ST_UND : st[ia];
+        const int64_t rb = live ? row_ptr[ia] : 0, re = live ? row_ptr[ia + 1] : 0;
+        const bool lng = re - rb > SETUP_LONG;   // k_vote_long_*
+        const bool act = sti == ST_UND && !lng;
+        int br = -1;
+        double bs = 0.0;
+        int32_t bj = 0x7fffffff;
+        const int64_t kb = act ? rb : 0, ke = act ? re : 0;
+        for (int64_t k0 = kb + gl; k0 < ke; k0 += 4 * G) {
+            double sv[4];
+            int32_t jj[4];
+            int rr[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int64_t k = k0 + u * G;
+                sv[u] = k < ke ? __ldcs(&S[k]) : 0.0;
+                jj[u] = k < ke ? __ldcs(&col[k]) : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++)   // filter 2^-t, w != 0 (O-R13)
+                rr[u] = (sv[u] == 0.0 || sv[u] < filt) ? ST_DEC : (int)st[jj[u]];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int r = rr[u];
+                if (r == ST_DEC) continue;                  // (O-R12)
+                if (r > br || (r == br && (sv[u] > bs || (sv[u] == bs && jj[u] < bj)))) { br = r; bs = sv[u]; bj = jj[u]; }
+            }
+        }
+        for (int o = G / 2; o > 0; o >>= 1) {               // group arg-max under (rank, S, -j)
+            int r2 = __shfl_xor_sync(0xffffffffu, br, o);
+            double s2 = __shfl_xor_sync(0xffffffffu, bs, o);
+            int32_t j2 = __shfl_xor_sync(0xffffffffu, bj, o);
+            if (r2 > br || (r2 == br && (s2 > bs || (s2 == bs && j2 < bj)))) { br = r2; bs = s2; bj = j2; }
+        }
+        if (act && gl == 0) {
+            const bool dec = br == ST_SEED;
+            nst[ia] = dec ? (int8_t)ST_DEC : (int8_t)ST_UND;
+            nidx[ia] = dec ? bj : (int32_t)ia;               // an Undecided row's idx is its own id
+            if (br == ST_UND) atomicAdd(&votes[bj], 1);
+        }
+    GROUP_LOOP_END
+}
+__global__ void k_vote_commit(const int32_t *__restrict__ list, int64_t lo, const int32_t *__restrict__ nact_p,
+                              const int8_t *__restrict__ nst, const int32_t *__restrict__ nidx,
+                              const int32_t *__restrict__ votes, int thr, int8_t *__restrict__ st,
+                              int32_t *__restrict__ idx, int32_t *__restrict__ out, int32_t *__restrict__ out_cnt) {
+    const int64_t nact = *nact_p;
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31LL; base < nact; base += stride) {
+        const int64_t t = base + lane;
+        bool keep = false;
+        int32_t i = 0;
+        if (t < nact) {
+            i = list ? list[t] : (int32_t)(lo + t);
+            const bool fin = !list && st[i] != ST_UND;  // no list: rows already final are skipped
+            int sv = fin ? -1 : nst[i];
+            if (sv == ST_UND && votes[i] >= thr) sv = ST_SEED;  // promotion
+            if (sv == ST_DEC || sv == ST_SEED) {                // (st[i] is Undecided, idx[i] = i)
+                st[i] = (int8_t)sv;
+                if (sv == ST_DEC) idx[i] = nidx[i];
+            }
+            keep = sv == ST_UND;
+        }
+        if (!out) continue;  // plain row order: no list
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        int pos = 0;
+        if (lane == 0 && m) pos = atomicAdd(out_cnt, __popc(m));
+        pos = __shfl_sync(0xffffffffu, pos, 0);
+        if (keep) out[pos + __popc(m & ((1u << lane) - 1))] = i;
+    }
 }
 __global__ void k_root_flags(int64_t n, const int8_t *st, int64_t *flag) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -2672,13 +2710,21 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
         k_vote_long_init<<<ge, 256, 0, s>>>(n, vbest.p, vbestj.p);
         ++g_kl;
     }
+    // the active list: this process's rows (all of them without a communicator or
+    // on a virtual grid), compacted after every round
+    const int64_t alo = R.rb[R.mine.front()], ahi = R.rb[R.mine.back() + 1];
+    DBuf<int32_t> alist(ahi - alo, s), blist(ahi - alo, s), acnt(2, s);
+    k_act_init<<<1, 1, 0, s>>>(alo, ahi, acnt.p); ++g_kl;
+    int32_t *cur = nullptr, *nxt = alist.p, *ccur = acnt.p, *cnxt = acnt.p + 1;
+    const char *vle = getenv("LAP_VOTE_LIST");  // 0 / 1: force (tests); default by row length
+    const bool vlist = vle ? vle[0] == '1' : nnz >= 10 * n;
     for (int t = 1; t <= p.vote_rounds; t++) {
         double filt = ldexp(1.0, -t);
-        for (int r : R.mine) {
-            const int64_t r0 = R.rb[r], r1 = R.rb[r + 1];
-            LAUNCH_G(Gv, k_vote_round, r1 - r0, s, r0, r1, L.row_ptr, L.col, S.p, filt, st.p, idx.p, nst.p, nidx.p,
-                     vp);
-            if (nlc > 0) {
+        LAUNCH_G(Gv, k_vote_round_list, ahi - alo, s, cur, alo, ccur, L.row_ptr, L.col, S.p, filt, st.p, nst.p, nidx.p,
+                 vp);
+        if (nlc > 0) {
+            for (int r : R.mine) {
+                const int64_t r0 = R.rb[r], r1 = R.rb[r + 1];
                 const unsigned gc = grid_for(nlc * 32, 256, 148 * 16);
                 k_vote_long_max<<<gc, 256, 0, s>>>(nlc, lc_row, lc_idx, r0, r1, L.row_ptr, L.col, S.p, filt, st.p,
                                                    vbest.p);
@@ -2689,15 +2735,22 @@ static int64_t aggregate_attempt(lap_hierarchy *h, Level &L, int l, int attempt,
                 g_kl += 3;
             }
         }
-        if (R.on) {  // the round's new states of every rank's rows, and the summed votes
-            setup_share(nst.p, R.rb, s);
-            setup_share(nidx.p, R.bytes(R.rb, 4), s);
-            if (vsum) setup_sum_i32(vloc.p, votes.p, n, s);
-        }
-        k_vote_promote<<<ge, 256, 0, s>>>(n, nst.p, votes.p, p.vote_threshold); ++g_kl;
+        if (vsum) setup_sum_i32(vloc.p, votes.p, n, s);  // the round's votes summed over the ranks (K4)
+        if (vlist) LAP_CUDA(cudaMemsetAsync(cnxt, 0, sizeof(int32_t), s));
+        k_vote_commit<<<grid_for(ahi - alo, 256, 148 * 8), 256, 0, s>>>(cur, alo, ccur, nst.p, nidx.p, votes.p,
+                                                                        p.vote_threshold, st.p, idx.p,
+                                                                        vlist ? nxt : nullptr, cnxt);
+        ++g_kl;
         LAP_CHECK_LAUNCH();
-        std::swap(st.p, nst.p);
-        std::swap(idx.p, nidx.p);
+        if (R.on) {  // every rank's rows of the committed states (NCCL; no-op on one process)
+            setup_share(st.p, R.rb, s);
+            setup_share(idx.p, R.bytes(R.rb, 4), s);
+        }
+        if (vlist) {
+            cur = nxt;  // the list just written; the next round writes the other one
+            nxt = cur == alist.p ? blist.p : alist.p;
+            std::swap(ccur, cnxt);
+        }
         h->cur.edges += nnz;
     }
     tmark("  votes");

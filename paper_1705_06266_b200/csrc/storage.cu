@@ -269,47 +269,83 @@ __global__ void __launch_bounds__(256) k_perm_sort_thread(int64_t n, const int32
         }
     }
 }
-// rows longer than minlen copied (columns translated) into the scratch at their output positions; warp per row
-__global__ void __launch_bounds__(256) k_perm_fill_long(int64_t n, int64_t minlen, const int32_t *__restrict__ sid,
-                                                        const int32_t *__restrict__ spos, const int64_t *__restrict__ rp,
-                                                        const int32_t *__restrict__ col, const double *__restrict__ w,
-                                                        const int64_t *__restrict__ srp, int32_t *__restrict__ kt,
-                                                        double *__restrict__ vt, int64_t maxlen = INT64_MAX,
-                                                        int32_t *__restrict__ kbig = nullptr,
-                                                        double *__restrict__ vbig = nullptr,
-                                                        int64_t band_hi = INT64_MAX) {
-    // rows of (minlen, maxlen] -> kt / vt (to be sorted); rows longer than maxlen
-    // (left unsorted) straight to kbig / vbig
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t p = warp; p < n; p += nwarps) {
-        const int64_t o = srp[p], len = srp[p + 1] - o;
-        if (len <= minlen) continue;
-        const bool unsorted = len > maxlen && len <= band_hi;  // (maxlen, band_hi]: left in place, unsorted
-        int32_t *kd = unsorted ? kbig : kt;
-        double *vd = unsorted ? vbig : vt;
-        const int64_t a0 = rp[sid[p]];
-        int64_t q = lane;
-        for (; q + 96 < len; q += 128) {  // 4 column loads, then their 4 spos gathers, in flight
-            int32_t c[4];
-            double v[4];
+// rows longer than minlen copied (columns translated through spos) to their
+// output positions: rows of (minlen, maxlen] -> kt / vt (to be sorted); rows
+// longer than maxlen and at most band_hi (left unsorted) straight to kbig / vbig
+struct PermFill {
+    int64_t n, minlen, maxlen, band_hi;
+    const int32_t *__restrict__ sid;
+    const int32_t *__restrict__ spos;
+    const int64_t *__restrict__ rp;
+    const int32_t *__restrict__ col;
+    const double *__restrict__ w;
+    const int64_t *__restrict__ srp;
+    int32_t *__restrict__ kt;
+    double *__restrict__ vt;
+    int32_t *__restrict__ kbig;
+    double *__restrict__ vbig;
+};
+constexpr int64_t PFILL_LONG = 1024;  // longer rows: a CTA each (k_perm_fill_rows)
+// row p's entries [q0, len) with stride st: 4 column loads, then their 4 spos
+// gathers, in flight per thread
+__device__ __forceinline__ void perm_fill_row(const PermFill &A, int64_t p, int64_t o, int64_t len, int64_t q0,
+                                              int64_t st) {
+    const bool unsorted = len > A.maxlen && len <= A.band_hi;
+    int32_t *kd = unsorted ? A.kbig : A.kt;
+    double *vd = unsorted ? A.vbig : A.vt;
+    const int64_t a0 = A.rp[A.sid[p]];
+    int64_t q = q0;
+    for (; q + 3 * st < len; q += 4 * st) {
+        int32_t c[4];
+        double v[4];
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
-                c[u] = col[a0 + q + 32 * u];  // (cached: short rows of neighbouring warps share lines)
-                v[u] = w ? w[a0 + q + 32 * u] : 1.0;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                kd[o + q + 32 * u] = spos[c[u]];
-                vd[o + q + 32 * u] = v[u];
-            }
+        for (int u = 0; u < 4; u++) {
+            c[u] = A.col[a0 + q + st * u];
+            v[u] = A.w ? A.w[a0 + q + st * u] : 1.0;
         }
-        for (; q < len; q += 32) {
-            kd[o + q] = spos[col[a0 + q]];
-            vd[o + q] = w ? w[a0 + q] : 1.0;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            kd[o + q + st * u] = A.spos[c[u]];
+            vd[o + q + st * u] = v[u];
         }
     }
+    for (; q < len; q += st) {
+        kd[o + q] = A.spos[A.col[a0 + q]];
+        vd[o + q] = A.w ? A.w[a0 + q] : 1.0;
+    }
+}
+// G lanes per row (G near the average row length: several short rows per warp
+// in flight instead of a warp per row with most lanes idle); rows longer than
+// PFILL_LONG are listed for k_perm_fill_rows
+template <int G>
+__global__ void __launch_bounds__(256) k_perm_fill_grp(PermFill A, int32_t *__restrict__ longs,
+                                                       int32_t *__restrict__ nlong) {
+    GROUP_LOOP_BEGIN(G, A.n)
+        const int64_t o = live ? A.srp[i] : 0, len = live ? A.srp[i + 1] - o : 0;
+        if (len > PFILL_LONG) {
+            if (gl == 0) longs[atomicAdd(nlong, 1)] = (int32_t)i;
+        } else if (len > A.minlen) {
+            perm_fill_row(A, i, o, len, gl, G);
+        }
+    GROUP_LOOP_END
+}
+__global__ void __launch_bounds__(256) k_perm_fill_rows(PermFill A, const int32_t *__restrict__ longs,
+                                                        const int32_t *__restrict__ nlong) {
+    const int64_t m = *nlong;
+    for (int64_t b = blockIdx.x; b < m; b += gridDim.x) {
+        const int64_t p = longs[b], o = A.srp[p], len = A.srp[p + 1] - o;
+        perm_fill_row(A, p, o, len, threadIdx.x, blockDim.x);
+    }
+}
+static void perm_fill(const PermFill &A, int64_t nnz, cudaStream_t s) {
+    if (A.n <= 0) return;
+    const double avg = (double)nnz / (double)A.n;
+    const int G = avg <= 8.0 ? 4 : avg <= 32.0 ? 8 : avg <= 128.0 ? 16 : 32;
+    DBuf<int32_t> longs(nnz / PFILL_LONG + 1, s), nlong(1, s);
+    LAP_CUDA(cudaMemsetAsync(nlong.p, 0, sizeof(int32_t), s));
+    LAUNCH_G(G, k_perm_fill_grp, A.n, s, A, longs.p, nlong.p);
+    k_perm_fill_rows<<<grid_for(nnz / PFILL_LONG + 1, 1, 148 * 4), 256, 0, s>>>(A, longs.p, nlong.p);
+    g_kl += 2;
 }
 template <int NH>
 __device__ __forceinline__ void warp_bitonic(int (&k)[2], double (&v)[2], int lane) {
@@ -587,8 +623,7 @@ void permute_csr(int64_t n, int64_t nnz, const int32_t *sid, const int32_t *spos
     scan_excl(deg.p, srp, n + 1, s);
     if (nnz <= 0) return;
     if (!sort_cols) {  // warp per row (a row's source entries are contiguous): 2.4 -> 1.2 ms on cfg 4 level 0
-        k_perm_fill_long<<<grid_for(n * 32, 256, 148 * 8), 256, 0, s>>>(n, 0, sid, spos, rp, col, w, srp, scol, sw);
-        g_kl++;
+        perm_fill(PermFill{n, 0, INT64_MAX, INT64_MAX, sid, spos, rp, col, w, srp, scol, sw, nullptr, nullptr}, nnz, s);
         LAP_CHECK_LAUNCH();
         return;
     }
@@ -603,9 +638,7 @@ void permute_sorted_rows(int64_t n, int64_t nnz, const int32_t *sid, const int32
         const bool any_long = maxlen > band_hi;
         DBuf<int32_t> c2(any_long ? nnz : 1, s);
         DBuf<double> w2(any_long ? nnz : 1, s);
-        k_perm_fill_long<<<grid_for(n * 32, 256, 148 * 8), 256, 0, s>>>(n, 0, sid, spos, rp, col, w, srp, c2.p, w2.p, 0,
-                                                                        scol, sw, band_hi);
-        g_kl++;
+        perm_fill(PermFill{n, 0, 0, band_hi, sid, spos, rp, col, w, srp, c2.p, w2.p, scol, sw}, nnz, s);
         trace_mark("    permute: rows filled");
         if (any_long)
             sort_rows_min(n, srp, nnz, bitlen_u64((uint64_t)n), band_hi, c2.p, w2.p, scol, sw, s, 0, false, band_hi);
@@ -620,9 +653,7 @@ void permute_sorted_rows(int64_t n, int64_t nnz, const int32_t *sid, const int32
     if (maxlen > 32) {  // longer rows: copied into a scratch at their positions, then sorted by length class
         DBuf<int32_t> c2(nnz, s);
         DBuf<double> w2(nnz, s);
-        k_perm_fill_long<<<grid_for(n * 32, 256, 148 * 8), 256, 0, s>>>(n, 32, sid, spos, rp, col, w, srp, c2.p, w2.p,
-                                                                        sort_max, scol, sw, band_hi);
-        g_kl++;
+        perm_fill(PermFill{n, 32, sort_max, band_hi, sid, spos, rp, col, w, srp, c2.p, w2.p, scol, sw}, nnz, s);
         trace_mark("    permute: long rows filled");
         sort_rows_min(n, srp, nnz, bitlen_u64((uint64_t)n), 32, c2.p, w2.p, scol, sw, s, sort_max, false, band_hi);
     }

@@ -300,7 +300,7 @@ def _vote_worker(rank, world, port, q):
                         buf[a0:a1] = seg
                 dist.all_reduce(votes.copy_(vloc), op=dist.ReduceOp.SUM)   # setup_sum_i32
                 st, idx = ts.numpy().copy(), ti.numpy().copy()
-                st[(st == UND) & (votes.numpy() >= 8)] = SEED              # k_vote_promote (replicated)
+                st[(st == UND) & (votes.numpy() >= 8)] = SEED              # the promotion of k_vote_commit
             root = st != DEC
             rid = np.cumsum(root) - 1
             agg = np.where(root, rid, rid[idx]).astype(np.int32)

@@ -459,3 +459,25 @@ def test_solves_bitwise_reproducible_with_hub_rows(P, mk):
     B = np.stack([lapgen.rhs(g.n, seed=j) for j in range(3)])
     Xs = {h.solve_block(B)[0].tobytes() for _ in range(4)}
     assert len(Xs) == 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["0", "1"], ids=["row-order", "active-list"])
+@pytest.mark.parametrize("mk", [SMALL[0], SMALL[2], SMALL[3], SMALL[4], SMALL[7], SMALL[10]],
+                         ids=["cfg1", "grid3d12", "rmat12", "ba5000", "star40000", "dense6000"])
+def test_vote_round_modes_bit_exact(P, mk, mode, monkeypatch):
+    """Alg. 3's vote rounds in both execution orders: every row of
+    the level each round (LAP_VOTE_LIST=0, the default below 10 entries per row)
+    or only the rows still Undecided, from a list compacted after every round
+    (LAP_VOTE_LIST=1, the default above) -- the aggregates, and so every coarse
+    operator, equal the oracle's bit for bit either way."""
+    monkeypatch.setenv("LAP_VOTE_LIST", mode)
+    g = mk()
+    h, ho = P.Hierarchy(g), oracle.Hierarchy(g)
+    assert h.nlev == ho.nlev
+    for l in range(ho.nlev):
+        a, o = h.level(l), ho.level(l)
+        assert a["kind"] == o.kind and (a["n"], a["nnz"]) == (o.n, o.nnz), l
+        assert np.array_equal(a["col"], o.col) and a["w"].tobytes() == o.w.tobytes(), l
+        if o.kind == oracle.AGG:
+            assert np.array_equal(a["agg"], o.agg), l
