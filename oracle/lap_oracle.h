@@ -14,12 +14,16 @@
  * Citations: P:NNN = /root/reference/PAPER.md line NNN; S:NNN = SPEC.md line;
  * O-xx = SURVEY.md §8(c) row.
  *
- * Parity-unpinned functions (no external truth beyond invariants, SURVEY
- * O-P16): the aggregates / F sets / coarse operators produced for the five
- * BASELINE.json configs as a whole.  Every building block below is pinned by
- * tests/test_oracle_*.py (brute force, closed forms, SPEC worked examples);
- * the K-cycle (orc_kcycle / orc_kcoarse, N2) by the FCG Gram-system identity
- * and the V-cycle/PCG special cases (tests/test_oracle_kcycle.py).
+ * Pins: every function below is pinned by tests/test_oracle_*.py and
+ * tests/test_golden_streams.py against something other than itself (SPEC /
+ * SURVEY worked examples and goldens, closed forms, brute force on tiny
+ * graphs, dense library routines); the K-cycle (orc_kcycle / orc_kcoarse,
+ * N2) by the FCG Gram-system identity and the V-cycle/PCG special cases
+ * (tests/test_oracle_kcycle.py).  No function is parity-unpinned.  What has
+ * no external truth (SURVEY O-P16) is only the OUTPUT of these pinned
+ * functions on the five BASELINE.json configs as a whole (nobody publishes
+ * the aggregates of a 4M-vertex graph): there the check is the invariants
+ * at full size plus "oracle == GPU bit for bit".
  */
 #ifndef LAP_ORACLE_H
 #define LAP_ORACLE_H

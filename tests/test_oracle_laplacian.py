@@ -80,3 +80,43 @@ def test_validate_rejects_bad_graphs():
 def test_graph_generators_are_valid_laplacians():
     for g in [lapgen.config(1), lapgen.grid3d(8), lapgen.rmat(10), lapgen.barabasi_albert(2000, 8)]:
         assert oracle.validate(g) == oracle.ORC_OK, g.name
+
+
+def test_relabel_hand_example():
+    """O-S1: level 0 = Pi L Pi^T with perm[old] = new.  Path
+    0 -1.5- 1 -2.5- 2 under perm = [2, 0, 1]: new vertex 0 = old 1 (neighbours
+    old 2 -> new 1 with 2.5, old 0 -> new 2 with 1.5), new 1 = old 2, new 2 = old 0
+    (worked by hand; a swapped perm / inverse gives new row 0 one neighbour)."""
+    g = lapgen.path(3, w=[1.5, 2.5])
+    rp, col, w = oracle.relabel(g, np.array([2, 0, 1], np.int64))
+    assert rp.tolist() == [0, 2, 3, 4]
+    assert col.tolist() == [1, 2, 0, 0]
+    assert w.tolist() == [2.5, 1.5, 2.5, 1.5]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_relabel_is_permutation_similarity(seed):
+    """Pi L Pi^T against scipy's sparse product with the permutation matrix
+    Pi[perm[i], i] = 1 (exact: every product is 1 * w * 1, every sum has one
+    term), rows in ascending column order; unit weights for w = None; and the
+    relabelled Laplacian applied to the permuted vector is the permuted L x."""
+    import scipy.sparse as sp
+    g = lapgen.random_connected(30 + 7 * seed, 50, seed, weighted=(seed % 2 == 0))
+    n = g.n
+    perm = np.random.default_rng(100 + seed).permutation(n).astype(np.int64)
+    rp, col, w = oracle.relabel(g, perm)
+    gw = np.ones(g.nnz) if g.w is None else g.w
+    A = sp.csr_matrix((gw, g.col, g.row_ptr), shape=(n, n))
+    Pi = sp.csr_matrix((np.ones(n), (perm, np.arange(n))), shape=(n, n))
+    B = (Pi @ A @ Pi.T).tocsr()
+    B.sort_indices()
+    assert rp.tolist() == B.indptr.tolist()
+    assert col.tolist() == B.indices.tolist()
+    assert w.tolist() == B.data.tolist()
+    x = np.random.default_rng(seed).standard_normal(n)
+    d = oracle.row_sums(n, g.row_ptr, gw)
+    y = oracle.spmv(n, g.row_ptr, g.col, gw, d, x)
+    d2 = oracle.row_sums(n, rp, w)
+    xp = np.empty(n); xp[perm] = x
+    y2 = oracle.spmv(n, rp, col, w, d2, xp)
+    assert np.allclose(y2[perm], y, rtol=0, atol=1e-12 * np.abs(y).max())
